@@ -1,0 +1,181 @@
+"""The sparse-delta codec written per element and per byte in pure Python.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__).  For tiny inputs: this is the
+definition, read off the paper and the SPEC byte layout, with no vectorisation.
+``oracle.codec`` (numpy) is checked against it.
+
+Definitions followed, in order (SURVEY.md §8(c) O1-O10 restates them):
+  O1  A logical tensor is the concatenation of its spans in fusion order
+      ("stacking split HuggingFace blocks in a fixed order";
+      SPEC.md:52-57 FusionMap offsets = prefix sums).  Lanes are unsigned
+      integers of width w in {2, 4} bytes ("opaque fixed-width
+      byte lanes").
+  O2  changed lanes: j with old[j] != new[j] as integers (SPEC.md:136,
+      DESIGN.md reading R2), ascending ("stores the non-zeros as
+      two 1D arrays, idx and val").
+  O3  gaps: first index as-is, then differences.
+  O4  LEB128 of every gap, concatenated (oracle.leb128).
+  O5  values: the NEW lanes at idx (replace mode, reading R1).
+  O6  record = u16 name_len | name | u64 N | u64 nnz | u64 idx_len |
+      idx_stream | values | u8 mode(=0), little-endian.
+  O7  offset table row per record (north_star "per-tensor offset tables").
+  O9  apply: validate every record fully, then W[idx_i] = val_i
+      ("validate fully before mutating").
+  O10 rho = sum nnz / sum N (Eq. 1).
+"""
+
+from . import leb128
+from .errors import DeltaError
+
+HEADER_FIXED = 2 + 8 + 8 + 8 + 1  # u16 name_len, u64 N, u64 nnz, u64 idx_len, u8 mode
+
+
+def _u(n: int, nbytes: int) -> bytes:
+    """Little-endian unsigned integer of ``nbytes`` bytes, written byte by byte."""
+    return bytes((n >> (8 * i)) & 0xFF for i in range(nbytes))
+
+
+def _read_u(buf: bytes, pos: int, nbytes: int) -> tuple[int, int]:
+    if pos + nbytes > len(buf):
+        raise DeltaError("layout", f"header field at byte {pos} runs past the body")
+    v = 0
+    for i in range(nbytes):
+        v |= buf[pos + i] << (8 * i)
+    return v, pos + nbytes
+
+
+def fuse(spans: list[list[int]]) -> list[int]:
+    """O1: the fused tensor's flat lanes are the spans concatenated in order."""
+    out: list[int] = []
+    for s in spans:
+        out.extend(s)
+    return out
+
+
+def changed_indices(old: list[int], new: list[int]) -> list[int]:
+    """O2: ascending j where the lanes differ bitwise."""
+    if len(old) != len(new):
+        raise DeltaError("shape", "old and new have different element counts")
+    return [j for j in range(len(old)) if old[j] != new[j]]
+
+
+def encode_indices(idx: list[int]) -> bytes:
+    """O3+O4: LEB128(idx[0]) then LEB128(idx[i]-idx[i-1])."""
+    out = bytearray()
+    prev = None
+    for x in idx:
+        if prev is not None and x <= prev:
+            raise DeltaError("nonincreasing", "encode_indices needs strictly increasing input")
+        out += leb128.encode(x if prev is None else x - prev)
+        prev = x
+    return bytes(out)
+
+
+def decode_indices(stream: bytes) -> list[int]:
+    """Inverse of encode_indices with the strict checks of SPEC.md:80 and
+    the strictly-increasing invariant: every gap after the
+    first must be >= 1."""
+    idx: list[int] = []
+    pos = 0
+    while pos < len(stream):
+        g, pos = leb128.decode(stream, pos)
+        if idx and g == 0:
+            raise DeltaError("nonincreasing", f"zero gap after index {idx[-1]}")
+        idx.append(g if not idx else idx[-1] + g)
+    return idx
+
+
+def record(name: str, old: list[int], new: list[int], width: int) -> bytes:
+    """O2..O6 for one fused tensor."""
+    nb = name.encode("utf-8")
+    if len(nb) > 0xFFFF:
+        raise DeltaError("layout", "name longer than the u16 length field (SPEC.md:148)")
+    idx = changed_indices(old, new)
+    stream = encode_indices(idx)
+    vals = b"".join(_u(new[j], width) for j in idx)
+    return (_u(len(nb), 2) + nb + _u(len(old), 8) + _u(len(idx), 8)
+            + _u(len(stream), 8) + stream + vals + _u(0, 1))
+
+
+def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: int):
+    """Body and offset table for (name, old_spans, new_spans) in list order.
+
+    Table rows: (record_off, N, nnz, idx_off, idx_len, val_off, record_bytes),
+    with idx_off = record_off + 2 + name_len + 24 and val_off = idx_off +
+    idx_len (O7, from the O6 layout)."""
+    body = bytearray()
+    table = []
+    for name, old_spans, new_spans in tensors:
+        if len(old_spans) != len(new_spans) or any(
+                len(a) != len(b) for a, b in zip(old_spans, new_spans)):
+            raise DeltaError("shape", f"tensor {name!r}: span structure differs")
+        old, new = fuse(old_spans), fuse(new_spans)
+        rec = record(name, old, new, width)
+        nl = len(name.encode("utf-8"))
+        nnz = sum(1 for j in range(len(old)) if old[j] != new[j])
+        idx_off = len(body) + 2 + nl + 24
+        idx_len, _ = _read_u(rec, 2 + nl + 16, 8)
+        table.append((len(body), len(old), nnz, idx_off, idx_len, idx_off + idx_len, len(rec)))
+        body += rec
+    return bytes(body), table
+
+
+def parse(body: bytes, width: int):
+    """Split a body into records [(name, N, idx list, value list, mode)],
+    decoding and validating everything."""
+    recs = []
+    pos = 0
+    while pos < len(body):
+        nl, pos = _read_u(body, pos, 2)
+        if pos + nl > len(body):
+            raise DeltaError("layout", "name runs past the body")
+        name = body[pos:pos + nl].decode("utf-8", errors="strict")
+        pos += nl
+        n, pos = _read_u(body, pos, 8)
+        nnz, pos = _read_u(body, pos, 8)
+        ilen, pos = _read_u(body, pos, 8)
+        if pos + ilen > len(body):
+            raise DeltaError("layout", f"index stream of {name!r} runs past the body")
+        idx = decode_indices(body[pos:pos + ilen])
+        pos += ilen
+        if len(idx) != nnz:
+            raise DeltaError("count", f"{name!r}: {len(idx)} indices decoded, nnz says {nnz}")
+        if idx and idx[-1] >= n:
+            raise DeltaError("range", f"{name!r}: index {idx[-1]} >= element_count {n}")
+        vals = []
+        for _ in range(nnz):
+            v, pos = _read_u(body, pos, width)
+            vals.append(v)
+        mode, pos = _read_u(body, pos, 1)
+        if mode != 0:
+            raise DeltaError("mode", f"{name!r}: mode byte {mode} (only replace=0)")
+        recs.append((name, n, idx, vals, mode))
+    return recs
+
+
+def apply(targets: list[tuple[str, list[int]]], body: bytes, width: int) -> list[list[int]]:
+    """O9: returns new lane lists; raises DeltaError (inputs untouched) if any
+    record is malformed or does not match its target (name, element count,
+    record count)."""
+    recs = parse(body, width)
+    if len(recs) != len(targets):
+        raise DeltaError("layout", f"{len(recs)} records for {len(targets)} targets")
+    for (name, n, _, _, _), (tname, lanes) in zip(recs, targets):
+        if name != tname:
+            raise DeltaError("name", f"record {name!r} vs target {tname!r}")
+        if n != len(lanes):
+            raise DeltaError("numel", f"{name!r}: record N={n}, target has {len(lanes)}")
+    out = []
+    for (_, _, idx, vals, _), (_, lanes) in zip(recs, targets):
+        w = list(lanes)
+        for j, v in zip(idx, vals):
+            w[j] = v
+        out.append(w)
+    return out
+
+
+def rho(pairs: list[tuple[list[int], list[int]]]) -> float:
+    """O10, Eq. 1 with bitwise inequality as 'nonzero'."""
+    total = sum(len(o) for o, _ in pairs)
+    nz = sum(1 for o, n in pairs for a, b in zip(o, n) if a != b)
+    return nz / total if total else 0.0
