@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse-delta hot path (SparrowRL, arXiv 2602.11456 §5.1) on B200.
+
+One step = one pass of the whole path over one synthetic weight set:
+    delta_size (K1 compare+compaction, K2 LEB128 lengths, K3 offset table, size readback)
+  + delta_extract (K4 LEB128 bytes + values, K5 headers; consumes the cached scan)
+  + [N>1: NCCL size all-gather + assembly of the packed body on rank 0]
+  + delta_apply (A1 locate, A2 decode+validate, A3 scans, A4 gated scatter-store)
+Metric (BASELINE.json): GB/s of weights scanned (old + new bytes compared, all ranks) per
+second of step time; the payload ratio W / body is reported beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config M3] [--impl reference]
+
+Multi-GPU: launched by torchrun (one rank per GPU, NCCL); tensors are sharded by
+contiguous balanced ranges (paper_2602_11456_b200.dist), the step time is the max over
+ranks of the CUDA-event time of the K timed steps.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (model or None, rho, pattern, description)
+    "M1": ("M1", 0.01, "exact", "single 16M-element bf16 tensor, 1% changed (configs[0])"),
+    "M2": ("4B", 0.01, "uniform", "Qwen3-4B-shaped bf16 set, 1% uniform (configs[1])"),
+    "M3": ("8B", 0.01, "uniform", "Qwen3-8B-shaped bf16 set, 1% uniform (configs[2])"),
+    "M4": ("14B", 0.01, "uniform", "Qwen3-14B-shaped bf16 set, 1% uniform (configs[3])"),
+    "M5": ("8B", None, None, "Qwen3-8B sweep (configs[4]); pick --rho/--pattern"),
+}
+METRIC = "delta extract+apply GB/s of weights scanned vs HBM peak; payload ratio, Qwen3-8B"
+PAPER_CPU = "paper: ~5 s CPU extraction for Qwen3-8B (PAPER.md:405), 79x payload (PAPER.md:51), other hardware"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="M3", choices=sorted(CONFIGS))
+    p.add_argument("--rho", type=float, default=None)
+    p.add_argument("--pattern", default=None, choices=[None, "uniform", "rowblock", "exact"])
+    p.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    p.add_argument("--no-clocks", action="store_true")
+    return p.parse_args()
+
+
+def workload(args):
+    from workload import m1_specs, qwen3
+    model, rho, pattern, desc = CONFIGS[args.config]
+    rho = args.rho if args.rho is not None else (rho if rho is not None else 0.01)
+    pattern = args.pattern or pattern or "uniform"
+    specs = m1_specs() if model == "M1" else qwen3(model)
+    return specs, rho, pattern, desc
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index, enabled=True):
+        self.index, self.enabled, self.proc, self.lines = index, enabled, None, []
+
+    def start(self):
+        if not self.enabled:
+            return
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle timing (CPU)
+class OracleSample:
+    """A bounded sample of the workload for timing the oracle (oracle.codec, plain numpy,
+    as it stands) on the host: whole tensors in list order (the embedding moved last so a
+    short sample is layer tensors), generated once with the shared seeded generator (on
+    cuda:0 when there is one, then copied to host) until the estimated oracle time reaches
+    ``budget_s``."""
+
+    def __init__(self, specs, rho, pattern, seed, dtype, budget_s):
+        import numpy as np
+        import torch
+
+        import oracle
+        from workload import generate_pair
+        self.oracle = oracle
+        gdev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+        order = list(range(len(specs)))
+        if len(order) > 3:
+            order = order[1:] + order[:1]
+        self.items, est, self.lanes, self.scanned = [], 0.0, 0, 0
+        for k in order:
+            s = specs[k]
+            o, w = generate_pair(s, k, seed, rho=rho, pattern=pattern, dtype=dtype, device=gdev)
+            lt = torch.int16 if o.element_size() == 2 else torch.int32
+            nt = np.uint16 if o.element_size() == 2 else np.uint32
+            on, wn = o.view(lt).cpu().numpy().view(nt), w.view(lt).cpu().numpy().view(nt)
+            self.items.append((s.name, on, wn))
+            self.lanes += s.numel
+            self.scanned += 2 * s.numel * on.dtype.itemsize
+            if not est:  # calibrate on the first tensor
+                t0 = time.perf_counter()
+                self._one(self.items[0])
+                per_byte = (time.perf_counter() - t0) / self.scanned
+            est = per_byte * self.scanned
+            if est >= budget_s:
+                break
+        self.sample = (f"{len(self.items)} whole tensors ({self.lanes} lanes, "
+                       f"{self.scanned / 1e9:.3f} GB of old+new) of the same workload; "
+                       f"oracle.codec extract+apply, 1 thread (numpy); inputs from the shared "
+                       f"seeded generator on {gdev}")
+
+    def _one(self, item):
+        name, on, wn = item
+        body, _ = self.oracle.codec.extract([(name, [on], [wn])])
+        got = self.oracle.codec.apply([(name, on)], body, on.dtype.itemsize)[0]
+        return got
+
+    def run(self):
+        """One timed pass: returns (GB/s of weights scanned, seconds)."""
+        import numpy as np
+        spent = 0.0
+        for item in self.items:
+            t0 = time.perf_counter()
+            got = self._one(item)
+            spent += time.perf_counter() - t0
+            if not np.array_equal(got, item[2]):
+                raise SystemExit("oracle round trip mismatch")
+        return self.scanned / spent / 1e9, spent
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores, per step a bounded
+    sample of this workload; rank 0 only (other ranks exit 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    specs, rho, pattern, desc = workload(args)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    budget = max(0.5, min(args.cpu_seconds, 90.0 / max(1, args.steps + args.warmup)))
+    smp = OracleSample(specs, rho, pattern, args.seed, dtype, budget)
+    for _ in range(args.warmup):
+        smp.run()
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        v, s = smp.run()
+        vals.append(v)
+        secs += s
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * secs / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u16" if args.dtype == "bf16" else "u32",
+        "data": "synthetic", "config": {"workload": desc, "config": args.config, "rho": rho,
+                                        "pattern": pattern},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": smp.sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__ as entry
+    entry.build()
+    import paper_2602_11456_b200 as sd
+    from paper_2602_11456_b200 import dist as sdist
+    from workload import generate_pair
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    specs, rho, pattern, desc = workload(args)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    width = 2 if args.dtype == "bf16" else 4
+    ranges = sdist.shard_plan([s.numel for s in specs], world)
+    b, e = ranges[rank]
+    mine = list(range(b, e))
+
+    # ---- inputs resident in HBM before timing (per-tensor seeds: rank-independent data)
+    olds, news, targets = [], [], []
+    for k in mine:
+        o, w = generate_pair(specs[k], k, args.seed, rho=rho, pattern=pattern, dtype=dtype, device=dev)
+        olds.append(o)
+        news.append(w)
+        targets.append(o.clone())
+    torch.cuda.synchronize()
+    tl = sd.TensorList([(specs[k].name, o, w) for k, o, w in zip(mine, olds, news)])
+    tg = sd.TargetList([(specs[k].name, t) for k, t in zip(mine, targets)])
+    ctx = sd.DeltaContext(dev)
+    ctx.set_profiling(True)
+    local_lanes = sum(specs[k].numel for k in mine)
+    total_lanes = sum(s.numel for s in specs)
+    scanned_total = 2 * total_lanes * width            # old + new bytes, all ranks
+    size0 = ctx.delta_size(tl)
+    out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
+    root_out = None
+    stream = torch.cuda.current_stream()
+
+    def step(acc=None):
+        size = ctx.delta_size(tl)
+        t1 = ctx.last_timing()
+        body, table = ctx.delta_extract(tl, out=out, table=True)
+        t2 = ctx.last_timing()
+        nonlocal root_out
+        if world > 1:
+            sizes, off, tot = sdist.gather_sizes(size, dev)
+            if rank == 0 and (root_out is None or root_out.numel() < tot):
+                root_out = torch.empty(tot + tot // 8, dtype=torch.uint8, device=dev)
+            sdist.assemble(body, sizes, root_out)
+        ctx.delta_apply(tg, body, table=table)
+        t3 = ctx.last_timing()
+        if acc is not None:
+            for kname in ("scan_ms", "lens_ms", "finalize_ms"):
+                acc[kname] = acc.get(kname, 0.0) + t1[kname]
+            for kname in ("emit_ms", "headers_ms"):
+                acc[kname] = acc.get(kname, 0.0) + t2[kname]
+            for kname in ("locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
+                acc[kname] = acc.get(kname, 0.0) + t3[kname]
+        return size, table
+
+    for _ in range(max(args.warmup, 0)):
+        size, table = step()
+    # correctness guard on the timed configuration: apply(extract(old,new)) == new
+    ok = all(torch.equal(t.view(torch.int16 if width == 2 else torch.int32),
+                         w.view(torch.int16 if width == 2 else torch.int32))
+             for t, w in zip(targets, news))
+    if not ok:
+        raise SystemExit("bench: round trip mismatch")
+
+    clocks = Clocks(local, enabled=not args.no_clocks)
+    acc = {}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        size, table = step(acc)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = scanned_total * args.steps / (ms / 1e3) / 1e9
+
+    # ---- payload (global) and kernel-level roofline of the dominant kernel (K1)
+    body_local = size
+    nnz_local = sum(r[2] for r in table)
+    idx_local = sum(r[4] for r in table)
+    if world > 1:
+        t = torch.tensor([body_local, nnz_local, idx_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        body_total, nnz_total, idx_total = (int(x) for x in t.tolist())
+    else:
+        body_total, nnz_total, idx_total = body_local, nnz_local, idx_local
+    k1_ms = acc.get("scan_ms", 0.0) / args.steps
+    idx_size = 4 if max(specs[k].numel for k in mine) < 2**32 else 8
+    k1_bytes = 2 * local_lanes * width + nnz_local * (idx_size + width)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None
+    kernel_ms = {k: round(v / args.steps, 4) for k, v in acc.items()}
+
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u16" if width == 2 else "u32", "data": "synthetic",
+        "config": {"workload": desc, "config": args.config, "tensors": len(specs),
+                   "lanes": total_lanes, "weights_bytes": total_lanes * width,
+                   "scanned_bytes_per_step": scanned_total, "rho": rho, "pattern": pattern,
+                   "seed": args.seed, "shard": "contiguous balanced tensor ranges",
+                   "l2": f"inputs ({scanned_total / 1e9:.1f} GB per step) larger than L2 (126 MB); no flush"},
+        "payload": {"body_bytes": body_total, "ratio": round(total_lanes * width / body_total, 3),
+                    "nnz": nnz_total, "rho_measured": nnz_total / total_lanes,
+                    "index_bytes_per_entry": round(idx_total / max(nnz_total, 1), 4),
+                    "paper_context": PAPER_CPU},
+        "kernel_ms_per_step": kernel_ms,
+        "roofline": {"kernel": "k_scan_compact (K1)", "bound": "hbm",
+                     "achieved": round(achieved, 1) if achieved else None,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4) if achieved else None,
+                     "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks
+                     else "fallback 6650 GB/s (B200_PROFILING.md)",
+                     "algorithmic_bytes_per_launch": k1_bytes},
+        "gpu_launches": 9 * args.steps,
+        "clocks": clk,
+    }
+    if k1_ms > 0:
+        result["roofline"]["k1_share_of_step"] = round(k1_ms / ms_step, 4)
+
+    # ---- e2e: the same step with inputs copied from pinned host memory every step
+    if not args.no_e2e:
+        result["e2e"] = e2e(args, ctx, tl, tg, olds, news, out, dev, scanned_total, world, rank,
+                            body_total)
+    # ---- CPU oracle beside it (rank 0, N=1 only)
+    if not args.no_cpu_baseline and world == 1:
+        smp = OracleSample(specs, rho, pattern, args.seed, dtype, args.cpu_seconds)
+        v, secs = smp.run()
+        result["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                                  "sample": smp.sample, "seconds": round(secs, 2),
+                                  "host_cpus": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e(args, ctx, tl, tg, olds, news, out, dev, scanned_total, world, rank, body_total):
+    """Same metric through the public API with host buffers: every step copies old and new
+    from pinned host memory (H2D) and reads the packed body back (D2H), on the same
+    stream as the kernels; CUDA events around the whole step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
+    h_old = [o.cpu().pin_memory() for o in olds]
+    h_new = [w.cpu().pin_memory() for w in news]
+    h_body = torch.empty(out.numel(), dtype=torch.uint8).pin_memory()
+    h2d = sum(o.numel() * o.element_size() * 2 for o in olds)
+    d2h = 0
+
+    def one():
+        nonlocal d2h
+        for o, w, ho, hw in zip(olds, news, h_old, h_new):
+            o.copy_(ho, non_blocking=True)
+            w.copy_(hw, non_blocking=True)
+        size = ctx.delta_size(tl)
+        body, table = ctx.delta_extract(tl, out=out, table=True)
+        h_body[:size].copy_(body, non_blocking=True)
+        ctx.delta_apply(tg, body, table=table)
+        d2h = size
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.e2e_steps):
+        one()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(scanned_total * args.e2e_steps / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "ms_per_step": round(ms / args.e2e_steps, 3),
+            "note": "per rank; old+new H2D from pinned host, body D2H, apply on device"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

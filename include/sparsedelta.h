@@ -1,0 +1,207 @@
+/*
+ * sparsedelta.h — C ABI of the B200 sparse-delta codec (SparrowRL, arXiv 2602.11456).
+ *
+ * The operation (§3 Eq. 1; §5.1 "Sparse encoding",
+ * "Lossless precision"): given K parameter tensors before (W_t) and after (W_{t+1}) one
+ * RL step, the trainer "flattens each tensor's delta into a one-dimensional index space
+ * and stores the non-zeros as two 1D arrays, idx and val", encodes idx by
+ * "delta encoding" — first index as-is, then differences — written as
+ * unsigned LEB128; Actors "apply the update with a flat scatter-add
+ * over the parameter's storage" so they hold "exactly the same update as
+ * the Trainer".
+ *
+ * Readings fixed at this boundary:
+ *   R1 replace mode: values are the NEW lane bits; apply is a scatter-STORE (bit-exact).
+ *   R2 "changed" = bitwise lane inequality (-0.0 vs +0.0 changes; equal NaN bits do not).
+ *   R3 the first index is stored as its absolute value, also LEB128.
+ *   R4 one index space per logical (fused) tensor; the gap chain restarts per record.
+ *   R5 a fused tensor's lanes are its spans concatenated in the order given (Q,K,V; Gate,Up).
+ *
+ * Body layout (little-endian), one record per tensor in descriptor order,
+ * also when nothing changed:
+ *     u16 name_len | name | u64 element_count | u64 nnz | u64 index_bytes |
+ *     index_stream[index_bytes] | values[nnz * w] | u8 mode (= 0, replace)
+ * record_bytes = 27 + name_len + index_bytes + w * nnz.
+ *
+ * Conventions
+ *   - Pointers named *_dev are CUDA global memory on the context's device; everything
+ *     else is host memory.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default stream).  All device work is ordered on `stream`.
+ *   - The caller owns every buffer and descriptor array; they are read only during the
+ *     call (device buffers: until the stream work of the call has completed).
+ *   - The context owns a grow-only device workspace reused across calls; no device
+ *     allocation happens in steady state.  One context per (host thread, stream); a
+ *     context is not thread-safe.
+ *   - Every call returns DELTA_OK (0) or a negative status; delta_last_error() then
+ *     describes it.  Nothing aborts the process.
+ *   - There is no CPU fallback: without a usable CUDA device every call that needs one
+ *     returns DELTA_ECUDA.
+ */
+#ifndef SPARSEDELTA_H
+#define SPARSEDELTA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. */
+enum {
+    DELTA_OK = 0,
+    DELTA_EINVAL = -1,    /* NULL pointer, n_spans == 0, name_len > 65535, bad elem, misaligned target */
+    DELTA_ESHAPE = -2,    /* old/new span structure mismatch */
+    DELTA_ECAPACITY = -3, /* out_capacity too small; *body_bytes holds the size needed */
+    DELTA_ECORRUPT = -4,  /* malformed body; see delta_last_detail() */
+    DELTA_ENAME = -5,     /* record name / element count does not match its target */
+    DELTA_ECUDA = -6,     /* CUDA runtime error or no device */
+    DELTA_ENOMEM = -7     /* device workspace allocation failed */
+};
+
+/* Detail of a DELTA_ECORRUPT / DELTA_ENAME status (delta_last_detail). */
+enum {
+    DELTA_D_NONE = 0,
+    DELTA_D_TRUNCATED = 1,     /* index stream ends inside a varint */
+    DELTA_D_OVERLONG = 2,      /* non-minimal varint, e.g. 80 00 */
+    DELTA_D_OVERFLOW = 3,      /* varint exceeds 64 bits */
+    DELTA_D_NONINCREASING = 4, /* zero gap after the first index */
+    DELTA_D_RANGE = 5,         /* decoded index >= element_count */
+    DELTA_D_COUNT = 6,         /* number of varints != nnz */
+    DELTA_D_NAME = 7,          /* record name != target name */
+    DELTA_D_NUMEL = 8,         /* record element_count != target numel */
+    DELTA_D_MODE = 9,          /* mode byte != 0 (replace) */
+    DELTA_D_LAYOUT = 10        /* record past the body end, trailing bytes, record count != n */
+};
+
+/* Element lane widths (SPEC.md:147 element-type codes). */
+enum { DELTA_ELEM16 = 0, /* bf16 / fp16: 2-byte lanes */
+       DELTA_ELEM32 = 1  /* fp32: 4-byte lanes */ };
+
+/* One contiguous block of a logical tensor (e.g. the q_proj block of qkv_proj).
+ * old_dev / new_dev: numel lanes each, any alignment (16-byte aligned pairs take the
+ * vectorised path, others a lane-by-lane path of the same kernel). */
+typedef struct {
+    const void *old_dev;
+    const void *new_dev;
+    uint64_t numel;
+} delta_span;
+
+/* One logical (fused) tensor: the concatenation of n_spans spans (reading R5).
+ * name: name_len UTF-8 bytes (not NUL-terminated, <= 65535), host memory. */
+typedef struct {
+    const char *name;
+    uint32_t name_len;
+    uint32_t n_spans;
+    const delta_span *spans;
+} delta_tensor;
+
+/* One apply target: the resident fused parameter, numel lanes, lane-aligned. */
+typedef struct {
+    void *w_dev;
+    uint64_t numel;
+    const char *name;
+    uint32_t name_len;
+} delta_target;
+
+/* Per-record offset table row (north_star "per-tensor offset tables"); byte offsets are
+ * relative to the start of the body. */
+typedef struct {
+    uint64_t record_offset;
+    uint64_t element_count;
+    uint64_t nnz;
+    uint64_t index_offset;  /* = record_offset + 2 + name_len + 24 */
+    uint64_t index_bytes;
+    uint64_t values_offset; /* = index_offset + index_bytes */
+    uint64_t record_bytes;  /* = 27 + name_len + index_bytes + w * nnz */
+} delta_record_info;
+
+typedef struct delta_ctx delta_ctx; /* opaque: device, workspace, cached plan + scan */
+
+/* Create a context bound to CUDA device `device` (makes it current on this thread).
+ * *ctx is NULL on failure: DELTA_ECUDA if the device is unusable. */
+int delta_ctx_create(delta_ctx **ctx, int device);
+
+/* Free the context and its workspace.  Waits for no stream; the caller must make sure
+ * no call's device work on this context is still pending.  NULL is a no-op. */
+void delta_ctx_destroy(delta_ctx *ctx);
+
+/* Message for the last non-OK status on this context ("" if none).  Owned by ctx. */
+const char *delta_last_error(const delta_ctx *ctx);
+
+/* DELTA_D_* detail of the last DELTA_ECORRUPT / DELTA_ENAME status. */
+int delta_last_detail(const delta_ctx *ctx);
+
+/* Library build string (compile flags, target arch). */
+const char *delta_version(void);
+
+/* delta_size — size of the packed body for `tensors` (E1-E3 + size readback E7).
+ *
+ * Runs the bitwise compare + ordered compaction over all n tensors (one grouped launch),
+ * the LEB128 length pass and the offset-table pass, then synchronises `stream` once and
+ * writes the body size in bytes to *body_bytes (host).  The compaction is cached on ctx:
+ * a following delta_extract with identical descriptors (same pointers, sizes, names,
+ * elem) reuses it without re-reading old/new — the caller must not modify old/new in
+ * between (two-phase, as CUB's temp-storage query).
+ *   tensors: n descriptors (host); elem: DELTA_ELEM16 or DELTA_ELEM32.
+ * Errors: DELTA_EINVAL, DELTA_ESHAPE (a span with numel but NULL pointers), DELTA_ECUDA,
+ * DELTA_ENOMEM. */
+int delta_size(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int elem,
+               void *stream, uint64_t *body_bytes);
+
+/* delta_extract — write the packed body (records in descriptor order) to out_dev.
+ *
+ * If the previous call on ctx was delta_size with identical descriptors, its cached
+ * compaction is consumed; otherwise the whole extraction runs here.  Synchronises
+ * `stream` once (size readback) and, if `table` is non-NULL, a second time to copy the
+ * n offset-table rows to `table` (host, n entries).  *body_bytes (host, required)
+ * receives the body size.
+ *   out_dev: device buffer of out_capacity bytes, any alignment.
+ * Errors: as delta_size, plus DELTA_ECAPACITY (nothing written; *body_bytes = needed). */
+int delta_extract(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int elem,
+                  void *out_dev, uint64_t out_capacity, delta_record_info *table,
+                  void *stream, uint64_t *body_bytes);
+
+/* delta_apply — validate the whole body, then scatter-store its values into the targets
+ * (A1-A4; "validate fully before mutating").
+ *
+ * targets: n descriptors (host), one per record in body order; each w_dev is lane-aligned.
+ * body_dev: device, body_bytes bytes, any alignment.
+ * table_hint: optional host array of n rows as produced by delta_extract.  With it the
+ *   record headers are located in one parallel pass and every field is re-verified
+ *   against the body; a hint that does not match the body is ignored (the headers are
+ *   then walked sequentially), so a wrong hint can cost time but never correctness.
+ * All-or-nothing: on any non-OK status the targets are bitwise unchanged.  The call
+ * synchronises `stream` once at the end to read the device status word.
+ * Errors: DELTA_EINVAL, DELTA_ECORRUPT, DELTA_ENAME (detail via delta_last_detail),
+ * DELTA_ECUDA, DELTA_ENOMEM. */
+int delta_apply(delta_ctx *ctx, const delta_target *targets, uint32_t n, int elem,
+                const void *body_dev, uint64_t body_bytes,
+                const delta_record_info *table_hint, void *stream);
+
+/* Per-kernel device times of the last delta_size/delta_extract/delta_apply on this ctx,
+ * in milliseconds, measured with CUDA events recorded on the call's stream around each
+ * kernel (only while profiling is enabled; zero otherwise).  A field is the time of the
+ * most recent launch of that kernel; *_count fields say how many launches it covers. */
+typedef struct {
+    float scan_ms;      /* K1 compare + ordered compaction (reads old and new) */
+    float lens_ms;      /* K2 gap LEB128 lengths */
+    float finalize_ms;  /* K3 offset table */
+    float emit_ms;      /* K4 index bytes + values */
+    float headers_ms;   /* K5 record headers */
+    float locate_ms;    /* A1 record headers located + verified */
+    float decode_ms;    /* A2 LEB128 decode + validation */
+    float apply_scan_ms;/* A3 per-record scans + count/range checks */
+    float scatter_ms;   /* A4 gated scatter-store */
+} delta_timing;
+
+/* Enable (1) or disable (0) per-kernel event timing on ctx.  Default: disabled. */
+int delta_set_profiling(delta_ctx *ctx, int enable);
+
+/* Copy the timings of the last calls (see delta_timing) to *out (host). */
+int delta_last_timing(const delta_ctx *ctx, delta_timing *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -97,6 +97,15 @@ def record(name: str, old: list[int], new: list[int], width: int) -> bytes:
             + _u(len(stream), 8) + stream + vals + _u(0, 1))
 
 
+def record_from_sparse(name: str, n: int, idx: list[int], vals: list[int], width: int) -> bytes:
+    """O3..O6 when the change set is given directly (a tensor too large to hold as a
+    Python list, e.g. one with more than 2^32 lanes): idx ascending, vals the new lanes."""
+    nb = name.encode("utf-8")
+    stream = encode_indices(idx)
+    return (_u(len(nb), 2) + nb + _u(n, 8) + _u(len(idx), 8) + _u(len(stream), 8) + stream
+            + b"".join(_u(v, width) for v in vals) + _u(0, 1))
+
+
 def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: int):
     """Body and offset table for (name, old_spans, new_spans) in list order.
 

@@ -1,0 +1,89 @@
+"""ctypes declarations of include/sparsedelta.h (argument marshalling only).
+
+Loads the in-tree ``libsparsedelta.so`` built by ``__graft_entry__.build()``.  There is
+no fallback: if the library is missing or fails to load, importing the binding's
+compute entry points raises.
+"""
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_int, c_uint32, c_uint64, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsparsedelta.so")
+
+DELTA_OK, DELTA_EINVAL, DELTA_ESHAPE, DELTA_ECAPACITY = 0, -1, -2, -3
+DELTA_ECORRUPT, DELTA_ENAME, DELTA_ECUDA, DELTA_ENOMEM = -4, -5, -6, -7
+DELTA_ELEM16, DELTA_ELEM32 = 0, 1
+
+STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "ESHAPE", -3: "ECAPACITY", -4: "ECORRUPT",
+                -5: "ENAME", -6: "ECUDA", -7: "ENOMEM"}
+DETAIL_NAMES = {0: None, 1: "truncated", 2: "overlong", 3: "overflow", 4: "nonincreasing",
+                5: "range", 6: "count", 7: "name", 8: "numel", 9: "mode", 10: "layout"}
+
+# Every symbol include/sparsedelta.h declares (tests/test_abi.py checks the export list).
+EXPORTS = ("delta_ctx_create", "delta_ctx_destroy", "delta_last_error", "delta_last_detail",
+           "delta_version", "delta_size", "delta_extract", "delta_apply", "delta_set_profiling",
+           "delta_last_timing")
+
+
+class Span(ctypes.Structure):
+    _fields_ = [("old_dev", c_void_p), ("new_dev", c_void_p), ("numel", c_uint64)]
+
+
+class Tensor(ctypes.Structure):
+    _fields_ = [("name", c_char_p), ("name_len", c_uint32), ("n_spans", c_uint32),
+                ("spans", POINTER(Span))]
+
+
+class Target(ctypes.Structure):
+    _fields_ = [("w_dev", c_void_p), ("numel", c_uint64), ("name", c_char_p), ("name_len", c_uint32)]
+
+
+class RecordInfo(ctypes.Structure):
+    _fields_ = [("record_offset", c_uint64), ("element_count", c_uint64), ("nnz", c_uint64),
+                ("index_offset", c_uint64), ("index_bytes", c_uint64), ("values_offset", c_uint64),
+                ("record_bytes", c_uint64)]
+
+
+class Timing(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_float) for f in (
+        "scan_ms", "lens_ms", "finalize_ms", "emit_ms", "headers_ms", "locate_ms", "decode_ms",
+        "apply_scan_ms", "scatter_ms")]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded library (loaded once).  Raises if it is missing: no CPU fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built; run __graft_entry__.build() (there is no "
+                               "fallback implementation)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.delta_ctx_create.argtypes = [POINTER(c_void_p), c_int]
+        L.delta_ctx_create.restype = c_int
+        L.delta_ctx_destroy.argtypes = [c_void_p]
+        L.delta_ctx_destroy.restype = None
+        L.delta_last_error.argtypes = [c_void_p]
+        L.delta_last_error.restype = c_char_p
+        L.delta_last_detail.argtypes = [c_void_p]
+        L.delta_last_detail.restype = c_int
+        L.delta_version.argtypes = []
+        L.delta_version.restype = c_char_p
+        L.delta_size.argtypes = [c_void_p, POINTER(Tensor), c_uint32, c_int, c_void_p, POINTER(c_uint64)]
+        L.delta_size.restype = c_int
+        L.delta_extract.argtypes = [c_void_p, POINTER(Tensor), c_uint32, c_int, c_void_p, c_uint64,
+                                    POINTER(RecordInfo), c_void_p, POINTER(c_uint64)]
+        L.delta_extract.restype = c_int
+        L.delta_apply.argtypes = [c_void_p, POINTER(Target), c_uint32, c_int, c_void_p, c_uint64,
+                                  POINTER(RecordInfo), c_void_p]
+        L.delta_apply.restype = c_int
+        L.delta_set_profiling.argtypes = [c_void_p, c_int]
+        L.delta_set_profiling.restype = c_int
+        L.delta_last_timing.argtypes = [c_void_p, POINTER(Timing)]
+        L.delta_last_timing.restype = c_int
+        _lib = L
+    return _lib

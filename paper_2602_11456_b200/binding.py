@@ -1,0 +1,236 @@
+"""Thin Python binding of the C ABI (include/sparsedelta.h): argument marshalling only.
+
+Every step of the path runs in the CUDA kernels behind ``libsparsedelta.so``; this module
+turns torch tensors into descriptor arrays (pointers + sizes), passes the current CUDA
+stream, and turns status codes into exceptions.  PyTorch supplies device memory and
+streams only.
+"""
+
+import ctypes
+from ctypes import byref, c_uint64, c_void_p
+
+import torch
+
+from . import _abi
+from ._abi import RecordInfo, Span, Target, Tensor
+
+_ELEM = {2: _abi.DELTA_ELEM16, 4: _abi.DELTA_ELEM32}
+TABLE_FIELDS = ("record_offset", "element_count", "nnz", "index_offset", "index_bytes",
+                "values_offset", "record_bytes")
+
+
+class DeltaError(RuntimeError):
+    """A non-OK status from the library; ``status``/``detail`` are the C codes and
+    ``kind`` the DELTA_D_* name (e.g. "truncated", "name") when there is one."""
+
+    def __init__(self, status, detail, msg):
+        self.status, self.detail = status, detail
+        self.kind = _abi.DETAIL_NAMES.get(detail)
+        super().__init__(f"{_abi.STATUS_NAMES.get(status, status)}: {msg}")
+
+
+def _stream_handle(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return c_void_p(s.cuda_stream)
+
+
+def _width(t: torch.Tensor) -> int:
+    w = t.element_size()
+    if w not in (2, 4):
+        raise ValueError(f"lanes must be 2 or 4 bytes wide, got {t.dtype}")
+    return w
+
+
+class TensorList:
+    """Descriptor array for a list of logical tensors, built once and reusable.
+
+    ``tensors``: sequence of ``(name, old, new)`` where old/new are CUDA tensors (one
+    span) or equal-length sequences of CUDA tensors (the spans of a fused tensor, in
+    fusion order — PAPER.md:383).  Tensors must stay alive while this object is used."""
+
+    def __init__(self, tensors):
+        self.names = []
+        self._keep = []
+        n = len(tensors)
+        self.arr = (Tensor * max(n, 1))()
+        self.n = n
+        self.width = None
+        self.numel = []
+        self.device = None
+        for k, (name, old, new) in enumerate(tensors):
+            olds = [old] if isinstance(old, torch.Tensor) else list(old)
+            news = [new] if isinstance(new, torch.Tensor) else list(new)
+            if len(olds) != len(news) or not olds:
+                raise ValueError(f"tensor {name!r}: old/new span lists differ")
+            spans = (Span * len(olds))()
+            tot = 0
+            for s, (o, w) in enumerate(zip(olds, news)):
+                if not (o.is_cuda and w.is_cuda):
+                    raise ValueError(f"tensor {name!r}: spans must be CUDA tensors")
+                if o.numel() != w.numel() or o.element_size() != w.element_size():
+                    raise ValueError(f"tensor {name!r} span {s}: old/new shape or width differ")
+                if not (o.is_contiguous() and w.is_contiguous()):
+                    raise ValueError(f"tensor {name!r} span {s}: spans must be contiguous")
+                ww = _width(o)
+                if self.width is None:
+                    self.width = ww
+                elif self.width != ww:
+                    raise ValueError("all tensors must have the same lane width (SPEC.md:34)")
+                self.device = o.device if self.device is None else self.device
+                spans[s].old_dev = o.data_ptr()
+                spans[s].new_dev = w.data_ptr()
+                spans[s].numel = o.numel()
+                tot += o.numel()
+            nb = name.encode("utf-8")
+            self.arr[k].name = nb
+            self.arr[k].name_len = len(nb)
+            self.arr[k].n_spans = len(olds)
+            self.arr[k].spans = spans
+            self._keep += [nb, spans, olds, news]
+            self.names.append(name)
+            self.numel.append(tot)
+        if self.width is None:
+            self.width = 2
+
+
+class TargetList:
+    """Descriptor array for apply targets: sequence of ``(name, w)`` with ``w`` the
+    resident fused parameter (contiguous CUDA tensor)."""
+
+    def __init__(self, targets):
+        n = len(targets)
+        self.arr = (Target * max(n, 1))()
+        self.n = n
+        self._keep = []
+        self.width = None
+        for k, (name, w) in enumerate(targets):
+            if not w.is_cuda or not w.is_contiguous():
+                raise ValueError(f"target {name!r} must be a contiguous CUDA tensor")
+            ww = _width(w)
+            if self.width is None:
+                self.width = ww
+            elif self.width != ww:
+                raise ValueError("all targets must have the same lane width")
+            nb = name.encode("utf-8")
+            self.arr[k].w_dev = w.data_ptr()
+            self.arr[k].numel = w.numel()
+            self.arr[k].name = nb
+            self.arr[k].name_len = len(nb)
+            self._keep += [nb, w]
+        if self.width is None:
+            self.width = 2
+
+
+class DeltaContext:
+    """One ``delta_ctx`` (device workspace + cached plan) bound to a CUDA device."""
+
+    def __init__(self, device=None):
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = dev
+        self._lib = _abi.lib()
+        h = c_void_p()
+        rc = self._lib.delta_ctx_create(byref(h), dev.index)
+        if rc != 0:
+            raise DeltaError(rc, 0, f"delta_ctx_create(device={dev.index}) failed")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            torch.cuda.synchronize(self.device)
+            self._lib.delta_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = self._lib.delta_last_error(self._h).decode(errors="replace")
+            raise DeltaError(rc, self._lib.delta_last_detail(self._h), msg)
+
+    def set_profiling(self, enable: bool):
+        """Per-kernel CUDA-event timing inside the library (see delta_last_timing)."""
+        self._check(self._lib.delta_set_profiling(self._h, 1 if enable else 0))
+
+    def last_timing(self) -> dict:
+        t = _abi.Timing()
+        self._check(self._lib.delta_last_timing(self._h, byref(t)))
+        return {f: getattr(t, f) for f, _ in _abi.Timing._fields_}
+
+    # --------------------------------------------------------------- C-ABI mirrors
+    def delta_size(self, tensors, stream=None) -> int:
+        """Body size in bytes (runs and caches the compare + compaction)."""
+        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        out = c_uint64()
+        self._check(self._lib.delta_size(self._h, tl.arr, tl.n, _ELEM[tl.width],
+                                         _stream_handle(stream), byref(out)))
+        return out.value
+
+    def delta_extract(self, tensors, out=None, stream=None, table=True):
+        """Pack the delta.  Returns ``(body, rows)``: ``body`` a uint8 CUDA tensor view of
+        exactly the body bytes (``out``'s prefix if ``out`` is given), ``rows`` a list of
+        offset-table tuples (TABLE_FIELDS order) or None if ``table`` is False."""
+        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        st = _stream_handle(stream)
+        nbytes = c_uint64()
+        rows = (RecordInfo * max(tl.n, 1))() if table else None
+        if out is None:
+            self._check(self._lib.delta_size(self._h, tl.arr, tl.n, _ELEM[tl.width], st, byref(nbytes)))
+            out = torch.empty(max(nbytes.value, 1), dtype=torch.uint8, device=tl.device or self.device)
+        if out.dtype != torch.uint8 or not out.is_contiguous() or not out.is_cuda:
+            raise ValueError("out must be a contiguous uint8 CUDA tensor")
+        self._check(self._lib.delta_extract(self._h, tl.arr, tl.n, _ELEM[tl.width], out.data_ptr(),
+                                            out.numel(), rows, st, byref(nbytes)))
+        body = out[:nbytes.value]
+        if rows is None:
+            return body, None
+        return body, [tuple(getattr(rows[k], f) for f in TABLE_FIELDS) for k in range(tl.n)]
+
+    def delta_apply(self, targets, body, table=None, stream=None):
+        """Validate ``body`` fully, then scatter its values into ``targets`` in place
+        (all-or-nothing).  ``table``: optional offset-table rows from delta_extract."""
+        tg = targets if isinstance(targets, TargetList) else TargetList(targets)
+        if body.dtype != torch.uint8 or not body.is_contiguous() or not body.is_cuda:
+            raise ValueError("body must be a contiguous uint8 CUDA tensor")
+        hint = None
+        if table is not None:
+            hint = table if isinstance(table, ctypes.Array) else _rows_to_ctypes(table)
+        self._check(self._lib.delta_apply(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(),
+                                          body.numel(), hint, _stream_handle(stream)))
+
+
+def _rows_to_ctypes(rows):
+    arr = (RecordInfo * max(len(rows), 1))()
+    for k, r in enumerate(rows):
+        for f, v in zip(TABLE_FIELDS, r):
+            setattr(arr[k], f, int(v))
+    return arr
+
+
+_default = {}
+
+
+def context(device=None) -> DeltaContext:
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    if dev not in _default:
+        _default[dev] = DeltaContext(torch.device("cuda", dev))
+    return _default[dev]
+
+
+def delta_size(tensors, stream=None) -> int:
+    return context().delta_size(tensors, stream=stream)
+
+
+def delta_extract(tensors, out=None, stream=None, table=True):
+    return context().delta_extract(tensors, out=out, stream=stream, table=table)
+
+
+def delta_apply(targets, body, table=None, stream=None):
+    return context().delta_apply(targets, body, table=table, stream=stream)
+
+
+def version() -> str:
+    return _abi.lib().delta_version().decode()

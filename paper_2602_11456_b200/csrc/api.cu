@@ -1,0 +1,538 @@
+// api.cu — the C ABI of include/sparsedelta.h: context, workspace, extract plan (tile
+// table) cache, descriptor validation, kernel launches, size readback and error reporting.
+// Host code compiled by nvcc into libsparsedelta.so (static cudart).  Product code.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sparsedelta.h"
+#include "sd_internal.cuh"
+
+using namespace sd;
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int grow(size_t bytes) {  // grow-only; contents are not preserved
+        if (bytes <= cap) return DELTA_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(bytes, 256);
+        if (cudaMalloc(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            return DELTA_ENOMEM;
+        }
+        cap = want;
+        return DELTA_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T> T *as() const { return static_cast<T *>(p); }
+};
+
+uint64_t fnv(uint64_t h, const void *data, size_t n) {
+    const uint8_t *b = static_cast<const uint8_t *>(data);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= b[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+}  // namespace
+
+struct delta_ctx {
+    int device = 0;
+    int sm_count = 148;
+    std::string err;
+    int detail = DELTA_D_NONE;
+
+    // ---- extract plan (rebuilt only when the descriptor key changes)
+    uint64_t plan_key = 0;
+    bool plan_valid = false;
+    uint32_t ntiles = 0, ntensors = 0;
+    int width = 2;
+    bool idx64 = false;
+    unsigned long long total_lanes = 0;
+    DevBuf tiles, name_len, name_off, names, numel;
+    // ---- extract workspace
+    DevBuf tile_state, ticket, ws_idx, ws_val, entry_begin, tstart_partial, chunk_bytes,
+        chunk_prefix, tensor_byte_begin, table, summary;
+    unsigned long long ws_cap = 0;  // entries
+    bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
+    ExtractSummary *h_summary = nullptr;  // pinned
+
+    // ---- apply workspace
+    DevBuf a_targets, a_names, a_hint, a_recs, a_rcb, a_cnt, a_sum, a_ord, a_idx, a_state;
+    ApplyState *h_state = nullptr;  // pinned
+
+    // ---- optional per-kernel event timing
+    bool profiling = false;
+    cudaEvent_t ev_scan[4] = {}, ev_emit[3] = {}, ev_apply[5] = {};
+    delta_timing timing = {};
+};
+
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.f;
+    }
+    return ms;
+}
+
+static int fail(delta_ctx *c, int code, int detail, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        c->detail = detail;
+    }
+    return code;
+}
+
+static int cuda_fail(delta_ctx *c, cudaError_t e, const char *where) {
+    return fail(c, DELTA_ECUDA, DELTA_D_NONE, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(call, where)                                       \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, where); \
+    } while (0)
+
+#define GROW(buf, bytes)                                                                  \
+    do {                                                                                  \
+        if ((buf).grow(bytes) != DELTA_OK)                                                \
+            return fail(ctx, DELTA_ENOMEM, DELTA_D_NONE, "device allocation of %zu bytes failed", \
+                        (size_t)(bytes));                                                 \
+    } while (0)
+
+extern "C" {
+
+const char *delta_version(void) {
+    return "sparsedelta 1 (sm_100a; K1 ticket/look-back scan, LEB128 emit, gated scatter)";
+}
+
+int delta_ctx_create(delta_ctx **out, int device) {
+    if (!out) return DELTA_EINVAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return DELTA_ECUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return DELTA_ECUDA;
+    delta_ctx *c = new delta_ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMallocHost(&c->h_summary, sizeof(ExtractSummary)) != cudaSuccess ||
+        cudaMallocHost(&c->h_state, sizeof(ApplyState)) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return DELTA_ECUDA;
+    }
+    *out = c;
+    return DELTA_OK;
+}
+
+void delta_ctx_destroy(delta_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
+                      &c->tile_state, &c->ticket, &c->ws_idx, &c->ws_val, &c->entry_begin,
+                      &c->tstart_partial, &c->chunk_bytes, &c->chunk_prefix,
+                      &c->tensor_byte_begin, &c->table, &c->summary, &c->a_targets,
+                      &c->a_names, &c->a_hint, &c->a_recs, &c->a_rcb, &c->a_cnt, &c->a_sum,
+                      &c->a_ord, &c->a_idx, &c->a_state};
+    for (DevBuf *b : bufs) b->release();
+    if (c->profiling) {
+        for (auto &e : c->ev_scan) cudaEventDestroy(e);
+        for (auto &e : c->ev_emit) cudaEventDestroy(e);
+        for (auto &e : c->ev_apply) cudaEventDestroy(e);
+    }
+    if (c->h_summary) cudaFreeHost(c->h_summary);
+    if (c->h_state) cudaFreeHost(c->h_state);
+    delete c;
+}
+
+const char *delta_last_error(const delta_ctx *c) { return c ? c->err.c_str() : "no context"; }
+
+int delta_last_detail(const delta_ctx *c) { return c ? c->detail : DELTA_D_NONE; }
+
+int delta_set_profiling(delta_ctx *c, int enable) {
+    if (!c) return DELTA_EINVAL;
+    if (cudaSetDevice(c->device) != cudaSuccess) return DELTA_ECUDA;
+    if (enable && !c->profiling) {
+        for (auto &e : c->ev_scan) cudaEventCreate(&e);
+        for (auto &e : c->ev_emit) cudaEventCreate(&e);
+        for (auto &e : c->ev_apply) cudaEventCreate(&e);
+        if (cudaGetLastError() != cudaSuccess) return DELTA_ECUDA;
+        c->profiling = true;
+    } else if (!enable && c->profiling) {
+        cudaDeviceSynchronize();
+        for (auto &e : c->ev_scan) cudaEventDestroy(e);
+        for (auto &e : c->ev_emit) cudaEventDestroy(e);
+        for (auto &e : c->ev_apply) cudaEventDestroy(e);
+        c->profiling = false;
+    }
+    c->timing = delta_timing{};
+    return DELTA_OK;
+}
+
+int delta_last_timing(const delta_ctx *c, delta_timing *out) {
+    if (!c || !out) return DELTA_EINVAL;
+    *out = c->timing;
+    return DELTA_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------- extract
+static int elem_width(int elem) { return elem == DELTA_ELEM16 ? 2 : (elem == DELTA_ELEM32 ? 4 : 0); }
+
+static int validate_tensors(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int w) {
+    if (n && !t) return fail(ctx, DELTA_EINVAL, 0, "tensors is NULL");
+    if (n >= (1u << 30)) return fail(ctx, DELTA_EINVAL, 0, "too many tensors (%u)", n);
+    for (uint32_t k = 0; k < n; ++k) {
+        if (t[k].name_len > 0xFFFF)
+            return fail(ctx, DELTA_EINVAL, 0, "tensor %u: name_len %u exceeds u16 (SPEC.md:148)", k,
+                        t[k].name_len);
+        if (t[k].name_len && !t[k].name) return fail(ctx, DELTA_EINVAL, 0, "tensor %u: name is NULL", k);
+        if (t[k].n_spans == 0 || !t[k].spans)
+            return fail(ctx, DELTA_EINVAL, 0, "tensor %u: no spans", k);
+        for (uint32_t s = 0; s < t[k].n_spans; ++s) {
+            const delta_span &sp = t[k].spans[s];
+            if (sp.numel && (!sp.old_dev || !sp.new_dev))
+                return fail(ctx, DELTA_ESHAPE, 0, "tensor %u span %u: NULL old/new with numel %llu", k, s,
+                            (unsigned long long)sp.numel);
+            if ((reinterpret_cast<uintptr_t>(sp.old_dev) | reinterpret_cast<uintptr_t>(sp.new_dev)) % w)
+                return fail(ctx, DELTA_EINVAL, 0, "tensor %u span %u: pointers not %d-byte aligned", k, s, w);
+        }
+    }
+    return DELTA_OK;
+}
+
+static uint64_t plan_key_of(const delta_tensor *t, uint32_t n, int w) {
+    uint64_t h = 1469598103934665603ull;
+    h = fnv(h, &w, sizeof w);
+    h = fnv(h, &n, sizeof n);
+    for (uint32_t k = 0; k < n; ++k) {
+        h = fnv(h, &t[k].name_len, sizeof t[k].name_len);
+        h = fnv(h, t[k].name, t[k].name_len);
+        h = fnv(h, &t[k].n_spans, sizeof t[k].n_spans);
+        h = fnv(h, t[k].spans, sizeof(delta_span) * t[k].n_spans);
+    }
+    return h;
+}
+
+static int build_plan(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int w, cudaStream_t s) {
+    const uint64_t key = plan_key_of(t, n, w);
+    if (ctx->plan_valid && ctx->plan_key == key) return DELTA_OK;
+    ctx->plan_valid = false;
+    ctx->scan_cached = false;
+    const uint32_t lanes_per_tile = kTileBytes / w;
+    std::vector<TileDesc> tiles;
+    std::vector<uint32_t> nlen(n), noff(n);
+    std::vector<unsigned long long> numel(n);
+    std::string blob;
+    unsigned long long total = 0, maxn = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+        nlen[k] = t[k].name_len;
+        noff[k] = (uint32_t)blob.size();
+        blob.append(t[k].name ? t[k].name : "", t[k].name_len);
+        unsigned long long base = 0;
+        bool first = true;
+        for (uint32_t sidx = 0; sidx < t[k].n_spans; ++sidx) {
+            const delta_span &sp = t[k].spans[sidx];
+            const bool aligned = ((reinterpret_cast<uintptr_t>(sp.old_dev) |
+                                   reinterpret_cast<uintptr_t>(sp.new_dev)) % 16) == 0;
+            for (unsigned long long off = 0; off < sp.numel; off += lanes_per_tile) {
+                TileDesc d;
+                d.old_p = static_cast<const uint8_t *>(sp.old_dev) + off * w;
+                d.new_p = static_cast<const uint8_t *>(sp.new_dev) + off * w;
+                d.lane_base = base + off;
+                d.nlanes = (uint32_t)std::min<unsigned long long>(lanes_per_tile, sp.numel - off);
+                d.flags_tensor = k | (first ? kTileFirstOfTensor : 0u) | (aligned ? kTileAligned : 0u);
+                first = false;
+                tiles.push_back(d);
+            }
+            base += sp.numel;
+        }
+        if (first) {  // empty tensor: a placeholder tile records its entry offset E_k
+            TileDesc d{};
+            d.flags_tensor = k | kTileFirstOfTensor;
+            tiles.push_back(d);
+        }
+        numel[k] = base;
+        total += base;
+        maxn = std::max(maxn, base);
+    }
+    if (tiles.empty()) {  // n == 0: one placeholder so K1 still writes M = 0
+        TileDesc d{};
+        tiles.push_back(d);
+    }
+    if (tiles.size() >= 0x7FFFFFFFull) return fail(ctx, DELTA_EINVAL, 0, "too many tiles");
+    GROW(ctx->tiles, tiles.size() * sizeof(TileDesc));
+    GROW(ctx->name_len, std::max<size_t>(n, 1) * 4);
+    GROW(ctx->name_off, std::max<size_t>(n, 1) * 4);
+    GROW(ctx->names, std::max<size_t>(blob.size(), 1));
+    GROW(ctx->numel, std::max<size_t>(n, 1) * 8);
+    CK(cudaMemcpyAsync(ctx->tiles.p, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice, s), "upload tiles");
+    if (n) {
+        CK(cudaMemcpyAsync(ctx->name_len.p, nlen.data(), n * 4, cudaMemcpyHostToDevice, s), "upload");
+        CK(cudaMemcpyAsync(ctx->name_off.p, noff.data(), n * 4, cudaMemcpyHostToDevice, s), "upload");
+        CK(cudaMemcpyAsync(ctx->numel.p, numel.data(), n * 8, cudaMemcpyHostToDevice, s), "upload");
+    }
+    if (!blob.empty()) CK(cudaMemcpyAsync(ctx->names.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s), "upload");
+    // the host vectors die at return: make the pageable copies complete first
+    CK(cudaStreamSynchronize(s), "plan upload");
+    ctx->ntiles = (uint32_t)tiles.size();
+    ctx->ntensors = n;
+    ctx->width = w;
+    ctx->idx64 = maxn > 0xFFFFFFFFull;
+    ctx->total_lanes = total;
+    ctx->plan_key = key;
+    ctx->plan_valid = true;
+    return DELTA_OK;
+}
+
+static ExtractArgs extract_args(delta_ctx *ctx) {
+    ExtractArgs a;
+    a.tiles = ctx->tiles.as<TileDesc>();
+    a.ntiles = ctx->ntiles;
+    a.ntensors = ctx->ntensors;
+    a.tile_state = ctx->tile_state.as<unsigned long long>();
+    a.ticket = ctx->ticket.as<unsigned int>();
+    a.ws_idx = ctx->ws_idx.p;
+    a.ws_val = ctx->ws_val.p;
+    a.ws_cap = ctx->ws_cap;
+    a.entry_begin = ctx->entry_begin.as<unsigned long long>();
+    a.tstart_partial = ctx->tstart_partial.as<unsigned long long>();
+    a.chunk_bytes = ctx->chunk_bytes.as<unsigned int>();
+    a.chunk_prefix = ctx->chunk_prefix.as<unsigned long long>();
+    a.chunk_cap = ctx->ws_cap / kEntryChunk + 2;
+    a.tensor_byte_begin = ctx->tensor_byte_begin.as<unsigned long long>();
+    a.table = ctx->table.as<RecordRow>();
+    a.name_len = ctx->name_len.as<uint32_t>();
+    a.name_off = ctx->name_off.as<uint32_t>();
+    a.names = ctx->names.as<uint8_t>();
+    a.numel = ctx->numel.as<unsigned long long>();
+    a.summary = ctx->summary.as<ExtractSummary>();
+    a.width = ctx->width;
+    a.idx64 = ctx->idx64;
+    a.persist_ctas = ctx->sm_count * 8;
+    return a;
+}
+
+static int reserve_entries(delta_ctx *ctx, unsigned long long cap) {
+    const size_t isz = ctx->idx64 ? 8 : 4;
+    GROW(ctx->ws_idx, cap * isz + 64);
+    GROW(ctx->ws_val, cap * ctx->width + 64);
+    const size_t nch = cap / kEntryChunk + 2;
+    GROW(ctx->chunk_bytes, nch * 4);
+    GROW(ctx->chunk_prefix, nch * 8);
+    ctx->ws_cap = cap;
+    return DELTA_OK;
+}
+
+// K1-K3 + the single size readback; retries once with a larger entry workspace.
+static int run_scan(delta_ctx *ctx, cudaStream_t s) {
+    const uint32_t T = ctx->ntensors;
+    GROW(ctx->tile_state, (size_t)ctx->ntiles * 8);
+    GROW(ctx->ticket, 4);
+    GROW(ctx->entry_begin, (size_t)(T + 1) * 8);
+    GROW(ctx->tstart_partial, (size_t)(T + 1) * 8);
+    GROW(ctx->tensor_byte_begin, (size_t)(T + 1) * 8);
+    GROW(ctx->table, (size_t)std::max<uint32_t>(T, 1) * sizeof(RecordRow));
+    GROW(ctx->summary, sizeof(ExtractSummary));
+    if (ctx->ws_cap == 0) {
+        // first guess: 3% of the lanes (grows to the exact need on overflow)
+        unsigned long long guess = std::max<unsigned long long>(1ull << 20, ctx->total_lanes / 32);
+        int rc = reserve_entries(ctx, guess);
+        if (rc) return rc;
+    }
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        CK(cudaMemsetAsync(ctx->tile_state.p, 0, (size_t)ctx->ntiles * 8, s), "memset");
+        CK(cudaMemsetAsync(ctx->ticket.p, 0, 4, s), "memset");
+        CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
+        CK(launch_extract_scan(extract_args(ctx), s, ctx->profiling ? ctx->ev_scan : nullptr),
+           "extract scan launch");
+        CK(cudaMemcpyAsync(ctx->h_summary, ctx->summary.p, sizeof(ExtractSummary), cudaMemcpyDeviceToHost, s), "readback");
+        CK(cudaStreamSynchronize(s), "extract scan");
+        if (ctx->profiling) {
+            ctx->timing.scan_ms = ev_ms(ctx->ev_scan[0], ctx->ev_scan[1]);
+            ctx->timing.lens_ms = ev_ms(ctx->ev_scan[1], ctx->ev_scan[2]);
+            ctx->timing.finalize_ms = ev_ms(ctx->ev_scan[2], ctx->ev_scan[3]);
+        }
+        if (!ctx->h_summary->overflow) {
+            ctx->scan_cached = true;
+            return DELTA_OK;
+        }
+        const unsigned long long need = ctx->h_summary->M;
+        int rc = reserve_entries(ctx, need + need / 8 + 1024);
+        if (rc) return rc;
+    }
+    return fail(ctx, DELTA_ENOMEM, 0, "entry workspace overflow after resize");
+}
+
+extern "C" int delta_size(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *stream,
+                          uint64_t *body_bytes) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    const int w = elem_width(elem);
+    if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
+    if (!body_bytes) return fail(ctx, DELTA_EINVAL, 0, "body_bytes is NULL");
+    int rc = validate_tensors(ctx, t, n, w);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rc = build_plan(ctx, t, n, w, s);
+    if (rc) return rc;
+    rc = run_scan(ctx, s);
+    if (rc) return rc;
+    *body_bytes = ctx->h_summary->body_bytes;
+    return DELTA_OK;
+}
+
+extern "C" int delta_extract(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *out,
+                             uint64_t cap, delta_record_info *table, void *stream,
+                             uint64_t *body_bytes) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    const int w = elem_width(elem);
+    if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
+    if (!body_bytes) return fail(ctx, DELTA_EINVAL, 0, "body_bytes is NULL");
+    int rc = validate_tensors(ctx, t, n, w);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t key = plan_key_of(t, n, w);
+    const bool reuse = ctx->scan_cached && ctx->plan_valid && ctx->plan_key == key;
+    if (!reuse) {
+        rc = build_plan(ctx, t, n, w, s);
+        if (rc) return rc;
+        rc = run_scan(ctx, s);
+        if (rc) return rc;
+    }
+    ctx->scan_cached = false;  // consumed
+    const unsigned long long need = ctx->h_summary->body_bytes;
+    *body_bytes = need;
+    if (need > cap)
+        return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < body size %llu",
+                    (unsigned long long)cap, need);
+    if (need && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
+    if (n)
+        CK(launch_extract_emit(extract_args(ctx), static_cast<uint8_t *>(out), s,
+                               ctx->profiling ? ctx->ev_emit : nullptr),
+           "extract emit launch");
+    if (table && n) {
+        CK(cudaMemcpyAsync(table, ctx->table.p, (size_t)n * sizeof(RecordRow), cudaMemcpyDeviceToHost, s), "table readback");
+    }
+    if ((table && n) || (ctx->profiling && n)) CK(cudaStreamSynchronize(s), "extract emit");
+    if (ctx->profiling && n) {
+        ctx->timing.emit_ms = ev_ms(ctx->ev_emit[0], ctx->ev_emit[1]);
+        ctx->timing.headers_ms = ev_ms(ctx->ev_emit[1], ctx->ev_emit[2]);
+    }
+    return DELTA_OK;
+}
+
+// --------------------------------------------------------------------------- apply
+static const int kDetailToStatus[] = {
+    DELTA_OK,        DELTA_ECORRUPT, DELTA_ECORRUPT, DELTA_ECORRUPT, DELTA_ECORRUPT, DELTA_ECORRUPT,
+    DELTA_ECORRUPT,  DELTA_ENAME,    DELTA_ENAME,    DELTA_ECORRUPT, DELTA_ECORRUPT};
+static const char *kDetailName[] = {"ok", "truncated varint", "overlong varint", "varint exceeds 64 bits",
+                                    "non-increasing index", "index >= element_count", "index count != nnz",
+                                    "record name != target name", "record element_count != target numel",
+                                    "mode byte != 0", "record layout"};
+
+extern "C" int delta_apply(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem,
+                           const void *body, uint64_t body_bytes, const delta_record_info *hint,
+                           void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    const int w = elem_width(elem);
+    if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
+    if (n && !tg) return fail(ctx, DELTA_EINVAL, 0, "targets is NULL");
+    if (body_bytes && !body) return fail(ctx, DELTA_EINVAL, 0, "body_dev is NULL");
+    std::vector<TargetDesc> td(n);
+    std::string blob;
+    for (uint32_t k = 0; k < n; ++k) {
+        if (tg[k].name_len > 0xFFFF || (tg[k].name_len && !tg[k].name))
+            return fail(ctx, DELTA_EINVAL, 0, "target %u: bad name", k);
+        if (tg[k].numel && !tg[k].w_dev) return fail(ctx, DELTA_EINVAL, 0, "target %u: NULL w_dev", k);
+        if (reinterpret_cast<uintptr_t>(tg[k].w_dev) % w)
+            return fail(ctx, DELTA_EINVAL, 0, "target %u: w_dev not %d-byte aligned", k, w);
+        td[k].w = static_cast<uint8_t *>(tg[k].w_dev);
+        td[k].numel = tg[k].numel;
+        td[k].name_off = (uint32_t)blob.size();
+        td[k].name_len = tg[k].name_len;
+        blob.append(tg[k].name ? tg[k].name : "", tg[k].name_len);
+    }
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t nn = std::max<uint32_t>(n, 1);
+    GROW(ctx->a_targets, nn * sizeof(TargetDesc));
+    GROW(ctx->a_names, std::max<size_t>(blob.size(), 1));
+    GROW(ctx->a_recs, nn * sizeof(ApplyRec));
+    GROW(ctx->a_rcb, (nn + 1) * 8);
+    GROW(ctx->a_state, sizeof(ApplyState));
+    const size_t nch = body_bytes / kByteChunk + n + 2;
+    GROW(ctx->a_cnt, nch * 4);
+    GROW(ctx->a_sum, nch * 8);
+    GROW(ctx->a_ord, nch * 8);
+    GROW(ctx->a_idx, nch * 8);
+    if (hint && n) GROW(ctx->a_hint, n * sizeof(RecordRow));
+    // pageable sources: these copies complete before the call returns (sync below)
+    if (n) CK(cudaMemcpyAsync(ctx->a_targets.p, td.data(), n * sizeof(TargetDesc), cudaMemcpyHostToDevice, s), "upload");
+    if (!blob.empty()) CK(cudaMemcpyAsync(ctx->a_names.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s), "upload");
+    if (hint && n) CK(cudaMemcpyAsync(ctx->a_hint.p, hint, n * sizeof(RecordRow), cudaMemcpyHostToDevice, s), "upload");
+    CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(ApplyState), s), "memset");
+    ApplyArgs a;
+    a.body = static_cast<const uint8_t *>(body);
+    a.body_bytes = body_bytes;
+    a.targets = ctx->a_targets.as<TargetDesc>();
+    a.n = n;
+    a.names = ctx->a_names.as<uint8_t>();
+    a.hint = (hint && n) ? ctx->a_hint.as<RecordRow>() : nullptr;
+    a.recs = ctx->a_recs.as<ApplyRec>();
+    a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
+    a.chunk_count = ctx->a_cnt.as<unsigned int>();
+    a.chunk_sum = ctx->a_sum.as<unsigned long long>();
+    a.chunk_ord_base = ctx->a_ord.as<unsigned long long>();
+    a.chunk_idx_base = ctx->a_idx.as<unsigned long long>();
+    a.chunk_cap = nch;
+    a.state = ctx->a_state.as<ApplyState>();
+    a.width = w;
+    a.persist_ctas = ctx->sm_count * 8;
+    CK(launch_apply(a, s, ctx->profiling ? ctx->ev_apply : nullptr), "apply launch");
+    CK(cudaMemcpyAsync(ctx->h_state, ctx->a_state.p, sizeof(ApplyState), cudaMemcpyDeviceToHost, s), "status readback");
+    CK(cudaStreamSynchronize(s), "apply");
+    if (ctx->profiling) {
+        ctx->timing.locate_ms = ev_ms(ctx->ev_apply[0], ctx->ev_apply[1]);
+        ctx->timing.decode_ms = ev_ms(ctx->ev_apply[1], ctx->ev_apply[2]);
+        ctx->timing.apply_scan_ms = ev_ms(ctx->ev_apply[2], ctx->ev_apply[3]);
+        ctx->timing.scatter_ms = ev_ms(ctx->ev_apply[3], ctx->ev_apply[4]);
+    }
+    const uint32_t st = ctx->h_state->status;
+    if (st == 0) return DELTA_OK;
+    if (st > 10) return fail(ctx, DELTA_ECORRUPT, (int)st, "unknown status %u", st);
+    return fail(ctx, kDetailToStatus[st], (int)st, "delta_apply: %s", kDetailName[st]);
+}

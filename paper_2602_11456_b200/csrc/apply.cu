@@ -1,0 +1,358 @@
+// apply.cu — sm_100a kernels for delta application.
+//
+//   A1 k_locate        header walk: find every record, check it fits the body, its mode
+//                      byte, its name and element count against the target.
+//                      With a table hint all records are verified in one parallel pass;
+//                      otherwise (or if any hint field disagrees with the body) one thread
+//                      walks the records in order.
+//   A2 k_decode_count  parallel LEB128 decode of 4 KiB index-stream chunks: terminator
+//                      bytes (MSB clear) end an entry; each entry is decoded by reading
+//                      back from its terminator; strict checks (truncated, overlong,
+//                      > 64-bit, zero gap after the first, gap >= N); per-chunk entry count
+//                      and gap sum.
+//   A3 k_apply_scan    per record: scan of chunk (count, gap sum) -> each chunk's ordinal
+//                      and index base; count == nnz and last index < N.
+//   A4 k_scatter       gated on the device status word (all-or-nothing):
+//                      decode again, absolute index = base + running gap sum, value read
+//                      from the record's value array, W[index] = value (replace mode, R1).
+//
+// Product code; shares nothing with oracle/.
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+#include "sd_device.cuh"
+#include "sd_internal.cuh"
+
+namespace sd {
+
+__device__ __forceinline__ void set_status(ApplyState *st, uint32_t code) {
+    atomicCAS(&st->status, 0u, code);
+}
+
+__device__ __forceinline__ unsigned long long rd_le(const uint8_t *p, int nbytes) {
+    unsigned long long x = 0;
+    for (int b = 0; b < nbytes; ++b) x |= (unsigned long long)p[b] << (8 * b);
+    return x;
+}
+
+// ------------------------------------------------------------------------------ A1
+// Checks one record header at `ro` against target k; returns a status code and the
+// record's geometry.  Bounds are checked before every read (the body is untrusted).
+__device__ uint32_t check_record(const uint8_t *body, unsigned long long body_bytes,
+                                 unsigned long long ro, const TargetDesc &tg,
+                                 const uint8_t *names, int width, ApplyRec &rec,
+                                 unsigned long long &end) {
+    if (ro > body_bytes || body_bytes - ro < 2) return kLayout;
+    const unsigned long long nl = rd_le(body + ro, 2);
+    if (body_bytes - ro - 2 < nl + 24) return kLayout;
+    const unsigned long long p = ro + 2 + nl;
+    const unsigned long long N = rd_le(body + p, 8);
+    const unsigned long long nnz = rd_le(body + p + 8, 8);
+    const unsigned long long ilen = rd_le(body + p + 16, 8);
+    const unsigned long long q = p + 24;
+    const unsigned long long rem = body_bytes - q;
+    if (ilen > rem || nnz > (rem - ilen) / (unsigned long long)width) return kLayout;
+    end = q + ilen + nnz * width + 1;
+    if (end > body_bytes) return kLayout;
+    if (body[end - 1] != 0) return kMode;
+    if (nl != tg.name_len) return kName;
+    for (unsigned long long b = 0; b < nl; ++b)
+        if (body[ro + 2 + b] != names[tg.name_off + b]) return kName;
+    if (N != tg.numel) return kNumel;
+    rec.idx_off = q;
+    rec.idx_len = ilen;
+    rec.val_off = q + ilen;
+    rec.nnz = nnz;
+    rec.numel = N;
+    rec.w = tg.w;
+    return kOk;
+}
+
+__global__ void __launch_bounds__(256)
+k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
+         const TargetDesc *__restrict__ tg, uint32_t n, const uint8_t *__restrict__ names,
+         const RecordRow *__restrict__ hint, ApplyRec *__restrict__ recs,
+         unsigned long long *__restrict__ rec_chunk_begin, ApplyState *st, int width) {
+    bool ok = hint != nullptr;
+    if (hint != nullptr) {
+        for (uint32_t k = threadIdx.x; k < n && ok; k += blockDim.x) {
+            const RecordRow h = hint[k];
+            const unsigned long long expect_ro =
+                k == 0 ? 0ull : hint[k - 1].record_offset + hint[k - 1].record_bytes;
+            ApplyRec r;
+            unsigned long long end = 0;
+            if (h.record_offset != expect_ro ||
+                check_record(body, body_bytes, h.record_offset, tg[k], names, width, r, end) != kOk ||
+                end - h.record_offset != h.record_bytes || r.idx_off != h.index_offset ||
+                r.idx_len != h.index_bytes || r.nnz != h.nnz || r.val_off != h.values_offset ||
+                (k == n - 1 && end != body_bytes)) {
+                ok = false;
+            } else {
+                recs[k] = r;
+            }
+        }
+    }
+    ok = __syncthreads_and(ok) && (n > 0 || body_bytes == 0);
+    if (!ok && threadIdx.x == 0) {  // authoritative sequential walk
+        unsigned long long pos = 0;
+        uint32_t code = kOk;
+        for (uint32_t k = 0; k < n && code == kOk; ++k) {
+            unsigned long long end = 0;
+            code = check_record(body, body_bytes, pos, tg[k], names, width, recs[k], end);
+            pos = end;
+        }
+        if (code == kOk && pos != body_bytes) code = kLayout;
+        if (code != kOk) set_status(st, code);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long acc = 0;
+        if (st->status == kOk) {
+            for (uint32_t k = 0; k < n; ++k) {
+                rec_chunk_begin[k] = acc;
+                acc += (recs[k].idx_len + kByteChunk - 1) / kByteChunk;
+            }
+        }
+        rec_chunk_begin[n] = acc;
+        st->n_chunks = acc;
+    }
+}
+
+// ---------------------------------------------------------------- chunk staging (A2, A4)
+__device__ __forceinline__ uint32_t record_of_chunk(const unsigned long long *rcb, uint32_t n,
+                                                    unsigned long long c) {
+    uint32_t lo = 0, hi = n;  // largest k with rcb[k] <= c; records without chunks are skipped
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(rcb + mid) <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+struct ChunkView {
+    unsigned long long cs;   // chunk start within the record's index stream
+    uint32_t len;            // bytes in this chunk
+    bool last;               // chunk holds the stream's final byte
+};
+
+// Stage bytes [cs - halo, cs + len) of the record's stream into sb (sb[kHalo] = byte cs).
+__device__ __forceinline__ ChunkView stage_chunk(const uint8_t *body, const ApplyRec &R,
+                                                 unsigned long long j, uint8_t *sb) {
+    ChunkView v;
+    v.cs = j * kByteChunk;
+    const unsigned long long ce = min(R.idx_len, v.cs + kByteChunk);
+    v.len = (uint32_t)(ce - v.cs);
+    v.last = (ce == R.idx_len);
+    const uint32_t hs = (uint32_t)min(v.cs, (unsigned long long)kHalo);
+    const uint8_t *src = body + R.idx_off + v.cs - hs;
+    for (uint32_t b = threadIdx.x; b < hs + v.len; b += blockDim.x) sb[kHalo - hs + b] = __ldg(src + b);
+    __syncthreads();
+    return v;
+}
+
+// Decode the varint whose terminator is at chunk position p; returns its status code.
+__device__ __forceinline__ uint32_t decode_at(const uint8_t *sb, const ChunkView &v, int p,
+                                              unsigned long long numel,
+                                              unsigned long long &val) {
+    int q = p;
+    int nb = 1;
+    while ((long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80)) {
+        --q;
+        if (++nb > 10) return kOverflow;
+    }
+    const uint8_t last = sb[kHalo + p];
+    unsigned long long x = 0;
+    for (int i = 0; i < nb; ++i) x |= (unsigned long long)(sb[kHalo + q + i] & 0x7F) << (7 * i);
+    val = x;
+    if (nb == 10 && last > 1) return kOverflow;
+    if (nb > 1 && last == 0) return kOverlong;
+    const bool first = ((long long)v.cs + q == 0);
+    if (!first && x == 0) return kNonIncreasing;
+    if (x >= numel) return kRange;
+    return kOk;
+}
+
+// ------------------------------------------------------------------------------ A2
+__global__ void __launch_bounds__(256)
+k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
+               const unsigned long long *__restrict__ rcb, unsigned int *__restrict__ chunk_count,
+               unsigned long long *__restrict__ chunk_sum, ApplyState *st) {
+    if (st->status != kOk) return;
+    const unsigned long long nch = st->n_chunks;
+    __shared__ uint8_t sb[kHalo + kByteChunk];
+    __shared__ uint32_t s_cnt[8];
+    __shared__ unsigned long long s_sum[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        const uint32_t k = record_of_chunk(rcb, n, c);
+        const ApplyRec R = recs[k];
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
+        uint32_t cnt = 0, err = kOk;
+        unsigned long long sum = 0;
+        const int p0 = threadIdx.x * 16;
+        for (int p = p0; p < p0 + 16 && p < (int)v.len; ++p) {
+            if (sb[kHalo + p] & 0x80) {
+                if (v.last && p == (int)v.len - 1) err = err ? err : kTruncated;
+                continue;
+            }
+            unsigned long long x = 0;
+            const uint32_t e = decode_at(sb, v, p, R.numel, x);
+            if (e != kOk && err == kOk) err = e;
+            ++cnt;
+            sum = sat_add(sum, x);
+        }
+        if (err != kOk) set_status(st, err);
+        // block reduction of (count, saturating sum)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            sum = sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        }
+        if (lane == 0) {
+            s_cnt[warp] = cnt;
+            s_sum[warp] = sum;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tc = 0;
+            unsigned long long ts = 0;
+            for (int w = 0; w < 8; ++w) {
+                tc += s_cnt[w];
+                ts = sat_add(ts, s_sum[w]);
+            }
+            chunk_count[c] = tc;
+            chunk_sum[c] = ts;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------ A3
+__global__ void __launch_bounds__(1024)
+k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long long *__restrict__ rcb,
+             const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
+             unsigned long long *__restrict__ ord_base, unsigned long long *__restrict__ idx_base,
+             ApplyState *st) {
+    if (st->status != kOk) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t k = warp; k < n; k += 32) {
+        const unsigned long long c0 = rcb[k], c1 = rcb[k + 1];
+        unsigned long long cc = 0, cs = 0;  // carries: entries and gap sum before the window
+        for (unsigned long long b = c0; b < c1; b += 32) {
+            const unsigned long long c = b + lane;
+            unsigned long long x = c < c1 ? chunk_count[c] : 0;
+            unsigned long long y = c < c1 ? chunk_sum[c] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long xx = __shfl_up_sync(0xffffffffu, x, o);
+                const unsigned long long yy = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) {
+                    x += xx;
+                    y = sat_add(y, yy);
+                }
+            }
+            unsigned long long xe = __shfl_up_sync(0xffffffffu, x, 1);
+            unsigned long long ye = __shfl_up_sync(0xffffffffu, y, 1);
+            if (lane == 0) xe = ye = 0;
+            if (c < c1) {
+                ord_base[c] = cc + xe;
+                idx_base[c] = sat_add(cs, ye);
+            }
+            cc += __shfl_sync(0xffffffffu, x, 31);
+            cs = sat_add(cs, __shfl_sync(0xffffffffu, y, 31));
+        }
+        if (lane == 0) {
+            const ApplyRec R = recs[k];
+            if (cc != R.nnz) set_status(st, kCount);
+            else if (R.nnz > 0 && cs >= R.numel) set_status(st, kRange);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------ A4
+template <int W>
+__global__ void __launch_bounds__(256)
+k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
+          const unsigned long long *__restrict__ rcb, const unsigned long long *__restrict__ ord_base,
+          const unsigned long long *__restrict__ idx_base, const ApplyState *st) {
+    using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
+    if (st->status != kOk) return;  // the gate: nothing is written unless all checks passed
+    const unsigned long long nch = st->n_chunks;
+    __shared__ uint8_t sb[kHalo + kByteChunk];
+    __shared__ uint32_t s_cnt[8];
+    __shared__ unsigned long long s_sum[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        const uint32_t k = record_of_chunk(rcb, n, c);
+        const ApplyRec R = recs[k];
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
+        const int p0 = threadIdx.x * 16;
+        const int p1 = min(p0 + 16, (int)v.len);
+        uint32_t cnt = 0;
+        unsigned long long sum = 0;
+        for (int p = p0; p < p1; ++p) {
+            if (sb[kHalo + p] & 0x80) continue;
+            unsigned long long x = 0;
+            decode_at(sb, v, p, ~0ull, x);
+            ++cnt;
+            sum += x;
+        }
+        // block exclusive scan of (cnt, sum)
+        uint32_t ci = warp_inclusive_sum(cnt);
+        unsigned long long si = warp_inclusive_sum(sum);
+        if (lane == 31) {
+            s_cnt[warp] = ci;
+            s_sum[warp] = si;
+        }
+        __syncthreads();
+        uint32_t cpre = 0;
+        unsigned long long spre = 0;
+        for (int w = 0; w < warp; ++w) {
+            cpre += s_cnt[w];
+            spre += s_sum[w];
+        }
+        unsigned long long ord = ord_base[c] + cpre + ci - cnt;
+        unsigned long long idx = idx_base[c] + spre + si - sum;
+        LT *w = reinterpret_cast<LT *>(R.w);
+        const uint8_t *vals = body + R.val_off;
+        for (int p = p0; p < p1; ++p) {
+            if (sb[kHalo + p] & 0x80) continue;
+            unsigned long long x = 0;
+            decode_at(sb, v, p, ~0ull, x);
+            idx += x;
+            const uint8_t *vp = vals + ord * W;
+            LT val;
+            if constexpr (W == 2) val = (LT)(__ldg(vp) | (__ldg(vp + 1) << 8));
+            else val = (LT)__ldg(vp) | ((LT)__ldg(vp + 1) << 8) | ((LT)__ldg(vp + 2) << 16) | ((LT)__ldg(vp + 3) << 24);
+            w[idx] = val;
+            ++ord;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------ launchers
+cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
+    if (ev) cudaEventRecord(ev[0], s);
+    k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.targets, a.n, a.names, a.hint, a.recs,
+                               a.rec_chunk_begin, a.state, a.width);
+    if (ev) cudaEventRecord(ev[1], s);
+    k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin,
+                                                  a.chunk_count, a.chunk_sum, a.state);
+    if (ev) cudaEventRecord(ev[2], s);
+    k_apply_scan<<<1, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
+                                    a.chunk_ord_base, a.chunk_idx_base, a.state);
+    if (ev) cudaEventRecord(ev[3], s);
+    if (a.width == 2)
+        k_scatter<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin,
+                                                    a.chunk_ord_base, a.chunk_idx_base, a.state);
+    else
+        k_scatter<4><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin,
+                                                    a.chunk_ord_base, a.chunk_idx_base, a.state);
+    if (ev) cudaEventRecord(ev[4], s);
+    return cudaGetLastError();
+}
+
+}  // namespace sd

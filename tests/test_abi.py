@@ -1,0 +1,86 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports every symbol
+include/sparsedelta.h declares; the product path never imports the oracle (no GPU)."""
+
+import ast
+import os
+import re
+import subprocess
+
+import pytest
+import torch
+
+import __graft_entry__ as entry
+from conftest import ROOT
+
+
+@pytest.fixture(scope="module")
+def built():
+    entry.build()
+    from paper_2602_11456_b200 import _abi
+    return _abi
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "sparsedelta.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(delta_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(built):
+    declared = _declared()
+    assert set(declared) == set(built.EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", built.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (delta_\w+)", out))
+    assert set(declared) <= exported, set(declared) - exported
+    lib = built.lib()
+    for name in declared:
+        assert hasattr(lib, name)
+
+
+def test_sm100a_code_in_library(built):
+    out = subprocess.run(["cuobjdump", "--list-elf", built.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU error path")
+def test_no_gpu_fails_loudly(built):
+    import paper_2602_11456_b200 as sd
+    with pytest.raises(sd.DeltaError) as e:
+        sd.DeltaContext("cuda:0")
+    assert e.value.status == built.DELTA_ECUDA
+
+
+def test_null_context_is_einval(built):
+    from ctypes import byref, c_uint64
+    lib = built.lib()
+    n = c_uint64()
+    assert lib.delta_size(None, None, 0, 0, None, byref(n)) == built.DELTA_EINVAL
+    assert lib.delta_apply(None, None, 0, 0, None, 0, None, None) == built.DELTA_EINVAL
+    assert lib.delta_last_error(None) == b"no context"
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2602_11456_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                tree = ast.parse(open(os.path.join(dirpath, f)).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert not any(a.name.split(".")[0] == "oracle" for a in node.names), f
+                    if isinstance(node, ast.ImportFrom):
+                        assert (node.module or "").split(".")[0] != "oracle", f
+            if f.endswith((".cu", ".cuh", ".h", ".cpp")):
+                for ln in open(os.path.join(dirpath, f)):
+                    assert not (ln.lstrip().startswith("#include") and "oracle" in ln), (f, ln)
+
+
+def test_product_container_matches_oracle_container():
+    import oracle
+    import paper_2602_11456_b200 as sd
+    body = bytes(range(200)) * 3
+    a = sd.pack_container(body, 8, 7, 2, 5)
+    b = oracle.container.pack(body, 8, 7, 2, 5)
+    assert a == b
+    assert sd.unpack_container(a) == oracle.container.unpack(b)

@@ -1,0 +1,355 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element, on the same seeded inputs.  Bit-exact for every byte of the packed body, every
+offset-table row and every lane of the reconstructed weights (integer views).
+
+Cases: configs[0] (M1), ragged / multi-tile / multi-span / unaligned tensors, full-range
+bit patterns (NaN, +-0, Inf, subnormals), gap boundaries of the LEB128 encoding, the
+degenerate cases (nothing / everything / first / last lane changed, empty tensors),
+workspace regrowth, the two-phase size+extract path, the corruption suite (error kind
+equal to the oracle's, targets untouched) and, at full size, Qwen3-8B (configs[2], in
+the launch configuration bench.py times) with sampled records checked against the oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gpu_helpers import (as_list, assert_body_equal, assert_lanes_equal, fused, lane_view,
+                         oracle_extract, to_np)
+from workload import TensorSpec, generate_pair, m1_specs, qwen3
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def sd():
+    import __graft_entry__ as entry
+    entry.build()
+    import paper_2602_11456_b200 as m
+    torch.cuda.set_device(DEV)
+    return m
+
+
+def _roundtrip(sd, tensors, ctx=None, check_oracle=True):
+    """Extract on the GPU, compare with the oracle, apply (with and without the table
+    hint) to copies of old, compare with new."""
+    ctx = ctx or sd.context()
+    body, table = ctx.delta_extract(tensors)
+    torch.cuda.synchronize()
+    if check_oracle:
+        ref_body, ref_table = oracle_extract(tensors)
+        assert_body_equal(body, ref_body)
+        assert [tuple(r) for r in table] == [tuple(r) for r in ref_table]
+    for use_hint in (True, False):
+        targets = [(n, fused(o).clone()) for n, o, _ in tensors]
+        ctx.delta_apply(targets, body, table=table if use_hint else None)
+        torch.cuda.synchronize()
+        for (_, w), (_, _, nw) in zip(targets, tensors):
+            assert_lanes_equal(w, fused(nw))
+    return body, table
+
+
+def test_m1_config0(sd):
+    spec = m1_specs()[0]
+    old, new = generate_pair(spec, 0, 0, rho=0.01, pattern="exact", device=DEV)
+    body, table = _roundtrip(sd, [(spec.name, old, new)])
+    assert table[0][2] == 167_772
+    # idempotent re-apply on new (replace mode, R14)
+    w = new.clone()
+    sd.delta_apply([(spec.name, w)], body, table=table)
+    assert_lanes_equal(w, new)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("rho", [0.0, 0.001, 0.01, 0.3, 1.0])
+def test_ragged_bit_patterns(sd, dtype, rho):
+    sizes = [1, 7, 8, 9, 1000, 8191, 8192, 16384, 16385, 16384 * 3 + 5, 100_003, 0, 2]
+    tensors = []
+    for k, n in enumerate(sizes):
+        spec = TensorSpec(f"t.{k}.weight", (n,), "matrix")
+        o, w = generate_pair(spec, k, 17, rho=rho, dtype=dtype, device=DEV, values="bits")
+        tensors.append((spec.name, o, w))
+    _roundtrip(sd, tensors)
+
+
+def test_fused_unaligned_spans(sd):
+    # spans are slices of one buffer at odd lane offsets (not 16-byte aligned), including
+    # an empty span: exercises the lane-by-lane path and span-local tiling.
+    n = 300_001
+    spec = TensorSpec("buf", (n,), "matrix")
+    o, w = generate_pair(spec, 0, 5, rho=0.02, device=DEV, values="bits")
+    cuts = [1, 50_001, 50_001, 50_002, 130_001, 299_999]
+    so = [o[a:b] for a, b in zip(cuts[:-1], cuts[1:])]
+    sw = [w[a:b] for a, b in zip(cuts[:-1], cuts[1:])]
+    tensors = [("model.layers.0.self_attn.qkv_proj.weight", so, sw),
+               ("aligned.tail", o[299_999:].clone(), w[299_999:].clone())]
+    _roundtrip(sd, tensors)
+
+
+def _with_changes(n, positions, dtype=torch.bfloat16):
+    old = torch.zeros(n, dtype=dtype, device=DEV)
+    new = old.clone()
+    if positions:
+        p = torch.tensor(positions, dtype=torch.int64, device=DEV)
+        lane_view(new)[p] = 0x3F80 if dtype == torch.bfloat16 else 0x3F800000
+    return old, new
+
+
+def test_gap_boundaries(sd):
+    gaps = [0, 127, 128, 16383, 16384, 2**21 - 1, 2**21, 1, 1, 300]
+    pos = list(np.cumsum(gaps))
+    n = pos[-1] + 5
+    old, new = _with_changes(n, pos)
+    body, table = _roundtrip(sd, [("gaps", old, new)])
+    # index stream by hand: first index 0 -> 00; 127 -> 7F; 128 -> 80 01; ...
+    ref = oracle.brute.encode_indices([int(x) for x in pos])
+    s = body[table[0][3]:table[0][3] + table[0][4]].cpu().numpy().tobytes()
+    assert s == ref
+
+
+def test_degenerate_change_sets(sd):
+    n = 16384 * 2 + 3
+    cases = {"none": [], "first": [0], "last": [n - 1], "first_last": [0, n - 1],
+             "all": list(range(n))}
+    tensors = []
+    for name, p in cases.items():
+        o, w = _with_changes(n, p)
+        tensors.append((name, o, w))
+    body, table = _roundtrip(sd, tensors)
+    assert [r[2] for r in table] == [0, 1, 1, 2, n]
+
+
+def test_many_small_tensors(sd):
+    rng = np.random.default_rng(3)
+    tensors = []
+    for k in range(400):
+        n = int(rng.integers(0, 5000))
+        spec = TensorSpec(f"layer.{k}", (n,), "norm")
+        o, w = generate_pair(spec, k, 2, rho=float(rng.choice([0, 0.01, 0.5])), device=DEV)
+        tensors.append((spec.name + "é" * (k % 3), o, w))
+    _roundtrip(sd, tensors)
+
+
+def test_workspace_regrowth_high_density(sd):
+    ctx = sd.DeltaContext(DEV)  # fresh: initial entry workspace is max(1M, N/32)
+    spec = TensorSpec("dense", (4096, 2048), "matrix")
+    o, w = generate_pair(spec, 0, 9, rho=0.5, device=DEV)
+    _roundtrip(sd, [(spec.name, o, w)], ctx=ctx)
+    o2, w2 = generate_pair(spec, 1, 9, rho=0.99, device=DEV)  # grows again
+    _roundtrip(sd, [(spec.name, o2, w2)], ctx=ctx)
+    ctx.close()
+
+
+def test_size_then_extract_and_capacity(sd):
+    spec = TensorSpec("x", (100_000,), "matrix")
+    o, w = generate_pair(spec, 0, 1, rho=0.05, device=DEV)
+    tl = sd.TensorList([(spec.name, o, w)])
+    ctx = sd.context()
+    size = ctx.delta_size(tl)
+    out = torch.empty(size, dtype=torch.uint8, device=DEV)
+    body, table = ctx.delta_extract(tl, out=out)  # consumes the cached compaction
+    ref_body, ref_table = oracle_extract([(spec.name, o, w)])
+    assert size == len(ref_body)
+    assert_body_equal(body, ref_body)
+    small = torch.empty(size - 1, dtype=torch.uint8, device=DEV)
+    with pytest.raises(sd.DeltaError) as e:
+        ctx.delta_extract(tl, out=small)
+    assert e.value.status == -3  # DELTA_ECAPACITY
+
+
+def test_fp32_m1_shape(sd):
+    spec = m1_specs()[0]
+    o, w = generate_pair(spec, 0, 4, rho=0.01, dtype=torch.float32, device=DEV)
+    _roundtrip(sd, [(spec.name, o, w)])
+
+
+# ------------------------------------------------------------------ corruption suite
+def _small_valid():
+    spec_a = TensorSpec("a", (5000,), "matrix")
+    spec_b = TensorSpec("b", (300,), "norm")
+    oa, wa = generate_pair(spec_a, 0, 3, rho=0.05)
+    ob, wb = generate_pair(spec_b, 1, 3, rho=0.05)
+    return [("a", oa, wa), ("b", ob, wb)]
+
+
+def _mutations(body: bytes, table):
+    """(label, mutated body, targets numel overrides) — each with exactly one fault."""
+    b = bytearray(body)
+    ra, rb = table[0], table[1]
+    out = []
+    m = bytearray(b)
+    m[ra[3] + ra[4] - 1] |= 0x80                         # last stream byte keeps going
+    out.append(("truncated", m, None))
+    # zero gap: find a 1-byte varint after the first entry and make it 0
+    s = ra[3]
+    m = bytearray(b)
+    pos = s + 1
+    while m[pos - 1] & 0x80 or m[pos] & 0x80:
+        pos += 1
+    m[pos] = 0x00
+    out.append(("nonincreasing", m, None))
+    m = bytearray(b)
+    m[ra[6] - 1] = 1                                     # mode byte
+    out.append(("mode", m, None))
+    m = bytearray(b)
+    m[2] ^= 0x01                                         # name byte of record a ('a' -> '`')
+    out.append(("name", m, None))
+    out.append(("numel", bytearray(b), {"a": 5001}))
+    out.append(("layout", bytearray(b[:-1]), None))
+    out.append(("layout", bytearray(b + b"\x00"), None))
+    # count: nnz field of record b says one more (values region shifts: also make room)
+    m = bytearray(b)
+    nl = 1
+    nnz_off = rb[0] + 2 + nl + 8
+    nnz = int.from_bytes(m[nnz_off:nnz_off + 8], "little")
+    m[nnz_off:nnz_off + 8] = (nnz + 1).to_bytes(8, "little")
+    m[rb[0] + rb[6] - 1:rb[0] + rb[6] - 1] = b"\x00\x00"  # two more value bytes before mode
+    out.append(("count", m, None))
+    return out
+
+
+def _hand_record(name, n, nnz, stream, vals, mode=0):
+    import struct
+    nb = name.encode()
+    return (struct.pack("<H", len(nb)) + nb + struct.pack("<QQQ", n, nnz, len(stream))
+            + bytes(stream) + bytes(vals) + bytes([mode]))
+
+
+_HAND = [
+    ("overlong", _hand_record("a", 10, 1, b"\x85\x00", b"\x01\x00")),
+    ("overflow", _hand_record("a", 10, 1, b"\xff" * 9 + b"\x02", b"\x01\x00")),
+    ("overflow", _hand_record("a", 10, 1, b"\xff" * 10 + b"\x01", b"\x01\x00")),
+    ("range", _hand_record("a", 10, 2, b"\x05\x05", b"\x01\x00\x02\x00")),
+    ("range", _hand_record("a", 10, 1, b"\x0a", b"\x01\x00")),
+    ("truncated", _hand_record("a", 10, 1, b"\x85", b"\x01\x00")),
+    ("count", _hand_record("a", 10, 1, b"\x01\x01", b"\x01\x00")),
+]
+
+
+def _expect_reject(sd, body: bytes, targets_np, kind_expected):
+    """targets_np: [(name, np lanes)]; the oracle and the GPU must both reject with the
+    same kind, and the GPU targets must be bitwise untouched."""
+    with pytest.raises(oracle.DeltaError) as eo:
+        oracle.codec.apply(targets_np, body, 2)
+    assert eo.value.kind == kind_expected
+    dev_body = torch.tensor(list(body), dtype=torch.uint8, device=DEV)
+    targets = [(n, torch.from_numpy(a.view(np.int16).copy()).to(DEV).view(torch.bfloat16))
+               for n, a in targets_np]
+    before = [t.clone() for _, t in targets]
+    for hint in (None, "valid-looking"):
+        table = None
+        if hint:  # a hint computed from the body's own (corrupt) headers
+            table = _naive_table(body, len(targets))
+            if table is None:
+                continue
+        with pytest.raises(sd.DeltaError) as eg:
+            sd.delta_apply(targets, dev_body, table=table)
+        assert eg.value.kind == kind_expected, (eg.value, kind_expected)
+        for (_, t), b in zip(targets, before):
+            assert_lanes_equal(t, b)
+
+
+def _naive_table(body: bytes, n):
+    import struct
+    rows, pos = [], 0
+    try:
+        for _ in range(n):
+            nl = struct.unpack_from("<H", body, pos)[0]
+            N, nnz, il = struct.unpack_from("<QQQ", body, pos + 2 + nl)
+            io = pos + 2 + nl + 24
+            rb = 27 + nl + il + 2 * nnz
+            rows.append((pos, N, nnz, io, il, io + il, rb))
+            pos += rb
+    except struct.error:
+        return None
+    return rows
+
+
+def test_corruption_suite(sd):
+    ts = _small_valid()
+    body, table = oracle_extract(ts)
+    for kind, mbody, override in _mutations(body, table):
+        targets = [(n, to_np(o).copy()) for n, o, _ in ts]
+        if override:
+            targets = [(n, np.zeros(override.get(n, a.size), np.uint16)) for n, a in targets]
+        _expect_reject(sd, bytes(mbody), targets, kind)
+
+
+@pytest.mark.parametrize("kind,body", _HAND)
+def test_corruption_hand(sd, kind, body):
+    _expect_reject(sd, body, [("a", np.arange(10, dtype=np.uint16))], kind)
+
+
+def test_corruption_deep_in_a_multichunk_stream(sd):
+    # a fault in a later 4 KiB chunk of a long stream (M1-sized record)
+    spec = m1_specs()[0]
+    o, w = generate_pair(spec, 0, 0, rho=0.01, pattern="exact")
+    body, table = oracle.codec.extract([(spec.name, [to_np(o)], [to_np(w)])])
+    r = table[0]
+    assert r[4] > 5 * 4096
+    m = bytearray(body)
+    p = r[3] + 3 * 4096 + 100
+    while m[p - 1] & 0x80 or m[p] & 0x80:  # a 1-byte varint that is not the first
+        p += 1
+    m[p] = 0
+    _expect_reject(sd, bytes(m), [(spec.name, to_np(o).copy())], "nonincreasing")
+
+
+# ------------------------------------------------------------------ full-size configs
+def _sample_records(sd, specs, tensors, body, table, picks):
+    for k in picks:
+        name, o, w = tensors[k]
+        rec = oracle.codec.record(name, oracle.codec.fuse([to_np(x) for x in as_list(o)]),
+                                  oracle.codec.fuse([to_np(x) for x in as_list(w)]))
+        r = table[k]
+        got = body[r[0]:r[0] + r[6]].cpu().numpy().tobytes()
+        assert got == rec, f"record {k} ({name}) differs from the oracle"
+
+
+def test_m3_qwen3_8b_full(sd):
+    """configs[2] at N=1: Qwen3-8B fused set, 1% uniform, the bench's launch config."""
+    specs = qwen3("8B")
+    tensors = []
+    for k, s in enumerate(specs):
+        o, w = generate_pair(s, k, 0, rho=0.01, device=DEV)
+        tensors.append((s.name, o, w))
+    tl = sd.TensorList(tensors)
+    ctx = sd.context()
+    body, table = ctx.delta_extract(tl)
+    torch.cuda.synchronize()
+    # every table row obeys the record-size closed form and the rows tile the body
+    off = 0
+    for (name, o, w), r in zip(tensors, table):
+        assert r[0] == off and r[1] == o.numel()
+        assert r[6] == 27 + len(name.encode()) + r[4] + 2 * r[2]
+        off += r[6]
+    assert off == body.numel()
+    # nnz per tensor equals the number of differing lanes (torch compare on int views)
+    for (name, o, w), r in zip(tensors, table):
+        assert r[2] == int((lane_view(o) != lane_view(w)).sum())
+    # sampled records byte-exact against the oracle: first, largest, a qkv, a norm, last
+    _sample_records(sd, specs, tensors, body, table, [0, 1, 3, 5, 150, len(tensors) - 2, len(tensors) - 1])
+    # the round trip at full size: apply onto old gives new, bit for bit
+    targets = [(n, o) for n, o, _ in tensors]  # apply in place onto old
+    ctx.delta_apply(targets, body, table=table)
+    torch.cuda.synchronize()
+    for (_, o, w) in tensors:
+        assert_lanes_equal(o, w)
+
+
+def test_u64_index_path(sd):
+    """A tensor with more than 2^32 lanes (reading R13): 64-bit indices and 5-byte gaps."""
+    n = 2**32 + 1000
+    pos = [0, 2**31, 2**32 - 1, 2**32, 2**32 + 999]
+    old, new = _with_changes(n, pos)
+    ctx = sd.DeltaContext(DEV)
+    body, table = ctx.delta_extract([("huge", old, new)])
+    want = oracle.brute.record_from_sparse("huge", n, pos, [0x3F80] * len(pos), 2)
+    assert body.cpu().numpy().tobytes() == want
+    w = old.clone()
+    del old
+    ctx.delta_apply([("huge", w)], body, table=table)
+    assert_lanes_equal(w, new)
+    ctx.close()
