@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     p.add_argument("--no-clocks", action="store_true")
+    p.add_argument("--tensors", type=int, default=0,
+                   help="profiling only: keep the first N tensors of the config")
     return p.parse_args()
 
 
@@ -65,6 +67,9 @@ def workload(args):
     rho = args.rho if args.rho is not None else (rho if rho is not None else 0.01)
     pattern = args.pattern or pattern or "uniform"
     specs = m1_specs() if model == "M1" else qwen3(model)
+    if getattr(args, "tensors", 0):
+        specs = specs[:args.tensors]
+        desc += f" [first {args.tensors} tensors only: profiling run]"
     return specs, rho, pattern, desc
 
 
