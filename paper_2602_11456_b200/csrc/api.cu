@@ -63,13 +63,12 @@ struct delta_ctx {
     bool plan_valid = false;
     uint32_t ntiles = 0, ntensors = 0;
     int width = 2;
-    bool idx64 = false;
     unsigned long long total_lanes = 0;
-    DevBuf tiles, name_len, name_off, names, numel;
+    DevBuf tiles, name_len, name_off, names, numel, tensor_first_tile;
     // ---- extract workspace
-    DevBuf tile_state, ticket, ws_idx, ws_val, entry_begin, tstart_partial, chunk_bytes,
-        chunk_prefix, tensor_byte_begin, table, summary;
-    unsigned long long ws_cap = 0;  // entries
+    DevBuf slot_off, slot_val, meta, tile_entry, tile_byte, tile_pred, tile_bytes, blk_a, blk_key,
+        entry_begin, tensor_byte_begin, table, summary;
+    uint32_t slot_cap = 0;          // entries per tile slot (grows on overflow)
     bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
     ExtractSummary *h_summary = nullptr;  // pinned
 
@@ -125,7 +124,7 @@ static int cuda_fail(delta_ctx *c, cudaError_t e, const char *where) {
 extern "C" {
 
 const char *delta_version(void) {
-    return "sparsedelta 1 (sm_100a; K1 ticket/look-back scan, LEB128 emit, gated scatter)";
+    return "sparsedelta 2 (sm_100a; K1 tile-slot compaction, tile scans, warp-per-tile LEB128 emit, gated scatter)";
 }
 
 int delta_ctx_create(delta_ctx **out, int device) {
@@ -154,9 +153,10 @@ void delta_ctx_destroy(delta_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
-                      &c->tile_state, &c->ticket, &c->ws_idx, &c->ws_val, &c->entry_begin,
-                      &c->tstart_partial, &c->chunk_bytes, &c->chunk_prefix,
-                      &c->tensor_byte_begin, &c->table, &c->summary, &c->a_targets,
+                      &c->tensor_first_tile, &c->slot_off, &c->slot_val, &c->meta,
+                      &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->blk_a,
+                      &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
+                      &c->summary, &c->a_targets,
                       &c->a_names, &c->a_hint, &c->a_recs, &c->a_rcb, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
@@ -249,14 +249,16 @@ static int build_plan(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int w, 
     std::vector<TileDesc> tiles;
     std::vector<uint32_t> nlen(n), noff(n);
     std::vector<unsigned long long> numel(n);
+    std::vector<uint32_t> first_tile(n);
     std::string blob;
-    unsigned long long total = 0, maxn = 0;
+    unsigned long long total = 0;
     for (uint32_t k = 0; k < n; ++k) {
         nlen[k] = t[k].name_len;
         noff[k] = (uint32_t)blob.size();
         blob.append(t[k].name ? t[k].name : "", t[k].name_len);
         unsigned long long base = 0;
         bool first = true;
+        first_tile[k] = (uint32_t)tiles.size();
         for (uint32_t sidx = 0; sidx < t[k].n_spans; ++sidx) {
             const delta_span &sp = t[k].spans[sidx];
             const bool aligned = ((reinterpret_cast<uintptr_t>(sp.old_dev) |
@@ -280,7 +282,6 @@ static int build_plan(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int w, 
         }
         numel[k] = base;
         total += base;
-        maxn = std::max(maxn, base);
     }
     if (tiles.empty()) {  // n == 0: one placeholder so K1 still writes M = 0
         TileDesc d{};
@@ -292,11 +293,13 @@ static int build_plan(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int w, 
     GROW(ctx->name_off, std::max<size_t>(n, 1) * 4);
     GROW(ctx->names, std::max<size_t>(blob.size(), 1));
     GROW(ctx->numel, std::max<size_t>(n, 1) * 8);
+    GROW(ctx->tensor_first_tile, std::max<size_t>(n, 1) * 4);
     CK(cudaMemcpyAsync(ctx->tiles.p, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice, s), "upload tiles");
     if (n) {
         CK(cudaMemcpyAsync(ctx->name_len.p, nlen.data(), n * 4, cudaMemcpyHostToDevice, s), "upload");
         CK(cudaMemcpyAsync(ctx->name_off.p, noff.data(), n * 4, cudaMemcpyHostToDevice, s), "upload");
         CK(cudaMemcpyAsync(ctx->numel.p, numel.data(), n * 8, cudaMemcpyHostToDevice, s), "upload");
+        CK(cudaMemcpyAsync(ctx->tensor_first_tile.p, first_tile.data(), n * 4, cudaMemcpyHostToDevice, s), "upload");
     }
     if (!blob.empty()) CK(cudaMemcpyAsync(ctx->names.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s), "upload");
     // the host vectors die at return: make the pageable copies complete first
@@ -304,7 +307,6 @@ static int build_plan(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int w, 
     ctx->ntiles = (uint32_t)tiles.size();
     ctx->ntensors = n;
     ctx->width = w;
-    ctx->idx64 = maxn > 0xFFFFFFFFull;
     ctx->total_lanes = total;
     ctx->plan_key = key;
     ctx->plan_valid = true;
@@ -316,16 +318,18 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.tiles = ctx->tiles.as<TileDesc>();
     a.ntiles = ctx->ntiles;
     a.ntensors = ctx->ntensors;
-    a.tile_state = ctx->tile_state.as<unsigned long long>();
-    a.ticket = ctx->ticket.as<unsigned int>();
-    a.ws_idx = ctx->ws_idx.p;
-    a.ws_val = ctx->ws_val.p;
-    a.ws_cap = ctx->ws_cap;
+    a.slot_cap = ctx->slot_cap;
+    a.slot_off = ctx->slot_off.as<uint16_t>();
+    a.slot_val = ctx->slot_val.p;
+    a.meta = ctx->meta.as<TileMeta>();
+    a.tile_entry = ctx->tile_entry.as<unsigned long long>();
+    a.tile_byte = ctx->tile_byte.as<unsigned long long>();
+    a.tile_pred = ctx->tile_pred.as<unsigned long long>();
+    a.tile_bytes_tmp = ctx->tile_bytes.as<unsigned int>();
+    a.blk_a = ctx->blk_a.as<unsigned long long>();
+    a.blk_key = ctx->blk_key.as<long long>();
+    a.tensor_first_tile = ctx->tensor_first_tile.as<uint32_t>();
     a.entry_begin = ctx->entry_begin.as<unsigned long long>();
-    a.tstart_partial = ctx->tstart_partial.as<unsigned long long>();
-    a.chunk_bytes = ctx->chunk_bytes.as<unsigned int>();
-    a.chunk_prefix = ctx->chunk_prefix.as<unsigned long long>();
-    a.chunk_cap = ctx->ws_cap / kEntryChunk + 2;
     a.tensor_byte_begin = ctx->tensor_byte_begin.as<unsigned long long>();
     a.table = ctx->table.as<RecordRow>();
     a.name_len = ctx->name_len.as<uint32_t>();
@@ -334,41 +338,42 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.numel = ctx->numel.as<unsigned long long>();
     a.summary = ctx->summary.as<ExtractSummary>();
     a.width = ctx->width;
-    a.idx64 = ctx->idx64;
     a.persist_ctas = ctx->sm_count * 8;
     return a;
 }
 
-static int reserve_entries(delta_ctx *ctx, unsigned long long cap) {
-    const size_t isz = ctx->idx64 ? 8 : 4;
-    GROW(ctx->ws_idx, cap * isz + 64);
-    GROW(ctx->ws_val, cap * ctx->width + 64);
-    const size_t nch = cap / kEntryChunk + 2;
-    GROW(ctx->chunk_bytes, nch * 4);
-    GROW(ctx->chunk_prefix, nch * 8);
-    ctx->ws_cap = cap;
+static int reserve_slots(delta_ctx *ctx, uint32_t cap) {
+    GROW(ctx->slot_off, (size_t)ctx->ntiles * cap * sizeof(uint16_t) + 64);
+    GROW(ctx->slot_val, (size_t)ctx->ntiles * cap * ctx->width + 64);
+    ctx->slot_cap = cap;
     return DELTA_OK;
 }
 
-// K1-K3 + the single size readback; retries once with a larger entry workspace.
+// K1-K3 + the single size readback; on slot overflow grows the slots to the largest
+// per-tile count seen and runs again (first call at a new density only).
 static int run_scan(delta_ctx *ctx, cudaStream_t s) {
-    const uint32_t T = ctx->ntensors;
-    GROW(ctx->tile_state, (size_t)ctx->ntiles * 8);
-    GROW(ctx->ticket, 4);
+    const uint32_t T = ctx->ntensors, nt = ctx->ntiles;
+    const uint32_t nblk = (nt + kTileBlock - 1) / kTileBlock;
+    const uint32_t lanes_per_tile = kTileBytes / ctx->width;
+    GROW(ctx->meta, (size_t)nt * sizeof(TileMeta));
+    GROW(ctx->tile_entry, (size_t)nt * 8);
+    GROW(ctx->tile_byte, (size_t)nt * 8);
+    GROW(ctx->tile_pred, (size_t)nt * 8);
+    GROW(ctx->tile_bytes, (size_t)nt * 4);
+    GROW(ctx->blk_a, (size_t)nblk * 2 * 8);
+    GROW(ctx->blk_key, (size_t)nblk * 8);
     GROW(ctx->entry_begin, (size_t)(T + 1) * 8);
-    GROW(ctx->tstart_partial, (size_t)(T + 1) * 8);
     GROW(ctx->tensor_byte_begin, (size_t)(T + 1) * 8);
     GROW(ctx->table, (size_t)std::max<uint32_t>(T, 1) * sizeof(RecordRow));
     GROW(ctx->summary, sizeof(ExtractSummary));
-    if (ctx->ws_cap == 0) {
-        // first guess: 3% of the lanes (grows to the exact need on overflow)
-        unsigned long long guess = std::max<unsigned long long>(1ull << 20, ctx->total_lanes / 32);
-        int rc = reserve_entries(ctx, guess);
+    // slots: start at 1/16 of a tile (6.25% density); grown to the exact need on overflow
+    uint32_t cap = std::max<uint32_t>(ctx->slot_cap, lanes_per_tile / 16);
+    if (cap > lanes_per_tile) cap = lanes_per_tile;
+    if (cap != ctx->slot_cap || ctx->slot_off.cap < (size_t)nt * cap * 2) {
+        int rc = reserve_slots(ctx, cap);
         if (rc) return rc;
     }
     for (int attempt = 0; attempt < 2; ++attempt) {
-        CK(cudaMemsetAsync(ctx->tile_state.p, 0, (size_t)ctx->ntiles * 8, s), "memset");
-        CK(cudaMemsetAsync(ctx->ticket.p, 0, 4, s), "memset");
         CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
         CK(launch_extract_scan(extract_args(ctx), s, ctx->profiling ? ctx->ev_scan : nullptr),
            "extract scan launch");
@@ -383,11 +388,12 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
             ctx->scan_cached = true;
             return DELTA_OK;
         }
-        const unsigned long long need = ctx->h_summary->M;
-        int rc = reserve_entries(ctx, need + need / 8 + 1024);
+        uint32_t need = 1;
+        while (need < ctx->h_summary->max_count) need <<= 1;
+        int rc = reserve_slots(ctx, std::min(need, lanes_per_tile));
         if (rc) return rc;
     }
-    return fail(ctx, DELTA_ENOMEM, 0, "entry workspace overflow after resize");
+    return fail(ctx, DELTA_ENOMEM, 0, "tile slot overflow after resize");
 }
 
 extern "C" int delta_size(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *stream,

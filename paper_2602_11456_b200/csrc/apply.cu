@@ -138,6 +138,7 @@ struct ChunkView {
 };
 
 // Stage bytes [cs - halo, cs + len) of the record's stream into sb (sb[kHalo] = byte cs).
+// The caller synchronises before reading.
 __device__ __forceinline__ ChunkView stage_chunk(const uint8_t *body, const ApplyRec &R,
                                                  unsigned long long j, uint8_t *sb) {
     ChunkView v;
@@ -148,27 +149,52 @@ __device__ __forceinline__ ChunkView stage_chunk(const uint8_t *body, const Appl
     const uint32_t hs = (uint32_t)min(v.cs, (unsigned long long)kHalo);
     const uint8_t *src = body + R.idx_off + v.cs - hs;
     for (uint32_t b = threadIdx.x; b < hs + v.len; b += blockDim.x) sb[kHalo - hs + b] = __ldg(src + b);
-    __syncthreads();
     return v;
 }
 
-// Decode the varint whose terminator is at chunk position p; returns its status code.
-__device__ __forceinline__ uint32_t decode_at(const uint8_t *sb, const ChunkView &v, int p,
-                                              unsigned long long numel,
-                                              unsigned long long &val) {
-    int q = p;
-    int nb = 1;
-    while ((long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80)) {
+// Forward LEB128 decode of the varints whose terminator byte lies in this thread's 16
+// bytes of the chunk.  The first of them may begin in earlier bytes (up to 9 back, kept in
+// the halo / the previous thread's bytes): walk back to its first byte, then decode
+// forward once.  f(value, nbytes, last_byte, is_first_of_record) is called per varint in
+// stream order; nbytes is capped at 11 (anything > 10 is an error for the caller).
+template <typename F>
+__device__ __forceinline__ void decode_thread(const uint8_t *sb, const ChunkView &v, F &&f) {
+    const int p0 = threadIdx.x * 16;
+    const int p1 = min(p0 + 16, (int)v.len);
+    if (p0 >= p1) return;
+    int q = p0;
+    int back = 0;
+    while ((long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80) && back < 10) {
         --q;
-        if (++nb > 10) return kOverflow;
+        ++back;
     }
-    const uint8_t last = sb[kHalo + p];
-    unsigned long long x = 0;
-    for (int i = 0; i < nb; ++i) x |= (unsigned long long)(sb[kHalo + q + i] & 0x7F) << (7 * i);
-    val = x;
+    unsigned long long acc = 0;
+    int nb = back;  // bytes of the current varint before p0 (decoded below)
+    bool first = ((long long)v.cs + q == 0);
+    // a run of >= 10 continuation bytes before p0: the varint is already too long
+    if (back == 10 && (long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80)) nb = 11;
+    for (int i = 0; i < back && nb <= 10; ++i)
+        acc |= (unsigned long long)(sb[kHalo + q + i] & 0x7F) << (7 * i);
+    for (int p = p0; p < p1; ++p) {
+        const uint8_t b = sb[kHalo + p];
+        if (nb < 10) acc |= (unsigned long long)(b & 0x7F) << (7 * nb);
+        else if (nb == 10) acc |= (unsigned long long)(b & 0x01) << 63;
+        if (nb < 11) ++nb;
+        if (!(b & 0x80)) {
+            f(acc, nb, b, first);
+            acc = 0;
+            nb = 0;
+            first = false;
+        }
+    }
+}
+
+// Status of one decoded varint (SPEC.md:80 and the strictly-increasing invariant).
+__device__ __forceinline__ uint32_t varint_status(unsigned long long x, int nb, uint8_t last, bool first,
+                                                  unsigned long long numel) {
+    if (nb > 10) return kOverflow;
     if (nb == 10 && last > 1) return kOverflow;
     if (nb > 1 && last == 0) return kOverlong;
-    const bool first = ((long long)v.cs + q == 0);
     if (!first && x == 0) return kNonIncreasing;
     if (x >= numel) return kRange;
     return kOk;
@@ -189,22 +215,19 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
         const uint32_t k = record_of_chunk(rcb, n, c);
         const ApplyRec R = recs[k];
         const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
+        __syncthreads();
         uint32_t cnt = 0, err = kOk;
         unsigned long long sum = 0;
-        const int p0 = threadIdx.x * 16;
-        for (int p = p0; p < p0 + 16 && p < (int)v.len; ++p) {
-            if (sb[kHalo + p] & 0x80) {
-                if (v.last && p == (int)v.len - 1) err = err ? err : kTruncated;
-                continue;
-            }
-            unsigned long long x = 0;
-            const uint32_t e = decode_at(sb, v, p, R.numel, x);
+        decode_thread(sb, v, [&](unsigned long long x, int nb, uint8_t last, bool first) {
+            const uint32_t e = varint_status(x, nb, last, first, R.numel);
             if (e != kOk && err == kOk) err = e;
             ++cnt;
             sum = sat_add(sum, x);
-        }
+        });
+        const int pl = (int)v.len - 1;  // the stream's last byte must end a varint
+        if (v.last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (sb[kHalo + pl] & 0x80))
+            err = err ? err : kTruncated;
         if (err != kOk) set_status(st, err);
-        // block reduction of (count, saturating sum)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -230,20 +253,24 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
 }
 
 // ------------------------------------------------------------------------------ A3
+// One CTA per record: exclusive scan of its chunks' (count, gap sum) -> ordinal and index
+// base of every chunk; count == nnz and last index (= total gap sum) < N.
 __global__ void __launch_bounds__(1024)
 k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long long *__restrict__ rcb,
              const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
              unsigned long long *__restrict__ ord_base, unsigned long long *__restrict__ idx_base,
              ApplyState *st) {
     if (st->status != kOk) return;
+    __shared__ unsigned long long s_c[32], s_s[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t k = warp; k < n; k += 32) {
+    for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
         const unsigned long long c0 = rcb[k], c1 = rcb[k + 1];
-        unsigned long long cc = 0, cs = 0;  // carries: entries and gap sum before the window
-        for (unsigned long long b = c0; b < c1; b += 32) {
-            const unsigned long long c = b + lane;
+        unsigned long long cc = 0, cs = 0;
+        for (unsigned long long b = c0; b < c1; b += 1024) {
+            const unsigned long long c = b + threadIdx.x;
             unsigned long long x = c < c1 ? chunk_count[c] : 0;
             unsigned long long y = c < c1 ? chunk_sum[c] : 0;
+            const unsigned long long x0 = x, y0 = y;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned long long xx = __shfl_up_sync(0xffffffffu, x, o);
@@ -253,17 +280,34 @@ k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long 
                     y = sat_add(y, yy);
                 }
             }
-            unsigned long long xe = __shfl_up_sync(0xffffffffu, x, 1);
-            unsigned long long ye = __shfl_up_sync(0xffffffffu, y, 1);
-            if (lane == 0) xe = ye = 0;
-            if (c < c1) {
-                ord_base[c] = cc + xe;
-                idx_base[c] = sat_add(cs, ye);
+            if (lane == 31) {
+                s_c[warp] = x;
+                s_s[warp] = y;
             }
-            cc += __shfl_sync(0xffffffffu, x, 31);
-            cs = sat_add(cs, __shfl_sync(0xffffffffu, y, 31));
+            __syncthreads();
+            unsigned long long pc = 0, ps = 0, tc = 0, ts = 0;
+            for (int w = 0; w < 32; ++w) {
+                if (w < warp) {
+                    pc += s_c[w];
+                    ps = sat_add(ps, s_s[w]);
+                }
+                tc += s_c[w];
+                ts = sat_add(ts, s_s[w]);
+            }
+            __syncthreads();
+            // exclusive = prefix of earlier warps + inclusive within warp - own
+            // (the gap sum is saturating: recompute the exclusive part via a shuffle)
+            unsigned long long ye = __shfl_up_sync(0xffffffffu, y, 1);
+            if (lane == 0) ye = 0;
+            if (c < c1) {
+                ord_base[c] = cc + pc + (x - x0);
+                idx_base[c] = sat_add(cs, sat_add(ps, ye));
+            }
+            (void)y0;
+            cc += tc;
+            cs = sat_add(cs, ts);
         }
-        if (lane == 0) {
+        if (threadIdx.x == 0) {
             const ApplyRec R = recs[k];
             if (cc != R.nnz) set_status(st, kCount);
             else if (R.nnz > 0 && cs >= R.numel) set_status(st, kRange);
@@ -272,15 +316,19 @@ k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long 
 }
 
 // ------------------------------------------------------------------------------ A4
+// Gated scatter-store: decode again, absolute index = chunk base + running gap sum, value
+// from the chunk's slice of the record's value array (staged in shared memory).
 template <int W>
 __global__ void __launch_bounds__(256)
 k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
-          const unsigned long long *__restrict__ rcb, const unsigned long long *__restrict__ ord_base,
-          const unsigned long long *__restrict__ idx_base, const ApplyState *st) {
+          const unsigned long long *__restrict__ rcb, const unsigned int *__restrict__ chunk_count,
+          const unsigned long long *__restrict__ ord_base, const unsigned long long *__restrict__ idx_base,
+          const ApplyState *st) {
     using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
     if (st->status != kOk) return;  // the gate: nothing is written unless all checks passed
     const unsigned long long nch = st->n_chunks;
     __shared__ uint8_t sb[kHalo + kByteChunk];
+    __shared__ LT sv[kByteChunk];  // at most one varint per byte
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -288,20 +336,22 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         const uint32_t k = record_of_chunk(rcb, n, c);
         const ApplyRec R = recs[k];
         const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
-        const int p0 = threadIdx.x * 16;
-        const int p1 = min(p0 + 16, (int)v.len);
+        const unsigned long long ob = ord_base[c];
+        const uint32_t cn = chunk_count[c];
+        {  // stage this chunk's values (cn lanes, any alignment in the body)
+            const uint8_t *src = body + R.val_off + ob * W;
+            uint8_t *dst = reinterpret_cast<uint8_t *>(sv);
+            for (uint32_t b = threadIdx.x; b < cn * W; b += blockDim.x) dst[b] = __ldg(src + b);
+        }
+        __syncthreads();
         uint32_t cnt = 0;
         unsigned long long sum = 0;
-        for (int p = p0; p < p1; ++p) {
-            if (sb[kHalo + p] & 0x80) continue;
-            unsigned long long x = 0;
-            decode_at(sb, v, p, ~0ull, x);
+        decode_thread(sb, v, [&](unsigned long long x, int, uint8_t, bool) {
             ++cnt;
             sum += x;
-        }
-        // block exclusive scan of (cnt, sum)
-        uint32_t ci = warp_inclusive_sum(cnt);
-        unsigned long long si = warp_inclusive_sum(sum);
+        });
+        const uint32_t ci = warp_inclusive_sum(cnt);
+        const unsigned long long si = warp_inclusive_sum(sum);
         if (lane == 31) {
             s_cnt[warp] = ci;
             s_sum[warp] = si;
@@ -313,22 +363,14 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
             cpre += s_cnt[w];
             spre += s_sum[w];
         }
-        unsigned long long ord = ord_base[c] + cpre + ci - cnt;
+        uint32_t ord = cpre + ci - cnt;
         unsigned long long idx = idx_base[c] + spre + si - sum;
         LT *w = reinterpret_cast<LT *>(R.w);
-        const uint8_t *vals = body + R.val_off;
-        for (int p = p0; p < p1; ++p) {
-            if (sb[kHalo + p] & 0x80) continue;
-            unsigned long long x = 0;
-            decode_at(sb, v, p, ~0ull, x);
+        decode_thread(sb, v, [&](unsigned long long x, int, uint8_t, bool) {
             idx += x;
-            const uint8_t *vp = vals + ord * W;
-            LT val;
-            if constexpr (W == 2) val = (LT)(__ldg(vp) | (__ldg(vp + 1) << 8));
-            else val = (LT)__ldg(vp) | ((LT)__ldg(vp + 1) << 8) | ((LT)__ldg(vp + 2) << 16) | ((LT)__ldg(vp + 3) << 24);
-            w[idx] = val;
+            w[idx] = sv[ord];
             ++ord;
-        }
+        });
         __syncthreads();
     }
 }
@@ -342,14 +384,15 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin,
                                                   a.chunk_count, a.chunk_sum, a.state);
     if (ev) cudaEventRecord(ev[2], s);
-    k_apply_scan<<<1, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
-                                    a.chunk_ord_base, a.chunk_idx_base, a.state);
+    const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
+    k_apply_scan<<<nb, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
+                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[3], s);
     if (a.width == 2)
-        k_scatter<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin,
+        k_scatter<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
                                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
     else
-        k_scatter<4><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin,
+        k_scatter<4><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
                                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[4], s);
     return cudaGetLastError();

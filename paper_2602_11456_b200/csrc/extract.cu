@@ -1,20 +1,24 @@
 // extract.cu — sm_100a kernels for delta extraction.
 //
-//   K1 k_scan_compact   E2+E3: bitwise compare of old/new (16-byte streaming loads),
-//                       per-vector lane masks, packed block scan of counts, decoupled
-//                       look-back across tiles (ticket-ordered), ordered write of the
-//                       compacted (index, value) entries.  The only kernel that reads the
-//                       2W bytes of weights: it bounds the whole path (HBM roofline).
-//   K2 k_entry_lens     E4+E5 lengths: gap of every entry (first index of a tensor as-is,
-//                       PAPER.md:389), LEB128 length, per-chunk byte sums and the partial
-//                       sums at tensor starts.
-//   K3 k_finalize       E6: scan of chunk sums, per-tensor index-stream lengths, record
-//                       sizes and offsets (the offset table), body size.
-//   K4 k_emit           E5+E6: LEB128 bytes and raw values written to their final offsets.
-//   K5 k_headers        E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
+//   K1  k_scan_tiles    E2+E3: the only kernel that reads the 2W bytes of weights.  One
+//                       CTA per tile (16 Ki 16-bit lanes = 32 KiB of old + 32 KiB of new),
+//                       16-byte streaming loads, bitwise lane compare, per-vector change
+//                       masks, one packed block scan for the ranks, ordered compaction into
+//                       shared memory, coalesced copy into the tile's workspace slot (u16
+//                       lane offset + raw lane), per-tile count / first / last / internal
+//                       LEB128 bytes.  No inter-CTA communication: a pure streaming pass.
+//   K2  k_tiles_reduce / k_blocks_scan / k_tiles_bytes / k_tiles_place
+//                       E3+E4+E5 sizes: scans over the (small) per-tile metadata — entry
+//                       prefix, nearest earlier non-empty tile (its last change is the
+//                       predecessor of the tile's first change), each tile's
+//                       LEB128 bytes, byte prefix, per-tensor entry/byte begins.
+//   K3  k_finalize      E6: record sizes and offsets (the offset table), body size.
+//   K4  k_emit_tiles    E5+E6: one warp per tile writes LEB128 bytes and raw values to their
+//                       final body offsets.
+//   K5  k_headers       E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
 //
-// Every kernel here is product code written for this library; none shares code with
-// oracle/.  Semantics: DESIGN.md §3 readings R1-R5, R12-R15.
+// Product code written for this library; none of it is shared with the test oracle.
+// Semantics: DESIGN.md §3 readings R1-R5, R12-R15.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -73,27 +77,64 @@ __device__ __forceinline__ uint32_t diff_mask(const uint4 &a, const uint4 &b) {
     }
 }
 
+template <int NW, typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T *s_warp, T &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const T inc = warp_inclusive_sum(v);
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    T pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const T x = s_warp[w];
+        if (w < warp) pre += x;
+        tot += x;
+    }
+    __syncthreads();
+    total = tot;
+    return pre + inc - v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const T y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y > v ? y : v;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_max(T v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o && y > v) v = y;
+    }
+    return v;
+}
+
 // ------------------------------------------------------------------------------ K1
-template <int W, typename IdxT>
+template <int W>
 __global__ void __launch_bounds__(kScanThreads)
-k_scan_compact(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t ntensors,
-               unsigned long long *tile_state, unsigned int *ticket,
-               IdxT *__restrict__ ws_idx, typename LaneOf<W>::T *__restrict__ ws_val,
-               unsigned long long ws_cap, unsigned long long *__restrict__ entry_begin,
-               ExtractSummary *summary) {
+k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint16_t *__restrict__ slot_off,
+             typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
+             ExtractSummary *summary) {
     using LT = typename LaneOf<W>::T;
-    constexpr int LPV = 16 / W;  // lanes per 16-byte vector
+    constexpr int LPV = 16 / W;                            // lanes per 16-byte vector
+    constexpr int LANES = kScanThreads * kScanVecs * LPV;  // lanes per tile
     static_assert(kScanVecs == 8, "count packing assumes 8 vectors per thread");
-    __shared__ uint32_t s_tile;
+    static_assert(LANES <= 65536, "lane offsets are u16");
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);                 // LANES
+    LT *s_val = reinterpret_cast<LT *>(smem + LANES * sizeof(uint16_t));  // LANES
     __shared__ uint32_t s_warp[kScanThreads / 32][4];
-    __shared__ unsigned long long s_excl;
+    __shared__ uint32_t s_red[kScanThreads / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // Ticket order = look-back order: every tile with a smaller id belongs to a CTA that
-    // is already running, so the look-back below always makes progress.
-    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t t = s_tile;
+    const uint32_t t = blockIdx.x;
     const TileDesc d = tiles[t];
     const uint32_t nl = d.nlanes;
 
@@ -129,15 +170,14 @@ k_scan_compact(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t nte
         }
     }
 
-    // Per-vector change masks and counts; 8 counts (<= LPV each) packed as 16-bit
-    // fields into 4 words so one block scan yields all 8 per-vector prefixes.
+    // Per-vector change masks; 8 counts (<= LPV each) packed as 16-bit fields into 4 words
+    // so one block scan yields every vector's rank base.
     uint32_t m[kScanVecs];
     uint32_t pk[4];
 #pragma unroll
     for (int r = 0; r < kScanVecs; ++r) m[r] = diff_mask<W>(vo[r], vn[r]);
 #pragma unroll
     for (int q = 0; q < 4; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
-
     uint32_t inc[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) inc[q] = warp_inclusive_sum(pk[q]);
@@ -156,208 +196,250 @@ k_scan_compact(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t nte
             tot[q] += x;
         }
     }
-    uint32_t agg = 0;
+    uint32_t c = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) agg += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
+    for (int q = 0; q < 4; ++q) c += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
 
-    // Decoupled look-back (warp 0): publish the aggregate, then sum predecessors until an
-    // inclusive prefix is found, then publish our inclusive prefix.
-    if (warp == 0) {
-        unsigned long long excl = 0;
-        if (t == 0) {
-            if (lane == 0) st_release_u64(&tile_state[0], kFlagIncl | agg);
-        } else {
-            if (lane == 0) st_release_u64(&tile_state[t], kFlagAgg | agg);
-            long long pred = (long long)t - 1;
-            while (true) {
-                const long long i = pred - lane;
-                unsigned long long s = kFlagIncl;  // before tile 0: inclusive prefix 0
-                if (i >= 0) {
-                    do {
-                        s = ld_acquire_u64(&tile_state[i]);
-                    } while ((s >> 62) == 0);
-                }
-                const unsigned incl = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-                unsigned long long v = s & kValMask;
-                if (incl) {
-                    const int k = __ffs(incl) - 1;
-                    if (lane > k) v = 0;
-                    excl += warp_sum(v);
-                    break;
-                }
-                excl += warp_sum(v);
-                pred -= 32;
-            }
-            if (lane == 0) st_release_u64(&tile_state[t], kFlagIncl | (excl + agg));
-        }
-        if (lane == 0) s_excl = excl;
-    }
-    __syncthreads();
-    const unsigned long long base = s_excl;
-
-    if (tid == 0) {
-        if (d.flags_tensor & kTileFirstOfTensor)
-            entry_begin[d.flags_tensor & kTileTensorMask] = base;
-        if (t == ntiles - 1) {
-            summary->M = base + agg;
-            entry_begin[ntensors] = base + agg;
-        }
-    }
-    if (base + agg > ws_cap) {
-        if (tid == 0) summary->overflow = 1;
-        return;
-    }
-    // Ordered write: entry (r, tid, j) goes to base + sum_{r'<r} tot_r' + prefix_r(tid) + rank_j.
-    unsigned long long rbase = base;
+    // Ordered compaction into shared memory: entry (r, tid, j) gets rank
+    // sum_{r'<r} tot_r' + prefix_r(tid) + popc(mask below j) — lane order.
+    uint32_t rbase = 0;
 #pragma unroll
     for (int r = 0; r < kScanVecs; ++r) {
         const int q = r >> 1, sh = (r & 1) * 16;
-        unsigned long long pos = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
+        uint32_t pos = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
         uint32_t mm = m[r];
         while (mm) {
             const int j = __ffs(mm) - 1;
             mm &= mm - 1;
-            const uint64_t li = (uint64_t)(r * kScanThreads + tid) * LPV + j;
-            ws_idx[pos] = (IdxT)(d.lane_base + li);
-            ws_val[pos] = (LT)lane_of<W>(vn[r], j);
+            s_off[pos] = (uint16_t)((r * kScanThreads + tid) * LPV + j);
+            s_val[pos] = (LT)lane_of<W>(vn[r], j);
             ++pos;
         }
         rbase += (tot[q] >> sh) & 0xFFFFu;
     }
-}
+    __syncthreads();
 
-// ---------------------------------------------------------------- entry helpers (K2, K4)
-// Largest k in [0, T] with E[k] <= i (E nondecreasing, E[0] = 0).
-__device__ __forceinline__ uint32_t tensor_of(const unsigned long long *E, uint32_t T,
-                                              unsigned long long i) {
-    uint32_t lo = 0, hi = T;  // invariant: E[lo] <= i
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(E + mid) <= i) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
-template <typename IdxT>
-__device__ __forceinline__ void load_entries(const IdxT *ws_idx, unsigned long long i0,
-                                             unsigned long long M, IdxT (&v)[kEntryPerThread]) {
-    if (i0 + kEntryPerThread <= M) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(ws_idx + i0);
-        constexpr int NV = kEntryPerThread * sizeof(IdxT) / 16;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            uint4 x = __ldg(p + q);
-            IdxT *dst = reinterpret_cast<IdxT *>(&x);
-#pragma unroll
-            for (int e = 0; e < (int)(16 / sizeof(IdxT)); ++e) v[q * (16 / sizeof(IdxT)) + e] = dst[e];
+    if (c > slot_cap) {  // slot too small: report, write nothing (host grows slots, reruns)
+        if (tid == 0) {
+            meta[t] = TileMeta{c, 0, 0, 0, 0};
+            summary->overflow = 1;
+            atomicMax(&summary->max_count, (unsigned long long)c);
         }
-    } else {
-#pragma unroll
-        for (int e = 0; e < kEntryPerThread; ++e) v[e] = (i0 + e < M) ? __ldg(ws_idx + i0 + e) : 0;
+        return;
     }
-}
-
-template <int NW, typename T>
-__device__ __forceinline__ T block_excl_scan(T v, T *s_warp, T &total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const T inc = warp_inclusive_sum(v);
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    T pre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        const T x = s_warp[w];
-        if (w < warp) pre += x;
-        tot += x;
+    // Coalesced copy of the slot + LEB128 bytes of the gaps inside the tile.
+    uint16_t *so = slot_off + (size_t)t * slot_cap;
+    LT *sv = slot_val + (size_t)t * slot_cap;
+    uint32_t L = 0;
+    for (uint32_t i = tid; i < c; i += kScanThreads) {
+        const uint16_t o = s_off[i];
+        so[i] = o;
+        sv[i] = s_val[i];
+        if (i > 0) L += leb_len((unsigned long long)(o - s_off[i - 1]));
     }
+    L = warp_sum(L);
+    if (lane == 0) s_red[warp] = L;
     __syncthreads();
-    total = tot;
-    return pre + inc - v;
+    if (tid == 0) {
+        uint32_t tl = 0;
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; ++w) tl += s_red[w];
+        meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
+    }
 }
 
 // ------------------------------------------------------------------------------ K2
-template <typename IdxT>
-__global__ void __launch_bounds__(256)
-k_entry_lens(const IdxT *__restrict__ ws_idx, const unsigned long long *__restrict__ E,
-             uint32_t T, const ExtractSummary *summary, unsigned int *__restrict__ chunk_bytes,
-             unsigned long long *__restrict__ tstart_partial) {
+// Tile-level scans over blocks of kTileBlock tiles (1024 threads x 4 tiles).
+__global__ void __launch_bounds__(1024)
+k_tiles_reduce(const TileMeta *__restrict__ meta, uint32_t ntiles, unsigned long long *__restrict__ blk_cnt,
+               long long *__restrict__ blk_key, const ExtractSummary *summary) {
     if (summary->overflow) return;
-    const unsigned long long M = summary->M;
-    const unsigned long long nchunks = (M + kEntryChunk - 1) / kEntryChunk;
-    __shared__ uint32_t s_warp[8];
-    for (unsigned long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const unsigned long long i0 = c * kEntryChunk + (unsigned long long)threadIdx.x * kEntryPerThread;
-        IdxT v[kEntryPerThread];
-        load_entries<IdxT>(ws_idx, i0, M, v);
-        uint32_t k = tensor_of(E, T, i0 < M ? i0 : M);
-        unsigned long long prev = (i0 > 0 && i0 < M) ? (unsigned long long)__ldg(ws_idx + i0 - 1) : 0;
-        uint32_t lens[kEntryPerThread];
-        uint32_t S = 0;
-        bool has_start = false;
+    __shared__ unsigned long long s_c[32];
+    __shared__ long long s_k[32];
+    const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
+    unsigned long long c = 0;
+    long long key = -1;
 #pragma unroll
-        for (int e = 0; e < kEntryPerThread; ++e) {
-            const unsigned long long i = i0 + e;
-            uint32_t L = 0;
-            if (i < M) {
-                while (__ldg(E + k + 1) <= i) ++k;
-                const bool first = (i == __ldg(E + k));
-                has_start |= first;
-                const unsigned long long g = (unsigned long long)v[e] - (first ? 0ull : prev);
-                L = leb_len(g);
-                prev = v[e];
-            }
-            lens[e] = L;
-            S += L;
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t t = t0 + e;
+        if (t < ntiles) {
+            const uint32_t n = meta[t].count;
+            c += n;
+            if (n) key = t;
         }
-        uint32_t total;
-        const uint32_t P = block_excl_scan<8, uint32_t>(S, s_warp, total);
-        if (threadIdx.x == 0) chunk_bytes[c] = total;
-        if (has_start) {  // byte offset (within the chunk) of every tensor start we hold
-            uint32_t acc = P;
-            k = tensor_of(E, T, i0);
-            for (int e = 0; e < kEntryPerThread; ++e) {
-                const unsigned long long i = i0 + e;
-                if (i >= M) break;
-                while (__ldg(E + k + 1) <= i) ++k;
-                if (i == __ldg(E + k)) {
-                    // tensor k starts here, and so do any empty tensors just before it
-                    for (int kk = (int)k; kk >= 0 && __ldg(E + kk) == i; --kk) tstart_partial[kk] = acc;
-                }
-                acc += lens[e];
-            }
+    }
+    c = warp_sum(c);
+    key = warp_max(key);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_c[warp] = c;
+        s_k[warp] = key;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tc = 0;
+        long long tk = -1;
+        for (int w = 0; w < 32; ++w) {
+            tc += s_c[w];
+            tk = s_k[w] > tk ? s_k[w] : tk;
         }
+        blk_cnt[blockIdx.x] = tc;
+        blk_key[blockIdx.x] = tk;
+    }
+}
+
+// One CTA: exclusive sum-scan of blk_a (in place) and, if blk_key != nullptr, exclusive
+// max-scan of blk_key (in place, identity -1).
+__global__ void __launch_bounds__(1024)
+k_blocks_scan(unsigned long long *__restrict__ blk_a, long long *__restrict__ blk_key, uint32_t nblk,
+              const ExtractSummary *summary) {
+    if (summary->overflow) return;
+    __shared__ unsigned long long s_w[32];
+    __shared__ long long s_m[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long carry = 0;
+    long long mcarry = -1;
+    for (uint32_t b = 0; b < nblk; b += 1024) {
+        const uint32_t i = b + threadIdx.x;
+        const unsigned long long x = i < nblk ? blk_a[i] : 0;
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan<32, unsigned long long>(x, s_w, tot);
+        if (blk_key) {
+            const long long k = i < nblk ? blk_key[i] : -1;
+            const long long inc = warp_inclusive_max(k);
+            if (lane == 31) s_m[warp] = inc;
+            __syncthreads();
+            long long pre = -1, all = -1;
+            for (int w = 0; w < 32; ++w) {
+                if (w < warp && s_m[w] > pre) pre = s_m[w];
+                if (s_m[w] > all) all = s_m[w];
+            }
+            long long exm = __shfl_up_sync(0xffffffffu, inc, 1);
+            if (lane == 0) exm = -1;
+            if (pre > exm) exm = pre;
+            if (mcarry > exm) exm = mcarry;
+            __syncthreads();
+            if (i < nblk) blk_key[i] = exm;
+            if (all > mcarry) mcarry = all;
+        }
+        if (i < nblk) blk_a[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+// Per tile: entry prefix E_t, predecessor of its first change, its LEB128 bytes.
+__global__ void __launch_bounds__(1024)
+k_tiles_bytes(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
+              const unsigned long long *__restrict__ blk_cnt, const long long *__restrict__ blk_key,
+              const uint32_t *__restrict__ tensor_first_tile, unsigned long long *__restrict__ tile_entry,
+              unsigned long long *__restrict__ tile_pred, unsigned int *__restrict__ tile_bytes,
+              unsigned long long *__restrict__ blk_bytes, const ExtractSummary *summary) {
+    if (summary->overflow) return;
+    __shared__ unsigned long long s_w[32];
+    __shared__ long long s_m[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
+    TileMeta mt[4];
+    unsigned long long c = 0;
+    long long key = -1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        mt[e] = t0 + e < ntiles ? meta[t0 + e] : TileMeta{0, 0, 0, 0, 0};
+        c += mt[e].count;
+        if (mt[e].count) key = t0 + e;
+    }
+    unsigned long long tot;
+    unsigned long long cex = block_excl_scan<32, unsigned long long>(c, s_w, tot) + blk_cnt[blockIdx.x];
+    const long long kinc = warp_inclusive_max(key);
+    if (lane == 31) s_m[warp] = kinc;
+    __syncthreads();
+    long long kex = __shfl_up_sync(0xffffffffu, kinc, 1);
+    if (lane == 0) kex = -1;
+    for (int w = 0; w < warp; ++w)
+        if (s_m[w] > kex) kex = s_m[w];
+    if (blk_key[blockIdx.x] > kex) kex = blk_key[blockIdx.x];
+    unsigned int mybytes = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t t = t0 + e;
+        if (t >= ntiles) break;
+        unsigned long long pred = 0;
+        unsigned int b = 0;
+        if (mt[e].count) {
+            const TileDesc d = tiles[t];
+            const uint32_t k = d.flags_tensor & kTileTensorMask;
+            if (kex >= 0 && (unsigned long long)kex >= tensor_first_tile[k]) {
+                pred = tiles[kex].lane_base + meta[kex].last_off;  // last change before this tile
+            }
+            const unsigned long long first = d.lane_base + mt[e].first_off;
+            b = mt[e].internal_bytes + leb_len(first - pred);
+            kex = t;
+        }
+        tile_entry[t] = cex;
+        tile_pred[t] = pred;
+        tile_bytes[t] = b;
+        cex += mt[e].count;
+        mybytes += b;
+    }
+    __syncthreads();  // s_w reuse
+    unsigned long long bs = warp_sum((unsigned long long)mybytes);
+    if (lane == 0) s_w[warp] = bs;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long x = 0;
+        for (int w = 0; w < 32; ++w) x += s_w[w];
+        blk_bytes[blockIdx.x] = x;
+    }
+}
+
+// Per tile: byte prefix; per tensor: E_k and B_k at its first tile; totals.
+__global__ void __launch_bounds__(1024)
+k_tiles_place(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
+              uint32_t ntensors, const unsigned long long *__restrict__ tile_entry,
+              const unsigned int *__restrict__ tile_bytes, const unsigned long long *__restrict__ blk_bytes,
+              unsigned long long *__restrict__ tile_byte, unsigned long long *__restrict__ entry_begin,
+              unsigned long long *__restrict__ tensor_byte_begin, ExtractSummary *summary) {
+    if (summary->overflow) return;
+    __shared__ unsigned long long s_w[32];
+    const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
+    unsigned int b[4];
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        b[e] = t0 + e < ntiles ? tile_bytes[t0 + e] : 0;
+        mine += b[e];
+    }
+    unsigned long long tot;
+    unsigned long long ex = block_excl_scan<32, unsigned long long>(mine, s_w, tot) + blk_bytes[blockIdx.x];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t t = t0 + e;
+        if (t >= ntiles) break;
+        tile_byte[t] = ex;
+        const uint32_t f = tiles[t].flags_tensor;
+        if (f & kTileFirstOfTensor) {
+            entry_begin[f & kTileTensorMask] = tile_entry[t];
+            tensor_byte_begin[f & kTileTensorMask] = ex;
+        }
+        if (t == ntiles - 1) {
+            const unsigned long long M = tile_entry[t] + meta[t].count;
+            entry_begin[ntensors] = M;
+            tensor_byte_begin[ntensors] = ex + b[e];
+            summary->M = M;
+            summary->idx_bytes = ex + b[e];
+        }
+        ex += b[e];
     }
 }
 
 // ------------------------------------------------------------------------------ K3
 __global__ void __launch_bounds__(1024)
-k_finalize(const unsigned long long *__restrict__ E, uint32_t T, const uint32_t *__restrict__ name_len,
-           const unsigned int *__restrict__ chunk_bytes, unsigned long long *__restrict__ chunk_prefix,
-           const unsigned long long *__restrict__ tstart_partial,
-           unsigned long long *__restrict__ Bk, RecordRow *__restrict__ table, int width,
-           const unsigned long long *__restrict__ numel, ExtractSummary *summary) {
+k_finalize(const unsigned long long *__restrict__ E, const unsigned long long *__restrict__ Bk, uint32_t T,
+           const uint32_t *__restrict__ name_len, const unsigned long long *__restrict__ numel,
+           RecordRow *__restrict__ table, int width, ExtractSummary *summary) {
     if (summary->overflow) return;
     __shared__ unsigned long long s_warp[32];
-    const unsigned long long M = summary->M;
-    const unsigned long long nchunks = (M + kEntryChunk - 1) / kEntryChunk;
     unsigned long long carry = 0;
-    for (unsigned long long b = 0; b < nchunks; b += 1024) {
-        const unsigned long long c = b + threadIdx.x;
-        const unsigned long long x = c < nchunks ? chunk_bytes[c] : 0;
-        unsigned long long tot;
-        const unsigned long long ex = block_excl_scan<32, unsigned long long>(x, s_warp, tot);
-        if (c < nchunks) chunk_prefix[c] = carry + ex;
-        carry += tot;
-    }
-    const unsigned long long total_idx = carry;
-    __syncthreads();
-    for (uint32_t k = threadIdx.x; k <= T; k += 1024) {
-        const unsigned long long e = E[k];
-        Bk[k] = (e >= M) ? total_idx : chunk_prefix[e / kEntryChunk] + tstart_partial[k];
-    }
-    __syncthreads();
-    carry = 0;
     for (uint32_t b = 0; b < T; b += 1024) {
         const uint32_t k = b + threadIdx.x;
         unsigned long long rb = 0, nnz = 0, ilen = 0;
@@ -381,69 +463,59 @@ k_finalize(const unsigned long long *__restrict__ E, uint32_t T, const uint32_t 
         }
         carry += tot;
     }
-    if (threadIdx.x == 0) {
-        summary->idx_bytes = total_idx;
-        summary->body_bytes = carry;
-    }
+    if (threadIdx.x == 0) summary->body_bytes = carry;
 }
 
 // ------------------------------------------------------------------------------ K4
-template <int W, typename IdxT>
+// One warp per tile: LEB128 bytes of the tile's gaps and its raw values, written to their
+// final offsets in the body.
+template <int W>
 __global__ void __launch_bounds__(256)
-k_emit(const IdxT *__restrict__ ws_idx, const typename LaneOf<W>::T *__restrict__ ws_val,
-       const unsigned long long *__restrict__ E, uint32_t T, const ExtractSummary *summary,
-       const unsigned long long *__restrict__ chunk_prefix, const unsigned long long *__restrict__ Bk,
-       const RecordRow *__restrict__ table, uint8_t *__restrict__ out) {
+k_emit_tiles(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
+             uint32_t slot_cap, const uint16_t *__restrict__ slot_off,
+             const typename LaneOf<W>::T *__restrict__ slot_val,
+             const unsigned long long *__restrict__ tile_entry, const unsigned long long *__restrict__ tile_byte,
+             const unsigned long long *__restrict__ tile_pred, const unsigned long long *__restrict__ E,
+             const unsigned long long *__restrict__ Bk, const RecordRow *__restrict__ table,
+             uint8_t *__restrict__ out) {
     using LT = typename LaneOf<W>::T;
-    const unsigned long long M = summary->M;
-    const unsigned long long nchunks = (M + kEntryChunk - 1) / kEntryChunk;
-    __shared__ uint32_t s_warp[8];
-    for (unsigned long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const unsigned long long i0 = c * kEntryChunk + (unsigned long long)threadIdx.x * kEntryPerThread;
-        IdxT v[kEntryPerThread];
-        load_entries<IdxT>(ws_idx, i0, M, v);
-        const uint32_t k0 = tensor_of(E, T, i0 < M ? i0 : M);
-        const unsigned long long prev0 = (i0 > 0 && i0 < M) ? (unsigned long long)__ldg(ws_idx + i0 - 1) : 0;
-        uint32_t k = k0;
-        unsigned long long prev = prev0;
-        uint32_t S = 0;
-#pragma unroll
-        for (int e = 0; e < kEntryPerThread; ++e) {
-            const unsigned long long i = i0 + e;
-            if (i < M) {
-                while (__ldg(E + k + 1) <= i) ++k;
-                const bool first = (i == __ldg(E + k));
-                S += leb_len((unsigned long long)v[e] - (first ? 0ull : prev));
-                prev = v[e];
+    const int lane = threadIdx.x & 31;
+    const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t t = wg; t < ntiles; t += nw) {
+        const uint32_t c = meta[t].count;
+        if (c == 0) continue;
+        const TileDesc d = tiles[t];
+        const uint32_t k = d.flags_tensor & kTileTensorMask;
+        uint8_t *ib = out + table[k].index_offset + (tile_byte[t] - Bk[k]);
+        uint8_t *vb = out + table[k].values_offset + (tile_entry[t] - E[k]) * W;
+        const uint16_t *so = slot_off + (size_t)t * slot_cap;
+        const LT *sv = slot_val + (size_t)t * slot_cap;
+        unsigned long long prev = tile_pred[t];
+        unsigned long long pos = 0;
+        for (uint32_t base = 0; base < c; base += 32) {
+            const uint32_t i = base + lane;
+            const bool valid = i < c;
+            const unsigned long long abs = valid ? d.lane_base + so[i] : 0;
+            unsigned long long pa = __shfl_up_sync(0xffffffffu, abs, 1);
+            if (lane == 0) pa = prev;
+            unsigned long long g = abs - pa;
+            const uint32_t L = valid ? leb_len(g) : 0;
+            const uint32_t incl = warp_inclusive_sum(L);
+            if (valid) {
+                uint8_t *dst = ib + pos + (incl - L);
+                uint32_t n = 0;
+                while (g >= 0x80) {
+                    dst[n++] = (uint8_t)(g | 0x80);
+                    g >>= 7;
+                }
+                dst[n] = (uint8_t)g;
             }
+            pos += __shfl_sync(0xffffffffu, incl, 31);
+            prev = __shfl_sync(0xffffffffu, abs, 31);
         }
-        uint32_t total;
-        const uint32_t P = block_excl_scan<8, uint32_t>(S, s_warp, total);
-        unsigned long long pos = chunk_prefix[c] + P;  // position in the concatenated streams
-        k = k0;
-        prev = prev0;
-        for (int e = 0; e < kEntryPerThread; ++e) {
-            const unsigned long long i = i0 + e;
-            if (i >= M) break;
-            while (__ldg(E + k + 1) <= i) ++k;
-            const unsigned long long Ek = __ldg(E + k);
-            const bool first = (i == Ek);
-            unsigned long long g = (unsigned long long)v[e] - (first ? 0ull : prev);
-            prev = v[e];
-            const RecordRow &row = table[k];
-            uint8_t *dst = out + __ldg(&row.index_offset) + (pos - __ldg(Bk + k));
-            uint32_t n = 0;
-            while (g >= 0x80) {
-                dst[n++] = (uint8_t)(g | 0x80);
-                g >>= 7;
-            }
-            dst[n++] = (uint8_t)g;
-            pos += n;
-            const LT val = __ldg(ws_val + i);
-            uint8_t *vd = out + __ldg(&row.values_offset) + (i - Ek) * W;
-#pragma unroll
-            for (int b = 0; b < W; ++b) vd[b] = (uint8_t)(val >> (8 * b));
-        }
+        const uint32_t nb = c * W;
+        for (uint32_t b = lane; b < nb; b += 32) vb[b] = (uint8_t)(sv[b / W] >> (8 * (b % W)));
     }
 }
 
@@ -474,32 +546,41 @@ k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__res
 }
 
 // ------------------------------------------------------------------------------ launchers
-template <int W, typename IdxT>
+template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
+    constexpr int LANES = kScanThreads * kScanVecs * (16 / W);
+    const size_t smem = (size_t)LANES * (sizeof(uint16_t) + W);
+    cudaFuncSetAttribute(k_scan_tiles<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
-    k_scan_compact<W, IdxT><<<a.ntiles, kScanThreads, 0, s>>>(
-        a.tiles, a.ntiles, a.ntensors, a.tile_state, a.ticket, static_cast<IdxT *>(a.ws_idx),
-        static_cast<LT *>(a.ws_val), a.ws_cap, a.entry_begin, a.summary);
+    k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_off,
+                                                         static_cast<LT *>(a.slot_val), a.meta, a.summary);
     if (ev) cudaEventRecord(ev[1], s);
-    k_entry_lens<IdxT><<<a.persist_ctas, 256, 0, s>>>(static_cast<const IdxT *>(a.ws_idx),
-                                                      a.entry_begin, a.ntensors, a.summary,
-                                                      a.chunk_bytes, a.tstart_partial);
+    const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
+    k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
+    k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);
+    k_tiles_bytes<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.blk_a, a.blk_key, a.tensor_first_tile,
+                                        a.tile_entry, a.tile_pred, a.tile_bytes_tmp, a.blk_a + nblk,
+                                        a.summary);
+    k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a + nblk, nullptr, nblk, a.summary);
+    k_tiles_place<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.ntensors, a.tile_entry,
+                                        a.tile_bytes_tmp, a.blk_a + nblk, a.tile_byte, a.entry_begin,
+                                        a.tensor_byte_begin, a.summary);
     if (ev) cudaEventRecord(ev[2], s);
-    k_finalize<<<1, 1024, 0, s>>>(a.entry_begin, a.ntensors, a.name_len, a.chunk_bytes,
-                                  a.chunk_prefix, a.tstart_partial, a.tensor_byte_begin, a.table,
-                                  a.width, a.numel, a.summary);
+    k_finalize<<<1, 1024, 0, s>>>(a.entry_begin, a.tensor_byte_begin, a.ntensors, a.name_len, a.numel,
+                                  a.table, a.width, a.summary);
     if (ev) cudaEventRecord(ev[3], s);
     return cudaGetLastError();
 }
 
-template <int W, typename IdxT>
+template <int W>
 static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
-    k_emit<W, IdxT><<<a.persist_ctas, 256, 0, s>>>(
-        static_cast<const IdxT *>(a.ws_idx), static_cast<const LT *>(a.ws_val), a.entry_begin,
-        a.ntensors, a.summary, a.chunk_prefix, a.tensor_byte_begin, a.table, out);
+    k_emit_tiles<W><<<a.persist_ctas, 256, 0, s>>>(a.tiles, a.meta, a.ntiles, a.slot_cap, a.slot_off,
+                                                   static_cast<const LT *>(a.slot_val), a.tile_entry,
+                                                   a.tile_byte, a.tile_pred, a.entry_begin,
+                                                   a.tensor_byte_begin, a.table, out);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
     k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out);
@@ -508,13 +589,11 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
 }
 
 cudaError_t launch_extract_scan(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
-    if (a.width == 2) return a.idx64 ? scan_impl<2, uint64_t>(a, s, ev) : scan_impl<2, uint32_t>(a, s, ev);
-    return a.idx64 ? scan_impl<4, uint64_t>(a, s, ev) : scan_impl<4, uint32_t>(a, s, ev);
+    return a.width == 2 ? scan_impl<2>(a, s, ev) : scan_impl<4>(a, s, ev);
 }
 
 cudaError_t launch_extract_emit(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev) {
-    if (a.width == 2) return a.idx64 ? emit_impl<2, uint64_t>(a, out, s, ev) : emit_impl<2, uint32_t>(a, out, s, ev);
-    return a.idx64 ? emit_impl<4, uint64_t>(a, out, s, ev) : emit_impl<4, uint32_t>(a, out, s, ev);
+    return a.width == 2 ? emit_impl<2>(a, out, s, ev) : emit_impl<4>(a, out, s, ev);
 }
 
 }  // namespace sd

@@ -10,15 +10,10 @@ namespace sd {
 constexpr int kScanThreads = 256;  // K1 block
 constexpr int kScanVecs = 8;       // 16-byte vectors per thread per operand per tile
 constexpr int kTileBytes = kScanThreads * kScanVecs * 16;  // 32 KiB of old + 32 KiB of new
-constexpr int kEntryChunk = 4096;  // entries per K2/K4 chunk (256 threads x 16)
-constexpr int kEntryPerThread = kEntryChunk / 256;
+// lanes per tile: 16384 (16-bit lanes) or 8192 (32-bit lanes) -> a lane offset fits a u16
+constexpr int kTileBlock = 4096;   // tiles per block of the tile-level scans (1024 thr x 4)
 constexpr int kByteChunk = 4096;   // index-stream bytes per A2/A4 chunk (256 threads x 16)
 constexpr int kHalo = 16;          // bytes before a chunk kept for varints that straddle it
-
-// Tile-state words for the decoupled look-back (K1): top two bits are the flag.
-constexpr unsigned long long kFlagAgg = 1ull << 62;
-constexpr unsigned long long kFlagIncl = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 constexpr uint32_t kTileFirstOfTensor = 1u << 31;
 constexpr uint32_t kTileAligned = 1u << 30;
@@ -34,10 +29,22 @@ struct TileDesc {
 };
 static_assert(sizeof(TileDesc) == 32, "TileDesc is 32 bytes");
 
+// K1 output per tile: changed-lane count, lane offsets (within the tile) of the first and
+// last changed lane, and the LEB128 bytes of the gaps between consecutive changes inside
+// the tile (the first change's gap depends on earlier tiles and is added by K2b).
+struct TileMeta {
+    uint32_t count;
+    uint16_t first_off, last_off;
+    uint32_t internal_bytes;
+    uint32_t pad;
+};
+static_assert(sizeof(TileMeta) == 16, "TileMeta is 16 bytes");
+
 // Device-written summary of one extract, read back by the host after the single sync.
 struct ExtractSummary {
     unsigned long long M;           // total changed lanes (entries) over all tensors
-    unsigned long long overflow;    // != 0: the entry workspace was too small
+    unsigned long long overflow;    // != 0: some tile had more entries than its slot holds
+    unsigned long long max_count;   // largest per-tile count seen (sizes the slots on retry)
     unsigned long long idx_bytes;   // total LEB128 bytes over all tensors
     unsigned long long body_bytes;  // packed body size
 };
@@ -79,16 +86,18 @@ struct ExtractArgs {
     const TileDesc *tiles;
     uint32_t ntiles;
     uint32_t ntensors;
-    unsigned long long *tile_state;   // ntiles, zeroed
-    unsigned int *ticket;             // zeroed
-    void *ws_idx;                     // u32 or u64 entries
-    void *ws_val;                     // lanes
-    unsigned long long ws_cap;        // entries
+    uint32_t slot_cap;                // C: entries per tile slot
+    uint16_t *slot_off;               // ntiles x C lane offsets
+    void *slot_val;                   // ntiles x C lanes
+    TileMeta *meta;                   // ntiles
+    unsigned long long *tile_entry;   // ntiles: entries before the tile (all tensors)
+    unsigned long long *tile_byte;    // ntiles: LEB128 bytes before the tile (all tensors)
+    unsigned long long *tile_pred;    // ntiles: absolute index of the previous change in the tensor, or 0
+    unsigned int *tile_bytes_tmp;     // ntiles: the tile's own LEB128 bytes
+    unsigned long long *blk_a;        // per tile block: entry count, then LEB128 bytes
+    long long *blk_key;               // per tile block: last non-empty tile
+    const uint32_t *tensor_first_tile;  // ntensors
     unsigned long long *entry_begin;  // ntensors + 1 (E_k)
-    unsigned long long *tstart_partial;  // ntensors + 1
-    unsigned int *chunk_bytes;        // per entry chunk
-    unsigned long long *chunk_prefix; // per entry chunk
-    unsigned long long chunk_cap;     // capacity of the chunk arrays
     unsigned long long *tensor_byte_begin;  // ntensors + 1 (B_k)
     RecordRow *table;                 // ntensors
     const uint32_t *name_len;         // ntensors
@@ -97,12 +106,11 @@ struct ExtractArgs {
     const unsigned long long *numel;  // ntensors (N_k)
     ExtractSummary *summary;
     int width;                        // 2 or 4
-    bool idx64;
     int persist_ctas;                 // grid for grid-stride kernels
 };
 
-// ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1, K2,
-// K3; emit: 3 = before K4, after K4, after K5).
+// ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1,
+// after the tile scans K2, after K3; emit: 3 = before K4, after K4, after K5).
 cudaError_t launch_extract_scan(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev);    // K1-K3
 cudaError_t launch_extract_emit(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev);  // K4-K5
 
