@@ -43,7 +43,7 @@ PAPER_CPU = "paper: ~5 s CPU extraction for Qwen3-8B (PAPER.md:405), 79x payload
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="M3", choices=sorted(CONFIGS))
     p.add_argument("--rho", type=float, default=None)
@@ -75,7 +75,7 @@ def workload(args):
 
 # ------------------------------------------------------------------ clocks sampler
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -97,11 +97,16 @@ class Clocks:
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.time(), ln.strip()))
 
-    def stop(self):
+    def mark(self):
+        """Call right before and right after the timed region."""
+        return time.time()
+
+    def stop(self, t0=None, t1=None):
         if not self.proc:
             return None
+        time.sleep(0.3)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -110,8 +115,12 @@ class Clocks:
         self.t.join(timeout=2)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
+        window = [(ts, ln) for ts, ln in self.lines
+                  if t0 is None or (t0 - 0.15 <= ts <= t1 + 0.25)]
+        if not window:  # timed region shorter than the sampling period: nearest samples
+            window = sorted(self.lines, key=lambda x: abs(x[0] - (t0 or 0)))[:3]
+        for _, ln in window:
+            f = [x.strip() for x in ln.split(",")][1:]
             if len(f) < 8:
                 continue
             try:
@@ -306,19 +315,22 @@ def main():
 
     clocks = Clocks(local, enabled=not args.no_clocks)
     acc = {}
+    clocks.start()
+    time.sleep(1.0)  # sampler up and running before the timed region
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
     ev0.record(stream)
     for _ in range(args.steps):
         size, table = step(acc)
     ev1.record(stream)
     torch.cuda.synchronize()
+    w1 = time.time()
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(w0, w1)
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -338,8 +350,7 @@ def main():
     else:
         body_total, nnz_total, idx_total = body_local, nnz_local, idx_local
     k1_ms = acc.get("scan_ms", 0.0) / args.steps
-    idx_size = 4 if max(specs[k].numel for k in mine) < 2**32 else 8
-    k1_bytes = 2 * local_lanes * width + nnz_local * (idx_size + width)
+    k1_bytes = 2 * local_lanes * width + nnz_local * (2 + width)  # reads + slot writes
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -364,7 +375,7 @@ def main():
                     "index_bytes_per_entry": round(idx_total / max(nnz_total, 1), 4),
                     "paper_context": PAPER_CPU},
         "kernel_ms_per_step": kernel_ms,
-        "roofline": {"kernel": "k_scan_compact (K1)", "bound": "hbm",
+        "roofline": {"kernel": "k_scan_tiles (K1)", "bound": "hbm",
                      "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,

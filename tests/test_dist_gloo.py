@@ -1,0 +1,114 @@
+"""Multi-GPU orchestration logic on CPU (no GPU): shard_plan properties, and the size
+all-gather + body assembly over a world_size-2 gloo group, with each rank's body produced
+by the oracle for its shard (the extract itself is mocked; the GPU path is covered by
+tests/test_gpu_parity.py).  The assembled body must be byte-identical to the body of the
+whole tensor list (G-way assembly == G = 1)."""
+
+import itertools
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2602_11456_b200.dist import assemble, gather_sizes, shard_plan, shift_table
+
+
+def _best_max(numels, world):
+    """Brute force: smallest possible largest contiguous shard."""
+    n = len(numels)
+    best = None
+    for cuts in itertools.combinations(range(1, n), min(world - 1, n - 1)):
+        b = [0, *cuts, n]
+        m = max(sum(numels[b[i]:b[i + 1]]) for i in range(len(b) - 1))
+        best = m if best is None or m < best else best
+    return best if best is not None else sum(numels)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_plan_properties(world):
+    rng = np.random.default_rng(world)
+    for _ in range(30):
+        n = int(rng.integers(1, 10))
+        numels = [int(x) for x in rng.integers(0, 1000, n)]
+        r = shard_plan(numels, world)
+        assert len(r) == world
+        assert r[0][0] == 0 and r[-1][1] == n
+        for (a, b), (c, _) in zip(r, r[1:]):
+            assert a <= b == c
+        assert shard_plan(numels, world) == r  # deterministic
+        got = max(sum(numels[a:b]) for a, b in r)
+        assert got == _best_max(numels, world)
+
+
+def test_shard_plan_qwen3_balance():
+    from workload import qwen3
+    numels = [s.numel for s in qwen3("8B")]
+    for world, bound in ((2, 1.001), (4, 1.02), (8, 1.045)):
+        r = shard_plan(numels, world)
+        ideal = sum(numels) / world
+        assert max(sum(numels[a:b]) for a, b in r) / ideal <= bound
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _tensors():
+    import oracle  # noqa: F401
+    rng = np.random.default_rng(0)
+    out = []
+    for k in range(7):
+        n = int(rng.integers(0, 3000))
+        o = rng.integers(0, 2**16, n, dtype=np.uint64).astype(np.uint16)
+        w = o.copy()
+        m = rng.random(n) < 0.05
+        w[m] ^= 1
+        out.append((f"t{k}", o, w))
+    return out
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        ts = _tensors()
+        ranges = shard_plan([o.size for _, o, _ in ts], world)
+        a, b = ranges[rank]
+        body, table = oracle.codec.extract([(n, [o], [w]) for n, o, w in ts[a:b]])
+        local = torch.frombuffer(bytearray(body), dtype=torch.uint8) if body else torch.empty(0, dtype=torch.uint8)
+        sizes, off, tot = gather_sizes(len(body), "cpu")
+        root_out = torch.empty(tot, dtype=torch.uint8) if rank == 0 else None
+        got = assemble(local, sizes, root_out)
+        shifted = shift_table(table, off)
+        all_rows = [None] * world
+        dist.all_gather_object(all_rows, shifted)
+        if rank == 0:
+            full_body, full_table = oracle.codec.extract([(n, [o], [w]) for n, o, w in ts])
+            q.put((got.numpy().tobytes() == full_body,
+                   [r for rows in all_rows for r in rows] == [tuple(r) for r in full_table]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_assembly_gloo_world2(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    body_ok, table_ok = q.get(timeout=10)
+    assert body_ok and table_ok
