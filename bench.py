@@ -383,7 +383,7 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": k1_bytes},
-        "gpu_launches": 9 * args.steps,
+        "gpu_launches": 13 * args.steps,  # per rank: 7 (size) + 2 (extract) + 4 (apply) per step
         "clocks": clk,
     }
     if k1_ms > 0:

@@ -179,6 +179,20 @@ int delta_apply(delta_ctx *ctx, const delta_target *targets, uint32_t n, int ele
                 const void *body_dev, uint64_t body_bytes,
                 const delta_record_info *table_hint, void *stream);
 
+/* delta_apply_async — delta_apply without the final synchronisation: validates and
+ * scatters on `stream` (same all-or-nothing gate per call) and returns once the work is
+ * enqueued.  Errors found on the device are kept in a sticky status word read by
+ * delta_apply_wait.  Host-side argument errors are returned immediately.  Several calls
+ * may be enqueued on one stream (each call's targets/body must stay valid until the
+ * matching wait); do not mix streams on one ctx. */
+int delta_apply_async(delta_ctx *ctx, const delta_target *targets, uint32_t n, int elem,
+                      const void *body_dev, uint64_t body_bytes,
+                      const delta_record_info *table_hint, void *stream);
+
+/* delta_apply_wait — synchronise `stream` and return the first device-side error of the
+ * delta_apply_async calls since the previous wait (DELTA_OK if none), then clear it. */
+int delta_apply_wait(delta_ctx *ctx, void *stream);
+
 /* Per-kernel device times of the last delta_size/delta_extract/delta_apply on this ctx,
  * in milliseconds, measured with CUDA events recorded on the call's stream around each
  * kernel (only while profiling is enabled; zero otherwise).  A field is the time of the

@@ -189,17 +189,23 @@ class DeltaContext:
             return body, None
         return body, [tuple(getattr(rows[k], f) for f in TABLE_FIELDS) for k in range(tl.n)]
 
-    def delta_apply(self, targets, body, table=None, stream=None):
+    def delta_apply(self, targets, body, table=None, stream=None, wait=True):
         """Validate ``body`` fully, then scatter its values into ``targets`` in place
-        (all-or-nothing).  ``table``: optional offset-table rows from delta_extract."""
+        (all-or-nothing).  ``table``: optional offset-table rows from delta_extract.
+        ``wait=False`` enqueues only (delta_apply_async); call ``apply_wait`` later."""
         tg = targets if isinstance(targets, TargetList) else TargetList(targets)
         if body.dtype != torch.uint8 or not body.is_contiguous() or not body.is_cuda:
             raise ValueError("body must be a contiguous uint8 CUDA tensor")
         hint = None
         if table is not None:
             hint = table if isinstance(table, ctypes.Array) else _rows_to_ctypes(table)
-        self._check(self._lib.delta_apply(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(),
-                                          body.numel(), hint, _stream_handle(stream)))
+        fn = self._lib.delta_apply if wait else self._lib.delta_apply_async
+        self._check(fn(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(), body.numel(), hint,
+                       _stream_handle(stream)))
+
+    def apply_wait(self, stream=None):
+        """Synchronise and raise the first error of the async applies since the last wait."""
+        self._check(self._lib.delta_apply_wait(self._h, _stream_handle(stream)))
 
 
 def _rows_to_ctypes(rows):

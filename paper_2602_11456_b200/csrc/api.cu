@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -22,7 +23,10 @@ struct DevBuf {
     size_t cap = 0;
     int grow(size_t bytes) {  // grow-only; contents are not preserved
         if (bytes <= cap) return DELTA_OK;
-        if (p) cudaFree(p);
+        if (p) {
+            cudaDeviceSynchronize();  // async work (delta_apply_async) may still read it
+            cudaFree(p);
+        }
         p = nullptr;
         cap = 0;
         size_t want = std::max<size_t>(bytes, 256);
@@ -66,7 +70,7 @@ struct delta_ctx {
     unsigned long long total_lanes = 0;
     DevBuf tiles, name_len, name_off, names, numel, tensor_first_tile;
     // ---- extract workspace
-    DevBuf slot_off, slot_val, meta, tile_entry, tile_byte, tile_pred, tile_bytes, blk_a, blk_key,
+    DevBuf slot_bytes, slot_val, meta, tile_entry, tile_byte, tile_pred, tile_bytes, blk_a, blk_key,
         entry_begin, tensor_byte_begin, table, summary;
     uint32_t slot_cap = 0;          // entries per tile slot (grows on overflow)
     bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
@@ -153,7 +157,7 @@ void delta_ctx_destroy(delta_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
-                      &c->tensor_first_tile, &c->slot_off, &c->slot_val, &c->meta,
+                      &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->blk_a,
                       &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
                       &c->summary, &c->a_targets,
@@ -319,7 +323,7 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.ntiles = ctx->ntiles;
     a.ntensors = ctx->ntensors;
     a.slot_cap = ctx->slot_cap;
-    a.slot_off = ctx->slot_off.as<uint16_t>();
+    a.slot_bytes = ctx->slot_bytes.as<uint8_t>();
     a.slot_val = ctx->slot_val.p;
     a.meta = ctx->meta.as<TileMeta>();
     a.tile_entry = ctx->tile_entry.as<unsigned long long>();
@@ -343,7 +347,7 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
 }
 
 static int reserve_slots(delta_ctx *ctx, uint32_t cap) {
-    GROW(ctx->slot_off, (size_t)ctx->ntiles * cap * sizeof(uint16_t) + 64);
+    GROW(ctx->slot_bytes, (size_t)ctx->ntiles * cap * 2 + 64);
     GROW(ctx->slot_val, (size_t)ctx->ntiles * cap * ctx->width + 64);
     ctx->slot_cap = cap;
     return DELTA_OK;
@@ -369,7 +373,7 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
     // slots: start at 1/16 of a tile (6.25% density); grown to the exact need on overflow
     uint32_t cap = std::max<uint32_t>(ctx->slot_cap, lanes_per_tile / 16);
     if (cap > lanes_per_tile) cap = lanes_per_tile;
-    if (cap != ctx->slot_cap || ctx->slot_off.cap < (size_t)nt * cap * 2) {
+    if (cap != ctx->slot_cap || ctx->slot_bytes.cap < (size_t)nt * cap * 2 + 64) {
         int rc = reserve_slots(ctx, cap);
         if (rc) return rc;
     }
@@ -388,7 +392,7 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
             ctx->scan_cached = true;
             return DELTA_OK;
         }
-        uint32_t need = 1;
+        uint32_t need = 2;
         while (need < ctx->h_summary->max_count) need <<= 1;
         int rc = reserve_slots(ctx, std::min(need, lanes_per_tile));
         if (rc) return rc;
@@ -468,10 +472,8 @@ static const char *kDetailName[] = {"ok", "truncated varint", "overlong varint",
                                     "record name != target name", "record element_count != target numel",
                                     "mode byte != 0", "record layout"};
 
-extern "C" int delta_apply(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem,
-                           const void *body, uint64_t body_bytes, const delta_record_info *hint,
-                           void *stream) {
-    if (!ctx) return DELTA_EINVAL;
+static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem, const void *body,
+                         uint64_t body_bytes, const delta_record_info *hint, cudaStream_t s) {
     ctx->err.clear();
     ctx->detail = 0;
     const int w = elem_width(elem);
@@ -493,24 +495,27 @@ extern "C" int delta_apply(delta_ctx *ctx, const delta_target *tg, uint32_t n, i
         blob.append(tg[k].name ? tg[k].name : "", tg[k].name_len);
     }
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t nn = std::max<uint32_t>(n, 1);
     GROW(ctx->a_targets, nn * sizeof(TargetDesc));
     GROW(ctx->a_names, std::max<size_t>(blob.size(), 1));
     GROW(ctx->a_recs, nn * sizeof(ApplyRec));
     GROW(ctx->a_rcb, (nn + 1) * 8);
-    GROW(ctx->a_state, sizeof(ApplyState));
+    if (!ctx->a_state.p) {
+        GROW(ctx->a_state, sizeof(ApplyState));
+        CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(ApplyState), s), "memset");
+    }
     const size_t nch = body_bytes / kByteChunk + n + 2;
     GROW(ctx->a_cnt, nch * 4);
     GROW(ctx->a_sum, nch * 8);
     GROW(ctx->a_ord, nch * 8);
     GROW(ctx->a_idx, nch * 8);
     if (hint && n) GROW(ctx->a_hint, n * sizeof(RecordRow));
-    // pageable sources: these copies complete before the call returns (sync below)
+    // pageable sources: cudaMemcpyAsync stages them before returning, so the host vectors
+    // may die; the device copies are stream-ordered after any earlier call's kernels.
     if (n) CK(cudaMemcpyAsync(ctx->a_targets.p, td.data(), n * sizeof(TargetDesc), cudaMemcpyHostToDevice, s), "upload");
     if (!blob.empty()) CK(cudaMemcpyAsync(ctx->a_names.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s), "upload");
     if (hint && n) CK(cudaMemcpyAsync(ctx->a_hint.p, hint, n * sizeof(RecordRow), cudaMemcpyHostToDevice, s), "upload");
-    CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(ApplyState), s), "memset");
+    CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(uint32_t), s), "memset");  // this call's gate
     ApplyArgs a;
     a.body = static_cast<const uint8_t *>(body);
     a.body_bytes = body_bytes;
@@ -529,16 +534,42 @@ extern "C" int delta_apply(delta_ctx *ctx, const delta_target *tg, uint32_t n, i
     a.width = w;
     a.persist_ctas = ctx->sm_count * 8;
     CK(launch_apply(a, s, ctx->profiling ? ctx->ev_apply : nullptr), "apply launch");
+    return DELTA_OK;
+}
+
+extern "C" int delta_apply_async(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem,
+                                 const void *body, uint64_t body_bytes, const delta_record_info *hint,
+                                 void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    return apply_enqueue(ctx, tg, n, elem, body, body_bytes, hint, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int delta_apply_wait(delta_ctx *ctx, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    if (!ctx->a_state.p) return DELTA_OK;  // nothing was ever enqueued
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     CK(cudaMemcpyAsync(ctx->h_state, ctx->a_state.p, sizeof(ApplyState), cudaMemcpyDeviceToHost, s), "status readback");
     CK(cudaStreamSynchronize(s), "apply");
+    CK(cudaMemsetAsync(static_cast<uint8_t *>(ctx->a_state.p) + offsetof(ApplyState, first_error), 0,
+                       sizeof(uint32_t), s), "memset");
     if (ctx->profiling) {
         ctx->timing.locate_ms = ev_ms(ctx->ev_apply[0], ctx->ev_apply[1]);
         ctx->timing.decode_ms = ev_ms(ctx->ev_apply[1], ctx->ev_apply[2]);
         ctx->timing.apply_scan_ms = ev_ms(ctx->ev_apply[2], ctx->ev_apply[3]);
         ctx->timing.scatter_ms = ev_ms(ctx->ev_apply[3], ctx->ev_apply[4]);
     }
-    const uint32_t st = ctx->h_state->status;
+    const uint32_t st = ctx->h_state->first_error;
     if (st == 0) return DELTA_OK;
     if (st > 10) return fail(ctx, DELTA_ECORRUPT, (int)st, "unknown status %u", st);
     return fail(ctx, kDetailToStatus[st], (int)st, "delta_apply: %s", kDetailName[st]);
+}
+
+extern "C" int delta_apply(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem,
+                           const void *body, uint64_t body_bytes, const delta_record_info *hint,
+                           void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    int rc = apply_enqueue(ctx, tg, n, elem, body, body_bytes, hint, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    return delta_apply_wait(ctx, stream);
 }

@@ -323,9 +323,13 @@ __global__ void __launch_bounds__(256)
 k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
           const unsigned long long *__restrict__ rcb, const unsigned int *__restrict__ chunk_count,
           const unsigned long long *__restrict__ ord_base, const unsigned long long *__restrict__ idx_base,
-          const ApplyState *st) {
+          ApplyState *st) {
     using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
-    if (st->status != kOk) return;  // the gate: nothing is written unless all checks passed
+    const uint32_t gate = st->status;
+    if (gate != kOk) {  // the gate: nothing is written unless all checks passed
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&st->first_error, 0u, gate);
+        return;
+    }
     const unsigned long long nch = st->n_chunks;
     __shared__ uint8_t sb[kHalo + kByteChunk];
     __shared__ LT sv[kByteChunk];  // at most one varint per byte

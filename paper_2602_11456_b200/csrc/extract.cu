@@ -4,17 +4,18 @@
 //                       CTA per tile (16 Ki 16-bit lanes = 32 KiB of old + 32 KiB of new),
 //                       16-byte streaming loads, bitwise lane compare, per-vector change
 //                       masks, one packed block scan for the ranks, ordered compaction into
-//                       shared memory, coalesced copy into the tile's workspace slot (u16
-//                       lane offset + raw lane), per-tile count / first / last / internal
-//                       LEB128 bytes.  No inter-CTA communication: a pure streaming pass.
+//                       shared memory, then the tile's workspace slot: raw values and the
+//                       LEB128 bytes of the gaps inside the tile (< 2^14 lanes: 1-2 bytes),
+//                       plus per-tile count / first / last / internal byte count.  No
+//                       inter-CTA communication: a pure streaming pass.
 //   K2  k_tiles_reduce / k_blocks_scan / k_tiles_bytes / k_tiles_place
 //                       E3+E4+E5 sizes: scans over the (small) per-tile metadata — entry
 //                       prefix, nearest earlier non-empty tile (its last change is the
 //                       predecessor of the tile's first change), each tile's
 //                       LEB128 bytes, byte prefix, per-tensor entry/byte begins.
 //   K3  k_finalize      E6: record sizes and offsets (the offset table), body size.
-//   K4  k_emit_tiles    E5+E6: one warp per tile writes LEB128 bytes and raw values to their
-//                       final body offsets.
+//   K4  k_emit_tiles    E5+E6: one warp per tile writes the first gap's LEB128 bytes and
+//                       copies the pre-encoded gaps and the raw values to their final offsets.
 //   K5  k_headers       E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
 //
 // Product code written for this library; none of it is shared with the test oracle.
@@ -119,7 +120,7 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 // ------------------------------------------------------------------------------ K1
 template <int W>
 __global__ void __launch_bounds__(kScanThreads)
-k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint16_t *__restrict__ slot_off,
+k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
     using LT = typename LaneOf<W>::T;
@@ -227,25 +228,29 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint16_t *__
         }
         return;
     }
-    // Coalesced copy of the slot + LEB128 bytes of the gaps inside the tile.
-    uint16_t *so = slot_off + (size_t)t * slot_cap;
+    // Slot: raw values (coalesced copy) and the LEB128 bytes of the gaps between
+    // consecutive changes inside the tile (each < 2^14 lanes, so 1 or 2 bytes), encoded
+    // here in order; the first change's gap depends on earlier tiles and is written by K4.
+    uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
     LT *sv = slot_val + (size_t)t * slot_cap;
+    for (uint32_t i = tid; i < c; i += kScanThreads) sv[i] = s_val[i];
+    const uint32_t q = (c + kScanThreads - 1) / kScanThreads;  // contiguous entries per thread
+    const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
     uint32_t L = 0;
-    for (uint32_t i = tid; i < c; i += kScanThreads) {
-        const uint16_t o = s_off[i];
-        so[i] = o;
-        sv[i] = s_val[i];
-        if (i > 0) L += leb_len((unsigned long long)(o - s_off[i - 1]));
+    for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) L += 1u + ((s_off[i] - s_off[i - 1]) >= 128u);
+    uint32_t tl;
+    uint32_t pos = block_excl_scan<kScanThreads / 32, uint32_t>(L, s_red, tl);
+    for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) {
+        const uint32_t g = s_off[i] - s_off[i - 1];
+        if (g < 128u) {
+            sb[pos++] = (uint8_t)g;
+        } else {
+            sb[pos++] = (uint8_t)(g | 0x80u);
+            sb[pos++] = (uint8_t)(g >> 7);
+        }
     }
-    L = warp_sum(L);
-    if (lane == 0) s_red[warp] = L;
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t tl = 0;
-#pragma unroll
-        for (int w = 0; w < kScanThreads / 32; ++w) tl += s_red[w];
+    if (tid == 0)
         meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
-    }
 }
 
 // ------------------------------------------------------------------------------ K2
@@ -467,55 +472,55 @@ k_finalize(const unsigned long long *__restrict__ E, const unsigned long long *_
 }
 
 // ------------------------------------------------------------------------------ K4
-// One warp per tile: LEB128 bytes of the tile's gaps and its raw values, written to their
-// final offsets in the body.
+// Warp-wide copy of n bytes from a 4-byte aligned source to any destination: byte head up
+// to the destination's 4-byte boundary, funnel-shifted 4-byte words, byte tail.  Reads at
+// most 3 bytes past the source range (slots are padded).
+__device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
+    const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
+    if ((uint32_t)lane < head) dst[lane] = src[lane];
+    const uint32_t rest = n - head, nw = rest >> 2;
+    uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + head);
+    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+    const uint32_t sh = 8u * head;  // source byte offset of word j is head + 4j
+    for (uint32_t j = lane; j < nw; j += 32) {
+        const uint32_t w0 = __ldg(s32 + j), w1 = __ldg(s32 + j + 1);
+        d32[j] = sh ? __funnelshift_r(w0, w1, sh) : w0;
+    }
+    for (uint32_t b = (nw << 2) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
+}
+
+// One warp per tile: the LEB128 bytes of the tile's first gap, then the tile's pre-encoded
+// internal gaps and its raw values copied to their final offsets in the body.
 template <int W>
 __global__ void __launch_bounds__(256)
 k_emit_tiles(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
-             uint32_t slot_cap, const uint16_t *__restrict__ slot_off,
+             uint32_t slot_cap, const uint8_t *__restrict__ slot_bytes,
              const typename LaneOf<W>::T *__restrict__ slot_val,
              const unsigned long long *__restrict__ tile_entry, const unsigned long long *__restrict__ tile_byte,
              const unsigned long long *__restrict__ tile_pred, const unsigned long long *__restrict__ E,
              const unsigned long long *__restrict__ Bk, const RecordRow *__restrict__ table,
              uint8_t *__restrict__ out) {
-    using LT = typename LaneOf<W>::T;
     const int lane = threadIdx.x & 31;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
     for (uint32_t t = wg; t < ntiles; t += nw) {
-        const uint32_t c = meta[t].count;
-        if (c == 0) continue;
+        const TileMeta m = meta[t];
+        if (m.count == 0) continue;
         const TileDesc d = tiles[t];
         const uint32_t k = d.flags_tensor & kTileTensorMask;
         uint8_t *ib = out + table[k].index_offset + (tile_byte[t] - Bk[k]);
         uint8_t *vb = out + table[k].values_offset + (tile_entry[t] - E[k]) * W;
-        const uint16_t *so = slot_off + (size_t)t * slot_cap;
-        const LT *sv = slot_val + (size_t)t * slot_cap;
-        unsigned long long prev = tile_pred[t];
-        unsigned long long pos = 0;
-        for (uint32_t base = 0; base < c; base += 32) {
-            const uint32_t i = base + lane;
-            const bool valid = i < c;
-            const unsigned long long abs = valid ? d.lane_base + so[i] : 0;
-            unsigned long long pa = __shfl_up_sync(0xffffffffu, abs, 1);
-            if (lane == 0) pa = prev;
-            unsigned long long g = abs - pa;
-            const uint32_t L = valid ? leb_len(g) : 0;
-            const uint32_t incl = warp_inclusive_sum(L);
-            if (valid) {
-                uint8_t *dst = ib + pos + (incl - L);
-                uint32_t n = 0;
-                while (g >= 0x80) {
-                    dst[n++] = (uint8_t)(g | 0x80);
-                    g >>= 7;
-                }
-                dst[n] = (uint8_t)g;
+        unsigned long long g = d.lane_base + m.first_off - tile_pred[t];
+        const uint32_t L0 = leb_len(g);
+        if (lane == 0) {
+            for (uint32_t n = 0; n + 1 < L0; ++n) {
+                ib[n] = (uint8_t)(g | 0x80);
+                g >>= 7;
             }
-            pos += __shfl_sync(0xffffffffu, incl, 31);
-            prev = __shfl_sync(0xffffffffu, abs, 31);
+            ib[L0 - 1] = (uint8_t)g;
         }
-        const uint32_t nb = c * W;
-        for (uint32_t b = lane; b < nb; b += 32) vb[b] = (uint8_t)(sv[b / W] >> (8 * (b % W)));
+        warp_copy(ib + L0, slot_bytes + (size_t)t * 2 * slot_cap, m.internal_bytes, lane);
+        warp_copy(vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), m.count * W, lane);
     }
 }
 
@@ -553,7 +558,7 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     const size_t smem = (size_t)LANES * (sizeof(uint16_t) + W);
     cudaFuncSetAttribute(k_scan_tiles<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
-    k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_off,
+    k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
                                                          static_cast<LT *>(a.slot_val), a.meta, a.summary);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
@@ -577,7 +582,7 @@ template <int W>
 static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
-    k_emit_tiles<W><<<a.persist_ctas, 256, 0, s>>>(a.tiles, a.meta, a.ntiles, a.slot_cap, a.slot_off,
+    k_emit_tiles<W><<<a.persist_ctas, 256, 0, s>>>(a.tiles, a.meta, a.ntiles, a.slot_cap, a.slot_bytes,
                                                    static_cast<const LT *>(a.slot_val), a.tile_entry,
                                                    a.tile_byte, a.tile_pred, a.entry_begin,
                                                    a.tensor_byte_begin, a.table, out);

@@ -76,8 +76,8 @@ enum : uint32_t {
 };
 
 struct ApplyState {
-    uint32_t status;     // first error code (0 = ok)
-    uint32_t pad;
+    uint32_t status;       // first error code of the current call (0 = ok): the gate
+    uint32_t first_error;  // first error since the last delta_apply_wait (sticky)
     unsigned long long n_chunks;
 };
 
@@ -86,8 +86,8 @@ struct ExtractArgs {
     const TileDesc *tiles;
     uint32_t ntiles;
     uint32_t ntensors;
-    uint32_t slot_cap;                // C: entries per tile slot
-    uint16_t *slot_off;               // ntiles x C lane offsets
+    uint32_t slot_cap;                // C: entries per tile slot (even)
+    uint8_t *slot_bytes;              // ntiles x 2C LEB128 bytes of the gaps inside the tile
     void *slot_val;                   // ntiles x C lanes
     TileMeta *meta;                   // ntiles
     unsigned long long *tile_entry;   // ntiles: entries before the tile (all tensors)
