@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     p.add_argument("--no-clocks", action="store_true")
+    p.add_argument("--pipeline", type=int, default=1,
+                   help="G > 1: extract and apply in G pipelined groups on two streams")
+    p.add_argument("--apply-ctas", type=int, default=0, help="apply kernels' CTAs per SM (0 = default)")
     p.add_argument("--tensors", type=int, default=0,
                    help="profiling only: keep the first N tensors of the config")
     return p.parse_args()
@@ -270,42 +273,63 @@ def main():
         news.append(w)
         targets.append(o.clone())
     torch.cuda.synchronize()
-    tl = sd.TensorList([(specs[k].name, o, w) for k, o, w in zip(mine, olds, news)])
-    tg = sd.TargetList([(specs[k].name, t) for k, t in zip(mine, targets)])
-    ctx = sd.DeltaContext(dev)
-    ctx.set_profiling(True)
     local_lanes = sum(specs[k].numel for k in mine)
     total_lanes = sum(s.numel for s in specs)
     scanned_total = 2 * total_lanes * width            # old + new bytes, all ranks
-    size0 = ctx.delta_size(tl)
-    out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
+    tensors = [(specs[k].name, o, w) for k, o, w in zip(mine, olds, news)]
+    tgts = [(specs[k].name, t) for k, t in zip(mine, targets)]
     root_out = None
     stream = torch.cuda.current_stream()
 
-    def step(acc=None):
-        size = ctx.delta_size(tl)
-        t1 = ctx.last_timing()
-        body, table = ctx.delta_extract(tl, out=out, table=True)
-        t2 = ctx.last_timing()
+    def assemble(size, body):
         nonlocal root_out
-        if world > 1:
-            sizes, off, tot = sdist.gather_sizes(size, dev)
-            if rank == 0 and (root_out is None or root_out.numel() < tot):
-                root_out = torch.empty(tot + tot // 8, dtype=torch.uint8, device=dev)
-            sdist.assemble(body, sizes, root_out)
-        ctx.delta_apply(tg, body, table=table)
-        t3 = ctx.last_timing()
-        if acc is not None:
-            for kname in ("scan_ms", "lens_ms", "finalize_ms"):
-                acc[kname] = acc.get(kname, 0.0) + t1[kname]
-            for kname in ("emit_ms", "headers_ms"):
-                acc[kname] = acc.get(kname, 0.0) + t2[kname]
-            for kname in ("locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
-                acc[kname] = acc.get(kname, 0.0) + t3[kname]
-        return size, table
+        sizes, off, tot = sdist.gather_sizes(size, dev)
+        if rank == 0 and (root_out is None or root_out.numel() < tot):
+            root_out = torch.empty(tot + tot // 8, dtype=torch.uint8, device=dev)
+        sdist.assemble(body, sizes, root_out)
+
+    if args.pipeline > 1:
+        from paper_2602_11456_b200.pipeline import RoundTrip
+        rt = RoundTrip(tensors, tgts, groups=args.pipeline, device=dev,
+                       apply_ctas_per_sm=args.apply_ctas or None)
+        rt.set_profiling(True)
+        ctx = rt.cx
+
+        def step(acc=None):
+            body = rt.step(acc)
+            if world > 1:
+                assemble(body.numel(), body)
+            return body, rt.table()
+    else:
+        tl = sd.TensorList(tensors)
+        tg = sd.TargetList(tgts)
+        ctx = sd.DeltaContext(dev)
+        if args.apply_ctas:
+            ctx.set_option(1, args.apply_ctas)
+        ctx.set_profiling(True)
+        size0 = ctx.delta_size(tl)
+        out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
+
+        def step(acc=None):
+            size = ctx.delta_size(tl)
+            t1 = ctx.last_timing()
+            body, table = ctx.delta_extract(tl, out=out, table=True)
+            t2 = ctx.last_timing()
+            if world > 1:
+                assemble(size, body)
+            ctx.delta_apply(tg, body, table=table)
+            t3 = ctx.last_timing()
+            if acc is not None:
+                for kname in ("scan_ms", "lens_ms", "finalize_ms"):
+                    acc[kname] = acc.get(kname, 0.0) + t1[kname]
+                for kname in ("emit_ms", "headers_ms"):
+                    acc[kname] = acc.get(kname, 0.0) + t2[kname]
+                for kname in ("locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
+                    acc[kname] = acc.get(kname, 0.0) + t3[kname]
+            return body, table
 
     for _ in range(max(args.warmup, 0)):
-        size, table = step()
+        body, table = step()
     # correctness guard on the timed configuration: apply(extract(old,new)) == new
     ok = all(torch.equal(t.view(torch.int16 if width == 2 else torch.int32),
                          w.view(torch.int16 if width == 2 else torch.int32))
@@ -324,7 +348,7 @@ def main():
     w0 = time.time()
     ev0.record(stream)
     for _ in range(args.steps):
-        size, table = step(acc)
+        body, table = step(acc)
     ev1.record(stream)
     torch.cuda.synchronize()
     w1 = time.time()
@@ -340,7 +364,7 @@ def main():
     value = scanned_total * args.steps / (ms / 1e3) / 1e9
 
     # ---- payload (global) and kernel-level roofline of the dominant kernel (K1)
-    body_local = size
+    body_local = body.numel()
     nnz_local = sum(r[2] for r in table)
     idx_local = sum(r[4] for r in table)
     if world > 1:
@@ -391,8 +415,7 @@ def main():
 
     # ---- e2e: the same step with inputs copied from pinned host memory every step
     if not args.no_e2e:
-        result["e2e"] = e2e(args, ctx, tl, tg, olds, news, out, dev, scanned_total, world, rank,
-                            body_total)
+        result["e2e"] = e2e(args, step, olds, news, body_local, dev, scanned_total, world)
     # ---- CPU oracle beside it (rank 0, N=1 only)
     if not args.no_cpu_baseline and world == 1:
         smp = OracleSample(specs, rho, pattern, args.seed, dtype, args.cpu_seconds)
@@ -408,16 +431,16 @@ def main():
     return 0
 
 
-def e2e(args, ctx, tl, tg, olds, news, out, dev, scanned_total, world, rank, body_total):
+def e2e(args, step, olds, news, body_cap, dev, scanned_total, world):
     """Same metric through the public API with host buffers: every step copies old and new
-    from pinned host memory (H2D) and reads the packed body back (D2H), on the same
-    stream as the kernels; CUDA events around the whole step, max over ranks."""
+    from pinned host memory (H2D), runs the step and reads the packed body back (D2H), on
+    the same stream as the kernels; CUDA events around the whole step, max over ranks."""
     import torch
     import torch.distributed as dist
     stream = torch.cuda.current_stream()
     h_old = [o.cpu().pin_memory() for o in olds]
     h_new = [w.cpu().pin_memory() for w in news]
-    h_body = torch.empty(out.numel(), dtype=torch.uint8).pin_memory()
+    h_body = torch.empty(body_cap + body_cap // 8 + 4096, dtype=torch.uint8).pin_memory()
     h2d = sum(o.numel() * o.element_size() * 2 for o in olds)
     d2h = 0
 
@@ -426,11 +449,9 @@ def e2e(args, ctx, tl, tg, olds, news, out, dev, scanned_total, world, rank, bod
         for o, w, ho, hw in zip(olds, news, h_old, h_new):
             o.copy_(ho, non_blocking=True)
             w.copy_(hw, non_blocking=True)
-        size = ctx.delta_size(tl)
-        body, table = ctx.delta_extract(tl, out=out, table=True)
-        h_body[:size].copy_(body, non_blocking=True)
-        ctx.delta_apply(tg, body, table=table)
-        d2h = size
+        body, _ = step()
+        h_body[:body.numel()].copy_(body, non_blocking=True)
+        d2h = body.numel()
     one()
     torch.cuda.synchronize()
     if world > 1:
@@ -449,7 +470,7 @@ def e2e(args, ctx, tl, tg, olds, news, out, dev, scanned_total, world, rank, bod
     return {"value": round(scanned_total * args.e2e_steps / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
             "ms_per_step": round(ms / args.e2e_steps, 3),
-            "note": "per rank; old+new H2D from pinned host, body D2H, apply on device"}
+            "note": "bytes per rank; old+new H2D from pinned host, body D2H, apply on device"}
 
 
 if __name__ == "__main__":

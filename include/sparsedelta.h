@@ -209,6 +209,15 @@ typedef struct {
     float scatter_ms;   /* A4 gated scatter-store */
 } delta_timing;
 
+/* Launch-shape options (performance only; results never depend on them). */
+enum {
+    DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode/scatter kernels, CTAs per SM (default 8) */
+    DELTA_OPT_EMIT_CTAS_PER_SM = 2   /* grid of the extract emit kernel, CTAs per SM (default 8) */
+};
+
+/* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */
+int delta_set_option(delta_ctx *ctx, int option, int64_t value);
+
 /* Enable (1) or disable (0) per-kernel event timing on ctx.  Default: disabled. */
 int delta_set_profiling(delta_ctx *ctx, int enable);
 

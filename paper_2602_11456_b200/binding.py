@@ -151,6 +151,10 @@ class DeltaContext:
             msg = self._lib.delta_last_error(self._h).decode(errors="replace")
             raise DeltaError(rc, self._lib.delta_last_detail(self._h), msg)
 
+    def set_option(self, option: int, value: int):
+        """DELTA_OPT_* launch-shape option (performance only)."""
+        self._check(self._lib.delta_set_option(self._h, option, value))
+
     def set_profiling(self, enable: bool):
         """Per-kernel CUDA-event timing inside the library (see delta_last_timing)."""
         self._check(self._lib.delta_set_profiling(self._h, 1 if enable else 0))

@@ -80,6 +80,9 @@ struct delta_ctx {
     DevBuf a_targets, a_names, a_hint, a_recs, a_rcb, a_cnt, a_sum, a_ord, a_idx, a_state;
     ApplyState *h_state = nullptr;  // pinned
 
+    // ---- launch options
+    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8;
+
     // ---- optional per-kernel event timing
     bool profiling = false;
     cudaEvent_t ev_scan[4] = {}, ev_emit[3] = {}, ev_apply[5] = {};
@@ -177,6 +180,14 @@ void delta_ctx_destroy(delta_ctx *c) {
 const char *delta_last_error(const delta_ctx *c) { return c ? c->err.c_str() : "no context"; }
 
 int delta_last_detail(const delta_ctx *c) { return c ? c->detail : DELTA_D_NONE; }
+
+int delta_set_option(delta_ctx *c, int option, int64_t value) {
+    if (!c || value < 1 || value > 64) return DELTA_EINVAL;
+    if (option == DELTA_OPT_APPLY_CTAS_PER_SM) c->apply_ctas_per_sm = (int)value;
+    else if (option == DELTA_OPT_EMIT_CTAS_PER_SM) c->emit_ctas_per_sm = (int)value;
+    else return DELTA_EINVAL;
+    return DELTA_OK;
+}
 
 int delta_set_profiling(delta_ctx *c, int enable) {
     if (!c) return DELTA_EINVAL;
@@ -342,7 +353,7 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.numel = ctx->numel.as<unsigned long long>();
     a.summary = ctx->summary.as<ExtractSummary>();
     a.width = ctx->width;
-    a.persist_ctas = ctx->sm_count * 8;
+    a.persist_ctas = ctx->sm_count * ctx->emit_ctas_per_sm;
     return a;
 }
 
@@ -532,7 +543,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.chunk_cap = nch;
     a.state = ctx->a_state.as<ApplyState>();
     a.width = w;
-    a.persist_ctas = ctx->sm_count * 8;
+    a.persist_ctas = ctx->sm_count * ctx->apply_ctas_per_sm;
     CK(launch_apply(a, s, ctx->profiling ? ctx->ev_apply : nullptr), "apply launch");
     return DELTA_OK;
 }

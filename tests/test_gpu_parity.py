@@ -353,3 +353,53 @@ def test_u64_index_path(sd):
     ctx.delta_apply([("huge", w)], body, table=table)
     assert_lanes_equal(w, new)
     ctx.close()
+
+
+# ------------------------------------------------------------------ pipelined round trip
+def test_pipelined_roundtrip_matches_oracle(sd):
+    from paper_2602_11456_b200.pipeline import RoundTrip
+    rng = np.random.default_rng(11)
+    tensors = []
+    for k in range(23):
+        n = int(rng.integers(0, 200_000))
+        spec = TensorSpec(f"model.layers.{k}.w", (n,), "matrix")
+        o, w = generate_pair(spec, k, 5, rho=float(rng.choice([0.0, 0.01, 0.2])), device=DEV)
+        tensors.append((spec.name, o, w))
+    targets = [(n, o.clone()) for n, o, _ in tensors]
+    for groups, ctas in ((1, None), (4, 2), (7, None)):
+        for _, t in targets:
+            t.zero_()
+        rt = RoundTrip(tensors, targets, groups=groups, device=DEV, apply_ctas_per_sm=ctas)
+        for (n, t), (_, o, _) in zip(targets, tensors):
+            t.copy_(o)
+        body = rt.step()
+        torch.cuda.synchronize()
+        ref_body, ref_table = oracle_extract(tensors)
+        assert_body_equal(body, ref_body)
+        assert rt.table() == [tuple(r) for r in ref_table]
+        for (_, t), (_, _, w) in zip(targets, tensors):
+            assert_lanes_equal(t, w)
+        rt.close()
+
+
+def test_async_apply_error_is_reported_at_wait(sd):
+    ts = _small_valid()
+    body, table = oracle_extract(ts)
+    bad = bytearray(body)
+    bad[table[0][6] - 1] = 1  # mode byte of record a
+    targets = [(n, torch.from_numpy(to_np(o).view(np.int16).copy()).to(DEV).view(torch.bfloat16))
+               for n, o, _ in ts]
+    before = [t.clone() for _, t in targets]
+    ctx = sd.DeltaContext(DEV)
+    ctx.delta_apply(targets, torch.tensor(list(bad), dtype=torch.uint8, device=DEV), wait=False)
+    with pytest.raises(sd.DeltaError) as e:
+        ctx.apply_wait()
+    assert e.value.kind == "mode"
+    for (_, t), b in zip(targets, before):
+        assert_lanes_equal(t, b)
+    # the sticky error is cleared by the wait: a valid body now applies
+    ctx.delta_apply(targets, torch.tensor(list(body), dtype=torch.uint8, device=DEV), wait=False)
+    ctx.apply_wait()
+    for (_, t), (_, _, w) in zip(targets, ts):
+        assert_lanes_equal(t, w.to(DEV))
+    ctx.close()
