@@ -77,8 +77,16 @@ struct delta_ctx {
     ExtractSummary *h_summary = nullptr;  // pinned
 
     // ---- apply workspace
-    DevBuf a_targets, a_names, a_hint, a_recs, a_rcb, a_cnt, a_sum, a_ord, a_idx, a_state;
+    DevBuf a_upload, a_recs, a_rcb, a_cnt, a_sum, a_ord, a_idx, a_state;
     ApplyState *h_state = nullptr;  // pinned
+    // pinned staging ring for the per-call apply uploads (targets, hint, names): with a
+    // pinned source cudaMemcpyAsync does not wait for earlier work on the stream, so
+    // delta_apply_async never blocks the host on a previous scatter.
+    static constexpr int kRing = 8;
+    void *ring[kRing] = {};
+    size_t ring_cap[kRing] = {};
+    cudaEvent_t ring_ev[kRing] = {};
+    int ring_next = 0;
 
     // ---- launch options
     int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8;
@@ -163,8 +171,7 @@ void delta_ctx_destroy(delta_ctx *c) {
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->blk_a,
                       &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
-                      &c->summary, &c->a_targets,
-                      &c->a_names, &c->a_hint, &c->a_recs, &c->a_rcb, &c->a_cnt, &c->a_sum,
+                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
     if (c->profiling) {
@@ -174,6 +181,10 @@ void delta_ctx_destroy(delta_ctx *c) {
     }
     if (c->h_summary) cudaFreeHost(c->h_summary);
     if (c->h_state) cudaFreeHost(c->h_state);
+    for (int i = 0; i < delta_ctx::kRing; ++i) {
+        if (c->ring[i]) cudaFreeHost(c->ring[i]);
+        if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
+    }
     delete c;
 }
 
@@ -507,8 +518,11 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     }
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     const size_t nn = std::max<uint32_t>(n, 1);
-    GROW(ctx->a_targets, nn * sizeof(TargetDesc));
-    GROW(ctx->a_names, std::max<size_t>(blob.size(), 1));
+    // one upload per call: [TargetDesc x n | RecordRow x n (hint) | names]
+    const size_t off_hint = (n * sizeof(TargetDesc) + 63) & ~size_t(63);
+    const size_t off_names = off_hint + ((hint ? n * sizeof(RecordRow) : 0) + 63 & ~size_t(63));
+    const size_t up_bytes = off_names + blob.size();
+    GROW(ctx->a_upload, std::max<size_t>(up_bytes, 64));
     GROW(ctx->a_recs, nn * sizeof(ApplyRec));
     GROW(ctx->a_rcb, (nn + 1) * 8);
     if (!ctx->a_state.p) {
@@ -520,20 +534,33 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     GROW(ctx->a_sum, nch * 8);
     GROW(ctx->a_ord, nch * 8);
     GROW(ctx->a_idx, nch * 8);
-    if (hint && n) GROW(ctx->a_hint, n * sizeof(RecordRow));
-    // pageable sources: cudaMemcpyAsync stages them before returning, so the host vectors
-    // may die; the device copies are stream-ordered after any earlier call's kernels.
-    if (n) CK(cudaMemcpyAsync(ctx->a_targets.p, td.data(), n * sizeof(TargetDesc), cudaMemcpyHostToDevice, s), "upload");
-    if (!blob.empty()) CK(cudaMemcpyAsync(ctx->a_names.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s), "upload");
-    if (hint && n) CK(cudaMemcpyAsync(ctx->a_hint.p, hint, n * sizeof(RecordRow), cudaMemcpyHostToDevice, s), "upload");
+    {
+        const int r = ctx->ring_next;
+        ctx->ring_next = (r + 1) % delta_ctx::kRing;
+        if (ctx->ring_ev[r]) CK(cudaEventSynchronize(ctx->ring_ev[r]), "ring");  // its last copy is done
+        else CK(cudaEventCreateWithFlags(&ctx->ring_ev[r], cudaEventDisableTiming), "ring event");
+        if (ctx->ring_cap[r] < up_bytes) {
+            if (ctx->ring[r]) cudaFreeHost(ctx->ring[r]);
+            ctx->ring[r] = nullptr;
+            ctx->ring_cap[r] = 0;
+            CK(cudaMallocHost(&ctx->ring[r], std::max<size_t>(up_bytes, 4096)), "pinned ring");
+            ctx->ring_cap[r] = std::max<size_t>(up_bytes, 4096);
+        }
+        uint8_t *h = static_cast<uint8_t *>(ctx->ring[r]);
+        if (n) memcpy(h, td.data(), n * sizeof(TargetDesc));
+        if (hint && n) memcpy(h + off_hint, hint, n * sizeof(RecordRow));
+        if (!blob.empty()) memcpy(h + off_names, blob.data(), blob.size());
+        if (up_bytes) CK(cudaMemcpyAsync(ctx->a_upload.p, h, up_bytes, cudaMemcpyHostToDevice, s), "upload");
+        CK(cudaEventRecord(ctx->ring_ev[r], s), "ring event");
+    }
     CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(uint32_t), s), "memset");  // this call's gate
     ApplyArgs a;
     a.body = static_cast<const uint8_t *>(body);
     a.body_bytes = body_bytes;
-    a.targets = ctx->a_targets.as<TargetDesc>();
+    a.targets = ctx->a_upload.as<TargetDesc>();
     a.n = n;
-    a.names = ctx->a_names.as<uint8_t>();
-    a.hint = (hint && n) ? ctx->a_hint.as<RecordRow>() : nullptr;
+    a.names = ctx->a_upload.as<uint8_t>() + off_names;
+    a.hint = (hint && n) ? reinterpret_cast<const RecordRow *>(ctx->a_upload.as<uint8_t>() + off_hint) : nullptr;
     a.recs = ctx->a_recs.as<ApplyRec>();
     a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
     a.chunk_count = ctx->a_cnt.as<unsigned int>();

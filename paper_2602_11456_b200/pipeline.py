@@ -34,20 +34,23 @@ class RoundTrip:
                   for _, o, _ in tensors]
         ranges = [r for r in shard_plan(numels, max(1, min(groups, len(tensors)))) if r[1] > r[0]]
         self.groups = [(TensorList(tensors[a:b]), TargetList(targets[a:b])) for a, b in ranges]
-        self.cx = DeltaContext(self.device)
+        # one extract context per group: each caches its own plan (tile table) and slots
+        self.cxs = [DeltaContext(self.device) for _ in self.groups]
+        self.cx = self.cxs[0]
         self.ca = DeltaContext(self.device)
         if apply_ctas_per_sm:
             self.ca.set_option(_abi.DELTA_OPT_APPLY_CTAS_PER_SM, apply_ctas_per_sm)
         self.sx = torch.cuda.Stream(self.device)
         self.sa = torch.cuda.Stream(self.device, priority=apply_priority)
-        sizes = [self.cx.delta_size(tl, stream=self.sx) for tl, _ in self.groups]
+        sizes = [cx.delta_size(tl, stream=self.sx) for cx, (tl, _) in zip(self.cxs, self.groups)]
         total = sum(sizes)
         self.out = torch.empty(total + total // 8 + 4096, dtype=torch.uint8, device=self.device)
         self.tables = None
         self.body_bytes = 0
 
     def set_profiling(self, on: bool):
-        self.cx.set_profiling(on)
+        for cx in self.cxs:
+            cx.set_profiling(on)
         self.ca.set_profiling(on)
 
     def step(self, timing=None):
@@ -56,17 +59,17 @@ class RoundTrip:
         self.sx.wait_stream(cur)
         self.sa.wait_stream(cur)
         off, tables = 0, []
-        for tl, tg in self.groups:
-            size = self.cx.delta_size(tl, stream=self.sx)
+        for cx, (tl, tg) in zip(self.cxs, self.groups):
+            size = cx.delta_size(tl, stream=self.sx)
             if timing is not None:
-                t = self.cx.last_timing()
+                t = cx.last_timing()
                 for k in ("scan_ms", "lens_ms", "finalize_ms"):
                     timing[k] = timing.get(k, 0.0) + t[k]
             if off + size > self.out.numel():
                 raise RuntimeError("body buffer too small (weights changed density?)")
-            body, table = self.cx.delta_extract(tl, out=self.out[off:], stream=self.sx, table=True)
+            body, table = cx.delta_extract(tl, out=self.out[off:], stream=self.sx, table=True)
             if timing is not None:
-                t = self.cx.last_timing()
+                t = cx.last_timing()
                 for k in ("emit_ms", "headers_ms"):
                     timing[k] = timing.get(k, 0.0) + t[k]
             ev = torch.cuda.Event()
@@ -89,5 +92,6 @@ class RoundTrip:
         return rows
 
     def close(self):
-        self.cx.close()
+        for cx in self.cxs:
+            cx.close()
         self.ca.close()
