@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--pipeline", type=int, default=1,
                    help="G > 1: extract and apply in G pipelined groups on two streams")
     p.add_argument("--apply-ctas", type=int, default=0, help="apply kernels' CTAs per SM (0 = default)")
+    p.add_argument("--scan-kernel", type=int, default=0,
+                   help="1 = one CTA per tile, 2 = persistent TMA pipeline (0 = library default)")
     p.add_argument("--tensors", type=int, default=0,
                    help="profiling only: keep the first N tensors of the config")
     return p.parse_args()
@@ -291,7 +293,7 @@ def main():
     if args.pipeline > 1:
         from paper_2602_11456_b200.pipeline import RoundTrip
         rt = RoundTrip(tensors, tgts, groups=args.pipeline, device=dev,
-                       apply_ctas_per_sm=args.apply_ctas or None)
+                       apply_ctas_per_sm=args.apply_ctas or None, scan_kernel=args.scan_kernel or None)
         rt.set_profiling(True)
         ctx = rt.cx
 
@@ -306,6 +308,8 @@ def main():
         ctx = sd.DeltaContext(dev)
         if args.apply_ctas:
             ctx.set_option(1, args.apply_ctas)
+        if args.scan_kernel:
+            ctx.set_option(3, args.scan_kernel)
         ctx.set_profiling(True)
         size0 = ctx.delta_size(tl)
         out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)

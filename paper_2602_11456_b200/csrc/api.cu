@@ -89,7 +89,7 @@ struct delta_ctx {
     int ring_next = 0;
 
     // ---- launch options
-    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8;
+    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scan_kernel = 0;
 
     // ---- optional per-kernel event timing
     bool profiling = false;
@@ -196,6 +196,7 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     if (!c || value < 1 || value > 64) return DELTA_EINVAL;
     if (option == DELTA_OPT_APPLY_CTAS_PER_SM) c->apply_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_EMIT_CTAS_PER_SM) c->emit_ctas_per_sm = (int)value;
+    else if (option == DELTA_OPT_SCAN_KERNEL) c->scan_kernel = (int)value - 1;
     else return DELTA_EINVAL;
     return DELTA_OK;
 }
@@ -365,6 +366,8 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.summary = ctx->summary.as<ExtractSummary>();
     a.width = ctx->width;
     a.persist_ctas = ctx->sm_count * ctx->emit_ctas_per_sm;
+    a.sm_count = ctx->sm_count;
+    a.scan_kernel = ctx->scan_kernel;
     return a;
 }
 

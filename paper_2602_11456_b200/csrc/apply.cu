@@ -152,52 +152,80 @@ __device__ __forceinline__ ChunkView stage_chunk(const uint8_t *body, const Appl
     return v;
 }
 
+// Walk back from the thread's first byte p0 over continuation bytes (at most 10) to the
+// first byte of the varint that straddles into this thread's 16 bytes; returns its start q
+// (p0 if the previous byte ends a varint) and sets `longrun` if 10 continuation bytes
+// precede p0 (the varint is already longer than 10 bytes).
+__device__ __forceinline__ int varint_start(const uint8_t *sb, const ChunkView &v, int p0, bool &longrun) {
+    int q = p0, back = 0;
+    while ((long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80) && back < 10) {
+        --q;
+        ++back;
+    }
+    longrun = back == 10 && (long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80);
+    return q;
+}
+
 // Forward LEB128 decode of the varints whose terminator byte lies in this thread's 16
-// bytes of the chunk.  The first of them may begin in earlier bytes (up to 9 back, kept in
-// the halo / the previous thread's bytes): walk back to its first byte, then decode
-// forward once.  f(value, nbytes, last_byte, is_first_of_record) is called per varint in
-// stream order; nbytes is capped at 11 (anything > 10 is an error for the caller).
+// bytes; f(value) is called per varint in stream order.  Only used after validation.
 template <typename F>
 __device__ __forceinline__ void decode_thread(const uint8_t *sb, const ChunkView &v, F &&f) {
     const int p0 = threadIdx.x * 16;
     const int p1 = min(p0 + 16, (int)v.len);
     if (p0 >= p1) return;
-    int q = p0;
-    int back = 0;
-    while ((long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80) && back < 10) {
-        --q;
-        ++back;
-    }
+    bool longrun;
+    const int q = varint_start(sb, v, p0, longrun);
     unsigned long long acc = 0;
-    int nb = back;  // bytes of the current varint before p0 (decoded below)
-    bool first = ((long long)v.cs + q == 0);
-    // a run of >= 10 continuation bytes before p0: the varint is already too long
-    if (back == 10 && (long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80)) nb = 11;
-    for (int i = 0; i < back && nb <= 10; ++i)
-        acc |= (unsigned long long)(sb[kHalo + q + i] & 0x7F) << (7 * i);
-    for (int p = p0; p < p1; ++p) {
-        const uint8_t b = sb[kHalo + p];
-        if (nb < 10) acc |= (unsigned long long)(b & 0x7F) << (7 * nb);
-        else if (nb == 10) acc |= (unsigned long long)(b & 0x01) << 63;
-        if (nb < 11) ++nb;
-        if (!(b & 0x80)) {
-            f(acc, nb, b, first);
+    int d = 0;
+    for (int p = q; p < p1; ++p) {
+        const uint32_t b = sb[kHalo + p];
+        if (d < 10) acc |= (unsigned long long)(b & 0x7F) << (7 * d);
+        if (b & 0x80) {
+            ++d;
+        } else {
+            if (p >= p0) f(acc);
             acc = 0;
-            nb = 0;
-            first = false;
+            d = 0;
         }
     }
 }
 
-// Status of one decoded varint (SPEC.md:80 and the strictly-increasing invariant).
-__device__ __forceinline__ uint32_t varint_status(unsigned long long x, int nb, uint8_t last, bool first,
-                                                  unsigned long long numel) {
-    if (nb > 10) return kOverflow;
-    if (nb == 10 && last > 1) return kOverflow;
-    if (nb > 1 && last == 0) return kOverlong;
-    if (!first && x == 0) return kNonIncreasing;
-    if (x >= numel) return kRange;
-    return kOk;
+// A2's per-thread pass: count and (saturating) sum of the varints ending in this thread's
+// bytes, and the first decode error (zero gap after the first index):
+//   > 10 bytes, or a 10th byte carrying more than bit 63  -> overflow
+//   a 0x00 byte ending a multi-byte varint                -> overlong
+//   a lone 0x00 byte (gap 0) that is not the record's first -> non-increasing
+// Indices >= N are caught by A3 (last index = total sum, gaps >= 1).
+__device__ __forceinline__ void validate_thread(const uint8_t *sb, const ChunkView &v, uint32_t &cnt,
+                                                unsigned long long &sum, uint32_t &err) {
+    const int p0 = threadIdx.x * 16;
+    const int p1 = min(p0 + 16, (int)v.len);
+    if (p0 >= p1) return;
+    bool longrun;
+    const int q = varint_start(sb, v, p0, longrun);
+    bool first = ((long long)v.cs + q == 0);
+    unsigned long long acc = 0;
+    int d = longrun ? 11 : 0;
+    for (int p = q; p < p1; ++p) {
+        const uint32_t b = sb[kHalo + p];
+        if (d < 10) acc |= (unsigned long long)(b & 0x7F) << (7 * d);
+        if (b & 0x80) {
+            d = d < 11 ? d + 1 : 11;
+            continue;
+        }
+        if (p >= p0) {
+            uint32_t e = kOk;
+            if (d >= 10 || (d == 9 && b > 1)) e = kOverflow;
+            else if (b == 0 && d > 0) e = kOverlong;
+            else if (b == 0 && !first) e = kNonIncreasing;
+            if (e != kOk && err == kOk) err = e;
+            ++cnt;
+            sum = sat_add(sum, acc);
+        }
+        acc = 0;
+        d = 0;
+        first = false;
+    }
 }
 
 // ------------------------------------------------------------------------------ A2
@@ -218,12 +246,7 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
         __syncthreads();
         uint32_t cnt = 0, err = kOk;
         unsigned long long sum = 0;
-        decode_thread(sb, v, [&](unsigned long long x, int nb, uint8_t last, bool first) {
-            const uint32_t e = varint_status(x, nb, last, first, R.numel);
-            if (e != kOk && err == kOk) err = e;
-            ++cnt;
-            sum = sat_add(sum, x);
-        });
+        validate_thread(sb, v, cnt, sum, err);
         const int pl = (int)v.len - 1;  // the stream's last byte must end a varint
         if (v.last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (sb[kHalo + pl] & 0x80))
             err = err ? err : kTruncated;
@@ -350,7 +373,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         __syncthreads();
         uint32_t cnt = 0;
         unsigned long long sum = 0;
-        decode_thread(sb, v, [&](unsigned long long x, int, uint8_t, bool) {
+        decode_thread(sb, v, [&](unsigned long long x) {
             ++cnt;
             sum += x;
         });
@@ -370,7 +393,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         uint32_t ord = cpre + ci - cnt;
         unsigned long long idx = idx_base[c] + spre + si - sum;
         LT *w = reinterpret_cast<LT *>(R.w);
-        decode_thread(sb, v, [&](unsigned long long x, int, uint8_t, bool) {
+        decode_thread(sb, v, [&](unsigned long long x) {
             idx += x;
             w[idx] = sv[ord];
             ++ord;

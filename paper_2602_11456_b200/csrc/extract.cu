@@ -253,6 +253,172 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__r
         meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
 }
 
+// ------------------------------------------------------------------------------ K1 (TMA)
+// Persistent variant of K1: one CTA per SM, one producer warp that streams tiles into a
+// STAGES-deep shared-memory ring with 1-D bulk copies (TMA engine, L2 evict-first) and
+// eight consumer warps that compare + compact from shared memory.  The producer runs
+// STAGES tiles ahead, so DRAM stays busy while the consumers scan and write a tile.
+// Same per-tile output as k_scan_tiles.  Tiles are assigned statically (t = CTA + i*grid).
+template <int W, int STAGES>
+__global__ void __launch_bounds__(kScanThreads + 32, 1)
+k_scan_tiles_tma(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t slot_cap,
+                 uint8_t *__restrict__ slot_bytes, typename LaneOf<W>::T *__restrict__ slot_val,
+                 TileMeta *__restrict__ meta, ExtractSummary *summary) {
+    using LT = typename LaneOf<W>::T;
+    constexpr int LPV = 16 / W;
+    constexpr uint32_t TB = kTileBytes;  // bytes per operand per tile
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t *st_old = smem;
+    uint8_t *st_new = smem + STAGES * TB;
+    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem + 2 * STAGES * TB);  // LANES
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    __shared__ uint32_t s_warp[kScanThreads / 32][4];
+    __shared__ uint32_t s_red[kScanThreads / 32];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kScanThreads / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kScanThreads / 32) {  // ---------------------------------------- producer
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(&empty[s], ph ^ 1);  // the consumers released this stage
+                const TileDesc d = tiles[t];
+                const uint32_t bytes = (d.flags_tensor & kTileAligned) ? ((d.nlanes * W) & ~15u) : 0u;
+                mbar_arrive_expect_tx(&full[s], 2 * bytes);
+                if (bytes) {
+                    bulk_g2s(st_old + s * TB, d.old_p, bytes, &full[s], pol);
+                    bulk_g2s(st_new + s * TB, d.new_p, bytes, &full[s], pol);
+                }
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------------------ consumers
+    int s = 0;
+    uint32_t ph = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileDesc d = tiles[t];
+        const uint32_t nl = d.nlanes;
+        const uint32_t bulk_lanes = (d.flags_tensor & kTileAligned) ? ((nl * W) & ~15u) / W : 0u;
+        uint8_t *bo = st_old + s * TB;
+        uint8_t *bn = st_new + s * TB;
+        mbar_wait(&full[s], ph);
+        if (bulk_lanes < nl) {  // ragged tail or unaligned span: the rest lane by lane
+            for (uint32_t j = bulk_lanes + tid; j < nl; j += kScanThreads) {
+                reinterpret_cast<LT *>(bo)[j] = __ldg(reinterpret_cast<const LT *>(d.old_p) + j);
+                reinterpret_cast<LT *>(bn)[j] = __ldg(reinterpret_cast<const LT *>(d.new_p) + j);
+            }
+            named_bar_sync(1, kScanThreads);
+        }
+        uint32_t m[kScanVecs];
+#pragma unroll
+        for (int r = 0; r < kScanVecs; ++r) {
+            const uint32_t v = r * kScanThreads + tid;
+            m[r] = 0;
+            if (v * LPV < nl) {
+                const uint4 a = *reinterpret_cast<const uint4 *>(bo + v * 16);
+                const uint4 b = *reinterpret_cast<const uint4 *>(bn + v * 16);
+                m[r] = diff_mask<W>(a, b);
+                if ((v + 1) * LPV > nl) m[r] &= (1u << (nl - v * LPV)) - 1u;
+            }
+        }
+        uint32_t pk[4], inc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) inc[q] = warp_inclusive_sum(pk[q]);
+        if (lane == 31) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s_warp[warp][q] = inc[q];
+        }
+        named_bar_sync(1, kScanThreads);
+        uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; ++w) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t x = s_warp[w][q];
+                if (w < warp) pre[q] += x;
+                tot[q] += x;
+            }
+        }
+        uint32_t c = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
+        uint32_t rbase = 0;
+#pragma unroll
+        for (int r = 0; r < kScanVecs; ++r) {
+            const int q = r >> 1, sh = (r & 1) * 16;
+            uint32_t pos = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
+            uint32_t mm = m[r];
+            while (mm) {
+                const int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                s_off[pos++] = (uint16_t)((r * kScanThreads + tid) * LPV + j);
+            }
+            rbase += (tot[q] >> sh) & 0xFFFFu;
+        }
+        named_bar_sync(1, kScanThreads);  // s_off complete; s_warp free again
+        if (c > slot_cap) {
+            if (tid == 0) {
+                meta[t] = TileMeta{c, 0, 0, 0, 0};
+                summary->overflow = 1;
+                atomicMax(&summary->max_count, (unsigned long long)c);
+            }
+        } else {
+            uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
+            LT *sv = slot_val + (size_t)t * slot_cap;
+            for (uint32_t i = tid; i < c; i += kScanThreads) sv[i] = reinterpret_cast<const LT *>(bn)[s_off[i]];
+            const uint32_t q = (c + kScanThreads - 1) / kScanThreads;
+            const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
+            uint32_t L = 0;
+            for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) L += 1u + ((s_off[i] - s_off[i - 1]) >= 128u);
+            // block exclusive scan over the 256 consumer threads (named barrier)
+            const uint32_t incl = warp_inclusive_sum(L);
+            if (lane == 31) s_red[warp] = incl;
+            named_bar_sync(1, kScanThreads);
+            uint32_t pos = incl - L, tl = 0;
+#pragma unroll
+            for (int w = 0; w < kScanThreads / 32; ++w) {
+                if (w < warp) pos += s_red[w];
+                tl += s_red[w];
+            }
+            for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) {
+                const uint32_t g = s_off[i] - s_off[i - 1];
+                if (g < 128u) {
+                    sb[pos++] = (uint8_t)g;
+                } else {
+                    sb[pos++] = (uint8_t)(g | 0x80u);
+                    sb[pos++] = (uint8_t)(g >> 7);
+                }
+            }
+            if (tid == 0)
+                meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
+        }
+        named_bar_sync(1, kScanThreads);  // everyone is done with stage s, s_off, s_red
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------ K2
 // Tile-level scans over blocks of kTileBlock tiles (1024 threads x 4 tiles).
 __global__ void __launch_bounds__(1024)
@@ -558,8 +724,17 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     const size_t smem = (size_t)LANES * (sizeof(uint16_t) + W);
     cudaFuncSetAttribute(k_scan_tiles<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
-    k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
-                                                         static_cast<LT *>(a.slot_val), a.meta, a.summary);
+    if (a.scan_kernel == 1) {
+        constexpr int STAGES = 3;
+        const size_t tsmem = 2 * STAGES * (size_t)kTileBytes + (size_t)LANES * sizeof(uint16_t);
+        cudaFuncSetAttribute(k_scan_tiles_tma<W, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+        const uint32_t grid = a.ntiles < (uint32_t)a.sm_count ? a.ntiles : (uint32_t)a.sm_count;
+        k_scan_tiles_tma<W, STAGES><<<grid, kScanThreads + 32, tsmem, s>>>(
+            a.tiles, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<LT *>(a.slot_val), a.meta, a.summary);
+    } else {
+        k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
+                                                             static_cast<LT *>(a.slot_val), a.meta, a.summary);
+    }
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);

@@ -107,6 +107,8 @@ struct ExtractArgs {
     ExtractSummary *summary;
     int width;                        // 2 or 4
     int persist_ctas;                 // grid for grid-stride kernels
+    int sm_count;
+    int scan_kernel;                  // 0: one CTA per tile; 1: persistent TMA pipeline
 };
 
 // ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1,

@@ -27,7 +27,7 @@ class RoundTrip:
     """
 
     def __init__(self, tensors, targets, groups=8, device=None, apply_ctas_per_sm=None,
-                 apply_priority=-1):
+                 apply_priority=-1, scan_kernel=None):
         assert len(tensors) == len(targets)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         numels = [sum(x.numel() for x in ([o] if isinstance(o, torch.Tensor) else o))
@@ -37,6 +37,9 @@ class RoundTrip:
         # one extract context per group: each caches its own plan (tile table) and slots
         self.cxs = [DeltaContext(self.device) for _ in self.groups]
         self.cx = self.cxs[0]
+        if scan_kernel:
+            for cx in self.cxs:
+                cx.set_option(_abi.DELTA_OPT_SCAN_KERNEL, scan_kernel)
         self.ca = DeltaContext(self.device)
         if apply_ctas_per_sm:
             self.ca.set_option(_abi.DELTA_OPT_APPLY_CTAS_PER_SM, apply_ctas_per_sm)

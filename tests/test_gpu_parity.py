@@ -403,3 +403,26 @@ def test_async_apply_error_is_reported_at_wait(sd):
     for (_, t), (_, _, w) in zip(targets, ts):
         assert_lanes_equal(t, w.to(DEV))
     ctx.close()
+
+
+# ------------------------------------------------------------------ TMA-pipelined K1
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_tma_scan_kernel_parity(sd, dtype):
+    """The persistent, bulk-copy pipelined compare+compaction (DELTA_OPT_SCAN_KERNEL = 2)
+    on ragged / unaligned / multi-tile / dense inputs, byte-exact against the oracle."""
+    from paper_2602_11456_b200 import _abi
+    ctx = sd.DeltaContext(DEV)
+    ctx.set_option(_abi.DELTA_OPT_SCAN_KERNEL, 2)
+    rng = np.random.default_rng(21)
+    tensors = []
+    for k, n in enumerate([1, 9, 16384, 16385, 16384 * 7 + 3, 250_001, 0, 3_000_000]):
+        spec = TensorSpec(f"t{k}", (n,), "matrix")
+        o, w = generate_pair(spec, k, 3, rho=float(rng.choice([0.0, 0.01, 0.5, 1.0])), dtype=dtype,
+                             device=DEV, values="bits")
+        tensors.append((spec.name, o, w))
+    # an unaligned multi-span tensor
+    spec = TensorSpec("u", (100_003,), "matrix")
+    o, w = generate_pair(spec, 99, 3, rho=0.05, dtype=dtype, device=DEV)
+    tensors.append(("unaligned", [o[1:40_000], o[40_000:]], [w[1:40_000], w[40_000:]]))
+    _roundtrip(sd, tensors, ctx=ctx)
+    ctx.close()
