@@ -135,20 +135,34 @@ struct ChunkView {
     unsigned long long cs;   // chunk start within the record's index stream
     uint32_t len;            // bytes in this chunk
     bool last;               // chunk holds the stream's final byte
+    const uint8_t *b;        // b[p] = stream byte cs + p, valid for -min(cs, kHalo) <= p < len
 };
 
-// Stage bytes [cs - halo, cs + len) of the record's stream into sb (sb[kHalo] = byte cs).
-// The caller synchronises before reading.
+// Bytes [src, src + n) into shared memory with 16-byte loads of the aligned superset (one
+// or two per thread for a 4 KiB chunk); returns p with p[i] = src[i].  buf is 16-byte
+// aligned with room for n + 32 bytes.  The over-read stays inside the 16-byte aligned
+// vectors that hold the range (never across an allocation granule).
+__device__ __forceinline__ const uint8_t *stage_bytes(uint8_t *buf, const uint8_t *src, uint32_t n) {
+    const uint4 *a = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+    const uint32_t o = (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15);
+    const uint32_t nv = (o + n + 15) / 16;
+    for (uint32_t j = threadIdx.x; j < nv; j += blockDim.x) reinterpret_cast<uint4 *>(buf)[j] = __ldg(a + j);
+    return buf + o;
+}
+
+constexpr int kStageBytes = kHalo + kByteChunk + 32;
+
+// Stage bytes [cs - halo, cs + len) of the record's stream.  The caller synchronises
+// before reading.
 __device__ __forceinline__ ChunkView stage_chunk(const uint8_t *body, const ApplyRec &R,
-                                                 unsigned long long j, uint8_t *sb) {
+                                                 unsigned long long j, uint8_t *buf) {
     ChunkView v;
     v.cs = j * kByteChunk;
     const unsigned long long ce = min(R.idx_len, v.cs + kByteChunk);
     v.len = (uint32_t)(ce - v.cs);
     v.last = (ce == R.idx_len);
     const uint32_t hs = (uint32_t)min(v.cs, (unsigned long long)kHalo);
-    const uint8_t *src = body + R.idx_off + v.cs - hs;
-    for (uint32_t b = threadIdx.x; b < hs + v.len; b += blockDim.x) sb[kHalo - hs + b] = __ldg(src + b);
+    v.b = stage_bytes(buf, body + R.idx_off + v.cs - hs, hs + v.len) + hs;
     return v;
 }
 
@@ -156,29 +170,29 @@ __device__ __forceinline__ ChunkView stage_chunk(const uint8_t *body, const Appl
 // first byte of the varint that straddles into this thread's 16 bytes; returns its start q
 // (p0 if the previous byte ends a varint) and sets `longrun` if 10 continuation bytes
 // precede p0 (the varint is already longer than 10 bytes).
-__device__ __forceinline__ int varint_start(const uint8_t *sb, const ChunkView &v, int p0, bool &longrun) {
+__device__ __forceinline__ int varint_start(const ChunkView &v, int p0, bool &longrun) {
     int q = p0, back = 0;
-    while ((long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80) && back < 10) {
+    while ((long long)v.cs + q > 0 && (v.b[q - 1] & 0x80) && back < 10) {
         --q;
         ++back;
     }
-    longrun = back == 10 && (long long)v.cs + q > 0 && (sb[kHalo + q - 1] & 0x80);
+    longrun = back == 10 && (long long)v.cs + q > 0 && (v.b[q - 1] & 0x80);
     return q;
 }
 
 // Forward LEB128 decode of the varints whose terminator byte lies in this thread's 16
 // bytes; f(value) is called per varint in stream order.  Only used after validation.
 template <typename F>
-__device__ __forceinline__ void decode_thread(const uint8_t *sb, const ChunkView &v, F &&f) {
+__device__ __forceinline__ void decode_thread(const ChunkView &v, F &&f) {
     const int p0 = threadIdx.x * 16;
     const int p1 = min(p0 + 16, (int)v.len);
     if (p0 >= p1) return;
     bool longrun;
-    const int q = varint_start(sb, v, p0, longrun);
+    const int q = varint_start(v, p0, longrun);
     unsigned long long acc = 0;
     int d = 0;
     for (int p = q; p < p1; ++p) {
-        const uint32_t b = sb[kHalo + p];
+        const uint32_t b = v.b[p];
         if (d < 10) acc |= (unsigned long long)(b & 0x7F) << (7 * d);
         if (b & 0x80) {
             ++d;
@@ -196,18 +210,18 @@ __device__ __forceinline__ void decode_thread(const uint8_t *sb, const ChunkView
 //   a 0x00 byte ending a multi-byte varint                -> overlong
 //   a lone 0x00 byte (gap 0) that is not the record's first -> non-increasing
 // Indices >= N are caught by A3 (last index = total sum, gaps >= 1).
-__device__ __forceinline__ void validate_thread(const uint8_t *sb, const ChunkView &v, uint32_t &cnt,
+__device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cnt,
                                                 unsigned long long &sum, uint32_t &err) {
     const int p0 = threadIdx.x * 16;
     const int p1 = min(p0 + 16, (int)v.len);
     if (p0 >= p1) return;
     bool longrun;
-    const int q = varint_start(sb, v, p0, longrun);
+    const int q = varint_start(v, p0, longrun);
     bool first = ((long long)v.cs + q == 0);
     unsigned long long acc = 0;
     int d = longrun ? 11 : 0;
     for (int p = q; p < p1; ++p) {
-        const uint32_t b = sb[kHalo + p];
+        const uint32_t b = v.b[p];
         if (d < 10) acc |= (unsigned long long)(b & 0x7F) << (7 * d);
         if (b & 0x80) {
             d = d < 11 ? d + 1 : 11;
@@ -235,7 +249,7 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
                unsigned long long *__restrict__ chunk_sum, ApplyState *st) {
     if (st->status != kOk) return;
     const unsigned long long nch = st->n_chunks;
-    __shared__ uint8_t sb[kHalo + kByteChunk];
+    __shared__ __align__(16) uint8_t sb[kStageBytes];
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -246,9 +260,9 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
         __syncthreads();
         uint32_t cnt = 0, err = kOk;
         unsigned long long sum = 0;
-        validate_thread(sb, v, cnt, sum, err);
+        validate_thread(v, cnt, sum, err);
         const int pl = (int)v.len - 1;  // the stream's last byte must end a varint
-        if (v.last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (sb[kHalo + pl] & 0x80))
+        if (v.last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (v.b[pl] & 0x80))
             err = err ? err : kTruncated;
         if (err != kOk) set_status(st, err);
 #pragma unroll
@@ -354,8 +368,8 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         return;
     }
     const unsigned long long nch = st->n_chunks;
-    __shared__ uint8_t sb[kHalo + kByteChunk];
-    __shared__ LT sv[kByteChunk];  // at most one varint per byte
+    __shared__ __align__(16) uint8_t sb[kStageBytes];
+    __shared__ __align__(16) uint8_t svb[kByteChunk * W + 32];  // at most one varint per byte
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -365,15 +379,12 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
         const unsigned long long ob = ord_base[c];
         const uint32_t cn = chunk_count[c];
-        {  // stage this chunk's values (cn lanes, any alignment in the body)
-            const uint8_t *src = body + R.val_off + ob * W;
-            uint8_t *dst = reinterpret_cast<uint8_t *>(sv);
-            for (uint32_t b = threadIdx.x; b < cn * W; b += blockDim.x) dst[b] = __ldg(src + b);
-        }
+        // this chunk's values (cn lanes, any alignment in the body)
+        const uint8_t *vals = stage_bytes(svb, body + R.val_off + ob * W, cn * W);
         __syncthreads();
         uint32_t cnt = 0;
         unsigned long long sum = 0;
-        decode_thread(sb, v, [&](unsigned long long x) {
+        decode_thread(v, [&](unsigned long long x) {
             ++cnt;
             sum += x;
         });
@@ -393,9 +404,12 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         uint32_t ord = cpre + ci - cnt;
         unsigned long long idx = idx_base[c] + spre + si - sum;
         LT *w = reinterpret_cast<LT *>(R.w);
-        decode_thread(sb, v, [&](unsigned long long x) {
+        decode_thread(v, [&](unsigned long long x) {
             idx += x;
-            w[idx] = sv[ord];
+            LT val;
+            if constexpr (W == 2) val = (LT)(vals[2 * ord] | (vals[2 * ord + 1] << 8));
+            else val = (LT)vals[4 * ord] | ((LT)vals[4 * ord + 1] << 8) | ((LT)vals[4 * ord + 2] << 16) | ((LT)vals[4 * ord + 3] << 24);
+            w[idx] = val;
             ++ord;
         });
         __syncthreads();

@@ -119,7 +119,7 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 
 // ------------------------------------------------------------------------------ K1
 template <int W>
-__global__ void __launch_bounds__(kScanThreads)
+__global__ void __launch_bounds__(kScanThreads, 4)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
@@ -129,8 +129,7 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__r
     static_assert(kScanVecs == 8, "count packing assumes 8 vectors per thread");
     static_assert(LANES <= 65536, "lane offsets are u16");
     extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);                 // LANES
-    LT *s_val = reinterpret_cast<LT *>(smem + LANES * sizeof(uint16_t));  // LANES
+    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);  // LANES
     __shared__ uint32_t s_warp[kScanThreads / 32][4];
     __shared__ uint32_t s_red[kScanThreads / 32];
 
@@ -201,8 +200,11 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__r
 #pragma unroll
     for (int q = 0; q < 4; ++q) c += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
 
-    // Ordered compaction into shared memory: entry (r, tid, j) gets rank
-    // sum_{r'<r} tot_r' + prefix_r(tid) + popc(mask below j) — lane order.
+    // Ordered compaction: entry (r, tid, j) gets rank sum_{r'<r} tot_r' + prefix_r(tid) +
+    // popc(mask below j) — lane order.  Values go straight from registers to the tile's
+    // slot; lane offsets to shared memory (for the in-tile gaps below).
+    const bool fits = c <= slot_cap;
+    LT *sv = slot_val + (size_t)t * slot_cap;
     uint32_t rbase = 0;
 #pragma unroll
     for (int r = 0; r < kScanVecs; ++r) {
@@ -213,14 +215,14 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__r
             const int j = __ffs(mm) - 1;
             mm &= mm - 1;
             s_off[pos] = (uint16_t)((r * kScanThreads + tid) * LPV + j);
-            s_val[pos] = (LT)lane_of<W>(vn[r], j);
+            if (fits) sv[pos] = (LT)lane_of<W>(vn[r], j);
             ++pos;
         }
         rbase += (tot[q] >> sh) & 0xFFFFu;
     }
     __syncthreads();
 
-    if (c > slot_cap) {  // slot too small: report, write nothing (host grows slots, reruns)
+    if (!fits) {  // slot too small: report (host grows slots, reruns)
         if (tid == 0) {
             meta[t] = TileMeta{c, 0, 0, 0, 0};
             summary->overflow = 1;
@@ -228,12 +230,10 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__r
         }
         return;
     }
-    // Slot: raw values (coalesced copy) and the LEB128 bytes of the gaps between
-    // consecutive changes inside the tile (each < 2^14 lanes, so 1 or 2 bytes), encoded
-    // here in order; the first change's gap depends on earlier tiles and is written by K4.
+    // The LEB128 bytes of the gaps between consecutive changes inside the tile (each
+    // < 2^14 lanes, so 1 or 2 bytes), encoded in order; the first change's gap depends on
+    // earlier tiles and is written by K4.
     uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
-    LT *sv = slot_val + (size_t)t * slot_cap;
-    for (uint32_t i = tid; i < c; i += kScanThreads) sv[i] = s_val[i];
     const uint32_t q = (c + kScanThreads - 1) / kScanThreads;  // contiguous entries per thread
     const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
     uint32_t L = 0;
@@ -721,7 +721,7 @@ template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     constexpr int LANES = kScanThreads * kScanVecs * (16 / W);
-    const size_t smem = (size_t)LANES * (sizeof(uint16_t) + W);
+    const size_t smem = (size_t)LANES * sizeof(uint16_t);
     cudaFuncSetAttribute(k_scan_tiles<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
     if (a.scan_kernel == 1) {
