@@ -119,7 +119,7 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 
 // ------------------------------------------------------------------------------ K1
 template <int W>
-__global__ void __launch_bounds__(kScanThreads, 4)
+__global__ void __launch_bounds__(kScanThreads, 3)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
