@@ -213,8 +213,9 @@ typedef struct {
 enum {
     DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode/scatter kernels, CTAs per SM (default 8) */
     DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 8) */
-    DELTA_OPT_SCAN_KERNEL = 3        /* compare+compaction kernel: 1 = one CTA per tile (default),
-                                        2 = persistent, TMA bulk-copy pipelined */
+    DELTA_OPT_SCAN_KERNEL = 3        /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
+                                        vectors (default); 2 = persistent, TMA bulk-copy pipelined;
+                                        3 = one CTA per tile, 128-byte runs per thread */
 };
 
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */

@@ -253,6 +253,109 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__r
         meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
 }
 
+// ------------------------------------------------------------------------------ K1 (runs)
+// Variant of K1 where each thread owns one contiguous 128-byte run of the tile (64 bf16 /
+// 32 fp32 lanes) loaded with four 256-bit streaming loads per operand.  Lane order is then
+// thread order, so one single-word block scan gives every thread's rank base; the change
+// flags of a 32-bit word come from (x & 0x7FFF7FFF) + 0x7FFF7FFF | x (bit 15 / 31 set iff
+// the low / high half differs).  Values are re-read (L2) for the changed lanes only.
+template <int W>
+__global__ void __launch_bounds__(kScanThreads, 3)
+k_scan_runs(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
+            typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
+            ExtractSummary *summary) {
+    using LT = typename LaneOf<W>::T;
+    constexpr int RUN = kTileBytes / kScanThreads;  // 128 bytes per thread
+    constexpr int LPT = RUN / W;                     // lanes per thread
+    constexpr int NW = RUN / 4;                      // 32-bit words per thread per operand
+    static_assert(LPT <= 64, "lane mask is 64 bits");
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);
+    __shared__ uint32_t s_w[kScanThreads / 32];
+
+    const int tid = threadIdx.x;
+    const uint32_t t = blockIdx.x;
+    const TileDesc d = tiles[t];
+    const uint32_t nl = d.nlanes;
+    const uint32_t l0 = tid * LPT;  // first lane of this thread's run
+
+    const bool full_run = (d.flags_tensor & kTileAligned) && (l0 + LPT <= nl) &&
+                          ((reinterpret_cast<uintptr_t>(d.old_p) | reinterpret_cast<uintptr_t>(d.new_p)) % 32 == 0);
+    uint32_t mlo = 0, mhi = 0;  // 64-bit change mask of the run, in lane order
+    if (full_run) {
+        uint32_t a[NW], b[NW];
+#pragma unroll
+        for (int q = 0; q < NW / 8; ++q) {
+            ld_stream_v8(d.old_p + (size_t)tid * RUN + 32 * q, a + 8 * q);
+            ld_stream_v8(d.new_p + (size_t)tid * RUN + 32 * q, b + 8 * q);
+        }
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            const uint32_t x = a[i] ^ b[i];
+            if constexpr (W == 2) {
+                const uint32_t f = (((x & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x) & 0x80008000u;
+                const uint32_t bits = ((f >> 15) & 1u) | (f >> 30);
+                if (2 * i < 32) mlo |= bits << (2 * i);
+                else mhi |= bits << (2 * i - 32);
+            } else {
+                mlo |= (uint32_t)(x != 0) << i;
+            }
+        }
+    } else {  // ragged tail / unaligned span: lane by lane
+        const LT *op = reinterpret_cast<const LT *>(d.old_p), *nq = reinterpret_cast<const LT *>(d.new_p);
+        for (uint32_t j = 0; j < (uint32_t)LPT && l0 + j < nl; ++j) {
+            if (__ldg(op + l0 + j) != __ldg(nq + l0 + j)) {
+                if (j < 32) mlo |= 1u << j;
+                else mhi |= 1u << (j - 32);
+            }
+        }
+    }
+    const uint32_t cnt = __popc(mlo) + __popc(mhi);
+    uint32_t c;
+    const uint32_t base = block_excl_scan<kScanThreads / 32, uint32_t>(cnt, s_w, c);
+    const bool fits = c <= slot_cap;
+    LT *sv = slot_val + (size_t)t * slot_cap;
+    const LT *np = reinterpret_cast<const LT *>(d.new_p);
+    // ordered compaction: offsets to shared memory, values (re-read) to the slot
+    uint32_t pos = base, L = 0, prev = 0;
+    unsigned long long mm = ((unsigned long long)mhi << 32) | mlo;
+    while (mm) {
+        const uint32_t j = __ffsll(mm) - 1;
+        mm &= mm - 1;
+        const uint32_t off = l0 + j;
+        s_off[pos] = (uint16_t)off;
+        if (fits) sv[pos] = __ldg(np + off);
+        if (pos > base) L += 1u + ((off - prev) >= 128u);
+        prev = off;
+        ++pos;
+    }
+    __syncthreads();
+    if (!fits) {
+        if (tid == 0) {
+            meta[t] = TileMeta{c, 0, 0, 0, 0};
+            summary->overflow = 1;
+            atomicMax(&summary->max_count, (unsigned long long)c);
+        }
+        return;
+    }
+    // the first own entry's gap: predecessor is the previous thread's last entry
+    if (cnt && base > 0) L += 1u + ((uint32_t)(s_off[base] - s_off[base - 1]) >= 128u);
+    uint32_t tl;
+    uint32_t bp = block_excl_scan<kScanThreads / 32, uint32_t>(L, s_w, tl);
+    uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
+    for (uint32_t i = (base ? base : 1); i < base + cnt; ++i) {
+        const uint32_t g = s_off[i] - s_off[i - 1];
+        if (g < 128u) {
+            sb[bp++] = (uint8_t)g;
+        } else {
+            sb[bp++] = (uint8_t)(g | 0x80u);
+            sb[bp++] = (uint8_t)(g >> 7);
+        }
+    }
+    if (tid == 0)
+        meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
+}
+
 // ------------------------------------------------------------------------------ K1 (TMA)
 // Persistent variant of K1: one CTA per SM, one producer warp that streams tiles into a
 // STAGES-deep shared-memory ring with 1-D bulk copies (TMA engine, L2 evict-first) and
@@ -731,6 +834,10 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
         const uint32_t grid = a.ntiles < (uint32_t)a.sm_count ? a.ntiles : (uint32_t)a.sm_count;
         k_scan_tiles_tma<W, STAGES><<<grid, kScanThreads + 32, tsmem, s>>>(
             a.tiles, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<LT *>(a.slot_val), a.meta, a.summary);
+    } else if (a.scan_kernel == 2) {
+        cudaFuncSetAttribute(k_scan_runs<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_scan_runs<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
+                                                            static_cast<LT *>(a.slot_val), a.meta, a.summary);
     } else {
         k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
                                                              static_cast<LT *>(a.slot_val), a.meta, a.summary);

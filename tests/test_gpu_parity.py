@@ -406,13 +406,15 @@ def test_async_apply_error_is_reported_at_wait(sd):
 
 
 # ------------------------------------------------------------------ TMA-pipelined K1
+@pytest.mark.parametrize("kernel", [2, 3])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-def test_tma_scan_kernel_parity(sd, dtype):
-    """The persistent, bulk-copy pipelined compare+compaction (DELTA_OPT_SCAN_KERNEL = 2)
-    on ragged / unaligned / multi-tile / dense inputs, byte-exact against the oracle."""
+def test_scan_kernel_variants_parity(sd, dtype, kernel):
+    """The other compare+compaction kernels (DELTA_OPT_SCAN_KERNEL = 2: persistent, TMA
+    bulk-copy pipelined; 3: 128-byte runs per thread) on ragged / unaligned / multi-tile /
+    dense inputs, byte-exact against the oracle."""
     from paper_2602_11456_b200 import _abi
     ctx = sd.DeltaContext(DEV)
-    ctx.set_option(_abi.DELTA_OPT_SCAN_KERNEL, 2)
+    ctx.set_option(_abi.DELTA_OPT_SCAN_KERNEL, kernel)
     rng = np.random.default_rng(21)
     tensors = []
     for k, n in enumerate([1, 9, 16384, 16385, 16384 * 7 + 3, 250_001, 0, 3_000_000]):
