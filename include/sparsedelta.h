@@ -211,11 +211,12 @@ typedef struct {
 
 /* Launch-shape options (performance only; results never depend on them). */
 enum {
-    DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode/scatter kernels, CTAs per SM (default 8) */
+    DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode kernel, CTAs per SM (default 8) */
     DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 8) */
-    DELTA_OPT_SCAN_KERNEL = 3        /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
+    DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
                                         vectors (default); 2 = persistent, TMA bulk-copy pipelined;
                                         3 = one CTA per tile, 128-byte runs per thread */
+    DELTA_OPT_SCATTER_CTAS_PER_SM = 4 /* grid of the apply scatter kernel, CTAs per SM (default 2) */
 };
 
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */

@@ -19,6 +19,37 @@ TABLE_FIELDS = ("record_offset", "element_count", "nnz", "index_offset", "index_
                 "values_offset", "record_bytes")
 
 
+class Table:
+    """Offset-table rows of one extract (TABLE_FIELDS order), kept as the ctypes array the
+    library filled, so it can be handed back to delta_apply as a hint without conversion.
+    Indexing / iteration yield plain tuples."""
+
+    __slots__ = ("arr", "n")
+
+    def __init__(self, arr, n):
+        self.arr, self.n = arr, n
+
+    def __len__(self):
+        return self.n
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(self.n))]
+        if k < 0:
+            k += self.n
+        if not 0 <= k < self.n:
+            raise IndexError(k)
+        r = self.arr[k]
+        return (r.record_offset, r.element_count, r.nnz, r.index_offset, r.index_bytes,
+                r.values_offset, r.record_bytes)
+
+    def __iter__(self):
+        return (self[k] for k in range(self.n))
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+
 class DeltaError(RuntimeError):
     """A non-OK status from the library; ``status``/``detail`` are the C codes and
     ``kind`` the DELTA_D_* name (e.g. "truncated", "name") when there is one."""
@@ -174,9 +205,9 @@ class DeltaContext:
         return out.value
 
     def delta_extract(self, tensors, out=None, stream=None, table=True):
-        """Pack the delta.  Returns ``(body, rows)``: ``body`` a uint8 CUDA tensor view of
-        exactly the body bytes (``out``'s prefix if ``out`` is given), ``rows`` a list of
-        offset-table tuples (TABLE_FIELDS order) or None if ``table`` is False."""
+        """Pack the delta.  Returns ``(body, table)``: ``body`` a uint8 CUDA tensor view of
+        exactly the body bytes (``out``'s prefix if ``out`` is given), ``table`` a Table of
+        offset-table rows (TABLE_FIELDS order) or None if ``table`` is False."""
         tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
         st = _stream_handle(stream)
         nbytes = c_uint64()
@@ -191,7 +222,7 @@ class DeltaContext:
         body = out[:nbytes.value]
         if rows is None:
             return body, None
-        return body, [tuple(getattr(rows[k], f) for f in TABLE_FIELDS) for k in range(tl.n)]
+        return body, Table(rows, tl.n)
 
     def delta_apply(self, targets, body, table=None, stream=None, wait=True):
         """Validate ``body`` fully, then scatter its values into ``targets`` in place
@@ -202,7 +233,12 @@ class DeltaContext:
             raise ValueError("body must be a contiguous uint8 CUDA tensor")
         hint = None
         if table is not None:
-            hint = table if isinstance(table, ctypes.Array) else _rows_to_ctypes(table)
+            if isinstance(table, Table):
+                hint = table.arr
+            elif isinstance(table, ctypes.Array):
+                hint = table
+            else:
+                hint = _rows_to_ctypes(table)
         fn = self._lib.delta_apply if wait else self._lib.delta_apply_async
         self._check(fn(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(), body.numel(), hint,
                        _stream_handle(stream)))

@@ -89,7 +89,7 @@ struct delta_ctx {
     int ring_next = 0;
 
     // ---- launch options
-    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scan_kernel = 0;
+    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scatter_ctas_per_sm = 2, scan_kernel = 0;
 
     // ---- optional per-kernel event timing
     bool profiling = false;
@@ -197,6 +197,7 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     if (option == DELTA_OPT_APPLY_CTAS_PER_SM) c->apply_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_EMIT_CTAS_PER_SM) c->emit_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_SCAN_KERNEL) c->scan_kernel = (int)value - 1;
+    else if (option == DELTA_OPT_SCATTER_CTAS_PER_SM) c->scatter_ctas_per_sm = (int)value;
     else return DELTA_EINVAL;
     return DELTA_OK;
 }
@@ -574,6 +575,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.state = ctx->a_state.as<ApplyState>();
     a.width = w;
     a.persist_ctas = ctx->sm_count * ctx->apply_ctas_per_sm;
+    a.scatter_ctas = ctx->sm_count * ctx->scatter_ctas_per_sm;
     CK(launch_apply(a, s, ctx->profiling ? ctx->ev_apply : nullptr), "apply launch");
     return DELTA_OK;
 }

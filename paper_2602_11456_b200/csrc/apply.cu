@@ -430,10 +430,10 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[3], s);
     if (a.width == 2)
-        k_scatter<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
+        k_scatter<2><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
                                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
     else
-        k_scatter<4><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
+        k_scatter<4><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
                                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[4], s);
     return cudaGetLastError();

@@ -133,6 +133,7 @@ struct ApplyArgs {
     ApplyState *state;
     int width;
     int persist_ctas;
+    int scatter_ctas;
 };
 
 // ev: nullptr, or 5 events: before A1, after A1, A2, A3, A4.
