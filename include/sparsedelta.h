@@ -216,7 +216,9 @@ enum {
     DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
                                         vectors (default); 2 = persistent, TMA bulk-copy pipelined;
                                         3 = one CTA per tile, 128-byte runs per thread */
-    DELTA_OPT_SCATTER_CTAS_PER_SM = 4 /* grid of the apply scatter kernel, CTAs per SM (default 2) */
+    DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 2) */
+    DELTA_OPT_PREFETCH_WAVES = 5      /* 1 + distance, in waves of resident tiles, of the L2 bulk
+                                         prefetch issued by the default compare kernel (1 = off) */
 };
 
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */

@@ -90,6 +90,7 @@ struct delta_ctx {
 
     // ---- launch options
     int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scatter_ctas_per_sm = 2, scan_kernel = 0;
+    int prefetch_waves = 0;  // K1 L2 prefetch distance in waves of resident tiles (0 = off)
 
     // ---- optional per-kernel event timing
     bool profiling = false;
@@ -198,6 +199,7 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     else if (option == DELTA_OPT_EMIT_CTAS_PER_SM) c->emit_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_SCAN_KERNEL) c->scan_kernel = (int)value - 1;
     else if (option == DELTA_OPT_SCATTER_CTAS_PER_SM) c->scatter_ctas_per_sm = (int)value;
+    else if (option == DELTA_OPT_PREFETCH_WAVES) c->prefetch_waves = (int)value - 1;
     else return DELTA_EINVAL;
     return DELTA_OK;
 }
@@ -369,6 +371,7 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.persist_ctas = ctx->sm_count * ctx->emit_ctas_per_sm;
     a.sm_count = ctx->sm_count;
     a.scan_kernel = ctx->scan_kernel;
+    a.prefetch_dist = (uint32_t)(ctx->prefetch_waves * ctx->sm_count * 3);  // 3 resident CTAs per SM
     return a;
 }
 

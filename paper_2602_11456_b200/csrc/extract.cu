@@ -120,7 +120,8 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 // ------------------------------------------------------------------------------ K1
 template <int W>
 __global__ void __launch_bounds__(kScanThreads, 3)
-k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
+k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
+             uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
     using LT = typename LaneOf<W>::T;
@@ -135,6 +136,18 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__r
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x;
+    // L2 prefetch of a tile about prefetch_dist tiles ahead (CTAs run roughly in blockIdx
+    // order): the TMA engine keeps DRAM streaming while this CTA's loads hit L2.
+    if (prefetch_dist && tid == 0 && t + prefetch_dist < ntiles) {
+        const TileDesc p = tiles[t + prefetch_dist];
+        if (p.flags_tensor & kTileAligned) {
+            const uint32_t bytes = (p.nlanes * W) & ~15u;
+            if (bytes) {
+                bulk_prefetch_l2(p.old_p, bytes);
+                bulk_prefetch_l2(p.new_p, bytes);
+            }
+        }
+    }
     const TileDesc d = tiles[t];
     const uint32_t nl = d.nlanes;
 
@@ -839,8 +852,9 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
         k_scan_runs<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
                                                             static_cast<LT *>(a.slot_val), a.meta, a.summary);
     } else {
-        k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
-                                                             static_cast<LT *>(a.slot_val), a.meta, a.summary);
+        k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
+                                                             a.slot_bytes, static_cast<LT *>(a.slot_val),
+                                                             a.meta, a.summary);
     }
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;

@@ -108,7 +108,8 @@ struct ExtractArgs {
     int width;                        // 2 or 4
     int persist_ctas;                 // grid for grid-stride kernels
     int sm_count;
-    int scan_kernel;                  // 0: one CTA per tile; 1: persistent TMA pipeline
+    int scan_kernel;                  // 0: one CTA per tile; 1: persistent TMA pipeline; 2: runs
+    uint32_t prefetch_dist;           // K1 (0): L2 bulk prefetch distance in tiles (0 = off)
 };
 
 // ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1,
