@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--apply-ctas", type=int, default=0, help="apply kernels' CTAs per SM (0 = default)")
     p.add_argument("--scatter-ctas", type=int, default=0, help="scatter kernel CTAs per SM (0 = default)")
     p.add_argument("--prefetch-waves", type=int, default=0, help="K1 L2 prefetch distance in waves + 1 (0 = default)")
+    p.add_argument("--scatter-order", type=int, default=0, help="1 thread-major, 2 entry-major (0 = default)")
     p.add_argument("--scan-kernel", type=int, default=0,
                    help="1 = one CTA per tile, 2 = persistent TMA pipeline (0 = library default)")
     p.add_argument("--tensors", type=int, default=0,
@@ -316,6 +317,8 @@ def main():
             ctx.set_option(4, args.scatter_ctas)
         if args.prefetch_waves:
             ctx.set_option(5, args.prefetch_waves)
+        if args.scatter_order:
+            ctx.set_option(6, args.scatter_order)
         ctx.set_profiling(True)
         size0 = ctx.delta_size(tl)
         out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)

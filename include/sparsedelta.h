@@ -217,8 +217,10 @@ enum {
                                         vectors (default); 2 = persistent, TMA bulk-copy pipelined;
                                         3 = one CTA per tile, 128-byte runs per thread */
     DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 2) */
-    DELTA_OPT_PREFETCH_WAVES = 5      /* 1 + distance, in waves of resident tiles, of the L2 bulk
+    DELTA_OPT_PREFETCH_WAVES = 5,     /* 1 + distance, in waves of resident tiles, of the L2 bulk
                                          prefetch issued by the default compare kernel (1 = off) */
+    DELTA_OPT_SCATTER_ORDER = 6       /* 1 = each thread stores the entries it decoded (default),
+                                         2 = entry-major: thread i stores entries i, i+256, ... */
 };
 
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */

@@ -91,6 +91,7 @@ struct delta_ctx {
     // ---- launch options
     int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scatter_ctas_per_sm = 2, scan_kernel = 0;
     int prefetch_waves = 0;  // K1 L2 prefetch distance in waves of resident tiles (0 = off)
+    bool entry_major = false;
 
     // ---- optional per-kernel event timing
     bool profiling = false;
@@ -200,6 +201,7 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     else if (option == DELTA_OPT_SCAN_KERNEL) c->scan_kernel = (int)value - 1;
     else if (option == DELTA_OPT_SCATTER_CTAS_PER_SM) c->scatter_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_PREFETCH_WAVES) c->prefetch_waves = (int)value - 1;
+    else if (option == DELTA_OPT_SCATTER_ORDER) c->entry_major = value == 2;
     else return DELTA_EINVAL;
     return DELTA_OK;
 }
@@ -579,6 +581,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.width = w;
     a.persist_ctas = ctx->sm_count * ctx->apply_ctas_per_sm;
     a.scatter_ctas = ctx->sm_count * ctx->scatter_ctas_per_sm;
+    a.entry_major = ctx->entry_major;
     CK(launch_apply(a, s, ctx->profiling ? ctx->ev_apply : nullptr), "apply launch");
     return DELTA_OK;
 }

@@ -355,7 +355,7 @@ k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long 
 // ------------------------------------------------------------------------------ A4
 // Gated scatter-store: decode again, absolute index = chunk base + running gap sum, value
 // from the chunk's slice of the record's value array (staged in shared memory).
-template <int W>
+template <int W, bool ENTRY_MAJOR>
 __global__ void __launch_bounds__(256)
 k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
           const unsigned long long *__restrict__ rcb, const unsigned int *__restrict__ chunk_count,
@@ -372,6 +372,9 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     __shared__ __align__(16) uint8_t svb[kByteChunk * W + 32];  // at most one varint per byte
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
+    // entry-major order: absolute indices of the chunk's entries by ordinal, then the
+    // stores are issued entry i by thread i mod 256 (a warp covers 32 consecutive entries)
+    __shared__ unsigned long long s_idx[ENTRY_MAJOR ? kByteChunk : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = record_of_chunk(rcb, n, c);
@@ -404,14 +407,24 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         uint32_t ord = cpre + ci - cnt;
         unsigned long long idx = idx_base[c] + spre + si - sum;
         LT *w = reinterpret_cast<LT *>(R.w);
-        decode_thread(v, [&](unsigned long long x) {
-            idx += x;
-            LT val;
-            if constexpr (W == 2) val = (LT)(vals[2 * ord] | (vals[2 * ord + 1] << 8));
-            else val = (LT)vals[4 * ord] | ((LT)vals[4 * ord + 1] << 8) | ((LT)vals[4 * ord + 2] << 16) | ((LT)vals[4 * ord + 3] << 24);
-            w[idx] = val;
-            ++ord;
-        });
+        auto value = [&](uint32_t o) -> LT {
+            if constexpr (W == 2) return (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
+            else return (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) | ((LT)vals[4 * o + 3] << 24);
+        };
+        if constexpr (ENTRY_MAJOR) {
+            decode_thread(v, [&](unsigned long long x) {
+                idx += x;
+                s_idx[ord++] = idx;
+            });
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) w[s_idx[i]] = value(i);
+        } else {
+            decode_thread(v, [&](unsigned long long x) {
+                idx += x;
+                w[idx] = value(ord);
+                ++ord;
+            });
+        }
         __syncthreads();
     }
 }
@@ -429,12 +442,16 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     k_apply_scan<<<nb, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[3], s);
-    if (a.width == 2)
-        k_scatter<2><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
-                                                    a.chunk_ord_base, a.chunk_idx_base, a.state);
-    else
-        k_scatter<4><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count,
-                                                    a.chunk_ord_base, a.chunk_idx_base, a.state);
+#define SCATTER(WW, EM)                                                                                 \
+    k_scatter<WW, EM><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count, \
+                                                     a.chunk_ord_base, a.chunk_idx_base, a.state)
+    if (a.width == 2) {
+        if (a.entry_major) SCATTER(2, true);
+        else SCATTER(2, false);
+    } else {
+        SCATTER(4, false);  // entry-major's index staging would exceed 48 KB static smem at W = 4
+    }
+#undef SCATTER
     if (ev) cudaEventRecord(ev[4], s);
     return cudaGetLastError();
 }

@@ -135,6 +135,7 @@ struct ApplyArgs {
     int width;
     int persist_ctas;
     int scatter_ctas;
+    bool entry_major;                 // scatter store order (see k_scatter)
 };
 
 // ev: nullptr, or 5 events: before A1, after A1, A2, A3, A4.

@@ -428,3 +428,21 @@ def test_scan_kernel_variants_parity(sd, dtype, kernel):
     tensors.append(("unaligned", [o[1:40_000], o[40_000:]], [w[1:40_000], w[40_000:]]))
     _roundtrip(sd, tensors, ctx=ctx)
     ctx.close()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("scatter_ctas", [1, 8])
+def test_scatter_launch_options_parity(sd, order, scatter_ctas):
+    """Scatter store order (thread-major / entry-major) and grid size change only speed."""
+    from paper_2602_11456_b200 import _abi
+    ctx = sd.DeltaContext(DEV)
+    ctx.set_option(_abi.DELTA_OPT_SCATTER_ORDER, order)
+    ctx.set_option(_abi.DELTA_OPT_SCATTER_CTAS_PER_SM, scatter_ctas)
+    ctx.set_option(_abi.DELTA_OPT_PREFETCH_WAVES, 3)
+    tensors = []
+    for k, (n, rho) in enumerate([(16_777_216, 0.01), (100_003, 0.9), (5, 1.0), (0, 0.0), (70_000, 0.0005)]):
+        spec = TensorSpec(f"s{k}", (n,), "matrix")
+        o, w = generate_pair(spec, k, 8, rho=rho, device=DEV, values="bits")
+        tensors.append((spec.name, o, w))
+    _roundtrip(sd, tensors, ctx=ctx)
+    ctx.close()
