@@ -60,7 +60,7 @@ def parse():
                    help="G > 1: extract and apply in G pipelined groups on two streams")
     p.add_argument("--apply-ctas", type=int, default=0, help="apply kernels' CTAs per SM (0 = default)")
     p.add_argument("--scatter-ctas", type=int, default=0, help="scatter kernel CTAs per SM (0 = default)")
-    p.add_argument("--prefetch-waves", type=int, default=0, help="K1 L2 prefetch distance in waves + 1 (0 = default)")
+    p.add_argument("--prefetch-tiles", type=int, default=0, help="K1 L2 prefetch distance in tiles + 1 (0 = default)")
     p.add_argument("--scatter-order", type=int, default=0, help="1 thread-major, 2 entry-major (0 = default)")
     p.add_argument("--scan-kernel", type=int, default=0,
                    help="1 = one CTA per tile, 2 = persistent TMA pipeline (0 = library default)")
@@ -315,8 +315,8 @@ def main():
             ctx.set_option(3, args.scan_kernel)
         if args.scatter_ctas:
             ctx.set_option(4, args.scatter_ctas)
-        if args.prefetch_waves:
-            ctx.set_option(5, args.prefetch_waves)
+        if args.prefetch_tiles:
+            ctx.set_option(5, args.prefetch_tiles)
         if args.scatter_order:
             ctx.set_option(6, args.scatter_order)
         ctx.set_profiling(True)

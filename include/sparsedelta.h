@@ -216,11 +216,13 @@ enum {
     DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
                                         vectors (default); 2 = persistent, TMA bulk-copy pipelined;
                                         3 = one CTA per tile, 128-byte runs per thread */
-    DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 2) */
-    DELTA_OPT_PREFETCH_WAVES = 5,     /* 1 + distance, in waves of resident tiles, of the L2 bulk
-                                         prefetch issued by the default compare kernel (1 = off) */
-    DELTA_OPT_SCATTER_ORDER = 6       /* 1 = each thread stores the entries it decoded (default),
-                                         2 = entry-major: thread i stores entries i, i+256, ... */
+    DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 8) */
+    DELTA_OPT_PREFETCH_TILES = 5,     /* 1 + distance, in tiles, of the L2 bulk prefetch issued by
+                                         the default compare kernel (1 = off; default: one wave of
+                                         resident tiles, 3 x SMs) */
+    DELTA_OPT_SCATTER_ORDER = 6       /* 1 = each thread stores the entries it decoded,
+                                         2 = entry-major: thread i stores entries i, i+256, ...
+                                         (default for 16-bit lanes) */
 };
 
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */

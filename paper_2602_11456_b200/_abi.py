@@ -26,7 +26,7 @@ EXPORTS = ("delta_ctx_create", "delta_ctx_destroy", "delta_last_error", "delta_l
            "delta_version", "delta_size", "delta_extract", "delta_apply", "delta_set_profiling",
            "delta_last_timing", "delta_apply_async", "delta_apply_wait", "delta_set_option")
 DELTA_OPT_APPLY_CTAS_PER_SM, DELTA_OPT_EMIT_CTAS_PER_SM, DELTA_OPT_SCAN_KERNEL = 1, 2, 3
-DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_WAVES, DELTA_OPT_SCATTER_ORDER = 4, 5, 6
+DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER = 4, 5, 6
 
 
 class Span(ctypes.Structure):

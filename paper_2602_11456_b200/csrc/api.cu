@@ -89,9 +89,9 @@ struct delta_ctx {
     int ring_next = 0;
 
     // ---- launch options
-    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scatter_ctas_per_sm = 2, scan_kernel = 0;
-    int prefetch_waves = 0;  // K1 L2 prefetch distance in waves of resident tiles (0 = off)
-    bool entry_major = false;
+    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scatter_ctas_per_sm = 8, scan_kernel = 0;
+    int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
+    bool entry_major = true;
 
     // ---- optional per-kernel event timing
     bool profiling = false;
@@ -195,12 +195,12 @@ const char *delta_last_error(const delta_ctx *c) { return c ? c->err.c_str() : "
 int delta_last_detail(const delta_ctx *c) { return c ? c->detail : DELTA_D_NONE; }
 
 int delta_set_option(delta_ctx *c, int option, int64_t value) {
-    if (!c || value < 1 || value > 64) return DELTA_EINVAL;
+    if (!c || value < 1 || value > (1 << 20)) return DELTA_EINVAL;
     if (option == DELTA_OPT_APPLY_CTAS_PER_SM) c->apply_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_EMIT_CTAS_PER_SM) c->emit_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_SCAN_KERNEL) c->scan_kernel = (int)value - 1;
     else if (option == DELTA_OPT_SCATTER_CTAS_PER_SM) c->scatter_ctas_per_sm = (int)value;
-    else if (option == DELTA_OPT_PREFETCH_WAVES) c->prefetch_waves = (int)value - 1;
+    else if (option == DELTA_OPT_PREFETCH_TILES) c->prefetch_tiles = (int)value - 1;
     else if (option == DELTA_OPT_SCATTER_ORDER) c->entry_major = value == 2;
     else return DELTA_EINVAL;
     return DELTA_OK;
@@ -373,7 +373,7 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.persist_ctas = ctx->sm_count * ctx->emit_ctas_per_sm;
     a.sm_count = ctx->sm_count;
     a.scan_kernel = ctx->scan_kernel;
-    a.prefetch_dist = (uint32_t)(ctx->prefetch_waves * ctx->sm_count * 3);  // 3 resident CTAs per SM
+    a.prefetch_dist = (uint32_t)(ctx->prefetch_tiles < 0 ? ctx->sm_count * 3 : ctx->prefetch_tiles);
     return a;
 }
 

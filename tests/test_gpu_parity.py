@@ -438,7 +438,7 @@ def test_scatter_launch_options_parity(sd, order, scatter_ctas):
     ctx = sd.DeltaContext(DEV)
     ctx.set_option(_abi.DELTA_OPT_SCATTER_ORDER, order)
     ctx.set_option(_abi.DELTA_OPT_SCATTER_CTAS_PER_SM, scatter_ctas)
-    ctx.set_option(_abi.DELTA_OPT_PREFETCH_WAVES, 3)
+    ctx.set_option(_abi.DELTA_OPT_PREFETCH_TILES, 1000)
     tensors = []
     for k, (n, rho) in enumerate([(16_777_216, 0.01), (100_003, 0.9), (5, 1.0), (0, 0.0), (70_000, 0.0005)]):
         spec = TensorSpec(f"s{k}", (n,), "matrix")
