@@ -343,13 +343,6 @@ def main():
 
     for _ in range(max(args.warmup, 0)):
         body, table = step()
-    # correctness guard on the timed configuration: apply(extract(old,new)) == new
-    ok = all(torch.equal(t.view(torch.int16 if width == 2 else torch.int32),
-                         w.view(torch.int16 if width == 2 else torch.int32))
-             for t, w in zip(targets, news))
-    if not ok:
-        raise SystemExit("bench: round trip mismatch")
-
     clocks = Clocks(local, enabled=not args.no_clocks)
     acc = {}
     clocks.start()
@@ -368,6 +361,12 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop(w0, w1)
+    # correctness guard on the timed configuration: apply(extract(old,new)) == new
+    ok = all(torch.equal(t.view(torch.int16 if width == 2 else torch.int32),
+                         w.view(torch.int16 if width == 2 else torch.int32))
+             for t, w in zip(targets, news))
+    if not ok:
+        raise SystemExit("bench: round trip mismatch")
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)

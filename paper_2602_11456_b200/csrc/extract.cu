@@ -64,14 +64,20 @@ __device__ __forceinline__ void set_lane(uint4 &v, int j, uint32_t x) {
 }
 
 // Bit j set iff lane j of the two vectors differs as an unsigned integer (reading R2).
+// 16-bit lanes without compares: for x = a ^ b, ((x & 0x7FFF7FFF) + 0x7FFF7FFF) | x has
+// bit 15 (31) set iff the low (high) half of x is nonzero; PRMT gathers those bytes and a
+// multiply packs their top bits into lane order.
 template <int W>
 __device__ __forceinline__ uint32_t diff_mask(const uint4 &a, const uint4 &b) {
     const uint32_t x0 = a.x ^ b.x, x1 = a.y ^ b.y, x2 = a.z ^ b.z, x3 = a.w ^ b.w;
     if constexpr (W == 2) {
-        return (uint32_t)((x0 & 0xFFFFu) != 0) | ((uint32_t)((x0 >> 16) != 0) << 1) |
-               ((uint32_t)((x1 & 0xFFFFu) != 0) << 2) | ((uint32_t)((x1 >> 16) != 0) << 3) |
-               ((uint32_t)((x2 & 0xFFFFu) != 0) << 4) | ((uint32_t)((x2 >> 16) != 0) << 5) |
-               ((uint32_t)((x3 & 0xFFFFu) != 0) << 6) | ((uint32_t)((x3 >> 16) != 0) << 7);
+        const uint32_t f0 = ((x0 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x0;
+        const uint32_t f1 = ((x1 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x1;
+        const uint32_t f2 = ((x2 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x2;
+        const uint32_t f3 = ((x3 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x3;
+        const uint32_t u = (__byte_perm(f0, f1, 0x7531) >> 7) & 0x01010101u;  // lanes 0..3
+        const uint32_t v = (__byte_perm(f2, f3, 0x7531) >> 7) & 0x01010101u;  // lanes 4..7
+        return ((u * 0x01020408u) >> 24) | (((v * 0x01020408u) >> 20) & 0xF0u);
     } else {
         return (uint32_t)(x0 != 0) | ((uint32_t)(x1 != 0) << 1) | ((uint32_t)(x2 != 0) << 2) |
                ((uint32_t)(x3 != 0) << 3);
@@ -132,22 +138,13 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);  // LANES
     __shared__ uint32_t s_warp[kScanThreads / 32][4];
+    __shared__ uint32_t s_pre[kScanThreads / 32][4];
+    __shared__ uint32_t s_tot[4];
     __shared__ uint32_t s_red[kScanThreads / 32];
+    static_assert(kScanThreads / 32 * 4 == 32, "warp-0 scan covers 8 warps x 4 words");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x;
-    // L2 prefetch of a tile about prefetch_dist tiles ahead (CTAs run roughly in blockIdx
-    // order): the TMA engine keeps DRAM streaming while this CTA's loads hit L2.
-    if (prefetch_dist && tid == 0 && t + prefetch_dist < ntiles) {
-        const TileDesc p = tiles[t + prefetch_dist];
-        if (p.flags_tensor & kTileAligned) {
-            const uint32_t bytes = (p.nlanes * W) & ~15u;
-            if (bytes) {
-                bulk_prefetch_l2(p.old_p, bytes);
-                bulk_prefetch_l2(p.new_p, bytes);
-            }
-        }
-    }
     const TileDesc d = tiles[t];
     const uint32_t nl = d.nlanes;
 
@@ -183,6 +180,19 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         }
     }
 
+    // (after this tile's loads are in flight) L2 prefetch of a tile about prefetch_dist tiles ahead (CTAs run roughly in blockIdx
+    // order): the TMA engine keeps DRAM streaming while this CTA's loads hit L2.
+    if (prefetch_dist && tid == 0 && t + prefetch_dist < ntiles) {
+        const TileDesc p = tiles[t + prefetch_dist];
+        if (p.flags_tensor & kTileAligned) {
+            const uint32_t bytes = (p.nlanes * W) & ~15u;
+            if (bytes) {
+                bulk_prefetch_l2(p.old_p, bytes);
+                bulk_prefetch_l2(p.new_p, bytes);
+            }
+        }
+    }
+
     // Per-vector change masks; 8 counts (<= LPV each) packed as 16-bit fields into 4 words
     // so one block scan yields every vector's rank base.
     uint32_t m[kScanVecs];
@@ -199,15 +209,24 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         for (int q = 0; q < 4; ++q) s_warp[warp][q] = inc[q];
     }
     __syncthreads();
-    uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
+    // warp 0 scans the 8 x 4 warp totals across warps (lane = 4 * warp + word)
+    if (warp == 0) {
+        const uint32_t x = s_warp[lane >> 2][lane & 3];
+        uint32_t y = x;
 #pragma unroll
-    for (int w = 0; w < kScanThreads / 32; ++w) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t x = s_warp[w][q];
-            if (w < warp) pre[q] += x;
-            tot[q] += x;
+        for (int o = 4; o < 32; o <<= 1) {
+            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
         }
+        s_pre[lane >> 2][lane & 3] = y - x;
+        if (lane >= 28) s_tot[lane & 3] = y;
+    }
+    __syncthreads();
+    uint32_t pre[4], tot[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        pre[q] = s_pre[warp][q];
+        tot[q] = s_tot[q];
     }
     uint32_t c = 0;
 #pragma unroll
