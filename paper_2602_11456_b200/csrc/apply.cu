@@ -210,11 +210,74 @@ __device__ __forceinline__ void decode_thread(const ChunkView &v, F &&f) {
 //   a 0x00 byte ending a multi-byte varint                -> overlong
 //   a lone 0x00 byte (gap 0) that is not the record's first -> non-increasing
 // Indices >= N are caught by A3 (last index = total sum, gaps >= 1).
+// Bit 7 of byte i of the result is set iff byte i of w is nonzero (exact, no borrows).
+__device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
+    return (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
+}
+
+// The top bits of the four bytes of x (bits 7, 15, 23, 31) as a 4-bit value.
+__device__ __forceinline__ uint32_t gather_top_bits(uint32_t x) {
+    return (((x >> 7) & 0x01010101u) * 0x01020408u) >> 24;
+}
+
+// A 4-bit mask expanded to a byte mask (0xFF in byte i iff bit i).
+__device__ __forceinline__ uint32_t expand_nibble(uint32_t nib) {
+    return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+
+// Fast path of validate_thread for a full 16-byte window whose varints are all 1-3 bytes
+// long and contain no 0x00 byte (the common case at any density): the terminator mask
+// (MSB clear) gives every byte's position d in its varint, and the sum of the window's
+// varint values is sum_d 128^d * (sum of the payloads at position d), three byte-masked
+// dot products.  Returns false if the window needs the byte loop.
+__device__ __forceinline__ bool validate_fast(const ChunkView &v, int p0, uint32_t &cnt,
+                                              unsigned long long &sum) {
+    int c_in = 0;  // continuation bytes of a varint that started before p0
+    while (c_in < 3 && (long long)v.cs + p0 - c_in > 0 && (v.b[p0 - c_in - 1] & 0x80)) ++c_in;
+    if (c_in >= 3) return false;
+    const uint8_t *ptr = v.b + p0;
+    const uint32_t *a4 = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(ptr) & ~uintptr_t(3));
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(ptr) & 3) * 8;
+    uint32_t W[5], w[4];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) W[j] = a4[j];
+    uint32_t T = 0, Z = 0;  // terminator / zero-byte masks, bit i = byte i of the window
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        w[k] = sh ? __funnelshift_r(W[k], W[k + 1], sh) : W[k];
+        T |= gather_top_bits(~w[k] & 0x80808080u) << (4 * k);
+        Z |= gather_top_bits(~nonzero_bytes(w[k]) & 0x80808080u) << (4 * k);
+    }
+    if (T == 0) return true;  // no varint ends in this window (a long one is its owner's concern)
+    const uint32_t valid = (2u << (31 - __clz(T))) - 1u;  // bytes up to the last terminator
+    // E: terminator flags at positions -3..15 (bits 0..18); positions before p0 from c_in
+    const uint32_t E = (T << 3) | (0x7u & ((1u << (3 - c_in)) - 1u));
+    const uint32_t D0 = (E >> 2) & valid;
+    const uint32_t D1 = ~(E >> 2) & (E >> 1) & valid;
+    const uint32_t D2 = ~(E >> 2) & ~(E >> 1) & E & valid;
+    if ((~(E >> 2) & ~(E >> 1) & ~E & valid) || (Z & valid)) return false;
+    uint32_t s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t pw = w[k] & 0x7F7F7F7Fu;
+        s0 = __dp4a(pw & expand_nibble((D0 >> (4 * k)) & 0xF), 0x01010101u, s0);
+        s1 = __dp4a(pw & expand_nibble((D1 >> (4 * k)) & 0xF), 0x01010101u, s1);
+        s2 = __dp4a(pw & expand_nibble((D2 >> (4 * k)) & 0xF), 0x01010101u, s2);
+    }
+    uint32_t carry = 0;  // low bits of the straddling varint, from the bytes before p0
+    if (c_in == 1) carry = v.b[p0 - 1] & 0x7F;
+    else if (c_in == 2) carry = (v.b[p0 - 2] & 0x7F) | ((uint32_t)(v.b[p0 - 1] & 0x7F) << 7);
+    cnt += __popc(T);
+    sum = sat_add(sum, (unsigned long long)carry + s0 + (s1 << 7) + (s2 << 14));
+    return true;
+}
+
 __device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cnt,
                                                 unsigned long long &sum, uint32_t &err) {
     const int p0 = threadIdx.x * 16;
     const int p1 = min(p0 + 16, (int)v.len);
     if (p0 >= p1) return;
+    if (p1 - p0 == 16 && validate_fast(v, p0, cnt, sum)) return;
     bool longrun;
     const int q = varint_start(v, p0, longrun);
     bool first = ((long long)v.cs + q == 0);

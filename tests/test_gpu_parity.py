@@ -446,3 +446,23 @@ def test_scatter_launch_options_parity(sd, order, scatter_ctas):
         tensors.append((spec.name, o, w))
     _roundtrip(sd, tensors, ctx=ctx)
     ctx.close()
+
+
+def test_mixed_varint_lengths(sd):
+    """Index streams mixing 1-, 2-, 3- and 4-byte gaps at every alignment (exercises the
+    bit-parallel decode fast path and its byte-loop fallback at window boundaries)."""
+    rng = np.random.default_rng(77)
+    n = 1 << 26
+    gaps, pos, cur = [], [], 0
+    while True:
+        kind = rng.choice([1, 1, 1, 2, 2, 3, 4], p=[0.3, 0.2, 0.1, 0.15, 0.1, 0.1, 0.05])
+        g = {1: int(rng.integers(1, 128)), 2: int(rng.integers(128, 16384)),
+             3: int(rng.integers(16384, 2**21)), 4: int(rng.integers(2**21, 2**22))}[kind]
+        if cur + g >= n:
+            break
+        cur += g
+        pos.append(cur)
+    pos = [0] + pos  # first index 0 (a 0x00 first varint)
+    old, new = _with_changes(n, pos)
+    body, table = _roundtrip(sd, [("mixed", old, new)])
+    assert table[0][2] == len(pos)
