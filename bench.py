@@ -286,12 +286,18 @@ def main():
     root_out = None
     stream = torch.cuda.current_stream()
 
+    comm = torch.cuda.Stream(dev) if world > 1 else None
+
     def assemble(size, body):
+        """S2+S3 on a side stream: the NVLink transfer of the body to rank 0 overlaps this
+        rank's apply (which needs no collective); the step ends when both are done."""
         nonlocal root_out
-        sizes, off, tot = sdist.gather_sizes(size, dev)
-        if rank == 0 and (root_out is None or root_out.numel() < tot):
-            root_out = torch.empty(tot + tot // 8, dtype=torch.uint8, device=dev)
-        sdist.assemble(body, sizes, root_out)
+        comm.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(comm):
+            sizes, off, tot = sdist.gather_sizes(size, dev)
+            if rank == 0 and (root_out is None or root_out.numel() < tot):
+                root_out = torch.empty(tot + tot // 8, dtype=torch.uint8, device=dev)
+            sdist.assemble(body, sizes, root_out)
 
     if args.pipeline > 1:
         from paper_2602_11456_b200.pipeline import RoundTrip
@@ -304,6 +310,7 @@ def main():
             body = rt.step(acc)
             if world > 1:
                 assemble(body.numel(), body)
+                torch.cuda.current_stream().wait_stream(comm)
             return body, rt.table()
     else:
         tl = sd.TensorList(tensors)
@@ -331,6 +338,8 @@ def main():
             if world > 1:
                 assemble(size, body)
             ctx.delta_apply(tg, body, table=table)
+            if world > 1:
+                torch.cuda.current_stream().wait_stream(comm)
             t3 = ctx.last_timing()
             if acc is not None:
                 for kname in ("scan_ms", "lens_ms", "finalize_ms"):

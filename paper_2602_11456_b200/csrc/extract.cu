@@ -124,35 +124,39 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 }
 
 // ------------------------------------------------------------------------------ K1
-template <int W>
-__global__ void __launch_bounds__(kScanThreads, 3)
+// THREADS x VECS = 2048 16-byte vectors per operand per tile (32 KiB); instantiated as
+// 256 x 8 (3 CTAs / SM) and 512 x 4 (2 CTAs / SM, more warps, fewer registers each).
+template <int W, int THREADS, int VECS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
              uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
     using LT = typename LaneOf<W>::T;
-    constexpr int LPV = 16 / W;                            // lanes per 16-byte vector
-    constexpr int LANES = kScanThreads * kScanVecs * LPV;  // lanes per tile
-    static_assert(kScanVecs == 8, "count packing assumes 8 vectors per thread");
+    constexpr int LPV = 16 / W;                  // lanes per 16-byte vector
+    constexpr int LANES = THREADS * VECS * LPV;  // lanes per tile
+    constexpr int NWARP = THREADS / 32;
+    constexpr int NQ = VECS / 2;                 // packed count words (two 16-bit fields each)
+    static_assert(THREADS * VECS * 16 == kTileBytes, "tile geometry is fixed by the plan");
     static_assert(LANES <= 65536, "lane offsets are u16");
+    static_assert(NWARP * NQ == 32, "warp-0 scan covers NWARP warps x NQ words");
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);  // LANES
-    __shared__ uint32_t s_warp[kScanThreads / 32][4];
-    __shared__ uint32_t s_pre[kScanThreads / 32][4];
-    __shared__ uint32_t s_tot[4];
-    __shared__ uint32_t s_red[kScanThreads / 32];
-    static_assert(kScanThreads / 32 * 4 == 32, "warp-0 scan covers 8 warps x 4 words");
+    __shared__ uint32_t s_warp[NWARP][NQ];
+    __shared__ uint32_t s_pre[NWARP][NQ];
+    __shared__ uint32_t s_tot[NQ];
+    __shared__ uint32_t s_red[NWARP];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x;
     const TileDesc d = tiles[t];
     const uint32_t nl = d.nlanes;
 
-    uint4 vo[kScanVecs], vn[kScanVecs];
+    uint4 vo[VECS], vn[VECS];
     if (d.flags_tensor & kTileAligned) {
 #pragma unroll
-        for (int r = 0; r < kScanVecs; ++r) {
-            const uint32_t v = r * kScanThreads + tid;
+        for (int r = 0; r < VECS; ++r) {
+            const uint32_t v = r * THREADS + tid;
             if ((v + 1) * LPV <= nl) {
                 vo[r] = ld_stream_v4(d.old_p + (size_t)v * 16);
                 vn[r] = ld_stream_v4(d.new_p + (size_t)v * 16);
@@ -169,8 +173,8 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         }
     } else {  // span not 16-byte aligned: same lane order, lane-by-lane loads
 #pragma unroll
-        for (int r = 0; r < kScanVecs; ++r) {
-            const uint32_t v = r * kScanThreads + tid;
+        for (int r = 0; r < VECS; ++r) {
+            const uint32_t v = r * THREADS + tid;
             vo[r] = make_uint4(0, 0, 0, 0);
             vn[r] = vo[r];
             for (int j = 0; j < LPV && v * LPV + j < nl; ++j) {
@@ -193,44 +197,44 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         }
     }
 
-    // Per-vector change masks; 8 counts (<= LPV each) packed as 16-bit fields into 4 words
-    // so one block scan yields every vector's rank base.
-    uint32_t m[kScanVecs];
-    uint32_t pk[4];
+    // Per-vector change masks; VECS counts (<= LPV each) packed as 16-bit fields into NQ
+    // words so one block scan yields every vector's rank base.
+    uint32_t m[VECS];
+    uint32_t pk[NQ];
 #pragma unroll
-    for (int r = 0; r < kScanVecs; ++r) m[r] = diff_mask<W>(vo[r], vn[r]);
+    for (int r = 0; r < VECS; ++r) m[r] = diff_mask<W>(vo[r], vn[r]);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
-    uint32_t inc[4];
+    for (int q = 0; q < NQ; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
+    uint32_t inc[NQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) inc[q] = warp_inclusive_sum(pk[q]);
+    for (int q = 0; q < NQ; ++q) inc[q] = warp_inclusive_sum(pk[q]);
     if (lane == 31) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s_warp[warp][q] = inc[q];
+        for (int q = 0; q < NQ; ++q) s_warp[warp][q] = inc[q];
     }
     __syncthreads();
-    // warp 0 scans the 8 x 4 warp totals across warps (lane = 4 * warp + word)
+    // warp 0 scans the NWARP x NQ warp totals across warps (lane = NQ * warp + word)
     if (warp == 0) {
-        const uint32_t x = s_warp[lane >> 2][lane & 3];
+        const uint32_t x = s_warp[lane / NQ][lane % NQ];
         uint32_t y = x;
 #pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
+        for (int o = NQ; o < 32; o <<= 1) {
             const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
             if (lane >= o) y += z;
         }
-        s_pre[lane >> 2][lane & 3] = y - x;
-        if (lane >= 28) s_tot[lane & 3] = y;
+        s_pre[lane / NQ][lane % NQ] = y - x;
+        if (lane >= 32 - NQ) s_tot[lane % NQ] = y;
     }
     __syncthreads();
-    uint32_t pre[4], tot[4];
+    uint32_t pre[NQ], tot[NQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
         pre[q] = s_pre[warp][q];
         tot[q] = s_tot[q];
     }
     uint32_t c = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) c += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
+    for (int q = 0; q < NQ; ++q) c += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
 
     // Ordered compaction: entry (r, tid, j) gets rank sum_{r'<r} tot_r' + prefix_r(tid) +
     // popc(mask below j) — lane order.  Values go straight from registers to the tile's
@@ -239,14 +243,14 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
     LT *sv = slot_val + (size_t)t * slot_cap;
     uint32_t rbase = 0;
 #pragma unroll
-    for (int r = 0; r < kScanVecs; ++r) {
+    for (int r = 0; r < VECS; ++r) {
         const int q = r >> 1, sh = (r & 1) * 16;
         uint32_t pos = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
         uint32_t mm = m[r];
         while (mm) {
             const int j = __ffs(mm) - 1;
             mm &= mm - 1;
-            s_off[pos] = (uint16_t)((r * kScanThreads + tid) * LPV + j);
+            s_off[pos] = (uint16_t)((r * THREADS + tid) * LPV + j);
             if (fits) sv[pos] = (LT)lane_of<W>(vn[r], j);
             ++pos;
         }
@@ -266,12 +270,12 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
     // < 2^14 lanes, so 1 or 2 bytes), encoded in order; the first change's gap depends on
     // earlier tiles and is written by K4.
     uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
-    const uint32_t q = (c + kScanThreads - 1) / kScanThreads;  // contiguous entries per thread
+    const uint32_t q = (c + THREADS - 1) / THREADS;  // contiguous entries per thread
     const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
     uint32_t L = 0;
     for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) L += 1u + ((s_off[i] - s_off[i - 1]) >= 128u);
     uint32_t tl;
-    uint32_t pos = block_excl_scan<kScanThreads / 32, uint32_t>(L, s_red, tl);
+    uint32_t pos = block_excl_scan<NWARP, uint32_t>(L, s_red, tl);
     for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) {
         const uint32_t g = s_off[i] - s_off[i - 1];
         if (g < 128u) {
@@ -857,7 +861,8 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     using LT = typename LaneOf<W>::T;
     constexpr int LANES = kScanThreads * kScanVecs * (16 / W);
     const size_t smem = (size_t)LANES * sizeof(uint16_t);
-    cudaFuncSetAttribute(k_scan_tiles<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tiles<W, 512, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
     if (a.scan_kernel == 1) {
         constexpr int STAGES = 3;
@@ -871,9 +876,14 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
         k_scan_runs<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
                                                             static_cast<LT *>(a.slot_val), a.meta, a.summary);
     } else {
-        k_scan_tiles<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
-                                                             a.slot_bytes, static_cast<LT *>(a.slot_val),
-                                                             a.meta, a.summary);
+        if (a.scan_kernel == 3)
+            k_scan_tiles<W, 512, 4, 2><<<a.ntiles, 512, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
+                                                                   a.slot_bytes, static_cast<LT *>(a.slot_val),
+                                                                   a.meta, a.summary);
+        else
+            k_scan_tiles<W, 256, 8, 3><<<a.ntiles, 256, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
+                                                                   a.slot_bytes, static_cast<LT *>(a.slot_val),
+                                                                   a.meta, a.summary);
     }
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
