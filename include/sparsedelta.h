@@ -189,6 +189,18 @@ int delta_apply_async(delta_ctx *ctx, const delta_target *targets, uint32_t n, i
                       const void *body_dev, uint64_t body_bytes,
                       const delta_record_info *table_hint, void *stream);
 
+/* delta_apply_async_dev — delta_apply_async with the table hint in DEVICE memory (same
+ * layout as delta_record_info, n rows), e.g. delta_table_dev() of the context that
+ * extracted the body, so no host round trip is needed between extract and apply.  The
+ * hint must stay valid until the stream work is done; it is verified like the host hint. */
+int delta_apply_async_dev(delta_ctx *ctx, const delta_target *targets, uint32_t n, int elem,
+                          const void *body_dev, uint64_t body_bytes,
+                          const delta_record_info *table_hint_dev, void *stream);
+
+/* Device address of the offset table written by the last delta_size/delta_extract on ctx
+ * (n rows; NULL if none).  Valid until the next extract call on ctx. */
+const delta_record_info *delta_table_dev(const delta_ctx *ctx);
+
 /* delta_apply_wait — synchronise `stream` and return the first device-side error of the
  * delta_apply_async calls since the previous wait (DELTA_OK if none), then clear it. */
 int delta_apply_wait(delta_ctx *ctx, void *stream);

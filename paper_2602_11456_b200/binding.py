@@ -50,6 +50,19 @@ class Table:
         return list(self) == list(other)
 
 
+class DeviceTable:
+    """The offset table of the last extract on ``ctx``, left in device memory (no host
+    round trip); valid until the next extract on that context.  Pass it to delta_apply."""
+
+    __slots__ = ("ptr", "n", "ctx")
+
+    def __init__(self, ptr, n, ctx):
+        self.ptr, self.n, self.ctx = ptr, n, ctx
+
+    def __len__(self):
+        return self.n
+
+
 class DeltaError(RuntimeError):
     """A non-OK status from the library; ``status``/``detail`` are the C codes and
     ``kind`` the DELTA_D_* name (e.g. "truncated", "name") when there is one."""
@@ -206,12 +219,13 @@ class DeltaContext:
 
     def delta_extract(self, tensors, out=None, stream=None, table=True):
         """Pack the delta.  Returns ``(body, table)``: ``body`` a uint8 CUDA tensor view of
-        exactly the body bytes (``out``'s prefix if ``out`` is given), ``table`` a Table of
-        offset-table rows (TABLE_FIELDS order) or None if ``table`` is False."""
+        exactly the body bytes (``out``'s prefix if ``out`` is given); ``table``: True -> a
+        host Table of offset-table rows (TABLE_FIELDS order; one extra synchronisation),
+        "device" -> a DeviceTable (no extra synchronisation), False -> None."""
         tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
         st = _stream_handle(stream)
         nbytes = c_uint64()
-        rows = (RecordInfo * max(tl.n, 1))() if table else None
+        rows = (RecordInfo * max(tl.n, 1))() if table is True else None
         if out is None:
             self._check(self._lib.delta_size(self._h, tl.arr, tl.n, _ELEM[tl.width], st, byref(nbytes)))
             out = torch.empty(max(nbytes.value, 1), dtype=torch.uint8, device=tl.device or self.device)
@@ -220,6 +234,8 @@ class DeltaContext:
         self._check(self._lib.delta_extract(self._h, tl.arr, tl.n, _ELEM[tl.width], out.data_ptr(),
                                             out.numel(), rows, st, byref(nbytes)))
         body = out[:nbytes.value]
+        if table == "device":
+            return body, DeviceTable(self._lib.delta_table_dev(self._h), tl.n, self)
         if rows is None:
             return body, None
         return body, Table(rows, tl.n)
@@ -232,6 +248,12 @@ class DeltaContext:
         if body.dtype != torch.uint8 or not body.is_contiguous() or not body.is_cuda:
             raise ValueError("body must be a contiguous uint8 CUDA tensor")
         hint = None
+        if isinstance(table, DeviceTable):
+            self._check(self._lib.delta_apply_async_dev(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(),
+                                                        body.numel(), c_void_p(table.ptr), _stream_handle(stream)))
+            if wait:
+                self.apply_wait(stream)
+            return
         if table is not None:
             if isinstance(table, Table):
                 hint = table.arr

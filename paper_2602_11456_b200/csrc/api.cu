@@ -504,7 +504,8 @@ static const char *kDetailName[] = {"ok", "truncated varint", "overlong varint",
                                     "mode byte != 0", "record layout"};
 
 static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem, const void *body,
-                         uint64_t body_bytes, const delta_record_info *hint, cudaStream_t s) {
+                         uint64_t body_bytes, const delta_record_info *hint, cudaStream_t s,
+                         const delta_record_info *hint_dev = nullptr) {
     ctx->err.clear();
     ctx->detail = 0;
     const int w = elem_width(elem);
@@ -570,6 +571,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.n = n;
     a.names = ctx->a_upload.as<uint8_t>() + off_names;
     a.hint = (hint && n) ? reinterpret_cast<const RecordRow *>(ctx->a_upload.as<uint8_t>() + off_hint) : nullptr;
+    if (hint_dev && n) a.hint = reinterpret_cast<const RecordRow *>(hint_dev);
     a.recs = ctx->a_recs.as<ApplyRec>();
     a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
     a.chunk_count = ctx->a_cnt.as<unsigned int>();
@@ -591,6 +593,19 @@ extern "C" int delta_apply_async(delta_ctx *ctx, const delta_target *tg, uint32_
                                  void *stream) {
     if (!ctx) return DELTA_EINVAL;
     return apply_enqueue(ctx, tg, n, elem, body, body_bytes, hint, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int delta_apply_async_dev(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem,
+                                     const void *body, uint64_t body_bytes,
+                                     const delta_record_info *table_hint_dev, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    return apply_enqueue(ctx, tg, n, elem, body, body_bytes, nullptr, static_cast<cudaStream_t>(stream),
+                         table_hint_dev);
+}
+
+extern "C" const delta_record_info *delta_table_dev(const delta_ctx *ctx) {
+    if (!ctx || !ctx->table.p || ctx->ntensors == 0) return nullptr;
+    return static_cast<const delta_record_info *>(ctx->table.p);
 }
 
 extern "C" int delta_apply_wait(delta_ctx *ctx, void *stream) {

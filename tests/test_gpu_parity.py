@@ -42,9 +42,14 @@ def _roundtrip(sd, tensors, ctx=None, check_oracle=True):
         ref_body, ref_table = oracle_extract(tensors)
         assert_body_equal(body, ref_body)
         assert [tuple(r) for r in table] == [tuple(r) for r in ref_table]
-    for use_hint in (True, False):
+    for hint in ("host", "none", "device"):
         targets = [(n, fused(o).clone()) for n, o, _ in tensors]
-        ctx.delta_apply(targets, body, table=table if use_hint else None)
+        if hint == "device":  # the table left on the device by a second extract
+            dbody, dtab = ctx.delta_extract(tensors, table="device")
+            assert torch.equal(dbody, body)
+            ctx.delta_apply(targets, dbody, table=dtab)
+        else:
+            ctx.delta_apply(targets, body, table=table if hint == "host" else None)
         torch.cuda.synchronize()
         for (_, w), (_, _, nw) in zip(targets, tensors):
             assert_lanes_equal(w, fused(nw))
