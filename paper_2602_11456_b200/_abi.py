@@ -86,7 +86,8 @@ def lib():
         L.delta_apply.restype = c_int
         L.delta_apply_async.argtypes = L.delta_apply.argtypes
         L.delta_apply_async.restype = c_int
-        L.delta_apply_async_dev.argtypes = L.delta_apply.argtypes
+        L.delta_apply_async_dev.argtypes = [c_void_p, POINTER(Target), c_uint32, c_int, c_void_p, c_uint64,
+                                            c_void_p, c_void_p]
         L.delta_apply_async_dev.restype = c_int
         L.delta_table_dev.argtypes = [c_void_p]
         L.delta_table_dev.restype = c_void_p

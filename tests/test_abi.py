@@ -52,12 +52,28 @@ def test_no_gpu_fails_loudly(built):
 
 
 def test_null_context_is_einval(built):
-    from ctypes import byref, c_uint64
+    """Every entry point marshals its Python-side argument types and rejects a NULL
+    context without touching a device."""
+    from ctypes import byref, c_uint64, c_void_p
     lib = built.lib()
     n = c_uint64()
-    assert lib.delta_size(None, None, 0, 0, None, byref(n)) == built.DELTA_EINVAL
-    assert lib.delta_apply(None, None, 0, 0, None, 0, None, None) == built.DELTA_EINVAL
+    tl = (built.Tensor * 1)()
+    tg = (built.Target * 1)()
+    rows = (built.RecordInfo * 1)()
+    E = built.DELTA_EINVAL
+    assert lib.delta_size(None, tl, 0, 0, None, byref(n)) == E
+    assert lib.delta_extract(None, tl, 0, 0, None, 0, rows, None, byref(n)) == E
+    assert lib.delta_apply(None, tg, 0, 0, None, 0, rows, None) == E
+    assert lib.delta_apply_async(None, tg, 0, 0, None, 0, rows, None) == E
+    assert lib.delta_apply_async_dev(None, tg, 0, 0, None, 0, c_void_p(0), None) == E
+    assert lib.delta_apply_wait(None, None) == E
+    assert lib.delta_set_option(None, 1, 1) == E
+    assert lib.delta_set_profiling(None, 1) == E
+    assert lib.delta_last_timing(None, byref(built.Timing())) == E
+    assert lib.delta_table_dev(None) is None
+    assert lib.delta_last_detail(None) == 0
     assert lib.delta_last_error(None) == b"no context"
+    assert b"sm_100a" in lib.delta_version()
 
 
 def test_product_never_imports_oracle():
