@@ -126,12 +126,12 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 // ------------------------------------------------------------------------------ K1
 // THREADS x VECS = 2048 16-byte vectors per operand per tile (32 KiB); instantiated as
 // 256 x 8 (3 CTAs / SM) and 512 x 4 (2 CTAs / SM, more warps, fewer registers each).
-template <int W, int THREADS, int VECS, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB)
-k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
-             uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
-             typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
-             ExtractSummary *summary) {
+template <int W, int THREADS, int VECS>
+__device__ __forceinline__ void
+scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
+          uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
+          typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
+          ExtractSummary *summary) {
     using LT = typename LaneOf<W>::T;
     constexpr int LPV = 16 / W;                  // lanes per 16-byte vector
     constexpr int LANES = THREADS * VECS * LPV;  // lanes per tile
@@ -148,7 +148,6 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
     __shared__ uint32_t s_red[NWARP];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t t = blockIdx.x;
     const TileDesc d = tiles[t];
     const uint32_t nl = d.nlanes;
 
@@ -287,6 +286,30 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
     }
     if (tid == 0)
         meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
+}
+
+template <int W, int THREADS, int VECS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
+             uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
+             typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
+             ExtractSummary *summary) {
+    scan_tile<W, THREADS, VECS>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
+                                meta, summary);
+}
+
+// Persistent form: 3 CTAs per SM loop over the tiles (t = CTA, CTA + grid, ...), no
+// per-tile CTA launch.
+template <int W>
+__global__ void __launch_bounds__(256, 3)
+k_scan_tiles_persist(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
+                     uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
+                     typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
+                     ExtractSummary *summary) {
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        scan_tile<W, 256, 8>(t, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val, meta, summary);
+        __syncthreads();  // shared scratch is reused by the next tile
+    }
 }
 
 // ------------------------------------------------------------------------------ K1 (runs)
@@ -876,7 +899,13 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
         k_scan_runs<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
                                                             static_cast<LT *>(a.slot_val), a.meta, a.summary);
     } else {
-        if (a.scan_kernel == 3)
+        if (a.scan_kernel == 4) {
+            cudaFuncSetAttribute(k_scan_tiles_persist<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const uint32_t grid = a.ntiles < 3u * a.sm_count ? a.ntiles : 3u * a.sm_count;
+            k_scan_tiles_persist<W><<<grid, 256, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
+                                                           a.slot_bytes, static_cast<LT *>(a.slot_val),
+                                                           a.meta, a.summary);
+        } else if (a.scan_kernel == 3)
             k_scan_tiles<W, 512, 4, 2><<<a.ntiles, 512, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
                                                                    a.slot_bytes, static_cast<LT *>(a.slot_val),
                                                                    a.meta, a.summary);

@@ -411,7 +411,7 @@ def test_async_apply_error_is_reported_at_wait(sd):
 
 
 # ------------------------------------------------------------------ TMA-pipelined K1
-@pytest.mark.parametrize("kernel", [2, 3, 4])
+@pytest.mark.parametrize("kernel", [2, 3, 4, 5])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_scan_kernel_variants_parity(sd, dtype, kernel):
     """The other compare+compaction kernels (DELTA_OPT_SCAN_KERNEL = 2: persistent, TMA
