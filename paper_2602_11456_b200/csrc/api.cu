@@ -70,14 +70,14 @@ struct delta_ctx {
     unsigned long long total_lanes = 0;
     DevBuf tiles, name_len, name_off, names, numel, tensor_first_tile;
     // ---- extract workspace
-    DevBuf slot_bytes, slot_val, meta, tile_entry, tile_byte, tile_pred, tile_bytes, blk_a, blk_key,
+    DevBuf slot_bytes, slot_val, meta, tile_entry, tile_byte, tile_pred, tile_bytes, tile_plan, blk_a, blk_key,
         entry_begin, tensor_byte_begin, table, summary;
     uint32_t slot_cap = 0;          // entries per tile slot (grows on overflow)
     bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
     ExtractSummary *h_summary = nullptr;  // pinned
 
     // ---- apply workspace
-    DevBuf a_upload, a_recs, a_rcb, a_cnt, a_sum, a_ord, a_idx, a_state;
+    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state;
     ApplyState *h_state = nullptr;  // pinned
     // pinned staging ring for the per-call apply uploads (targets, hint, names): with a
     // pinned source cudaMemcpyAsync does not wait for earlier work on the stream, so
@@ -171,9 +171,9 @@ void delta_ctx_destroy(delta_ctx *c) {
     cudaSetDevice(c->device);
     DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
-                      &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->blk_a,
+                      &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->tile_plan, &c->blk_a,
                       &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
-                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_cnt, &c->a_sum,
+                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
     if (c->profiling) {
@@ -358,6 +358,7 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.tile_byte = ctx->tile_byte.as<unsigned long long>();
     a.tile_pred = ctx->tile_pred.as<unsigned long long>();
     a.tile_bytes_tmp = ctx->tile_bytes.as<unsigned int>();
+    a.plan = ctx->tile_plan.as<TileEmit>();
     a.blk_a = ctx->blk_a.as<unsigned long long>();
     a.blk_key = ctx->blk_key.as<long long>();
     a.tensor_first_tile = ctx->tensor_first_tile.as<uint32_t>();
@@ -395,6 +396,7 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
     GROW(ctx->tile_byte, (size_t)nt * 8);
     GROW(ctx->tile_pred, (size_t)nt * 8);
     GROW(ctx->tile_bytes, (size_t)nt * 4);
+    GROW(ctx->tile_plan, (size_t)nt * sizeof(TileEmit));
     GROW(ctx->blk_a, (size_t)nblk * 2 * 8);
     GROW(ctx->blk_key, (size_t)nblk * 8);
     GROW(ctx->entry_begin, (size_t)(T + 1) * 8);
@@ -541,6 +543,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     }
     const size_t nch = body_bytes / kByteChunk + n + 2;
     GROW(ctx->a_cnt, nch * 4);
+    GROW(ctx->a_crec, nch * 4);
     GROW(ctx->a_sum, nch * 8);
     GROW(ctx->a_ord, nch * 8);
     GROW(ctx->a_idx, nch * 8);
@@ -574,6 +577,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     if (hint_dev && n) a.hint = reinterpret_cast<const RecordRow *>(hint_dev);
     a.recs = ctx->a_recs.as<ApplyRec>();
     a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
+    a.chunk_rec = ctx->a_crec.as<uint32_t>();
     a.chunk_count = ctx->a_cnt.as<unsigned int>();
     a.chunk_sum = ctx->a_sum.as<unsigned long long>();
     a.chunk_ord_base = ctx->a_ord.as<unsigned long long>();

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(256)
 k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
          const TargetDesc *__restrict__ tg, uint32_t n, const uint8_t *__restrict__ names,
          const RecordRow *__restrict__ hint, ApplyRec *__restrict__ recs,
-         unsigned long long *__restrict__ rec_chunk_begin, ApplyState *st, int width) {
+         unsigned long long *__restrict__ rec_chunk_begin, uint32_t *__restrict__ chunk_rec, ApplyState *st,
+         int width) {
     bool ok = hint != nullptr;
     if (hint != nullptr) {
         for (uint32_t k = threadIdx.x; k < n && ok; k += blockDim.x) {
@@ -117,20 +118,18 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
         rec_chunk_begin[n] = acc;
         st->n_chunks = acc;
     }
+    __syncthreads();
+    // chunk -> record map (one load per chunk in A2/A4 instead of a binary search)
+    if (st->status == kOk) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (uint32_t k = warp; k < n; k += blockDim.x >> 5) {
+            const unsigned long long c0 = rec_chunk_begin[k], c1 = rec_chunk_begin[k + 1];
+            for (unsigned long long c = c0 + lane; c < c1; c += 32) chunk_rec[c] = k;
+        }
+    }
 }
 
 // ---------------------------------------------------------------- chunk staging (A2, A4)
-__device__ __forceinline__ uint32_t record_of_chunk(const unsigned long long *rcb, uint32_t n,
-                                                    unsigned long long c) {
-    uint32_t lo = 0, hi = n;  // largest k with rcb[k] <= c; records without chunks are skipped
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(rcb + mid) <= c) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
 struct ChunkView {
     unsigned long long cs;   // chunk start within the record's index stream
     uint32_t len;            // bytes in this chunk
@@ -308,7 +307,8 @@ __device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cn
 // ------------------------------------------------------------------------------ A2
 __global__ void __launch_bounds__(256)
 k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
-               const unsigned long long *__restrict__ rcb, unsigned int *__restrict__ chunk_count,
+               const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
+               unsigned int *__restrict__ chunk_count,
                unsigned long long *__restrict__ chunk_sum, ApplyState *st) {
     if (st->status != kOk) return;
     const unsigned long long nch = st->n_chunks;
@@ -317,7 +317,7 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
     __shared__ unsigned long long s_sum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
-        const uint32_t k = record_of_chunk(rcb, n, c);
+        const uint32_t k = __ldg(chunk_rec + c);
         const ApplyRec R = recs[k];
         const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
         __syncthreads();
@@ -421,7 +421,8 @@ k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long 
 template <int W, bool ENTRY_MAJOR>
 __global__ void __launch_bounds__(256)
 k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
-          const unsigned long long *__restrict__ rcb, const unsigned int *__restrict__ chunk_count,
+          const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
+          const unsigned int *__restrict__ chunk_count,
           const unsigned long long *__restrict__ ord_base, const unsigned long long *__restrict__ idx_base,
           ApplyState *st) {
     using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
@@ -440,7 +441,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     __shared__ unsigned long long s_idx[ENTRY_MAJOR ? kByteChunk : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
-        const uint32_t k = record_of_chunk(rcb, n, c);
+        const uint32_t k = __ldg(chunk_rec + c);
         const ApplyRec R = recs[k];
         const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
         const unsigned long long ob = ord_base[c];
@@ -496,9 +497,9 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
 cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], s);
     k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.targets, a.n, a.names, a.hint, a.recs,
-                               a.rec_chunk_begin, a.state, a.width);
+                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width);
     if (ev) cudaEventRecord(ev[1], s);
-    k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin,
+    k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
                                                   a.chunk_count, a.chunk_sum, a.state);
     if (ev) cudaEventRecord(ev[2], s);
     const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
@@ -506,7 +507,7 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[3], s);
 #define SCATTER(WW, EM)                                                                                 \
-    k_scatter<WW, EM><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_count, \
+    k_scatter<WW, EM><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec, a.chunk_count, \
                                                      a.chunk_ord_base, a.chunk_idx_base, a.state)
     if (a.width == 2) {
         if (a.entry_major) SCATTER(2, true);

@@ -817,28 +817,45 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
     for (uint32_t b = (nw << 2) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
 }
 
+// K3b: per tile, the final body offsets of its index bytes and values and its first gap
+// (one thread per tile; turns K4's chain of dependent loads into one 32-byte load).
+template <int W>
+__global__ void __launch_bounds__(256)
+k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
+                 const unsigned long long *__restrict__ tile_entry, const unsigned long long *__restrict__ tile_byte,
+                 const unsigned long long *__restrict__ tile_pred, const unsigned long long *__restrict__ E,
+                 const unsigned long long *__restrict__ Bk, const RecordRow *__restrict__ table,
+                 TileEmit *__restrict__ plan, const ExtractSummary *summary) {
+    if (summary->overflow) return;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+        const TileMeta m = meta[t];
+        TileEmit e{0, 0, 0, m.count, m.internal_bytes};
+        if (m.count) {
+            const TileDesc d = tiles[t];
+            const uint32_t k = d.flags_tensor & kTileTensorMask;
+            e.ib = table[k].index_offset + (tile_byte[t] - Bk[k]);
+            e.vb = table[k].values_offset + (tile_entry[t] - E[k]) * W;
+            e.g0 = d.lane_base + m.first_off - tile_pred[t];
+        }
+        plan[t] = e;
+    }
+}
+
 // One warp per tile: the LEB128 bytes of the tile's first gap, then the tile's pre-encoded
 // internal gaps and its raw values copied to their final offsets in the body.
 template <int W>
 __global__ void __launch_bounds__(256)
-k_emit_tiles(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
-             uint32_t slot_cap, const uint8_t *__restrict__ slot_bytes,
-             const typename LaneOf<W>::T *__restrict__ slot_val,
-             const unsigned long long *__restrict__ tile_entry, const unsigned long long *__restrict__ tile_byte,
-             const unsigned long long *__restrict__ tile_pred, const unsigned long long *__restrict__ E,
-             const unsigned long long *__restrict__ Bk, const RecordRow *__restrict__ table,
+k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
+             const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out) {
     const int lane = threadIdx.x & 31;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
     for (uint32_t t = wg; t < ntiles; t += nw) {
-        const TileMeta m = meta[t];
-        if (m.count == 0) continue;
-        const TileDesc d = tiles[t];
-        const uint32_t k = d.flags_tensor & kTileTensorMask;
-        uint8_t *ib = out + table[k].index_offset + (tile_byte[t] - Bk[k]);
-        uint8_t *vb = out + table[k].values_offset + (tile_entry[t] - E[k]) * W;
-        unsigned long long g = d.lane_base + m.first_off - tile_pred[t];
+        const TileEmit e = plan[t];
+        if (e.count == 0) continue;
+        uint8_t *ib = out + e.ib;
+        unsigned long long g = e.g0;
         const uint32_t L0 = leb_len(g);
         if (lane == 0) {
             for (uint32_t n = 0; n + 1 < L0; ++n) {
@@ -847,8 +864,8 @@ k_emit_tiles(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ me
             }
             ib[L0 - 1] = (uint8_t)g;
         }
-        warp_copy(ib + L0, slot_bytes + (size_t)t * 2 * slot_cap, m.internal_bytes, lane);
-        warp_copy(vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), m.count * W, lane);
+        warp_copy(ib + L0, slot_bytes + (size_t)t * 2 * slot_cap, e.internal_bytes, lane);
+        warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), e.count * W, lane);
     }
 }
 
@@ -928,6 +945,13 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     if (ev) cudaEventRecord(ev[2], s);
     k_finalize<<<1, 1024, 0, s>>>(a.entry_begin, a.tensor_byte_begin, a.ntensors, a.name_len, a.numel,
                                   a.table, a.width, a.summary);
+    {
+        const uint32_t g = (a.ntiles + 255) / 256;
+        k_tiles_emitplan<W><<<g < 65535u ? g : 65535u, 256, 0, s>>>(a.tiles, a.meta, a.ntiles, a.tile_entry,
+                                                                   a.tile_byte, a.tile_pred, a.entry_begin,
+                                                                   a.tensor_byte_begin, a.table, a.plan,
+                                                                   a.summary);
+    }
     if (ev) cudaEventRecord(ev[3], s);
     return cudaGetLastError();
 }
@@ -936,10 +960,8 @@ template <int W>
 static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
-    k_emit_tiles<W><<<a.persist_ctas, 256, 0, s>>>(a.tiles, a.meta, a.ntiles, a.slot_cap, a.slot_bytes,
-                                                   static_cast<const LT *>(a.slot_val), a.tile_entry,
-                                                   a.tile_byte, a.tile_pred, a.entry_begin,
-                                                   a.tensor_byte_begin, a.table, out);
+    k_emit_tiles<W><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
+                                                   static_cast<const LT *>(a.slot_val), out);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
     k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out);

@@ -40,6 +40,16 @@ struct TileMeta {
 };
 static_assert(sizeof(TileMeta) == 16, "TileMeta is 16 bytes");
 
+// K3b output per tile: everything K4 needs in one 32-byte load.
+struct TileEmit {
+    unsigned long long ib;   // body offset of the tile's first LEB128 byte
+    unsigned long long vb;   // body offset of the tile's first value
+    unsigned long long g0;   // gap of the tile's first change (to the previous change, or absolute)
+    uint32_t count;          // changes in the tile
+    uint32_t internal_bytes; // LEB128 bytes of the gaps inside the tile (pre-encoded in the slot)
+};
+static_assert(sizeof(TileEmit) == 32, "TileEmit is 32 bytes");
+
 // Device-written summary of one extract, read back by the host after the single sync.
 struct ExtractSummary {
     unsigned long long M;           // total changed lanes (entries) over all tensors
@@ -94,6 +104,7 @@ struct ExtractArgs {
     unsigned long long *tile_byte;    // ntiles: LEB128 bytes before the tile (all tensors)
     unsigned long long *tile_pred;    // ntiles: absolute index of the previous change in the tensor, or 0
     unsigned int *tile_bytes_tmp;     // ntiles: the tile's own LEB128 bytes
+    TileEmit *plan;                   // ntiles: K4's per-tile plan
     unsigned long long *blk_a;        // per tile block: entry count, then LEB128 bytes
     long long *blk_key;               // per tile block: last non-empty tile
     const uint32_t *tensor_first_tile;  // ntensors
@@ -126,6 +137,7 @@ struct ApplyArgs {
     const RecordRow *hint;            // device copy of the host hint, or nullptr
     ApplyRec *recs;                   // n
     unsigned long long *rec_chunk_begin;  // n + 1
+    uint32_t *chunk_rec;              // chunk -> record
     unsigned int *chunk_count;
     unsigned long long *chunk_sum;
     unsigned long long *chunk_ord_base;
