@@ -230,7 +230,7 @@ enum {
                                         3 = one CTA per tile, 128-byte runs per thread;
                                         4 = as 1 with 512 threads x 4 vectors;
                                         5 = as 1, persistent (3 CTAs per SM loop over tiles) */
-    DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 8) */
+    DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 4) */
     DELTA_OPT_PREFETCH_TILES = 5,     /* 1 + distance, in tiles, of the L2 bulk prefetch issued by
                                          the default compare kernel (1 = off; default: one wave of
                                          resident tiles, 3 x SMs) */

@@ -422,10 +422,11 @@ template <int W, bool ENTRY_MAJOR>
 __global__ void __launch_bounds__(256)
 k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
           const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
-          const unsigned int *__restrict__ chunk_count,
+          const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
           const unsigned long long *__restrict__ ord_base, const unsigned long long *__restrict__ idx_base,
           ApplyState *st) {
     using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
+    constexpr uint32_t WIN = 8192;  // lanes per dense merge window
     const uint32_t gate = st->status;
     if (gate != kOk) {  // the gate: nothing is written unless all checks passed
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&st->first_error, 0u, gate);
@@ -436,9 +437,12 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     __shared__ __align__(16) uint8_t svb[kByteChunk * W + 32];  // at most one varint per byte
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
-    // entry-major order: absolute indices of the chunk's entries by ordinal, then the
-    // stores are issued entry i by thread i mod 256 (a warp covers 32 consecutive entries)
-    __shared__ unsigned long long s_idx[ENTRY_MAJOR ? kByteChunk : 1];
+    // entry-major order: the chunk's indices relative to idx_base[c], by ordinal; stores are
+    // issued entry i by thread i mod 256 (a warp covers 32 consecutive entries), or, for a
+    // dense chunk, merged into 16 KiB windows of the target and written back whole.
+    __shared__ uint32_t s_rel[ENTRY_MAJOR ? kByteChunk : 1];
+    __shared__ __align__(16) uint8_t s_win[ENTRY_MAJOR ? WIN * W + 32 : 16];
+    __shared__ uint32_t s_iend;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = __ldg(chunk_rec + c);
@@ -469,19 +473,67 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
             spre += s_sum[w];
         }
         uint32_t ord = cpre + ci - cnt;
-        unsigned long long idx = idx_base[c] + spre + si - sum;
+        const unsigned long long base = idx_base[c];
+        unsigned long long idx = base + spre + si - sum;
         LT *w = reinterpret_cast<LT *>(R.w);
         auto value = [&](uint32_t o) -> LT {
             if constexpr (W == 2) return (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
             else return (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) | ((LT)vals[4 * o + 3] << 24);
         };
-        if constexpr (ENTRY_MAJOR) {
+        // entry-major needs the chunk's span to fit 32-bit relative indices
+        if (ENTRY_MAJOR && chunk_sum[c] < 0xFFFFFFFFull) {
             decode_thread(v, [&](unsigned long long x) {
                 idx += x;
-                s_idx[ord++] = idx;
+                s_rel[ord++] = (uint32_t)(idx - base);
             });
             __syncthreads();
-            for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) w[s_idx[i]] = value(i);
+            const uint32_t lo = s_rel[0], hi = s_rel[cn - 1];
+            const unsigned long long span = (unsigned long long)hi - lo + 1;
+            if (cn >= 256 && span <= 24ull * cn) {
+                // dense chunk: merge into windows [ws, we) of the target (this chunk owns
+                // exactly the lanes lo..hi, so the write-back never touches another CTA's)
+                uint32_t ibeg = 0;
+                for (unsigned long long ws = lo; ws <= hi; ws += WIN) {
+                    const unsigned long long we = min((unsigned long long)hi + 1, ws + WIN);
+                    LT *gdst = w + base + ws;
+                    const uint32_t nl = (uint32_t)(we - ws);
+                    if (threadIdx.x == 0) {  // entries of this window: [ibeg, iend)
+                        uint32_t l = ibeg, r = cn;
+                        while (l < r) {
+                            const uint32_t m = (l + r) >> 1;
+                            if ((unsigned long long)s_rel[m] < we) l = m + 1;
+                            else r = m;
+                        }
+                        s_iend = l;
+                    }
+                    __syncthreads();
+                    const uint32_t iend = s_iend;
+                    if (iend == ibeg) {  // nothing changes in this window
+                        __syncthreads();
+                        continue;
+                    }
+                    // stage the target lanes (plain loads: the kernel writes this memory)
+                    const uint4 *ga = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(gdst) & ~uintptr_t(15));
+                    const uint32_t o16 = (uint32_t)(reinterpret_cast<uintptr_t>(gdst) & 15);
+                    for (uint32_t j = threadIdx.x; j < (o16 + nl * W + 15) / 16; j += blockDim.x)
+                        reinterpret_cast<uint4 *>(s_win)[j] = ga[j];
+                    __syncthreads();
+                    LT *wl = reinterpret_cast<LT *>(s_win + o16);
+                    for (uint32_t i = ibeg + threadIdx.x; i < iend; i += blockDim.x) wl[s_rel[i] - ws] = value(i);
+                    __syncthreads();
+                    // write back exactly lanes [ws, we): lane head, 16-byte body, lane tail
+                    const uint32_t head = min(nl, ((16u - o16) & 15u) / W);
+                    const uint32_t nv = (nl - head) * W / 16;
+                    if (threadIdx.x < head) gdst[threadIdx.x] = wl[threadIdx.x];
+                    for (uint32_t j = threadIdx.x; j < nv; j += blockDim.x)
+                        reinterpret_cast<uint4 *>(gdst + head)[j] = reinterpret_cast<const uint4 *>(wl + head)[j];
+                    for (uint32_t l2 = head + nv * 16 / W + threadIdx.x; l2 < nl; l2 += blockDim.x) gdst[l2] = wl[l2];
+                    ibeg = iend;
+                    __syncthreads();
+                }
+            } else {
+                for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) w[base + s_rel[i]] = value(i);
+            }
         } else {
             decode_thread(v, [&](unsigned long long x) {
                 idx += x;
@@ -507,7 +559,7 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[3], s);
 #define SCATTER(WW, EM)                                                                                 \
-    k_scatter<WW, EM><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec, a.chunk_count, \
+    k_scatter<WW, EM><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec, a.chunk_count, a.chunk_sum, \
                                                      a.chunk_ord_base, a.chunk_idx_base, a.state)
     if (a.width == 2) {
         if (a.entry_major) SCATTER(2, true);
