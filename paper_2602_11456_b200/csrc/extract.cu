@@ -268,9 +268,13 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     // The LEB128 bytes of the gaps between consecutive changes inside the tile (each
     // < 2^14 lanes, so 1 or 2 bytes), encoded in order; the first change's gap depends on
     // earlier tiles and is written by K4.
-    // Encoded into shared memory first, then copied to the slot with 16-byte stores (at
-    // high density one byte store per thread per instruction would hit 32 sectors).
-    uint8_t *s_bytes = smem + LANES * sizeof(uint16_t);  // 2 * LANES bytes
+    // Dense slots (slot_cap > kStageGapBytes) encode into shared memory first and copy to
+    // the slot with 16-byte stores (one byte store per thread per instruction would hit 32
+    // sectors); sparse ones write the few bytes directly (and launch with less shared
+    // memory, so more tiles stay resident).
+    const bool staged = slot_cap > kStageGapBytes;
+    uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;  // 16-byte aligned (slot_cap >= 8)
+    uint8_t *s_bytes = staged ? smem + LANES * sizeof(uint16_t) : sb;  // 2 * LANES bytes
     const uint32_t q = (c + THREADS - 1) / THREADS;  // contiguous entries per thread
     const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
     uint32_t L = 0;
@@ -286,11 +290,12 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
             s_bytes[pos++] = (uint8_t)(g >> 7);
         }
     }
-    __syncthreads();
-    uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;  // 16-byte aligned (slot_cap >= 8)
-    for (uint32_t j = tid; j < tl / 16; j += THREADS)
-        reinterpret_cast<uint4 *>(sb)[j] = reinterpret_cast<const uint4 *>(s_bytes)[j];
-    if (tid < (tl & 15u)) sb[(tl & ~15u) + tid] = s_bytes[(tl & ~15u) + tid];
+    if (staged) {
+        __syncthreads();
+        for (uint32_t j = tid; j < tl / 16; j += THREADS)
+            reinterpret_cast<uint4 *>(sb)[j] = reinterpret_cast<const uint4 *>(s_bytes)[j];
+        if (tid < (tl & 15u)) sb[(tl & ~15u) + tid] = s_bytes[(tl & ~15u) + tid];
+    }
     if (tid == 0)
         meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
 }
@@ -907,7 +912,8 @@ template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     constexpr int LANES = kScanThreads * kScanVecs * (16 / W);
-    const size_t smem = (size_t)LANES * (sizeof(uint16_t) + 2);  // lane offsets + encoded gap bytes
+    // lane offsets (+ encoded gap bytes for dense slots, see scan_tile)
+    const size_t smem = (size_t)LANES * (sizeof(uint16_t) + (a.slot_cap > kStageGapBytes ? 2 : 0));
     cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_tiles<W, 512, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
