@@ -426,6 +426,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
           const unsigned long long *__restrict__ ord_base, const unsigned long long *__restrict__ idx_base,
           ApplyState *st) {
     using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
+    constexpr uint32_t WIN = 8192;  // lanes per dense merge window
     const uint32_t gate = st->status;
     if (gate != kOk) {  // the gate: nothing is written unless all checks passed
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&st->first_error, 0u, gate);
@@ -438,8 +439,10 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     __shared__ unsigned long long s_sum[8];
     // entry-major order: the chunk's indices relative to idx_base[c], by ordinal; stores are
     // issued entry i by thread i mod 256 (a warp covers 32 consecutive entries), or, for a
-    // dense chunk, merged per 32-byte block of the target.
+    // dense chunk, merged into 16 KiB windows of the target and written back whole.
     __shared__ uint32_t s_rel[ENTRY_MAJOR ? kByteChunk : 1];
+    __shared__ __align__(16) uint8_t s_win[ENTRY_MAJOR ? WIN * W + 32 : 16];
+    __shared__ uint32_t s_iend;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = __ldg(chunk_rec + c);
@@ -486,40 +489,47 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
             __syncthreads();
             const uint32_t lo = s_rel[0], hi = s_rel[cn - 1];
             const unsigned long long span = (unsigned long long)hi - lo + 1;
-            if (span <= 24ull * cn) {
-                // dense chunk: one thread per touched 32-byte block of the target reads the
-                // block, merges every entry that falls in it and writes the whole block back
-                // (a full-sector store: no read-modify-write fill).  Only blocks lying
-                // entirely inside this chunk's own lanes [lo, hi] are merged; at the edges
-                // the entries are stored lane by lane, so no other CTA's lanes are touched.
-                const uintptr_t own0 = reinterpret_cast<uintptr_t>(w + base + lo);
-                const uintptr_t own1 = reinterpret_cast<uintptr_t>(w + base + hi) + W;  // exclusive
-                for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) {
-                    LT *pi = w + base + s_rel[i];
-                    const uintptr_t blk = reinterpret_cast<uintptr_t>(pi) & ~uintptr_t(31);
-                    if (i > 0 && (reinterpret_cast<uintptr_t>(w + base + s_rel[i - 1]) & ~uintptr_t(31)) == blk)
-                        continue;  // not the first entry of its block
-                    if (blk >= own0 && blk + 32 <= own1) {
-                        uint32_t r[8];
-                        ld_v8(reinterpret_cast<const void *>(blk), r);
-                        uint32_t j = i;
-                        do {  // lane l of the block: word l*W/4, bits (l*W*8) mod 32 (registers only)
-                            const uint32_t byte = (uint32_t)(reinterpret_cast<uintptr_t>(w + base + s_rel[j]) - blk);
-                            const uint32_t x = value(j), q = byte >> 2, sh = (byte & 3u) * 8;
-                            const uint32_t m = (W == 4) ? 0xFFFFFFFFu : (0xFFFFu << sh);
-#pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                if ((uint32_t)u == q) r[u] = (r[u] & ~m) | ((x << sh) & m);
-                            ++j;
-                        } while (j < cn && (reinterpret_cast<uintptr_t>(w + base + s_rel[j]) & ~uintptr_t(31)) == blk);
-                        st_v8(reinterpret_cast<void *>(blk), r);
-                    } else {
-                        uint32_t j = i;
-                        do {
-                            w[base + s_rel[j]] = value(j);
-                            ++j;
-                        } while (j < cn && (reinterpret_cast<uintptr_t>(w + base + s_rel[j]) & ~uintptr_t(31)) == blk);
+            if (cn >= 256 && span <= 4ull * cn) {  // >= 25 % dense: window merge
+                // dense chunk: merge into windows [ws, we) of the target (this chunk owns
+                // exactly the lanes lo..hi, so the write-back never touches another CTA's)
+                uint32_t ibeg = 0;
+                for (unsigned long long ws = lo; ws <= hi; ws += WIN) {
+                    const unsigned long long we = min((unsigned long long)hi + 1, ws + WIN);
+                    LT *gdst = w + base + ws;
+                    const uint32_t nl = (uint32_t)(we - ws);
+                    if (threadIdx.x == 0) {  // entries of this window: [ibeg, iend)
+                        uint32_t l = ibeg, r = cn;
+                        while (l < r) {
+                            const uint32_t m = (l + r) >> 1;
+                            if ((unsigned long long)s_rel[m] < we) l = m + 1;
+                            else r = m;
+                        }
+                        s_iend = l;
                     }
+                    __syncthreads();
+                    const uint32_t iend = s_iend;
+                    if (iend == ibeg) {  // nothing changes in this window
+                        __syncthreads();
+                        continue;
+                    }
+                    // stage the target lanes (plain loads: the kernel writes this memory)
+                    const uint4 *ga = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(gdst) & ~uintptr_t(15));
+                    const uint32_t o16 = (uint32_t)(reinterpret_cast<uintptr_t>(gdst) & 15);
+                    for (uint32_t j = threadIdx.x; j < (o16 + nl * W + 15) / 16; j += blockDim.x)
+                        reinterpret_cast<uint4 *>(s_win)[j] = ga[j];
+                    __syncthreads();
+                    LT *wl = reinterpret_cast<LT *>(s_win + o16);
+                    for (uint32_t i = ibeg + threadIdx.x; i < iend; i += blockDim.x) wl[s_rel[i] - ws] = value(i);
+                    __syncthreads();
+                    // write back exactly lanes [ws, we): lane head, 16-byte body, lane tail
+                    const uint32_t head = min(nl, ((16u - o16) & 15u) / W);
+                    const uint32_t nv = (nl - head) * W / 16;
+                    if (threadIdx.x < head) gdst[threadIdx.x] = wl[threadIdx.x];
+                    for (uint32_t j = threadIdx.x; j < nv; j += blockDim.x)
+                        reinterpret_cast<uint4 *>(gdst + head)[j] = reinterpret_cast<const uint4 *>(wl + head)[j];
+                    for (uint32_t l2 = head + nv * 16 / W + threadIdx.x; l2 < nl; l2 += blockDim.x) gdst[l2] = wl[l2];
+                    ibeg = iend;
+                    __syncthreads();
                 }
             } else {
                 for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) w[base + s_rel[i]] = value(i);
