@@ -404,6 +404,18 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except (OSError, ValueError):
         pass
+    # DRAM traffic of one K1 launch from the committed ncu capture of this exact workload
+    # (profiles/ncu_traffic.json; null for other configurations)
+    k1_traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        c = tr["config"]
+        if (c["config"] == args.config and abs(c["rho"] - rho) < 1e-12 and c["pattern"] == pattern
+                and c["dtype"] == args.dtype and c["n_gpus"] == world):
+            k = tr["kernels"]["k_scan_tiles"]
+            k1_traffic = k["dram_read_bytes"] + k["dram_write_bytes"]
+    except (OSError, ValueError, KeyError):
+        pass
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None
     kernel_ms = {k: round(v / args.steps, 4) for k, v in acc.items()}
@@ -427,7 +439,9 @@ def main():
                      "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": None,
+                     "traffic": k1_traffic,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write.sum, one launch)"
+                     if k1_traffic else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": k1_bytes},
