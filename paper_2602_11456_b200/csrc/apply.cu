@@ -455,10 +455,20 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         __syncthreads();
         uint32_t cnt = 0;
         unsigned long long sum = 0;
-        decode_thread(v, [&](unsigned long long x) {
-            ++cnt;
-            sum += x;
-        });
+        const int p0 = threadIdx.x * 16;
+        const bool full16 = p0 + 16 <= (int)v.len;
+        // all 16 bytes single-byte varints (and the previous byte ends a varint)?
+        const bool ones = full16 && ((long long)v.cs + p0 == 0 || !(v.b[p0 - 1] & 0x80)) && [&] {
+            uint32_t any_cont = 0;
+            for (int j = 0; j < 16; ++j) any_cont |= v.b[p0 + j];
+            return !(any_cont & 0x80);
+        }();
+        if (!(full16 && validate_fast(v, p0, cnt, sum))) {
+            decode_thread(v, [&](unsigned long long x) {
+                ++cnt;
+                sum += x;
+            });
+        }
         const uint32_t ci = warp_inclusive_sum(cnt);
         const unsigned long long si = warp_inclusive_sum(sum);
         if (lane == 31) {
@@ -482,10 +492,19 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         };
         // entry-major needs the chunk's span to fit 32-bit relative indices
         if (ENTRY_MAJOR && chunk_sum[c] < 0xFFFFFFFFull) {
-            decode_thread(v, [&](unsigned long long x) {
-                idx += x;
-                s_rel[ord++] = (uint32_t)(idx - base);
-            });
+            if (ones) {  // 16 one-byte gaps: no continuation handling
+                uint32_t r = (uint32_t)(idx - base);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    r += v.b[p0 + j];
+                    s_rel[ord + j] = r;
+                }
+            } else {
+                decode_thread(v, [&](unsigned long long x) {
+                    idx += x;
+                    s_rel[ord++] = (uint32_t)(idx - base);
+                });
+            }
             __syncthreads();
             const uint32_t lo = s_rel[0], hi = s_rel[cn - 1];
             const unsigned long long span = (unsigned long long)hi - lo + 1;

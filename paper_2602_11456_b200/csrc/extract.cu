@@ -275,21 +275,38 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     const bool staged = slot_cap > kStageGapBytes;
     uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;  // 16-byte aligned (slot_cap >= 8)
     uint8_t *s_bytes = staged ? smem + LANES * sizeof(uint16_t) : sb;  // 2 * LANES bytes
-    const uint32_t q = (c + THREADS - 1) / THREADS;  // contiguous entries per thread
+    // Each thread takes a contiguous run of entries, a multiple of 8 long, so its offsets
+    // come in as 16-byte shared loads (8 lane offsets each) instead of one dependent load
+    // per entry; gaps are taken against the previous offset carried in a register.
+    const uint32_t q = ((c + THREADS - 1) / THREADS + 7) & ~7u;
     const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
+    const uint32_t prev0 = i0 ? s_off[i0 - 1] : 0u;
+    auto for_each_gap = [&](auto &&f) {  // f(gap) for entries max(i0, 1) .. i1 - 1, in order
+        uint32_t prev = prev0;
+        for (uint32_t b = i0; b < i1; b += 8) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(s_off + b);
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t i = b + e;
+                const uint32_t o = (w4[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                if (i < i1 && i > 0) f(o - prev);
+                prev = o;
+            }
+        }
+    };
     uint32_t L = 0;
-    for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) L += 1u + ((s_off[i] - s_off[i - 1]) >= 128u);
+    for_each_gap([&](uint32_t g) { L += 1u + (g >= 128u); });
     uint32_t tl;
     uint32_t pos = block_excl_scan<NWARP, uint32_t>(L, s_red, tl);
-    for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) {
-        const uint32_t g = s_off[i] - s_off[i - 1];
+    for_each_gap([&](uint32_t g) {
         if (g < 128u) {
             s_bytes[pos++] = (uint8_t)g;
         } else {
             s_bytes[pos++] = (uint8_t)(g | 0x80u);
             s_bytes[pos++] = (uint8_t)(g >> 7);
         }
-    }
+    });
     if (staged) {
         __syncthreads();
         for (uint32_t j = tid; j < tl / 16; j += THREADS)
