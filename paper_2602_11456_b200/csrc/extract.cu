@@ -829,21 +829,32 @@ k_finalize(const unsigned long long *__restrict__ E, const unsigned long long *_
 }
 
 // ------------------------------------------------------------------------------ K4
-// Warp-wide copy of n bytes from a 4-byte aligned source to any destination: byte head up
-// to the destination's 4-byte boundary, funnel-shifted 4-byte words, byte tail.  Reads at
-// most 3 bytes past the source range (slots are padded).
+// Warp-wide copy of n bytes from a 16-byte aligned source to any destination: byte head
+// up to the destination's 16-byte boundary, 16-byte stores assembled from funnel-shifted
+// source words, byte tail.  Reads at most 4 bytes past the source range (slots are padded).
 __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
-    const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
+    // byte head up to the destination's 16-byte boundary
+    const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
     if ((uint32_t)lane < head) dst[lane] = src[lane];
-    const uint32_t rest = n - head, nw = rest >> 2;
-    uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + head);
+    const uint32_t rest = n - head, nv = rest >> 4;
+    uint4 *d16 = reinterpret_cast<uint4 *>(dst + head);
+    // source 16-byte aligned: output vector j = source bytes [head + 16j, head + 16j + 16),
+    // i.e. words q .. q+4 of the source shifted right by 8 * (head % 4) bits, q = head/4 + 4j
     const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-    const uint32_t sh = 8u * head;  // source byte offset of word j is head + 4j
-    for (uint32_t j = lane; j < nw; j += 32) {
-        const uint32_t w0 = __ldg(s32 + j), w1 = __ldg(s32 + j + 1);
-        d32[j] = sh ? __funnelshift_r(w0, w1, sh) : w0;
+    const uint32_t q0 = head >> 2, sh = 8u * (head & 3u);
+#pragma unroll 2
+    for (uint32_t j = lane; j < nv; j += 32) {
+        const uint32_t q = q0 + 4 * j;
+        const uint32_t a0 = __ldg(s32 + q), a1 = __ldg(s32 + q + 1), a2 = __ldg(s32 + q + 2),
+                       a3 = __ldg(s32 + q + 3), a4 = __ldg(s32 + q + 4);
+        uint4 o;
+        o.x = __funnelshift_r(a0, a1, sh);
+        o.y = __funnelshift_r(a1, a2, sh);
+        o.z = __funnelshift_r(a2, a3, sh);
+        o.w = __funnelshift_r(a3, a4, sh);
+        d16[j] = o;
     }
-    for (uint32_t b = (nw << 2) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
+    for (uint32_t b = (nv << 4) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
 }
 
 // K3b: per tile, the final body offsets of its index bytes and values and its first gap
