@@ -230,7 +230,7 @@ __device__ __forceinline__ uint32_t expand_nibble(uint32_t nib) {
 // varint values is sum_d 128^d * (sum of the payloads at position d), three byte-masked
 // dot products.  Returns false if the window needs the byte loop.
 __device__ __forceinline__ bool validate_fast(const ChunkView &v, int p0, uint32_t &cnt,
-                                              unsigned long long &sum) {
+                                              unsigned long long &sum, bool *ones = nullptr) {
     int c_in = 0;  // continuation bytes of a varint that started before p0
     while (c_in < 3 && (long long)v.cs + p0 - c_in > 0 && (v.b[p0 - c_in - 1] & 0x80)) ++c_in;
     if (c_in >= 3) return false;
@@ -263,6 +263,7 @@ __device__ __forceinline__ bool validate_fast(const ChunkView &v, int p0, uint32
         s1 = __dp4a(pw & expand_nibble((D1 >> (4 * k)) & 0xF), 0x01010101u, s1);
         s2 = __dp4a(pw & expand_nibble((D2 >> (4 * k)) & 0xF), 0x01010101u, s2);
     }
+    if (ones) *ones = (T == 0xFFFFu && c_in == 0);  // 16 one-byte varints
     uint32_t carry = 0;  // low bits of the straddling varint, from the bytes before p0
     if (c_in == 1) carry = v.b[p0 - 1] & 0x7F;
     else if (c_in == 2) carry = (v.b[p0 - 2] & 0x7F) | ((uint32_t)(v.b[p0 - 1] & 0x7F) << 7);
@@ -457,13 +458,8 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         unsigned long long sum = 0;
         const int p0 = threadIdx.x * 16;
         const bool full16 = p0 + 16 <= (int)v.len;
-        // all 16 bytes single-byte varints (and the previous byte ends a varint)?
-        const bool ones = full16 && ((long long)v.cs + p0 == 0 || !(v.b[p0 - 1] & 0x80)) && [&] {
-            uint32_t any_cont = 0;
-            for (int j = 0; j < 16; ++j) any_cont |= v.b[p0 + j];
-            return !(any_cont & 0x80);
-        }();
-        if (!(full16 && validate_fast(v, p0, cnt, sum))) {
+        bool ones = false;  // all 16 bytes are single-byte varints
+        if (!(full16 && validate_fast(v, p0, cnt, sum, &ones))) {
             decode_thread(v, [&](unsigned long long x) {
                 ++cnt;
                 sum += x;

@@ -295,18 +295,27 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
             }
         }
     };
+    // sparse tiles: one entry per thread, simple loop (shorter critical path)
+    const uint32_t qs = (c + THREADS - 1) / THREADS;
+    const uint32_t j0 = min(c, tid * qs), j1 = min(c, j0 + qs);
+    auto for_each_gap_sparse = [&](auto &&f) {
+        for (uint32_t i = (j0 ? j0 : 1); i < j1; ++i) f((uint32_t)(s_off[i] - s_off[i - 1]));
+    };
+    auto emit = [&](uint32_t &p, uint32_t g) {
+        if (g < 128u) {
+            s_bytes[p++] = (uint8_t)g;
+        } else {
+            s_bytes[p++] = (uint8_t)(g | 0x80u);
+            s_bytes[p++] = (uint8_t)(g >> 7);
+        }
+    };
     uint32_t L = 0;
-    for_each_gap([&](uint32_t g) { L += 1u + (g >= 128u); });
+    if (staged) for_each_gap([&](uint32_t g) { L += 1u + (g >= 128u); });
+    else for_each_gap_sparse([&](uint32_t g) { L += 1u + (g >= 128u); });
     uint32_t tl;
     uint32_t pos = block_excl_scan<NWARP, uint32_t>(L, s_red, tl);
-    for_each_gap([&](uint32_t g) {
-        if (g < 128u) {
-            s_bytes[pos++] = (uint8_t)g;
-        } else {
-            s_bytes[pos++] = (uint8_t)(g | 0x80u);
-            s_bytes[pos++] = (uint8_t)(g >> 7);
-        }
-    });
+    if (staged) for_each_gap([&](uint32_t g) { emit(pos, g); });
+    else for_each_gap_sparse([&](uint32_t g) { emit(pos, g); });
     if (staged) {
         __syncthreads();
         for (uint32_t j = tid; j < tl / 16; j += THREADS)
@@ -832,7 +841,25 @@ k_finalize(const unsigned long long *__restrict__ E, const unsigned long long *_
 // Warp-wide copy of n bytes from a 16-byte aligned source to any destination: byte head
 // up to the destination's 16-byte boundary, 16-byte stores assembled from funnel-shifted
 // source words, byte tail.  Reads at most 4 bytes past the source range (slots are padded).
+__device__ __forceinline__ void warp_copy4(uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
+    const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
+    if ((uint32_t)lane < head) dst[lane] = src[lane];
+    const uint32_t rest = n - head, nw = rest >> 2;
+    uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + head);
+    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+    const uint32_t sh = 8u * head;  // source byte offset of word j is head + 4j
+    for (uint32_t j = lane; j < nw; j += 32) {
+        const uint32_t w0 = __ldg(s32 + j), w1 = __ldg(s32 + j + 1);
+        d32[j] = sh ? __funnelshift_r(w0, w1, sh) : w0;
+    }
+    for (uint32_t b = (nw << 2) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
+}
+
 __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
+    if (n < 1024) {  // a few words per lane: the 4-byte path has the shorter critical path
+        warp_copy4(dst, src, n, lane);
+        return;
+    }
     // byte head up to the destination's 16-byte boundary
     const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
     if ((uint32_t)lane < head) dst[lane] = src[lane];
