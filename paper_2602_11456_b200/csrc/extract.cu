@@ -911,7 +911,7 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
 // One warp per tile: the LEB128 bytes of the tile's first gap, then the tile's pre-encoded
 // internal gaps and its raw values copied to their final offsets in the body.
 template <int W>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 8)
 k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out) {
