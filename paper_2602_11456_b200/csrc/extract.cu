@@ -126,7 +126,7 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 // ------------------------------------------------------------------------------ K1
 // THREADS x VECS = 2048 16-byte vectors per operand per tile (32 KiB); instantiated as
 // 256 x 8 (3 CTAs / SM) and 512 x 4 (2 CTAs / SM, more warps, fewer registers each).
-template <int W, int THREADS, int VECS>
+template <int W, int THREADS, int VECS, bool STAGED>
 __device__ __forceinline__ void
 scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
           uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
@@ -272,7 +272,7 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     // the slot with 16-byte stores (one byte store per thread per instruction would hit 32
     // sectors); sparse ones write the few bytes directly (and launch with less shared
     // memory, so more tiles stay resident).
-    const bool staged = slot_cap > kStageGapBytes;
+    constexpr bool staged = STAGED;  // == (slot_cap > kStageGapBytes), chosen at launch
     uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;  // 16-byte aligned (slot_cap >= 8)
     uint8_t *s_bytes = staged ? smem + LANES * sizeof(uint16_t) : sb;  // 2 * LANES bytes
     // Each thread takes a contiguous run of entries, a multiple of 8 long, so its offsets
@@ -310,13 +310,13 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         }
     };
     uint32_t L = 0;
-    if (staged) for_each_gap([&](uint32_t g) { L += 1u + (g >= 128u); });
+    if constexpr (STAGED) for_each_gap([&](uint32_t g) { L += 1u + (g >= 128u); });
     else for_each_gap_sparse([&](uint32_t g) { L += 1u + (g >= 128u); });
     uint32_t tl;
     uint32_t pos = block_excl_scan<NWARP, uint32_t>(L, s_red, tl);
-    if (staged) for_each_gap([&](uint32_t g) { emit(pos, g); });
+    if constexpr (STAGED) for_each_gap([&](uint32_t g) { emit(pos, g); });
     else for_each_gap_sparse([&](uint32_t g) { emit(pos, g); });
-    if (staged) {
+    if constexpr (STAGED) {
         __syncthreads();
         for (uint32_t j = tid; j < tl / 16; j += THREADS)
             reinterpret_cast<uint4 *>(sb)[j] = reinterpret_cast<const uint4 *>(s_bytes)[j];
@@ -326,13 +326,13 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
 }
 
-template <int W, int THREADS, int VECS, int MINB>
+template <int W, int THREADS, int VECS, int MINB, bool STAGED>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
              uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
-    scan_tile<W, THREADS, VECS>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
+    scan_tile<W, THREADS, VECS, STAGED>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
                                 meta, summary);
 }
 
@@ -345,7 +345,7 @@ k_scan_tiles_persist(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32
                      typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
                      ExtractSummary *summary) {
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        scan_tile<W, 256, 8>(t, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val, meta, summary);
+        scan_tile<W, 256, 8, false>(t, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val, meta, summary);
         __syncthreads();  // shared scratch is reused by the next tile
     }
 }
@@ -969,8 +969,9 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     constexpr int LANES = kScanThreads * kScanVecs * (16 / W);
     // lane offsets (+ encoded gap bytes for dense slots, see scan_tile)
     const size_t smem = (size_t)LANES * (sizeof(uint16_t) + (a.slot_cap > kStageGapBytes ? 2 : 0));
-    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_scan_tiles<W, 512, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tiles<W, 512, 4, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
     if (a.scan_kernel == 1) {
         constexpr int STAGES = 3;
@@ -991,11 +992,12 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
                                                            a.slot_bytes, static_cast<LT *>(a.slot_val),
                                                            a.meta, a.summary);
         } else if (a.scan_kernel == 3)
-            k_scan_tiles<W, 512, 4, 2><<<a.ntiles, 512, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
+            k_scan_tiles<W, 512, 4, 2, false><<<a.ntiles, 512, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
                                                                    a.slot_bytes, static_cast<LT *>(a.slot_val),
                                                                    a.meta, a.summary);
         else
-            k_scan_tiles<W, 256, 8, 3><<<a.ntiles, 256, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
+            (a.slot_cap > kStageGapBytes ? k_scan_tiles<W, 256, 8, 3, true> : k_scan_tiles<W, 256, 8, 3, false>)
+                <<<a.ntiles, 256, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
                                                                    a.slot_bytes, static_cast<LT *>(a.slot_val),
                                                                    a.meta, a.summary);
     }
