@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     p.add_argument("--no-clocks", action="store_true")
+    p.add_argument("--assembly", default="nvlink", choices=["nvlink", "nccl"],
+                   help="N>1: body assembly by the delta_assemble NVLink kernel or NCCL P2P")
     p.add_argument("--pipeline", type=int, default=1,
                    help="G > 1: extract and apply in G pipelined groups on two streams")
     p.add_argument("--apply-ctas", type=int, default=0, help="apply kernels' CTAs per SM (0 = default)")
@@ -287,12 +289,16 @@ def main():
     stream = torch.cuda.current_stream()
 
     comm = torch.cuda.Stream(dev) if world > 1 else None
+    nvasm = None
 
     def assemble(size, body):
-        """S2+S3 on a side stream: the NVLink transfer of the body to rank 0 overlaps this
-        rank's apply (which needs no collective); the step ends when both are done."""
+        """S2+S3 on a side stream: the transfer of the body to rank 0 overlaps this rank's
+        apply (which needs no collective); the step ends when both are done."""
         nonlocal root_out
         comm.wait_stream(torch.cuda.current_stream())
+        if nvasm is not None:  # delta_assemble kernel over NVLink peer memory
+            nvasm.assemble(body, size, stream=comm)
+            return
         with torch.cuda.stream(comm):
             sizes, off, tot = sdist.gather_sizes(size, dev)
             if rank == 0 and (root_out is None or root_out.numel() < tot):
@@ -329,6 +335,13 @@ def main():
         ctx.set_profiling(True)
         size0 = ctx.delta_size(tl)
         out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
+        if world > 1 and args.assembly == "nvlink":
+            tot0 = torch.tensor([size0], dtype=torch.int64, device=dev)
+            dist.all_reduce(tot0)
+            total0 = int(tot0.item())
+            nvasm = sdist.NvlinkAssembler(ctx, total0 + total0 // 8 + 4096, dev)
+            if rank == 0:
+                out = nvasm.buf  # rank 0's records are the head of the assembled body
 
         def step(acc=None):
             # delta_extract runs the compare/compaction itself (delta_size's work) and

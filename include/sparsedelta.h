@@ -205,6 +205,21 @@ const delta_record_info *delta_table_dev(const delta_ctx *ctx);
  * delta_apply_async calls since the previous wait (DELTA_OK if none), then clear it. */
 int delta_apply_wait(delta_ctx *ctx, void *stream);
 
+/* delta_assemble — S3 of the multi-GPU path as one kernel over NVLink peer memory: copy
+ * this rank's body (src_dev, sizes_dev[rank] bytes; this GPU, 16-byte aligned) into the
+ * assembled body on the root GPU, dst_peer_dev (the root's buffer mapped into this process
+ * with CUDA IPC, dst_capacity bytes), at offset sum(sizes_dev[0..rank-1]).  sizes_dev: the
+ * n_ranks body sizes in device memory (e.g. an NCCL all-gather); the offset is computed on
+ * the device, so no host round trip is needed.  Asynchronous on `stream`; a destination
+ * overflow is reported by delta_assemble_wait.  The caller orders the copy against the
+ * root's readers (e.g. an NCCL all-reduce on the same stream after it). */
+int delta_assemble(delta_ctx *ctx, const void *src_dev, void *dst_peer_dev, uint64_t dst_capacity,
+                   const uint64_t *sizes_dev, uint32_t n_ranks, uint32_t rank, void *stream);
+
+/* Synchronise `stream`; DELTA_ECAPACITY if a delta_assemble since the last wait would have
+ * overflowed its destination (nothing was written by that copy), else DELTA_OK. */
+int delta_assemble_wait(delta_ctx *ctx, void *stream);
+
 /* Per-kernel device times of the last delta_size/delta_extract/delta_apply on this ctx,
  * in milliseconds, measured with CUDA events recorded on the call's stream around each
  * kernel (only while profiling is enabled; zero otherwise).  A field is the time of the

@@ -265,6 +265,18 @@ class DeltaContext:
         self._check(fn(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(), body.numel(), hint,
                        _stream_handle(stream)))
 
+    def assemble(self, src, dst_peer, sizes, rank, stream=None):
+        """Copy this rank's body ``src`` (uint8 CUDA tensor) into ``dst_peer`` (the root's
+        assembled-body tensor mapped into this process) at the offset given by the device
+        tensor ``sizes`` (int64, one per rank); see delta_assemble."""
+        self._check(self._lib.delta_assemble(self._h, c_void_p(src.data_ptr() if src.numel() else 0),
+                                             c_void_p(dst_peer.data_ptr()), dst_peer.numel(),
+                                             c_void_p(sizes.data_ptr()), sizes.numel(), rank,
+                                             _stream_handle(stream)))
+
+    def assemble_wait(self, stream=None):
+        self._check(self._lib.delta_assemble_wait(self._h, _stream_handle(stream)))
+
     def apply_wait(self, stream=None):
         """Synchronise and raise the first error of the async applies since the last wait."""
         self._check(self._lib.delta_apply_wait(self._h, _stream_handle(stream)))

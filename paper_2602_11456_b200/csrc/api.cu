@@ -77,7 +77,8 @@ struct delta_ctx {
     ExtractSummary *h_summary = nullptr;  // pinned
 
     // ---- apply workspace
-    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state;
+    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status;
+    uint32_t *h_asm = nullptr;  // pinned
     ApplyState *h_state = nullptr;  // pinned
     // pinned staging ring for the per-call apply uploads (targets, hint, names): with a
     // pinned source cudaMemcpyAsync does not wait for earlier work on the stream, so
@@ -173,7 +174,7 @@ void delta_ctx_destroy(delta_ctx *c) {
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->tile_plan, &c->blk_a,
                       &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
-                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->a_cnt, &c->a_sum,
+                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
     if (c->profiling) {
@@ -183,6 +184,7 @@ void delta_ctx_destroy(delta_ctx *c) {
     }
     if (c->h_summary) cudaFreeHost(c->h_summary);
     if (c->h_state) cudaFreeHost(c->h_state);
+    if (c->h_asm) cudaFreeHost(c->h_asm);
     for (int i = 0; i < delta_ctx::kRing; ++i) {
         if (c->ring[i]) cudaFreeHost(c->ring[i]);
         if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
@@ -640,4 +642,38 @@ extern "C" int delta_apply(delta_ctx *ctx, const delta_target *tg, uint32_t n, i
     int rc = apply_enqueue(ctx, tg, n, elem, body, body_bytes, hint, static_cast<cudaStream_t>(stream));
     if (rc) return rc;
     return delta_apply_wait(ctx, stream);
+}
+
+extern "C" int delta_assemble(delta_ctx *ctx, const void *src, void *dst, uint64_t cap, const uint64_t *sizes,
+                              uint32_t n_ranks, uint32_t rank, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!sizes || rank >= n_ranks || (!src && rank != 0) || !dst)
+        return fail(ctx, DELTA_EINVAL, 0, "delta_assemble: bad arguments");
+    if (reinterpret_cast<uintptr_t>(src) % 16) return fail(ctx, DELTA_EINVAL, 0, "delta_assemble: src not 16-byte aligned");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->asm_status.p) {
+        GROW(ctx->asm_status, 16);
+        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
+    }
+    CK(launch_assemble(static_cast<const uint8_t *>(src), static_cast<uint8_t *>(dst), cap,
+                       reinterpret_cast<const unsigned long long *>(sizes), rank, ctx->asm_status.as<uint32_t>(),
+                       ctx->sm_count * 2, s),
+       "assemble launch");
+    return DELTA_OK;
+}
+
+extern "C" int delta_assemble_wait(delta_ctx *ctx, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    if (!ctx->asm_status.p) return DELTA_OK;
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->h_asm) CK(cudaMallocHost(&ctx->h_asm, 16), "pinned");
+    CK(cudaMemcpyAsync(ctx->h_asm, ctx->asm_status.p, 4, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaStreamSynchronize(s), "assemble");
+    CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
+    if (*ctx->h_asm) return fail(ctx, DELTA_ECAPACITY, 0, "delta_assemble: destination too small");
+    return DELTA_OK;
 }

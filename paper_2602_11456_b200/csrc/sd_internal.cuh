@@ -151,6 +151,10 @@ struct ApplyArgs {
     bool entry_major;                 // scatter store order (see k_scatter)
 };
 
+cudaError_t launch_assemble(const uint8_t *src, uint8_t *dst, unsigned long long capacity,
+                            const unsigned long long *sizes, uint32_t rank, uint32_t *status, int ctas,
+                            cudaStream_t s);
+
 // ev: nullptr, or 5 events: before A1, after A1, A2, A3, A4.
 cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev);  // A1-A4
 

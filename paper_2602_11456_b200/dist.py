@@ -14,6 +14,7 @@ S3  ``assemble``: the rank bodies are sent to the root into their final offsets
 
 import torch
 import torch.distributed as dist
+from torch.multiprocessing.reductions import reduce_tensor
 
 
 def shard_plan(numels, world: int):
@@ -89,3 +90,42 @@ def assemble(local_body: torch.Tensor, sizes, root_out: torch.Tensor = None, roo
 def shift_table(rows, offset: int):
     """Offset-table rows of a rank's body, shifted to the global body's byte offsets."""
     return [(r[0] + offset, r[1], r[2], r[3] + offset, r[4], r[5] + offset, r[6]) for r in rows]
+
+
+class NvlinkAssembler:
+    """S3 as one kernel over NVLink peer memory (delta_assemble): the root owns the
+    assembled-body buffer ``buf``; every other rank maps it into its own address space with
+    CUDA IPC once, and per step writes its body straight into it at the offset the kernel
+    computes on the device from the all-gathered sizes (no host round trip, no receive
+    posted on the root).  A one-element all-reduce on the same stream after the copies
+    orders them before anything the root does next.  Rank 0's own body is extracted
+    directly into ``buf`` (offset 0)."""
+
+    def __init__(self, ctx, capacity: int, device, group=None, root: int = 0):
+        assert root == 0, "the assembled body starts with rank 0's records"
+        self.ctx, self.group, self.root = ctx, group, root
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.device(device)
+        self.buf = torch.empty(capacity, dtype=torch.uint8, device=self.device) if self.rank == root else None
+        handles = [None] * self.world
+        dist.all_gather_object(handles, reduce_tensor(self.buf) if self.rank == root else None, group=group)
+        if self.rank != root:
+            fn, args = handles[root]
+            args = list(args)
+            args[6] = self.device.index  # rebuild on this process's device (peer mapping)
+            self.peer = fn(*args)
+        self.sizes = torch.zeros(self.world, dtype=torch.int64, device=self.device)
+        self.size1 = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.token = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    def assemble(self, body: torch.Tensor, size: int, stream=None):
+        """Enqueue: sizes all-gather, this rank's NVLink copy into the root, completion
+        all-reduce.  Returns the assembled view on the root, None elsewhere."""
+        stream = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(stream):
+            self.size1.fill_(size)
+            dist.all_gather_into_tensor(self.sizes, self.size1, group=self.group)
+            if self.rank != self.root:
+                self.ctx.assemble(body, self.peer, self.sizes, self.rank, stream=stream)
+            dist.all_reduce(self.token, group=self.group)
+        return self.buf if self.rank == self.root else None

@@ -46,6 +46,18 @@ def main():
         ref_body, ref_table = oracle_extract([(s.name, pairs[k][0], pairs[k][1]) for k, s in enumerate(specs)])
         ok &= got.cpu().numpy().tobytes() == ref_body
         print(f"[rank0] assembled {tot} bytes from sizes {sizes}: match single-GPU and oracle = {ok}", flush=True)
+    # the same assembly through the delta_assemble kernel over NVLink (CUDA IPC mapping)
+    asm = sdist.NvlinkAssembler(ctx, tot + 4096, dev)
+    if rank == 0 and mine:
+        b0, _ = ctx.delta_extract(mine, out=asm.buf)
+        body = b0
+    got2 = asm.assemble(body, body.numel())
+    torch.cuda.synchronize()
+    ctx.assemble_wait()
+    if rank == 0:
+        ok2 = torch.equal(got2[:tot].cpu(), full_body.cpu())
+        print(f"[rank0] NVLink delta_assemble: match = {ok2}", flush=True)
+        ok &= ok2
     if mine:
         targets = [(n, o.clone()) for n, o, _ in mine]
         ctx.delta_apply(targets, body, table=table)

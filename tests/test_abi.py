@@ -71,6 +71,8 @@ def test_null_context_is_einval(built):
     assert lib.delta_set_profiling(None, 1) == E
     assert lib.delta_last_timing(None, byref(built.Timing())) == E
     assert lib.delta_table_dev(None) is None
+    assert lib.delta_assemble(None, None, None, 0, None, 1, 0, None) == E
+    assert lib.delta_assemble_wait(None, None) == E
     assert lib.delta_last_detail(None) == 0
     assert lib.delta_last_error(None) == b"no context"
     assert b"sm_100a" in lib.delta_version()
