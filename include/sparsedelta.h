@@ -220,6 +220,12 @@ int delta_assemble(delta_ctx *ctx, const void *src_dev, void *dst_peer_dev, uint
  * overflowed its destination (nothing was written by that copy), else DELTA_OK. */
 int delta_assemble_wait(delta_ctx *ctx, void *stream);
 
+/* delta_digest — BLAKE3-256 of body_dev[0..bytes) computed on the GPU (NEXT f1: the delta
+ * checkpoint's integrity hash; reading R10: BLAKE3 over exactly the
+ * body bytes).  Writes the 32-byte digest to out32 (host) after synchronising
+ * `stream` once. */
+int delta_digest(delta_ctx *ctx, const void *body_dev, uint64_t bytes, uint8_t *out32, void *stream);
+
 /* Per-kernel device times of the last delta_size/delta_extract/delta_apply on this ctx,
  * in milliseconds, measured with CUDA events recorded on the call's stream around each
  * kernel (only while profiling is enabled; zero otherwise).  A field is the time of the

@@ -25,7 +25,8 @@ DETAIL_NAMES = {0: None, 1: "truncated", 2: "overlong", 3: "overflow", 4: "nonin
 EXPORTS = ("delta_ctx_create", "delta_ctx_destroy", "delta_last_error", "delta_last_detail",
            "delta_version", "delta_size", "delta_extract", "delta_apply", "delta_set_profiling",
            "delta_last_timing", "delta_apply_async", "delta_apply_wait", "delta_set_option",
-           "delta_apply_async_dev", "delta_table_dev", "delta_assemble", "delta_assemble_wait")
+           "delta_apply_async_dev", "delta_table_dev", "delta_assemble", "delta_assemble_wait",
+           "delta_digest")
 DELTA_OPT_APPLY_CTAS_PER_SM, DELTA_OPT_EMIT_CTAS_PER_SM, DELTA_OPT_SCAN_KERNEL = 1, 2, 3
 DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER = 4, 5, 6
 
@@ -96,6 +97,8 @@ def lib():
         L.delta_assemble.restype = c_int
         L.delta_assemble_wait.argtypes = [c_void_p, c_void_p]
         L.delta_assemble_wait.restype = c_int
+        L.delta_digest.argtypes = [c_void_p, c_void_p, c_uint64, ctypes.c_char_p, c_void_p]
+        L.delta_digest.restype = c_int
         L.delta_apply_wait.argtypes = [c_void_p, c_void_p]
         L.delta_apply_wait.restype = c_int
         L.delta_set_option.argtypes = [c_void_p, c_int, ctypes.c_int64]

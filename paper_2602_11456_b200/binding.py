@@ -274,6 +274,13 @@ class DeltaContext:
                                              c_void_p(sizes.data_ptr()), sizes.numel(), rank,
                                              _stream_handle(stream)))
 
+    def digest(self, body, stream=None) -> bytes:
+        """BLAKE3-256 of a uint8 CUDA tensor, computed on the GPU (delta_digest)."""
+        out = ctypes.create_string_buffer(32)
+        self._check(self._lib.delta_digest(self._h, c_void_p(body.data_ptr() if body.numel() else 0),
+                                           body.numel(), out, _stream_handle(stream)))
+        return out.raw
+
     def assemble_wait(self, stream=None):
         self._check(self._lib.delta_assemble_wait(self._h, _stream_handle(stream)))
 

@@ -3,8 +3,9 @@
 Header (67 bytes, little-endian): "SPDC" | format_version u16 (= 1) | version u64 |
 base_version u64 | element-type code u8 (0 = 16-bit, 1 = 32-bit) | tensor count u32 |
 body length u64 | BLAKE3-256 of exactly the body bytes (readings R9, R10).
-The body is what ``delta_extract`` writes.  Hashing runs on the host in this version (a
-GPU tree hash is the next step).
+The body is what ``delta_extract`` writes.  The digest is computed on the GPU
+(``delta_digest``, NEXT f1); ``unpack_container`` (a reader, host side) verifies it with the
+``blake3`` package.
 """
 
 import struct
@@ -16,13 +17,20 @@ _FMT = "<4sHQQBIQ32s"
 HEADER_BYTES = struct.calcsize(_FMT)
 
 
-def pack_container(body: bytes, version: int, base_version: int, width: int, n_tensors: int) -> bytes:
+def pack_container(body, version: int, base_version: int, width: int, n_tensors: int, ctx=None) -> bytes:
+    """``body``: a uint8 CUDA tensor (as written by delta_extract) or host bytes (uploaded
+    first).  The digest is always computed on the GPU (delta_digest)."""
+    import torch
+
+    from .binding import context
     if version != base_version + 1:
         raise ValueError("version must be base_version + 1")
-    body = bytes(body)
     code = {2: 0, 4: 1}[width]
-    return struct.pack(_FMT, _MAGIC, 1, version, base_version, code, n_tensors, len(body),
-                       blake3.blake3(body).digest()) + body
+    if not (hasattr(body, "is_cuda") and body.is_cuda):
+        body = torch.frombuffer(bytearray(bytes(body)) or bytearray(1), dtype=torch.uint8)[:len(body)].cuda()
+    h = (ctx or context(body.device)).digest(body)
+    raw = body.cpu().numpy().tobytes()
+    return struct.pack(_FMT, _MAGIC, 1, version, base_version, code, n_tensors, len(raw), h) + raw
 
 
 def unpack_container(blob: bytes):

@@ -77,7 +77,7 @@ struct delta_ctx {
     ExtractSummary *h_summary = nullptr;  // pinned
 
     // ---- apply workspace
-    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status;
+    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status, dg_ws;
     uint32_t *h_asm = nullptr;  // pinned
     ApplyState *h_state = nullptr;  // pinned
     // pinned staging ring for the per-call apply uploads (targets, hint, names): with a
@@ -174,7 +174,7 @@ void delta_ctx_destroy(delta_ctx *c) {
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->tile_plan, &c->blk_a,
                       &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
-                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->a_cnt, &c->a_sum,
+                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->dg_ws, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
     if (c->profiling) {
@@ -670,10 +670,29 @@ extern "C" int delta_assemble_wait(delta_ctx *ctx, void *stream) {
     if (!ctx->asm_status.p) return DELTA_OK;
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!ctx->h_asm) CK(cudaMallocHost(&ctx->h_asm, 16), "pinned");
+    if (!ctx->h_asm) CK(cudaMallocHost(&ctx->h_asm, 64), "pinned");
     CK(cudaMemcpyAsync(ctx->h_asm, ctx->asm_status.p, 4, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaStreamSynchronize(s), "assemble");
     CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
     if (*ctx->h_asm) return fail(ctx, DELTA_ECAPACITY, 0, "delta_assemble: destination too small");
+    return DELTA_OK;
+}
+
+extern "C" int delta_digest(delta_ctx *ctx, const void *body, uint64_t bytes, uint8_t *out32, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!out32 || (bytes && !body)) return fail(ctx, DELTA_EINVAL, 0, "delta_digest: bad arguments");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned long long nch = bytes == 0 ? 1 : (bytes + 1023) / 1024;
+    GROW(ctx->dg_ws, (size_t)(2 * nch * 32 + 64));
+    uint32_t *ws = ctx->dg_ws.as<uint32_t>();
+    uint32_t *dout = ws + 2 * nch * 8;
+    CK(launch_blake3(static_cast<const uint8_t *>(body), bytes, ws, dout, s), "digest launch");
+    if (!ctx->h_asm) CK(cudaMallocHost(&ctx->h_asm, 64), "pinned");
+    CK(cudaMemcpyAsync(ctx->h_asm, dout, 32, cudaMemcpyDeviceToHost, s), "digest readback");
+    CK(cudaStreamSynchronize(s), "digest");
+    memcpy(out32, ctx->h_asm, 32);
     return DELTA_OK;
 }

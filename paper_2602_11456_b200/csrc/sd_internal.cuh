@@ -151,6 +151,8 @@ struct ApplyArgs {
     bool entry_major;                 // scatter store order (see k_scatter)
 };
 
+cudaError_t launch_blake3(const uint8_t *in, unsigned long long n, uint32_t *ws, uint32_t *out32, cudaStream_t s);
+
 cudaError_t launch_assemble(const uint8_t *src, uint8_t *dst, unsigned long long capacity,
                             const unsigned long long *sizes, uint32_t rank, uint32_t *status, int ctas,
                             cudaStream_t s);

@@ -471,3 +471,29 @@ def test_mixed_varint_lengths(sd):
     old, new = _with_changes(n, pos)
     body, table = _roundtrip(sd, [("mixed", old, new)])
     assert table[0][2] == len(pos)
+
+
+# ------------------------------------------------------------------ GPU digest (NEXT f1)
+def test_gpu_digest_and_container(sd):
+    """delta_digest (BLAKE3-256 on the GPU) equals the oracle container's digest (the
+    `blake3` package) for sizes around every chunk / tree boundary, and the product's SPDC
+    container is byte-identical to the oracle's."""
+    import oracle
+    rng = np.random.default_rng(5)
+    ctx = sd.DeltaContext(DEV)
+    for n in [0, 1, 63, 64, 65, 1023, 1024, 1025, 2047, 2048, 2049, 3072, 4097, 65536, 100_000,
+              1 << 20, (1 << 20) + 7, 5_000_001]:
+        data = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        buf = torch.tensor(list(data) if n < 5000 else np.frombuffer(data, np.uint8).copy(),
+                           dtype=torch.uint8, device=DEV)
+        assert ctx.digest(buf) == oracle.container.digest(data), n
+        # unaligned start
+        if n > 3:
+            assert ctx.digest(buf[3:]) == oracle.container.digest(data[3:]), n
+    spec = m1_specs()[0]
+    o, w = generate_pair(spec, 0, 0, rho=0.01, pattern="exact", device=DEV)
+    body, table = ctx.delta_extract([(spec.name, o, w)])
+    blob = sd.pack_container(body, 9, 8, 2, 1, ctx=ctx)
+    ref = oracle.container.pack(body.cpu().numpy().tobytes(), 9, 8, 2, 1)
+    assert blob == ref
+    ctx.close()
