@@ -24,8 +24,43 @@ Definitions followed, in order (SURVEY.md §8(c) O1-O10 restates them):
   O10 rho = sum nnz / sum N (Eq. 1).
 """
 
+import math
+import struct
+
 from . import leb128
 from .errors import DeltaError
+
+MODE_REPLACE, MODE_ADDITIVE = 0, 1
+
+
+def _f32(bits: int) -> float:
+    return struct.unpack("<f", struct.pack("<I", bits & 0xFFFFFFFF))[0]
+
+
+def _f32_bits(x: float) -> int:
+    """Round a Python float (f64) to fp32, round-to-nearest-even (struct 'f'); for the
+    sum / difference of two fp32 values this equals the fp32 operation (53 >= 2*24 + 2)."""
+    if math.isnan(x):
+        return 0x7FC00000
+    try:
+        return struct.unpack("<I", struct.pack("<f", x))[0]
+    except OverflowError:  # beyond fp32 range after rounding: +-Inf
+        return 0x7F800000 if x > 0 else 0xFF800000
+
+
+def _bf16_rne(bits32: int) -> int:
+    """fp32 bits -> bf16 bits, round to nearest even; NaN -> 0x7FC0 (R17)."""
+    if (bits32 & 0x7FFFFFFF) > 0x7F800000:
+        return 0x7FC0
+    return ((bits32 + 0x7FFF + ((bits32 >> 16) & 1)) >> 16) & 0xFFFF
+
+
+def lane_op(a: int, b: int, width: int, sign: int) -> int:
+    """a + sign * b in the lane's float type: bf16 (width 2) via fp32, or fp32."""
+    if width == 2:
+        fa, fb = _f32(a << 16), _f32(b << 16)
+        return _bf16_rne(_f32_bits(fa + sign * fb))
+    return _f32_bits(_f32(a) + sign * _f32(b))
 
 HEADER_FIXED = 2 + 8 + 8 + 8 + 1  # u16 name_len, u64 N, u64 nnz, u64 idx_len, u8 mode (SPEC.md:148)
 
@@ -85,16 +120,19 @@ def decode_indices(stream: bytes) -> list[int]:
     return idx
 
 
-def record(name: str, old: list[int], new: list[int], width: int) -> bytes:
-    """O2..O6 for one fused tensor."""
+def record(name: str, old: list[int], new: list[int], width: int, mode: int = MODE_REPLACE) -> bytes:
+    """O2..O6 for one fused tensor.  Additive mode: values are new - old."""
     nb = name.encode("utf-8")
     if len(nb) > 0xFFFF:
         raise DeltaError("layout", "name longer than the u16 length field (SPEC.md:148)")
     idx = changed_indices(old, new)
     stream = encode_indices(idx)
-    vals = b"".join(_u(new[j], width) for j in idx)
+    if mode == MODE_REPLACE:
+        vals = b"".join(_u(new[j], width) for j in idx)
+    else:
+        vals = b"".join(_u(lane_op(new[j], old[j], width, -1), width) for j in idx)
     return (_u(len(nb), 2) + nb + _u(len(old), 8) + _u(len(idx), 8)
-            + _u(len(stream), 8) + stream + vals + _u(0, 1))
+            + _u(len(stream), 8) + stream + vals + _u(mode, 1))
 
 
 def record_from_sparse(name: str, n: int, idx: list[int], vals: list[int], width: int) -> bytes:
@@ -106,7 +144,8 @@ def record_from_sparse(name: str, n: int, idx: list[int], vals: list[int], width
             + b"".join(_u(v, width) for v in vals) + _u(0, 1))
 
 
-def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: int):
+def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: int,
+            mode: int = MODE_REPLACE):
     """Body and offset table for (name, old_spans, new_spans) in list order.
 
     Table rows: (record_off, N, nnz, idx_off, idx_len, val_off, record_bytes),
@@ -119,7 +158,7 @@ def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: 
                 len(a) != len(b) for a, b in zip(old_spans, new_spans)):
             raise DeltaError("shape", f"tensor {name!r}: span structure differs")
         old, new = fuse(old_spans), fuse(new_spans)
-        rec = record(name, old, new, width)
+        rec = record(name, old, new, width, mode)
         nl = len(name.encode("utf-8"))
         nnz = sum(1 for j in range(len(old)) if old[j] != new[j])
         idx_off = len(body) + 2 + nl + 24
@@ -156,8 +195,8 @@ def parse(body: bytes, width: int):
             v, pos = _read_u(body, pos, width)
             vals.append(v)
         mode, pos = _read_u(body, pos, 1)
-        if mode != 0:
-            raise DeltaError("mode", f"{name!r}: mode byte {mode} (only replace=0)")
+        if mode not in (MODE_REPLACE, MODE_ADDITIVE):
+            raise DeltaError("mode", f"{name!r}: mode byte {mode} (replace=0, additive=1)")
         recs.append((name, n, idx, vals, mode))
     return recs
 
@@ -175,10 +214,10 @@ def apply(targets: list[tuple[str, list[int]]], body: bytes, width: int) -> list
         if n != len(lanes):
             raise DeltaError("numel", f"{name!r}: record N={n}, target has {len(lanes)}")
     out = []
-    for (_, _, idx, vals, _), (_, lanes) in zip(recs, targets):
+    for (_, _, idx, vals, mode), (_, lanes) in zip(recs, targets):
         w = list(lanes)
         for j, v in zip(idx, vals):
-            w[j] = v
+            w[j] = v if mode == MODE_REPLACE else lane_op(w[j], v, width, +1)
         out.append(w)
     return out
 

@@ -96,17 +96,60 @@ def decode_gaps(stream: np.ndarray) -> np.ndarray:
     return g
 
 
-def record(name: str, old: np.ndarray, new: np.ndarray) -> bytes:
-    """O2..O6 for one fused tensor (SPEC.md:148 layout, little-endian)."""
+# ---- additive mode ("the arithmetic difference when mode=additive";
+# scatter-ADD on apply).  Lanes are read as bf16 (16-bit) or fp32 (32-bit);
+# the difference and the sum are taken in fp32 and rounded to the lane type with
+# round-to-nearest-even; a NaN result becomes the canonical quiet NaN (R17).
+MODE_REPLACE, MODE_ADDITIVE = 0, 1
+
+
+def bf16_to_f32(lanes16: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns -> float32 (exact: the bf16 bits are the top half)."""
+    return (lanes16.astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def f32_to_bf16_rne(x: np.ndarray) -> np.ndarray:
+    """float32 -> bf16 bit patterns, round to nearest, ties to even; NaN -> 0x7FC0."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16).astype(np.uint16)
+    return np.where(np.isnan(x), np.uint16(0x7FC0), r)
+
+
+def lane_sub(new: np.ndarray, old: np.ndarray) -> np.ndarray:
+    """Additive value: new - old in the lane's float type (fp32 arithmetic)."""
+    with np.errstate(all="ignore"):  # Inf - Inf, overflow: IEEE results are intended
+        if new.dtype.itemsize == 2:
+            return f32_to_bf16_rne(bf16_to_f32(new) - bf16_to_f32(old))
+        return _canon_f32(new.view(np.float32) - old.view(np.float32))
+
+
+def _canon_f32(d: np.ndarray) -> np.ndarray:
+    bits = d.astype(np.float32).view(np.uint32)
+    return np.where(np.isnan(d), np.uint32(0x7FC00000), bits)
+
+
+def lane_add(w: np.ndarray, val: np.ndarray) -> np.ndarray:
+    """Additive apply: w + val in the lane's float type (fp32 arithmetic)."""
+    with np.errstate(all="ignore"):
+        if w.dtype.itemsize == 2:
+            return f32_to_bf16_rne(bf16_to_f32(w) + bf16_to_f32(val))
+        return _canon_f32(w.view(np.float32) + val.view(np.float32))
+
+
+def record(name: str, old: np.ndarray, new: np.ndarray, mode: int = MODE_REPLACE) -> bytes:
+    """O2..O6 for one fused tensor (SPEC.md:148 layout, little-endian).  mode 0: values are
+    the new lanes (replace, reading R1); mode 1: the arithmetic differences (additive)."""
     nb = name.encode("utf-8")
     if len(nb) > 0xFFFF:
         raise DeltaError("layout", "name longer than the u16 length field")
     idx = changed_indices(old, new)
     stream = encode_gaps(gaps(idx))
-    vals = new[idx.astype(np.int64)].astype(new.dtype.newbyteorder("<"), copy=False)
+    ii = idx.astype(np.int64)
+    vals = new[ii] if mode == MODE_REPLACE else lane_sub(new[ii], old[ii])
+    vals = vals.astype(new.dtype.newbyteorder("<"), copy=False)
     return b"".join((struct.pack("<H", len(nb)), nb,
                      struct.pack("<QQQ", old.size, idx.size, stream.size),
-                     stream.tobytes(), vals.tobytes(), b"\x00"))
+                     stream.tobytes(), vals.tobytes(), bytes([mode])))
 
 
 def table_row(record_off: int, rec: bytes) -> tuple:
@@ -118,7 +161,7 @@ def table_row(record_off: int, rec: bytes) -> tuple:
     return (record_off, n, nnz, idx_off, ilen, idx_off + ilen, len(rec))
 
 
-def extract(tensors):
+def extract(tensors, mode: int = MODE_REPLACE):
     """tensors: [(name, old_spans, new_spans)] -> (body bytes, table rows).
     Records appear in list order (reading R15), one per tensor even
     when nothing changed (R12)."""
@@ -126,7 +169,7 @@ def extract(tensors):
     for name, old_spans, new_spans in tensors:
         if len(old_spans) != len(new_spans):
             raise DeltaError("shape", f"{name!r}: span count differs")
-        rec = record(name, fuse(old_spans), fuse(new_spans))
+        rec = record(name, fuse(old_spans), fuse(new_spans), mode)
         table.append(table_row(off, rec))
         parts.append(rec)
         off += len(rec)
@@ -164,9 +207,9 @@ def parse(body, width: int):
             raise DeltaError("range", f"{name!r}: index >= element_count {n}")
         vals = np.frombuffer(body[p + ilen:p + ilen + nnz * width], dtype=dt)
         mode = body[end - 1]
-        if mode != 0:
+        if mode not in (MODE_REPLACE, MODE_ADDITIVE):
             raise DeltaError("mode", f"{name!r}: mode byte {mode}")
-        recs.append((name, n, idx, vals))
+        recs.append((name, n, idx, vals, mode))
         pos = end
     return recs
 
@@ -178,15 +221,16 @@ def apply(targets, body, width: int, inplace: bool = False):
     recs = parse(body, width)
     if len(recs) != len(targets):
         raise DeltaError("layout", f"{len(recs)} records for {len(targets)} targets")
-    for (name, n, _, _), (tname, w) in zip(recs, targets):
+    for (name, n, _, _, _), (tname, w) in zip(recs, targets):
         if name != tname:
             raise DeltaError("name", f"record {name!r} vs target {tname!r}")
         if n != lanes(w).size:
             raise DeltaError("numel", f"{name!r}: N={n} vs target {lanes(w).size}")
     out = []
-    for (_, _, idx, vals), (_, w) in zip(recs, targets):
+    for (_, _, idx, vals, mode), (_, w) in zip(recs, targets):
         dst = lanes(w) if inplace else lanes(w).copy()
-        dst[idx.astype(np.int64)] = vals
+        ii = idx.astype(np.int64)
+        dst[ii] = vals if mode == MODE_REPLACE else lane_add(dst[ii], vals)
         out.append(dst)
     return out
 

@@ -196,7 +196,7 @@ def _mutations(body: bytes, table):
     m[pos] = 0x00
     out.append(("nonincreasing", m, None))
     m = bytearray(b)
-    m[ra[6] - 1] = 1                                     # mode byte
+    m[ra[6] - 1] = 2                                     # mode byte (0 replace, 1 additive)
     out.append(("mode", m, None))
     m = bytearray(b)
     m[2] ^= 0x01                                         # name byte of record a ('a' -> '`')
@@ -391,7 +391,7 @@ def test_async_apply_error_is_reported_at_wait(sd):
     ts = _small_valid()
     body, table = oracle_extract(ts)
     bad = bytearray(body)
-    bad[table[0][6] - 1] = 1  # mode byte of record a
+    bad[table[0][6] - 1] = 2  # mode byte of record a (0 replace, 1 additive)
     targets = [(n, torch.from_numpy(to_np(o).view(np.int16).copy()).to(DEV).view(torch.bfloat16))
                for n, o, _ in ts]
     before = [t.clone() for _, t in targets]

@@ -68,7 +68,7 @@ _BAD = [
     ("count", _rec("a", 10, 3, b"\x01\x01", b"\x01\x00\x02\x00\x03\x00"), [("a", 10)]),
     ("name", _rec("a", 10, 1, b"\x01", b"\x01\x00"), [("b", 10)]),
     ("numel", _rec("a", 10, 1, b"\x01", b"\x01\x00"), [("a", 11)]),
-    ("mode", _rec("a", 10, 1, b"\x01", b"\x01\x00", mode=1), [("a", 10)]),
+    ("mode", _rec("a", 10, 1, b"\x01", b"\x01\x00", mode=2), [("a", 10)]),
     ("layout", _rec("a", 10, 1, b"\x01", b"\x01\x00")[:-1], [("a", 10)]),
     ("layout", _rec("a", 10, 1, b"\x01", b"\x01\x00") + b"\x00", [("a", 10)]),
     ("layout", _rec("a", 10, 1, b"\x01", b"\x01\x00"), [("a", 10), ("b", 3)]),
@@ -94,3 +94,43 @@ def test_valid_control_for_malformed_set():
     out = codec.apply([("a", np.zeros(10, np.uint16))], body, 2)[0]
     assert out.tolist() == [0, 0, 0, 0, 0, 1, 0, 0, 0, 2]
     assert brute.apply([("a", [0] * 10)], body, 2)[0] == out.tolist()
+
+
+@pytest.mark.parametrize("width", [2, 4])
+def test_additive_mode_brute_vs_numpy(width):
+    """Additive mode: values = new - old in the lane's float type; apply
+    adds.  numpy (float32 arrays) against the per-element definition (Python floats rounded
+    to fp32, then RNE to bf16), on random bit patterns incl. NaN / Inf / subnormals."""
+    rng = np.random.default_rng(7 + width)
+    for _ in range(30):
+        ts = _rand_case(rng, width)
+        body, table = codec.extract(ts, mode=codec.MODE_ADDITIVE)
+        bbody, btable = brute.extract([(n, [o.tolist() for o in os_], [x.tolist() for x in ns])
+                                       for n, os_, ns in ts], width, mode=brute.MODE_ADDITIVE)
+        assert body == bbody and table == btable
+        targets = [(n, codec.fuse(os_)) for n, os_, _ in ts]
+        got = codec.apply(targets, body, width)
+        bgot = brute.apply([(n, w.tolist()) for n, w in targets], body, width)
+        for g, bg in zip(got, bgot):
+            assert g.tolist() == bg
+
+
+def test_additive_hand_examples():
+    # bf16: 1.0 = 0x3F80, 1.0078125 = 0x3F81 -> difference 2^-7 = 0x3C00; 1.0 + 2^-7 = 0x3F81
+    assert brute.lane_op(0x3F81, 0x3F80, 2, -1) == 0x3C00
+    assert brute.lane_op(0x3F80, 0x3C00, 2, +1) == 0x3F81
+    # tie: 256 (0x4380) + 1.0 = 257 lies halfway between 256 and 258 -> even mantissa: 256
+    assert brute.lane_op(0x4380, 0x3F80, 2, +1) == 0x4380
+    # ... and 258 (0x4381) + 1.0 = 259 -> halfway between 258 and 260 -> 260 (0x4382)
+    assert brute.lane_op(0x4381, 0x3F80, 2, +1) == 0x4382
+    # fp32: 1.0 + 2^-24 is a tie between 1.0 and 1 + 2^-23 -> 1.0 (even)
+    assert brute.lane_op(0x3F800000, 0x33800000, 4, +1) == 0x3F800000
+    # numpy agrees on the same lanes
+    assert codec.lane_add(np.array([0x4380, 0x4381], np.uint16), np.array([0x3F80, 0x3F80], np.uint16)).tolist() \
+        == [0x4380, 0x4382]
+    # additive with exactly representable differences reconstructs new exactly
+    old = np.array([0x3F80, 0x4000, 0x4040], np.uint16)   # 1, 2, 3
+    new = np.array([0x3F80, 0x40A0, 0x4040], np.uint16)   # 1, 5, 3
+    body, _ = codec.extract([("w", [old], [new])], mode=codec.MODE_ADDITIVE)
+    assert body[-1] == 1 and body[-3:-1] == bytes([0x40, 0x40])  # value 3.0 = 5 - 2
+    assert codec.apply([("w", old)], body, 2)[0].tolist() == new.tolist()

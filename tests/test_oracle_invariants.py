@@ -90,6 +90,6 @@ def test_strictly_increasing_decoded():
     w = o.copy()
     w[rng.random(o.size) < 0.05] ^= 1
     body, _ = codec.extract([("x", [o], [w])])
-    (_, _, idx, _), = codec.parse(body, 2)
+    (_, _, idx, _, _), = codec.parse(body, 2)
     assert np.all(idx[1:] > idx[:-1])
     assert np.array_equal(idx, np.flatnonzero(o != w).astype(np.uint64))
