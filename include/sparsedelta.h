@@ -255,9 +255,16 @@ enum {
     DELTA_OPT_PREFETCH_TILES = 5,     /* 1 + distance, in tiles, of the L2 bulk prefetch issued by
                                          the default compare kernel (1 = off; default: one wave of
                                          resident tiles, 3 x SMs) */
-    DELTA_OPT_SCATTER_ORDER = 6       /* 1 = each thread stores the entries it decoded,
+    DELTA_OPT_SCATTER_ORDER = 6,      /* 1 = each thread stores the entries it decoded,
                                          2 = entry-major: thread i stores entries i, i+256, ...
                                          (default for 16-bit lanes) */
+    DELTA_OPT_MODE = 7                /* records written by extract: 1 = replace (default; values
+                                         are the new lanes, apply stores them, bit-exact),
+                                         2 = additive (values are new - old and apply adds them,
+                                         SPEC.md:99, 135: 16-bit lanes read as bf16, 32-bit as
+                                         fp32, fp32 arithmetic rounded to nearest even — lossy,
+                                         for fidelity experiments).  delta_apply follows each
+                                         record's mode byte. */
 };
 
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */

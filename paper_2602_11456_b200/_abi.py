@@ -28,7 +28,7 @@ EXPORTS = ("delta_ctx_create", "delta_ctx_destroy", "delta_last_error", "delta_l
            "delta_apply_async_dev", "delta_table_dev", "delta_assemble", "delta_assemble_wait",
            "delta_digest")
 DELTA_OPT_APPLY_CTAS_PER_SM, DELTA_OPT_EMIT_CTAS_PER_SM, DELTA_OPT_SCAN_KERNEL = 1, 2, 3
-DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER = 4, 5, 6
+DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER, DELTA_OPT_MODE = 4, 5, 6, 7
 
 
 class Span(ctypes.Structure):

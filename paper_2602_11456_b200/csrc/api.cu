@@ -93,6 +93,7 @@ struct delta_ctx {
     int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scatter_ctas_per_sm = 4, scan_kernel = 0;
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
     bool entry_major = true;
+    int mode = 0;  // records written by extract: 0 replace, 1 additive
 
     // ---- optional per-kernel event timing
     bool profiling = false;
@@ -204,6 +205,11 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     else if (option == DELTA_OPT_SCATTER_CTAS_PER_SM) c->scatter_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_PREFETCH_TILES) c->prefetch_tiles = (int)value - 1;
     else if (option == DELTA_OPT_SCATTER_ORDER) c->entry_major = value == 2;
+    else if (option == DELTA_OPT_MODE) {
+        if (value > 2) return DELTA_EINVAL;
+        if (c->mode != (int)value - 1) c->scan_cached = false;
+        c->mode = (int)value - 1;
+    }
     else return DELTA_EINVAL;
     return DELTA_OK;
 }
@@ -377,6 +383,7 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.sm_count = ctx->sm_count;
     a.scan_kernel = ctx->scan_kernel;
     a.prefetch_dist = (uint32_t)(ctx->prefetch_tiles < 0 ? ctx->sm_count * 3 : ctx->prefetch_tiles);
+    a.mode = ctx->mode;
     return a;
 }
 

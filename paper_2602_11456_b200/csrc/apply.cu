@@ -55,7 +55,8 @@ __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_by
     if (ilen > rem || nnz > (rem - ilen) / (unsigned long long)width) return kLayout;
     end = q + ilen + nnz * width + 1;
     if (end > body_bytes) return kLayout;
-    if (body[end - 1] != 0) return kMode;
+    const uint8_t mode = body[end - 1];
+    if (mode > 1) return kMode;  // 0 replace, 1 additive
     if (nl != tg.name_len) return kName;
     for (unsigned long long b = 0; b < nl; ++b)
         if (body[ro + 2 + b] != names[tg.name_off + b]) return kName;
@@ -66,6 +67,7 @@ __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_by
     rec.nnz = nnz;
     rec.numel = N;
     rec.w = tg.w;
+    rec.mode = mode;
     return kOk;
 }
 
@@ -482,6 +484,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         const unsigned long long base = idx_base[c];
         unsigned long long idx = base + spre + si - sum;
         LT *w = reinterpret_cast<LT *>(R.w);
+        const bool add = R.mode == 1;  // additive record: scatter-add
         auto value = [&](uint32_t o) -> LT {
             if constexpr (W == 2) return (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
             else return (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) | ((LT)vals[4 * o + 3] << 24);
@@ -534,7 +537,10 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
                         reinterpret_cast<uint4 *>(s_win)[j] = ga[j];
                     __syncthreads();
                     LT *wl = reinterpret_cast<LT *>(s_win + o16);
-                    for (uint32_t i = ibeg + threadIdx.x; i < iend; i += blockDim.x) wl[s_rel[i] - ws] = value(i);
+                    for (uint32_t i = ibeg + threadIdx.x; i < iend; i += blockDim.x) {
+                        LT &t = wl[s_rel[i] - ws];
+                        t = add ? (LT)lane_combine<W>(t, value(i), false) : value(i);
+                    }
                     __syncthreads();
                     // write back exactly lanes [ws, we): lane head, 16-byte body, lane tail
                     const uint32_t head = min(nl, ((16u - o16) & 15u) / W);
@@ -547,12 +553,15 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
                     __syncthreads();
                 }
             } else {
-                for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) w[base + s_rel[i]] = value(i);
+                for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) {
+                    LT &t = w[base + s_rel[i]];
+                    t = add ? (LT)lane_combine<W>(t, value(i), false) : value(i);
+                }
             }
         } else {
             decode_thread(v, [&](unsigned long long x) {
                 idx += x;
-                w[idx] = value(ord);
+                w[idx] = add ? (LT)lane_combine<W>(w[idx], value(ord), false) : value(ord);
                 ++ord;
             });
         }

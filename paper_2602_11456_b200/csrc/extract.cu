@@ -126,7 +126,7 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 // ------------------------------------------------------------------------------ K1
 // THREADS x VECS = 2048 16-byte vectors per operand per tile (32 KiB); instantiated as
 // 256 x 8 (3 CTAs / SM) and 512 x 4 (2 CTAs / SM, more warps, fewer registers each).
-template <int W, int THREADS, int VECS, bool STAGED>
+template <int W, int THREADS, int VECS, bool STAGED, bool ADDITIVE = false>
 __device__ __forceinline__ void
 scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
           uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
@@ -250,7 +250,12 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
             const int j = __ffs(mm) - 1;
             mm &= mm - 1;
             s_off[pos] = (uint16_t)((r * THREADS + tid) * LPV + j);
-            if (fits) sv[pos] = (LT)lane_of<W>(vn[r], j);
+            if (fits) {
+                if constexpr (ADDITIVE)  // the arithmetic difference new - old
+                    sv[pos] = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
+                else
+                    sv[pos] = (LT)lane_of<W>(vn[r], j);
+            }
             ++pos;
         }
         rbase += (tot[q] >> sh) & 0xFFFFu;
@@ -326,13 +331,13 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
 }
 
-template <int W, int THREADS, int VECS, int MINB, bool STAGED>
+template <int W, int THREADS, int VECS, int MINB, bool STAGED, bool ADDITIVE = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
              uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
-    scan_tile<W, THREADS, VECS, STAGED>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
+    scan_tile<W, THREADS, VECS, STAGED, ADDITIVE>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
                                 meta, summary);
 }
 
@@ -945,7 +950,7 @@ __device__ __forceinline__ void put_u64(uint8_t *p, unsigned long long x) {
 __global__ void __launch_bounds__(128)
 k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__restrict__ name_len,
           const uint32_t *__restrict__ name_off, const uint8_t *__restrict__ names,
-          uint8_t *__restrict__ out) {
+          uint8_t *__restrict__ out, int mode) {
     for (uint32_t k = blockIdx.x; k < T; k += gridDim.x) {
         const RecordRow r = table[k];
         uint8_t *o = out + r.record_offset;
@@ -957,7 +962,7 @@ k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__res
             put_u64(o + 2 + nl, r.element_count);
             put_u64(o + 2 + nl + 8, r.nnz);
             put_u64(o + 2 + nl + 16, r.index_bytes);
-            o[r.record_bytes - 1] = 0;  // mode: replace (reading R1/R9)
+            o[r.record_bytes - 1] = (uint8_t)mode;  // 0 replace (reading R1/R9), 1 additive
         }
     }
 }
@@ -971,6 +976,8 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     const size_t smem = (size_t)LANES * (sizeof(uint16_t) + (a.slot_cap > kStageGapBytes ? 2 : 0));
     cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_tiles<W, 512, 4, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ev) cudaEventRecord(ev[0], s);
     if (a.scan_kernel == 1) {
@@ -996,7 +1003,10 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
                                                                    a.slot_bytes, static_cast<LT *>(a.slot_val),
                                                                    a.meta, a.summary);
         else
-            (a.slot_cap > kStageGapBytes ? k_scan_tiles<W, 256, 8, 3, true> : k_scan_tiles<W, 256, 8, 3, false>)
+            (a.mode == 1 ? (a.slot_cap > kStageGapBytes ? k_scan_tiles<W, 256, 8, 2, true, true>
+                                                        : k_scan_tiles<W, 256, 8, 2, false, true>)
+                         : (a.slot_cap > kStageGapBytes ? k_scan_tiles<W, 256, 8, 3, true>
+                                                        : k_scan_tiles<W, 256, 8, 3, false>))
                 <<<a.ntiles, 256, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
                                                                    a.slot_bytes, static_cast<LT *>(a.slot_val),
                                                                    a.meta, a.summary);
@@ -1034,7 +1044,7 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
                                                    static_cast<const LT *>(a.slot_val), out);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
-    k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out);
+    k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode);
     if (ev) cudaEventRecord(ev[2], s);
     return cudaGetLastError();
 }

@@ -77,6 +77,32 @@ __device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsi
 
 }  // namespace sd
 
+// ---------------------------------------------------------------- additive-mode lane arithmetic
+// (R17): 16-bit lanes are bf16, 32-bit lanes fp32; arithmetic in
+// fp32 (IEEE, round to nearest even), bf16 results rounded to nearest even, NaN results
+// canonical (0x7FC0 / 0x7FC00000).
+namespace sd {
+
+__device__ __forceinline__ uint32_t f32_to_bf16_rne(float f) {
+    const uint32_t b = __float_as_uint(f);
+    if ((b & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FC0u;
+    return (b + 0x7FFFu + ((b >> 16) & 1u)) >> 16;
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t lane_combine(uint32_t a, uint32_t b, bool subtract) {
+    if constexpr (W == 2) {
+        const float fa = __uint_as_float(a << 16), fb = __uint_as_float(b << 16);
+        return f32_to_bf16_rne(subtract ? __fsub_rn(fa, fb) : __fadd_rn(fa, fb));
+    } else {
+        const float r = subtract ? __fsub_rn(__uint_as_float(a), __uint_as_float(b))
+                                 : __fadd_rn(__uint_as_float(a), __uint_as_float(b));
+        return (__float_as_uint(r) & 0x7FFFFFFFu) > 0x7F800000u ? 0x7FC00000u : __float_as_uint(r);
+    }
+}
+
+}  // namespace sd
+
 // ---------------------------------------------------------------- mbarrier + bulk copy (TMA)
 namespace sd {
 

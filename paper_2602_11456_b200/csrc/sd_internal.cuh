@@ -78,6 +78,7 @@ struct TargetDesc {
 struct ApplyRec {  // located + verified record
     unsigned long long idx_off, idx_len, val_off, nnz, numel;
     uint8_t *w;
+    unsigned long long mode;  // 0 replace (scatter-store), 1 additive (scatter-add)
 };
 
 // Status word codes written by the apply kernels (DELTA_D_* of sparsedelta.h).
@@ -122,6 +123,7 @@ struct ExtractArgs {
     int sm_count;
     int scan_kernel;                  // 0: one CTA per tile; 1: persistent TMA pipeline; 2: runs
     uint32_t prefetch_dist;           // K1 (0): L2 bulk prefetch distance in tiles (0 = off)
+    int mode;                         // record mode: 0 replace, 1 additive
 };
 
 // ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1,

@@ -497,3 +497,35 @@ def test_gpu_digest_and_container(sd):
     ref = oracle.container.pack(body.cpu().numpy().tobytes(), 9, 8, 2, 1)
     assert blob == ref
     ctx.close()
+
+
+# ------------------------------------------------------------------ additive mode (NEXT f3)
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_additive_mode_parity(sd, dtype):
+    """DELTA_OPT_MODE = 2: values are new - old (fp32 arithmetic, RNE to bf16) and apply
+    adds them — body bytes and the applied lanes byte-exact against the
+    oracle's additive codec, on sparse, dense (window-merge) and full-range bit patterns."""
+    import oracle
+    from paper_2602_11456_b200 import _abi
+    ctx = sd.DeltaContext(DEV)
+    ctx.set_option(_abi.DELTA_OPT_MODE, 2)
+    tensors = []
+    for k, (n, rho, vals) in enumerate([(16_777_216, 0.01, "weights"), (300_001, 0.6, "weights"),
+                                        (100_003, 0.3, "bits"), (9, 1.0, "bits"), (0, 0.0, "weights")]):
+        spec = TensorSpec(f"a{k}", (n,), "matrix")
+        o, w = generate_pair(spec, k, 12, rho=rho, dtype=dtype, device=DEV, values=vals)
+        tensors.append((spec.name, o, w))
+    body, table = ctx.delta_extract(tensors)
+    ref_body, ref_table = oracle.codec.extract([(n, [to_np(o)], [to_np(w)]) for n, o, w in tensors],
+                                               mode=oracle.codec.MODE_ADDITIVE)
+    assert_body_equal(body, ref_body)
+    assert [tuple(r) for r in table] == [tuple(r) for r in ref_table]
+    width = 2 if dtype == torch.bfloat16 else 4
+    ref_out = oracle.codec.apply([(n, to_np(o)) for n, o, _ in tensors], ref_body, width)
+    for hint in (True, False):
+        targets = [(n, o.clone()) for n, o, _ in tensors]
+        ctx.delta_apply(targets, body, table=table if hint else None)
+        torch.cuda.synchronize()
+        for (_, t), r in zip(targets, ref_out):
+            assert np.array_equal(to_np(t), r)
+    ctx.close()
