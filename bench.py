@@ -483,8 +483,11 @@ def main():
                                   "host_cpus": os.cpu_count()}
     if rank == 0:
         print(json.dumps(result), flush=True)
+    if nvasm is not None:  # drop the CUDA IPC mapping of rank 0's buffer before rank 0 exits
+        nvasm.close()
     ctx.close()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

@@ -129,3 +129,9 @@ class NvlinkAssembler:
                 self.ctx.assemble(body, self.peer, self.sizes, self.rank, stream=stream)
             dist.all_reduce(self.token, group=self.group)
         return self.buf if self.rank == self.root else None
+
+    def close(self):
+        """Release the IPC mapping (non-root ranks) before the root frees or exits."""
+        torch.cuda.synchronize(self.device)
+        self.peer = None
+        dist.barrier(group=self.group)
