@@ -58,6 +58,9 @@ def parse():
     p.add_argument("--no-clocks", action="store_true")
     p.add_argument("--assembly", default="nvlink", choices=["nvlink", "nccl"],
                    help="N>1: body assembly by the delta_assemble NVLink kernel or NCCL P2P")
+    p.add_argument("--sync-step", action="store_true",
+                   help="host-sized step (size readback between extract and apply) instead of the "
+                        "chained device-sized one")
     p.add_argument("--pipeline", type=int, default=1,
                    help="G > 1: extract and apply in G pipelined groups on two streams")
     p.add_argument("--apply-ctas", type=int, default=0, help="apply kernels' CTAs per SM (0 = default)")
@@ -343,26 +346,40 @@ def main():
             if rank == 0:
                 out = nvasm.buf  # rank 0's records are the head of the assembled body
 
-        def step(acc=None):
-            # delta_extract runs the compare/compaction itself (delta_size's work) and
-            # leaves the offset table on the device for the apply: 2 host syncs per step
-            body, table = ctx.delta_extract(tl, out=out, table="device")
-            t1 = t2 = ctx.last_timing()
-            size = body.numel()
-            if world > 1:
-                assemble(size, body)
-            ctx.delta_apply(tg, body, table=table)
-            if world > 1:
-                torch.cuda.current_stream().wait_stream(comm)
-            t3 = ctx.last_timing()
+        size_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+
+        def record(acc):
+            t = ctx.last_timing()
             if acc is not None:
-                for kname in ("scan_ms", "lens_ms", "finalize_ms"):
-                    acc[kname] = acc.get(kname, 0.0) + t1[kname]
-                for kname in ("emit_ms", "headers_ms"):
-                    acc[kname] = acc.get(kname, 0.0) + t2[kname]
-                for kname in ("locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
-                    acc[kname] = acc.get(kname, 0.0) + t3[kname]
-            return body, table
+                for kname in ("scan_ms", "lens_ms", "finalize_ms", "emit_ms", "headers_ms",
+                              "locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
+                    acc[kname] = acc.get(kname, 0.0) + t[kname]
+
+        if args.sync_step or (world > 1 and nvasm is None):
+            def step(acc=None):
+                # host-sized path: delta_extract reads the size back (sync), the apply takes
+                # the device table; 2 host syncs per step
+                body, table = ctx.delta_extract(tl, out=out, table="device")
+                if world > 1:
+                    assemble(body.numel(), body)
+                ctx.delta_apply(tg, body, table=table)
+                if world > 1:
+                    torch.cuda.current_stream().wait_stream(comm)
+                record(acc)
+                return body, table
+        else:
+            def before_apply(buf, size):
+                if world > 1:
+                    assemble(size, buf)
+
+            def step(acc=None):
+                # one stream of kernels: extract (size + table stay on the device) -> [assembly
+                # on the comm stream] -> chained apply; the host waits once, at the end
+                n = ctx.round_trip(tl, tg, out, size_dev, before_apply=before_apply)
+                if world > 1:
+                    torch.cuda.current_stream().wait_stream(comm)
+                record(acc)
+                return out[:n], None
 
     for _ in range(max(args.warmup, 0)):
         body, table = step()
@@ -399,7 +416,7 @@ def main():
     value = scanned_total * args.steps / (ms / 1e3) / 1e9
 
     # ---- payload (global) and kernel-level roofline of the dominant kernel (K1)
-    if isinstance(table, sd.DeviceTable):  # host copy of the rows for the statistics (untimed)
+    if table is None or isinstance(table, sd.DeviceTable):  # host rows for the statistics (untimed)
         body, table = ctx.delta_extract(tl, out=out, table=True)
     body_local = body.numel()
     nnz_local = sum(r[2] for r in table)

@@ -56,7 +56,9 @@ enum {
     DELTA_ECORRUPT = -4,  /* malformed body; see delta_last_detail() */
     DELTA_ENAME = -5,     /* record name / element count does not match its target */
     DELTA_ECUDA = -6,     /* CUDA runtime error or no device */
-    DELTA_ENOMEM = -7     /* device workspace allocation failed */
+    DELTA_ENOMEM = -7,    /* device workspace allocation failed */
+    DELTA_EAGAIN = -8     /* delta_extract_wait: tile slots overflowed at a new density; the
+                             workspace has been grown, nothing was written — issue again */
 };
 
 /* Detail of a DELTA_ECORRUPT / DELTA_ENAME status (delta_last_detail). */
@@ -162,6 +164,27 @@ int delta_extract(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int e
                   void *out_dev, uint64_t out_capacity, delta_record_info *table,
                   void *stream, uint64_t *body_bytes);
 
+/* delta_extract_async — delta_extract as enqueue-only work: no host synchronisation
+ * (except the one-time plan upload when the descriptors change).  The same K1-K5
+ * kernels run on `stream`; K4/K5 write the body only if every tile's changes fitted the
+ * context's tile slots and the body fits out_capacity (the "emit gate"), and write the
+ * body size — or UINT64_MAX when the gate is closed — to body_bytes_dev (device, 8-byte
+ * aligned u64, may be NULL).  The offset table is left on the device (delta_table_dev).
+ * Pair every call with delta_extract_wait.  Work chained after it on the same stream
+ * (delta_apply_async_chain) reads the size and table on the device.
+ * Errors (immediate): as delta_size. */
+int delta_extract_async(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int elem,
+                        void *out_dev, uint64_t out_capacity, uint64_t *body_bytes_dev,
+                        void *stream);
+
+/* delta_extract_wait — wait for the last delta_extract_async on ctx (an event, not the
+ * whole stream) and report its outcome; *body_bytes (host, may be NULL) = body size.
+ * DELTA_EAGAIN: a tile held more changes than the slots (first call at a higher density);
+ * the slots have been grown, no body was written, repeat the extract (and anything
+ * chained on it, which refused to run: see delta_apply_async_chain).  DELTA_ECAPACITY:
+ * body larger than out_capacity, nothing written, *body_bytes = size needed. */
+int delta_extract_wait(delta_ctx *ctx, uint64_t *body_bytes);
+
 /* delta_apply — validate the whole body, then scatter-store its values into the targets
  * (A1-A4; "validate fully before mutating").
  *
@@ -196,6 +219,16 @@ int delta_apply_async(delta_ctx *ctx, const delta_target *targets, uint32_t n, i
 int delta_apply_async_dev(delta_ctx *ctx, const delta_target *targets, uint32_t n, int elem,
                           const void *body_dev, uint64_t body_bytes,
                           const delta_record_info *table_hint_dev, void *stream);
+
+/* delta_apply_async_chain — delta_apply_async_dev with the body SIZE in device memory as
+ * well: body_bytes_dev (u64, 8-byte aligned) as written by delta_extract_async, body_dev
+ * a buffer of body_capacity bytes.  A size above body_capacity (UINT64_MAX: the extract's
+ * emit gate was closed) fails the call's gate with detail DELTA_D_LAYOUT and mutates
+ * nothing.  With delta_extract_async this makes extract -> apply one stream of kernels
+ * with no host round trip between them. */
+int delta_apply_async_chain(delta_ctx *ctx, const delta_target *targets, uint32_t n, int elem,
+                            const void *body_dev, uint64_t body_capacity, const uint64_t *body_bytes_dev,
+                            const delta_record_info *table_hint_dev, void *stream);
 
 /* Device address of the offset table written by the last delta_size/delta_extract on ctx
  * (n rows; NULL if none).  Valid until the next extract call on ctx. */

@@ -17,7 +17,9 @@ DELTA_ECORRUPT, DELTA_ENAME, DELTA_ECUDA, DELTA_ENOMEM = -4, -5, -6, -7
 DELTA_ELEM16, DELTA_ELEM32 = 0, 1
 
 STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "ESHAPE", -3: "ECAPACITY", -4: "ECORRUPT",
-                -5: "ENAME", -6: "ECUDA", -7: "ENOMEM"}
+                -5: "ENAME", -6: "ECUDA", -7: "ENOMEM",
+                -8: "EAGAIN"}
+DELTA_EAGAIN = -8
 DETAIL_NAMES = {0: None, 1: "truncated", 2: "overlong", 3: "overflow", 4: "nonincreasing",
                 5: "range", 6: "count", 7: "name", 8: "numel", 9: "mode", 10: "layout"}
 
@@ -26,7 +28,7 @@ EXPORTS = ("delta_ctx_create", "delta_ctx_destroy", "delta_last_error", "delta_l
            "delta_version", "delta_size", "delta_extract", "delta_apply", "delta_set_profiling",
            "delta_last_timing", "delta_apply_async", "delta_apply_wait", "delta_set_option",
            "delta_apply_async_dev", "delta_table_dev", "delta_assemble", "delta_assemble_wait",
-           "delta_digest")
+           "delta_digest", "delta_extract_async", "delta_extract_wait", "delta_apply_async_chain")
 DELTA_OPT_APPLY_CTAS_PER_SM, DELTA_OPT_EMIT_CTAS_PER_SM, DELTA_OPT_SCAN_KERNEL = 1, 2, 3
 DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER, DELTA_OPT_MODE = 4, 5, 6, 7
 
@@ -90,6 +92,14 @@ def lib():
         L.delta_apply_async_dev.argtypes = [c_void_p, POINTER(Target), c_uint32, c_int, c_void_p, c_uint64,
                                             c_void_p, c_void_p]
         L.delta_apply_async_dev.restype = c_int
+        L.delta_extract_async.argtypes = [c_void_p, POINTER(Tensor), c_uint32, c_int, c_void_p, c_uint64,
+                                          c_void_p, c_void_p]
+        L.delta_extract_async.restype = c_int
+        L.delta_extract_wait.argtypes = [c_void_p, POINTER(c_uint64)]
+        L.delta_extract_wait.restype = c_int
+        L.delta_apply_async_chain.argtypes = [c_void_p, POINTER(Target), c_uint32, c_int, c_void_p, c_uint64,
+                                              c_void_p, c_void_p, c_void_p]
+        L.delta_apply_async_chain.restype = c_int
         L.delta_table_dev.argtypes = [c_void_p]
         L.delta_table_dev.restype = c_void_p
         L.delta_assemble.argtypes = [c_void_p, c_void_p, c_void_p, c_uint64, c_void_p, c_uint32, c_uint32,

@@ -240,7 +240,55 @@ class DeltaContext:
             return body, None
         return body, Table(rows, tl.n)
 
-    def delta_apply(self, targets, body, table=None, stream=None, wait=True):
+    def delta_extract_async(self, tensors, out, size, stream=None) -> "DeviceTable":
+        """Enqueue the extraction into ``out`` (uint8 CUDA tensor, its numel the capacity)
+        with no host synchronisation; ``size`` (int64 CUDA tensor, 1 element) receives the
+        body size on the device (or -1 = UINT64_MAX if nothing was written).  Returns the
+        device-resident offset table.  Pair with ``extract_wait``."""
+        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        if out.dtype != torch.uint8 or not out.is_contiguous() or not out.is_cuda:
+            raise ValueError("out must be a contiguous uint8 CUDA tensor")
+        if size.dtype != torch.int64 or not size.is_cuda or size.numel() != 1:
+            raise ValueError("size must be a one-element int64 CUDA tensor")
+        self._check(self._lib.delta_extract_async(self._h, tl.arr, tl.n, _ELEM[tl.width], out.data_ptr(),
+                                                  out.numel(), c_void_p(size.data_ptr()), _stream_handle(stream)))
+        return DeviceTable(self._lib.delta_table_dev(self._h), tl.n, self)
+
+    def extract_wait(self) -> int:
+        """Wait for the last delta_extract_async; returns the body size.  Raises DeltaError
+        with status EAGAIN after a slot overflow (workspace grown: issue the extract, and
+        whatever was chained on it, again) or ECAPACITY."""
+        nbytes = c_uint64()
+        self._check(self._lib.delta_extract_wait(self._h, byref(nbytes)))
+        return nbytes.value
+
+    def round_trip(self, tensors, targets, out, size, stream=None, before_apply=None):
+        """extract(tensors) -> apply into ``targets`` as one stream of kernels: the apply
+        reads the body size and offset table on the device (delta_apply_async_chain), so
+        the host waits once, at the end.  ``before_apply(out, size)`` may enqueue work
+        between the two (e.g. the multi-GPU body assembly).  A first call at a higher
+        density that overflows the tile slots (EAGAIN) is re-issued once.  Returns the
+        body size."""
+        for attempt in range(2):
+            table = self.delta_extract_async(tensors, out, size, stream)
+            if before_apply is not None:
+                before_apply(out, size)
+            self.delta_apply(targets, out, table=table, size=size, stream=stream, wait=False)
+            try:
+                n = self.extract_wait()
+            except DeltaError as e:
+                if e.status != _abi.DELTA_EAGAIN or attempt:
+                    raise
+                try:  # the chained apply refused to run (gate closed): clear its status
+                    self.apply_wait(stream)
+                except DeltaError:
+                    pass
+                continue
+            self.apply_wait(stream)
+            return n
+        raise AssertionError("unreachable")
+
+    def delta_apply(self, targets, body, table=None, stream=None, wait=True, size=None):
         """Validate ``body`` fully, then scatter its values into ``targets`` in place
         (all-or-nothing).  ``table``: optional offset-table rows from delta_extract.
         ``wait=False`` enqueues only (delta_apply_async); call ``apply_wait`` later."""
@@ -248,6 +296,15 @@ class DeltaContext:
         if body.dtype != torch.uint8 or not body.is_contiguous() or not body.is_cuda:
             raise ValueError("body must be a contiguous uint8 CUDA tensor")
         hint = None
+        if size is not None:  # chained: size (int64 CUDA tensor) and table on the device
+            if not isinstance(table, DeviceTable):
+                raise ValueError("a device-resident size needs a DeviceTable")
+            self._check(self._lib.delta_apply_async_chain(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(),
+                                                          body.numel(), c_void_p(size.data_ptr()),
+                                                          c_void_p(table.ptr), _stream_handle(stream)))
+            if wait:
+                self.apply_wait(stream)
+            return
         if isinstance(table, DeviceTable):
             self._check(self._lib.delta_apply_async_dev(self._h, tg.arr, tg.n, _ELEM[tg.width], body.data_ptr(),
                                                         body.numel(), c_void_p(table.ptr), _stream_handle(stream)))

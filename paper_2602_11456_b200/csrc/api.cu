@@ -74,6 +74,10 @@ struct delta_ctx {
         entry_begin, tensor_byte_begin, table, summary;
     uint32_t slot_cap = 0;          // entries per tile slot (grows on overflow)
     bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
+    // delta_extract_async: readback of the summary lands in h_summary when ev_extract fires
+    bool async_pending = false;
+    unsigned long long async_cap = 0;
+    cudaEvent_t ev_extract = nullptr;
     ExtractSummary *h_summary = nullptr;  // pinned
 
     // ---- apply workspace
@@ -169,6 +173,7 @@ int delta_ctx_create(delta_ctx **out, int device) {
 }
 
 void delta_ctx_destroy(delta_ctx *c) {
+    if (c && c->ev_extract) cudaEventDestroy(c->ev_extract);
     if (!c) return;
     cudaSetDevice(c->device);
     DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
@@ -396,7 +401,7 @@ static int reserve_slots(delta_ctx *ctx, uint32_t cap) {
 
 // K1-K3 + the single size readback; on slot overflow grows the slots to the largest
 // per-tile count seen and runs again (first call at a new density only).
-static int run_scan(delta_ctx *ctx, cudaStream_t s) {
+static int prepare_scan(delta_ctx *ctx) {
     const uint32_t T = ctx->ntensors, nt = ctx->ntiles;
     const uint32_t nblk = (nt + kTileBlock - 1) / kTileBlock;
     const uint32_t lanes_per_tile = kTileBytes / ctx->width;
@@ -419,6 +424,13 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
         int rc = reserve_slots(ctx, cap);
         if (rc) return rc;
     }
+    return DELTA_OK;
+}
+
+static int run_scan(delta_ctx *ctx, cudaStream_t s) {
+    const uint32_t lanes_per_tile = kTileBytes / ctx->width;
+    int rc0 = prepare_scan(ctx);
+    if (rc0) return rc0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
         CK(launch_extract_scan(extract_args(ctx), s, ctx->profiling ? ctx->ev_scan : nullptr),
@@ -505,6 +517,81 @@ extern "C" int delta_extract(delta_ctx *ctx, const delta_tensor *t, uint32_t n, 
     return DELTA_OK;
 }
 
+// Enqueue-only extract (no host synchronisation when the plan is cached): K1-K5 run
+// back to back; K4/K5 write the body only if the scan fitted its tile slots and the body
+// fits `cap`, and write the size (or ~0) to body_bytes_dev.  delta_extract_wait reports
+// the outcome.
+extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *out,
+                                   uint64_t cap, uint64_t *body_bytes_dev, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    const int w = elem_width(elem);
+    if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
+    if (cap && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
+    if (reinterpret_cast<uintptr_t>(body_bytes_dev) % 8)
+        return fail(ctx, DELTA_EINVAL, 0, "body_bytes_dev not 8-byte aligned");
+    int rc = validate_tensors(ctx, t, n, w);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rc = build_plan(ctx, t, n, w, s);
+    if (rc) return rc;
+    rc = prepare_scan(ctx);
+    if (rc) return rc;
+    ctx->scan_cached = false;
+    if (!ctx->ev_extract) CK(cudaEventCreateWithFlags(&ctx->ev_extract, cudaEventDisableTiming), "event");
+    CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
+    ExtractArgs a = extract_args(ctx);
+    a.out_cap = cap;
+    a.size_out = reinterpret_cast<unsigned long long *>(body_bytes_dev);
+    CK(launch_extract_scan(a, s, ctx->profiling ? ctx->ev_scan : nullptr), "extract scan launch");
+    if (n) {
+        CK(launch_extract_emit(a, static_cast<uint8_t *>(out), s, ctx->profiling ? ctx->ev_emit : nullptr),
+           "extract emit launch");
+    } else if (body_bytes_dev) {
+        CK(cudaMemsetAsync(body_bytes_dev, 0, 8, s), "memset");
+    }
+    CK(cudaMemcpyAsync(ctx->h_summary, ctx->summary.p, sizeof(ExtractSummary), cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaEventRecord(ctx->ev_extract, s), "event");
+    ctx->async_pending = true;
+    ctx->async_cap = cap;
+    return DELTA_OK;
+}
+
+extern "C" int delta_extract_wait(delta_ctx *ctx, uint64_t *body_bytes) {
+    if (!ctx) return DELTA_EINVAL;
+    if (!ctx->async_pending) return fail(ctx, DELTA_EINVAL, 0, "no delta_extract_async pending");
+    ctx->async_pending = false;
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(cudaEventSynchronize(ctx->ev_extract), "extract");
+    if (ctx->profiling) {
+        ctx->timing.scan_ms = ev_ms(ctx->ev_scan[0], ctx->ev_scan[1]);
+        ctx->timing.lens_ms = ev_ms(ctx->ev_scan[1], ctx->ev_scan[2]);
+        ctx->timing.finalize_ms = ev_ms(ctx->ev_scan[2], ctx->ev_scan[3]);
+        if (ctx->ntensors) {
+            ctx->timing.emit_ms = ev_ms(ctx->ev_emit[0], ctx->ev_emit[1]);
+            ctx->timing.headers_ms = ev_ms(ctx->ev_emit[1], ctx->ev_emit[2]);
+        }
+    }
+    const ExtractSummary &sm = *ctx->h_summary;
+    if (sm.overflow) {
+        const uint32_t lanes_per_tile = kTileBytes / ctx->width;
+        uint32_t need = 2;
+        while (need < sm.max_count) need <<= 1;
+        int rc = reserve_slots(ctx, std::min(need, lanes_per_tile));
+        if (rc) return rc;
+        return fail(ctx, DELTA_EAGAIN, 0,
+                    "tile slots overflowed (largest tile count %llu); workspace grown, issue the call again",
+                    (unsigned long long)sm.max_count);
+    }
+    if (body_bytes) *body_bytes = sm.body_bytes;
+    if (sm.body_bytes > ctx->async_cap)
+        return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < body size %llu",
+                    (unsigned long long)ctx->async_cap, (unsigned long long)sm.body_bytes);
+    return DELTA_OK;
+}
+
 // --------------------------------------------------------------------------- apply
 static const int kDetailToStatus[] = {
     DELTA_OK,        DELTA_ECORRUPT, DELTA_ECORRUPT, DELTA_ECORRUPT, DELTA_ECORRUPT, DELTA_ECORRUPT,
@@ -516,7 +603,8 @@ static const char *kDetailName[] = {"ok", "truncated varint", "overlong varint",
 
 static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem, const void *body,
                          uint64_t body_bytes, const delta_record_info *hint, cudaStream_t s,
-                         const delta_record_info *hint_dev = nullptr) {
+                         const delta_record_info *hint_dev = nullptr,
+                         const uint64_t *body_bytes_dev = nullptr) {
     ctx->err.clear();
     ctx->detail = 0;
     const int w = elem_width(elem);
@@ -579,6 +667,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     ApplyArgs a;
     a.body = static_cast<const uint8_t *>(body);
     a.body_bytes = body_bytes;
+    a.body_bytes_dev = reinterpret_cast<const unsigned long long *>(body_bytes_dev);
     a.targets = ctx->a_upload.as<TargetDesc>();
     a.n = n;
     a.names = ctx->a_upload.as<uint8_t>() + off_names;
@@ -614,6 +703,16 @@ extern "C" int delta_apply_async_dev(delta_ctx *ctx, const delta_target *tg, uin
     if (!ctx) return DELTA_EINVAL;
     return apply_enqueue(ctx, tg, n, elem, body, body_bytes, nullptr, static_cast<cudaStream_t>(stream),
                          table_hint_dev);
+}
+
+extern "C" int delta_apply_async_chain(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem,
+                                       const void *body, uint64_t body_cap, const uint64_t *body_bytes_dev,
+                                       const delta_record_info *table_hint_dev, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    if (!body_bytes_dev || reinterpret_cast<uintptr_t>(body_bytes_dev) % 8)
+        return fail(ctx, DELTA_EINVAL, 0, "body_bytes_dev NULL or not 8-byte aligned");
+    return apply_enqueue(ctx, tg, n, elem, body, body_cap, nullptr, static_cast<cudaStream_t>(stream),
+                         table_hint_dev, body_bytes_dev);
 }
 
 extern "C" const delta_record_info *delta_table_dev(const delta_ctx *ctx) {

@@ -73,10 +73,23 @@ __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_by
 
 __global__ void __launch_bounds__(256)
 k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
+         const unsigned long long *__restrict__ body_bytes_dev,
          const TargetDesc *__restrict__ tg, uint32_t n, const uint8_t *__restrict__ names,
          const RecordRow *__restrict__ hint, ApplyRec *__restrict__ recs,
          unsigned long long *__restrict__ rec_chunk_begin, uint32_t *__restrict__ chunk_rec, ApplyState *st,
          int width) {
+    if (body_bytes_dev != nullptr) {  // chained after delta_extract_async: size on the device
+        const unsigned long long b = *body_bytes_dev;
+        if (b > body_bytes) {  // ~0: the extract's gate was closed (no body was written)
+            if (threadIdx.x == 0) {
+                set_status(st, kLayout);
+                rec_chunk_begin[n] = 0;
+                st->n_chunks = 0;
+            }
+            return;
+        }
+        body_bytes = b;
+    }
     bool ok = hint != nullptr;
     if (hint != nullptr) {
         for (uint32_t k = threadIdx.x; k < n && ok; k += blockDim.x) {
@@ -572,7 +585,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
 // ------------------------------------------------------------------------------ launchers
 cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], s);
-    k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.targets, a.n, a.names, a.hint, a.recs,
+    k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
                                a.rec_chunk_begin, a.chunk_rec, a.state, a.width);
     if (ev) cudaEventRecord(ev[1], s);
     k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,

@@ -23,9 +23,13 @@ __global__ void __launch_bounds__(256)
 k_assemble(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst_base, unsigned long long capacity,
            const unsigned long long *__restrict__ sizes, uint32_t rank, uint32_t *status) {
     unsigned long long off = 0;
-    for (uint32_t q = 0; q < rank; ++q) off += sizes[q];
+    bool bad = false;
+    for (uint32_t q = 0; q < rank; ++q) {  // each size <= capacity: the sum cannot wrap
+        bad |= sizes[q] > capacity;
+        off += bad ? 0ull : sizes[q];
+    }
     const unsigned long long n = sizes[rank];
-    if (off + n > capacity || off + n < off) {
+    if (bad || n > capacity || off + n > capacity) {  // incl. ~0 sizes from a closed extract gate
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(status, 1u);
         return;
     }

@@ -919,7 +919,8 @@ template <int W>
 __global__ void __launch_bounds__(256, 8)
 k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
-             uint8_t *__restrict__ out) {
+             uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
+    if (summary->overflow || summary->body_bytes > cap) return;  // emit gate (async extract)
     const int lane = threadIdx.x & 31;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
@@ -950,7 +951,11 @@ __device__ __forceinline__ void put_u64(uint8_t *p, unsigned long long x) {
 __global__ void __launch_bounds__(128)
 k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__restrict__ name_len,
           const uint32_t *__restrict__ name_off, const uint8_t *__restrict__ names,
-          uint8_t *__restrict__ out, int mode) {
+          uint8_t *__restrict__ out, int mode, const ExtractSummary *summary, unsigned long long cap,
+          unsigned long long *size_out) {
+    const bool open = !summary->overflow && summary->body_bytes <= cap;
+    if (size_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *size_out = open ? summary->body_bytes : ~0ull;
+    if (!open) return;
     for (uint32_t k = blockIdx.x; k < T; k += gridDim.x) {
         const RecordRow r = table[k];
         uint8_t *o = out + r.record_offset;
@@ -1041,10 +1046,12 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
     k_emit_tiles<W><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
-                                                   static_cast<const LT *>(a.slot_val), out);
+                                                   static_cast<const LT *>(a.slot_val), out, a.summary,
+                                                   a.out_cap);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
-    k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode);
+    k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode, a.summary,
+                                 a.out_cap, a.size_out);
     if (ev) cudaEventRecord(ev[2], s);
     return cudaGetLastError();
 }

@@ -124,6 +124,10 @@ struct ExtractArgs {
     int scan_kernel;                  // 0: one CTA per tile; 1: persistent TMA pipeline; 2: runs
     uint32_t prefetch_dist;           // K1 (0): L2 bulk prefetch distance in tiles (0 = off)
     int mode;                         // record mode: 0 replace, 1 additive
+    // emit gate (K4/K5 write nothing unless the scan fitted its slots and body <= out_cap);
+    // size_out (device, may be NULL) receives the body size, or ~0 when the gate is closed
+    unsigned long long out_cap = ~0ull;
+    unsigned long long *size_out = nullptr;
 };
 
 // ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1,
@@ -133,7 +137,8 @@ cudaError_t launch_extract_emit(const ExtractArgs &a, uint8_t *out, cudaStream_t
 
 struct ApplyArgs {
     const uint8_t *body;
-    unsigned long long body_bytes;
+    unsigned long long body_bytes;                 // bytes, or the capacity when body_bytes_dev is set
+    const unsigned long long *body_bytes_dev = nullptr;  // device-resident size (chained apply)
     const TargetDesc *targets;
     uint32_t n;
     const uint8_t *names;

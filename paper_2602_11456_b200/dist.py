@@ -118,12 +118,17 @@ class NvlinkAssembler:
         self.size1 = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.token = torch.zeros(1, dtype=torch.float32, device=self.device)
 
-    def assemble(self, body: torch.Tensor, size: int, stream=None):
+    def assemble(self, body: torch.Tensor, size, stream=None):
         """Enqueue: sizes all-gather, this rank's NVLink copy into the root, completion
-        all-reduce.  Returns the assembled view on the root, None elsewhere."""
+        all-reduce.  ``size``: the body size as an int, or a one-element int64 CUDA tensor
+        (delta_extract_async's device-resident size: no host value needed).  Returns the
+        assembled buffer on the root, None elsewhere."""
         stream = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(stream):
-            self.size1.fill_(size)
+            if isinstance(size, torch.Tensor):
+                self.size1.copy_(size)
+            else:
+                self.size1.fill_(size)
             dist.all_gather_into_tensor(self.sizes, self.size1, group=self.group)
             if self.rank != self.root:
                 self.ctx.assemble(body, self.peer, self.sizes, self.rank, stream=stream)

@@ -74,6 +74,9 @@ def test_null_context_is_einval(built):
     assert lib.delta_assemble(None, None, None, 0, None, 1, 0, None) == E
     assert lib.delta_assemble_wait(None, None) == E
     assert lib.delta_digest(None, None, 0, None, None) == E
+    assert lib.delta_extract_async(None, tl, 0, 0, None, 0, c_void_p(0), None) == E
+    assert lib.delta_extract_wait(None, byref(n)) == E
+    assert lib.delta_apply_async_chain(None, tg, 0, 0, None, 0, c_void_p(0), c_void_p(0), None) == E
     assert lib.delta_last_detail(None) == 0
     assert lib.delta_last_error(None) == b"no context"
     assert b"sm_100a" in lib.delta_version()

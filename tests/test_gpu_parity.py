@@ -42,9 +42,15 @@ def _roundtrip(sd, tensors, ctx=None, check_oracle=True):
         ref_body, ref_table = oracle_extract(tensors)
         assert_body_equal(body, ref_body)
         assert [tuple(r) for r in table] == [tuple(r) for r in ref_table]
-    for hint in ("host", "none", "device"):
+    for hint in ("host", "none", "device", "chain"):
         targets = [(n, fused(o).clone()) for n, o, _ in tensors]
-        if hint == "device":  # the table left on the device by a second extract
+        if hint == "chain":  # extract -> apply with size and table on the device, one wait
+            out = torch.full((body.numel() + 64,), 0xA5, dtype=torch.uint8, device=DEV)
+            size = torch.zeros(1, dtype=torch.int64, device=DEV)
+            assert ctx.round_trip(tensors, targets, out, size) == body.numel()
+            assert int(size.item()) == body.numel()
+            assert torch.equal(out[:body.numel()], body)
+        elif hint == "device":  # the table left on the device by a second extract
             dbody, dtab = ctx.delta_extract(tensors, table="device")
             assert torch.equal(dbody, body)
             ctx.delta_apply(targets, dbody, table=dtab)
@@ -529,3 +535,53 @@ def test_additive_mode_parity(sd, dtype):
         for (_, t), r in zip(targets, ref_out):
             assert np.array_equal(to_np(t), r)
     ctx.close()
+
+
+def test_chained_round_trip_overflow_and_capacity(sd):
+    """delta_extract_async -> delta_apply_async_chain: a first call at a higher density
+    overflows the tile slots (EAGAIN, workspace grown, the chained apply refuses and
+    mutates nothing); a too-small output closes the emit gate (ECAPACITY, size = -1,
+    targets untouched); round_trip retries the overflow and matches the oracle."""
+    ctx = sd.DeltaContext(DEV)
+    spec = TensorSpec("d", (2048, 1024), "matrix")
+    o, w = generate_pair(spec, 0, 21, rho=0.4, device=DEV)  # > the initial 1/16 slots
+    tensors = [(spec.name, o, w)]
+    ref_body, _ = oracle_extract(tensors)
+    out = torch.zeros(len(ref_body) + 16, dtype=torch.uint8, device=DEV)
+    size = torch.zeros(1, dtype=torch.int64, device=DEV)
+    tgt = [(spec.name, o.clone())]
+    table = ctx.delta_extract_async(tensors, out, size)
+    ctx.delta_apply(tgt, out, table=table, size=size, wait=False)
+    with pytest.raises(sd.DeltaError) as e:
+        ctx.extract_wait()
+    assert e.value.status == -8  # DELTA_EAGAIN
+    with pytest.raises(sd.DeltaError) as e:
+        ctx.apply_wait()
+    assert e.value.kind == "layout"
+    assert int(size.item()) == -1
+    assert_lanes_equal(tgt[0][1], o)  # untouched
+    # the grown workspace now fits: the same calls succeed
+    n = ctx.round_trip(tensors, tgt, out, size)
+    assert n == len(ref_body)
+    assert_body_equal(out[:n], ref_body)
+    assert_lanes_equal(tgt[0][1], w)
+    # capacity: one byte short
+    small = torch.zeros(len(ref_body) - 1, dtype=torch.uint8, device=DEV)
+    tgt2 = [(spec.name, o.clone())]
+    table = ctx.delta_extract_async(tensors, small, size)
+    ctx.delta_apply(tgt2, small, table=table, size=size, wait=False)
+    with pytest.raises(sd.DeltaError) as e:
+        ctx.extract_wait()
+    assert e.value.status == -3
+    with pytest.raises(sd.DeltaError):
+        ctx.apply_wait()
+    assert int(size.item()) == -1
+    assert_lanes_equal(tgt2[0][1], o)
+    assert int(small.count_nonzero().item()) == 0  # nothing written
+    # a fresh context: round_trip absorbs the first-call overflow by itself
+    ctx2 = sd.DeltaContext(DEV)
+    tgt3 = [(spec.name, o.clone())]
+    assert ctx2.round_trip(tensors, tgt3, out, size) == len(ref_body)
+    assert_lanes_equal(tgt3[0][1], w)
+    ctx.close()
+    ctx2.close()
