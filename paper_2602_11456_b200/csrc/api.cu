@@ -206,7 +206,10 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     if (!c || value < 1 || value > (1 << 20)) return DELTA_EINVAL;
     if (option == DELTA_OPT_APPLY_CTAS_PER_SM) c->apply_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_EMIT_CTAS_PER_SM) c->emit_ctas_per_sm = (int)value;
-    else if (option == DELTA_OPT_SCAN_KERNEL) c->scan_kernel = (int)value - 1;
+    else if (option == DELTA_OPT_SCAN_KERNEL) {
+        if (value == 2 || value == 3 || value > 5) return DELTA_EINVAL;  // 2, 3: retired variants
+        c->scan_kernel = (int)value - 1;
+    }
     else if (option == DELTA_OPT_SCATTER_CTAS_PER_SM) c->scatter_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_PREFETCH_TILES) c->prefetch_tiles = (int)value - 1;
     else if (option == DELTA_OPT_SCATTER_ORDER) c->entry_major = value == 2;

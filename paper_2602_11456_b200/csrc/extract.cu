@@ -3,19 +3,21 @@
 //   K1  k_scan_tiles    E2+E3: the only kernel that reads the 2W bytes of weights.  One
 //                       CTA per tile (16 Ki 16-bit lanes = 32 KiB of old + 32 KiB of new),
 //                       16-byte streaming loads, bitwise lane compare, per-vector change
-//                       masks, one packed block scan for the ranks, ordered compaction into
-//                       shared memory, then the tile's workspace slot: raw values and the
-//                       LEB128 bytes of the gaps inside the tile (< 2^14 lanes: 1-2 bytes),
-//                       plus per-tile count / first / last / internal byte count.  No
-//                       inter-CTA communication: a pure streaming pass.
+//                       masks, one packed block scan for the ranks, ordered compaction
+//                       straight into the tile's workspace slot (u16 lane offsets + raw
+//                       values) and the tile's change count.  No inter-CTA communication
+//                       and no shared-memory staging: a pure streaming pass.
+//   K1b k_tiles_gaps    warp per tile: first / last offset and the LEB128 byte count of the
+//                       gaps inside the tile (< 2^14 lanes: 1-2 bytes each).
 //   K2  k_tiles_reduce / k_blocks_scan / k_tiles_bytes / k_tiles_place
 //                       E3+E4+E5 sizes: scans over the (small) per-tile metadata — entry
 //                       prefix, nearest earlier non-empty tile (its last change is the
 //                       predecessor of the tile's first change), each tile's
 //                       LEB128 bytes, byte prefix, per-tensor entry/byte begins.
 //   K3  k_finalize      E6: record sizes and offsets (the offset table), body size.
-//   K4  k_emit_tiles    E5+E6: one warp per tile writes the first gap's LEB128 bytes and
-//                       copies the pre-encoded gaps and the raw values to their final offsets.
+//   K4  k_emit_tiles    E5+E6: one warp per tile writes the LEB128 bytes of the first gap
+//                       and of the in-tile gaps (ballot-placed, 32 at a time) and copies the
+//                       raw values to their final offsets.
 //   K5  k_headers       E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
 //
 // Product code written for this library; none of it is shared with the test oracle.
@@ -84,6 +86,28 @@ __device__ __forceinline__ uint32_t diff_mask(const uint4 &a, const uint4 &b) {
     }
 }
 
+// 16-bit lanes: two masks per vector, lanes 0-3 (words x, y) and lanes 4-7 (words z, w),
+// lane k of a half at bit 8k + 7 — ascending bit order is lane order, and the pair of
+// words holding the half is what PRMT extracts lane k from (selector 0x22 k + 0x10).
+// f = ((x & 0x7FFF7FFF) + 0x7FFF7FFF) | x has bit 15 (31) set iff the low (high) 16-bit
+// half of x = a ^ b is nonzero; PRMT gathers the four high bytes of a half.
+__device__ __forceinline__ uint32_t nz16_hi(uint32_t a, uint32_t b) {
+    uint32_t t, f;
+    asm("lop3.b32 %0, %1, %2, 0x7FFF7FFF, 0x28;" : "=r"(t) : "r"(a), "r"(b));  // (a ^ b) & C
+    t += 0x7FFF7FFFu;
+    asm("lop3.b32 %0, %1, %2, %3, 0xF6;" : "=r"(f) : "r"(t), "r"(a), "r"(b));  // t | (a ^ b)
+    return f;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+__device__ __forceinline__ void diff_mask16(const uint4 &a, const uint4 &b, uint32_t &lo, uint32_t &hi) {
+    lo = __byte_perm(nz16_hi(a.x, b.x), nz16_hi(a.y, b.y), 0x7531) & 0x80808080u;
+    hi = __byte_perm(nz16_hi(a.z, b.z), nz16_hi(a.w, b.w), 0x7531) & 0x80808080u;
+}
+
 template <int NW, typename T>
 __device__ __forceinline__ T block_excl_scan(T v, T *s_warp, T &total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -126,7 +150,7 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 // ------------------------------------------------------------------------------ K1
 // THREADS x VECS = 2048 16-byte vectors per operand per tile (32 KiB); instantiated as
 // 256 x 8 (3 CTAs / SM) and 512 x 4 (2 CTAs / SM, more warps, fewer registers each).
-template <int W, int THREADS, int VECS, bool STAGED, bool ADDITIVE = false>
+template <int W, int THREADS, int VECS, bool DENSE, bool ADDITIVE = false>
 __device__ __forceinline__ void
 scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
           uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
@@ -140,12 +164,9 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     static_assert(THREADS * VECS * 16 == kTileBytes, "tile geometry is fixed by the plan");
     static_assert(LANES <= 65536, "lane offsets are u16");
     static_assert(NWARP * NQ == 32, "warp-0 scan covers NWARP warps x NQ words");
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);  // LANES
     __shared__ uint32_t s_warp[NWARP][NQ];
     __shared__ uint32_t s_pre[NWARP][NQ];
     __shared__ uint32_t s_tot[NQ];
-    __shared__ uint32_t s_red[NWARP];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TileDesc d = tiles[t];
@@ -198,10 +219,19 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
 
     // Per-vector change masks; VECS counts (<= LPV each) packed as 16-bit fields into NQ
     // words so one block scan yields every vector's rank base.
+    constexpr bool H16 = (W == 2);  // 16-bit lanes: lanes 0-3 at bits 8k+7, lanes 4-7 at bits 8k+3
     uint32_t m[VECS];
     uint32_t pk[NQ];
 #pragma unroll
-    for (int r = 0; r < VECS; ++r) m[r] = diff_mask<W>(vo[r], vn[r]);
+    for (int r = 0; r < VECS; ++r) {
+        if constexpr (H16) {
+            uint32_t lo, hi;
+            diff_mask16(vo[r], vn[r], lo, hi);
+            m[r] = lo | (hi >> 4);
+        } else {
+            m[r] = diff_mask<W>(vo[r], vn[r]);
+        }
+    }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
     uint32_t inc[NQ];
@@ -238,106 +268,74 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     // Ordered compaction: entry (r, tid, j) gets rank sum_{r'<r} tot_r' + prefix_r(tid) +
     // popc(mask below j) — lane order.  Values go straight from registers to the tile's
     // slot; lane offsets to shared memory (for the in-tile gaps below).
-    const bool fits = c <= slot_cap;
+    const bool fits = c <= slot_cap;  // CTA-uniform; an overflowing tile is redone after regrowth
+    if (tid == 0) {
+        meta[t] = TileMeta{c, 0, 0, 0, 0};  // first/last offsets and gap bytes: k_tiles_gaps
+        if (!fits) {
+            summary->overflow = 1;
+            atomicMax(&summary->max_count, (unsigned long long)c);
+        }
+    }
+    if (!fits) return;
     LT *sv = slot_val + (size_t)t * slot_cap;
+    uint16_t *sg = reinterpret_cast<uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
     uint32_t rbase = 0;
 #pragma unroll
     for (int r = 0; r < VECS; ++r) {
         const int q = r >> 1, sh = (r & 1) * 16;
-        uint32_t pos = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
-        uint32_t mm = m[r];
-        while (mm) {
-            const int j = __ffs(mm) - 1;
-            mm &= mm - 1;
-            s_off[pos] = (uint16_t)((r * THREADS + tid) * LPV + j);
-            if (fits) {
-                if constexpr (ADDITIVE)  // the arithmetic difference new - old
-                    sv[pos] = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
-                else
-                    sv[pos] = (LT)lane_of<W>(vn[r], j);
-            }
-            ++pos;
-        }
+        const uint32_t p0 = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
         rbase += (tot[q] >> sh) & 0xFFFFu;
-    }
-    __syncthreads();
-
-    if (!fits) {  // slot too small: report (host grows slots, reruns)
-        if (tid == 0) {
-            meta[t] = TileMeta{c, 0, 0, 0, 0};
-            summary->overflow = 1;
-            atomicMax(&summary->max_count, (unsigned long long)c);
-        }
-        return;
-    }
-    // The LEB128 bytes of the gaps between consecutive changes inside the tile (each
-    // < 2^14 lanes, so 1 or 2 bytes), encoded in order; the first change's gap depends on
-    // earlier tiles and is written by K4.
-    // Dense slots (slot_cap > kStageGapBytes) encode into shared memory first and copy to
-    // the slot with 16-byte stores (one byte store per thread per instruction would hit 32
-    // sectors); sparse ones write the few bytes directly (and launch with less shared
-    // memory, so more tiles stay resident).
-    constexpr bool staged = STAGED;  // == (slot_cap > kStageGapBytes), chosen at launch
-    uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;  // 16-byte aligned (slot_cap >= 8)
-    uint8_t *s_bytes = staged ? smem + LANES * sizeof(uint16_t) : sb;  // 2 * LANES bytes
-    // Each thread takes a contiguous run of entries, a multiple of 8 long, so its offsets
-    // come in as 16-byte shared loads (8 lane offsets each) instead of one dependent load
-    // per entry; gaps are taken against the previous offset carried in a register.
-    const uint32_t q = ((c + THREADS - 1) / THREADS + 7) & ~7u;
-    const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
-    const uint32_t prev0 = i0 ? s_off[i0 - 1] : 0u;
-    auto for_each_gap = [&](auto &&f) {  // f(gap) for entries max(i0, 1) .. i1 - 1, in order
-        uint32_t prev = prev0;
-        for (uint32_t b = i0; b < i1; b += 8) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(s_off + b);
-            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+        uint16_t *so = sg + p0;
+        LT *vp = sv + p0;
+        if constexpr (H16) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint32_t i = b + e;
-                const uint32_t o = (w4[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                if (i < i1 && i > 0) f(o - prev);
-                prev = o;
+            for (int h = 0; h < 2; ++h) {
+                uint32_t mm = (h ? m[r] << 4 : m[r]) & 0x80808080u;
+                const uint32_t na = h ? vn[r].z : vn[r].x, nb = h ? vn[r].w : vn[r].y;
+                const uint32_t oa = h ? vo[r].z : vo[r].x, ob = h ? vo[r].w : vo[r].y;
+                const uint32_t obase = (r * THREADS + tid) * LPV + 4 * h;
+                auto put = [&](uint32_t k, uint32_t sel) {
+                    *so++ = (uint16_t)(obase + k);
+                    const uint32_t nv = prmt(na, nb, sel);
+                    if constexpr (ADDITIVE)  // the arithmetic difference new - old
+                        *vp++ = (LT)lane_combine<W>(nv & 0xFFFFu, prmt(oa, ob, sel) & 0xFFFFu, true);
+                    else
+                        *vp++ = (LT)nv;
+                };
+                if constexpr (DENSE) {  // four predicated steps, no divergent loop
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (mm & (0x80u << (8 * k))) put(k, 0x22u * k + 0x10u);
+                } else {
+                    while (mm) {
+                        const uint32_t b = (uint32_t)__ffs(mm) - 1;  // 8k + 7
+                        mm &= mm - 1;
+                        put(b >> 3, __funnelshift_r(0x76543210u, 0u, b - 7));
+                    }
+                }
+            }
+        } else {
+            uint32_t mm = m[r];
+            while (mm) {
+                const int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                *so++ = (uint16_t)((r * THREADS + tid) * LPV + j);
+                if constexpr (ADDITIVE)
+                    *vp++ = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
+                else
+                    *vp++ = (LT)lane_of<W>(vn[r], j);
             }
         }
-    };
-    // sparse tiles: one entry per thread, simple loop (shorter critical path)
-    const uint32_t qs = (c + THREADS - 1) / THREADS;
-    const uint32_t j0 = min(c, tid * qs), j1 = min(c, j0 + qs);
-    auto for_each_gap_sparse = [&](auto &&f) {
-        for (uint32_t i = (j0 ? j0 : 1); i < j1; ++i) f((uint32_t)(s_off[i] - s_off[i - 1]));
-    };
-    auto emit = [&](uint32_t &p, uint32_t g) {
-        if (g < 128u) {
-            s_bytes[p++] = (uint8_t)g;
-        } else {
-            s_bytes[p++] = (uint8_t)(g | 0x80u);
-            s_bytes[p++] = (uint8_t)(g >> 7);
-        }
-    };
-    uint32_t L = 0;
-    if constexpr (STAGED) for_each_gap([&](uint32_t g) { L += 1u + (g >= 128u); });
-    else for_each_gap_sparse([&](uint32_t g) { L += 1u + (g >= 128u); });
-    uint32_t tl;
-    uint32_t pos = block_excl_scan<NWARP, uint32_t>(L, s_red, tl);
-    if constexpr (STAGED) for_each_gap([&](uint32_t g) { emit(pos, g); });
-    else for_each_gap_sparse([&](uint32_t g) { emit(pos, g); });
-    if constexpr (STAGED) {
-        __syncthreads();
-        for (uint32_t j = tid; j < tl / 16; j += THREADS)
-            reinterpret_cast<uint4 *>(sb)[j] = reinterpret_cast<const uint4 *>(s_bytes)[j];
-        if (tid < (tl & 15u)) sb[(tl & ~15u) + tid] = s_bytes[(tl & ~15u) + tid];
     }
-    if (tid == 0)
-        meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
 }
 
-template <int W, int THREADS, int VECS, int MINB, bool STAGED, bool ADDITIVE = false>
+template <int W, int THREADS, int VECS, int MINB, bool DENSE, bool ADDITIVE = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
              uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
              ExtractSummary *summary) {
-    scan_tile<W, THREADS, VECS, STAGED, ADDITIVE>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
+    scan_tile<W, THREADS, VECS, DENSE, ADDITIVE>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
                                 meta, summary);
 }
 
@@ -355,271 +353,28 @@ k_scan_tiles_persist(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32
     }
 }
 
-// ------------------------------------------------------------------------------ K1 (runs)
-// Variant of K1 where each thread owns one contiguous 128-byte run of the tile (64 bf16 /
-// 32 fp32 lanes) loaded with four 256-bit streaming loads per operand.  Lane order is then
-// thread order, so one single-word block scan gives every thread's rank base; the change
-// flags of a 32-bit word come from (x & 0x7FFF7FFF) + 0x7FFF7FFF | x (bit 15 / 31 set iff
-// the low / high half differs).  Values are re-read (L2) for the changed lanes only.
-template <int W>
-__global__ void __launch_bounds__(kScanThreads, 3)
-k_scan_runs(const TileDesc *__restrict__ tiles, uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
-            typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
-            ExtractSummary *summary) {
-    using LT = typename LaneOf<W>::T;
-    constexpr int RUN = kTileBytes / kScanThreads;  // 128 bytes per thread
-    constexpr int LPT = RUN / W;                     // lanes per thread
-    constexpr int NW = RUN / 4;                      // 32-bit words per thread per operand
-    static_assert(LPT <= 64, "lane mask is 64 bits");
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem);
-    __shared__ uint32_t s_w[kScanThreads / 32];
-
-    const int tid = threadIdx.x;
-    const uint32_t t = blockIdx.x;
-    const TileDesc d = tiles[t];
-    const uint32_t nl = d.nlanes;
-    const uint32_t l0 = tid * LPT;  // first lane of this thread's run
-
-    const bool full_run = (d.flags_tensor & kTileAligned) && (l0 + LPT <= nl) &&
-                          ((reinterpret_cast<uintptr_t>(d.old_p) | reinterpret_cast<uintptr_t>(d.new_p)) % 32 == 0);
-    uint32_t mlo = 0, mhi = 0;  // 64-bit change mask of the run, in lane order
-    if (full_run) {
-        uint32_t a[NW], b[NW];
-#pragma unroll
-        for (int q = 0; q < NW / 8; ++q) {
-            ld_stream_v8(d.old_p + (size_t)tid * RUN + 32 * q, a + 8 * q);
-            ld_stream_v8(d.new_p + (size_t)tid * RUN + 32 * q, b + 8 * q);
-        }
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-            const uint32_t x = a[i] ^ b[i];
-            if constexpr (W == 2) {
-                const uint32_t f = (((x & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x) & 0x80008000u;
-                const uint32_t bits = ((f >> 15) & 1u) | (f >> 30);
-                if (2 * i < 32) mlo |= bits << (2 * i);
-                else mhi |= bits << (2 * i - 32);
-            } else {
-                mlo |= (uint32_t)(x != 0) << i;
-            }
-        }
-    } else {  // ragged tail / unaligned span: lane by lane
-        const LT *op = reinterpret_cast<const LT *>(d.old_p), *nq = reinterpret_cast<const LT *>(d.new_p);
-        for (uint32_t j = 0; j < (uint32_t)LPT && l0 + j < nl; ++j) {
-            if (__ldg(op + l0 + j) != __ldg(nq + l0 + j)) {
-                if (j < 32) mlo |= 1u << j;
-                else mhi |= 1u << (j - 32);
-            }
-        }
-    }
-    const uint32_t cnt = __popc(mlo) + __popc(mhi);
-    uint32_t c;
-    const uint32_t base = block_excl_scan<kScanThreads / 32, uint32_t>(cnt, s_w, c);
-    const bool fits = c <= slot_cap;
-    LT *sv = slot_val + (size_t)t * slot_cap;
-    const LT *np = reinterpret_cast<const LT *>(d.new_p);
-    // ordered compaction: offsets to shared memory, values (re-read) to the slot
-    uint32_t pos = base, L = 0, prev = 0;
-    unsigned long long mm = ((unsigned long long)mhi << 32) | mlo;
-    while (mm) {
-        const uint32_t j = __ffsll(mm) - 1;
-        mm &= mm - 1;
-        const uint32_t off = l0 + j;
-        s_off[pos] = (uint16_t)off;
-        if (fits) sv[pos] = __ldg(np + off);
-        if (pos > base) L += 1u + ((off - prev) >= 128u);
-        prev = off;
-        ++pos;
-    }
-    __syncthreads();
-    if (!fits) {
-        if (tid == 0) {
-            meta[t] = TileMeta{c, 0, 0, 0, 0};
-            summary->overflow = 1;
-            atomicMax(&summary->max_count, (unsigned long long)c);
-        }
-        return;
-    }
-    // the first own entry's gap: predecessor is the previous thread's last entry
-    if (cnt && base > 0) L += 1u + ((uint32_t)(s_off[base] - s_off[base - 1]) >= 128u);
-    uint32_t tl;
-    uint32_t bp = block_excl_scan<kScanThreads / 32, uint32_t>(L, s_w, tl);
-    uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
-    for (uint32_t i = (base ? base : 1); i < base + cnt; ++i) {
-        const uint32_t g = s_off[i] - s_off[i - 1];
-        if (g < 128u) {
-            sb[bp++] = (uint8_t)g;
-        } else {
-            sb[bp++] = (uint8_t)(g | 0x80u);
-            sb[bp++] = (uint8_t)(g >> 7);
-        }
-    }
-    if (tid == 0)
-        meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
-}
-
-// ------------------------------------------------------------------------------ K1 (TMA)
-// Persistent variant of K1: one CTA per SM, one producer warp that streams tiles into a
-// STAGES-deep shared-memory ring with 1-D bulk copies (TMA engine, L2 evict-first) and
-// eight consumer warps that compare + compact from shared memory.  The producer runs
-// STAGES tiles ahead, so DRAM stays busy while the consumers scan and write a tile.
-// Same per-tile output as k_scan_tiles.  Tiles are assigned statically (t = CTA + i*grid).
-template <int W, int STAGES>
-__global__ void __launch_bounds__(kScanThreads + 32, 1)
-k_scan_tiles_tma(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t slot_cap,
-                 uint8_t *__restrict__ slot_bytes, typename LaneOf<W>::T *__restrict__ slot_val,
-                 TileMeta *__restrict__ meta, ExtractSummary *summary) {
-    using LT = typename LaneOf<W>::T;
-    constexpr int LPV = 16 / W;
-    constexpr uint32_t TB = kTileBytes;  // bytes per operand per tile
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint8_t *st_old = smem;
-    uint8_t *st_new = smem + STAGES * TB;
-    uint16_t *s_off = reinterpret_cast<uint16_t *>(smem + 2 * STAGES * TB);  // LANES
-    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-    __shared__ uint32_t s_warp[kScanThreads / 32][4];
-    __shared__ uint32_t s_red[kScanThreads / 32];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kScanThreads / 32);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == kScanThreads / 32) {  // ---------------------------------------- producer
+// ------------------------------------------------------------------------------ K1b
+// One warp per tile over the u16 lane offsets K1 left in the slot: the tile's first and
+// last change offsets and the LEB128 bytes of its internal gaps (each gap < 2^14 lanes:
+// 1 byte if < 128, else 2), i.e. (count - 1) + #{gaps >= 128}.
+__global__ void __launch_bounds__(256)
+k_tiles_gaps(TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t slot_cap,
+             const uint8_t *__restrict__ slot_bytes, const ExtractSummary *summary) {
+    if (summary->overflow) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t t = wg; t < ntiles; t += nw) {
+        const uint32_t c = meta[t].count;
+        if (c == 0) continue;
+        const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
+        uint32_t big = 0;
+        for (uint32_t i = 1 + lane; i < c; i += 32) big += (uint32_t)(so[i] - so[i - 1]) >= 128u;
+        big = __reduce_add_sync(0xffffffffu, big);
         if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
-            int s = 0;
-            uint32_t ph = 0;
-            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                mbar_wait(&empty[s], ph ^ 1);  // the consumers released this stage
-                const TileDesc d = tiles[t];
-                const uint32_t bytes = (d.flags_tensor & kTileAligned) ? ((d.nlanes * W) & ~15u) : 0u;
-                mbar_arrive_expect_tx(&full[s], 2 * bytes);
-                if (bytes) {
-                    bulk_g2s(st_old + s * TB, d.old_p, bytes, &full[s], pol);
-                    bulk_g2s(st_new + s * TB, d.new_p, bytes, &full[s], pol);
-                }
-                if (++s == STAGES) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-        return;
-    }
-
-    // ------------------------------------------------------------------------ consumers
-    int s = 0;
-    uint32_t ph = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const TileDesc d = tiles[t];
-        const uint32_t nl = d.nlanes;
-        const uint32_t bulk_lanes = (d.flags_tensor & kTileAligned) ? ((nl * W) & ~15u) / W : 0u;
-        uint8_t *bo = st_old + s * TB;
-        uint8_t *bn = st_new + s * TB;
-        mbar_wait(&full[s], ph);
-        if (bulk_lanes < nl) {  // ragged tail or unaligned span: the rest lane by lane
-            for (uint32_t j = bulk_lanes + tid; j < nl; j += kScanThreads) {
-                reinterpret_cast<LT *>(bo)[j] = __ldg(reinterpret_cast<const LT *>(d.old_p) + j);
-                reinterpret_cast<LT *>(bn)[j] = __ldg(reinterpret_cast<const LT *>(d.new_p) + j);
-            }
-            named_bar_sync(1, kScanThreads);
-        }
-        uint32_t m[kScanVecs];
-#pragma unroll
-        for (int r = 0; r < kScanVecs; ++r) {
-            const uint32_t v = r * kScanThreads + tid;
-            m[r] = 0;
-            if (v * LPV < nl) {
-                const uint4 a = *reinterpret_cast<const uint4 *>(bo + v * 16);
-                const uint4 b = *reinterpret_cast<const uint4 *>(bn + v * 16);
-                m[r] = diff_mask<W>(a, b);
-                if ((v + 1) * LPV > nl) m[r] &= (1u << (nl - v * LPV)) - 1u;
-            }
-        }
-        uint32_t pk[4], inc[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) inc[q] = warp_inclusive_sum(pk[q]);
-        if (lane == 31) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) s_warp[warp][q] = inc[q];
-        }
-        named_bar_sync(1, kScanThreads);
-        uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int w = 0; w < kScanThreads / 32; ++w) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t x = s_warp[w][q];
-                if (w < warp) pre[q] += x;
-                tot[q] += x;
-            }
-        }
-        uint32_t c = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) c += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
-        uint32_t rbase = 0;
-#pragma unroll
-        for (int r = 0; r < kScanVecs; ++r) {
-            const int q = r >> 1, sh = (r & 1) * 16;
-            uint32_t pos = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
-            uint32_t mm = m[r];
-            while (mm) {
-                const int j = __ffs(mm) - 1;
-                mm &= mm - 1;
-                s_off[pos++] = (uint16_t)((r * kScanThreads + tid) * LPV + j);
-            }
-            rbase += (tot[q] >> sh) & 0xFFFFu;
-        }
-        named_bar_sync(1, kScanThreads);  // s_off complete; s_warp free again
-        if (c > slot_cap) {
-            if (tid == 0) {
-                meta[t] = TileMeta{c, 0, 0, 0, 0};
-                summary->overflow = 1;
-                atomicMax(&summary->max_count, (unsigned long long)c);
-            }
-        } else {
-            uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
-            LT *sv = slot_val + (size_t)t * slot_cap;
-            for (uint32_t i = tid; i < c; i += kScanThreads) sv[i] = reinterpret_cast<const LT *>(bn)[s_off[i]];
-            const uint32_t q = (c + kScanThreads - 1) / kScanThreads;
-            const uint32_t i0 = min(c, tid * q), i1 = min(c, i0 + q);
-            uint32_t L = 0;
-            for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) L += 1u + ((s_off[i] - s_off[i - 1]) >= 128u);
-            // block exclusive scan over the 256 consumer threads (named barrier)
-            const uint32_t incl = warp_inclusive_sum(L);
-            if (lane == 31) s_red[warp] = incl;
-            named_bar_sync(1, kScanThreads);
-            uint32_t pos = incl - L, tl = 0;
-#pragma unroll
-            for (int w = 0; w < kScanThreads / 32; ++w) {
-                if (w < warp) pos += s_red[w];
-                tl += s_red[w];
-            }
-            for (uint32_t i = (i0 ? i0 : 1); i < i1; ++i) {
-                const uint32_t g = s_off[i] - s_off[i - 1];
-                if (g < 128u) {
-                    sb[pos++] = (uint8_t)g;
-                } else {
-                    sb[pos++] = (uint8_t)(g | 0x80u);
-                    sb[pos++] = (uint8_t)(g >> 7);
-                }
-            }
-            if (tid == 0)
-                meta[t] = TileMeta{c, c ? s_off[0] : (uint16_t)0, c ? s_off[c - 1] : (uint16_t)0, tl, 0};
-        }
-        named_bar_sync(1, kScanThreads);  // everyone is done with stage s, s_off, s_red
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+            meta[t].first_off = so[0];
+            meta[t].last_off = so[c - 1];
+            meta[t].internal_bytes = c - 1 + big;
         }
     }
 }
@@ -913,8 +668,10 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
     }
 }
 
-// One warp per tile: the LEB128 bytes of the tile's first gap, then the tile's pre-encoded
-// internal gaps and its raw values copied to their final offsets in the body.
+// One warp per tile: the LEB128 bytes of the tile's first gap, then the in-tile gaps
+// (differences of the slot's u16 lane offsets, < 2^14: one or two bytes each) encoded 32 at
+// a time — byte positions from a ballot of the two-byte ones — and the raw values copied
+// to their final offsets in the body.
 template <int W>
 __global__ void __launch_bounds__(256, 8)
 k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
@@ -922,6 +679,7 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
     if (summary->overflow || summary->body_bytes > cap) return;  // emit gate (async extract)
     const int lane = threadIdx.x & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
     for (uint32_t t = wg; t < ntiles; t += nw) {
@@ -937,7 +695,24 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
             }
             ib[L0 - 1] = (uint8_t)g;
         }
-        warp_copy(ib + L0, slot_bytes + (size_t)t * 2 * slot_cap, e.internal_bytes, lane);
+        const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
+        uint8_t *p = ib + L0;
+        for (uint32_t i0 = 1; i0 < e.count; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool act = i < e.count;
+            const uint32_t gi = act ? (uint32_t)(so[i] - so[i - 1]) : 0u;
+            const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
+            if (act) {
+                uint8_t *q = p + lane + __popc(two & lt_mask);
+                if (gi < 128u) {
+                    q[0] = (uint8_t)gi;
+                } else {
+                    q[0] = (uint8_t)(gi | 0x80u);
+                    q[1] = (uint8_t)(gi >> 7);
+                }
+            }
+            p += min(32u, e.count - i0) + __popc(two);
+        }
         warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), e.count * W, lane);
     }
 }
@@ -976,47 +751,25 @@ k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__res
 template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
-    constexpr int LANES = kScanThreads * kScanVecs * (16 / W);
-    // lane offsets (+ encoded gap bytes for dense slots, see scan_tile)
-    const size_t smem = (size_t)LANES * (sizeof(uint16_t) + (a.slot_cap > kStageGapBytes ? 2 : 0));
-    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_scan_tiles<W, 256, 8, 2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_scan_tiles<W, 512, 4, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // dense slots (> kStageGapBytes entries per tile seen): predicated compaction steps
+    const bool dense = a.slot_cap > kStageGapBytes;
     if (ev) cudaEventRecord(ev[0], s);
-    if (a.scan_kernel == 1) {
-        constexpr int STAGES = 3;
-        const size_t tsmem = 2 * STAGES * (size_t)kTileBytes + (size_t)LANES * sizeof(uint16_t);
-        cudaFuncSetAttribute(k_scan_tiles_tma<W, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-        const uint32_t grid = a.ntiles < (uint32_t)a.sm_count ? a.ntiles : (uint32_t)a.sm_count;
-        k_scan_tiles_tma<W, STAGES><<<grid, kScanThreads + 32, tsmem, s>>>(
-            a.tiles, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<LT *>(a.slot_val), a.meta, a.summary);
-    } else if (a.scan_kernel == 2) {
-        cudaFuncSetAttribute(k_scan_runs<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_scan_runs<W><<<a.ntiles, kScanThreads, smem, s>>>(a.tiles, a.slot_cap, a.slot_bytes,
-                                                            static_cast<LT *>(a.slot_val), a.meta, a.summary);
+    if (a.scan_kernel == 4) {
+        const uint32_t grid = a.ntiles < 3u * a.sm_count ? a.ntiles : 3u * a.sm_count;
+        k_scan_tiles_persist<W><<<grid, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
+                                                    static_cast<LT *>(a.slot_val), a.meta, a.summary);
+    } else if (a.scan_kernel == 3) {
+        k_scan_tiles<W, 512, 4, 2, false><<<a.ntiles, 512, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
+                                                                  a.slot_bytes, static_cast<LT *>(a.slot_val),
+                                                                  a.meta, a.summary);
     } else {
-        if (a.scan_kernel == 4) {
-            cudaFuncSetAttribute(k_scan_tiles_persist<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            const uint32_t grid = a.ntiles < 3u * a.sm_count ? a.ntiles : 3u * a.sm_count;
-            k_scan_tiles_persist<W><<<grid, 256, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
-                                                           a.slot_bytes, static_cast<LT *>(a.slot_val),
-                                                           a.meta, a.summary);
-        } else if (a.scan_kernel == 3)
-            k_scan_tiles<W, 512, 4, 2, false><<<a.ntiles, 512, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
-                                                                   a.slot_bytes, static_cast<LT *>(a.slot_val),
-                                                                   a.meta, a.summary);
-        else
-            (a.mode == 1 ? (a.slot_cap > kStageGapBytes ? k_scan_tiles<W, 256, 8, 2, true, true>
-                                                        : k_scan_tiles<W, 256, 8, 2, false, true>)
-                         : (a.slot_cap > kStageGapBytes ? k_scan_tiles<W, 256, 8, 3, true>
-                                                        : k_scan_tiles<W, 256, 8, 3, false>))
-                <<<a.ntiles, 256, smem, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
-                                                                   a.slot_bytes, static_cast<LT *>(a.slot_val),
-                                                                   a.meta, a.summary);
+        (a.mode == 1 ? (dense ? k_scan_tiles<W, 256, 8, 2, true, true> : k_scan_tiles<W, 256, 8, 2, false, true>)
+                     : (dense ? k_scan_tiles<W, 256, 8, 3, true> : k_scan_tiles<W, 256, 8, 3, false>))
+            <<<a.ntiles, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
+                                      static_cast<LT *>(a.slot_val), a.meta, a.summary);
     }
     if (ev) cudaEventRecord(ev[1], s);
+    k_tiles_gaps<<<a.persist_ctas, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
     k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);

@@ -14,7 +14,7 @@ constexpr int kTileBytes = kScanThreads * kScanVecs * 16;  // 32 KiB of old + 32
 constexpr int kTileBlock = 4096;   // tiles per block of the tile-level scans (1024 thr x 4)
 constexpr int kByteChunk = 4096;   // index-stream bytes per A2/A4 chunk (256 threads x 16)
 constexpr int kHalo = 16;          // bytes before a chunk kept for varints that straddle it
-constexpr uint32_t kStageGapBytes = 2048;  // K1 stages its gap bytes in smem above this slot size
+constexpr uint32_t kStageGapBytes = 2048;  // slot sizes above this: K1's predicated (dense) compaction
 
 constexpr uint32_t kTileFirstOfTensor = 1u << 31;
 constexpr uint32_t kTileAligned = 1u << 30;
@@ -47,7 +47,7 @@ struct TileEmit {
     unsigned long long vb;   // body offset of the tile's first value
     unsigned long long g0;   // gap of the tile's first change (to the previous change, or absolute)
     uint32_t count;          // changes in the tile
-    uint32_t internal_bytes; // LEB128 bytes of the gaps inside the tile (pre-encoded in the slot)
+    uint32_t internal_bytes; // LEB128 bytes of the gaps inside the tile (encoded by K4)
 };
 static_assert(sizeof(TileEmit) == 32, "TileEmit is 32 bytes");
 
