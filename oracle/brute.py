@@ -22,6 +22,12 @@ Definitions followed, in order (SURVEY.md §8(c) O1-O10 restates them):
   O9  apply: validate every record fully, then W[idx_i] = val_i
       (SPEC.md:106-110, "validate fully before mutating").
   O10 rho = sum nnz / sum N (Eq. 1).
+  F   the naive fixed-width index encoding the paper compares against
+      ("a naive int32/64 index encoding"; "two 1D arrays, idx and
+      val ... int32 or int64 (depending on tensor size)"): the
+      index stream is the nnz absolute indices, each as a little-endian
+      unsigned integer of 4 bytes if N - 1 <= 2^31 - 1, else 8 (DESIGN.md
+      reading R18); every other byte of the record is as in O6.
 """
 
 import math
@@ -120,13 +126,42 @@ def decode_indices(stream: bytes) -> list[int]:
     return idx
 
 
-def record(name: str, old: list[int], new: list[int], width: int, mode: int = MODE_REPLACE) -> bytes:
-    """O2..O6 for one fused tensor.  Additive mode: values are new - old."""
+def fixed_index_width(n: int) -> int:
+    """F ("int32 or int64 (depending on tensor size)"): 4 bytes iff the
+    largest index n - 1 fits a signed 32-bit integer."""
+    return 4 if n - 1 <= 2**31 - 1 else 8
+
+
+def encode_indices_fixed(idx: list[int], n: int) -> bytes:
+    """F: each absolute index as a little-endian integer of fixed_index_width(n) bytes."""
+    iw = fixed_index_width(n)
+    return b"".join(_u(x, iw) for x in idx)
+
+
+def decode_indices_fixed(stream: bytes, n: int) -> list[int]:
+    """Inverse of encode_indices_fixed: the stream must hold a whole number of
+    indices, strictly increasing."""
+    iw = fixed_index_width(n)
+    if len(stream) % iw:
+        raise DeltaError("truncated", f"fixed-width index stream of {len(stream)} bytes, width {iw}")
+    idx: list[int] = []
+    for pos in range(0, len(stream), iw):
+        x, _ = _read_u(stream, pos, iw)
+        if idx and x <= idx[-1]:
+            raise DeltaError("nonincreasing", f"index {x} after {idx[-1]}")
+        idx.append(x)
+    return idx
+
+
+def record(name: str, old: list[int], new: list[int], width: int, mode: int = MODE_REPLACE,
+           index_codec: str = "leb128") -> bytes:
+    """O2..O6 for one fused tensor.  Additive mode: values are new - old.
+    index_codec "fixed": the index stream of F instead of O3+O4."""
     nb = name.encode("utf-8")
     if len(nb) > 0xFFFF:
         raise DeltaError("layout", "name longer than the u16 length field (SPEC.md:148)")
     idx = changed_indices(old, new)
-    stream = encode_indices(idx)
+    stream = encode_indices(idx) if index_codec == "leb128" else encode_indices_fixed(idx, len(old))
     if mode == MODE_REPLACE:
         vals = b"".join(_u(new[j], width) for j in idx)
     else:
@@ -145,7 +180,7 @@ def record_from_sparse(name: str, n: int, idx: list[int], vals: list[int], width
 
 
 def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: int,
-            mode: int = MODE_REPLACE):
+            mode: int = MODE_REPLACE, index_codec: str = "leb128"):
     """Body and offset table for (name, old_spans, new_spans) in list order.
 
     Table rows: (record_off, N, nnz, idx_off, idx_len, val_off, record_bytes),
@@ -158,7 +193,7 @@ def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: 
                 len(a) != len(b) for a, b in zip(old_spans, new_spans)):
             raise DeltaError("shape", f"tensor {name!r}: span structure differs")
         old, new = fuse(old_spans), fuse(new_spans)
-        rec = record(name, old, new, width, mode)
+        rec = record(name, old, new, width, mode, index_codec)
         nl = len(name.encode("utf-8"))
         nnz = sum(1 for j in range(len(old)) if old[j] != new[j])
         idx_off = len(body) + 2 + nl + 24
@@ -168,7 +203,7 @@ def extract(tensors: list[tuple[str, list[list[int]], list[list[int]]]], width: 
     return bytes(body), table
 
 
-def parse(body: bytes, width: int):
+def parse(body: bytes, width: int, index_codec: str = "leb128"):
     """Split a body into records [(name, N, idx list, value list, mode)],
     decoding and validating everything."""
     recs = []
@@ -184,7 +219,8 @@ def parse(body: bytes, width: int):
         ilen, pos = _read_u(body, pos, 8)
         if pos + ilen > len(body):
             raise DeltaError("layout", f"index stream of {name!r} runs past the body")
-        idx = decode_indices(body[pos:pos + ilen])
+        stream = body[pos:pos + ilen]
+        idx = decode_indices(stream) if index_codec == "leb128" else decode_indices_fixed(stream, n)
         pos += ilen
         if len(idx) != nnz:
             raise DeltaError("count", f"{name!r}: {len(idx)} indices decoded, nnz says {nnz}")
@@ -201,11 +237,12 @@ def parse(body: bytes, width: int):
     return recs
 
 
-def apply(targets: list[tuple[str, list[int]]], body: bytes, width: int) -> list[list[int]]:
+def apply(targets: list[tuple[str, list[int]]], body: bytes, width: int,
+          index_codec: str = "leb128") -> list[list[int]]:
     """O9: returns new lane lists; raises DeltaError (inputs untouched) if any
     record is malformed or does not match its target (name, element count,
     record count)."""
-    recs = parse(body, width)
+    recs = parse(body, width, index_codec)
     if len(recs) != len(targets):
         raise DeltaError("layout", f"{len(recs)} records for {len(targets)} targets")
     for (name, n, _, _, _), (tname, lanes) in zip(recs, targets):

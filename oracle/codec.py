@@ -96,6 +96,26 @@ def decode_gaps(stream: np.ndarray) -> np.ndarray:
     return g
 
 
+# ---- naive fixed-width index encoding (reading R18): the
+# index stream is the absolute indices as little-endian u32 if N - 1 <= 2^31 - 1, else u64.
+def fixed_index_width(n: int) -> int:
+    return 4 if n - 1 <= 2**31 - 1 else 8
+
+
+def encode_fixed(idx: np.ndarray, n: int) -> np.ndarray:
+    dt = np.dtype("<u4") if fixed_index_width(n) == 4 else np.dtype("<u8")
+    return idx.astype(dt).view(np.uint8)
+
+
+def decode_fixed(stream: np.ndarray, n: int) -> np.ndarray:
+    """Inverse of encode_fixed; strictly increasing is checked by the caller (parse)."""
+    iw = fixed_index_width(n)
+    stream = np.ascontiguousarray(stream, dtype=np.uint8)
+    if stream.size % iw:
+        raise DeltaError("truncated", f"fixed-width index stream of {stream.size} bytes, width {iw}")
+    return stream.view("<u4" if iw == 4 else "<u8").astype(np.uint64)
+
+
 # ---- additive mode (SPEC.md:99, 135: "the arithmetic difference when mode=additive";
 # scatter-ADD on apply, PAPER.md:384).  Lanes are read as bf16 (16-bit) or fp32 (32-bit);
 # the difference and the sum are taken in fp32 and rounded to the lane type with
@@ -136,14 +156,16 @@ def lane_add(w: np.ndarray, val: np.ndarray) -> np.ndarray:
         return _canon_f32(w.view(np.float32) + val.view(np.float32))
 
 
-def record(name: str, old: np.ndarray, new: np.ndarray, mode: int = MODE_REPLACE) -> bytes:
+def record(name: str, old: np.ndarray, new: np.ndarray, mode: int = MODE_REPLACE,
+           index_codec: str = "leb128") -> bytes:
     """O2..O6 for one fused tensor (SPEC.md:148 layout, little-endian).  mode 0: values are
-    the new lanes (replace, reading R1); mode 1: the arithmetic differences (additive)."""
+    the new lanes (replace, reading R1); mode 1: the arithmetic differences (additive).
+    index_codec "fixed": absolute fixed-width indices (reading R18) instead of O3+O4."""
     nb = name.encode("utf-8")
     if len(nb) > 0xFFFF:
         raise DeltaError("layout", "name longer than the u16 length field")
     idx = changed_indices(old, new)
-    stream = encode_gaps(gaps(idx))
+    stream = encode_gaps(gaps(idx)) if index_codec == "leb128" else encode_fixed(idx, old.size)
     ii = idx.astype(np.int64)
     vals = new[ii] if mode == MODE_REPLACE else lane_sub(new[ii], old[ii])
     vals = vals.astype(new.dtype.newbyteorder("<"), copy=False)
@@ -161,7 +183,7 @@ def table_row(record_off: int, rec: bytes) -> tuple:
     return (record_off, n, nnz, idx_off, ilen, idx_off + ilen, len(rec))
 
 
-def extract(tensors, mode: int = MODE_REPLACE):
+def extract(tensors, mode: int = MODE_REPLACE, index_codec: str = "leb128"):
     """tensors: [(name, old_spans, new_spans)] -> (body bytes, table rows).
     Records appear in list order (reading R15), one per tensor even
     when nothing changed (R12)."""
@@ -169,14 +191,14 @@ def extract(tensors, mode: int = MODE_REPLACE):
     for name, old_spans, new_spans in tensors:
         if len(old_spans) != len(new_spans):
             raise DeltaError("shape", f"{name!r}: span count differs")
-        rec = record(name, fuse(old_spans), fuse(new_spans), mode)
+        rec = record(name, fuse(old_spans), fuse(new_spans), mode, index_codec)
         table.append(table_row(off, rec))
         parts.append(rec)
         off += len(rec)
     return b"".join(parts), table
 
 
-def parse(body, width: int):
+def parse(body, width: int, index_codec: str = "leb128"):
     """Walk and fully validate a body: [(name, N, idx uint64, vals)]."""
     body = memoryview(bytes(body))
     recs, pos = [], 0
@@ -195,12 +217,20 @@ def parse(body, width: int):
         end = p + ilen + nnz * width + 1
         if end > len(body):
             raise DeltaError("layout", f"{name!r}: record runs past the body")
-        g = decode_gaps(np.frombuffer(body[p:p + ilen], dtype=np.uint8))
-        if g.size != nnz:
-            raise DeltaError("count", f"{name!r}: {g.size} indices decoded, nnz says {nnz}")
-        if g.size > 1 and (g[1:] == 0).any():
-            raise DeltaError("nonincreasing", f"{name!r}: zero gap")
-        idx = np.cumsum(g, dtype=np.uint64)
+        stream = np.frombuffer(body[p:p + ilen], dtype=np.uint8)
+        if index_codec == "leb128":
+            g = decode_gaps(stream)
+            if g.size != nnz:
+                raise DeltaError("count", f"{name!r}: {g.size} indices decoded, nnz says {nnz}")
+            if g.size > 1 and (g[1:] == 0).any():
+                raise DeltaError("nonincreasing", f"{name!r}: zero gap")
+            idx = np.cumsum(g, dtype=np.uint64)
+        else:
+            idx = decode_fixed(stream, n)
+            if idx.size != nnz:
+                raise DeltaError("count", f"{name!r}: {idx.size} indices decoded, nnz says {nnz}")
+            if idx.size > 1 and (idx[1:] <= idx[:-1]).any():
+                raise DeltaError("nonincreasing", f"{name!r}: indices not strictly increasing")
         if idx.size and ((idx[1:] <= idx[:-1]).any() or idx[-1] >= np.uint64(n)):
             # a wrap of the 64-bit running sum also lands here: such an index
             # is >= 2^64 > N, i.e. out of range.
@@ -214,11 +244,11 @@ def parse(body, width: int):
     return recs
 
 
-def apply(targets, body, width: int, inplace: bool = False):
+def apply(targets, body, width: int, inplace: bool = False, index_codec: str = "leb128"):
     """O9: targets [(name, lanes)]; validate everything, then
     W[idx] = vals.  Returns the updated lane arrays (copies unless inplace).
     On any DeltaError no target has been modified."""
-    recs = parse(body, width)
+    recs = parse(body, width, index_codec)
     if len(recs) != len(targets):
         raise DeltaError("layout", f"{len(recs)} records for {len(targets)} targets")
     for (name, n, _, _, _), (tname, w) in zip(recs, targets):

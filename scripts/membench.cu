@@ -68,6 +68,93 @@ __global__ void k_scatter_sector(uint16_t *w, const unsigned long long *pos, con
     }
 }
 
+// v3 warp-batched sector read-modify-write: a warp takes 256 consecutive entries, loads
+// every 32-byte sector they touch with lane-pair 16-byte loads (several in flight), merges
+// the lanes in shared memory and writes the sectors back whole (lane pairs: full-sector
+// writes, no L2 fill).  The run's first / last sectors may be shared with the neighbouring
+// runs: those entries are stored lane-wise.  HINT 1: loads evict_first / stores evict_first.
+template <int HINT>
+__global__ void __launch_bounds__(128) k_scatter_batch(uint16_t *w, const unsigned long long *pos, const uint16_t *val, size_t n) {
+    __shared__ uint4 s_sec[4][256][2];
+    __shared__ unsigned long long s_addr[4][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t nrun = (n + 255) / 256;
+    const size_t nw = (size_t)gridDim.x * 4;
+    const uint32_t le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+    for (size_t r = (size_t)blockIdx.x * 4 + warp; r < nrun; r += nw) {
+        const size_t b = r * 256, e = b + 256 < n ? b + 256 : n;
+        const unsigned long long fs = pos[b] >> 4, ls = pos[e - 1] >> 4;
+        unsigned long long sec[8];
+        uint16_t v[8];
+        uint32_t rank[8];
+        uint32_t off[8];
+        bool inter[8];
+        uint32_t base = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const size_t i = b + 32 * j + lane;
+            const bool act = i < e;
+            const unsigned long long p = act ? pos[i] : ~0ull;
+            v[j] = act ? val[i] : 0;
+            sec[j] = p >> 4;
+            off[j] = (uint32_t)(p & 15);
+            unsigned long long ps = __shfl_up_sync(0xffffffffu, sec[j], 1);
+            const unsigned long long carry = __shfl_sync(0xffffffffu, sec[j ? j - 1 : 0], 31);
+            if (lane == 0) ps = j ? carry : ~0ull;
+            inter[j] = act && sec[j] != fs && sec[j] != ls;
+            const bool lead = inter[j] && sec[j] != ps;
+            const uint32_t bal = __ballot_sync(0xffffffffu, lead);
+            rank[j] = base + __popc(bal & le) - 1;
+            if (lead) s_addr[warp][rank[j]] = sec[j];
+            base += __popc(bal);
+            if (act && !inter[j]) w[p] = v[j];
+        }
+        __syncwarp();
+        const uint32_t nl = base;
+        for (uint32_t q0 = 0; q0 < nl; q0 += 64) {
+            uint4 t[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t q = q0 + 16 * k + (lane >> 1);
+                if (q < nl) {
+                    const uint4 *src = reinterpret_cast<const uint4 *>(w + (s_addr[warp][q] << 4)) + (lane & 1);
+                    if (HINT) asm volatile("ld.global.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(t[k].x), "=r"(t[k].y), "=r"(t[k].z), "=r"(t[k].w) : "l"(src));
+                    else t[k] = *src;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t q = q0 + 16 * k + (lane >> 1);
+                if (q < nl) s_sec[warp][q][lane & 1] = t[k];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (inter[j]) reinterpret_cast<uint16_t *>(&s_sec[warp][rank[j]][0])[off[j]] = v[j];
+        __syncwarp();
+        for (uint32_t q = lane >> 1; q < nl; q += 16)
+            reinterpret_cast<uint4 *>(w + (s_addr[warp][q] << 4))[lane & 1] = s_sec[warp][q][lane & 1];
+        __syncwarp();
+    }
+}
+
+// v5/v6: plain one-thread-per-entry stores with an L2 eviction-priority policy
+template <int POL>
+__global__ void k_scatter_hint(uint16_t *w, const unsigned long long *pos, const uint16_t *val, size_t n) {
+    unsigned long long pol;
+    if (POL == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const unsigned short x = val[i];
+        asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(w + pos[i]), "h"(x), "l"(pol) : "memory");
+    }
+}
+
+// v7: plain, one warp per 32 consecutive entries but the grid sweeps the entries in narrow
+// windows: CTA b handles entries [k*S + b*256, ...) for k = 0.. (S = grid*256) — same as plain
+// with a grid of 148 CTAs (small window in flight)
 extern "C" {
 int mb_read(const void *p, size_t bytes, void *out, int grid, int block, cudaStream_t s) {
     k_read<<<grid, block, 0, s>>>(static_cast<const uint4 *>(p), bytes / 16, static_cast<unsigned long long *>(out));
@@ -79,7 +166,11 @@ int mb_scatter(int variant, void *w, const void *pos, const void *val, size_t n,
     auto V = static_cast<const uint16_t *>(val);
     if (variant == 0) k_scatter_plain<<<grid, block, 0, s>>>(W, P, V, n);
     else if (variant == 1) k_scatter_pf<<<grid, block, 0, s>>>(W, P, V, n);
-    else k_scatter_sector<<<grid, block, 0, s>>>(W, P, V, n);
+    else if (variant == 2) k_scatter_sector<<<grid, block, 0, s>>>(W, P, V, n);
+    else if (variant == 3) k_scatter_batch<0><<<grid, 128, 0, s>>>(W, P, V, n);
+    else if (variant == 4) k_scatter_batch<1><<<grid, 128, 0, s>>>(W, P, V, n);
+    else if (variant == 5) k_scatter_hint<0><<<grid, block, 0, s>>>(W, P, V, n);
+    else if (variant == 6) k_scatter_hint<1><<<grid, block, 0, s>>>(W, P, V, n);
     return (int)cudaGetLastError();
 }
 }

@@ -44,7 +44,7 @@ def main():
     buf = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
     buf.random_(0, 255)
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
-    for grid_mul, block in ((4, 512), (8, 256), (16, 256), (32, 256)):
+    for grid_mul, block in (() if os.environ.get("MB_SCATTER") else ((4, 512), (8, 256), (16, 256), (32, 256))):
         ms = timeit(lambda: L.mb_read(ctypes.c_void_p(buf.data_ptr()), ctypes.c_size_t(buf.numel()),
                                       ctypes.c_void_p(out.data_ptr()), sm * grid_mul, block, st))
         print(json.dumps({"bench": "read", "grid": sm * grid_mul, "block": block, "ms": ms,
@@ -63,15 +63,32 @@ def main():
     del pos_chunks
     val = torch.randint(0, 65535, (pos.numel(),), dtype=torch.int32, device="cuda").to(torch.int16)
     w = buf.view(torch.int16)
-    for variant, name in ((0, "plain"), (1, "prefetch_L2"), (2, "sector_merge")):
-        for grid_mul, block in ((8, 256), (32, 256)):
-            ms = timeit(lambda: L.mb_scatter(variant, ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(pos.data_ptr()),
-                                             ctypes.c_void_p(val.data_ptr()), ctypes.c_size_t(pos.numel()),
-                                             sm * grid_mul, block, st))
+    only = os.environ.get("MB_SCATTER")
+    variants = ((0, "plain"), (1, "prefetch_L2"), (2, "sector_merge"), (3, "batch_sector_rmw"),
+                (4, "batch_sector_rmw_noL1"), (5, "plain_evict_first"), (6, "plain_evict_last"))
+    init = w.clone()
+    ref = None
+    for variant, name in variants:
+        if only and str(variant) not in only.split(","):
+            continue
+        shapes = ((8, 256), (32, 256)) if variant < 3 or variant > 4 else ((16, 128), (64, 128))
+        for grid_mul, block in shapes:
+            def run():
+                return L.mb_scatter(variant, ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(pos.data_ptr()),
+                                    ctypes.c_void_p(val.data_ptr()), ctypes.c_size_t(pos.numel()),
+                                    sm * grid_mul, block, st)
+            w.copy_(init)
+            run()
+            torch.cuda.synchronize()
+            if ref is None:
+                ref = w.clone()
+                ok = True
+            else:
+                ok = bool(torch.equal(w, ref))
+            ms = timeit(run)
             print(json.dumps({"bench": f"scatter_{name}", "entries": pos.numel(), "grid": sm * grid_mul,
-                              "block": block, "ms": ms,
+                              "block": block, "ms": ms, "matches_plain": ok,
                               "Gstores_per_s": pos.numel() / ms / 1e6}), flush=True)
-
 
 if __name__ == "__main__":
     sys.exit(main())
