@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--index-codec", default="leb128", choices=["leb128", "fixed"],
+                   help="fixed: the paper's naive int32/64 index encoding (PAPER.md:387, 609; R18)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -158,7 +160,8 @@ class OracleSample:
     cuda:0 when there is one, then copied to host) until the estimated oracle time reaches
     ``budget_s``."""
 
-    def __init__(self, specs, rho, pattern, seed, dtype, budget_s):
+    def __init__(self, specs, rho, pattern, seed, dtype, budget_s, index_codec="leb128"):
+        self.index_codec = index_codec
         import numpy as np
         import torch
 
@@ -193,8 +196,8 @@ class OracleSample:
 
     def _one(self, item):
         name, on, wn = item
-        body, _ = self.oracle.codec.extract([(name, [on], [wn])])
-        got = self.oracle.codec.apply([(name, on)], body, on.dtype.itemsize)[0]
+        body, _ = self.oracle.codec.extract([(name, [on], [wn])], index_codec=self.index_codec)
+        got = self.oracle.codec.apply([(name, on)], body, on.dtype.itemsize, index_codec=self.index_codec)[0]
         return got
 
     def run(self):
@@ -220,7 +223,7 @@ def run_reference(args):
     specs, rho, pattern, desc = workload(args)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     budget = max(0.5, min(args.cpu_seconds, 90.0 / max(1, args.steps + args.warmup)))
-    smp = OracleSample(specs, rho, pattern, args.seed, dtype, budget)
+    smp = OracleSample(specs, rho, pattern, args.seed, dtype, budget, args.index_codec)
     for _ in range(args.warmup):
         smp.run()
     vals, secs = [], 0.0
@@ -335,6 +338,8 @@ def main():
             ctx.set_option(5, args.prefetch_tiles)
         if args.scatter_order:
             ctx.set_option(6, args.scatter_order)
+        if args.index_codec == "fixed":
+            ctx.set_option(8, 2)
         ctx.set_profiling(True)
         size0 = ctx.delta_size(tl)
         out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
@@ -463,7 +468,8 @@ def main():
         "config": {"workload": desc, "config": args.config, "tensors": len(specs),
                    "lanes": total_lanes, "weights_bytes": total_lanes * width,
                    "scanned_bytes_per_step": scanned_total, "rho": rho, "pattern": pattern,
-                   "seed": args.seed, "shard": "contiguous balanced tensor ranges",
+                   "seed": args.seed, "index_codec": args.index_codec,
+                   "shard": "contiguous balanced tensor ranges",
                    "l2": f"inputs ({scanned_total / 1e9:.1f} GB per step) larger than L2 (126 MB); no flush"},
         "payload": {"body_bytes": body_total, "ratio": round(total_lanes * width / body_total, 3),
                     "nnz": nnz_total, "rho_measured": nnz_total / total_lanes,
@@ -493,7 +499,7 @@ def main():
         result["e2e"] = e2e(args, step, olds, news, body_local, dev, scanned_total, world)
     # ---- CPU oracle beside it (rank 0, N=1 only)
     if not args.no_cpu_baseline and world == 1:
-        smp = OracleSample(specs, rho, pattern, args.seed, dtype, args.cpu_seconds)
+        smp = OracleSample(specs, rho, pattern, args.seed, dtype, args.cpu_seconds, args.index_codec)
         v, secs = smp.run()
         result["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                                   "sample": smp.sample, "seconds": round(secs, 2),
