@@ -291,13 +291,37 @@ enum {
     DELTA_OPT_SCATTER_ORDER = 6,      /* 1 = each thread stores the entries it decoded,
                                          2 = entry-major: thread i stores entries i, i+256, ...
                                          (default for 16-bit lanes) */
-    DELTA_OPT_MODE = 7                /* records written by extract: 1 = replace (default; values
+    DELTA_OPT_MODE = 7,               /* records written by extract: 1 = replace (default; values
                                          are the new lanes, apply stores them, bit-exact),
                                          2 = additive (values are new - old and apply adds them,
                                          SPEC.md:99, 135: 16-bit lanes read as bf16, 32-bit as
                                          fp32, fp32 arithmetic rounded to nearest even — lossy,
                                          for fidelity experiments).  delta_apply follows each
                                          record's mode byte. */
+    DELTA_OPT_INDEX_CODEC = 8,        /* index stream of the records, for delta_extract* AND
+                                         delta_apply* on this ctx (the body does not say which;
+                                         the SPDC container's format_version does: 1 / 2):
+                                         1 = LEB128 gaps (default);
+                                         2 = the naive fixed-width encoding the paper compares
+                                         against ("int32 or int64 (depending on tensor
+                                         size)"): nnz absolute indices, little-endian,
+                                         4 bytes if element_count - 1 <= 2^31 - 1 else 8, so
+                                         index_bytes = nnz x width (reading R18).  Apply
+                                         of a fixed-width body: index_bytes not a multiple of the
+                                         width -> DELTA_D_TRUNCATED, != nnz indices -> DELTA_D_COUNT,
+                                         not strictly increasing -> DELTA_D_NONINCREASING, an index
+                                         >= element_count -> DELTA_D_RANGE (all-or-nothing as ever). */
+    DELTA_OPT_ADVANCE = 9             /* extract-and-advance (NEXT f3; the trainer keeps W_t only to
+                                         diff it against W_{t+1}): 2 = the
+                                         compare kernel also stores every changed lane of new into
+                                         old, so after delta_size / delta_extract every old_dev span
+                                         equals its new_dev span bitwise (old_dev must then be
+                                         writable; unchanged lanes are not written).  The body is
+                                         unchanged.  1 = off (default).  Replace mode only
+                                         (DELTA_EINVAL with DELTA_OPT_MODE = 2); delta_extract_async
+                                         returns DELTA_EINVAL while it is on (a slot-overflow retry
+                                         needs the host).  A second extract of the same pair after
+                                         an advance sees no change (all records empty). */
 };
 
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */

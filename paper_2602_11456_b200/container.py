@@ -1,6 +1,7 @@
 """SPDC delta-checkpoint container, host side.
 
-Header (67 bytes, little-endian): "SPDC" | format_version u16 (= 1) | version u64 |
+Header (67 bytes, little-endian): "SPDC" | format_version u16 (1 = LEB128 index streams,
+2 = fixed-width indices, R18) | version u64 |
 base_version u64 | element-type code u8 (0 = 16-bit, 1 = 32-bit) | tensor count u32 |
 body length u64 | BLAKE3-256 of exactly the body bytes (readings R9, R10).
 The body is what ``delta_extract`` writes.  The digest is computed on the GPU
@@ -17,7 +18,11 @@ _FMT = "<4sHQQBIQ32s"
 HEADER_BYTES = struct.calcsize(_FMT)
 
 
-def pack_container(body, version: int, base_version: int, width: int, n_tensors: int, ctx=None) -> bytes:
+_FORMAT = {"leb128": 1, "fixed": 2}
+
+
+def pack_container(body, version: int, base_version: int, width: int, n_tensors: int, ctx=None,
+                   index_codec: str = "leb128") -> bytes:
     """``body``: a uint8 CUDA tensor (as written by delta_extract) or host bytes (uploaded
     first).  The digest is always computed on the GPU (delta_digest)."""
     import torch
@@ -30,17 +35,18 @@ def pack_container(body, version: int, base_version: int, width: int, n_tensors:
         body = torch.frombuffer(bytearray(bytes(body)) or bytearray(1), dtype=torch.uint8)[:len(body)].cuda()
     h = (ctx or context(body.device)).digest(body)
     raw = body.cpu().numpy().tobytes()
-    return struct.pack(_FMT, _MAGIC, 1, version, base_version, code, n_tensors, len(raw), h) + raw
+    return struct.pack(_FMT, _MAGIC, _FORMAT[index_codec], version, base_version, code, n_tensors, len(raw), h) + raw
 
 
-def unpack_container(blob: bytes):
+def unpack_container(blob: bytes, index_codec: str = "leb128"):
     """-> (version, base_version, width, n_tensors, body); raises ValueError if the
-    magic, format version, length or hash does not match."""
+    magic, format version (1 for index_codec "leb128", 2 for "fixed"), length or hash
+    does not match."""
     if len(blob) < HEADER_BYTES:
         raise ValueError("short container")
     magic, fv, ver, base, code, nt, blen, h = struct.unpack_from(_FMT, blob, 0)
-    if magic != _MAGIC or fv != 1 or code not in (0, 1):
-        raise ValueError("not an SPDC v1 container")
+    if magic != _MAGIC or fv != _FORMAT[index_codec] or code not in (0, 1):
+        raise ValueError(f"not an SPDC v{_FORMAT[index_codec]} container")
     body = bytes(blob[HEADER_BYTES:])
     if len(body) != blen or blake3.blake3(body).digest() != h:
         raise ValueError("body length or hash mismatch")

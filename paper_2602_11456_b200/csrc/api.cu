@@ -98,6 +98,8 @@ struct delta_ctx {
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
     bool entry_major = true;
     int mode = 0;  // records written by extract: 0 replace, 1 additive
+    int index_codec = 0;  // 0 LEB128 gaps, 1 fixed-width absolute indices (extract and apply)
+    bool advance = false;  // extract-and-advance: old_dev is overwritten with new (synchronous extract only)
 
     // ---- optional per-kernel event timing
     bool profiling = false;
@@ -214,9 +216,20 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     else if (option == DELTA_OPT_PREFETCH_TILES) c->prefetch_tiles = (int)value - 1;
     else if (option == DELTA_OPT_SCATTER_ORDER) c->entry_major = value == 2;
     else if (option == DELTA_OPT_MODE) {
-        if (value > 2) return DELTA_EINVAL;
+        if (value > 2 || (value == 2 && c->advance)) return DELTA_EINVAL;
         if (c->mode != (int)value - 1) c->scan_cached = false;
         c->mode = (int)value - 1;
+    }
+    else if (option == DELTA_OPT_ADVANCE) {
+        if (value > 2) return DELTA_EINVAL;
+        if (value == 2 && c->mode != 0) return DELTA_EINVAL;  // replace mode only
+        c->advance = value == 2;
+        c->scan_cached = false;
+    }
+    else if (option == DELTA_OPT_INDEX_CODEC) {
+        if (value > 2) return DELTA_EINVAL;
+        if (c->index_codec != (int)value - 1) c->scan_cached = false;
+        c->index_codec = (int)value - 1;
     }
     else return DELTA_EINVAL;
     return DELTA_OK;
@@ -392,6 +405,8 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.scan_kernel = ctx->scan_kernel;
     a.prefetch_dist = (uint32_t)(ctx->prefetch_tiles < 0 ? ctx->sm_count * 3 : ctx->prefetch_tiles);
     a.mode = ctx->mode;
+    a.index_codec = ctx->index_codec;
+    a.advance = ctx->advance;
     return a;
 }
 
@@ -434,10 +449,12 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
     const uint32_t lanes_per_tile = kTileBytes / ctx->width;
     int rc0 = prepare_scan(ctx);
     if (rc0) return rc0;
+    uint32_t redo_cap = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
-        CK(launch_extract_scan(extract_args(ctx), s, ctx->profiling ? ctx->ev_scan : nullptr),
-           "extract scan launch");
+        ExtractArgs a = extract_args(ctx);
+        a.redo_cap = redo_cap;
+        CK(launch_extract_scan(a, s, ctx->profiling ? ctx->ev_scan : nullptr), "extract scan launch");
         CK(cudaMemcpyAsync(ctx->h_summary, ctx->summary.p, sizeof(ExtractSummary), cudaMemcpyDeviceToHost, s), "readback");
         CK(cudaStreamSynchronize(s), "extract scan");
         if (ctx->profiling) {
@@ -451,7 +468,28 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
         }
         uint32_t need = 2;
         while (need < ctx->h_summary->max_count) need <<= 1;
-        int rc = reserve_slots(ctx, std::min(need, lanes_per_tile));
+        need = std::min(need, lanes_per_tile);
+        if (ctx->advance) {
+            // the tiles that fitted were compacted AND advanced (old == new there now): keep
+            // their slots, move them into the larger layout, and redo only the overflowed tiles
+            DevBuf nb, nv;
+            if (nb.grow((size_t)ctx->ntiles * need * 2 + 64) || nv.grow((size_t)ctx->ntiles * need * ctx->width + 64)) {
+                nb.release();
+                nv.release();
+                return fail(ctx, DELTA_ENOMEM, 0, "slot regrowth allocation failed");
+            }
+            CK(launch_slots_regrow(ctx->meta.as<TileMeta>(), ctx->ntiles, ctx->width, ctx->slot_cap, ctx->slot_bytes.p,
+                                   ctx->slot_val.p, need, nb.p, nv.p, ctx->sm_count * 8, s), "slot regrowth");
+            CK(cudaStreamSynchronize(s), "slot regrowth");
+            ctx->slot_bytes.release();
+            ctx->slot_val.release();
+            ctx->slot_bytes = nb;
+            ctx->slot_val = nv;
+            redo_cap = ctx->slot_cap;
+            ctx->slot_cap = need;
+            continue;
+        }
+        int rc = reserve_slots(ctx, need);
         if (rc) return rc;
     }
     return fail(ctx, DELTA_ENOMEM, 0, "tile slot overflow after resize");
@@ -532,6 +570,8 @@ extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32
     const int w = elem_width(elem);
     if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
     if (cap && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
+    if (ctx->advance)  // an overflow retry needs the host: extract-and-advance is synchronous only
+        return fail(ctx, DELTA_EINVAL, 0, "DELTA_OPT_ADVANCE needs delta_size / delta_extract");
     if (reinterpret_cast<uintptr_t>(body_bytes_dev) % 8)
         return fail(ctx, DELTA_EINVAL, 0, "body_bytes_dev not 8-byte aligned");
     int rc = validate_tensors(ctx, t, n, w);
@@ -689,6 +729,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.persist_ctas = ctx->sm_count * ctx->apply_ctas_per_sm;
     a.scatter_ctas = ctx->sm_count * ctx->scatter_ctas_per_sm;
     a.entry_major = ctx->entry_major;
+    a.index_codec = ctx->index_codec;
     CK(launch_apply(a, s, ctx->profiling ? ctx->ev_apply : nullptr), "apply launch");
     return DELTA_OK;
 }

@@ -41,7 +41,7 @@ __device__ __forceinline__ unsigned long long rd_le(const uint8_t *p, int nbytes
 // record's geometry.  Bounds are checked before every read (the body is untrusted).
 __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_bytes,
                                  unsigned long long ro, const TargetDesc &tg,
-                                 const uint8_t *names, int width, ApplyRec &rec,
+                                 const uint8_t *names, int width, int fixed, ApplyRec &rec,
                                  unsigned long long &end) {
     if (ro > body_bytes || body_bytes - ro < 2) return kLayout;
     const unsigned long long nl = rd_le(body + ro, 2);
@@ -61,6 +61,11 @@ __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_by
     for (unsigned long long b = 0; b < nl; ++b)
         if (body[ro + 2 + b] != names[tg.name_off + b]) return kName;
     if (N != tg.numel) return kNumel;
+    if (fixed) {  // reading R18: a whole number of fixed-width indices, one per entry
+        const uint32_t iw = fixed_index_width(N);
+        if (ilen % iw) return kTruncated;
+        if (ilen / iw != nnz) return kCount;
+    }
     rec.idx_off = q;
     rec.idx_len = ilen;
     rec.val_off = q + ilen;
@@ -77,7 +82,7 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
          const TargetDesc *__restrict__ tg, uint32_t n, const uint8_t *__restrict__ names,
          const RecordRow *__restrict__ hint, ApplyRec *__restrict__ recs,
          unsigned long long *__restrict__ rec_chunk_begin, uint32_t *__restrict__ chunk_rec, ApplyState *st,
-         int width) {
+         int width, int fixed) {
     if (body_bytes_dev != nullptr) {  // chained after delta_extract_async: size on the device
         const unsigned long long b = *body_bytes_dev;
         if (b > body_bytes) {  // ~0: the extract's gate was closed (no body was written)
@@ -99,7 +104,7 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
             ApplyRec r;
             unsigned long long end = 0;
             if (h.record_offset != expect_ro ||
-                check_record(body, body_bytes, h.record_offset, tg[k], names, width, r, end) != kOk ||
+                check_record(body, body_bytes, h.record_offset, tg[k], names, width, fixed, r, end) != kOk ||
                 end - h.record_offset != h.record_bytes || r.idx_off != h.index_offset ||
                 r.idx_len != h.index_bytes || r.nnz != h.nnz || r.val_off != h.values_offset ||
                 (k == n - 1 && end != body_bytes)) {
@@ -115,7 +120,7 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
         uint32_t code = kOk;
         for (uint32_t k = 0; k < n && code == kOk; ++k) {
             unsigned long long end = 0;
-            code = check_record(body, body_bytes, pos, tg[k], names, width, recs[k], end);
+            code = check_record(body, body_bytes, pos, tg[k], names, width, fixed, recs[k], end);
             pos = end;
         }
         if (code == kOk && pos != body_bytes) code = kLayout;
@@ -582,12 +587,117 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     }
 }
 
+// ------------------------------------------------------------------------------ A2f / A4f
+// Fixed-width index codec (reading R18): chunk c of a record holds entries
+// [c * kByteChunk / iw, ...) of its absolute index array.  The chunk's indices (plus the
+// previous entry's, for the strictly-increasing check across chunks) are staged in shared
+// memory with 16-byte loads; the body gives no alignment.
+template <int IW>
+__device__ __forceinline__ unsigned long long fixed_at(const uint8_t *p) {
+    unsigned long long x = 0;
+#pragma unroll
+    for (int b = 0; b < IW; ++b) x |= (unsigned long long)p[b] << (8 * b);
+    return x;
+}
+
+__device__ __forceinline__ const uint8_t *stage_fixed_chunk(const uint8_t *body, const ApplyRec &R,
+                                                            unsigned long long j, uint32_t iw, uint8_t *buf,
+                                                            uint32_t &len, unsigned long long &cs) {
+    cs = j * kByteChunk;
+    const unsigned long long ce = min(R.idx_len, cs + kByteChunk);
+    len = (uint32_t)(ce - cs);
+    const uint32_t hs = cs ? iw : 0u;  // the previous entry
+    return stage_bytes(buf, body + R.idx_off + cs - hs, hs + len) + hs;
+}
+
+// Validation: idx[e] > idx[e - 1] (e >= 1), idx[e] < N.
+__global__ void __launch_bounds__(256)
+k_fixed_validate(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs,
+                 const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
+                 ApplyState *st) {
+    if (st->status != kOk) return;
+    const unsigned long long nch = st->n_chunks;
+    __shared__ __align__(16) uint8_t sb[kByteChunk + 48];
+    for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        const uint32_t k = __ldg(chunk_rec + c);
+        const ApplyRec R = recs[k];
+        const uint32_t iw = fixed_index_width(R.numel);
+        uint32_t len;
+        unsigned long long cs;
+        const uint8_t *b = stage_fixed_chunk(body, R, c - __ldg(rcb + k), iw, sb, len, cs);
+        __syncthreads();
+        uint32_t err = kOk;
+        for (uint32_t i = threadIdx.x; i < len / iw; i += blockDim.x) {
+            const uint8_t *p = b + (size_t)i * iw;
+            const unsigned long long x = iw == 4 ? fixed_at<4>(p) : fixed_at<8>(p);
+            if (cs + i * iw > 0) {
+                const unsigned long long y = iw == 4 ? fixed_at<4>(p - 4) : fixed_at<8>(p - 8);
+                if (x <= y && err == kOk) err = kNonIncreasing;
+            }
+            if (x >= R.numel && err == kOk) err = kRange;
+        }
+        if (err != kOk) set_status(st, err);
+        __syncthreads();
+    }
+}
+
+// Gated scatter: W[idx[e]] = val[e] (replace) or W[idx[e]] += val[e] (additive record).
+template <int W>
+__global__ void __launch_bounds__(256)
+k_fixed_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs,
+                const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
+                ApplyState *st) {
+    using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
+    const uint32_t gate = st->status;
+    if (gate != kOk) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&st->first_error, 0u, gate);
+        return;
+    }
+    const unsigned long long nch = st->n_chunks;
+    __shared__ __align__(16) uint8_t sb[kByteChunk + 48];
+    __shared__ __align__(16) uint8_t svb[kByteChunk / 4 * W + 32];
+    for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        const uint32_t k = __ldg(chunk_rec + c);
+        const ApplyRec R = recs[k];
+        const uint32_t iw = fixed_index_width(R.numel);
+        uint32_t len;
+        unsigned long long cs;
+        const uint8_t *b = stage_fixed_chunk(body, R, c - __ldg(rcb + k), iw, sb, len, cs);
+        const uint32_t ne = len / iw;
+        const uint8_t *vals = stage_bytes(svb, body + R.val_off + cs / iw * W, ne * W);
+        __syncthreads();
+        LT *w = reinterpret_cast<LT *>(R.w);
+        for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) {
+            const uint8_t *p = b + (size_t)i * iw;
+            const unsigned long long x = iw == 4 ? fixed_at<4>(p) : fixed_at<8>(p);
+            LT v;
+            if constexpr (W == 2) v = (LT)(vals[2 * i] | (vals[2 * i + 1] << 8));
+            else v = (LT)fixed_at<4>(vals + 4 * i);
+            w[x] = R.mode == 1 ? (LT)lane_combine<W>(w[x], v, false) : v;
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------------------ launchers
 cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], s);
     k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
-                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width);
+                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width, a.index_codec);
     if (ev) cudaEventRecord(ev[1], s);
+    if (a.index_codec) {  // fixed-width indices: validate, then the gated scatter (no scans)
+        k_fixed_validate<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.state);
+        if (ev) {
+            cudaEventRecord(ev[2], s);
+            cudaEventRecord(ev[3], s);
+        }
+        if (a.width == 2)
+            k_fixed_scatter<2><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.state);
+        else
+            k_fixed_scatter<4><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.state);
+        if (ev) cudaEventRecord(ev[4], s);
+        return cudaGetLastError();
+    }
     k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
                                                   a.chunk_count, a.chunk_sum, a.state);
     if (ev) cudaEventRecord(ev[2], s);

@@ -17,7 +17,7 @@
 //   K3  k_finalize      E6: record sizes and offsets (the offset table), body size.
 //   K4  k_emit_tiles    E5+E6: one warp per tile writes the LEB128 bytes of the first gap
 //                       and of the in-tile gaps (ballot-placed, 32 at a time) and copies the
-//                       raw values to their final offsets.
+//                       raw values to their final offsets (FIXED: absolute indices instead).
 //   K5  k_headers       E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
 //
 // Product code written for this library; none of it is shared with the test oracle.
@@ -150,12 +150,17 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 // ------------------------------------------------------------------------------ K1
 // THREADS x VECS = 2048 16-byte vectors per operand per tile (32 KiB); instantiated as
 // 256 x 8 (3 CTAs / SM) and 512 x 4 (2 CTAs / SM, more warps, fewer registers each).
-template <int W, int THREADS, int VECS, bool DENSE, bool ADDITIVE = false>
+// ADVANCE (extract-and-advance, NEXT f3): every changed lane of old is overwritten with the
+// new lane while the tile's sectors are still in L2, so old == new afterwards (the trainer's
+// shadow copy advances to the new version without a second pass).  Old is then read with
+// coherent loads, and on a retry after slot regrowth (redo_cap != 0) only the tiles that
+// overflowed a redo_cap-entry slot run again (the others were compacted AND advanced).
+template <int W, int THREADS, int VECS, bool DENSE, bool ADDITIVE = false, bool ADVANCE = false>
 __device__ __forceinline__ void
 scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
           uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
           typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
-          ExtractSummary *summary) {
+          ExtractSummary *summary, uint32_t redo_cap = 0) {
     using LT = typename LaneOf<W>::T;
     constexpr int LPV = 16 / W;                  // lanes per 16-byte vector
     constexpr int LANES = THREADS * VECS * LPV;  // lanes per tile
@@ -169,6 +174,9 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     __shared__ uint32_t s_tot[NQ];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if constexpr (ADVANCE) {
+        if (redo_cap && meta[t].count <= redo_cap) return;  // done (and advanced) by the first pass
+    }
     const TileDesc d = tiles[t];
     const uint32_t nl = d.nlanes;
 
@@ -178,7 +186,7 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         for (int r = 0; r < VECS; ++r) {
             const uint32_t v = r * THREADS + tid;
             if ((v + 1) * LPV <= nl) {
-                vo[r] = ld_stream_v4(d.old_p + (size_t)v * 16);
+                vo[r] = ADVANCE ? ld_noalloc_v4(d.old_p + (size_t)v * 16) : ld_stream_v4(d.old_p + (size_t)v * 16);
                 vn[r] = ld_stream_v4(d.new_p + (size_t)v * 16);
             } else {
                 vo[r] = make_uint4(0, 0, 0, 0);
@@ -198,7 +206,8 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
             vo[r] = make_uint4(0, 0, 0, 0);
             vn[r] = vo[r];
             for (int j = 0; j < LPV && v * LPV + j < nl; ++j) {
-                set_lane<W>(vo[r], j, __ldg(reinterpret_cast<const LT *>(d.old_p) + v * LPV + j));
+                set_lane<W>(vo[r], j, ADVANCE ? reinterpret_cast<const LT *>(d.old_p)[v * LPV + j]
+                                              : __ldg(reinterpret_cast<const LT *>(d.old_p) + v * LPV + j));
                 set_lane<W>(vn[r], j, __ldg(reinterpret_cast<const LT *>(d.new_p) + v * LPV + j));
             }
         }
@@ -297,6 +306,7 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
                 auto put = [&](uint32_t k, uint32_t sel) {
                     *so++ = (uint16_t)(obase + k);
                     const uint32_t nv = prmt(na, nb, sel);
+                    if constexpr (ADVANCE) const_cast<LT *>(reinterpret_cast<const LT *>(d.old_p))[obase + k] = (LT)nv;
                     if constexpr (ADDITIVE)  // the arithmetic difference new - old
                         *vp++ = (LT)lane_combine<W>(nv & 0xFFFFu, prmt(oa, ob, sel) & 0xFFFFu, true);
                     else
@@ -320,6 +330,9 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
                 const int j = __ffs(mm) - 1;
                 mm &= mm - 1;
                 *so++ = (uint16_t)((r * THREADS + tid) * LPV + j);
+                if constexpr (ADVANCE)
+                    const_cast<LT *>(reinterpret_cast<const LT *>(d.old_p))[(r * THREADS + tid) * LPV + j] =
+                        (LT)lane_of<W>(vn[r], j);
                 if constexpr (ADDITIVE)
                     *vp++ = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
                 else
@@ -329,14 +342,49 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     }
 }
 
-template <int W, int THREADS, int VECS, int MINB, bool DENSE, bool ADDITIVE = false>
+template <int W, int THREADS, int VECS, int MINB, bool DENSE, bool ADDITIVE = false, bool ADVANCE = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
              uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
              typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
-             ExtractSummary *summary) {
-    scan_tile<W, THREADS, VECS, DENSE, ADDITIVE>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val,
-                                meta, summary);
+             ExtractSummary *summary, uint32_t redo_cap) {
+    scan_tile<W, THREADS, VECS, DENSE, ADDITIVE, ADVANCE>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap,
+                                                          slot_bytes, slot_val, meta, summary, redo_cap);
+}
+
+// Slot regrowth that keeps the compaction of the tiles that fitted (extract-and-advance:
+// those tiles were advanced and cannot be compared again): entries of tile t move from the
+// old_cap-entry slot to the new_cap-entry slot.
+template <int W>
+__global__ void __launch_bounds__(256)
+k_slots_regrow(const TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t old_cap, const uint16_t *__restrict__ ob,
+               const typename LaneOf<W>::T *__restrict__ ov, uint32_t new_cap, uint16_t *__restrict__ nb,
+               typename LaneOf<W>::T *__restrict__ nv) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t t = wg; t < ntiles; t += nw) {
+        const uint32_t c = meta[t].count;
+        if (c > old_cap) continue;  // overflowed: recomputed by the retry
+        for (uint32_t i = lane; i < c; i += 32) {
+            nb[(size_t)t * new_cap + i] = ob[(size_t)t * old_cap + i];
+            nv[(size_t)t * new_cap + i] = ov[(size_t)t * old_cap + i];
+        }
+    }
+}
+
+cudaError_t launch_slots_regrow(const TileMeta *meta, uint32_t ntiles, int width, uint32_t old_cap,
+                                const void *ob, const void *ov, uint32_t new_cap, void *nb, void *nv, int ctas,
+                                cudaStream_t s) {
+    if (width == 2)
+        k_slots_regrow<2><<<ctas, 256, 0, s>>>(meta, ntiles, old_cap, static_cast<const uint16_t *>(ob),
+                                               static_cast<const uint16_t *>(ov), new_cap, static_cast<uint16_t *>(nb),
+                                               static_cast<uint16_t *>(nv));
+    else
+        k_slots_regrow<4><<<ctas, 256, 0, s>>>(meta, ntiles, old_cap, static_cast<const uint16_t *>(ob),
+                                               static_cast<const uint32_t *>(ov), new_cap, static_cast<uint16_t *>(nb),
+                                               static_cast<uint32_t *>(nv));
+    return cudaGetLastError();
 }
 
 // Persistent form: 3 CTAs per SM loop over the tiles (t = CTA, CTA + grid, ...), no
@@ -464,7 +512,8 @@ k_tiles_bytes(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ m
               const unsigned long long *__restrict__ blk_cnt, const long long *__restrict__ blk_key,
               const uint32_t *__restrict__ tensor_first_tile, unsigned long long *__restrict__ tile_entry,
               unsigned long long *__restrict__ tile_pred, unsigned int *__restrict__ tile_bytes,
-              unsigned long long *__restrict__ blk_bytes, const ExtractSummary *summary) {
+              unsigned long long *__restrict__ blk_bytes, const unsigned long long *__restrict__ numel,
+              int fixed, const ExtractSummary *summary) {
     if (summary->overflow) return;
     __shared__ unsigned long long s_w[32];
     __shared__ long long s_m[32];
@@ -503,7 +552,8 @@ k_tiles_bytes(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ m
                 pred = tiles[kex].lane_base + meta[kex].last_off;  // last change before this tile
             }
             const unsigned long long first = d.lane_base + mt[e].first_off;
-            b = mt[e].internal_bytes + leb_len(first - pred);
+            b = fixed ? mt[e].count * fixed_index_width(numel[k])  // reading R18: absolute indices
+                      : mt[e].internal_bytes + leb_len(first - pred);
             kex = t;
         }
         tile_entry[t] = cex;
@@ -601,6 +651,7 @@ k_finalize(const unsigned long long *__restrict__ E, const unsigned long long *_
 // Warp-wide copy of n bytes from a 16-byte aligned source to any destination: byte head
 // up to the destination's 16-byte boundary, 16-byte stores assembled from funnel-shifted
 // source words, byte tail.  Reads at most 4 bytes past the source range (slots are padded).
+template <bool GLOBAL_SRC = true>
 __device__ __forceinline__ void warp_copy4(uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
     const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
     if ((uint32_t)lane < head) dst[lane] = src[lane];
@@ -609,7 +660,7 @@ __device__ __forceinline__ void warp_copy4(uint8_t *dst, const uint8_t *src, uin
     const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
     const uint32_t sh = 8u * head;  // source byte offset of word j is head + 4j
     for (uint32_t j = lane; j < nw; j += 32) {
-        const uint32_t w0 = __ldg(s32 + j), w1 = __ldg(s32 + j + 1);
+        const uint32_t w0 = GLOBAL_SRC ? __ldg(s32 + j) : s32[j], w1 = GLOBAL_SRC ? __ldg(s32 + j + 1) : s32[j + 1];
         d32[j] = sh ? __funnelshift_r(w0, w1, sh) : w0;
     }
     for (uint32_t b = (nw << 2) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
@@ -652,7 +703,8 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
                  const unsigned long long *__restrict__ tile_entry, const unsigned long long *__restrict__ tile_byte,
                  const unsigned long long *__restrict__ tile_pred, const unsigned long long *__restrict__ E,
                  const unsigned long long *__restrict__ Bk, const RecordRow *__restrict__ table,
-                 TileEmit *__restrict__ plan, const ExtractSummary *summary) {
+                 TileEmit *__restrict__ plan, const unsigned long long *__restrict__ numel, int fixed,
+                 const ExtractSummary *summary) {
     if (summary->overflow) return;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
         const TileMeta m = meta[t];
@@ -662,7 +714,8 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
             const uint32_t k = d.flags_tensor & kTileTensorMask;
             e.ib = table[k].index_offset + (tile_byte[t] - Bk[k]);
             e.vb = table[k].values_offset + (tile_entry[t] - E[k]) * W;
-            e.g0 = d.lane_base + m.first_off - tile_pred[t];
+            e.g0 = fixed ? d.lane_base : d.lane_base + m.first_off - tile_pred[t];
+            if (fixed) e.internal_bytes = fixed_index_width(numel[k]);
         }
         plan[t] = e;
     }
@@ -672,7 +725,7 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
 // (differences of the slot's u16 lane offsets, < 2^14: one or two bytes each) encoded 32 at
 // a time — byte positions from a ballot of the two-byte ones — and the raw values copied
 // to their final offsets in the body.
-template <int W>
+template <int W, bool FIXED>
 __global__ void __launch_bounds__(256, 8)
 k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
@@ -682,9 +735,32 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
     const uint32_t lt_mask = (1u << lane) - 1u;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    // FIXED: absolute indices staged per warp in shared memory, then copied to the body
+    __shared__ __align__(16) unsigned long long s_fix[FIXED ? 8 * 256 + 2 : 1];
     for (uint32_t t = wg; t < ntiles; t += nw) {
         const TileEmit e = plan[t];
         if (e.count == 0) continue;
+        if constexpr (FIXED) {  // reading R18: lane_base + offset as u32 / u64, little-endian
+            const uint32_t iw = e.internal_bytes;  // the index width (set by K3b for FIXED)
+            const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
+            unsigned long long *buf = s_fix + 256 * (threadIdx.x >> 5);
+            uint8_t *dst = out + e.ib;
+            for (uint32_t b = 0; b < e.count; b += 256) {
+                const uint32_t n = min(256u, e.count - b);
+                for (uint32_t i = lane; i < n; i += 32) {
+                    const unsigned long long x = e.g0 + so[b + i];
+                    if (iw == 4) reinterpret_cast<uint32_t *>(buf)[i] = (uint32_t)x;
+                    else buf[i] = x;
+                }
+                __syncwarp();
+                warp_copy4<false>(dst, reinterpret_cast<const uint8_t *>(buf), n * iw, lane);
+                __syncwarp();
+                dst += (size_t)n * iw;
+            }
+            warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), e.count * W,
+                      lane);
+            continue;
+        }
         uint8_t *ib = out + e.ib;
         unsigned long long g = e.g0;
         const uint32_t L0 = leb_len(g);
@@ -754,28 +830,31 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     // dense slots (> kStageGapBytes entries per tile seen): predicated compaction steps
     const bool dense = a.slot_cap > kStageGapBytes;
     if (ev) cudaEventRecord(ev[0], s);
-    if (a.scan_kernel == 4) {
+    const bool variant_ok = !a.advance && a.mode == 0;  // the variants implement plain replace extraction
+    if (a.scan_kernel == 4 && variant_ok) {
         const uint32_t grid = a.ntiles < 3u * a.sm_count ? a.ntiles : 3u * a.sm_count;
         k_scan_tiles_persist<W><<<grid, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
                                                     static_cast<LT *>(a.slot_val), a.meta, a.summary);
-    } else if (a.scan_kernel == 3) {
+    } else if (a.scan_kernel == 3 && variant_ok) {
         k_scan_tiles<W, 512, 4, 2, false><<<a.ntiles, 512, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
                                                                   a.slot_bytes, static_cast<LT *>(a.slot_val),
-                                                                  a.meta, a.summary);
+                                                                  a.meta, a.summary, 0u);
     } else {
-        (a.mode == 1 ? (dense ? k_scan_tiles<W, 256, 8, 2, true, true> : k_scan_tiles<W, 256, 8, 2, false, true>)
-                     : (dense ? k_scan_tiles<W, 256, 8, 3, true> : k_scan_tiles<W, 256, 8, 3, false>))
+        (a.advance ? (dense ? k_scan_tiles<W, 256, 8, 3, true, false, true> : k_scan_tiles<W, 256, 8, 3, false, false, true>)
+         : a.mode == 1 ? (dense ? k_scan_tiles<W, 256, 8, 2, true, true> : k_scan_tiles<W, 256, 8, 2, false, true>)
+                       : (dense ? k_scan_tiles<W, 256, 8, 3, true> : k_scan_tiles<W, 256, 8, 3, false>))
             <<<a.ntiles, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
-                                      static_cast<LT *>(a.slot_val), a.meta, a.summary);
+                                      static_cast<LT *>(a.slot_val), a.meta, a.summary, a.redo_cap);
     }
     if (ev) cudaEventRecord(ev[1], s);
-    k_tiles_gaps<<<a.persist_ctas, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
+    if (!a.index_codec)  // the fixed-width codec needs no gap statistics
+        k_tiles_gaps<<<a.persist_ctas, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
     k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);
     k_tiles_bytes<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.blk_a, a.blk_key, a.tensor_first_tile,
                                         a.tile_entry, a.tile_pred, a.tile_bytes_tmp, a.blk_a + nblk,
-                                        a.summary);
+                                        a.numel, a.index_codec, a.summary);
     k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a + nblk, nullptr, nblk, a.summary);
     k_tiles_place<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.ntensors, a.tile_entry,
                                         a.tile_bytes_tmp, a.blk_a + nblk, a.tile_byte, a.entry_begin,
@@ -788,7 +867,7 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
         k_tiles_emitplan<W><<<g < 65535u ? g : 65535u, 256, 0, s>>>(a.tiles, a.meta, a.ntiles, a.tile_entry,
                                                                    a.tile_byte, a.tile_pred, a.entry_begin,
                                                                    a.tensor_byte_begin, a.table, a.plan,
-                                                                   a.summary);
+                                                                   a.numel, a.index_codec, a.summary);
     }
     if (ev) cudaEventRecord(ev[3], s);
     return cudaGetLastError();
@@ -798,9 +877,8 @@ template <int W>
 static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
-    k_emit_tiles<W><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
-                                                   static_cast<const LT *>(a.slot_val), out, a.summary,
-                                                   a.out_cap);
+    (a.index_codec ? k_emit_tiles<W, true> : k_emit_tiles<W, false>)<<<a.persist_ctas, 256, 0, s>>>(
+        a.plan, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<const LT *>(a.slot_val), out, a.summary, a.out_cap);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
     k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode, a.summary,

@@ -14,6 +14,16 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void *p) {
     return v;
 }
 
+// Coherent 128-bit load without L1 allocation, for data the same kernel later writes
+// (the extract-and-advance compare kernel stores new lanes into the old buffer).
+__device__ __forceinline__ uint4 ld_noalloc_v4(const void *p) {
+    uint4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 // Streaming 256-bit load (sm_100): 32 contiguous bytes per thread, no L1 allocation,
 // L2 evict-first (the old/new stream is read exactly once).
 __device__ __forceinline__ void ld_stream_v8(const void *p, uint32_t *r) {

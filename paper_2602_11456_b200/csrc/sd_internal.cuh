@@ -75,6 +75,11 @@ struct TargetDesc {
     uint32_t name_len;
 };
 
+// Fixed-width index codec (reading R18): 4-byte indices iff N - 1 fits int32.
+__host__ __device__ __forceinline__ uint32_t fixed_index_width(unsigned long long n) {
+    return n <= 0x80000000ull ? 4u : 8u;
+}
+
 struct ApplyRec {  // located + verified record
     unsigned long long idx_off, idx_len, val_off, nnz, numel;
     uint8_t *w;
@@ -124,6 +129,9 @@ struct ExtractArgs {
     int scan_kernel;                  // 0: one CTA per tile; 1: persistent TMA pipeline; 2: runs
     uint32_t prefetch_dist;           // K1 (0): L2 bulk prefetch distance in tiles (0 = off)
     int mode;                         // record mode: 0 replace, 1 additive
+    int index_codec;                  // 0 LEB128 gaps, 1 fixed-width absolute (R18)
+    bool advance = false;             // K1 also stores every changed new lane into old (extract-and-advance)
+    uint32_t redo_cap = 0;            // advance retry: only tiles with count > redo_cap run K1 again
     // emit gate (K4/K5 write nothing unless the scan fitted its slots and body <= out_cap);
     // size_out (device, may be NULL) receives the body size, or ~0 when the gate is closed
     unsigned long long out_cap = ~0ull;
@@ -134,6 +142,9 @@ struct ExtractArgs {
 // after the tile scans K2, after K3; emit: 3 = before K4, after K4, after K5).
 cudaError_t launch_extract_scan(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev);    // K1-K3
 cudaError_t launch_extract_emit(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev);  // K4-K5
+cudaError_t launch_slots_regrow(const TileMeta *meta, uint32_t ntiles, int width, uint32_t old_cap,
+                                const void *ob, const void *ov, uint32_t new_cap, void *nb, void *nv, int ctas,
+                                cudaStream_t s);
 
 struct ApplyArgs {
     const uint8_t *body;
@@ -156,6 +167,7 @@ struct ApplyArgs {
     int persist_ctas;
     int scatter_ctas;
     bool entry_major;                 // scatter store order (see k_scatter)
+    int index_codec;                  // 0 LEB128 gaps, 1 fixed-width absolute indices (R18)
 };
 
 cudaError_t launch_blake3(const uint8_t *in, unsigned long long n, uint32_t *ws, uint32_t *out32, cudaStream_t s);

@@ -589,3 +589,154 @@ def test_chained_round_trip_overflow_and_capacity(sd):
     assert_lanes_equal(tgt3[0][1], w)
     ctx.close()
     ctx2.close()
+
+
+# ------------------------------------------------------------------ fixed-width index codec (NEXT f4)
+def _fixed_ctx(sd):
+    from paper_2602_11456_b200 import _abi
+    ctx = sd.DeltaContext(DEV)
+    ctx.set_option(_abi.DELTA_OPT_INDEX_CODEC, 2)
+    return ctx
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_fixed_codec_parity(sd, dtype):
+    """DELTA_OPT_INDEX_CODEC = 2, the naive int32/64 encoding (R18):
+    body bytes and table rows equal the oracle's fixed-width codec; apply (host, device and
+    no table hint) reconstructs new bit for bit.  Multi-chunk, dense, ragged, fused and
+    empty tensors, full-range bit patterns."""
+    ctx = _fixed_ctx(sd)
+    tensors = []
+    for k, (n, rho, vals) in enumerate([(16_777_216, 0.01, "weights"), (300_001, 0.6, "weights"),
+                                        (100_003, 0.3, "bits"), (9, 1.0, "bits"), (0, 0.0, "weights"),
+                                        (16385, 0.001, "weights")]):
+        spec = TensorSpec(f"f{k}.w", (n,), "matrix")
+        o, w = generate_pair(spec, k, 21, rho=rho, dtype=dtype, device=DEV, values=vals)
+        tensors.append((spec.name, o, w))
+    o, w = tensors[1][1], tensors[1][2]  # a fused, unaligned 3-span tensor
+    tensors.append(("f.qkv", [o[:1001], o[1001:50001], o[50001:]], [w[:1001], w[1001:50001], w[50001:]]))
+    body, table = ctx.delta_extract(tensors)
+    ref_body, ref_table = oracle.codec.extract(
+        [(n, [to_np(s) for s in as_list(a)], [to_np(s) for s in as_list(b)]) for n, a, b in tensors],
+        index_codec="fixed")
+    assert_body_equal(body, ref_body)
+    assert [tuple(r) for r in table] == [tuple(r) for r in ref_table]
+    for hint in ("host", "none", "device"):
+        targets = [(n, fused(a).clone()) for n, a, _ in tensors]
+        if hint == "device":
+            dbody, dtab = ctx.delta_extract(tensors, table="device")
+            ctx.delta_apply(targets, dbody, table=dtab)
+        else:
+            ctx.delta_apply(targets, body, table=table if hint == "host" else None)
+        torch.cuda.synchronize()
+        for (_, t), (_, _, b) in zip(targets, tensors):
+            assert_lanes_equal(t, fused(b))
+    ctx.close()
+
+
+def test_fixed_codec_u64_indices(sd):
+    """N = 2^31 + 1000 lanes: N - 1 > INT32_MAX -> 8-byte indices (R18)."""
+    n = 2**31 + 1000
+    pos = [0, 5, 2**31 - 1, 2**31, 2**31 + 999]
+    old, new = _with_changes(n, pos)
+    ctx = _fixed_ctx(sd)
+    body, table = ctx.delta_extract([("big", old, new)])
+    import struct
+    vals = b"".join(struct.pack("<H", int(x)) for x in to_np(new[torch.tensor(pos, device=DEV)]))
+    stream = oracle.brute.encode_indices_fixed(pos, n)
+    assert len(stream) == 8 * len(pos)
+    want = _hand_record("big", n, len(pos), stream, vals)
+    assert body.cpu().numpy().tobytes() == want
+    w = old
+    del old
+    ctx.delta_apply([("big", w)], body, table=table)
+    assert_lanes_equal(w, new)
+    ctx.close()
+
+
+_HAND_FIXED = [
+    ("truncated", _hand_record("a", 10, 1, b"\x01\x00\x00", b"\x01\x00")),
+    ("count", _hand_record("a", 10, 1, b"\x01\x00\x00\x00\x02\x00\x00\x00", b"\x01\x00")),
+    ("nonincreasing", _hand_record("a", 10, 2, b"\x03\x00\x00\x00\x03\x00\x00\x00", b"\x01\x00\x02\x00")),
+    ("nonincreasing", _hand_record("a", 10, 2, b"\x04\x00\x00\x00\x03\x00\x00\x00", b"\x01\x00\x02\x00")),
+    ("range", _hand_record("a", 10, 2, b"\x03\x00\x00\x00\x0a\x00\x00\x00", b"\x01\x00\x02\x00")),
+]
+
+
+@pytest.mark.parametrize("kind,body", _HAND_FIXED)
+def test_fixed_codec_rejects(sd, kind, body):
+    """Single-fault fixed-width bodies: the GPU's error kind equals the oracle's and the
+    targets stay bitwise untouched (all-or-nothing)."""
+    a = np.arange(10, dtype=np.uint16)
+    with pytest.raises(oracle.DeltaError) as eo:
+        oracle.codec.apply([("a", a.copy())], body, 2, index_codec="fixed")
+    assert eo.value.kind == kind
+    ctx = _fixed_ctx(sd)
+    t = torch.from_numpy(a.view(np.int16).copy()).to(DEV).view(torch.bfloat16)
+    before = t.clone()
+    with pytest.raises(sd.DeltaError) as eg:
+        ctx.delta_apply([("a", t)], torch.tensor(list(body), dtype=torch.uint8, device=DEV))
+    assert eg.value.kind == kind
+    assert_lanes_equal(t, before)
+    ctx.close()
+
+
+def test_fixed_codec_fault_in_a_later_chunk(sd):
+    """A non-increasing index deep in a multi-chunk fixed-width stream (chunk boundary
+    carries the previous entry)."""
+    spec = m1_specs()[0]
+    o, w = generate_pair(spec, 0, 0, rho=0.01, pattern="exact")
+    body, table = oracle.codec.extract([(spec.name, [to_np(o)], [to_np(w)])], index_codec="fixed")
+    r = table[0]
+    m = bytearray(body)
+    e = 3 * 1024  # the first entry of the fourth 4 KiB chunk repeats the previous index
+    m[r[3] + 4 * e:r[3] + 4 * e + 4] = m[r[3] + 4 * (e - 1):r[3] + 4 * e]
+    ctx = _fixed_ctx(sd)
+    t = o.to(DEV)
+    before = t.clone()
+    with pytest.raises(sd.DeltaError) as eg:
+        ctx.delta_apply([(spec.name, t)], torch.tensor(list(m), dtype=torch.uint8, device=DEV))
+    assert eg.value.kind == "nonincreasing"
+    assert_lanes_equal(t, before)
+    ctx.close()
+
+
+# ------------------------------------------------------------------ extract-and-advance (NEXT f3)
+def test_extract_and_advance(sd):
+    """DELTA_OPT_ADVANCE = 2: the body equals the oracle's, and afterwards every old span
+    equals its new span bitwise (fused, unaligned and ragged spans included).  The first
+    call runs at a density that overflows the default slots, so the retry path (slots
+    regrown with the fitted tiles' compaction kept, only overflowed tiles redone) is
+    exercised; a second extract of the same pair sees no change."""
+    from paper_2602_11456_b200 import _abi
+    ctx = sd.DeltaContext(DEV)
+    ctx.set_option(_abi.DELTA_OPT_ADVANCE, 2)
+    tensors, keep_old = [], []
+    for k, (n, rho) in enumerate([(16_777_216, 0.01), (2_000_003, 0.3), (100_003, 0.001), (7, 1.0), (0, 0.0)]):
+        spec = TensorSpec(f"adv{k}", (n,), "matrix")
+        o, w = generate_pair(spec, k, 31, rho=rho, device=DEV)
+        tensors.append((spec.name, o, w))
+    o, w = generate_pair(TensorSpec("adv.qkv", (60_001,), "matrix"), 9, 31, rho=0.05, device=DEV)
+    tensors.append(("adv.qkv", [o[:1001].clone(), o[1001:50001].clone(), o[50001:].clone()],
+                    [w[:1001], w[1001:50001], w[50001:]]))
+    ref_body, ref_table = oracle_extract(tensors)
+    keep_old = [[s.clone() for s in as_list(a)] for _, a, _ in tensors]
+    body, table = ctx.delta_extract(tensors)
+    torch.cuda.synchronize()
+    assert_body_equal(body, ref_body)
+    assert [tuple(r) for r in table] == [tuple(r) for r in ref_table]
+    for (_, a, b) in tensors:
+        for sa, sb in zip(as_list(a), as_list(b)):
+            assert_lanes_equal(sa, sb)
+    # the body still applies onto the pre-advance copy
+    targets = [(n, fused(ko).clone()) for (n, _, _), ko in zip(tensors, keep_old)]
+    ctx.delta_apply(targets, body, table=table)
+    torch.cuda.synchronize()
+    for (_, t), (_, _, b) in zip(targets, tensors):
+        assert_lanes_equal(t, fused(b))
+    body2, table2 = ctx.delta_extract(tensors)
+    assert all(r[2] == 0 for r in table2)
+    with pytest.raises(sd.DeltaError):  # asynchronous extract refuses advance
+        ctx.delta_extract_async(tensors, torch.empty(1 << 20, dtype=torch.uint8, device=DEV),
+                                torch.zeros(1, dtype=torch.int64, device=DEV))
+    ctx.close()

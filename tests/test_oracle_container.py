@@ -42,3 +42,13 @@ def test_reject():
         container.unpack(bytes(bad))
     with pytest.raises(DeltaError):
         container.pack(body, 3, 1, 2, 1)                   # version != base + 1
+
+
+def test_fixed_codec_container_version():
+    # reading R18: format_version 2 marks fixed-width index streams; a LEB128 reader rejects it
+    body = b"\x01\x00w" + bytes(24) + b"\x00"
+    blob = container.pack(body, 2, 1, 2, 1, index_codec="fixed")
+    assert blob[4:6] == b"\x02\x00"
+    assert container.unpack(blob, index_codec="fixed") == (2, 1, 2, 1, body)
+    with pytest.raises(DeltaError):
+        container.unpack(blob)
