@@ -316,7 +316,9 @@ enum {
                                          compare kernel also stores every changed lane of new into
                                          old, so after delta_size / delta_extract every old_dev span
                                          equals its new_dev span bitwise (old_dev must then be
-                                         writable; unchanged lanes are not written).  The body is
+                                         writable; a lane is only ever overwritten with its own new
+                                         value: 32-byte sectors holding a change are rewritten
+                                         whole).  The body is
                                          unchanged.  1 = off (default).  Replace mode only
                                          (DELTA_EINVAL with DELTA_OPT_MODE = 2); delta_extract_async
                                          returns DELTA_EINVAL while it is on (a slot-overflow retry

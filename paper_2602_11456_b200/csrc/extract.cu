@@ -286,6 +286,27 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         }
     }
     if (!fits) return;
+    if constexpr (ADVANCE) {
+        // old <- new where anything changed: a thread pair (tid, tid ^ 1) holds one 32-byte
+        // sector; if either half changed both store their whole 16-byte vector (a full-sector
+        // write needs no DRAM fill; unchanged lanes are rewritten with their own value).
+        // Partial vectors at the end of a tile and unaligned tiles: changed lanes only.
+        LT *op = const_cast<LT *>(reinterpret_cast<const LT *>(d.old_p));
+        const bool aligned = d.flags_tensor & kTileAligned;
+#pragma unroll
+        for (int r = 0; r < VECS; ++r) {
+            const uint32_t v = r * THREADS + tid;
+            const bool any = (m[r] | __shfl_xor_sync(0xffffffffu, m[r], 1)) != 0;
+            if (aligned && any && (v + 1) * LPV <= nl) {
+                reinterpret_cast<uint4 *>(op)[v] = vn[r];
+            } else if (m[r]) {
+                for (int j = 0; j < LPV && v * LPV + j < nl; ++j) {
+                    const uint32_t bit = (W == 2) ? (j < 4 ? 8 * j + 7 : 8 * (j - 4) + 3) : j;
+                    if ((m[r] >> bit) & 1u) op[v * LPV + j] = (LT)lane_of<W>(vn[r], j);
+                }
+            }
+        }
+    }
     LT *sv = slot_val + (size_t)t * slot_cap;
     uint16_t *sg = reinterpret_cast<uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
     uint32_t rbase = 0;
@@ -306,7 +327,6 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
                 auto put = [&](uint32_t k, uint32_t sel) {
                     *so++ = (uint16_t)(obase + k);
                     const uint32_t nv = prmt(na, nb, sel);
-                    if constexpr (ADVANCE) const_cast<LT *>(reinterpret_cast<const LT *>(d.old_p))[obase + k] = (LT)nv;
                     if constexpr (ADDITIVE)  // the arithmetic difference new - old
                         *vp++ = (LT)lane_combine<W>(nv & 0xFFFFu, prmt(oa, ob, sel) & 0xFFFFu, true);
                     else
@@ -330,9 +350,6 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
                 const int j = __ffs(mm) - 1;
                 mm &= mm - 1;
                 *so++ = (uint16_t)((r * THREADS + tid) * LPV + j);
-                if constexpr (ADVANCE)
-                    const_cast<LT *>(reinterpret_cast<const LT *>(d.old_p))[(r * THREADS + tid) * LPV + j] =
-                        (LT)lane_of<W>(vn[r], j);
                 if constexpr (ADDITIVE)
                     *vp++ = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
                 else
