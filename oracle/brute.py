@@ -28,6 +28,12 @@ Definitions followed, in order (SURVEY.md §8(c) O1-O10 restates them):
       index stream is the nnz absolute indices, each as a little-endian
       unsigned integer of 4 bytes if N - 1 <= 2^31 - 1, else 8 (DESIGN.md
       reading R18); every other byte of the record is as in O6.
+  M   merge of two consecutive deltas D_a (v-1 -> v) and D_b (v -> v+1) into one
+      (v-1 -> v+1) for a laggard's catch-up ("laggards catch up
+      asynchronously"; SPEC.md:476 leaves merging open; reading R19):
+      per tensor the union of the two index sets, each value taken from D_b
+      where D_b has the index, else from D_a — so applying the merge equals
+      applying D_a then D_b.  Replace mode only.
 """
 
 import math
@@ -256,6 +262,35 @@ def apply(targets: list[tuple[str, list[int]]], body: bytes, width: int,
         for j, v in zip(idx, vals):
             w[j] = v if mode == MODE_REPLACE else lane_op(w[j], v, width, +1)
         out.append(w)
+    return out
+
+
+def merge(body_a: bytes, body_b: bytes, width: int, index_codec: str = "leb128") -> bytes:
+    """M: the delta equivalent to applying body_a then body_b (replace mode)."""
+    ra, rb = parse(body_a, width, index_codec), parse(body_b, width, index_codec)
+    if len(ra) != len(rb):
+        raise DeltaError("layout", f"{len(ra)} records vs {len(rb)}")
+    out = b""
+    for (na, n_a, ia, va, ma), (nb, n_b, ib, vb, mb) in zip(ra, rb):
+        if na != nb:
+            raise DeltaError("name", f"record {na!r} vs {nb!r}")
+        if n_a != n_b:
+            raise DeltaError("numel", f"{na!r}: N={n_a} vs {n_b}")
+        if ma != MODE_REPLACE or mb != MODE_REPLACE:
+            raise DeltaError("mode", f"{na!r}: merge needs replace-mode records")
+        d = {}
+        for j, v in zip(ia, va):
+            d[j] = v
+        for j, v in zip(ib, vb):  # the later delta wins
+            d[j] = v
+        idx = sorted(d)
+        if index_codec == "leb128":
+            out += record_from_sparse(na, n_a, idx, [d[j] for j in idx], width)
+        else:
+            nbytes = na.encode("utf-8")
+            stream = encode_indices_fixed(idx, n_a)
+            out += (_u(len(nbytes), 2) + nbytes + _u(n_a, 8) + _u(len(idx), 8) + _u(len(stream), 8) + stream
+                    + b"".join(_u(d[j], width) for j in idx) + _u(0, 1))
     return out
 
 

@@ -265,6 +265,33 @@ def apply(targets, body, width: int, inplace: bool = False, index_codec: str = "
     return out
 
 
+def merge(body_a, body_b, width: int, index_codec: str = "leb128") -> bytes:
+    """Merge of two consecutive replace-mode deltas (reading R19; brute.merge):
+    per tensor idx = union (numpy union1d), values of body_b where it has the index, else
+    body_a's.  apply(merge(a, b)) == apply(b) after apply(a)."""
+    ra, rb = parse(body_a, width, index_codec), parse(body_b, width, index_codec)
+    if len(ra) != len(rb):
+        raise DeltaError("layout", f"{len(ra)} records vs {len(rb)}")
+    parts = []
+    for (na, n_a, ia, va, ma), (nb, n_b, ib, vb, mb) in zip(ra, rb):
+        if na != nb:
+            raise DeltaError("name", f"record {na!r} vs {nb!r}")
+        if n_a != n_b:
+            raise DeltaError("numel", f"{na!r}: N={n_a} vs {n_b}")
+        if ma != MODE_REPLACE or mb != MODE_REPLACE:
+            raise DeltaError("mode", f"{na!r}: merge needs replace-mode records")
+        idx = np.union1d(ia, ib).astype(np.uint64)
+        vals = np.empty(idx.size, dtype=_LANE[width])
+        vals[np.searchsorted(idx, ia)] = va
+        vals[np.searchsorted(idx, ib)] = vb  # the later delta wins
+        stream = encode_gaps(gaps(idx)) if index_codec == "leb128" else encode_fixed(idx, n_a)
+        nbytes = na.encode("utf-8")
+        parts.append(b"".join((struct.pack("<H", len(nbytes)), nbytes,
+                               struct.pack("<QQQ", n_a, idx.size, stream.size),
+                               stream.tobytes(), vals.astype(_LANE[width], copy=False).tobytes(), b"\x00")))
+    return b"".join(parts)
+
+
 def rho(pairs) -> float:
     """O10, Eq. 1 (PAPER.md:297): sum_k ||dW_k||_0 / sum_k |W_k|, with
     bitwise inequality as nonzero (reading R2)."""
