@@ -259,6 +259,30 @@ int delta_assemble_wait(delta_ctx *ctx, void *stream);
  * `stream` once. */
 int delta_digest(delta_ctx *ctx, const void *body_dev, uint64_t bytes, uint8_t *out32, void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * delta_merge — NEXT f4 (reading R19): two consecutive bodies D_a (version v-1 ->
+ * v) and D_b (v -> v+1) over the same n tensors become ONE body (v-1 -> v+1) that a laggard
+ * applies instead of replaying both ("laggards catch up asynchronously";
+ * SPEC.md:476 leaves merging open).  Per record: the index set is the union of the two, the
+ * value is D_b's where D_b has the index and D_a's otherwise, so
+ * delta_apply(merge) == delta_apply(D_a) then delta_apply(D_b) for any base weights.  The
+ * merged body is canonical (sorted unique indices, minimal LEB128), in D_b's record order
+ * and names.
+ *   body_a_dev / body_b_dev  device, a_bytes / b_bytes long, read only; LEB128 index streams
+ *                            (DELTA_OPT_INDEX_CODEC = 1 on ctx, else DELTA_EINVAL);
+ *   n                        records expected in each body;
+ *   out_dev                  device, out_capacity bytes, receives the merged body;
+ *   *out_bytes (host)        the merged size (also on DELTA_ECAPACITY, nothing written).
+ * Both bodies are validated fully before anything is written: layout / record count, mode
+ * byte != 0 (replace only) -> DELTA_ECORRUPT (detail LAYOUT / MODE); names or element counts
+ * that differ between the bodies -> DELTA_ENAME (detail NAME / NUMEL); every decode check of
+ * delta_apply (TRUNCATED, OVERLONG, OVERFLOW, NONINCREASING, RANGE, COUNT) -> DELTA_ECORRUPT.
+ * Stream-ordered on `stream`; synchronises with the host four times (intermediate sizes);
+ * the emit is asynchronous (synchronise the stream before reading out_dev). */
+int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *body_a_dev, uint64_t a_bytes,
+                const void *body_b_dev, uint64_t b_bytes, void *out_dev, uint64_t out_capacity, void *stream,
+                uint64_t *out_bytes);
+
 /* Per-kernel device times of the last delta_size/delta_extract/delta_apply on this ctx,
  * in milliseconds, measured with CUDA events recorded on the call's stream around each
  * kernel (only while profiling is enabled; zero otherwise).  A field is the time of the

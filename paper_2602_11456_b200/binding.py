@@ -338,6 +338,24 @@ class DeltaContext:
                                            body.numel(), out, _stream_handle(stream)))
         return out.raw
 
+    def delta_merge(self, body_a, body_b, n: int, width: int = 2, out=None, stream=None):
+        """The body equivalent to applying ``body_a`` then ``body_b`` (both uint8 CUDA
+        tensors holding n records each; reading R19).  Returns a uint8 CUDA tensor view of
+        exactly the merged bytes (``out``'s prefix if given)."""
+        st = _stream_handle(stream)
+        nbytes = c_uint64()
+        elem = _ELEM[width]
+
+        def call(o, cap):
+            return self._lib.delta_merge(self._h, n, elem, c_void_p(body_a.data_ptr() if body_a.numel() else 0),
+                                         body_a.numel(), c_void_p(body_b.data_ptr() if body_b.numel() else 0),
+                                         body_b.numel(), c_void_p(o.data_ptr() if o is not None else 0), cap, st,
+                                         byref(nbytes))
+        if out is None:  # the merge is never longer than the two bodies together
+            out = torch.empty(max(body_a.numel() + body_b.numel(), 1), dtype=torch.uint8, device=body_b.device)
+        self._check(call(out, out.numel()))
+        return out[:nbytes.value]
+
     def assemble_wait(self, stream=None):
         self._check(self._lib.delta_assemble_wait(self._h, _stream_handle(stream)))
 

@@ -84,6 +84,9 @@ struct delta_ctx {
     DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status, dg_ws;
     uint32_t *h_asm = nullptr;  // pinned
     ApplyState *h_state = nullptr;  // pinned
+    // ---- delta_merge workspace
+    DevBuf m_targets, m_name_len, m_name_off, m_numel, m_ea, m_eb, m_eu, m_status, m_ia, m_ib, m_va, m_vb, m_lb,
+        m_dup, m_ds, m_u, m_uv, m_len, m_lo, m_blk, m_table, m_size;
     // pinned staging ring for the per-call apply uploads (targets, hint, names): with a
     // pinned source cudaMemcpyAsync does not wait for earlier work on the stream, so
     // delta_apply_async never blocks the host on a previous scatter.
@@ -178,6 +181,10 @@ void delta_ctx_destroy(delta_ctx *c) {
     if (c && c->ev_extract) cudaEventDestroy(c->ev_extract);
     if (!c) return;
     cudaSetDevice(c->device);
+    DevBuf *mbufs[] = {&c->m_targets, &c->m_name_len, &c->m_name_off, &c->m_numel, &c->m_ea, &c->m_eb, &c->m_eu,
+                       &c->m_status, &c->m_ia, &c->m_ib, &c->m_va, &c->m_vb, &c->m_lb, &c->m_dup, &c->m_ds,
+                       &c->m_u, &c->m_uv, &c->m_len, &c->m_lo, &c->m_blk, &c->m_table, &c->m_size};
+    for (DevBuf *b : mbufs) b->release();
     DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->tile_plan, &c->blk_a,
@@ -664,7 +671,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
             return fail(ctx, DELTA_EINVAL, 0, "target %u: w_dev not %d-byte aligned", k, w);
         td[k].w = static_cast<uint8_t *>(tg[k].w_dev);
         td[k].numel = tg[k].numel;
-        td[k].name_off = (uint32_t)blob.size();
+        td[k].name_off = blob.size();
         td[k].name_len = tg[k].name_len;
         blob.append(tg[k].name ? tg[k].name : "", tg[k].name_len);
     }
@@ -846,3 +853,151 @@ extern "C" int delta_digest(delta_ctx *ctx, const void *body, uint64_t bytes, ui
     memcpy(out32, ctx->h_asm, 32);
     return DELTA_OK;
 }
+
+// --------------------------------------------------------------------------- merge
+// delta_merge (NEXT f4, reading R19): validate both bodies (layout, pairwise names and
+// element counts, replace mode, full LEB128 decode with the apply's checks), decode them to
+// absolute (index, value) arrays, merge per record by rank, re-encode.  Four host syncs
+// (sizes of the intermediate arrays and of the result).
+extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *body_a, uint64_t a_bytes,
+                           const void *body_b, uint64_t b_bytes, void *out, uint64_t out_capacity, void *stream,
+                           uint64_t *out_bytes) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    const int w = elem_width(elem);
+    if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
+    if (!out_bytes) return fail(ctx, DELTA_EINVAL, 0, "out_bytes is NULL");
+    if ((a_bytes && !body_a) || (b_bytes && !body_b)) return fail(ctx, DELTA_EINVAL, 0, "body is NULL");
+    if (out_capacity && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
+    if (ctx->index_codec != 0) return fail(ctx, DELTA_EINVAL, 0, "delta_merge reads LEB128 bodies only");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t nn = std::max<uint32_t>(n, 1);
+    GROW(ctx->m_targets, nn * sizeof(TargetDesc));
+    GROW(ctx->m_name_len, nn * 4);
+    GROW(ctx->m_name_off, nn * 8);
+    GROW(ctx->m_numel, nn * 8);
+    GROW(ctx->m_ea, (nn + 1) * 8);
+    GROW(ctx->m_eb, (nn + 1) * 8);
+    GROW(ctx->m_eu, (nn + 1) * 8);
+    GROW(ctx->m_status, 64);
+    GROW(ctx->m_table, nn * sizeof(RecordRow));
+    GROW(ctx->m_size, 64);
+    MergeArgs m{};
+    m.a = static_cast<const uint8_t *>(body_a);
+    m.b = static_cast<const uint8_t *>(body_b);
+    m.a_bytes = a_bytes;
+    m.b_bytes = b_bytes;
+    m.n = n;
+    m.width = w;
+    m.targets = ctx->m_targets.as<TargetDesc>();
+    m.name_len = ctx->m_name_len.as<uint32_t>();
+    m.name_off = ctx->m_name_off.as<unsigned long long>();
+    m.numel = ctx->m_numel.as<unsigned long long>();
+    m.ea = ctx->m_ea.as<unsigned long long>();
+    m.eb = ctx->m_eb.as<unsigned long long>();
+    m.eu = ctx->m_eu.as<unsigned long long>();
+    m.status = ctx->m_status.as<uint32_t>();
+    m.table = ctx->m_table.as<RecordRow>();
+    m.body_size = ctx->m_size.as<unsigned long long>();
+    CK(launch_merge_walk(m, s), "merge walk");
+    unsigned long long h[3];
+    uint32_t st = 0;
+    CK(cudaMemcpyAsync(&st, m.status, 4, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaMemcpyAsync(&h[0], m.ea + n, 8, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaMemcpyAsync(&h[1], m.eb + n, 8, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaStreamSynchronize(s), "merge walk");
+    if (st != kOk)
+        return fail(ctx, st <= 10 ? kDetailToStatus[st] : DELTA_ECORRUPT, (int)st, "delta_merge: %s",
+                    st <= 10 ? kDetailName[st] : "?");
+    m.ma = h[0];
+    m.mb = h[1];
+    GROW(ctx->m_ia, std::max<size_t>(m.ma, 1) * 8);
+    GROW(ctx->m_ib, std::max<size_t>(m.mb, 1) * 8);
+    GROW(ctx->m_va, std::max<size_t>(m.ma, 1) * w);
+    GROW(ctx->m_vb, std::max<size_t>(m.mb, 1) * w);
+    GROW(ctx->m_lb, std::max<size_t>(m.ma, 1) * 8);
+    GROW(ctx->m_dup, std::max<size_t>(m.ma, 1) * 4);
+    GROW(ctx->m_ds, (m.ma + 1) * 8);
+    m.ia = ctx->m_ia.as<unsigned long long>();
+    m.ib = ctx->m_ib.as<unsigned long long>();
+    m.va = ctx->m_va.p;
+    m.vb = ctx->m_vb.p;
+    m.lb = ctx->m_lb.as<unsigned long long>();
+    m.dup = ctx->m_dup.as<uint32_t>();
+    m.ds = ctx->m_ds.as<unsigned long long>();
+    // decode both bodies with the apply's validation (A1-A3), targets = the walk's
+    if (!ctx->a_state.p) {
+        GROW(ctx->a_state, sizeof(ApplyState));
+        CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(ApplyState), s), "memset");
+    }
+    GROW(ctx->a_recs, nn * sizeof(ApplyRec));
+    GROW(ctx->a_rcb, (nn + 1) * 8);
+    const size_t nch = std::max(a_bytes, b_bytes) / kByteChunk + n + 2;
+    GROW(ctx->a_cnt, nch * 4);
+    GROW(ctx->a_crec, nch * 4);
+    GROW(ctx->a_sum, nch * 8);
+    GROW(ctx->a_ord, nch * 8);
+    GROW(ctx->a_idx, nch * 8);
+    uint32_t dst[2] = {0, 0};
+    for (int x = 0; x < 2; ++x) {
+        CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(uint32_t), s), "memset");  // this pass's gate
+        ApplyArgs a;
+        a.body = x ? m.b : m.a;
+        a.body_bytes = x ? b_bytes : a_bytes;
+        a.targets = m.targets;
+        a.n = n;
+        a.names = m.b;
+        a.hint = nullptr;
+        a.recs = ctx->a_recs.as<ApplyRec>();
+        a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
+        a.chunk_rec = ctx->a_crec.as<uint32_t>();
+        a.chunk_count = ctx->a_cnt.as<unsigned int>();
+        a.chunk_sum = ctx->a_sum.as<unsigned long long>();
+        a.chunk_ord_base = ctx->a_ord.as<unsigned long long>();
+        a.chunk_idx_base = ctx->a_idx.as<unsigned long long>();
+        a.chunk_cap = nch;
+        a.state = ctx->a_state.as<ApplyState>();
+        a.width = w;
+        a.persist_ctas = ctx->sm_count * ctx->apply_ctas_per_sm;
+        a.scatter_ctas = ctx->sm_count * ctx->scatter_ctas_per_sm;
+        a.entry_major = false;
+        a.index_codec = 0;
+        CK(launch_decode_only(a, x ? m.ib : m.ia, x ? m.vb : m.va, x ? m.eb : m.ea, s), "merge decode");
+        CK(cudaMemcpyAsync(&dst[x], ctx->a_state.p, 4, cudaMemcpyDeviceToHost, s), "readback");
+    }
+    CK(cudaStreamSynchronize(s), "merge decode");
+    for (int x = 0; x < 2; ++x)
+        if (dst[x] != kOk)
+            return fail(ctx, dst[x] <= 10 ? kDetailToStatus[dst[x]] : DELTA_ECORRUPT, (int)dst[x],
+                        "delta_merge: body %c: %s", x ? 'b' : 'a', dst[x] <= 10 ? kDetailName[dst[x]] : "?");
+    const size_t nblk_a = (m.ma + 4095) / 4096 + 1;
+    GROW(ctx->m_blk, std::max<size_t>(nblk_a, 1) * 8);
+    m.blk = ctx->m_blk.as<unsigned long long>();
+    CK(launch_merge_rank(m, s), "merge rank");
+    CK(cudaMemcpyAsync(&h[2], m.eu + n, 8, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaStreamSynchronize(s), "merge rank");
+    m.mu = h[2];
+    GROW(ctx->m_u, std::max<size_t>(m.mu, 1) * 8);
+    GROW(ctx->m_uv, std::max<size_t>(m.mu, 1) * w);
+    GROW(ctx->m_len, std::max<size_t>(m.mu, 1) * 4);
+    GROW(ctx->m_lo, (m.mu + 1) * 8);
+    GROW(ctx->m_blk, std::max<size_t>(std::max(nblk_a, (size_t)((m.mu + 4095) / 4096 + 1)), 1) * 8);
+    m.blk = ctx->m_blk.as<unsigned long long>();
+    m.u = ctx->m_u.as<unsigned long long>();
+    m.uv = ctx->m_uv.p;
+    m.len = ctx->m_len.as<uint32_t>();
+    m.lo = ctx->m_lo.as<unsigned long long>();
+    CK(launch_merge_place(m, s), "merge place");
+    unsigned long long size = 0;
+    CK(cudaMemcpyAsync(&size, m.body_size, 8, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaStreamSynchronize(s), "merge place");
+    *out_bytes = size;
+    if (size > out_capacity)
+        return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < merged body size %llu",
+                    (unsigned long long)out_capacity, size);
+    CK(launch_merge_emit(m, static_cast<uint8_t *>(out), s), "merge emit");
+    return DELTA_OK;
+}
+

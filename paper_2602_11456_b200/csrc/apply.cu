@@ -587,6 +587,67 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     }
 }
 
+// ------------------------------------------------------------------------------ decode-only
+// delta_merge's decode of a validated body (gated like A4): entry `ord` of record k gets
+// its absolute index and value written at entry_base[k] + ord.
+template <int W>
+__global__ void __launch_bounds__(256)
+k_decode_write(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs,
+               const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
+               const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ ord_base,
+               const unsigned long long *__restrict__ idx_base, const unsigned long long *__restrict__ entry_base,
+               unsigned long long *__restrict__ idx_out, typename std::conditional<W == 2, uint16_t, uint32_t>::type *val_out,
+               ApplyState *st) {
+    using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
+    if (st->status != kOk) return;
+    const unsigned long long nch = st->n_chunks;
+    __shared__ __align__(16) uint8_t sb[kStageBytes];
+    __shared__ __align__(16) uint8_t svb[kByteChunk * W + 32];
+    __shared__ uint32_t s_cnt[8];
+    __shared__ unsigned long long s_sum[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        const uint32_t k = __ldg(chunk_rec + c);
+        const ApplyRec R = recs[k];
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
+        const unsigned long long ob = ord_base[c];
+        const uint32_t cn = chunk_count[c];
+        const uint8_t *vals = stage_bytes(svb, body + R.val_off + ob * W, cn * W);
+        __syncthreads();
+        uint32_t cnt = 0;
+        unsigned long long sum = 0;
+        decode_thread(v, [&](unsigned long long x) {
+            ++cnt;
+            sum += x;
+        });
+        const uint32_t ci = warp_inclusive_sum(cnt);
+        const unsigned long long si = warp_inclusive_sum(sum);
+        if (lane == 31) {
+            s_cnt[warp] = ci;
+            s_sum[warp] = si;
+        }
+        __syncthreads();
+        uint32_t cpre = 0;
+        unsigned long long spre = 0;
+        for (int w = 0; w < warp; ++w) {
+            cpre += s_cnt[w];
+            spre += s_sum[w];
+        }
+        uint32_t o = cpre + ci - cnt;
+        unsigned long long idx = idx_base[c] + spre + si - sum;
+        const unsigned long long e0 = entry_base[k] + ob;
+        decode_thread(v, [&](unsigned long long x) {
+            idx += x;
+            idx_out[e0 + o] = idx;
+            if constexpr (W == 2) val_out[e0 + o] = (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
+            else val_out[e0 + o] = (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) |
+                                   ((LT)vals[4 * o + 3] << 24);
+            ++o;
+        });
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------------------ A2f / A4f
 // Fixed-width index codec (reading R18): chunk c of a record holds entries
 // [c * kByteChunk / iw, ...) of its absolute index array.  The chunk's indices (plus the
@@ -716,6 +777,26 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     }
 #undef SCATTER
     if (ev) cudaEventRecord(ev[4], s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_only(const ApplyArgs &a, unsigned long long *idx_out, void *val_out,
+                               const unsigned long long *entry_base, cudaStream_t s) {
+    k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
+                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width, 0);
+    k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
+                                                  a.chunk_count, a.chunk_sum, a.state);
+    const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
+    k_apply_scan<<<nb, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
+                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
+    if (a.width == 2)
+        k_decode_write<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.chunk_count,
+                                                         a.chunk_ord_base, a.chunk_idx_base, entry_base, idx_out,
+                                                         static_cast<uint16_t *>(val_out), a.state);
+    else
+        k_decode_write<4><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.chunk_count,
+                                                         a.chunk_ord_base, a.chunk_idx_base, entry_base, idx_out,
+                                                         static_cast<uint32_t *>(val_out), a.state);
     return cudaGetLastError();
 }
 

@@ -71,8 +71,8 @@ static_assert(sizeof(RecordRow) == 56, "RecordRow matches delta_record_info");
 struct TargetDesc {
     uint8_t *w;
     unsigned long long numel;
-    uint32_t name_off;  // into the names blob
-    uint32_t name_len;
+    unsigned long long name_off;  // into the names blob (delta_merge: into the second body)
+    unsigned long long name_len;
 };
 
 // Fixed-width index codec (reading R18): 4-byte indices iff N - 1 fits int32.
@@ -178,5 +178,39 @@ cudaError_t launch_assemble(const uint8_t *src, uint8_t *dst, unsigned long long
 
 // ev: nullptr, or 5 events: before A1, after A1, A2, A3, A4.
 cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev);  // A1-A4
+// A1-A3, then (gated) every entry's absolute index and value written to idx_out / val_out at
+// entry_base[record] + ordinal (delta_merge's decode of a body; targets carry no w).
+cudaError_t launch_decode_only(const ApplyArgs &a, unsigned long long *idx_out, void *val_out,
+                               const unsigned long long *entry_base, cudaStream_t s);
+// delta_merge (merge.cu): see api.cu
+struct MergeArgs {
+    const uint8_t *a, *b;                 // the two bodies
+    unsigned long long a_bytes, b_bytes;
+    uint32_t n;                           // records expected in each
+    int width;
+    TargetDesc *targets;                  // n: B's names / element counts, for A1 of both decodes
+    uint32_t *name_len;                   // n
+    unsigned long long *name_off;         // n (into body b)
+    unsigned long long *numel;            // n
+    unsigned long long *ea, *eb, *eu;     // n + 1 entry prefixes of a, b and the union
+    uint32_t *status;                     // walk status (kOk / k* code)
+    unsigned long long *ia, *ib;          // decoded absolute indices
+    void *va, *vb;                        // decoded values
+    unsigned long long *lb;               // ma: lower bound of each a entry in its b segment
+    uint32_t *dup;                        // ma + 1 (scan input), then the exclusive scan in ds
+    unsigned long long *ds;               // ma + 1
+    unsigned long long *u;                // mu merged indices
+    void *uv;                             // mu merged values
+    uint32_t *len;                        // mu LEB128 lengths
+    unsigned long long *lo;               // mu + 1 byte offsets (exclusive scan of len)
+    unsigned long long *blk;              // scan scratch
+    RecordRow *table;                     // n
+    unsigned long long *body_size;        // 1
+    unsigned long long ma, mb, mu;
+};
+cudaError_t launch_merge_walk(const MergeArgs &m, cudaStream_t s);
+cudaError_t launch_merge_rank(const MergeArgs &m, cudaStream_t s);     // lb, dup, ds, eu
+cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s);    // u, uv, len, lo, table, body_size
+cudaError_t launch_merge_emit(const MergeArgs &m, uint8_t *out, cudaStream_t s);
 
 }  // namespace sd

@@ -740,3 +740,81 @@ def test_extract_and_advance(sd):
         ctx.delta_extract_async(tensors, torch.empty(1 << 20, dtype=torch.uint8, device=DEV),
                                 torch.zeros(1, dtype=torch.int64, device=DEV))
     ctx.close()
+
+
+# ------------------------------------------------------------------ delta merge (NEXT f4)
+def _three_versions(n, seed, rho1, rho2, overlap):
+    """v0 -> v1 (rho1 uniform), v1 -> v2 (rho2 uniform, plus a share `overlap` of v1's
+    changed lanes changed again); bf16 lanes as numpy uint16."""
+    rng = np.random.default_rng(seed)
+    v0 = rng.integers(0, 2**16, n, dtype=np.uint64).astype(np.uint16)
+    m1 = rng.random(n) < rho1
+    v1 = v0.copy()
+    v1[m1] ^= rng.integers(1, 16, int(m1.sum()), dtype=np.uint64).astype(np.uint16)
+    m2 = rng.random(n) < rho2
+    again = np.flatnonzero(m1)
+    m2[again[rng.random(again.size) < overlap]] = True
+    v2 = v1.copy()
+    v2[m2] ^= rng.integers(1, 16, int(m2.sum()), dtype=np.uint64).astype(np.uint16)
+    return v0, v1, v2
+
+
+def _dev(a):
+    return torch.from_numpy(a.view(np.int16).copy()).to(DEV).view(torch.bfloat16)
+
+
+def test_merge_parity(sd):
+    """delta_merge on the GPU == oracle.codec.merge byte for byte, and applying the merge
+    to v0 gives v2 (M1-sized multi-chunk record, dense, overlapping, empty, 1-lane)."""
+    cases = [(16_777_216, 0.01, 0.01, 0.3), (300_001, 0.4, 0.2, 0.5), (5000, 0.0, 0.05, 0.0),
+             (5000, 0.05, 0.0, 0.0), (0, 0.0, 0.0, 0.0), (1, 1.0, 1.0, 1.0), (100_003, 0.001, 0.001, 1.0)]
+    names = [f"m{k}.weight" for k in range(len(cases))]
+    vs = [_three_versions(n, 70 + k, r1, r2, ov) for k, (n, r1, r2, ov) in enumerate(cases)]
+    ctx = sd.DeltaContext(DEV)
+    a, _ = ctx.delta_extract([(nm, _dev(v[0]), _dev(v[1])) for nm, v in zip(names, vs)])
+    a = a.clone()
+    b, _ = ctx.delta_extract([(nm, _dev(v[1]), _dev(v[2])) for nm, v in zip(names, vs)])
+    b = b.clone()
+    merged = ctx.delta_merge(a, b, len(names))
+    torch.cuda.synchronize()
+    want = oracle.codec.merge(a.cpu().numpy().tobytes(), b.cpu().numpy().tobytes(), 2)
+    assert_body_equal(merged, want)
+    targets = [(nm, _dev(v[0])) for nm, v in zip(names, vs)]
+    ctx.delta_apply(targets, merged)
+    torch.cuda.synchronize()
+    for (_, t), v in zip(targets, vs):
+        assert np.array_equal(to_np(t), v[2])
+    ctx.close()
+
+
+def test_merge_rejects(sd):
+    """Faults in either body: the GPU's error kind equals the oracle's (and nothing is
+    written to out)."""
+    x = np.arange(50, dtype=np.uint16)
+    y = x.copy()
+    y[[3, 30]] += 1
+
+    def body(name, o, n, mode=0):
+        bb, _ = oracle.codec.extract([(name, [o], [n])], mode=mode)
+        return bb
+    good = body("p", x, y)
+    cases = [("name", good, body("q", x, y)), ("numel", good, body("p", np.arange(51, dtype=np.uint16),
+                                                                     np.arange(51, dtype=np.uint16) + 1)),
+             ("mode", good, body("p", x, y, mode=oracle.codec.MODE_ADDITIVE)),
+             ("layout", good, good + good)]
+    trunc = bytearray(good)
+    trunc[2 + 1 + 24 + 1] |= 0x80  # second varint keeps going into the values
+    cases.append(("truncated", good, bytes(trunc)))
+    ctx = sd.DeltaContext(DEV)
+    for kind, ba, bb in cases:
+        with pytest.raises(oracle.DeltaError) as eo:
+            oracle.codec.merge(ba, bb, 2)
+        if kind is not None:
+            assert eo.value.kind == kind
+        out = torch.full((256,), 0x5A, dtype=torch.uint8, device=DEV)
+        with pytest.raises(sd.DeltaError) as eg:
+            ctx.delta_merge(torch.tensor(list(ba), dtype=torch.uint8, device=DEV),
+                            torch.tensor(list(bb), dtype=torch.uint8, device=DEV), 1, out=out)
+        assert eg.value.kind == eo.value.kind, (eg.value, eo.value.kind)
+        assert bool((out == 0x5A).all())
+    ctx.close()
