@@ -51,6 +51,10 @@ def parse():
     p.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--host-sync", default="end", choices=["end", "step"],
+                   help="chained path: 'end' = the host enqueues the timed steps without waiting "
+                        "(one wait after the last; kernel times accumulated on the device), "
+                        "'step' = the host waits for every step")
     p.add_argument("--index-codec", default="leb128", choices=["leb128", "fixed"],
                    help="fixed: the paper's naive int32/64 index encoding (PAPER.md:387, 609; R18)")
     p.add_argument("--no-e2e", action="store_true")
@@ -377,17 +381,25 @@ def main():
                 if world > 1:
                     assemble(size, buf)
 
-            def step(acc=None):
+            def step(acc=None, wait=True):
                 # one stream of kernels: extract (size + table stay on the device) -> [assembly
-                # on the comm stream] -> chained apply; the host waits once, at the end
-                n = ctx.round_trip(tl, tg, out, size_dev, before_apply=before_apply)
+                # on the comm stream] -> chained apply; the host waits once, at the end (or,
+                # wait=False, not at all: errors surface at the next extract_wait/apply_wait)
+                n = ctx.round_trip(tl, tg, out, size_dev, before_apply=before_apply, wait=wait)
                 if world > 1:
                     torch.cuda.current_stream().wait_stream(comm)
-                record(acc)
-                return out[:n], None
+                if wait:
+                    record(acc)
+                return (out[:n] if n is not None else None), None
 
+    chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None))
+    pipelined = chained and args.host_sync == "end"
     for _ in range(max(args.warmup, 0)):
         body, table = step()
+    if pipelined:  # kernel times accumulated on the device over the timed region
+        ctx.set_profiling(2)
+        step()  # one more waited warm-up step with the accumulating event ring
+        ctx.timing_totals()
     clocks = Clocks(local, enabled=not args.no_clocks)
     acc = {}
     clocks.start()
@@ -399,9 +411,20 @@ def main():
     w0 = time.time()
     ev0.record(stream)
     for _ in range(args.steps):
-        body, table = step(acc)
+        if pipelined:
+            step(wait=False)
+        else:
+            body, table = step(acc)
     ev1.record(stream)
     torch.cuda.synchronize()
+    if pipelined:
+        nb = ctx.extract_wait()   # raises if any step's extract overflowed (never after warm-up)
+        ctx.apply_wait()          # raises if any step's apply gate was closed
+        body, table = out[:nb], None
+        tot, calls = ctx.timing_totals()
+        if calls != args.steps:
+            raise SystemExit(f"bench: {calls} extract scans timed for {args.steps} steps")
+        acc = {k: v for k, v in tot.items()}
     w1 = time.time()
     if world > 1:
         dist.barrier()
@@ -488,11 +511,33 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": k1_bytes},
-        "gpu_launches": 13 * args.steps,  # per rank: 7 (size) + 2 (extract) + 4 (apply) per step
+        # per rank and step: K1, K1b, 5 tile scans, K3, K3b (9; no K1b with fixed-width
+        # indices) + K4, K5 + A1-A4 (fixed-width: A1, A2f, A4f) [+ delta_assemble when N > 1]
+        "gpu_launches": ((15 if args.index_codec == "leb128" else 13)
+                         + (1 if world > 1 and nvasm is not None else 0)) * args.steps,
         "clocks": clk,
     }
     if k1_ms > 0:
         result["roofline"]["k1_share_of_step"] = round(k1_ms / ms_step, 4)
+    result["config"]["host_sync"] = "end (steps enqueued back to back)" if pipelined else "every step"
+    if pipelined:  # the same steps with the host waiting for each one (latency view)
+        ks = max(3, args.steps // 2)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ks):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_s = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_s = float(t.item())
+        result["host_synced"] = {"steps": ks, "ms_per_step": round(ms_s / ks, 4),
+                                 "value": round(scanned_total * ks / (ms_s / 1e3) / 1e9, 2)}
 
     # ---- e2e: the same step with inputs copied from pinned host memory every step
     if not args.no_e2e:

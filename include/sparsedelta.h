@@ -353,11 +353,23 @@ enum {
 /* Set a DELTA_OPT_* option on ctx.  DELTA_EINVAL for an unknown option or a value < 1. */
 int delta_set_option(delta_ctx *ctx, int option, int64_t value);
 
-/* Enable (1) or disable (0) per-kernel event timing on ctx.  Default: disabled. */
+/* Per-kernel event timing on ctx: 0 = off (default); 1 = the timings of the last calls,
+ * read with delta_last_timing (the synchronising calls fill them); 2 = accumulate over calls
+ * without any extra host synchronisation (each call records into the next set of a ring of 8
+ * event sets; a set is folded into the running totals when it is reused), read and reset
+ * with delta_timing_totals — for timing loops that never wait on the host between calls.
+ * Changing the mode synchronises the device and resets all timings.  DELTA_EINVAL for other
+ * values. */
 int delta_set_profiling(delta_ctx *ctx, int enable);
 
-/* Copy the timings of the last calls (see delta_timing) to *out (host). */
+/* Copy the timings of the last calls (see delta_timing) to *out (host).  Mode 1 only (all
+ * zero in mode 2). */
 int delta_last_timing(const delta_ctx *ctx, delta_timing *out);
+
+/* Mode 2: waits for the recorded events, writes the per-kernel totals since the last call
+ * (or since delta_set_profiling) to *out and the number of extract scans they cover to
+ * *calls (host), then resets them.  DELTA_EINVAL unless profiling mode is 2. */
+int delta_timing_totals(delta_ctx *ctx, delta_timing *out, uint32_t *calls);
 
 #ifdef __cplusplus
 }

@@ -199,9 +199,19 @@ class DeltaContext:
         """DELTA_OPT_* launch-shape option (performance only)."""
         self._check(self._lib.delta_set_option(self._h, option, value))
 
-    def set_profiling(self, enable: bool):
-        """Per-kernel CUDA-event timing inside the library (see delta_last_timing)."""
-        self._check(self._lib.delta_set_profiling(self._h, 1 if enable else 0))
+    def set_profiling(self, enable):
+        """Per-kernel CUDA-event timing inside the library: True / 1 = last calls
+        (last_timing), 2 = accumulated over calls without host waits (timing_totals)."""
+        mode = 1 if enable is True else (0 if enable is False else int(enable))
+        self._check(self._lib.delta_set_profiling(self._h, mode))
+
+    def timing_totals(self):
+        """Profiling mode 2: (per-kernel totals in ms since the last call, extract scans
+        covered); resets the totals."""
+        t = _abi.Timing()
+        calls = ctypes.c_uint32()
+        self._check(self._lib.delta_timing_totals(self._h, byref(t), byref(calls)))
+        return {f: getattr(t, f) for f, _ in _abi.Timing._fields_}, calls.value
 
     def last_timing(self) -> dict:
         t = _abi.Timing()
@@ -262,13 +272,21 @@ class DeltaContext:
         self._check(self._lib.delta_extract_wait(self._h, byref(nbytes)))
         return nbytes.value
 
-    def round_trip(self, tensors, targets, out, size, stream=None, before_apply=None):
+    def round_trip(self, tensors, targets, out, size, stream=None, before_apply=None, wait=True):
         """extract(tensors) -> apply into ``targets`` as one stream of kernels: the apply
         reads the body size and offset table on the device (delta_apply_async_chain), so
         the host waits once, at the end.  ``before_apply(out, size)`` may enqueue work
         between the two (e.g. the multi-GPU body assembly).  A first call at a higher
         density that overflows the tile slots (EAGAIN) is re-issued once.  Returns the
-        body size."""
+        body size.  ``wait=False``: enqueue only and return None — the host never waits, an
+        overflow leaves the apply's gate closed (targets untouched) and is reported by the
+        next extract_wait / apply_wait (steady-state loops after a first waited call)."""
+        if not wait:  # enqueue only; errors surface at the next extract_wait / apply_wait
+            table = self.delta_extract_async(tensors, out, size, stream)
+            if before_apply is not None:
+                before_apply(out, size)
+            self.delta_apply(targets, out, table=table, size=size, stream=stream, wait=False)
+            return None
         for attempt in range(2):
             table = self.delta_extract_async(tensors, out, size, stream)
             if before_apply is not None:

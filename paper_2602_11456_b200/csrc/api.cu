@@ -105,8 +105,14 @@ struct delta_ctx {
     bool advance = false;  // extract-and-advance: old_dev is overwritten with new (synchronous extract only)
 
     // ---- optional per-kernel event timing
-    bool profiling = false;
+    int profiling = 0;  // 0 off, 1 timings of the last calls, 2 accumulate over calls (ring of event sets)
     cudaEvent_t ev_scan[4] = {}, ev_emit[3] = {}, ev_apply[5] = {};
+    static constexpr int kProfRing = 8;
+    cudaEvent_t rs_scan[kProfRing][4] = {}, rs_emit[kProfRing][3] = {}, rs_apply[kProfRing][5] = {};
+    bool ru_scan[kProfRing] = {}, ru_emit[kProfRing] = {}, ru_apply[kProfRing] = {};
+    unsigned ri_scan = 0, ri_emit = 0, ri_apply = 0;
+    delta_timing acc = {};
+    uint32_t acc_calls = 0;
     delta_timing timing = {};
 };
 
@@ -196,6 +202,11 @@ void delta_ctx_destroy(delta_ctx *c) {
         for (auto &e : c->ev_scan) cudaEventDestroy(e);
         for (auto &e : c->ev_emit) cudaEventDestroy(e);
         for (auto &e : c->ev_apply) cudaEventDestroy(e);
+        for (int j = 0; j < delta_ctx::kProfRing; ++j) {
+            for (auto &e : c->rs_scan[j]) cudaEventDestroy(e);
+            for (auto &e : c->rs_emit[j]) cudaEventDestroy(e);
+            for (auto &e : c->rs_apply[j]) cudaEventDestroy(e);
+        }
     }
     if (c->h_summary) cudaFreeHost(c->h_summary);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -243,28 +254,111 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
 }
 
 int delta_set_profiling(delta_ctx *c, int enable) {
-    if (!c) return DELTA_EINVAL;
+    if (!c || enable < 0 || enable > 2) return DELTA_EINVAL;
     if (cudaSetDevice(c->device) != cudaSuccess) return DELTA_ECUDA;
     if (enable && !c->profiling) {
         for (auto &e : c->ev_scan) cudaEventCreate(&e);
         for (auto &e : c->ev_emit) cudaEventCreate(&e);
         for (auto &e : c->ev_apply) cudaEventCreate(&e);
+        for (int j = 0; j < delta_ctx::kProfRing; ++j) {
+            for (auto &e : c->rs_scan[j]) cudaEventCreate(&e);
+            for (auto &e : c->rs_emit[j]) cudaEventCreate(&e);
+            for (auto &e : c->rs_apply[j]) cudaEventCreate(&e);
+        }
         if (cudaGetLastError() != cudaSuccess) return DELTA_ECUDA;
-        c->profiling = true;
     } else if (!enable && c->profiling) {
         cudaDeviceSynchronize();
         for (auto &e : c->ev_scan) cudaEventDestroy(e);
         for (auto &e : c->ev_emit) cudaEventDestroy(e);
         for (auto &e : c->ev_apply) cudaEventDestroy(e);
-        c->profiling = false;
+        for (int j = 0; j < delta_ctx::kProfRing; ++j) {
+            for (auto &e : c->rs_scan[j]) cudaEventDestroy(e);
+            for (auto &e : c->rs_emit[j]) cudaEventDestroy(e);
+            for (auto &e : c->rs_apply[j]) cudaEventDestroy(e);
+        }
     }
+    if (enable) cudaDeviceSynchronize();
+    c->profiling = enable;
     c->timing = delta_timing{};
+    c->acc = delta_timing{};
+    c->acc_calls = 0;
+    for (int j = 0; j < delta_ctx::kProfRing; ++j) c->ru_scan[j] = c->ru_emit[j] = c->ru_apply[j] = false;
     return DELTA_OK;
 }
 
 int delta_last_timing(const delta_ctx *c, delta_timing *out) {
     if (!c || !out) return DELTA_EINVAL;
     *out = c->timing;
+    return DELTA_OK;
+}
+
+}  // extern "C"
+
+// Accumulating profiling (mode 2): each call records into the next event set of a ring;
+// a set is folded into the totals when it is reused (it is kProfRing calls old, so its
+// events have long completed) or by delta_timing_totals.
+static void fold_scan(delta_ctx *c, int j) {
+    if (!c->ru_scan[j]) return;
+    cudaEventSynchronize(c->rs_scan[j][3]);
+    c->acc.scan_ms += ev_ms(c->rs_scan[j][0], c->rs_scan[j][1]);
+    c->acc.lens_ms += ev_ms(c->rs_scan[j][1], c->rs_scan[j][2]);
+    c->acc.finalize_ms += ev_ms(c->rs_scan[j][2], c->rs_scan[j][3]);
+    c->acc_calls += 1;
+    c->ru_scan[j] = false;
+}
+static void fold_emit(delta_ctx *c, int j) {
+    if (!c->ru_emit[j]) return;
+    cudaEventSynchronize(c->rs_emit[j][2]);
+    c->acc.emit_ms += ev_ms(c->rs_emit[j][0], c->rs_emit[j][1]);
+    c->acc.headers_ms += ev_ms(c->rs_emit[j][1], c->rs_emit[j][2]);
+    c->ru_emit[j] = false;
+}
+static void fold_apply(delta_ctx *c, int j) {
+    if (!c->ru_apply[j]) return;
+    cudaEventSynchronize(c->rs_apply[j][4]);
+    c->acc.locate_ms += ev_ms(c->rs_apply[j][0], c->rs_apply[j][1]);
+    c->acc.decode_ms += ev_ms(c->rs_apply[j][1], c->rs_apply[j][2]);
+    c->acc.apply_scan_ms += ev_ms(c->rs_apply[j][2], c->rs_apply[j][3]);
+    c->acc.scatter_ms += ev_ms(c->rs_apply[j][3], c->rs_apply[j][4]);
+    c->ru_apply[j] = false;
+}
+static cudaEvent_t *prof_scan(delta_ctx *c) {
+    if (c->profiling != 2) return c->profiling ? c->ev_scan : nullptr;
+    const int j = (int)(c->ri_scan++ % delta_ctx::kProfRing);
+    fold_scan(c, j);
+    c->ru_scan[j] = true;
+    return c->rs_scan[j];
+}
+static cudaEvent_t *prof_emit(delta_ctx *c) {
+    if (c->profiling != 2) return c->profiling ? c->ev_emit : nullptr;
+    const int j = (int)(c->ri_emit++ % delta_ctx::kProfRing);
+    fold_emit(c, j);
+    c->ru_emit[j] = true;
+    return c->rs_emit[j];
+}
+static cudaEvent_t *prof_apply(delta_ctx *c) {
+    if (c->profiling != 2) return c->profiling ? c->ev_apply : nullptr;
+    const int j = (int)(c->ri_apply++ % delta_ctx::kProfRing);
+    fold_apply(c, j);
+    c->ru_apply[j] = true;
+    return c->rs_apply[j];
+}
+
+extern "C" {
+
+int delta_timing_totals(delta_ctx *c, delta_timing *out, uint32_t *calls) {
+    if (!c || !out || !calls) return DELTA_EINVAL;
+    if (c->profiling != 2) return DELTA_EINVAL;
+    if (cudaSetDevice(c->device) != cudaSuccess) return DELTA_ECUDA;
+    for (int j = 0; j < delta_ctx::kProfRing; ++j) {
+        fold_scan(c, j);
+        fold_emit(c, j);
+        fold_apply(c, j);
+    }
+    *out = c->acc;
+    *calls = c->acc_calls;
+    c->acc = delta_timing{};
+    c->acc_calls = 0;
     return DELTA_OK;
 }
 
@@ -461,10 +555,10 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
         CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
         ExtractArgs a = extract_args(ctx);
         a.redo_cap = redo_cap;
-        CK(launch_extract_scan(a, s, ctx->profiling ? ctx->ev_scan : nullptr), "extract scan launch");
+        CK(launch_extract_scan(a, s, prof_scan(ctx)), "extract scan launch");
         CK(cudaMemcpyAsync(ctx->h_summary, ctx->summary.p, sizeof(ExtractSummary), cudaMemcpyDeviceToHost, s), "readback");
         CK(cudaStreamSynchronize(s), "extract scan");
-        if (ctx->profiling) {
+        if (ctx->profiling == 1) {
             ctx->timing.scan_ms = ev_ms(ctx->ev_scan[0], ctx->ev_scan[1]);
             ctx->timing.lens_ms = ev_ms(ctx->ev_scan[1], ctx->ev_scan[2]);
             ctx->timing.finalize_ms = ev_ms(ctx->ev_scan[2], ctx->ev_scan[3]);
@@ -552,13 +646,13 @@ extern "C" int delta_extract(delta_ctx *ctx, const delta_tensor *t, uint32_t n, 
     if (need && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
     if (n)
         CK(launch_extract_emit(extract_args(ctx), static_cast<uint8_t *>(out), s,
-                               ctx->profiling ? ctx->ev_emit : nullptr),
+                               prof_emit(ctx)),
            "extract emit launch");
     if (table && n) {
         CK(cudaMemcpyAsync(table, ctx->table.p, (size_t)n * sizeof(RecordRow), cudaMemcpyDeviceToHost, s), "table readback");
     }
-    if ((table && n) || (ctx->profiling && n)) CK(cudaStreamSynchronize(s), "extract emit");
-    if (ctx->profiling && n) {
+    if ((table && n) || (ctx->profiling == 1 && n)) CK(cudaStreamSynchronize(s), "extract emit");
+    if (ctx->profiling == 1 && n) {
         ctx->timing.emit_ms = ev_ms(ctx->ev_emit[0], ctx->ev_emit[1]);
         ctx->timing.headers_ms = ev_ms(ctx->ev_emit[1], ctx->ev_emit[2]);
     }
@@ -595,9 +689,9 @@ extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32
     ExtractArgs a = extract_args(ctx);
     a.out_cap = cap;
     a.size_out = reinterpret_cast<unsigned long long *>(body_bytes_dev);
-    CK(launch_extract_scan(a, s, ctx->profiling ? ctx->ev_scan : nullptr), "extract scan launch");
+    CK(launch_extract_scan(a, s, prof_scan(ctx)), "extract scan launch");
     if (n) {
-        CK(launch_extract_emit(a, static_cast<uint8_t *>(out), s, ctx->profiling ? ctx->ev_emit : nullptr),
+        CK(launch_extract_emit(a, static_cast<uint8_t *>(out), s, prof_emit(ctx)),
            "extract emit launch");
     } else if (body_bytes_dev) {
         CK(cudaMemsetAsync(body_bytes_dev, 0, 8, s), "memset");
@@ -615,7 +709,7 @@ extern "C" int delta_extract_wait(delta_ctx *ctx, uint64_t *body_bytes) {
     ctx->async_pending = false;
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     CK(cudaEventSynchronize(ctx->ev_extract), "extract");
-    if (ctx->profiling) {
+    if (ctx->profiling == 1) {
         ctx->timing.scan_ms = ev_ms(ctx->ev_scan[0], ctx->ev_scan[1]);
         ctx->timing.lens_ms = ev_ms(ctx->ev_scan[1], ctx->ev_scan[2]);
         ctx->timing.finalize_ms = ev_ms(ctx->ev_scan[2], ctx->ev_scan[3]);
@@ -737,7 +831,7 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.scatter_ctas = ctx->sm_count * ctx->scatter_ctas_per_sm;
     a.entry_major = ctx->entry_major;
     a.index_codec = ctx->index_codec;
-    CK(launch_apply(a, s, ctx->profiling ? ctx->ev_apply : nullptr), "apply launch");
+    CK(launch_apply(a, s, prof_apply(ctx)), "apply launch");
     return DELTA_OK;
 }
 
@@ -780,7 +874,7 @@ extern "C" int delta_apply_wait(delta_ctx *ctx, void *stream) {
     CK(cudaStreamSynchronize(s), "apply");
     CK(cudaMemsetAsync(static_cast<uint8_t *>(ctx->a_state.p) + offsetof(ApplyState, first_error), 0,
                        sizeof(uint32_t), s), "memset");
-    if (ctx->profiling) {
+    if (ctx->profiling == 1) {
         ctx->timing.locate_ms = ev_ms(ctx->ev_apply[0], ctx->ev_apply[1]);
         ctx->timing.decode_ms = ev_ms(ctx->ev_apply[1], ctx->ev_apply[2]);
         ctx->timing.apply_scan_ms = ev_ms(ctx->ev_apply[2], ctx->ev_apply[3]);
