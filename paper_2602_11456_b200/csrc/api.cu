@@ -85,7 +85,7 @@ struct delta_ctx {
     uint32_t *h_asm = nullptr;  // pinned
     ApplyState *h_state = nullptr;  // pinned
     // ---- delta_merge workspace
-    DevBuf m_targets, m_name_len, m_name_off, m_numel, m_ea, m_eb, m_eu, m_status, m_ia, m_ib, m_va, m_vb, m_lb,
+    DevBuf m_ha, m_hb, m_targets, m_name_len, m_name_off, m_numel, m_ea, m_eb, m_eu, m_status, m_ia, m_ib, m_va, m_vb, m_lb,
         m_dup, m_ds, m_u, m_uv, m_len, m_lo, m_blk, m_table, m_size;
     // pinned staging ring for the per-call apply uploads (targets, hint, names): with a
     // pinned source cudaMemcpyAsync does not wait for earlier work on the stream, so
@@ -187,7 +187,7 @@ void delta_ctx_destroy(delta_ctx *c) {
     if (c && c->ev_extract) cudaEventDestroy(c->ev_extract);
     if (!c) return;
     cudaSetDevice(c->device);
-    DevBuf *mbufs[] = {&c->m_targets, &c->m_name_len, &c->m_name_off, &c->m_numel, &c->m_ea, &c->m_eb, &c->m_eu,
+    DevBuf *mbufs[] = {&c->m_ha, &c->m_hb, &c->m_targets, &c->m_name_len, &c->m_name_off, &c->m_numel, &c->m_ea, &c->m_eb, &c->m_eu,
                        &c->m_status, &c->m_ia, &c->m_ib, &c->m_va, &c->m_vb, &c->m_lb, &c->m_dup, &c->m_ds,
                        &c->m_u, &c->m_uv, &c->m_len, &c->m_lo, &c->m_blk, &c->m_table, &c->m_size};
     for (DevBuf *b : mbufs) b->release();
@@ -951,8 +951,8 @@ extern "C" int delta_digest(delta_ctx *ctx, const void *body, uint64_t bytes, ui
 // --------------------------------------------------------------------------- merge
 // delta_merge (NEXT f4, reading R19): validate both bodies (layout, pairwise names and
 // element counts, replace mode, full LEB128 decode with the apply's checks), decode them to
-// absolute (index, value) arrays, merge per record by rank, re-encode.  Four host syncs
-// (sizes of the intermediate arrays and of the result).
+// (record, index) keys + values, merge the two key arrays by merge path, re-encode.  Four
+// host syncs (sizes of the intermediate arrays and of the result).
 extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *body_a, uint64_t a_bytes,
                            const void *body_b, uint64_t b_bytes, void *out, uint64_t out_capacity, void *stream,
                            uint64_t *out_bytes) {
@@ -969,6 +969,8 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t nn = std::max<uint32_t>(n, 1);
     GROW(ctx->m_targets, nn * sizeof(TargetDesc));
+    GROW(ctx->m_ha, nn * sizeof(RecordRow));
+    GROW(ctx->m_hb, nn * sizeof(RecordRow));
     GROW(ctx->m_name_len, nn * 4);
     GROW(ctx->m_name_off, nn * 8);
     GROW(ctx->m_numel, nn * 8);
@@ -986,6 +988,8 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     m.n = n;
     m.width = w;
     m.targets = ctx->m_targets.as<TargetDesc>();
+    m.ha = ctx->m_ha.as<RecordRow>();
+    m.hb = ctx->m_hb.as<RecordRow>();
     m.name_len = ctx->m_name_len.as<uint32_t>();
     m.name_off = ctx->m_name_off.as<unsigned long long>();
     m.numel = ctx->m_numel.as<unsigned long long>();
@@ -1002,6 +1006,8 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     CK(cudaMemcpyAsync(&h[0], m.ea + n, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaMemcpyAsync(&h[1], m.eb + n, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaStreamSynchronize(s), "merge walk");
+    if (st == kMergeTooLarge)
+        return fail(ctx, DELTA_EINVAL, 0, "delta_merge: element_count >= 2^40 is not supported");
     if (st != kOk)
         return fail(ctx, st <= 10 ? kDetailToStatus[st] : DELTA_ECORRUPT, (int)st, "delta_merge: %s",
                     st <= 10 ? kDetailName[st] : "?");
@@ -1011,16 +1017,10 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     GROW(ctx->m_ib, std::max<size_t>(m.mb, 1) * 8);
     GROW(ctx->m_va, std::max<size_t>(m.ma, 1) * w);
     GROW(ctx->m_vb, std::max<size_t>(m.mb, 1) * w);
-    GROW(ctx->m_lb, std::max<size_t>(m.ma, 1) * 8);
-    GROW(ctx->m_dup, std::max<size_t>(m.ma, 1) * 4);
-    GROW(ctx->m_ds, (m.ma + 1) * 8);
     m.ia = ctx->m_ia.as<unsigned long long>();
     m.ib = ctx->m_ib.as<unsigned long long>();
     m.va = ctx->m_va.p;
     m.vb = ctx->m_vb.p;
-    m.lb = ctx->m_lb.as<unsigned long long>();
-    m.dup = ctx->m_dup.as<uint32_t>();
-    m.ds = ctx->m_ds.as<unsigned long long>();
     // decode both bodies with the apply's validation (A1-A3), targets = the walk's
     if (!ctx->a_state.p) {
         GROW(ctx->a_state, sizeof(ApplyState));
@@ -1043,7 +1043,7 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
         a.targets = m.targets;
         a.n = n;
         a.names = m.b;
-        a.hint = nullptr;
+        a.hint = x ? m.hb : m.ha;  // the walk's rows: A1 verifies all records in parallel
         a.recs = ctx->a_recs.as<ApplyRec>();
         a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
         a.chunk_rec = ctx->a_crec.as<uint32_t>();
@@ -1066,19 +1066,21 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
         if (dst[x] != kOk)
             return fail(ctx, dst[x] <= 10 ? kDetailToStatus[dst[x]] : DELTA_ECORRUPT, (int)dst[x],
                         "delta_merge: body %c: %s", x ? 'b' : 'a', dst[x] <= 10 ? kDetailName[dst[x]] : "?");
-    const size_t nblk_a = (m.ma + 4095) / 4096 + 1;
-    GROW(ctx->m_blk, std::max<size_t>(nblk_a, 1) * 8);
+    m.ntiles = (m.ma + m.mb + 2047) / 2048;
+    GROW(ctx->m_dup, std::max<size_t>(m.ntiles, 1) * 4);
+    GROW(ctx->m_ds, (m.ntiles + 1) * 8);
+    GROW(ctx->m_blk, ((std::max<size_t>(m.ntiles, m.ma + m.mb) + 4095) / 4096 + 1) * 8);
+    m.tile_cnt = ctx->m_dup.as<uint32_t>();
+    m.tile_off = ctx->m_ds.as<unsigned long long>();
     m.blk = ctx->m_blk.as<unsigned long long>();
-    CK(launch_merge_rank(m, s), "merge rank");
-    CK(cudaMemcpyAsync(&h[2], m.eu + n, 8, cudaMemcpyDeviceToHost, s), "readback");
-    CK(cudaStreamSynchronize(s), "merge rank");
+    CK(launch_merge_count(m, s), "merge count");
+    CK(cudaMemcpyAsync(&h[2], m.tile_off + m.ntiles, 8, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaStreamSynchronize(s), "merge count");
     m.mu = h[2];
     GROW(ctx->m_u, std::max<size_t>(m.mu, 1) * 8);
     GROW(ctx->m_uv, std::max<size_t>(m.mu, 1) * w);
     GROW(ctx->m_len, std::max<size_t>(m.mu, 1) * 4);
     GROW(ctx->m_lo, (m.mu + 1) * 8);
-    GROW(ctx->m_blk, std::max<size_t>(std::max(nblk_a, (size_t)((m.mu + 4095) / 4096 + 1)), 1) * 8);
-    m.blk = ctx->m_blk.as<unsigned long long>();
     m.u = ctx->m_u.as<unsigned long long>();
     m.uv = ctx->m_uv.p;
     m.len = ctx->m_len.as<uint32_t>();

@@ -58,8 +58,9 @@ __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_by
     const uint8_t mode = body[end - 1];
     if (mode > 1) return kMode;  // 0 replace, 1 additive
     if (nl != tg.name_len) return kName;
-    for (unsigned long long b = 0; b < nl; ++b)
-        if (body[ro + 2 + b] != names[tg.name_off + b]) return kName;
+    uint32_t diff = 0;  // no early exit: the byte loads are independent
+    for (unsigned long long b = 0; b < nl; ++b) diff |= body[ro + 2 + b] ^ names[tg.name_off + b];
+    if (diff) return kName;
     if (N != tg.numel) return kNumel;
     if (fixed) {  // reading R18: a whole number of fixed-width indices, one per entry
         const uint32_t iw = fixed_index_width(N);
@@ -589,7 +590,8 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
 
 // ------------------------------------------------------------------------------ decode-only
 // delta_merge's decode of a validated body (gated like A4): entry `ord` of record k gets
-// its absolute index and value written at entry_base[k] + ord.
+// the key (k << kKeyShift) | index and its value written at entry_base[k] + ord — keys
+// ascend over the whole body, so the two bodies merge as two sorted arrays.
 template <int W>
 __global__ void __launch_bounds__(256)
 k_decode_write(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs,
@@ -636,9 +638,10 @@ k_decode_write(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
         uint32_t o = cpre + ci - cnt;
         unsigned long long idx = idx_base[c] + spre + si - sum;
         const unsigned long long e0 = entry_base[k] + ob;
+        const unsigned long long key = (unsigned long long)k << kKeyShift;  // (record, index) keys
         decode_thread(v, [&](unsigned long long x) {
             idx += x;
-            idx_out[e0 + o] = idx;
+            idx_out[e0 + o] = key | idx;
             if constexpr (W == 2) val_out[e0 + o] = (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
             else val_out[e0 + o] = (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) |
                                    ((LT)vals[4 * o + 3] << 24);

@@ -4,17 +4,21 @@
 // open).  Per tensor: the union of the two index sets, D_b's value where D_b has the
 // index, else D_a's — applying the merge equals applying D_a then D_b.
 //
-//   M1 k_merge_walk     one thread walks both bodies' record headers in order: layout,
-//                       mode byte (replace only), names and element counts equal pairwise;
-//                       entry prefixes E_a, E_b; apply targets (B's names) for the decodes.
+//   M1 k_merge_walk     one thread follows both bodies' chains of record offsets (layout,
+//                       entry prefixes E_a, E_b, table rows); k_merge_check per record in
+//                       parallel: mode byte (replace only), names and element counts equal
+//                       pairwise; apply targets (B's names) and table hints for the decodes.
 //   (decode)            each body through A1-A3 + k_decode_write (apply.cu): validated,
 //                       absolute indices + values per entry.
-//   M2 k_merge_rank     per a-entry: lower bound in its b-segment and duplicate flag;
-//                       exclusive scan of the flags; per-record union sizes E_u.
-//   M3 k_merge_place    rank-based merge: a-entry i (not a duplicate) lands at
-//                       E_u + i' + lb(i) - dups before i; b-entry j at E_u + j' + lb_a(b_j) -
-//                       dups among a-entries below b_j.  Then LEB128 lengths of the union's
-//                       gaps, their exclusive scan, the offset table and the body size.
+//   M2 k_merge_path     merge path over the two key arrays (keys = record << 40 | index
+//                       ascend over a whole body): 2048 merged positions per tile, split
+//                       by one binary search per tile boundary, staged in shared memory,
+//                       8 positions per thread (a second binary search in shared memory);
+//                       an a-entry is dropped when the b head equals it (b's value wins).
+//                       Pass 1 counts the kept entries per tile, pass 2 writes them at the
+//                       scanned offsets.
+//   M3 k_merge_bounds   record boundaries of the union; LEB128 length of every gap, their
+//                       exclusive scan, the offset table and the body size.
 //   M4 k_merge_emit     LEB128 bytes + values per entry; k_merge_headers per record.
 //
 // Product code; shares nothing with oracle/.
@@ -38,28 +42,7 @@ __device__ __forceinline__ unsigned long long rd_u(const uint8_t *p, int nbytes)
     return x;
 }
 
-// largest k in [0, n) with e[k] <= i (e ascending, e[0] = 0 <= i)
-__device__ __forceinline__ uint32_t record_of(const unsigned long long *e, uint32_t n, unsigned long long i) {
-    uint32_t lo = 0, hi = n;  // e[lo] <= i < e[hi] (e[n] = total > i)
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (e[mid] <= i) lo = mid;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// number of elements of the ascending array s[0, n) that are < x
-__device__ __forceinline__ unsigned long long lower_bound(const unsigned long long *s, unsigned long long n,
-                                                          unsigned long long x) {
-    unsigned long long lo = 0, hi = n;
-    while (lo < hi) {
-        const unsigned long long mid = (lo + hi) >> 1;
-        if (s[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
+constexpr unsigned long long kIdxMask = (1ull << kKeyShift) - 1;
 
 // ---------------------------------------------------------------- exclusive scan u32 -> u64
 constexpr int kScanPer = 4096;  // elements per block (1024 threads x 4)
@@ -144,49 +127,51 @@ cudaError_t scan_u32(const uint32_t *x, unsigned long long m, unsigned long long
 }
 
 // ---------------------------------------------------------------- M1
-// One thread: both bodies' record headers in order (the bodies are untrusted: every read
-// is bounds-checked).  Decoding errors are left to the decode passes.
+// Record geometry of one body at offset ro (bounds-checked: the bodies are untrusted).
+// Returns false on a layout fault.
+__device__ __forceinline__ bool header_at(const uint8_t *B, unsigned long long sz, unsigned long long ro,
+                                          int width, RecordRow &r) {
+    if (ro > sz || sz - ro < 2) return false;
+    const unsigned long long nl = rd_u(B + ro, 2);
+    if (sz - ro - 2 < nl + 24) return false;
+    const unsigned long long q = ro + 2 + nl;
+    const unsigned long long N = rd_u(B + q, 8), nnz = rd_u(B + q + 8, 8), il = rd_u(B + q + 16, 8);
+    const unsigned long long rem = sz - q - 24;
+    if (il > rem || nnz > (rem - il) / (unsigned long long)width || rem - il - nnz * width < 1) return false;
+    r.record_offset = ro;
+    r.element_count = N;
+    r.nnz = nnz;
+    r.index_offset = q + 24;
+    r.index_bytes = il;
+    r.values_offset = q + 24 + il;
+    r.record_bytes = 2 + nl + 24 + il + nnz * width + 1;
+    return true;
+}
+
+// One thread follows the chain of record offsets of both bodies (the only sequential part:
+// two dependent header loads per record, the two bodies interleaved); everything else is
+// checked per record in parallel by k_merge_check.  The rows double as the decodes' table
+// hints (A1 then verifies all records in parallel).
 __global__ void k_merge_walk(MergeArgs m) {
     if (blockIdx.x || threadIdx.x) return;
     unsigned long long pa = 0, pb = 0, ea = 0, eb = 0;
     uint32_t st = kOk;
-    for (uint32_t k = 0; k < m.n && st == kOk; ++k) {
-        unsigned long long hdr[2][5];  // name_len, N, nnz, ilen, end
-        const uint8_t *bodies[2] = {m.a, m.b};
-        const unsigned long long sizes[2] = {m.a_bytes, m.b_bytes}, pos[2] = {pa, pb};
-        for (int x = 0; x < 2 && st == kOk; ++x) {
-            const uint8_t *B = bodies[x];
-            const unsigned long long sz = sizes[x], ro = pos[x];
-            if (ro > sz || sz - ro < 2) { st = kLayout; break; }
-            const unsigned long long nl = rd_u(B + ro, 2);
-            if (sz - ro - 2 < nl + 24) { st = kLayout; break; }
-            const unsigned long long q = ro + 2 + nl;
-            const unsigned long long N = rd_u(B + q, 8), nnz = rd_u(B + q + 8, 8), il = rd_u(B + q + 16, 8);
-            const unsigned long long rem = sz - q - 24;
-            if (il > rem || nnz > (rem - il) / (unsigned long long)m.width || rem - il - nnz * m.width < 1) {
-                st = kLayout;
-                break;
-            }
-            const unsigned long long end = q + 24 + il + nnz * m.width + 1;
-            if (B[end - 1] != 0) { st = kMode; break; }  // replace-mode records only
-            hdr[x][0] = nl; hdr[x][1] = N; hdr[x][2] = nnz; hdr[x][3] = il; hdr[x][4] = end;
+    for (uint32_t k = 0; k < m.n; ++k) {
+        RecordRow ra, rb;
+        const bool oa = header_at(m.a, m.a_bytes, pa, m.width, ra);
+        const bool ob = header_at(m.b, m.b_bytes, pb, m.width, rb);
+        if (!oa || !ob) {
+            st = kLayout;
+            break;
         }
-        if (st != kOk) break;
-        if (hdr[0][0] != hdr[1][0]) { st = kName; break; }
-        for (unsigned long long j = 0; j < hdr[0][0]; ++j)
-            if (m.a[pa + 2 + j] != m.b[pb + 2 + j]) { st = kName; break; }
-        if (st != kOk) break;
-        if (hdr[0][1] != hdr[1][1]) { st = kNumel; break; }
-        m.targets[k] = TargetDesc{nullptr, hdr[1][1], pb + 2, hdr[1][0]};
-        m.name_len[k] = (uint32_t)hdr[1][0];
-        m.name_off[k] = pb + 2;
-        m.numel[k] = hdr[1][1];
+        m.ha[k] = ra;
+        m.hb[k] = rb;
         m.ea[k] = ea;
         m.eb[k] = eb;
-        ea += hdr[0][2];
-        eb += hdr[1][2];
-        pa = hdr[0][4];
-        pb = hdr[1][4];
+        ea += ra.nnz;
+        eb += rb.nnz;
+        pa += ra.record_bytes;
+        pb += rb.record_bytes;
     }
     if (st == kOk && (pa != m.a_bytes || pb != m.b_bytes)) st = kLayout;
     m.ea[m.n] = ea;
@@ -194,69 +179,160 @@ __global__ void k_merge_walk(MergeArgs m) {
     *m.status = st;
 }
 
-// ---------------------------------------------------------------- M2
-__global__ void __launch_bounds__(256) k_merge_rank(MergeArgs m) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m.ma; i += stride) {
-        const uint32_t k = record_of(m.ea, m.n, i);
-        const unsigned long long a = m.ia[i], b0 = m.eb[k], nb = m.eb[k + 1] - b0;
-        const unsigned long long l = lower_bound(m.ib + b0, nb, a);
-        m.lb[i] = l;
-        m.dup[i] = (l < nb && m.ib[b0 + l] == a) ? 1u : 0u;
+// Per record (parallel): replace-mode bytes, equal names and element counts, the element
+// count within the 40-bit index field of the merge keys; apply targets for the decodes.
+__global__ void __launch_bounds__(256) k_merge_check(MergeArgs m) {
+    if (*m.status != kOk) return;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < m.n; k += gridDim.x * blockDim.x) {
+        const RecordRow ra = m.ha[k], rb = m.hb[k];
+        uint32_t e = kOk;
+        if (m.a[ra.record_offset + ra.record_bytes - 1] != 0 || m.b[rb.record_offset + rb.record_bytes - 1] != 0) {
+            e = kMode;  // replace-mode records only
+        } else {
+            const unsigned long long nla = ra.index_offset - 24 - 2 - ra.record_offset;
+            const unsigned long long nlb = rb.index_offset - 24 - 2 - rb.record_offset;
+            uint32_t diff = nla != nlb;
+            for (unsigned long long j = 0; j < nlb && !diff; j += 16) {
+                const unsigned long long jn = min(nlb, j + 16);
+                for (unsigned long long x = j; x < jn; ++x)
+                    diff |= m.a[ra.record_offset + 2 + x] ^ m.b[rb.record_offset + 2 + x];
+            }
+            if (diff) e = kName;
+            else if (ra.element_count != rb.element_count) e = kNumel;
+            else if (rb.element_count > kIdxMask + 1) e = kMergeTooLarge;
+            m.targets[k] = TargetDesc{nullptr, rb.element_count, rb.record_offset + 2, nlb};
+            m.name_len[k] = (uint32_t)nlb;
+            m.name_off[k] = rb.record_offset + 2;
+            m.numel[k] = rb.element_count;
+        }
+        if (e != kOk) atomicCAS(m.status, (uint32_t)kOk, e);
     }
 }
 
-// per record: union size (one block; the record count is small)
-__global__ void __launch_bounds__(1024) k_merge_union(MergeArgs m) {
-    __shared__ unsigned long long s_w[32];
-    unsigned long long carry = 0;
-    for (uint32_t b = 0; b < m.n; b += 1024) {
-        const uint32_t k = b + threadIdx.x;
-        unsigned long long nu = 0;
-        if (k < m.n) {
-            const unsigned long long dups = m.ds[m.ea[k + 1]] - m.ds[m.ea[k]];
-            nu = (m.ea[k + 1] - m.ea[k]) + (m.eb[k + 1] - m.eb[k]) - dups;
-        }
-        unsigned long long tot;
-        const unsigned long long ex = block_scan_excl(nu, s_w, tot);
-        if (k < m.n) m.eu[k] = carry + ex;
-        carry += tot;
+// ---------------------------------------------------------------- M2
+constexpr int kMpTile = 2048;  // merged positions per tile (256 threads x 8)
+
+// number of A elements among the first d positions of merge(A, B), A first on ties
+template <typename T>
+__device__ __forceinline__ unsigned long long mp_split(const T *A, unsigned long long na, const T *B,
+                                                       unsigned long long nb, unsigned long long d) {
+    unsigned long long lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+    while (lo < hi) {
+        const unsigned long long mid = (lo + hi) >> 1;
+        if (A[mid] <= B[d - mid - 1]) lo = mid + 1;
+        else hi = mid;
     }
-    if (threadIdx.x == 0) m.eu[m.n] = carry;
+    return lo;
+}
+
+template <int W, bool WRITE>
+__global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
+    using LT = typename Lane<W>::T;
+    __shared__ unsigned long long sa[kMpTile + 1], sb[kMpTile + 1];
+    __shared__ unsigned long long s_cut[4];
+    __shared__ uint32_t s_w[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned long long total = m.ma + m.mb;
+    for (unsigned long long t = blockIdx.x; t < m.ntiles; t += gridDim.x) {
+        const unsigned long long d0 = t * kMpTile, d1 = min(d0 + kMpTile, total);
+        if (tid == 0) {
+            const unsigned long long i = mp_split(m.ia, m.ma, m.ib, m.mb, d0);
+            s_cut[0] = i;
+            s_cut[1] = d0 - i;
+        } else if (tid == 32) {
+            const unsigned long long i = mp_split(m.ia, m.ma, m.ib, m.mb, d1);
+            s_cut[2] = i;
+            s_cut[3] = d1 - i;
+        }
+        __syncthreads();
+        const unsigned long long i0 = s_cut[0], j0 = s_cut[1];
+        const uint32_t na = (uint32_t)(s_cut[2] - i0), nb = (uint32_t)(s_cut[3] - j0);
+        for (uint32_t x = tid; x < na; x += blockDim.x) sa[x] = m.ia[i0 + x];
+        for (uint32_t x = tid; x < nb; x += blockDim.x) sb[x] = m.ib[j0 + x];
+        if (tid == 0) {  // the heads just past the tile (a b head there can equal our last a)
+            sa[na] = i0 + na < m.ma ? m.ia[i0 + na] : ~0ull;
+            sb[nb] = j0 + nb < m.mb ? m.ib[j0 + nb] : ~0ull;
+        }
+        __syncthreads();
+        const uint32_t n = na + nb, e0 = min((uint32_t)tid * 8u, n), e1 = min(e0 + 8u, n);
+        const uint32_t i_start = (uint32_t)mp_split(sa, na, sb, nb, e0);
+        uint32_t keep = 0;
+        {
+            uint32_t i = i_start, j = e0 - i_start;
+            for (uint32_t e = e0; e < e1; ++e) {
+                if (j >= nb || (i < na && sa[i] <= sb[j])) {
+                    keep += sa[i] != sb[j];
+                    ++i;
+                } else {
+                    ++keep;
+                    ++j;
+                }
+            }
+        }
+        // block scan of the kept counts
+        uint32_t inc = keep;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_w[warp] = inc;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            if (w < warp) pre += s_w[w];
+            tot += s_w[w];
+        }
+        if constexpr (!WRITE) {
+            if (tid == 0) m.tile_cnt[t] = tot;
+        } else {
+            const LT *va = static_cast<const LT *>(m.va), *vb = static_cast<const LT *>(m.vb);
+            LT *uv = static_cast<LT *>(m.uv);
+            unsigned long long p = m.tile_off[t] + pre + inc - keep;
+            uint32_t i = i_start, j = e0 - i_start;
+            for (uint32_t e = e0; e < e1; ++e) {
+                if (j >= nb || (i < na && sa[i] <= sb[j])) {
+                    if (sa[i] != sb[j]) {
+                        m.u[p] = sa[i];
+                        uv[p] = va[i0 + i];
+                        ++p;
+                    }
+                    ++i;
+                } else {
+                    m.u[p] = sb[j];
+                    uv[p] = vb[j0 + j];
+                    ++p;
+                    ++j;
+                }
+            }
+        }
+        __syncthreads();  // shared staging reused by the next tile
+    }
 }
 
 // ---------------------------------------------------------------- M3
-template <int W>
-__global__ void __launch_bounds__(256) k_merge_place(MergeArgs m) {
-    using LT = typename Lane<W>::T;
-    const LT *va = static_cast<const LT *>(m.va), *vb = static_cast<const LT *>(m.vb);
-    LT *uv = static_cast<LT *>(m.uv);
+// record boundaries of the union: eu[k] = first position of record k (eu pre-set to ~0)
+__global__ void __launch_bounds__(256) k_merge_bounds(MergeArgs m) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    const unsigned long long t0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    for (unsigned long long i = t0; i < m.ma; i += stride) {
-        if (m.dup[i]) continue;  // b's value wins
-        const uint32_t k = record_of(m.ea, m.n, i);
-        const unsigned long long a0 = m.ea[k];
-        const unsigned long long p = m.eu[k] + (i - a0) + m.lb[i] - (m.ds[i] - m.ds[a0]);
-        m.u[p] = m.ia[i];
-        uv[p] = va[i];
+    for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < m.mu; p += stride) {
+        const unsigned long long k = m.u[p] >> kKeyShift;
+        if (p == 0 || (m.u[p - 1] >> kKeyShift) != k) m.eu[k] = p;
     }
-    for (unsigned long long j = t0; j < m.mb; j += stride) {
-        const uint32_t k = record_of(m.eb, m.n, j);
-        const unsigned long long a0 = m.ea[k], na = m.ea[k + 1] - a0, b = m.ib[j];
-        const unsigned long long l = lower_bound(m.ia + a0, na, b);
-        const unsigned long long p = m.eu[k] + (j - m.eb[k]) + l - (m.ds[a0 + l] - m.ds[a0]);
-        m.u[p] = b;
-        uv[p] = vb[j];
-    }
+}
+
+__global__ void k_merge_bounds_fill(MergeArgs m) {  // records without entries start where the next one does
+    if (blockIdx.x || threadIdx.x) return;
+    m.eu[m.n] = m.mu;
+    for (uint32_t k = m.n; k-- > 0;)
+        if (m.eu[k] == ~0ull) m.eu[k] = m.eu[k + 1];
 }
 
 // LEB128 length of every union entry's gap (first entry of a record: the index itself)
 __global__ void __launch_bounds__(256) k_merge_len(MergeArgs m) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < m.mu; p += stride) {
-        const uint32_t k = record_of(m.eu, m.n, p);
-        const unsigned long long g = p == m.eu[k] ? m.u[p] : m.u[p] - m.u[p - 1];
+        const unsigned long long k = m.u[p] >> kKeyShift, x = m.u[p] & kIdxMask;
+        const unsigned long long g = p == m.eu[k] ? x : x - (m.u[p - 1] & kIdxMask);
         m.len[p] = leb_len(g);
     }
 }
@@ -298,10 +374,10 @@ __global__ void __launch_bounds__(256) k_merge_emit(MergeArgs m, uint8_t *__rest
     const LT *uv = static_cast<const LT *>(m.uv);
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < m.mu; p += stride) {
-        const uint32_t k = record_of(m.eu, m.n, p);
+        const unsigned long long k = m.u[p] >> kKeyShift, x = m.u[p] & kIdxMask;
         const RecordRow r = m.table[k];
         const unsigned long long e0 = m.eu[k];
-        unsigned long long g = p == e0 ? m.u[p] : m.u[p] - m.u[p - 1];
+        unsigned long long g = p == e0 ? x : x - (m.u[p - 1] & kIdxMask);
         uint8_t *q = out + r.index_offset + (m.lo[p] - m.lo[e0]);
         const uint32_t L = m.len[p];
         for (uint32_t j = 0; j + 1 < L; ++j) {
@@ -344,25 +420,31 @@ uint32_t grid_for(unsigned long long m) {
 
 cudaError_t launch_merge_walk(const MergeArgs &m, cudaStream_t s) {
     k_merge_walk<<<1, 32, 0, s>>>(m);
+    if (m.n) k_merge_check<<<(m.n + 255) / 256, 256, 0, s>>>(m);
     return cudaGetLastError();
 }
 
-cudaError_t launch_merge_rank(const MergeArgs &m, cudaStream_t s) {
-    if (m.ma) k_merge_rank<<<grid_for(m.ma), 256, 0, s>>>(m);
-    cudaError_t e = scan_u32(m.dup, m.ma, m.ds, m.blk, s);
-    if (e != cudaSuccess) return e;
-    k_merge_union<<<1, 1024, 0, s>>>(m);
-    return cudaGetLastError();
+cudaError_t launch_merge_count(const MergeArgs &m, cudaStream_t s) {
+    if (m.ntiles) {
+        const uint32_t g = (uint32_t)(m.ntiles < 148ull * 8 ? m.ntiles : 148ull * 8);
+        if (m.width == 2) k_merge_path<2, false><<<g, 256, 0, s>>>(m);
+        else k_merge_path<4, false><<<g, 256, 0, s>>>(m);
+    }
+    return scan_u32(m.tile_cnt, m.ntiles, m.tile_off, m.blk, s);
 }
 
 cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s) {
-    const unsigned long long mx = m.ma > m.mb ? m.ma : m.mb;
-    if (mx) {
-        if (m.width == 2) k_merge_place<2><<<grid_for(mx), 256, 0, s>>>(m);
-        else k_merge_place<4><<<grid_for(mx), 256, 0, s>>>(m);
+    if (m.ntiles) {
+        const uint32_t g = (uint32_t)(m.ntiles < 148ull * 8 ? m.ntiles : 148ull * 8);
+        if (m.width == 2) k_merge_path<2, true><<<g, 256, 0, s>>>(m);
+        else k_merge_path<4, true><<<g, 256, 0, s>>>(m);
     }
+    cudaError_t e = cudaMemsetAsync(m.eu, 0xFF, (size_t)(m.n + 1) * 8, s);
+    if (e != cudaSuccess) return e;
+    if (m.mu) k_merge_bounds<<<grid_for(m.mu), 256, 0, s>>>(m);
+    k_merge_bounds_fill<<<1, 32, 0, s>>>(m);
     if (m.mu) k_merge_len<<<grid_for(m.mu), 256, 0, s>>>(m);
-    cudaError_t e = scan_u32(m.len, m.mu, m.lo, m.blk, s);
+    e = scan_u32(m.len, m.mu, m.lo, m.blk, s);
     if (e != cudaSuccess) return e;
     k_merge_table<<<1, 1024, 0, s>>>(m);
     return cudaGetLastError();

@@ -182,24 +182,28 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev);  
 // entry_base[record] + ordinal (delta_merge's decode of a body; targets carry no w).
 cudaError_t launch_decode_only(const ApplyArgs &a, unsigned long long *idx_out, void *val_out,
                                const unsigned long long *entry_base, cudaStream_t s);
-// delta_merge (merge.cu): see api.cu
+// delta_merge (merge.cu): see api.cu.  Entries are keyed (record << kKeyShift) | index, so
+// element counts must stay below 2^40 (checked by the walk).
+constexpr int kKeyShift = 40;
+constexpr uint32_t kMergeTooLarge = 11;  // walk status: an element count >= 2^40
 struct MergeArgs {
     const uint8_t *a, *b;                 // the two bodies
     unsigned long long a_bytes, b_bytes;
     uint32_t n;                           // records expected in each
     int width;
     TargetDesc *targets;                  // n: B's names / element counts, for A1 of both decodes
+    RecordRow *ha, *hb;                   // n: table rows of a and b (the decodes' hints)
     uint32_t *name_len;                   // n
     unsigned long long *name_off;         // n (into body b)
     unsigned long long *numel;            // n
     unsigned long long *ea, *eb, *eu;     // n + 1 entry prefixes of a, b and the union
     uint32_t *status;                     // walk status (kOk / k* code)
-    unsigned long long *ia, *ib;          // decoded absolute indices
+    unsigned long long *ia, *ib;          // decoded keys (record << kKeyShift | index), ascending
     void *va, *vb;                        // decoded values
-    unsigned long long *lb;               // ma: lower bound of each a entry in its b segment
-    uint32_t *dup;                        // ma + 1 (scan input), then the exclusive scan in ds
-    unsigned long long *ds;               // ma + 1
-    unsigned long long *u;                // mu merged indices
+    uint32_t *tile_cnt;                   // merge-path tiles: kept entries per tile (scan input)
+    unsigned long long *tile_off;         // tiles + 1: exclusive scan of tile_cnt
+    unsigned long long ntiles;
+    unsigned long long *u;                // mu merged keys
     void *uv;                             // mu merged values
     uint32_t *len;                        // mu LEB128 lengths
     unsigned long long *lo;               // mu + 1 byte offsets (exclusive scan of len)
@@ -209,8 +213,8 @@ struct MergeArgs {
     unsigned long long ma, mb, mu;
 };
 cudaError_t launch_merge_walk(const MergeArgs &m, cudaStream_t s);
-cudaError_t launch_merge_rank(const MergeArgs &m, cudaStream_t s);     // lb, dup, ds, eu
-cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s);    // u, uv, len, lo, table, body_size
+cudaError_t launch_merge_count(const MergeArgs &m, cudaStream_t s);    // tile_cnt, tile_off
+cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s);    // u, uv, eu, len, lo, table, body_size
 cudaError_t launch_merge_emit(const MergeArgs &m, uint8_t *out, cudaStream_t s);
 
 }  // namespace sd

@@ -101,28 +101,34 @@ class NvlinkAssembler:
     orders them before anything the root does next.  Rank 0's own body is extracted
     directly into ``buf`` (offset 0)."""
 
-    def __init__(self, ctx, capacity: int, device, group=None, root: int = 0):
+    def __init__(self, ctx, capacity: int, device, group=None, root: int = 0, nbuf: int = 1):
         assert root == 0, "the assembled body starts with rank 0's records"
         self.ctx, self.group, self.root = ctx, group, root
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.device = torch.device(device)
-        self.buf = torch.empty(capacity, dtype=torch.uint8, device=self.device) if self.rank == root else None
+        # nbuf assembled-body buffers on the root (2: step t's assembly overlaps step t+1)
+        self.bufs = ([torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
+                     if self.rank == root else [None] * nbuf)
+        self.buf = self.bufs[0]
         handles = [None] * self.world
-        dist.all_gather_object(handles, reduce_tensor(self.buf) if self.rank == root else None, group=group)
+        dist.all_gather_object(handles, [reduce_tensor(b) for b in self.bufs] if self.rank == root else None,
+                               group=group)
+        self.peers = []
         if self.rank != root:
-            fn, args = handles[root]
-            args = list(args)
-            args[6] = self.device.index  # rebuild on this process's device (peer mapping)
-            self.peer = fn(*args)
+            for fn, args in handles[root]:
+                args = list(args)
+                args[6] = self.device.index  # rebuild on this process's device (peer mapping)
+                self.peers.append(fn(*args))
+        self.peer = self.peers[0] if self.peers else None
         self.sizes = torch.zeros(self.world, dtype=torch.int64, device=self.device)
         self.size1 = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.token = torch.zeros(1, dtype=torch.float32, device=self.device)
 
-    def assemble(self, body: torch.Tensor, size, stream=None):
-        """Enqueue: sizes all-gather, this rank's NVLink copy into the root, completion
-        all-reduce.  ``size``: the body size as an int, or a one-element int64 CUDA tensor
-        (delta_extract_async's device-resident size: no host value needed).  Returns the
-        assembled buffer on the root, None elsewhere."""
+    def assemble(self, body: torch.Tensor, size, stream=None, slot: int = 0):
+        """Enqueue: sizes all-gather, this rank's NVLink copy into the root's buffer
+        ``slot``, completion all-reduce.  ``size``: the body size as an int, or a one-element
+        int64 CUDA tensor (delta_extract_async's device-resident size: no host value needed).
+        Returns the assembled buffer on the root, None elsewhere."""
         stream = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(stream):
             if isinstance(size, torch.Tensor):
@@ -131,12 +137,13 @@ class NvlinkAssembler:
                 self.size1.fill_(size)
             dist.all_gather_into_tensor(self.sizes, self.size1, group=self.group)
             if self.rank != self.root:
-                self.ctx.assemble(body, self.peer, self.sizes, self.rank, stream=stream)
+                self.ctx.assemble(body, self.peers[slot], self.sizes, self.rank, stream=stream)
             dist.all_reduce(self.token, group=self.group)
-        return self.buf if self.rank == self.root else None
+        return self.bufs[slot] if self.rank == self.root else None
 
     def close(self):
         """Release the IPC mapping (non-root ranks) before the root frees or exits."""
         torch.cuda.synchronize(self.device)
         self.peer = None
+        self.peers = []
         dist.barrier(group=self.group)
