@@ -493,10 +493,17 @@ def main():
     if not ok:
         raise SystemExit("bench: round trip mismatch")
     ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    rank_view = None
+    if world > 1:  # max over ranks; every rank's time and K1 / scatter time for the record
+        k1_local = acc.get("scan_ms", 0.0) / args.steps
+        sc_local = acc.get("scatter_ms", 0.0) / args.steps
+        t = torch.tensor([ms, k1_local, sc_local], dtype=torch.float64, device=dev)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        rank_view = {"ms_per_step": [round(float(x[0]) / args.steps, 4) for x in allt],
+                     "k1_ms": [round(float(x[1]), 4) for x in allt],
+                     "scatter_ms": [round(float(x[2]), 4) for x in allt]}
+        ms = max(float(x[0]) for x in allt)
     ms_step = ms / args.steps
     value = scanned_total * args.steps / (ms / 1e3) / 1e9
 
@@ -576,6 +583,8 @@ def main():
     }
     if k1_ms > 0:
         result["roofline"]["k1_share_of_step"] = round(k1_ms / ms_step, 4)
+    if rank_view is not None:
+        result["per_rank"] = rank_view
     result["config"]["host_sync"] = "end (steps enqueued back to back)" if pipelined else "every step"
     if pipelined:  # the same steps with the host waiting for each one (latency view)
         ks = max(3, args.steps // 2)

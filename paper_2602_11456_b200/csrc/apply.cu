@@ -116,16 +116,38 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
         }
     }
     ok = __syncthreads_and(ok) && (n > 0 || body_bytes == 0);
-    if (!ok && threadIdx.x == 0) {  // authoritative sequential walk
-        unsigned long long pos = 0;
-        uint32_t code = kOk;
-        for (uint32_t k = 0; k < n && code == kOk; ++k) {
-            unsigned long long end = 0;
-            code = check_record(body, body_bytes, pos, tg[k], names, width, fixed, recs[k], end);
-            pos = end;
+    if (!ok) {  // authoritative walk: thread 0 follows the chain of record offsets (two
+                // dependent header loads per record), then every record is checked in parallel
+        if (threadIdx.x == 0) {
+            unsigned long long pos = 0;
+            uint32_t code = kOk;
+            for (uint32_t k = 0; k < n; ++k) {
+                if (pos > body_bytes || body_bytes - pos < 2) { code = kLayout; break; }
+                const unsigned long long nl = rd_le(body + pos, 2);
+                if (body_bytes - pos - 2 < nl + 24) { code = kLayout; break; }
+                const unsigned long long q = pos + 2 + nl;
+                const unsigned long long nnz = rd_le(body + q + 8, 8), il = rd_le(body + q + 16, 8);
+                const unsigned long long rem = body_bytes - q - 24;
+                if (il > rem || nnz > (rem - il) / (unsigned long long)width || rem - il - nnz * width < 1) {
+                    code = kLayout;
+                    break;
+                }
+                recs[k].idx_off = pos;  // the record's offset, re-checked in full below
+                pos = q + 24 + il + nnz * width + 1;
+            }
+            if (code == kOk && pos != body_bytes) code = kLayout;
+            if (code != kOk) set_status(st, code);
         }
-        if (code == kOk && pos != body_bytes) code = kLayout;
-        if (code != kOk) set_status(st, code);
+        __syncthreads();
+        if (st->status == kOk) {
+            for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+                ApplyRec r;
+                unsigned long long end = 0;
+                const uint32_t c = check_record(body, body_bytes, recs[k].idx_off, tg[k], names, width, fixed, r, end);
+                if (c != kOk) set_status(st, c);
+                else recs[k] = r;
+            }
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
