@@ -244,6 +244,26 @@ def _oracle_task(i):
     return bool(np.array_equal(_ORACLE_SAMPLE._one(item), item[2]))
 
 
+def ops_view(k, lanes, width, nnz, idx_bytes, body, peak, value, scanned_total, total_lanes, nnz_total,
+             idx_total):
+    """Extract / apply split of this rank's kernel time with their algorithmic bytes
+    (extract: 2 w N read + body written; apply: body read + nnz w stored) and the round trip
+    against the measured copy peak."""
+    ex = sum(k.get(x, 0.0) for x in ("scan_ms", "lens_ms", "finalize_ms", "emit_ms", "headers_ms"))
+    ap = sum(k.get(x, 0.0) for x in ("locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"))
+    ex_b = 2 * lanes * width + body
+    ap_b = body + nnz * width
+    rt_per_lane = (2 * width * total_lanes + 2 * idx_total + 3 * width * nnz_total) / total_lanes
+    return {"extract": {"ms": round(ex, 4), "algorithmic_bytes": ex_b,
+                        "GBps": round(ex_b / ex / 1e6, 1) if ex else None},
+            "apply": {"ms": round(ap, 4), "algorithmic_bytes": ap_b,
+                      "GBps": round(ap_b / ap / 1e6, 1) if ap else None},
+            "round_trip": {"algorithmic_bytes_per_lane": round(rt_per_lane, 4),
+                           "algorithmic_GBps": round(value * rt_per_lane / (2 * width), 1),
+                           "frac_of_measured_peak": round(value * rt_per_lane / (2 * width) / peak, 4),
+                           "scanned_frac_of_measured_peak": round(value / peak, 4)}}
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -565,6 +585,11 @@ def main():
                     "varint_saving_vs_naive": round(naive_total / body_total, 3),
                     "paper_context": PAPER_CPU},
         "kernel_ms_per_step": kernel_ms,
+        # per-op time (this rank's kernels) and algorithmic bytes, and the round
+        # trip's algorithmic bytes per lane 2w + rho (3w + 2E) against the measured peak
+        "ops": ops_view(kernel_ms, local_lanes, width, nnz_local, idx_local, body_local,
+                        peaks.get("hbm_gbs", 6650.0), value, scanned_total, total_lanes, nnz_total,
+                        idx_total),
         "roofline": {"kernel": "k_scan_tiles (K1)", "bound": "hbm",
                      "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",

@@ -72,7 +72,7 @@ enum {
     DELTA_D_COUNT = 6,         /* number of varints != nnz */
     DELTA_D_NAME = 7,          /* record name != target name */
     DELTA_D_NUMEL = 8,         /* record element_count != target numel */
-    DELTA_D_MODE = 9,          /* mode byte != 0 (replace) */
+    DELTA_D_MODE = 9,          /* mode byte not 0 (replace) or 1 (additive); delta_merge: not 0 */
     DELTA_D_LAYOUT = 10        /* record past the body end, trailing bytes, record count != n */
 };
 

@@ -2,6 +2,8 @@
 // table) cache, descriptor validation, kernel launches, size readback and error reporting.
 // Host code compiled by nvcc into libsparsedelta.so (static cudart).  Product code.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstddef>
@@ -949,6 +951,25 @@ extern "C" int delta_digest(delta_ctx *ctx, const void *body, uint64_t bytes, ui
 }
 
 // --------------------------------------------------------------------------- merge
+// DELTA_MERGE_TIMING=1: host wall time of each delta_merge phase (each ends in a stream
+// synchronisation) printed to stderr — diagnostics for scripts/merge_bench.py.
+struct MergeTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    explicit MergeTimer(cudaStream_t s) : on(getenv("DELTA_MERGE_TIMING") != nullptr) {
+        if (on) {
+            cudaStreamSynchronize(s);
+            t = std::chrono::steady_clock::now();
+        }
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "delta_merge %-42s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 // delta_merge (NEXT f4, reading R19): validate both bodies (layout, pairwise names and
 // element counts, replace mode, full LEB128 decode with the apply's checks), decode them to
 // (record, index) keys + values, merge the two key arrays by merge path, re-encode.  Four
@@ -999,6 +1020,7 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     m.status = ctx->m_status.as<uint32_t>();
     m.table = ctx->m_table.as<RecordRow>();
     m.body_size = ctx->m_size.as<unsigned long long>();
+    MergeTimer mt(s);
     CK(launch_merge_walk(m, s), "merge walk");
     unsigned long long h[3];
     uint32_t st = 0;
@@ -1006,6 +1028,7 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     CK(cudaMemcpyAsync(&h[0], m.ea + n, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaMemcpyAsync(&h[1], m.eb + n, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaStreamSynchronize(s), "merge walk");
+    mt.mark("walk+check");
     if (st == kMergeTooLarge)
         return fail(ctx, DELTA_EINVAL, 0, "delta_merge: element_count >= 2^40 is not supported");
     if (st != kOk)
@@ -1062,6 +1085,7 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
         CK(cudaMemcpyAsync(&dst[x], ctx->a_state.p, 4, cudaMemcpyDeviceToHost, s), "readback");
     }
     CK(cudaStreamSynchronize(s), "merge decode");
+    mt.mark("decode a+b");
     for (int x = 0; x < 2; ++x)
         if (dst[x] != kOk)
             return fail(ctx, dst[x] <= 10 ? kDetailToStatus[dst[x]] : DELTA_ECORRUPT, (int)dst[x],
@@ -1076,6 +1100,7 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     CK(launch_merge_count(m, s), "merge count");
     CK(cudaMemcpyAsync(&h[2], m.tile_off + m.ntiles, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaStreamSynchronize(s), "merge count");
+    mt.mark("merge-path count");
     m.mu = h[2];
     GROW(ctx->m_u, std::max<size_t>(m.mu, 1) * 8);
     GROW(ctx->m_uv, std::max<size_t>(m.mu, 1) * w);
@@ -1089,11 +1114,16 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     unsigned long long size = 0;
     CK(cudaMemcpyAsync(&size, m.body_size, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaStreamSynchronize(s), "merge place");
+    mt.mark("merge-path write + bounds/len/scan/table");
     *out_bytes = size;
     if (size > out_capacity)
         return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < merged body size %llu",
                     (unsigned long long)out_capacity, size);
     CK(launch_merge_emit(m, static_cast<uint8_t *>(out), s), "merge emit");
+    if (mt.on) {
+        CK(cudaStreamSynchronize(s), "merge emit");
+        mt.mark("emit + headers");
+    }
     return DELTA_OK;
 }
 

@@ -790,6 +790,38 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
         }
         const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
         uint8_t *p = ib + L0;
+        const uint32_t c = e.count;
+        if (c <= 256) {  // ~all tiles up to a few % density: every load of the tile issued up front
+            uint32_t o[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t i = r * 32 + lane;
+                o[r] = i < c ? (uint32_t)so[i] : 0u;
+            }
+            warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if ((uint32_t)r * 32u >= c) break;
+                const uint32_t i = r * 32 + lane;
+                uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
+                const uint32_t carry = __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31);
+                if (lane == 0) prev = carry;
+                const bool act = i >= 1 && i < c;
+                const uint32_t gi = act ? o[r] - prev : 0u;
+                const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
+                if (act) {
+                    uint8_t *q = p + (lane - (r == 0 ? 1 : 0)) + __popc(two & lt_mask);
+                    if (gi < 128u) {
+                        q[0] = (uint8_t)gi;
+                    } else {
+                        q[0] = (uint8_t)(gi | 0x80u);
+                        q[1] = (uint8_t)(gi >> 7);
+                    }
+                }
+                p += min(32u, c - r * 32u) - (r == 0 ? 1u : 0u) + __popc(two);
+            }
+            continue;
+        }
         for (uint32_t i0 = 1; i0 < e.count; i0 += 32) {
             const uint32_t i = i0 + lane;
             const bool act = i < e.count;

@@ -743,41 +743,48 @@ def test_extract_and_advance(sd):
 
 
 # ------------------------------------------------------------------ delta merge (NEXT f4)
-def _three_versions(n, seed, rho1, rho2, overlap):
+def _three_versions(n, seed, rho1, rho2, overlap, dt=np.uint16):
     """v0 -> v1 (rho1 uniform), v1 -> v2 (rho2 uniform, plus a share `overlap` of v1's
-    changed lanes changed again); bf16 lanes as numpy uint16."""
+    changed lanes changed again); lanes as numpy uint16 (bf16) or uint32 (fp32)."""
     rng = np.random.default_rng(seed)
-    v0 = rng.integers(0, 2**16, n, dtype=np.uint64).astype(np.uint16)
+    v0 = rng.integers(0, 2**(8 * np.dtype(dt).itemsize), n, dtype=np.uint64).astype(dt)
     m1 = rng.random(n) < rho1
     v1 = v0.copy()
-    v1[m1] ^= rng.integers(1, 16, int(m1.sum()), dtype=np.uint64).astype(np.uint16)
+    v1[m1] ^= rng.integers(1, 16, int(m1.sum()), dtype=np.uint64).astype(dt)
     m2 = rng.random(n) < rho2
     again = np.flatnonzero(m1)
     m2[again[rng.random(again.size) < overlap]] = True
     v2 = v1.copy()
-    v2[m2] ^= rng.integers(1, 16, int(m2.sum()), dtype=np.uint64).astype(np.uint16)
+    v2[m2] ^= rng.integers(1, 16, int(m2.sum()), dtype=np.uint64).astype(dt)
     return v0, v1, v2
 
 
 def _dev(a):
+    if a.dtype == np.uint32:
+        return torch.from_numpy(a.view(np.int32).copy()).to(DEV).view(torch.float32)
     return torch.from_numpy(a.view(np.int16).copy()).to(DEV).view(torch.bfloat16)
 
 
-def test_merge_parity(sd):
+@pytest.mark.parametrize("dt", [np.uint16, np.uint32])
+def test_merge_parity(sd, dt):
     """delta_merge on the GPU == oracle.codec.merge byte for byte, and applying the merge
-    to v0 gives v2 (M1-sized multi-chunk record, dense, overlapping, empty, 1-lane)."""
+    to v0 gives v2 (M1-sized multi-chunk record, dense, overlapping, empty, 1-lane;
+    16- and 32-bit lanes)."""
     cases = [(16_777_216, 0.01, 0.01, 0.3), (300_001, 0.4, 0.2, 0.5), (5000, 0.0, 0.05, 0.0),
              (5000, 0.05, 0.0, 0.0), (0, 0.0, 0.0, 0.0), (1, 1.0, 1.0, 1.0), (100_003, 0.001, 0.001, 1.0)]
+    if dt == np.uint32:
+        cases[0] = (4_000_037, 0.01, 0.01, 0.3)
+    width = np.dtype(dt).itemsize
     names = [f"m{k}.weight" for k in range(len(cases))]
-    vs = [_three_versions(n, 70 + k, r1, r2, ov) for k, (n, r1, r2, ov) in enumerate(cases)]
+    vs = [_three_versions(n, 70 + k, r1, r2, ov, dt) for k, (n, r1, r2, ov) in enumerate(cases)]
     ctx = sd.DeltaContext(DEV)
     a, _ = ctx.delta_extract([(nm, _dev(v[0]), _dev(v[1])) for nm, v in zip(names, vs)])
     a = a.clone()
     b, _ = ctx.delta_extract([(nm, _dev(v[1]), _dev(v[2])) for nm, v in zip(names, vs)])
     b = b.clone()
-    merged = ctx.delta_merge(a, b, len(names))
+    merged = ctx.delta_merge(a, b, len(names), width=width)
     torch.cuda.synchronize()
-    want = oracle.codec.merge(a.cpu().numpy().tobytes(), b.cpu().numpy().tobytes(), 2)
+    want = oracle.codec.merge(a.cpu().numpy().tobytes(), b.cpu().numpy().tobytes(), width)
     assert_body_equal(merged, want)
     targets = [(nm, _dev(v[0])) for nm, v in zip(names, vs)]
     ctx.delta_apply(targets, merged)
