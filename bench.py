@@ -632,7 +632,12 @@ def main():
 
     # ---- e2e: the same step with inputs copied from pinned host memory every step
     if not args.no_e2e:
-        result["e2e"] = e2e(args, step, olds, news, body_local, dev, scanned_total, world)
+        # e2e: the shadow-resident trainer step (H2D of the new weights only), and beside it
+        # every input from the host (H2D of old and new)
+        result["e2e_full_inputs"] = e2e(args, step, olds, news, body_local, dev, scanned_total, world)
+        torch.cuda.synchronize()
+        result["e2e"] = e2e_shadow(args, sd, [specs[k].name for k in mine], mine, specs, olds, news, targets,
+                                   dev, scanned_total, world, rho, pattern, dtype)
     # ---- CPU oracle beside it (rank 0, N=1 only)
     if not args.no_cpu_baseline and world == 1:
         smp = OracleSample(specs, rho, pattern, args.seed, dtype, args.cpu_seconds, args.index_codec)
@@ -694,6 +699,77 @@ def e2e(args, step, olds, news, body_cap, dev, scanned_total, world):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
             "ms_per_step": round(ms / args.e2e_steps, 3),
             "note": "bytes per rank; old+new H2D from pinned host, body D2H, apply on device"}
+
+
+def e2e_shadow(args, sd, names, ks, specs, olds, news, targets, dev, scanned_total, world, rho, pattern, dtype):
+    """The trainer's view of e2e: W_t stays resident on the device as the extract-and-advance
+    shadow (DELTA_OPT_ADVANCE: the compare leaves old == new), so each step's input from the
+    host is only the new weights.  Every step: H2D of W_{t+1} from pinned host memory, extract
+    (advancing the shadow), apply to the actor copy, D2H of the body; versions alternate
+    V1, V2, V1, ... where V2 = V1 XOR the change pattern of a second seeded pair, so each
+    step changes the configured share of lanes.  Public API only; CUDA events around the
+    whole step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from workload import generate_pair
+    stream = torch.cuda.current_stream()
+    lt = torch.int16 if news[0].element_size() == 2 else torch.int32
+    h_v = [[], []]
+    for k, w in zip(ks, news):
+        o2, w2 = generate_pair(specs[k], k, args.seed + 1, rho=rho, pattern=pattern, dtype=dtype, device=dev)
+        x = o2.view(lt) ^ w2.view(lt)
+        del o2, w2
+        h_v[0].append(w.cpu().pin_memory())
+        h_v[1].append((w.view(lt) ^ x).view(w.dtype).cpu().pin_memory())
+        del x
+    ctx = sd.DeltaContext(dev)
+    ctx.set_option(9, 2)  # DELTA_OPT_ADVANCE
+    tl = sd.TensorList([(n, o, w) for n, o, w in zip(names, olds, news)])
+    tg = sd.TargetList([(n, t) for n, t in zip(names, targets)])
+    for o, t in zip(olds, targets):  # shadow and actor copy start at the same version
+        t.copy_(o)
+    cap = ctx.delta_size(tl)  # compaction cached for the first extract below
+    out = torch.empty(4 * cap + 4096, dtype=torch.uint8, device=dev)
+    h_body = torch.empty(out.numel(), dtype=torch.uint8).pin_memory()
+    d2h = [0]
+    state = {"v": 0}
+
+    def one():
+        hv = h_v[state["v"] % 2]
+        state["v"] += 1
+        for w, hw in zip(news, hv):
+            w.copy_(hw, non_blocking=True)
+        body, table = ctx.delta_extract(tl, out=out, table="device")
+        ctx.delta_apply(tg, body, table=table)
+        h_body[:body.numel()].copy_(body, non_blocking=True)
+        d2h[0] = body.numel()
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.e2e_steps):
+        one()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    ok = all(torch.equal(t.view(lt), w.view(lt)) and torch.equal(o.view(lt), w.view(lt))
+             for t, o, w in zip(targets, olds, news))
+    if not ok:
+        raise SystemExit("bench: e2e (shadow) round trip mismatch")
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ctx.close()
+    h2d = sum(w.numel() * w.element_size() for w in news)
+    return {"value": round(scanned_total * args.e2e_steps / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0], "steps": args.e2e_steps,
+            "ms_per_step": round(ms / args.e2e_steps, 3),
+            "note": ("bytes per rank; W_{t+1} H2D from pinned host (W_t resident as the extract-and-advance "
+                     "shadow), body D2H, apply on device; the compare still scans old+new")}
 
 
 if __name__ == "__main__":

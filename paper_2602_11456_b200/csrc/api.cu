@@ -1094,6 +1094,8 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     GROW(ctx->m_dup, std::max<size_t>(m.ntiles, 1) * 4);
     GROW(ctx->m_ds, (m.ntiles + 1) * 8);
     GROW(ctx->m_blk, ((std::max<size_t>(m.ntiles, m.ma + m.mb) + 4095) / 4096 + 1) * 8);
+    GROW(ctx->m_lb, (m.ntiles + 1) * 8);
+    m.split = ctx->m_lb.as<unsigned long long>();
     m.tile_cnt = ctx->m_dup.as<uint32_t>();
     m.tile_off = ctx->m_ds.as<unsigned long long>();
     m.blk = ctx->m_blk.as<unsigned long long>();

@@ -618,7 +618,8 @@ template <int W>
 __global__ void __launch_bounds__(256)
 k_decode_write(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs,
                const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
-               const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ ord_base,
+               const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
+               const unsigned long long *__restrict__ ord_base,
                const unsigned long long *__restrict__ idx_base, const unsigned long long *__restrict__ entry_base,
                unsigned long long *__restrict__ idx_out, typename std::conditional<W == 2, uint16_t, uint32_t>::type *val_out,
                ApplyState *st) {
@@ -629,6 +630,7 @@ k_decode_write(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
     __shared__ __align__(16) uint8_t svb[kByteChunk * W + 32];
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
+    __shared__ uint32_t s_rel[kByteChunk];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = __ldg(chunk_rec + c);
@@ -658,17 +660,33 @@ k_decode_write(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
             spre += s_sum[w];
         }
         uint32_t o = cpre + ci - cnt;
-        unsigned long long idx = idx_base[c] + spre + si - sum;
+        const unsigned long long base = idx_base[c];
+        unsigned long long idx = base + spre + si - sum;
         const unsigned long long e0 = entry_base[k] + ob;
         const unsigned long long key = (unsigned long long)k << kKeyShift;  // (record, index) keys
-        decode_thread(v, [&](unsigned long long x) {
-            idx += x;
-            idx_out[e0 + o] = key | idx;
-            if constexpr (W == 2) val_out[e0 + o] = (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
-            else val_out[e0 + o] = (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) |
-                                   ((LT)vals[4 * o + 3] << 24);
-            ++o;
-        });
+        auto value = [&](uint32_t x) -> LT {
+            if constexpr (W == 2) return (LT)(vals[2 * x] | (vals[2 * x + 1] << 8));
+            else return (LT)vals[4 * x] | ((LT)vals[4 * x + 1] << 8) | ((LT)vals[4 * x + 2] << 16) |
+                        ((LT)vals[4 * x + 3] << 24);
+        };
+        if (chunk_sum[c] < 0xFFFFFFFFull) {  // indices relative to the chunk fit u32: stage, then
+            decode_thread(v, [&](unsigned long long x) {  // write entry i from thread i % 256
+                idx += x;
+                s_rel[o++] = (uint32_t)(idx - base);
+            });
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) {
+                idx_out[e0 + i] = key | (base + s_rel[i]);
+                val_out[e0 + i] = value(i);
+            }
+        } else {
+            decode_thread(v, [&](unsigned long long x) {
+                idx += x;
+                idx_out[e0 + o] = key | idx;
+                val_out[e0 + o] = value(o);
+                ++o;
+            });
+        }
         __syncthreads();
     }
 }
@@ -816,11 +834,11 @@ cudaError_t launch_decode_only(const ApplyArgs &a, unsigned long long *idx_out, 
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (a.width == 2)
         k_decode_write<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.chunk_count,
-                                                         a.chunk_ord_base, a.chunk_idx_base, entry_base, idx_out,
+                                                         a.chunk_sum, a.chunk_ord_base, a.chunk_idx_base, entry_base, idx_out,
                                                          static_cast<uint16_t *>(val_out), a.state);
     else
         k_decode_write<4><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.chunk_count,
-                                                         a.chunk_ord_base, a.chunk_idx_base, entry_base, idx_out,
+                                                         a.chunk_sum, a.chunk_ord_base, a.chunk_idx_base, entry_base, idx_out,
                                                          static_cast<uint32_t *>(val_out), a.state);
     return cudaGetLastError();
 }

@@ -11,12 +11,13 @@
 //   (decode)            each body through A1-A3 + k_decode_write (apply.cu): validated,
 //                       absolute indices + values per entry.
 //   M2 k_merge_path     merge path over the two key arrays (keys = record << 40 | index
-//                       ascend over a whole body): 2048 merged positions per tile, split
-//                       by one binary search per tile boundary, staged in shared memory,
-//                       8 positions per thread (a second binary search in shared memory);
-//                       an a-entry is dropped when the b head equals it (b's value wins).
-//                       Pass 1 counts the kept entries per tile, pass 2 writes them at the
-//                       scanned offsets.
+//                       ascend over a whole body): 2048 merged positions per tile, tile
+//                       splits by one binary search per boundary (k_merge_splits, all in
+//                       parallel), tiles staged in shared memory, 8 positions per thread (a
+//                       second binary search in shared memory); an a-entry is dropped when
+//                       the b head equals it (b's value wins).  Pass 1 counts the kept
+//                       entries per tile, pass 2 stages them and writes them coalesced at
+//                       the scanned offsets.
 //   M3 k_merge_bounds   record boundaries of the union; LEB128 length of every gap, their
 //                       exclusive scan, the offset table and the body size.
 //   M4 k_merge_emit     LEB128 bytes + values per entry; k_merge_headers per record.
@@ -225,28 +226,29 @@ __device__ __forceinline__ unsigned long long mp_split(const T *A, unsigned long
     return lo;
 }
 
+// split[t] = A elements among the first t * kMpTile merged positions (t = 0 .. ntiles)
+__global__ void __launch_bounds__(256) k_merge_splits(MergeArgs m) {
+    const unsigned long long total = m.ma + m.mb;
+    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t <= m.ntiles;
+         t += (unsigned long long)gridDim.x * blockDim.x)
+        m.split[t] = mp_split(m.ia, m.ma, m.ib, m.mb, min(t * kMpTile, total));
+}
+
+// One tile of 2048 merged positions per iteration: the tile's a and b runs staged in
+// shared memory, 8 positions per thread (split by a binary search in shared memory),
+// pass 1 counts the kept entries, pass 2 stages them in shared memory (keys, and the source
+// position of each value) and writes them out coalesced.
 template <int W, bool WRITE>
 __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
     using LT = typename Lane<W>::T;
     __shared__ unsigned long long sa[kMpTile + 1], sb[kMpTile + 1];
-    __shared__ unsigned long long s_cut[4];
+    __shared__ uint32_t s_src[WRITE ? kMpTile : 1];  // kept entry -> source (bit 31: from b)
     __shared__ uint32_t s_w[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned long long total = m.ma + m.mb;
     for (unsigned long long t = blockIdx.x; t < m.ntiles; t += gridDim.x) {
-        const unsigned long long d0 = t * kMpTile, d1 = min(d0 + kMpTile, total);
-        if (tid == 0) {
-            const unsigned long long i = mp_split(m.ia, m.ma, m.ib, m.mb, d0);
-            s_cut[0] = i;
-            s_cut[1] = d0 - i;
-        } else if (tid == 32) {
-            const unsigned long long i = mp_split(m.ia, m.ma, m.ib, m.mb, d1);
-            s_cut[2] = i;
-            s_cut[3] = d1 - i;
-        }
-        __syncthreads();
-        const unsigned long long i0 = s_cut[0], j0 = s_cut[1];
-        const uint32_t na = (uint32_t)(s_cut[2] - i0), nb = (uint32_t)(s_cut[3] - j0);
+        const unsigned long long d0 = t * kMpTile, d1 = min(d0 + kMpTile, m.ma + m.mb);
+        const unsigned long long i0 = m.split[t], j0 = d0 - i0;
+        const uint32_t na = (uint32_t)(m.split[t + 1] - i0), nb = (uint32_t)(d1 - m.split[t + 1] - j0);
         for (uint32_t x = tid; x < na; x += blockDim.x) sa[x] = m.ia[i0 + x];
         for (uint32_t x = tid; x < nb; x += blockDim.x) sb[x] = m.ib[j0 + x];
         if (tid == 0) {  // the heads just past the tile (a b head there can equal our last a)
@@ -269,7 +271,6 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
                 }
             }
         }
-        // block scan of the kept counts
         uint32_t inc = keep;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -286,24 +287,26 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
         if constexpr (!WRITE) {
             if (tid == 0) m.tile_cnt[t] = tot;
         } else {
-            const LT *va = static_cast<const LT *>(m.va), *vb = static_cast<const LT *>(m.vb);
-            LT *uv = static_cast<LT *>(m.uv);
-            unsigned long long p = m.tile_off[t] + pre + inc - keep;
+            uint32_t q = pre + inc - keep;
             uint32_t i = i_start, j = e0 - i_start;
             for (uint32_t e = e0; e < e1; ++e) {
                 if (j >= nb || (i < na && sa[i] <= sb[j])) {
-                    if (sa[i] != sb[j]) {
-                        m.u[p] = sa[i];
-                        uv[p] = va[i0 + i];
-                        ++p;
-                    }
+                    if (sa[i] != sb[j]) s_src[q++] = i;
                     ++i;
                 } else {
-                    m.u[p] = sb[j];
-                    uv[p] = vb[j0 + j];
-                    ++p;
+                    s_src[q++] = 0x80000000u | j;
                     ++j;
                 }
+            }
+            __syncthreads();
+            const LT *va = static_cast<const LT *>(m.va), *vb = static_cast<const LT *>(m.vb);
+            LT *uv = static_cast<LT *>(m.uv);
+            const unsigned long long base = m.tile_off[t];
+            for (uint32_t x = tid; x < tot; x += blockDim.x) {
+                const uint32_t src = s_src[x], k = src & 0x7FFFFFFFu;
+                const bool fb = src >> 31;
+                m.u[base + x] = fb ? sb[k] : sa[k];
+                uv[base + x] = fb ? vb[j0 + k] : va[i0 + k];
             }
         }
         __syncthreads();  // shared staging reused by the next tile
@@ -425,6 +428,7 @@ cudaError_t launch_merge_walk(const MergeArgs &m, cudaStream_t s) {
 }
 
 cudaError_t launch_merge_count(const MergeArgs &m, cudaStream_t s) {
+    k_merge_splits<<<(uint32_t)((m.ntiles + 1 + 255) / 256), 256, 0, s>>>(m);
     if (m.ntiles) {
         const uint32_t g = (uint32_t)(m.ntiles < 148ull * 8 ? m.ntiles : 148ull * 8);
         if (m.width == 2) k_merge_path<2, false><<<g, 256, 0, s>>>(m);

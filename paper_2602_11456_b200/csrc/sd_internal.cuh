@@ -203,6 +203,7 @@ struct MergeArgs {
     uint32_t *tile_cnt;                   // merge-path tiles: kept entries per tile (scan input)
     unsigned long long *tile_off;         // tiles + 1: exclusive scan of tile_cnt
     unsigned long long ntiles;
+    unsigned long long *split;            // ntiles + 1: a-entries before each tile boundary
     unsigned long long *u;                // mu merged keys
     void *uv;                             // mu merged values
     uint32_t *len;                        // mu LEB128 lengths
