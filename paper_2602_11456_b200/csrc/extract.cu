@@ -434,7 +434,25 @@ k_tiles_gaps(TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t slot_cap,
         if (c == 0) continue;
         const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
         uint32_t big = 0;
-        for (uint32_t i = 1 + lane; i < c; i += 32) big += (uint32_t)(so[i] - so[i - 1]) >= 128u;
+        if (c <= 256) {  // every offset of the tile loaded up front, predecessors by shuffle
+            uint32_t o[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t i = r * 32 + lane;
+                o[r] = i < c ? (uint32_t)so[i] : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if ((uint32_t)r * 32u >= c) break;
+                const uint32_t i = r * 32 + lane;
+                uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
+                const uint32_t carry = __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31);
+                if (lane == 0) prev = carry;
+                big += (i >= 1 && i < c && o[r] - prev >= 128u);
+            }
+        } else {
+            for (uint32_t i = 1 + lane; i < c; i += 32) big += (uint32_t)(so[i] - so[i - 1]) >= 128u;
+        }
         big = __reduce_add_sync(0xffffffffu, big);
         if (lane == 0) {
             meta[t].first_off = so[0];
