@@ -55,6 +55,8 @@ def parse():
                    help="chained path: 'end' = the host enqueues the timed steps without waiting "
                         "(one wait after the last; kernel times accumulated on the device), "
                         "'step' = the host waits for every step")
+    p.add_argument("--shard", default="lpt", choices=["lpt", "contiguous"],
+                   help="tensor partition over the GPUs (SURVEY §8(e) S1); lpt needs --assembly nvlink")
     p.add_argument("--index-codec", default="leb128", choices=["leb128", "fixed"],
                    help="fixed: the paper's naive int32/64 index encoding (PAPER.md:387, 609; R18)")
     p.add_argument("--no-e2e", action="store_true")
@@ -333,9 +335,13 @@ def main():
     specs, rho, pattern, desc = workload(args)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     width = 2 if args.dtype == "bf16" else 4
-    ranges = sdist.shard_plan([s.numel for s in specs], world)
-    b, e = ranges[rank]
-    mine = list(range(b, e))
+    lpt = world > 1 and args.shard == "lpt" and args.assembly == "nvlink" and args.pipeline <= 1 \
+        and not args.sync_step
+    if lpt:  # LPT: balanced shards, records assembled one by one at their global offsets
+        mine = sdist.shard_lpt([s.numel for s in specs], world)[rank]
+    else:    # contiguous ranges: each rank's records are one byte range of the global body
+        b, e = sdist.shard_plan([s.numel for s in specs], world)[rank]
+        mine = list(range(b, e))
 
     # ---- inputs resident in HBM before timing (per-tensor seeds: rank-independent data)
     olds, news, targets = [], [], []
@@ -355,6 +361,7 @@ def main():
 
     comm = torch.cuda.Stream(dev) if world > 1 else None
     nvasm = None
+    recasm = None
 
     slot = {"t": 0, "cur": 0}
 
@@ -363,6 +370,9 @@ def main():
         apply (which needs no collective) and, with two body buffers, the next step."""
         nonlocal root_out
         comm.wait_stream(torch.cuda.current_stream())
+        if recasm is not None:  # record sizes were scattered on the extract's stream
+            recasm.assemble(body, slot=slot["cur"], stream=comm)
+            return
         if nvasm is not None:  # delta_assemble kernel over NVLink peer memory
             nvasm.assemble(body, size, stream=comm, slot=slot["cur"])
             return
@@ -408,15 +418,19 @@ def main():
             tot0 = torch.tensor([size0], dtype=torch.int64, device=dev)
             dist.all_reduce(tot0)
             total0 = int(tot0.item())
-            nvasm = sdist.NvlinkAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
-            if rank == 0:
-                out = nvasm.buf  # rank 0's records are the head of the assembled body
+            if lpt:
+                recasm = sdist.RecordAssembler(ctx, total0 + total0 // 8 + 4096, dev, mine, len(specs), nbuf=2)
+            else:
+                nvasm = sdist.NvlinkAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
+                if rank == 0:
+                    out = nvasm.buf  # rank 0's records are the head of the assembled body
 
         size_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         # two (body, size) slots when the NVLink assembly runs on the comm stream: step t+1
         # extracts into the other slot while step t's body is still being copied to rank 0
-        nslots = 2 if nvasm is not None else 1
-        outs = [out] + ([nvasm.bufs[1] if rank == 0 else torch.empty_like(out)] if nslots == 2 else [])
+        nslots = 2 if (nvasm is not None or recasm is not None) else 1
+        outs = [out] + ([nvasm.bufs[1] if (rank == 0 and nvasm is not None) else torch.empty_like(out)]
+                        if nslots == 2 else [])
         size_devs = [size_dev] + ([torch.zeros(1, dtype=torch.int64, device=dev)] if nslots == 2 else [])
         slot_free = [None] * nslots  # comm-stream event: the slot's last assembly is done
 
@@ -442,6 +456,8 @@ def main():
         else:
             def before_apply(buf, size):
                 if world > 1:
+                    if recasm is not None:  # on the extract's stream, before the next extract
+                        recasm.record_sizes(ctx.table_dev_ptr(), slot=slot["cur"])
                     assemble(size, buf)
 
             def step(acc=None, wait=True):
@@ -576,7 +592,8 @@ def main():
                    "lanes": total_lanes, "weights_bytes": total_lanes * width,
                    "scanned_bytes_per_step": scanned_total, "rho": rho, "pattern": pattern,
                    "seed": args.seed, "index_codec": args.index_codec,
-                   "shard": "contiguous balanced tensor ranges",
+                   "shard": ("LPT tensor partition, record-granular NVLink assembly" if lpt
+                             else "contiguous balanced tensor ranges"),
                    "l2": f"inputs ({scanned_total / 1e9:.1f} GB per step) larger than L2 (126 MB); no flush"},
         "payload": {"body_bytes": body_total, "ratio": round(total_lanes * width / body_total, 3),
                     "nnz": nnz_total, "rho_measured": nnz_total / total_lanes,
@@ -603,7 +620,8 @@ def main():
         # per rank and step: K1, K1b, 5 tile scans, K3, K3b (9; no K1b with fixed-width
         # indices) + K4, K5 + A1-A4 (fixed-width: A1, A2f, A4f) [+ delta_assemble when N > 1]
         "gpu_launches": ((15 if args.index_codec == "leb128" else 13)
-                         + (1 if world > 1 and nvasm is not None else 0)) * args.steps,
+                         + (1 if world > 1 and nvasm is not None else 0)
+                         + (3 if world > 1 and recasm is not None else 0)) * args.steps,
         "clocks": clk,
     }
     if k1_ms > 0:
@@ -652,6 +670,8 @@ def main():
         print(json.dumps(result), flush=True)
     if nvasm is not None:  # drop the CUDA IPC mapping of rank 0's buffer before rank 0 exits
         nvasm.close()
+    if recasm is not None:
+        recasm.close()
     ctx.close()
     if world > 1:
         dist.barrier()

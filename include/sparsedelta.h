@@ -249,6 +249,30 @@ int delta_apply_wait(delta_ctx *ctx, void *stream);
 int delta_assemble(delta_ctx *ctx, const void *src_dev, void *dst_peer_dev, uint64_t dst_capacity,
                    const uint64_t *sizes_dev, uint32_t n_ranks, uint32_t rank, void *stream);
 
+/* Record-granular assembly, for any tensor partition (LPT balances the
+ * shards better than contiguous ranges, but then a rank's records are not one byte range of
+ * the global body).  Global record order is the descriptor order of the whole list (R15).
+ *
+ * delta_record_sizes — write this rank's record sizes into sizes_dev (n_global uint64, device,
+ * global order; every other entry set to 0): sizes_dev[gidx_dev[j]] = table_dev[j].record_bytes
+ * for the n_local rows of table_dev (this rank's device offset table, e.g. delta_table_dev,
+ * rows in this rank's order) and gidx_dev (n_local uint32, device: global index of local
+ * record j, ascending).  Asynchronous on `stream`.  Summing sizes_dev over the ranks (one
+ * NCCL all-reduce) gives every record's size on every rank.
+ *
+ * delta_assemble_records — copy this rank's body (src_dev: its records back to back in local
+ * order) record by record into dst_dev (the root's assembled-body buffer, this GPU's own
+ * memory or a CUDA IPC peer mapping over NVLink, dst_capacity bytes): record j goes to the
+ * global offset sum(sizes_dev[0 .. gidx_dev[j] - 1]), computed on the device from the summed
+ * sizes_dev.  Asynchronous on `stream`; a total larger than dst_capacity (or a ~0 size from a
+ * closed extract gate) writes nothing and is reported by delta_assemble_wait.  The caller
+ * orders the copies against the root's readers (e.g. an all-reduce after them). */
+int delta_record_sizes(delta_ctx *ctx, const delta_record_info *table_dev, uint32_t n_local,
+                       const uint32_t *gidx_dev, uint64_t *sizes_dev, uint32_t n_global, void *stream);
+int delta_assemble_records(delta_ctx *ctx, const void *src_dev, const uint32_t *gidx_dev, uint32_t n_local,
+                           const uint64_t *sizes_dev, uint32_t n_global, void *dst_dev, uint64_t dst_capacity,
+                           void *stream);
+
 /* Synchronise `stream`; DELTA_ECAPACITY if a delta_assemble since the last wait would have
  * overflowed its destination (nothing was written by that copy), else DELTA_OK. */
 int delta_assemble_wait(delta_ctx *ctx, void *stream);

@@ -349,6 +349,27 @@ class DeltaContext:
                                              c_void_p(sizes.data_ptr()), sizes.numel(), rank,
                                              _stream_handle(stream)))
 
+    def table_dev_ptr(self) -> int:
+        """Device pointer of this context's offset table (delta_table_dev): valid after an
+        extract until the next one on the same context."""
+        return self._lib.delta_table_dev(self._h) or 0
+
+    def record_sizes(self, table_ptr: int, n_local: int, gidx, sizes, stream=None):
+        """This rank's record sizes into the global-order int64 CUDA tensor ``sizes`` (zeros
+        elsewhere); ``table_ptr``: device offset table (DeviceTable.ptr), ``gidx``: int32
+        CUDA tensor of the local records' global indices (delta_record_sizes)."""
+        self._check(self._lib.delta_record_sizes(self._h, c_void_p(table_ptr), n_local, c_void_p(gidx.data_ptr()),
+                                                 c_void_p(sizes.data_ptr()), sizes.numel(), _stream_handle(stream)))
+
+    def assemble_records(self, src, gidx, sizes, dst, stream=None):
+        """Copy this rank's body ``src`` record by record to the global offsets in ``dst``
+        (the root's buffer, local or IPC-mapped) from the summed global ``sizes``
+        (delta_assemble_records)."""
+        self._check(self._lib.delta_assemble_records(self._h, c_void_p(src.data_ptr() if src.numel() else 0),
+                                                     c_void_p(gidx.data_ptr()), gidx.numel(),
+                                                     c_void_p(sizes.data_ptr()), sizes.numel(),
+                                                     c_void_p(dst.data_ptr()), dst.numel(), _stream_handle(stream)))
+
     def digest(self, body, stream=None) -> bytes:
         """BLAKE3-256 of a uint8 CUDA tensor, computed on the GPU (delta_digest)."""
         out = ctypes.create_string_buffer(32)

@@ -83,7 +83,7 @@ struct delta_ctx {
     ExtractSummary *h_summary = nullptr;  // pinned
 
     // ---- apply workspace
-    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status, dg_ws;
+    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status, asm_off, dg_ws;
     uint32_t *h_asm = nullptr;  // pinned
     ApplyState *h_state = nullptr;  // pinned
     // ---- delta_merge workspace
@@ -197,7 +197,7 @@ void delta_ctx_destroy(delta_ctx *c) {
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->tile_plan, &c->blk_a,
                       &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
-                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->dg_ws, &c->a_cnt, &c->a_sum,
+                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->asm_off, &c->dg_ws, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
     if (c->profiling) {
@@ -915,6 +915,44 @@ extern "C" int delta_assemble(delta_ctx *ctx, const void *src, void *dst, uint64
                        reinterpret_cast<const unsigned long long *>(sizes), rank, ctx->asm_status.as<uint32_t>(),
                        ctx->sm_count * 2, s),
        "assemble launch");
+    return DELTA_OK;
+}
+
+extern "C" int delta_record_sizes(delta_ctx *ctx, const delta_record_info *table_dev, uint32_t n_local,
+                                  const uint32_t *gidx_dev, uint64_t *sizes_dev, uint32_t n_global, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!sizes_dev || (n_local && (!table_dev || !gidx_dev)) || n_local > n_global)
+        return fail(ctx, DELTA_EINVAL, 0, "delta_record_sizes: bad arguments");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(launch_record_sizes(reinterpret_cast<const RecordRow *>(table_dev), n_local, gidx_dev,
+                           reinterpret_cast<unsigned long long *>(sizes_dev), n_global,
+                           static_cast<cudaStream_t>(stream)),
+       "record sizes launch");
+    return DELTA_OK;
+}
+
+extern "C" int delta_assemble_records(delta_ctx *ctx, const void *src_dev, const uint32_t *gidx_dev, uint32_t n_local,
+                                      const uint64_t *sizes_dev, uint32_t n_global, void *dst_dev, uint64_t dst_capacity,
+                                      void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!sizes_dev || !dst_dev || (n_local && (!src_dev || !gidx_dev)) || n_local > n_global)
+        return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_records: bad arguments");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->asm_status.p) {
+        GROW(ctx->asm_status, 16);
+        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
+    }
+    GROW(ctx->asm_off, ((size_t)n_global + 1 + n_local + 1) * 8);
+    unsigned long long *goff = ctx->asm_off.as<unsigned long long>();
+    CK(launch_assemble_records(static_cast<const uint8_t *>(src_dev), static_cast<uint8_t *>(dst_dev), dst_capacity,
+                               reinterpret_cast<const unsigned long long *>(sizes_dev), gidx_dev, n_local, n_global,
+                               goff, goff + n_global + 1, ctx->asm_status.as<uint32_t>(), ctx->sm_count * 2, s),
+       "assemble records launch");
     return DELTA_OK;
 }
 

@@ -172,6 +172,12 @@ struct ApplyArgs {
 
 cudaError_t launch_blake3(const uint8_t *in, unsigned long long n, uint32_t *ws, uint32_t *out32, cudaStream_t s);
 
+cudaError_t launch_record_sizes(const RecordRow *table, uint32_t n_local, const uint32_t *gidx,
+                                unsigned long long *sizes, uint32_t n_global, cudaStream_t s);
+cudaError_t launch_assemble_records(const uint8_t *src, uint8_t *dst, unsigned long long capacity,
+                                    const unsigned long long *sizes, const uint32_t *gidx, uint32_t n_local,
+                                    uint32_t n_global, unsigned long long *goff, unsigned long long *loff,
+                                    uint32_t *status, int ctas, cudaStream_t s);
 cudaError_t launch_assemble(const uint8_t *src, uint8_t *dst, unsigned long long capacity,
                             const unsigned long long *sizes, uint32_t rank, uint32_t *status, int ctas,
                             cudaStream_t s);

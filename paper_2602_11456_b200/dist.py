@@ -56,6 +56,20 @@ def shard_plan(numels, world: int):
     return ranges
 
 
+def shard_lpt(numels, world: int):
+    """S1, LPT (max/ideal 1.0078 at G = 8 for Qwen3-8B vs 1.0406 for
+    contiguous ranges): tensors in decreasing size (ties: lower index first) each go to the
+    rank with the smallest load so far (ties: lower rank).  Deterministic; returns one
+    ascending list of global tensor indices per rank."""
+    loads = [0] * max(world, 1)
+    parts = [[] for _ in range(max(world, 1))]
+    for k in sorted(range(len(numels)), key=lambda i: (-numels[i], i)):
+        r = min(range(len(loads)), key=lambda q: (loads[q], q))
+        parts[r].append(k)
+        loads[r] += numels[k]
+    return [sorted(p) for p in parts]
+
+
 def gather_sizes(local_bytes: int, device, group=None):
     """S2: all-gather of one int64 per rank; returns (sizes list, my offset, total)."""
     world = dist.get_world_size(group)
@@ -147,3 +161,52 @@ class NvlinkAssembler:
         self.peer = None
         self.peers = []
         dist.barrier(group=self.group)
+
+
+class RecordAssembler:
+    """S2 + S3 for any partition (LPT): every rank's records go to their own global offsets
+    in the root's assembled-body buffer.  Per step: ``record_sizes(slot)`` on the extract's
+    stream (right after the extract: this rank's record sizes into a global-order array),
+    then ``assemble(body, slot)`` on a comm stream — an all-reduce (sum) of that array and
+    one delta_assemble_records kernel writing the records over NVLink (CUDA IPC mapping of
+    the root's buffer; the root copies its own records locally) — and a one-element
+    all-reduce as the completion token.  ``nbuf`` root buffers / size arrays: step t's copy
+    overlaps step t+1."""
+
+    def __init__(self, ctx, capacity: int, device, mine, n_global: int, group=None, root: int = 0,
+                 nbuf: int = 2):
+        self.ctx, self.group, self.root = ctx, group, root
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.device(device)
+        self.n_global = n_global
+        self.gidx = torch.tensor(list(mine), dtype=torch.int32, device=self.device)
+        self.sizes = [torch.zeros(n_global, dtype=torch.int64, device=self.device) for _ in range(nbuf)]
+        self.bufs = ([torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
+                     if self.rank == root else [None] * nbuf)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, [reduce_tensor(b) for b in self.bufs] if self.rank == root else None,
+                               group=group)
+        self.peers = list(self.bufs) if self.rank == root else []
+        if self.rank != root:
+            for fn, args in handles[root]:
+                args = list(args)
+                args[6] = self.device.index  # rebuild on this process's device (peer mapping)
+                self.peers.append(fn(*args))
+        self.token = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    def record_sizes(self, table_ptr: int, slot: int = 0, stream=None):
+        self.ctx.record_sizes(table_ptr, self.gidx.numel(), self.gidx, self.sizes[slot], stream=stream)
+
+    def assemble(self, body: torch.Tensor, slot: int = 0, stream=None):
+        stream = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(stream):
+            dist.all_reduce(self.sizes[slot], group=self.group)
+            self.ctx.assemble_records(body, self.gidx, self.sizes[slot], self.peers[slot], stream=stream)
+            dist.all_reduce(self.token, group=self.group)
+        return self.bufs[slot] if self.rank == self.root else None
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        self.peers = []
+        dist.barrier(group=self.group)
+

@@ -58,6 +58,27 @@ def main():
         ok2 = torch.equal(got2[:tot].cpu(), full_body.cpu())
         print(f"[rank0] NVLink delta_assemble: match = {ok2}", flush=True)
         ok &= ok2
+    # LPT partition + record-granular assembly (delta_record_sizes / delta_assemble_records)
+    lpt = sdist.shard_lpt([s.numel for s in specs], world)[rank]
+    mine_l = [(specs[k].name, pairs[k][0], pairs[k][1]) for k in lpt]
+    rasm = sdist.RecordAssembler(ctx, tot + 4096, dev, lpt, len(specs))
+    for slot in (0, 1):
+        if mine_l:
+            bl, _ = ctx.delta_extract(mine_l, table="device")
+        else:
+            bl = torch.empty(0, dtype=torch.uint8, device=dev)
+            rasm.sizes[slot].zero_()
+        if mine_l:
+            rasm.record_sizes(ctx.table_dev_ptr(), slot=slot)
+        got3 = rasm.assemble(bl, slot=slot)
+        torch.cuda.synchronize()
+        ctx.assemble_wait()
+        if rank == 0:
+            ok3 = torch.equal(got3[:tot].cpu(), full_body.cpu())
+            print(f"[rank0] LPT {[len(p) for p in sdist.shard_lpt([s.numel for s in specs], world)]} "
+                  f"record assembly slot {slot}: match = {ok3}", flush=True)
+            ok &= ok3
+    rasm.close()
     if mine:
         targets = [(n, o.clone()) for n, o, _ in mine]
         ctx.delta_apply(targets, body, table=table)

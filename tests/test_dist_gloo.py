@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2602_11456_b200.dist import assemble, gather_sizes, shard_plan, shift_table
+from paper_2602_11456_b200.dist import assemble, gather_sizes, shard_lpt, shard_plan, shift_table
 
 
 def _best_max(numels, world):
@@ -51,6 +51,38 @@ def test_shard_plan_qwen3_balance():
         r = shard_plan(numels, world)
         ideal = sum(numels) / world
         assert max(sum(numels[a:b]) for a, b in r) / ideal <= bound
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_lpt_properties(world):
+    """LPT: a partition (every tensor exactly once), ascending lists, deterministic, and
+    within Graham's 4/3 - 1/(3G) bound of the optimum (checked by brute force on small
+    lists)."""
+    rng = np.random.default_rng(100 + world)
+    for _ in range(30):
+        n = int(rng.integers(0, 9))
+        numels = [int(x) for x in rng.integers(0, 1000, n)]
+        parts = shard_lpt(numels, world)
+        assert len(parts) == world
+        assert sorted(k for p in parts for k in p) == list(range(n))
+        assert all(p == sorted(p) for p in parts)
+        assert shard_lpt(numels, world) == parts
+        if n and world <= 4:
+            best = min(max(sum(numels[k] for k in range(n) if assign[k] == r) for r in range(world))
+                       for assign in np.ndindex(*([world] * n)))
+            got = max(sum(numels[k] for k in p) for p in parts)
+            assert got <= (4 / 3 - 1 / (3 * world)) * best + 1e-9
+
+
+def test_shard_lpt_qwen3_balance():
+    """LPT on Qwen3-8B lanes gives max/ideal 1.0037 (G=4) and 1.0078 (G=8),
+    against 1.0160 / 1.0406 for contiguous ranges."""
+    from workload import qwen3
+    numels = [s.numel for s in qwen3("8B")]
+    for world, bound in ((2, 1.001), (4, 1.0040), (8, 1.0080)):
+        parts = shard_lpt(numels, world)
+        ideal = sum(numels) / world
+        assert max(sum(numels[k] for k in p) for p in parts) / ideal <= bound
 
 
 def _free_port():
