@@ -441,7 +441,7 @@ def main():
                               "locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
                     acc[kname] = acc.get(kname, 0.0) + t[kname]
 
-        if args.sync_step or (world > 1 and nvasm is None):
+        if args.sync_step or (world > 1 and nvasm is None and recasm is None):
             def step(acc=None):
                 # host-sized path: delta_extract reads the size back (sync), the apply takes
                 # the device table; 2 host syncs per step
@@ -483,7 +483,7 @@ def main():
                     record(acc)
                 return (outs[s][:n] if n is not None else None), None
 
-    chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None))
+    chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None and recasm is None))
     pipelined = chained and args.host_sync == "end"
     for _ in range(max(args.warmup, 0)):
         body, table = step()
