@@ -55,8 +55,9 @@ def parse():
                    help="chained path: 'end' = the host enqueues the timed steps without waiting "
                         "(one wait after the last; kernel times accumulated on the device), "
                         "'step' = the host waits for every step")
-    p.add_argument("--shard", default="lpt", choices=["lpt", "contiguous"],
-                   help="tensor partition over the GPUs (SURVEY §8(e) S1); lpt needs --assembly nvlink")
+    p.add_argument("--shard", default="contiguous", choices=["lpt", "contiguous"],
+                   help="tensor partition over the GPUs (SURVEY §8(e) S1); lpt (record-granular "
+                        "assembly) needs --assembly nvlink; measured no faster at N = 2, 4")
     p.add_argument("--index-codec", default="leb128", choices=["leb128", "fixed"],
                    help="fixed: the paper's naive int32/64 index encoding (PAPER.md:387, 609; R18)")
     p.add_argument("--no-e2e", action="store_true")
