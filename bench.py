@@ -65,8 +65,11 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     p.add_argument("--no-clocks", action="store_true")
-    p.add_argument("--assembly", default="nvlink", choices=["nvlink", "nccl"],
-                   help="N>1: body assembly by the delta_assemble NVLink kernel or NCCL P2P")
+    p.add_argument("--assembly", default="nvlink", choices=["nvlink", "nccl", "none"],
+                   help="N>1: body assembly by the delta_assemble NVLink kernel or NCCL P2P "
+                        "('none': diagnostics only — the sharded extract+apply without S2/S3)")
+    p.add_argument("--comm-priority", type=int, default=0,
+                   help="CUDA stream priority of the assembly stream (negative = higher)")
     p.add_argument("--sync-step", action="store_true",
                    help="host-sized step (size readback between extract and apply) instead of the "
                         "chained device-sized one")
@@ -360,7 +363,7 @@ def main():
     root_out = None
     stream = torch.cuda.current_stream()
 
-    comm = torch.cuda.Stream(dev) if world > 1 else None
+    comm = torch.cuda.Stream(dev, priority=args.comm_priority) if world > 1 else None
     nvasm = None
     recasm = None
 
@@ -370,6 +373,8 @@ def main():
         """S2+S3 on a side stream: the transfer of the body to rank 0 overlaps this rank's
         apply (which needs no collective) and, with two body buffers, the next step."""
         nonlocal root_out
+        if args.assembly == "none":
+            return
         comm.wait_stream(torch.cuda.current_stream())
         if recasm is not None:  # record sizes were scattered on the extract's stream
             recasm.assemble(body, slot=slot["cur"], stream=comm)
@@ -442,7 +447,7 @@ def main():
                               "locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
                     acc[kname] = acc.get(kname, 0.0) + t[kname]
 
-        if args.sync_step or (world > 1 and nvasm is None and recasm is None):
+        if args.sync_step or (world > 1 and nvasm is None and recasm is None and args.assembly != "none"):
             def step(acc=None):
                 # host-sized path: delta_extract reads the size back (sync), the apply takes
                 # the device table; 2 host syncs per step
@@ -484,7 +489,8 @@ def main():
                     record(acc)
                 return (outs[s][:n] if n is not None else None), None
 
-    chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None and recasm is None))
+    chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None and recasm is None
+                                                             and args.assembly != "none"))
     pipelined = chained and args.host_sync == "end"
     for _ in range(max(args.warmup, 0)):
         body, table = step()
@@ -630,6 +636,10 @@ def main():
     if rank_view is not None:
         result["per_rank"] = rank_view
     result["config"]["host_sync"] = "end (steps enqueued back to back)" if pipelined else "every step"
+    if world > 1:
+        result["config"]["assembly"] = {"nvlink": "delta_assemble over NVLink (CUDA IPC), 2 body buffers",
+                                        "nccl": "NCCL P2P batch", "none": "NONE (diagnostics: no S2/S3)"}[
+                                            args.assembly]
     if pipelined:  # the same steps with the host waiting for each one (latency view)
         ks = max(3, args.steps // 2)
         if world > 1:
