@@ -68,6 +68,7 @@ def parse():
     p.add_argument("--assembly", default="nvlink", choices=["nvlink", "nccl", "none"],
                    help="N>1: body assembly by the delta_assemble NVLink kernel or NCCL P2P "
                         "('none': diagnostics only — the sharded extract+apply without S2/S3)")
+    p.add_argument("--assemble-ctas", type=int, default=0, help="CTAs of the NVLink assembly kernel (0 = default)")
     p.add_argument("--comm-priority", type=int, default=0,
                    help="CUDA stream priority of the assembly stream (negative = higher)")
     p.add_argument("--sync-step", action="store_true",
@@ -417,6 +418,8 @@ def main():
             ctx.set_option(6, args.scatter_order)
         if args.index_codec == "fixed":
             ctx.set_option(8, 2)
+        if args.assemble_ctas:
+            ctx.set_option(10, args.assemble_ctas)
         ctx.set_profiling(True)
         size0 = ctx.delta_size(tl)
         out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)

@@ -326,7 +326,7 @@ typedef struct {
 /* Launch-shape options (performance only; results never depend on them). */
 enum {
     DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode kernel, CTAs per SM (default 8) */
-    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 8) */
+    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 6) */
     DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
                                         vectors (default); 4 = as 1 with 512 threads x 4 vectors;
                                         5 = as 1, persistent (3 CTAs per SM loop over tiles).
@@ -359,6 +359,9 @@ enum {
                                          width -> DELTA_D_TRUNCATED, != nnz indices -> DELTA_D_COUNT,
                                          not strictly increasing -> DELTA_D_NONINCREASING, an index
                                          >= element_count -> DELTA_D_RANGE (all-or-nothing as ever). */
+    DELTA_OPT_ASSEMBLE_CTAS = 10,     /* grid (CTAs, total) of delta_assemble / delta_assemble_records
+                                         (default 296): fewer CTAs take fewer SM slots from the
+                                         kernels the copy overlaps */
     DELTA_OPT_ADVANCE = 9             /* extract-and-advance (NEXT f3; the trainer keeps W_t only to
                                          diff it against W_{t+1}): 2 = the
                                          compare kernel also stores every changed lane of new into

@@ -34,6 +34,7 @@ DELTA_OPT_APPLY_CTAS_PER_SM, DELTA_OPT_EMIT_CTAS_PER_SM, DELTA_OPT_SCAN_KERNEL =
 DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER, DELTA_OPT_MODE = 4, 5, 6, 7
 DELTA_OPT_INDEX_CODEC = 8  # 1 LEB128 gaps (default), 2 fixed-width absolute indices (reading R18)
 DELTA_OPT_ADVANCE = 9      # 2: extract-and-advance (old spans overwritten with new; NEXT f3)
+DELTA_OPT_ASSEMBLE_CTAS = 10  # CTAs of the NVLink assembly kernels
 
 
 class Span(ctypes.Structure):

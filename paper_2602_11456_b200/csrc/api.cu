@@ -99,8 +99,9 @@ struct delta_ctx {
     int ring_next = 0;
 
     // ---- launch options
-    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 8, scatter_ctas_per_sm = 4, scan_kernel = 0;
+    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 6, scatter_ctas_per_sm = 4, scan_kernel = 0;
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
+    int assemble_ctas = 296;  // grid of the NVLink assembly kernels (peer stores)
     bool entry_major = true;
     int mode = 0;  // records written by extract: 0 replace, 1 additive
     int index_codec = 0;  // 0 LEB128 gaps, 1 fixed-width absolute indices (extract and apply)
@@ -240,6 +241,7 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
         if (c->mode != (int)value - 1) c->scan_cached = false;
         c->mode = (int)value - 1;
     }
+    else if (option == DELTA_OPT_ASSEMBLE_CTAS) c->assemble_ctas = (int)value;
     else if (option == DELTA_OPT_ADVANCE) {
         if (value > 2) return DELTA_EINVAL;
         if (value == 2 && c->mode != 0) return DELTA_EINVAL;  // replace mode only
@@ -913,7 +915,7 @@ extern "C" int delta_assemble(delta_ctx *ctx, const void *src, void *dst, uint64
     }
     CK(launch_assemble(static_cast<const uint8_t *>(src), static_cast<uint8_t *>(dst), cap,
                        reinterpret_cast<const unsigned long long *>(sizes), rank, ctx->asm_status.as<uint32_t>(),
-                       ctx->sm_count * 2, s),
+                       ctx->assemble_ctas, s),
        "assemble launch");
     return DELTA_OK;
 }
@@ -951,7 +953,7 @@ extern "C" int delta_assemble_records(delta_ctx *ctx, const void *src_dev, const
     unsigned long long *goff = ctx->asm_off.as<unsigned long long>();
     CK(launch_assemble_records(static_cast<const uint8_t *>(src_dev), static_cast<uint8_t *>(dst_dev), dst_capacity,
                                reinterpret_cast<const unsigned long long *>(sizes_dev), gidx_dev, n_local, n_global,
-                               goff, goff + n_global + 1, ctx->asm_status.as<uint32_t>(), ctx->sm_count * 2, s),
+                               goff, goff + n_global + 1, ctx->asm_status.as<uint32_t>(), ctx->assemble_ctas, s),
        "assemble records launch");
     return DELTA_OK;
 }
