@@ -326,7 +326,7 @@ typedef struct {
 /* Launch-shape options (performance only; results never depend on them). */
 enum {
     DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode kernel, CTAs per SM (default 8) */
-    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 6) */
+    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 8) */
     DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
                                         vectors (default); 4 = as 1 with 512 threads x 4 vectors;
                                         5 = as 1, persistent (3 CTAs per SM loop over tiles).

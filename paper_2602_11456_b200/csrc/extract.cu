@@ -755,12 +755,51 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
     }
 }
 
+// The in-tile gap bytes of a dense tile (count > 256), written from p on: batches of 256
+// entries, a batch's offsets loaded up front (8 per lane), predecessors by shuffle (across
+// batches: the carried last offset), byte positions from a ballot of the two-byte gaps.
+__device__ __noinline__ void emit_gaps_batched(const uint16_t *so, uint32_t c, uint8_t *p, int lane) {
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t last = 0;
+    for (uint32_t b0 = 0; b0 < c; b0 += 256) {
+        uint32_t o[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint32_t i = b0 + r * 32 + lane;
+            o[r] = i < c ? (uint32_t)so[i] : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (b0 + (uint32_t)r * 32u >= c) break;
+            const uint32_t i = b0 + r * 32 + lane;
+            uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
+            const uint32_t carry = r ? __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31) : last;
+            if (lane == 0) prev = carry;
+            const bool act = i >= 1 && i < c;
+            const uint32_t gi = act ? o[r] - prev : 0u;
+            const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
+            const uint32_t skip = (b0 == 0 && r == 0) ? 1u : 0u;  // entry 0 has no in-tile gap
+            if (act) {
+                uint8_t *q = p + (lane - skip) + __popc(two & lt_mask);
+                if (gi < 128u) {
+                    q[0] = (uint8_t)gi;
+                } else {
+                    q[0] = (uint8_t)(gi | 0x80u);
+                    q[1] = (uint8_t)(gi >> 7);
+                }
+            }
+            p += min(32u, c - b0 - r * 32u) - skip + __popc(two);
+        }
+        last = __shfl_sync(0xffffffffu, o[7], 31);
+    }
+}
+
 // One warp per tile: the LEB128 bytes of the tile's first gap, then the in-tile gaps
 // (differences of the slot's u16 lane offsets, < 2^14: one or two bytes each) encoded 32 at
 // a time — byte positions from a ballot of the two-byte ones — and the raw values copied
 // to their final offsets in the body.
 template <int W, bool FIXED>
-__global__ void __launch_bounds__(256, 6)
+__global__ void __launch_bounds__(256, 8)
 k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
@@ -808,31 +847,30 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
         const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
         uint8_t *p = ib + L0;
         const uint32_t c = e.count;
-        // the values first (their loads overlap the offsets'), then the in-tile gaps in
-        // batches of 256 entries: a batch's offsets are loaded up front (8 per lane), the
-        // predecessor of each entry comes by shuffle (across batches: the carried last one)
+        // the values first (their loads overlap the offsets'), then the in-tile gaps:
+        // tiles with <= 256 changes (all of them at ~1 % density) inline, denser ones in
+        // batches of 256 in a separate (non-inlined) function so its register pressure does
+        // not reach the common path
         warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
-        uint32_t last = 0;  // offset of the entry before the batch
-        for (uint32_t b0 = 0; b0 < c; b0 += 256) {
+        if (c <= 256) {
             uint32_t o[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                const uint32_t i = b0 + r * 32 + lane;
+                const uint32_t i = r * 32 + lane;
                 o[r] = i < c ? (uint32_t)so[i] : 0u;
             }
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                if (b0 + (uint32_t)r * 32u >= c) break;
-                const uint32_t i = b0 + r * 32 + lane;
+                if ((uint32_t)r * 32u >= c) break;
+                const uint32_t i = r * 32 + lane;
                 uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
-                const uint32_t carry = r ? __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31) : last;
+                const uint32_t carry = __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31);
                 if (lane == 0) prev = carry;
                 const bool act = i >= 1 && i < c;
                 const uint32_t gi = act ? o[r] - prev : 0u;
                 const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
-                const uint32_t skip = (b0 == 0 && r == 0) ? 1u : 0u;  // entry 0 has no in-tile gap
                 if (act) {
-                    uint8_t *q = p + (lane - skip) + __popc(two & lt_mask);
+                    uint8_t *q = p + (lane - (r == 0 ? 1 : 0)) + __popc(two & lt_mask);
                     if (gi < 128u) {
                         q[0] = (uint8_t)gi;
                     } else {
@@ -840,9 +878,10 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
                         q[1] = (uint8_t)(gi >> 7);
                     }
                 }
-                p += min(32u, c - b0 - r * 32u) - skip + __popc(two);
+                p += min(32u, c - r * 32u) - (r == 0 ? 1u : 0u) + __popc(two);
             }
-            last = __shfl_sync(0xffffffffu, o[7], 31);
+        } else {
+            emit_gaps_batched(so, c, p, lane);
         }
     }
 }
@@ -902,7 +941,7 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     }
     if (ev) cudaEventRecord(ev[1], s);
     if (!a.index_codec)  // the fixed-width codec needs no gap statistics
-        k_tiles_gaps<<<a.persist_ctas, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
+        k_tiles_gaps<<<a.sm_count * 8, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
     k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);
