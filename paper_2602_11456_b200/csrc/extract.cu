@@ -433,24 +433,25 @@ k_tiles_gaps(TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t slot_cap,
         const uint32_t c = meta[t].count;
         if (c == 0) continue;
         const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
-        uint32_t big = 0, last = 0;
-        for (uint32_t b0 = 0; b0 < c; b0 += 256) {  // batches of 256: offsets loaded up front,
-            uint32_t o[8];                           // predecessors by shuffle
+        uint32_t big = 0;
+        if (c <= 256) {  // every offset of the tile loaded up front, predecessors by shuffle
+            uint32_t o[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                const uint32_t i = b0 + r * 32 + lane;
+                const uint32_t i = r * 32 + lane;
                 o[r] = i < c ? (uint32_t)so[i] : 0u;
             }
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                if (b0 + (uint32_t)r * 32u >= c) break;
-                const uint32_t i = b0 + r * 32 + lane;
+                if ((uint32_t)r * 32u >= c) break;
+                const uint32_t i = r * 32 + lane;
                 uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
-                const uint32_t carry = r ? __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31) : last;
+                const uint32_t carry = __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31);
                 if (lane == 0) prev = carry;
                 big += (i >= 1 && i < c && o[r] - prev >= 128u);
             }
-            last = __shfl_sync(0xffffffffu, o[7], 31);
+        } else {
+            for (uint32_t i = 1 + lane; i < c; i += 32) big += (uint32_t)(so[i] - so[i - 1]) >= 128u;
         }
         big = __reduce_add_sync(0xffffffffu, big);
         if (lane == 0) {
@@ -755,45 +756,6 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
     }
 }
 
-// The in-tile gap bytes of a dense tile (count > 256), written from p on: batches of 256
-// entries, a batch's offsets loaded up front (8 per lane), predecessors by shuffle (across
-// batches: the carried last offset), byte positions from a ballot of the two-byte gaps.
-__device__ __noinline__ void emit_gaps_batched(const uint16_t *so, uint32_t c, uint8_t *p, int lane) {
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    uint32_t last = 0;
-    for (uint32_t b0 = 0; b0 < c; b0 += 256) {
-        uint32_t o[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const uint32_t i = b0 + r * 32 + lane;
-            o[r] = i < c ? (uint32_t)so[i] : 0u;
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            if (b0 + (uint32_t)r * 32u >= c) break;
-            const uint32_t i = b0 + r * 32 + lane;
-            uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
-            const uint32_t carry = r ? __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31) : last;
-            if (lane == 0) prev = carry;
-            const bool act = i >= 1 && i < c;
-            const uint32_t gi = act ? o[r] - prev : 0u;
-            const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
-            const uint32_t skip = (b0 == 0 && r == 0) ? 1u : 0u;  // entry 0 has no in-tile gap
-            if (act) {
-                uint8_t *q = p + (lane - skip) + __popc(two & lt_mask);
-                if (gi < 128u) {
-                    q[0] = (uint8_t)gi;
-                } else {
-                    q[0] = (uint8_t)(gi | 0x80u);
-                    q[1] = (uint8_t)(gi >> 7);
-                }
-            }
-            p += min(32u, c - b0 - r * 32u) - skip + __popc(two);
-        }
-        last = __shfl_sync(0xffffffffu, o[7], 31);
-    }
-}
-
 // One warp per tile: the LEB128 bytes of the tile's first gap, then the in-tile gaps
 // (differences of the slot's u16 lane offsets, < 2^14: one or two bytes each) encoded 32 at
 // a time — byte positions from a ballot of the two-byte ones — and the raw values copied
@@ -847,18 +809,14 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
         const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
         uint8_t *p = ib + L0;
         const uint32_t c = e.count;
-        // the values first (their loads overlap the offsets'), then the in-tile gaps:
-        // tiles with <= 256 changes (all of them at ~1 % density) inline, denser ones in
-        // batches of 256 in a separate (non-inlined) function so its register pressure does
-        // not reach the common path
-        warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
-        if (c <= 256) {
+        if (c <= 256) {  // ~all tiles up to a few % density: every load of the tile issued up front
             uint32_t o[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const uint32_t i = r * 32 + lane;
                 o[r] = i < c ? (uint32_t)so[i] : 0u;
             }
+            warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 if ((uint32_t)r * 32u >= c) break;
@@ -880,9 +838,25 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
                 }
                 p += min(32u, c - r * 32u) - (r == 0 ? 1u : 0u) + __popc(two);
             }
-        } else {
-            emit_gaps_batched(so, c, p, lane);
+            continue;
         }
+        for (uint32_t i0 = 1; i0 < e.count; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool act = i < e.count;
+            const uint32_t gi = act ? (uint32_t)(so[i] - so[i - 1]) : 0u;
+            const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
+            if (act) {
+                uint8_t *q = p + lane + __popc(two & lt_mask);
+                if (gi < 128u) {
+                    q[0] = (uint8_t)gi;
+                } else {
+                    q[0] = (uint8_t)(gi | 0x80u);
+                    q[1] = (uint8_t)(gi >> 7);
+                }
+            }
+            p += min(32u, e.count - i0) + __popc(two);
+        }
+        warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), e.count * W, lane);
     }
 }
 
@@ -941,7 +915,7 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     }
     if (ev) cudaEventRecord(ev[1], s);
     if (!a.index_codec)  // the fixed-width codec needs no gap statistics
-        k_tiles_gaps<<<a.sm_count * 8, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
+        k_tiles_gaps<<<a.persist_ctas, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
     k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);
