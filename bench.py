@@ -65,8 +65,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     p.add_argument("--no-clocks", action="store_true")
-    p.add_argument("--assembly", default="nvlink", choices=["nvlink", "nccl", "none"],
-                   help="N>1: body assembly by the delta_assemble NVLink kernel or NCCL P2P "
+    p.add_argument("--assembly", default="nvlink", choices=["nvlink", "flags", "nccl", "none"],
+                   help="N>1: body assembly by the delta_assemble NVLink kernel (sizes by NCCL "
+                        "all-gather), by delta_assemble_flags (sizes and completion through flags in "
+                        "the root's memory, no collective) or NCCL P2P "
                         "('none': diagnostics only — the sharded extract+apply without S2/S3)")
     p.add_argument("--assemble-ctas", type=int, default=0, help="CTAs of the NVLink assembly kernel (0 = default)")
     p.add_argument("--comm-priority", type=int, default=0,
@@ -367,6 +369,7 @@ def main():
     comm = torch.cuda.Stream(dev, priority=args.comm_priority) if world > 1 else None
     nvasm = None
     recasm = None
+    flasm = None
 
     slot = {"t": 0, "cur": 0}
 
@@ -379,6 +382,9 @@ def main():
         comm.wait_stream(torch.cuda.current_stream())
         if recasm is not None:  # record sizes were scattered on the extract's stream
             recasm.assemble(body, slot=slot["cur"], stream=comm)
+            return
+        if flasm is not None:  # sizes and completion through flags in rank 0's memory
+            flasm.assemble(body, size, slot=slot["cur"], stream=comm)
             return
         if nvasm is not None:  # delta_assemble kernel over NVLink peer memory
             nvasm.assemble(body, size, stream=comm, slot=slot["cur"])
@@ -423,6 +429,13 @@ def main():
         ctx.set_profiling(True)
         size0 = ctx.delta_size(tl)
         out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
+        if world > 1 and args.assembly == "flags":
+            tot0 = torch.tensor([size0], dtype=torch.int64, device=dev)
+            dist.all_reduce(tot0)
+            total0 = int(tot0.item())
+            flasm = sdist.FlagAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
+            if rank == 0:
+                out = flasm.buf  # rank 0's records are the head of the assembled body
         if world > 1 and args.assembly == "nvlink":
             tot0 = torch.tensor([size0], dtype=torch.int64, device=dev)
             dist.all_reduce(tot0)
@@ -437,8 +450,9 @@ def main():
         size_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         # two (body, size) slots when the NVLink assembly runs on the comm stream: step t+1
         # extracts into the other slot while step t's body is still being copied to rank 0
-        nslots = 2 if (nvasm is not None or recasm is not None) else 1
-        outs = [out] + ([nvasm.bufs[1] if (rank == 0 and nvasm is not None) else torch.empty_like(out)]
+        nslots = 2 if (nvasm is not None or recasm is not None or flasm is not None) else 1
+        root_bufs = nvasm.bufs if nvasm is not None else (flasm.bufs if flasm is not None else None)
+        outs = [out] + ([root_bufs[1] if (rank == 0 and root_bufs is not None) else torch.empty_like(out)]
                         if nslots == 2 else [])
         size_devs = [size_dev] + ([torch.zeros(1, dtype=torch.int64, device=dev)] if nslots == 2 else [])
         slot_free = [None] * nslots  # comm-stream event: the slot's last assembly is done
@@ -450,7 +464,8 @@ def main():
                               "locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
                     acc[kname] = acc.get(kname, 0.0) + t[kname]
 
-        if args.sync_step or (world > 1 and nvasm is None and recasm is None and args.assembly != "none"):
+        if args.sync_step or (world > 1 and nvasm is None and recasm is None and flasm is None
+                              and args.assembly != "none"):
             def step(acc=None):
                 # host-sized path: delta_extract reads the size back (sync), the apply takes
                 # the device table; 2 host syncs per step
@@ -493,7 +508,7 @@ def main():
                 return (outs[s][:n] if n is not None else None), None
 
     chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None and recasm is None
-                                                             and args.assembly != "none"))
+                                                             and flasm is None and args.assembly != "none"))
     pipelined = chained and args.host_sync == "end"
     for _ in range(max(args.warmup, 0)):
         body, table = step()
@@ -630,7 +645,8 @@ def main():
         # per rank and step: K1, K1b, 5 tile scans, K3, K3b (9; no K1b with fixed-width
         # indices) + K4, K5 + A1-A4 (fixed-width: A1, A2f, A4f) [+ delta_assemble when N > 1]
         "gpu_launches": ((15 if args.index_codec == "leb128" else 13)
-                         + (1 if world > 1 and nvasm is not None else 0)
+                         + (1 if world > 1 and (nvasm is not None or flasm is not None) else 0)
+                         + (1 if world > 1 and flasm is not None and rank == 0 else 0)
                          + (3 if world > 1 and recasm is not None else 0)) * args.steps,
         "clocks": clk,
     }
@@ -641,6 +657,7 @@ def main():
     result["config"]["host_sync"] = "end (steps enqueued back to back)" if pipelined else "every step"
     if world > 1:
         result["config"]["assembly"] = {"nvlink": "delta_assemble over NVLink (CUDA IPC), 2 body buffers",
+                                        "flags": "delta_assemble_flags over NVLink, no collective, 2 body buffers",
                                         "nccl": "NCCL P2P batch", "none": "NONE (diagnostics: no S2/S3)"}[
                                             args.assembly]
     if pipelined:  # the same steps with the host waiting for each one (latency view)
@@ -686,6 +703,8 @@ def main():
         nvasm.close()
     if recasm is not None:
         recasm.close()
+    if flasm is not None:
+        flasm.close()
     ctx.close()
     if world > 1:
         dist.barrier()

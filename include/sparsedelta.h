@@ -249,6 +249,25 @@ int delta_apply_wait(delta_ctx *ctx, void *stream);
 int delta_assemble(delta_ctx *ctx, const void *src_dev, void *dst_peer_dev, uint64_t dst_capacity,
                    const uint64_t *sizes_dev, uint32_t n_ranks, uint32_t rank, void *stream);
 
+/* Flag-based assembly for contiguous shards — the S2 + S3 exchange with no collective on the
+ * data path.  board_root_dev: n_ranks entries of 32 bytes {u64 size, u64 tag, u64 done, pad}
+ * in the ROOT's memory (zero-initialised once; mapped into every rank with CUDA IPC; one
+ * board per body buffer when buffers alternate).  delta_assemble_flags (every rank, rank 0
+ * included): publishes *size_dev (this rank's body size, device) and `tag` in board[rank]
+ * with release stores, waits (acquire loads over NVLink) until board[q].tag == tag for every
+ * q < rank, then copies src_dev (16-byte aligned; rank 0: nothing, its records are extracted
+ * in place) into dst_root_dev at sum(board[q].size, q < rank) and finally sets
+ * board[rank].done = tag.  delta_assemble_flags_wait (the root): waits until every rank's
+ * done == tag, ordering the root's readers after the copies.  `tag`: the step number, > 0,
+ * the same on every rank and increasing per board.  Waits are bounded (~10 s); a peer that
+ * never arrives, or an overflowing destination, is reported by delta_assemble_wait
+ * (DELTA_ECAPACITY).  Asynchronous on `stream`. */
+int delta_assemble_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *size_dev, void *dst_root_dev,
+                         uint64_t dst_capacity, void *board_root_dev, uint32_t n_ranks, uint32_t rank,
+                         uint64_t tag, void *stream);
+int delta_assemble_flags_wait(delta_ctx *ctx, const void *board_root_dev, uint32_t n_ranks, uint64_t tag,
+                              void *stream);
+
 /* Record-granular assembly, for any tensor partition (LPT balances the
  * shards better than contiguous ranges, but then a rank's records are not one byte range of
  * the global body).  Global record order is the descriptor order of the whole list (R15).

@@ -349,6 +349,19 @@ class DeltaContext:
                                              c_void_p(sizes.data_ptr()), sizes.numel(), rank,
                                              _stream_handle(stream)))
 
+    def assemble_flags(self, src, size, dst, board, n_ranks: int, rank: int, tag: int, stream=None):
+        """delta_assemble_flags: ``size`` one-element int64 CUDA tensor (this rank's body
+        size), ``dst`` the root's body buffer and ``board`` the root's board slice
+        (int64 CUDA tensor of 4 x n_ranks), both local or IPC-mapped."""
+        self._check(self._lib.delta_assemble_flags(self._h, c_void_p(src.data_ptr() if src.numel() else 0),
+                                                   c_void_p(size.data_ptr()), c_void_p(dst.data_ptr()), dst.numel(),
+                                                   c_void_p(board.data_ptr()), n_ranks, rank, tag,
+                                                   _stream_handle(stream)))
+
+    def assemble_flags_wait(self, board, n_ranks: int, tag: int, stream=None):
+        self._check(self._lib.delta_assemble_flags_wait(self._h, c_void_p(board.data_ptr()), n_ranks, tag,
+                                                        _stream_handle(stream)))
+
     def table_dev_ptr(self) -> int:
         """Device pointer of this context's offset table (delta_table_dev): valid after an
         extract until the next one on the same context."""

@@ -920,6 +920,45 @@ extern "C" int delta_assemble(delta_ctx *ctx, const void *src, void *dst, uint64
     return DELTA_OK;
 }
 
+extern "C" int delta_assemble_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *size_dev, void *dst_root_dev,
+                                    uint64_t dst_capacity, void *board_root_dev, uint32_t n_ranks, uint32_t rank,
+                                    uint64_t tag, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!size_dev || !dst_root_dev || !board_root_dev || rank >= n_ranks || tag == 0 || (rank && !src_dev))
+        return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_flags: bad arguments");
+    if (reinterpret_cast<uintptr_t>(src_dev) % 16) return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_flags: src not 16-byte aligned");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->asm_status.p) {
+        GROW(ctx->asm_status, 16);
+        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
+    }
+    uint32_t *counter = ctx->asm_status.as<uint32_t>() + 2;  // zero-initialised, reset by the last CTA
+    CK(launch_assemble_flags(static_cast<const uint8_t *>(src_dev), reinterpret_cast<const unsigned long long *>(size_dev),
+                             static_cast<uint8_t *>(dst_root_dev), dst_capacity,
+                             static_cast<uint8_t *>(board_root_dev) + (size_t)0, rank, tag, counter,
+                             ctx->asm_status.as<uint32_t>(), ctx->assemble_ctas, s),
+       "assemble flags launch");
+    return DELTA_OK;
+}
+
+extern "C" int delta_assemble_flags_wait(delta_ctx *ctx, const void *board_root_dev, uint32_t n_ranks, uint64_t tag,
+                                         void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    if (!board_root_dev || tag == 0) return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_flags_wait: bad arguments");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->asm_status.p) {
+        GROW(ctx->asm_status, 16);
+        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
+    }
+    CK(launch_assemble_flags_wait(board_root_dev, n_ranks, tag, ctx->asm_status.as<uint32_t>(), s),
+       "assemble flags wait launch");
+    return DELTA_OK;
+}
+
 extern "C" int delta_record_sizes(delta_ctx *ctx, const delta_record_info *table_dev, uint32_t n_local,
                                   const uint32_t *gidx_dev, uint64_t *sizes_dev, uint32_t n_global, void *stream) {
     if (!ctx) return DELTA_EINVAL;

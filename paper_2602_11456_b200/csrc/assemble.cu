@@ -7,6 +7,10 @@
 //                between the size exchange and the transfer.  Records are self-contained
 //                and in list order (R4, R15): the concatenation of the rank bodies
 //                in rank order IS the body of the whole tensor list.
+//   k_assemble_flags / k_assemble_flags_wait
+//                the contiguous-shard exchange with no collective: sizes, tags and
+//                completion through flags in the root's memory (release / acquire over
+//                NVLink).
 //   k_record_sizes / k_record_offsets / k_assemble_records
 //                the same for any tensor partition (LPT): each record to its own global
 //                offset, computed on the device from the all-reduced record sizes.
@@ -148,6 +152,119 @@ k_assemble_records(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, u
         }
         for (unsigned long long b = (nv << 4) + gtid; b < rest; b += nthreads) d[head + b] = sh0[b];
     }
+}
+
+// ---------------------------------------------------------------- flag-based assembly
+// The same S2 + S3 with no collective on the data path: the root's "board" (CUDA IPC
+// mapped by every rank) holds, per buffer slot and rank, {size, tag, done}.  Each rank's
+// kernel publishes its body size with a release store, waits (acquire loads over NVLink)
+// for the tags of the lower ranks, copies its body to the offset their sizes give, and the
+// last CTA to finish publishes `done`.  The root waits for every rank's `done` with
+// k_assemble_flags_wait.  `tag` is the caller's step number (identical on all ranks,
+// strictly increasing, > 0).  Waits are bounded: a peer that never arrives sets *status.
+struct BoardEntry {
+    unsigned long long size, tag, done, pad;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// spin until *p == want (bounded: ~10 s); false on timeout
+__device__ __forceinline__ bool wait_tag(const unsigned long long *p, unsigned long long want) {
+    for (unsigned long long it = 0; it < (1ull << 26); ++it) {
+        if (ld_acquire_sys(p) == want) return true;
+        __nanosleep(128);
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(256)
+k_assemble_flags(const uint8_t *__restrict__ src, const unsigned long long *__restrict__ size_dev,
+                 uint8_t *__restrict__ dst_base, unsigned long long capacity, BoardEntry *board, uint32_t rank,
+                 unsigned long long tag, uint32_t *counter, uint32_t *status) {
+    __shared__ unsigned long long s_off, s_n;
+    __shared__ bool s_ok;
+    if (threadIdx.x == 0) {
+        const unsigned long long n = *size_dev;
+        if (blockIdx.x == 0) {  // publish this rank's size, then its tag
+            board[rank].size = n;
+            __threadfence_system();
+            st_release_sys(&board[rank].tag, tag);
+        }
+        unsigned long long off = 0;
+        bool ok = n <= capacity;  // ~0: the extract's gate was closed
+        for (uint32_t q = 0; q < rank && ok; ++q) {
+            ok = wait_tag(&board[q].tag, tag);
+            const unsigned long long sq = ok ? board[q].size : 0ull;
+            ok = ok && sq <= capacity;
+            off += ok ? sq : 0ull;
+        }
+        ok = ok && off + n <= capacity;
+        s_off = off;
+        s_n = n;
+        s_ok = ok;
+        if (!ok && blockIdx.x == 0) atomicExch(status, 1u);
+    }
+    __syncthreads();
+    if (s_ok && rank != 0) {  // rank 0's records were extracted in place at offset 0
+        const unsigned long long n = s_n;
+        uint8_t *dst = dst_base + s_off;
+        const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+        const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+        const uint32_t head = (uint32_t)min(n, (unsigned long long)((16u - ((uintptr_t)dst & 15u)) & 15u));
+        if (gtid < head) dst[gtid] = src[gtid];
+        const unsigned long long rest = n - head, nv = rest >> 4;
+        uint4 *d16 = reinterpret_cast<uint4 *>(dst + head);
+        const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+        const uint32_t q0 = head >> 2, sh = 8u * (head & 3u);
+        for (unsigned long long j = gtid; j < nv; j += nthreads) {
+            const unsigned long long q = q0 + 4 * j;
+            const uint32_t a0 = __ldg(s32 + q), a1 = __ldg(s32 + q + 1), a2 = __ldg(s32 + q + 2),
+                           a3 = __ldg(s32 + q + 3), a4 = __ldg(s32 + q + 4);
+            uint4 o;
+            o.x = __funnelshift_r(a0, a1, sh);
+            o.y = __funnelshift_r(a1, a2, sh);
+            o.z = __funnelshift_r(a2, a3, sh);
+            o.w = __funnelshift_r(a3, a4, sh);
+            d16[j] = o;
+        }
+        for (unsigned long long b = (nv << 4) + gtid; b < rest; b += nthreads) dst[head + b] = src[head + b];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {  // the last CTA publishes `done`
+        if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+            *counter = 0;
+            __threadfence_system();
+            st_release_sys(&board[rank].done, tag);
+        }
+    }
+}
+
+__global__ void k_assemble_flags_wait(const BoardEntry *board, uint32_t n_ranks, unsigned long long tag,
+                                      uint32_t *status) {
+    if (blockIdx.x || threadIdx.x) return;
+    for (uint32_t q = 0; q < n_ranks; ++q)
+        if (!wait_tag(&board[q].done, tag)) atomicExch(status, 2u);
+}
+
+cudaError_t launch_assemble_flags(const uint8_t *src, const unsigned long long *size_dev, uint8_t *dst,
+                                  unsigned long long capacity, void *board, uint32_t rank, unsigned long long tag,
+                                  uint32_t *counter, uint32_t *status, int ctas, cudaStream_t s) {
+    k_assemble_flags<<<ctas, 256, 0, s>>>(src, size_dev, dst, capacity, static_cast<BoardEntry *>(board), rank, tag,
+                                         counter, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_flags_wait(const void *board, uint32_t n_ranks, unsigned long long tag, uint32_t *status,
+                                       cudaStream_t s) {
+    k_assemble_flags_wait<<<1, 32, 0, s>>>(static_cast<const BoardEntry *>(board), n_ranks, tag, status);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_record_sizes(const RecordRow *table, uint32_t n_local, const uint32_t *gidx,

@@ -210,3 +210,54 @@ class RecordAssembler:
         self.peers = []
         dist.barrier(group=self.group)
 
+
+class FlagAssembler:
+    """S2 + S3 for contiguous shards with no collective on the data path
+    (delta_assemble_flags): rank 0 owns ``nbuf`` assembled-body buffers and one board per
+    buffer (sizes, step tags, completion flags), all shared by CUDA IPC; each step every
+    rank publishes its size and copies its body over NVLink once the lower ranks' sizes are
+    on the board, and the root waits for every rank's completion flag on its comm stream.
+    Rank 0's records are extracted in place at the head of its buffer."""
+
+    def __init__(self, ctx, capacity: int, device, group=None, root: int = 0, nbuf: int = 2):
+        assert root == 0, "the assembled body starts with rank 0's records"
+        self.ctx, self.group, self.root = ctx, group, root
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.device(device)
+        if self.rank == root:
+            self.bufs = [torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
+            self.board = torch.zeros(nbuf, self.world, 4, dtype=torch.int64, device=self.device)
+            torch.cuda.synchronize(self.device)
+            share = [reduce_tensor(b) for b in self.bufs] + [reduce_tensor(self.board)]
+        else:
+            self.bufs, share = [None] * nbuf, None
+        handles = [None] * self.world
+        dist.all_gather_object(handles, share, group=group)
+        if self.rank == root:
+            self.peers, self.pboard = list(self.bufs), self.board
+        else:
+            mapped = []
+            for fn, args in handles[root]:
+                args = list(args)
+                args[6] = self.device.index  # rebuild on this process's device (peer mapping)
+                mapped.append(fn(*args))
+            self.peers, self.pboard = mapped[:-1], mapped[-1]
+        self.buf = self.bufs[0]
+        self.tag = 0
+
+    def assemble(self, body: torch.Tensor, size, slot: int = 0, stream=None):
+        """Enqueue on ``stream``: publish + copy (+ on the root: wait for every rank).
+        ``size``: one-element int64 CUDA tensor with this rank's body size."""
+        self.tag += 1
+        stream = stream or torch.cuda.current_stream(self.device)
+        board = self.pboard[slot]
+        self.ctx.assemble_flags(body, size, self.peers[slot], board, self.world, self.rank, self.tag, stream=stream)
+        if self.rank == self.root:
+            self.ctx.assemble_flags_wait(board, self.world, self.tag, stream=stream)
+        return self.bufs[slot] if self.rank == self.root else None
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        self.peers, self.pboard = [], None
+        dist.barrier(group=self.group)
+

@@ -58,6 +58,30 @@ def main():
         ok2 = torch.equal(got2[:tot].cpu(), full_body.cpu())
         print(f"[rank0] NVLink delta_assemble: match = {ok2}", flush=True)
         ok &= ok2
+    # flag-based assembly (no collective): three steps over two buffers
+    fasm = sdist.FlagAssembler(ctx, tot + 4096, dev, nbuf=2)
+    for step in range(3):
+        slot = step % 2
+        if rank == 0 and mine:
+            bf, _ = ctx.delta_extract(mine, out=fasm.bufs[slot])
+        elif mine:
+            bf, _ = ctx.delta_extract(mine)
+        else:
+            bf = torch.empty(0, dtype=torch.uint8, device=dev)
+        sz = torch.tensor([bf.numel()], dtype=torch.int64, device=dev)
+        got4 = fasm.assemble(bf, sz, slot=slot)
+        torch.cuda.synchronize()
+        rc4 = 0
+        try:
+            ctx.assemble_wait()
+        except Exception:
+            rc4 = 1
+        if rank == 0:
+            ok4 = rc4 == 0 and torch.equal(got4[:tot].cpu(), full_body.cpu())
+            print(f"[rank0] flag assembly step {step} slot {slot}: match = {ok4}", flush=True)
+            ok &= ok4
+        ok &= rc4 == 0
+    fasm.close()
     # LPT partition + record-granular assembly (delta_record_sizes / delta_assemble_records)
     lpt = sdist.shard_lpt([s.numel for s in specs], world)[rank]
     mine_l = [(specs[k].name, pairs[k][0], pairs[k][1]) for k in lpt]
