@@ -342,7 +342,7 @@ def main():
     specs, rho, pattern, desc = workload(args)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     width = 2 if args.dtype == "bf16" else 4
-    lpt = world > 1 and args.shard == "lpt" and args.assembly == "nvlink" and args.pipeline <= 1 \
+    lpt = world > 1 and args.shard == "lpt" and args.assembly in ("nvlink", "flags") and args.pipeline <= 1 \
         and not args.sync_step
     if lpt:  # LPT: balanced shards, records assembled one by one at their global offsets
         mine = sdist.shard_lpt([s.numel for s in specs], world)[rank]
@@ -429,19 +429,20 @@ def main():
         ctx.set_profiling(True)
         size0 = ctx.delta_size(tl)
         out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
-        if world > 1 and args.assembly == "flags":
+        if world > 1 and args.assembly == "flags" and not lpt:
             tot0 = torch.tensor([size0], dtype=torch.int64, device=dev)
             dist.all_reduce(tot0)
             total0 = int(tot0.item())
             flasm = sdist.FlagAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
             if rank == 0:
                 out = flasm.buf  # rank 0's records are the head of the assembled body
-        if world > 1 and args.assembly == "nvlink":
+        if world > 1 and (args.assembly == "nvlink" or (args.assembly == "flags" and lpt)):
             tot0 = torch.tensor([size0], dtype=torch.int64, device=dev)
             dist.all_reduce(tot0)
             total0 = int(tot0.item())
             if lpt:
-                recasm = sdist.RecordAssembler(ctx, total0 + total0 // 8 + 4096, dev, mine, len(specs), nbuf=2)
+                recasm = sdist.RecordAssembler(ctx, total0 + total0 // 8 + 4096, dev, mine, len(specs), nbuf=2,
+                                               mode="flags" if args.assembly == "flags" else "nccl")
             else:
                 nvasm = sdist.NvlinkAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
                 if rank == 0:

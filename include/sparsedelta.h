@@ -268,6 +268,18 @@ int delta_assemble_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *si
 int delta_assemble_flags_wait(delta_ctx *ctx, const void *board_root_dev, uint32_t n_ranks, uint64_t tag,
                               void *stream);
 
+/* delta_assemble_records_flags — the flag-based exchange for any partition (LPT): this rank's
+ * entries of local_sizes_dev (n_global uint64 in global order, from delta_record_sizes) are
+ * stored into root_sizes_dev (the root's global-order array, n_global uint64, IPC-mapped),
+ * then board[rank].tag = tag; once every rank's tag is there, each local record j is copied
+ * from src_dev (this rank's body, records back to back in local order) to dst_root_dev at
+ * the global offset sum(root_sizes_dev[0 .. gidx_dev[j] - 1]), and board[rank].done = tag.
+ * The root waits with delta_assemble_flags_wait.  Errors as delta_assemble_flags. */
+int delta_assemble_records_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *local_sizes_dev,
+                                 const uint32_t *gidx_dev, uint32_t n_local, uint32_t n_global, void *dst_root_dev,
+                                 uint64_t dst_capacity, void *board_root_dev, uint64_t *root_sizes_dev,
+                                 uint32_t n_ranks, uint32_t rank, uint64_t tag, void *stream);
+
 /* Record-granular assembly, for any tensor partition (LPT balances the
  * shards better than contiguous ranges, but then a rank's records are not one byte range of
  * the global body).  Global record order is the descriptor order of the whole list (R15).

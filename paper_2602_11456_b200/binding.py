@@ -358,6 +358,14 @@ class DeltaContext:
                                                    c_void_p(board.data_ptr()), n_ranks, rank, tag,
                                                    _stream_handle(stream)))
 
+    def assemble_records_flags(self, src, local_sizes, gidx, dst, board, root_sizes, n_ranks: int, rank: int,
+                               tag: int, stream=None):
+        """delta_assemble_records_flags (any partition, no collective)."""
+        self._check(self._lib.delta_assemble_records_flags(
+            self._h, c_void_p(src.data_ptr() if src.numel() else 0), c_void_p(local_sizes.data_ptr()),
+            c_void_p(gidx.data_ptr()), gidx.numel(), local_sizes.numel(), c_void_p(dst.data_ptr()), dst.numel(),
+            c_void_p(board.data_ptr()), c_void_p(root_sizes.data_ptr()), n_ranks, rank, tag, _stream_handle(stream)))
+
     def assemble_flags_wait(self, board, n_ranks: int, tag: int, stream=None):
         self._check(self._lib.delta_assemble_flags_wait(self._h, c_void_p(board.data_ptr()), n_ranks, tag,
                                                         _stream_handle(stream)))

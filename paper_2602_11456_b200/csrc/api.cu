@@ -944,6 +944,33 @@ extern "C" int delta_assemble_flags(delta_ctx *ctx, const void *src_dev, const u
     return DELTA_OK;
 }
 
+extern "C" int delta_assemble_records_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *local_sizes_dev,
+                                            const uint32_t *gidx_dev, uint32_t n_local, uint32_t n_global,
+                                            void *dst_root_dev, uint64_t dst_capacity, void *board_root_dev,
+                                            uint64_t *root_sizes_dev, uint32_t n_ranks, uint32_t rank, uint64_t tag,
+                                            void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!local_sizes_dev || !dst_root_dev || !board_root_dev || !root_sizes_dev || rank >= n_ranks || tag == 0 ||
+        n_local > n_global || (n_local && (!src_dev || !gidx_dev)))
+        return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_records_flags: bad arguments");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->asm_status.p) {
+        GROW(ctx->asm_status, 16);
+        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
+    }
+    CK(launch_assemble_records_flags(static_cast<const uint8_t *>(src_dev),
+                                     reinterpret_cast<const unsigned long long *>(local_sizes_dev), gidx_dev, n_local,
+                                     n_global, static_cast<uint8_t *>(dst_root_dev), dst_capacity, board_root_dev,
+                                     reinterpret_cast<unsigned long long *>(root_sizes_dev), rank, n_ranks, tag,
+                                     ctx->asm_status.as<uint32_t>() + 2, ctx->asm_status.as<uint32_t>(),
+                                     ctx->assemble_ctas, s),
+       "assemble records flags launch");
+    return DELTA_OK;
+}
+
 extern "C" int delta_assemble_flags_wait(delta_ctx *ctx, const void *board_root_dev, uint32_t n_ranks, uint64_t tag,
                                          void *stream) {
     if (!ctx) return DELTA_EINVAL;

@@ -253,6 +253,127 @@ __global__ void k_assemble_flags_wait(const BoardEntry *board, uint32_t n_ranks,
         if (!wait_tag(&board[q].done, tag)) atomicExch(status, 2u);
 }
 
+// Record-granular variant (any partition, e.g. LPT) with the same flags: each rank stores its
+// records' sizes into the root's global-order size array (its own entries only), publishes
+// its tag, waits for every rank's tag, derives all global offsets from that array (each CTA
+// scans it in shared memory), copies its records, and the last CTA publishes `done`.
+// local_sizes: this rank's global-order array from k_record_sizes (stable per slot).
+__global__ void __launch_bounds__(256)
+k_assemble_records_flags(const uint8_t *__restrict__ src, const unsigned long long *__restrict__ local_sizes,
+                         const uint32_t *__restrict__ gidx, uint32_t n_local, uint32_t n_global,
+                         uint8_t *__restrict__ dst, unsigned long long capacity, BoardEntry *board,
+                         unsigned long long *root_sizes, uint32_t rank, uint32_t n_ranks, unsigned long long tag,
+                         uint32_t *counter, uint32_t *status) {
+    extern __shared__ unsigned long long s_dyn[];  // n_global global offsets, then n_local local
+    unsigned long long *s_goff = s_dyn, *s_loff = s_dyn + n_global;
+    __shared__ bool s_ok;
+    __shared__ unsigned long long s_w[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x == 0) {
+        for (uint32_t j = threadIdx.x; j < n_local; j += blockDim.x) root_sizes[gidx[j]] = local_sizes[gidx[j]];
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_sys(&board[rank].tag, tag);
+    }
+    if (threadIdx.x == 0) {
+        bool ok = true;
+        for (uint32_t q = 0; q < n_ranks && ok; ++q) ok = wait_tag(&board[q].tag, tag);
+        s_ok = ok;
+        if (!ok) atomicExch(status, 1u);
+    }
+    __syncthreads();
+    if (s_ok) {
+        // exclusive scans: global sizes (from the root) -> offsets; local record sizes -> offsets
+        for (int pass = 0; pass < 2; ++pass) {
+            const uint32_t n = pass ? n_local : n_global;
+            unsigned long long *out = pass ? s_loff : s_goff;
+            unsigned long long carry = 0;
+            for (uint32_t b = 0; b < n; b += blockDim.x) {
+                const uint32_t i = b + threadIdx.x;
+                unsigned long long v = 0;
+                if (i < n) v = pass ? local_sizes[gidx[i]] : *(volatile unsigned long long *)&root_sizes[i];
+                unsigned long long inc = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                if (lane == 31) s_w[warp] = inc;
+                __syncthreads();
+                unsigned long long pre = 0, tot = 0;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                    if (w < warp) pre += s_w[w];
+                    tot += s_w[w];
+                }
+                __syncthreads();
+                if (i < n) out[i] = carry + pre + inc - v;
+                carry += tot;
+            }
+            if (pass == 0 && carry > capacity) {  // incl. ~0 sizes from a closed extract gate
+                if (threadIdx.x == 0) {
+                    s_ok = false;
+                    if (blockIdx.x == 0) atomicExch(status, 1u);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (s_ok) {
+        const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+        const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+        for (uint32_t j = 0; j < n_local; ++j) {
+            const uint32_t k = gidx[j];
+            const unsigned long long n = local_sizes[k];
+            const uint8_t *sp = src + s_loff[j];
+            uint8_t *d = dst + s_goff[k];
+            const uint32_t head = (uint32_t)min(n, (unsigned long long)((16u - ((uintptr_t)d & 15u)) & 15u));
+            if (gtid < head) d[gtid] = sp[gtid];
+            const unsigned long long rest = n - head, nv = rest >> 4;
+            const uint8_t *sh0 = sp + head;
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(sh0) & ~uintptr_t(3));
+            const uint32_t sh = 8u * (uint32_t)(reinterpret_cast<uintptr_t>(sh0) & 3u);
+            uint4 *d16 = reinterpret_cast<uint4 *>(d + head);
+            for (unsigned long long v = gtid; v < nv; v += nthreads) {
+                const uint32_t *q = w + 4 * v;
+                const uint32_t a0 = __ldg(q), a1 = __ldg(q + 1), a2 = __ldg(q + 2), a3 = __ldg(q + 3), a4 = __ldg(q + 4);
+                uint4 o;
+                o.x = __funnelshift_r(a0, a1, sh);
+                o.y = __funnelshift_r(a1, a2, sh);
+                o.z = __funnelshift_r(a2, a3, sh);
+                o.w = __funnelshift_r(a3, a4, sh);
+                d16[v] = o;
+            }
+            for (unsigned long long b = (nv << 4) + gtid; b < rest; b += nthreads) d[head + b] = sh0[b];
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+            *counter = 0;
+            __threadfence_system();
+            st_release_sys(&board[rank].done, tag);
+        }
+    }
+}
+
+cudaError_t launch_assemble_records_flags(const uint8_t *src, const unsigned long long *local_sizes,
+                                          const uint32_t *gidx, uint32_t n_local, uint32_t n_global, uint8_t *dst,
+                                          unsigned long long capacity, void *board, unsigned long long *root_sizes,
+                                          uint32_t rank, uint32_t n_ranks, unsigned long long tag, uint32_t *counter,
+                                          uint32_t *status, int ctas, cudaStream_t s) {
+    const size_t smem = ((size_t)n_global + n_local) * 8;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_assemble_records_flags, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k_assemble_records_flags<<<ctas, 256, smem, s>>>(src, local_sizes, gidx, n_local, n_global, dst, capacity,
+                                                     static_cast<BoardEntry *>(board), root_sizes, rank, n_ranks, tag,
+                                                     counter, status);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_assemble_flags(const uint8_t *src, const unsigned long long *size_dev, uint8_t *dst,
                                   unsigned long long capacity, void *board, uint32_t rank, unsigned long long tag,
                                   uint32_t *counter, uint32_t *status, int ctas, cudaStream_t s) {

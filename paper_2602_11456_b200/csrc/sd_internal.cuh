@@ -175,6 +175,11 @@ cudaError_t launch_blake3(const uint8_t *in, unsigned long long n, uint32_t *ws,
 cudaError_t launch_assemble_flags(const uint8_t *src, const unsigned long long *size_dev, uint8_t *dst,
                                   unsigned long long capacity, void *board, uint32_t rank, unsigned long long tag,
                                   uint32_t *counter, uint32_t *status, int ctas, cudaStream_t s);
+cudaError_t launch_assemble_records_flags(const uint8_t *src, const unsigned long long *local_sizes,
+                                          const uint32_t *gidx, uint32_t n_local, uint32_t n_global, uint8_t *dst,
+                                          unsigned long long capacity, void *board, unsigned long long *root_sizes,
+                                          uint32_t rank, uint32_t n_ranks, unsigned long long tag, uint32_t *counter,
+                                          uint32_t *status, int ctas, cudaStream_t s);
 cudaError_t launch_assemble_flags_wait(const void *board, uint32_t n_ranks, unsigned long long tag, uint32_t *status,
                                        cudaStream_t s);
 cudaError_t launch_record_sizes(const RecordRow *table, uint32_t n_local, const uint32_t *gidx,

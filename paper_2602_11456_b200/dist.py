@@ -174,31 +174,53 @@ class RecordAssembler:
     overlaps step t+1."""
 
     def __init__(self, ctx, capacity: int, device, mine, n_global: int, group=None, root: int = 0,
-                 nbuf: int = 2):
-        self.ctx, self.group, self.root = ctx, group, root
+                 nbuf: int = 2, mode: str = "nccl"):
+        self.ctx, self.group, self.root, self.mode = ctx, group, root, mode
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.device = torch.device(device)
         self.n_global = n_global
         self.gidx = torch.tensor(list(mine), dtype=torch.int32, device=self.device)
         self.sizes = [torch.zeros(n_global, dtype=torch.int64, device=self.device) for _ in range(nbuf)]
-        self.bufs = ([torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
-                     if self.rank == root else [None] * nbuf)
+        shared = []
+        if self.rank == root:
+            self.bufs = [torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
+            shared = list(self.bufs)
+            if mode == "flags":  # boards and the global-order size arrays live on the root
+                self.board = torch.zeros(nbuf, self.world, 4, dtype=torch.int64, device=self.device)
+                self.root_sizes = torch.zeros(nbuf, n_global, dtype=torch.int64, device=self.device)
+                shared += [self.board, self.root_sizes]
+            torch.cuda.synchronize(self.device)
+        else:
+            self.bufs = [None] * nbuf
         handles = [None] * self.world
-        dist.all_gather_object(handles, [reduce_tensor(b) for b in self.bufs] if self.rank == root else None,
+        dist.all_gather_object(handles, [reduce_tensor(b) for b in shared] if self.rank == root else None,
                                group=group)
-        self.peers = list(self.bufs) if self.rank == root else []
-        if self.rank != root:
+        if self.rank == root:
+            mapped = shared
+        else:
+            mapped = []
             for fn, args in handles[root]:
                 args = list(args)
                 args[6] = self.device.index  # rebuild on this process's device (peer mapping)
-                self.peers.append(fn(*args))
+                mapped.append(fn(*args))
+        self.peers = mapped[:nbuf]
+        if mode == "flags":
+            self.pboard, self.proot_sizes = mapped[nbuf], mapped[nbuf + 1]
         self.token = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.tag = 0
 
     def record_sizes(self, table_ptr: int, slot: int = 0, stream=None):
         self.ctx.record_sizes(table_ptr, self.gidx.numel(), self.gidx, self.sizes[slot], stream=stream)
 
     def assemble(self, body: torch.Tensor, slot: int = 0, stream=None):
         stream = stream or torch.cuda.current_stream(self.device)
+        if self.mode == "flags":  # sizes, tags and completion through the root's board
+            self.tag += 1
+            self.ctx.assemble_records_flags(body, self.sizes[slot], self.gidx, self.peers[slot], self.pboard[slot],
+                                            self.proot_sizes[slot], self.world, self.rank, self.tag, stream=stream)
+            if self.rank == self.root:
+                self.ctx.assemble_flags_wait(self.pboard[slot], self.world, self.tag, stream=stream)
+            return self.bufs[slot] if self.rank == self.root else None
         with torch.cuda.stream(stream):
             dist.all_reduce(self.sizes[slot], group=self.group)
             self.ctx.assemble_records(body, self.gidx, self.sizes[slot], self.peers[slot], stream=stream)
@@ -208,6 +230,7 @@ class RecordAssembler:
     def close(self):
         torch.cuda.synchronize(self.device)
         self.peers = []
+        self.pboard = self.proot_sizes = None
         dist.barrier(group=self.group)
 
 

@@ -103,6 +103,29 @@ def main():
                   f"record assembly slot {slot}: match = {ok3}", flush=True)
             ok &= ok3
     rasm.close()
+    # LPT + record assembly through the root's board (no collective)
+    rfa = sdist.RecordAssembler(ctx, tot + 4096, dev, lpt, len(specs), mode="flags")
+    for step in range(3):
+        slot = step % 2
+        if mine_l:
+            bl, _ = ctx.delta_extract(mine_l, table="device")
+            rfa.record_sizes(ctx.table_dev_ptr(), slot=slot)
+        else:
+            bl = torch.empty(0, dtype=torch.uint8, device=dev)
+            rfa.sizes[slot].zero_()
+        got5 = rfa.assemble(bl, slot=slot)
+        torch.cuda.synchronize()
+        rc5 = 0
+        try:
+            ctx.assemble_wait()
+        except Exception:
+            rc5 = 1
+        if rank == 0:
+            ok5 = rc5 == 0 and torch.equal(got5[:tot].cpu(), full_body.cpu())
+            print(f"[rank0] LPT record flags assembly step {step} slot {slot}: match = {ok5}", flush=True)
+            ok &= ok5
+        ok &= rc5 == 0
+    rfa.close()
     if mine:
         targets = [(n, o.clone()) for n, o, _ in mine]
         ctx.delta_apply(targets, body, table=table)
