@@ -204,7 +204,7 @@ class OracleSample:
                 break
         self.sample = (f"{len(self.items)} whole tensors ({self.lanes} lanes, "
                        f"{self.scanned / 1e9:.3f} GB of old+new) of the same workload; "
-                       f"oracle.codec extract+apply, 1 thread (numpy); inputs from the shared "
+                       f"oracle.codec extract+apply (plain numpy, one thread per process); inputs from the shared "
                        f"seeded generator on {gdev}")
 
     def _one(self, item):
