@@ -825,3 +825,61 @@ def test_merge_rejects(sd):
         assert eg.value.kind == eo.value.kind, (eg.value, eo.value.kind)
         assert bool((out == 0x5A).all())
     ctx.close()
+
+
+# ------------------------------------------------------------------ option combinations
+def test_fixed_codec_with_additive_and_advance(sd):
+    """The index codec, the record mode and extract-and-advance are independent: additive
+    records with fixed-width indices match the oracle (and apply adds), and advance with
+    fixed-width indices leaves old == new with the body unchanged."""
+    from paper_2602_11456_b200 import _abi
+    tensors = []
+    for k, (n, rho) in enumerate([(1_000_003, 0.02), (70_001, 0.4), (0, 0.0)]):
+        spec = TensorSpec(f"c{k}", (n,), "matrix")
+        o, w = generate_pair(spec, k, 41, rho=rho, device=DEV, values="bits")
+        tensors.append((spec.name, o, w))
+    ctx = sd.DeltaContext(DEV)
+    ctx.set_option(_abi.DELTA_OPT_INDEX_CODEC, 2)
+    ctx.set_option(_abi.DELTA_OPT_MODE, 2)
+    body, table = ctx.delta_extract(tensors)
+    npt = [(n, [to_np(o)], [to_np(w)]) for n, o, w in tensors]
+    ref, ref_table = oracle.codec.extract(npt, mode=oracle.codec.MODE_ADDITIVE, index_codec="fixed")
+    assert_body_equal(body, ref)
+    assert [tuple(r) for r in table] == [tuple(r) for r in ref_table]
+    want = oracle.codec.apply([(n, to_np(o)) for n, o, _ in tensors], ref, 2, index_codec="fixed")
+    targets = [(n, o.clone()) for n, o, _ in tensors]
+    ctx.delta_apply(targets, body, table=table)
+    torch.cuda.synchronize()
+    for (_, t), r in zip(targets, want):
+        assert np.array_equal(to_np(t), r)
+    ctx.close()
+    ctx = sd.DeltaContext(DEV)
+    ctx.set_option(_abi.DELTA_OPT_INDEX_CODEC, 2)
+    ctx.set_option(_abi.DELTA_OPT_ADVANCE, 2)
+    ref, _ = oracle.codec.extract(npt, index_codec="fixed")
+    body, _ = ctx.delta_extract(tensors)
+    torch.cuda.synchronize()
+    assert_body_equal(body, ref)
+    for _, o, w in tensors:
+        assert_lanes_equal(o, w)
+    ctx.close()
+
+
+def test_merge_degenerate(sd):
+    """delta_merge of bodies with no change at all, of an empty tensor list, and of a body
+    with itself (idempotent replace: the merge equals the body)."""
+    x = np.arange(300, dtype=np.uint16)
+    same, _ = oracle.codec.extract([("s", [x], [x]), ("t", [x[:7]], [x[:7]])])
+    y = x.copy()
+    y[[0, 5, 299]] ^= 3
+    one, _ = oracle.codec.extract([("s", [x], [y]), ("t", [x[:7]], [x[:7]])])
+    ctx = sd.DeltaContext(DEV)
+    dev = lambda b: torch.tensor(list(b), dtype=torch.uint8, device=DEV)
+    for a, b in ((same, same), (same, one), (one, same), (one, one)):
+        got = ctx.delta_merge(dev(a), dev(b), 2)
+        torch.cuda.synchronize()
+        assert_body_equal(got, oracle.codec.merge(a, b, 2))
+    assert_body_equal(ctx.delta_merge(dev(one), dev(one), 2), one)
+    empty = torch.empty(0, dtype=torch.uint8, device=DEV)
+    assert ctx.delta_merge(empty, empty, 0).numel() == 0
+    ctx.close()
