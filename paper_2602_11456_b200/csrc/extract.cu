@@ -332,25 +332,10 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
                     else
                         *vp++ = (LT)nv;
                 };
-                if constexpr (DENSE) {  // four independent predicated stores: lane k's slot
-                    // position is the half's base + the changes below it (no pointer chain)
-                    const uint32_t hb = (uint32_t)(so - sg);
+                if constexpr (DENSE) {  // four predicated steps, no divergent loop
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t bit = 0x80u << (8 * k);
-                        if (mm & bit) {
-                            const uint32_t pos = hb + __popc(mm & (bit - 1u));
-                            const uint32_t sel = 0x22u * k + 0x10u;
-                            const uint32_t nv = prmt(na, nb, sel);
-                            sg[pos] = (uint16_t)(obase + k);
-                            if constexpr (ADDITIVE)
-                                sv[pos] = (LT)lane_combine<W>(nv & 0xFFFFu, prmt(oa, ob, sel) & 0xFFFFu, true);
-                            else
-                                sv[pos] = (LT)nv;
-                        }
-                    }
-                    so += __popc(mm);
-                    vp += __popc(mm);
+                    for (int k = 0; k < 4; ++k)
+                        if (mm & (0x80u << (8 * k))) put(k, 0x22u * k + 0x10u);
                 } else {
                     while (mm) {
                         const uint32_t b = (uint32_t)__ffs(mm) - 1;  // 8k + 7
@@ -910,7 +895,7 @@ template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     // dense slots (> kStageGapBytes entries per tile seen): predicated compaction steps
-    const bool dense = a.slot_cap > kDenseSlot;
+    const bool dense = a.slot_cap > kStageGapBytes;
     if (ev) cudaEventRecord(ev[0], s);
     const bool variant_ok = !a.advance && a.mode == 0;  // the variants implement plain replace extraction
     if (a.scan_kernel == 4 && variant_ok) {
