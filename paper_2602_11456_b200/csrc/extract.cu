@@ -23,6 +23,7 @@
 // Product code written for this library; none of it is shared with the test oracle.
 // Semantics: DESIGN.md §3 readings R1-R5, R12-R15.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "sd_device.cuh"
@@ -895,7 +896,11 @@ template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     // dense slots (> kStageGapBytes entries per tile seen): predicated compaction steps
-    const bool dense = a.slot_cap > kStageGapBytes;
+    static const int dense_env = [] {  // DELTA_K1_DENSE=0/1 overrides the choice (diagnostics)
+        const char *e = getenv("DELTA_K1_DENSE");
+        return e ? atoi(e) : -1;
+    }();
+    const bool dense = dense_env >= 0 ? dense_env == 1 : a.slot_cap > kStageGapBytes;
     if (ev) cudaEventRecord(ev[0], s);
     const bool variant_ok = !a.advance && a.mode == 0;  // the variants implement plain replace extraction
     if (a.scan_kernel == 4 && variant_ok) {
