@@ -895,12 +895,13 @@ k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__res
 template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
-    // dense slots (> kStageGapBytes entries per tile seen): predicated compaction steps
-    static const int dense_env = [] {  // DELTA_K1_DENSE=0/1 overrides the choice (diagnostics)
+    // The ffs loop beats four predicated steps per half-vector at every density measured
+    // (check 56: 10 % K1 6.46 vs 7.80 ms, 50 % 19.99 vs 24.29 ms), so the predicated
+    // (DENSE) compaction is only a diagnostic: DELTA_K1_DENSE=1.
+    static const bool dense = [] {
         const char *e = getenv("DELTA_K1_DENSE");
-        return e ? atoi(e) : -1;
+        return e != nullptr && atoi(e) == 1;
     }();
-    const bool dense = dense_env >= 0 ? dense_env == 1 : a.slot_cap > kStageGapBytes;
     if (ev) cudaEventRecord(ev[0], s);
     const bool variant_ok = !a.advance && a.mode == 0;  // the variants implement plain replace extraction
     if (a.scan_kernel == 4 && variant_ok) {
