@@ -556,17 +556,20 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
                     const unsigned long long we = min((unsigned long long)hi + 1, ws + WIN);
                     LT *gdst = w + base + ws;
                     const uint32_t nl = (uint32_t)(we - ws);
-                    if (threadIdx.x == 0) {  // entries of this window: [ibeg, iend)
-                        uint32_t l = ibeg, r = cn;
-                        while (l < r) {
-                            const uint32_t m = (l + r) >> 1;
-                            if ((unsigned long long)s_rel[m] < we) l = m + 1;
-                            else r = m;
+                    uint32_t iend = cn;  // entries of this window: [ibeg, iend); a chunk
+                    if (span > WIN) {    // whose span fits one window needs no search
+                        if (threadIdx.x == 0) {
+                            uint32_t l = ibeg, r = cn;
+                            while (l < r) {
+                                const uint32_t m = (l + r) >> 1;
+                                if ((unsigned long long)s_rel[m] < we) l = m + 1;
+                                else r = m;
+                            }
+                            s_iend = l;
                         }
-                        s_iend = l;
+                        __syncthreads();
+                        iend = s_iend;
                     }
-                    __syncthreads();
-                    const uint32_t iend = s_iend;
                     if (iend == ibeg) {  // nothing changes in this window
                         __syncthreads();
                         continue;
@@ -574,6 +577,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
                     // stage the target lanes (plain loads: the kernel writes this memory)
                     const uint4 *ga = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(gdst) & ~uintptr_t(15));
                     const uint32_t o16 = (uint32_t)(reinterpret_cast<uintptr_t>(gdst) & 15);
+#pragma unroll 4
                     for (uint32_t j = threadIdx.x; j < (o16 + nl * W + 15) / 16; j += blockDim.x)
                         reinterpret_cast<uint4 *>(s_win)[j] = ga[j];
                     __syncthreads();
