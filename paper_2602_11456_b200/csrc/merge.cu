@@ -18,8 +18,8 @@
 //                       the b head equals it (b's value wins).  Pass 1 counts the kept
 //                       entries per tile, pass 2 stages them and writes them coalesced at
 //                       the scanned offsets.
-//   M3 k_merge_bounds   record boundaries of the union; LEB128 length of every gap, their
-//                       exclusive scan, the offset table and the body size.
+//   M3 (fused into the write pass) record starts of the union and the LEB128 length of
+//                       every gap; then their exclusive scan, the offset table, body size.
 //   M4 k_merge_emit     LEB128 bytes + values per entry; k_merge_headers per record.
 //
 // Product code; shares nothing with oracle/.
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
     __shared__ unsigned long long sa[kMpTile + 1], sb[kMpTile + 1];
     __shared__ uint32_t s_src[WRITE ? kMpTile : 1];  // kept entry -> source (bit 31: from b)
     __shared__ uint32_t s_w[8];
+    __shared__ unsigned long long s_prev;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (unsigned long long t = blockIdx.x; t < m.ntiles; t += gridDim.x) {
         const unsigned long long d0 = t * kMpTile, d1 = min(d0 + kMpTile, m.ma + m.mb);
@@ -298,6 +299,15 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
                     ++j;
                 }
             }
+            if (tid == 0) {  // the union's entry just before this tile (none: ~0)
+                const unsigned long long ap = i0 > 0 ? m.ia[i0 - 1] : ~0ull;
+                const unsigned long long bp = j0 > 0 ? m.ib[j0 - 1] : ~0ull;
+                // an a-entry equal to the b head at this tile's start (sb[0]: the tile's first b
+                // or the one just past it) was dropped: its b twin comes later
+                const unsigned long long aprev =
+                    (ap != ~0ull && ap == sb[0]) ? (i0 > 1 ? m.ia[i0 - 2] : ~0ull) : ap;
+                s_prev = aprev == ~0ull ? bp : (bp == ~0ull ? aprev : max(aprev, bp));
+            }
             __syncthreads();
             const LT *va = static_cast<const LT *>(m.va), *vb = static_cast<const LT *>(m.vb);
             LT *uv = static_cast<LT *>(m.uv);
@@ -305,8 +315,18 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
             for (uint32_t x = tid; x < tot; x += blockDim.x) {
                 const uint32_t src = s_src[x], k = src & 0x7FFFFFFFu;
                 const bool fb = src >> 31;
-                m.u[base + x] = fb ? sb[k] : sa[k];
+                const unsigned long long key = fb ? sb[k] : sa[k];
+                m.u[base + x] = key;
                 uv[base + x] = fb ? vb[j0 + k] : va[i0 + k];
+                // fused M3: record start and the LEB128 length of the entry's gap
+                unsigned long long prev = s_prev;
+                if (x > 0) {
+                    const uint32_t ps = s_src[x - 1], pk = ps & 0x7FFFFFFFu;
+                    prev = (ps >> 31) ? sb[pk] : sa[pk];
+                }
+                const bool first = prev == ~0ull || (prev >> kKeyShift) != (key >> kKeyShift);
+                if (first) m.eu[key >> kKeyShift] = base + x;
+                m.len[base + x] = leb_len(first ? (key & kIdxMask) : key - prev);
             }
         }
         __syncthreads();  // shared staging reused by the next tile
@@ -314,30 +334,11 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
 }
 
 // ---------------------------------------------------------------- M3
-// record boundaries of the union: eu[k] = first position of record k (eu pre-set to ~0)
-__global__ void __launch_bounds__(256) k_merge_bounds(MergeArgs m) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < m.mu; p += stride) {
-        const unsigned long long k = m.u[p] >> kKeyShift;
-        if (p == 0 || (m.u[p - 1] >> kKeyShift) != k) m.eu[k] = p;
-    }
-}
-
 __global__ void k_merge_bounds_fill(MergeArgs m) {  // records without entries start where the next one does
     if (blockIdx.x || threadIdx.x) return;
     m.eu[m.n] = m.mu;
     for (uint32_t k = m.n; k-- > 0;)
         if (m.eu[k] == ~0ull) m.eu[k] = m.eu[k + 1];
-}
-
-// LEB128 length of every union entry's gap (first entry of a record: the index itself)
-__global__ void __launch_bounds__(256) k_merge_len(MergeArgs m) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < m.mu; p += stride) {
-        const unsigned long long k = m.u[p] >> kKeyShift, x = m.u[p] & kIdxMask;
-        const unsigned long long g = p == m.eu[k] ? x : x - (m.u[p - 1] & kIdxMask);
-        m.len[p] = leb_len(g);
-    }
 }
 
 // offset table + body size (one block)
@@ -438,16 +439,14 @@ cudaError_t launch_merge_count(const MergeArgs &m, cudaStream_t s) {
 }
 
 cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(m.eu, 0xFF, (size_t)(m.n + 1) * 8, s);  // record starts: set by the write pass
+    if (e != cudaSuccess) return e;
     if (m.ntiles) {
         const uint32_t g = (uint32_t)(m.ntiles < 148ull * 8 ? m.ntiles : 148ull * 8);
         if (m.width == 2) k_merge_path<2, true><<<g, 256, 0, s>>>(m);
         else k_merge_path<4, true><<<g, 256, 0, s>>>(m);
     }
-    cudaError_t e = cudaMemsetAsync(m.eu, 0xFF, (size_t)(m.n + 1) * 8, s);
-    if (e != cudaSuccess) return e;
-    if (m.mu) k_merge_bounds<<<grid_for(m.mu), 256, 0, s>>>(m);
     k_merge_bounds_fill<<<1, 32, 0, s>>>(m);
-    if (m.mu) k_merge_len<<<grid_for(m.mu), 256, 0, s>>>(m);
     e = scan_u32(m.len, m.mu, m.lo, m.blk, s);
     if (e != cudaSuccess) return e;
     k_merge_table<<<1, 1024, 0, s>>>(m);
