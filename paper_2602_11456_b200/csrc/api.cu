@@ -1197,32 +1197,33 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
             return fail(ctx, dst[x] <= 10 ? kDetailToStatus[dst[x]] : DELTA_ECORRUPT, (int)dst[x],
                         "delta_merge: body %c: %s", x ? 'b' : 'a', dst[x] <= 10 ? kDetailName[dst[x]] : "?");
     m.ntiles = (m.ma + m.mb + 2047) / 2048;
-    GROW(ctx->m_dup, std::max<size_t>(m.ntiles, 1) * 4);
+    const size_t mx = std::max<size_t>(m.ma + m.mb, 1);  // the union is at most a + b entries
+    GROW(ctx->m_dup, std::max<size_t>(m.ntiles, 2) * 4);
     GROW(ctx->m_ds, (m.ntiles + 1) * 8);
-    GROW(ctx->m_blk, ((std::max<size_t>(m.ntiles, m.ma + m.mb) + 4095) / 4096 + 1) * 8);
+    GROW(ctx->m_blk, ((mx + 4095) / 4096 + 1) * 8);
     GROW(ctx->m_lb, (m.ntiles + 1) * 8);
+    GROW(ctx->m_u, mx * 8);
+    GROW(ctx->m_uv, mx * w);
+    GROW(ctx->m_len, mx * 4);
+    GROW(ctx->m_lo, (mx + 1) * 8);
     m.split = ctx->m_lb.as<unsigned long long>();
     m.tile_cnt = ctx->m_dup.as<uint32_t>();
     m.tile_off = ctx->m_ds.as<unsigned long long>();
     m.blk = ctx->m_blk.as<unsigned long long>();
-    CK(launch_merge_count(m, s), "merge count");
-    CK(cudaMemcpyAsync(&h[2], m.tile_off + m.ntiles, 8, cudaMemcpyDeviceToHost, s), "readback");
-    CK(cudaStreamSynchronize(s), "merge count");
-    mt.mark("merge-path count");
-    m.mu = h[2];
-    GROW(ctx->m_u, std::max<size_t>(m.mu, 1) * 8);
-    GROW(ctx->m_uv, std::max<size_t>(m.mu, 1) * w);
-    GROW(ctx->m_len, std::max<size_t>(m.mu, 1) * 4);
-    GROW(ctx->m_lo, (m.mu + 1) * 8);
     m.u = ctx->m_u.as<unsigned long long>();
     m.uv = ctx->m_uv.p;
     m.len = ctx->m_len.as<uint32_t>();
     m.lo = ctx->m_lo.as<unsigned long long>();
+    CK(launch_merge_count(m, s), "merge path");
+    CK(cudaMemcpyAsync(&h[2], m.tile_off + m.ntiles, 8, cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaStreamSynchronize(s), "merge path");
+    mt.mark("merge path (one pass, look-back offsets)");
+    m.mu = m.ntiles ? h[2] : 0;
     CK(launch_merge_place(m, s), "merge place");
     unsigned long long size = 0;
     CK(cudaMemcpyAsync(&size, m.body_size, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaStreamSynchronize(s), "merge place");
-    mt.mark("merge-path write + bounds/len/scan/table");
+    mt.mark("scan of lengths + table");
     *out_bytes = size;
     if (size > out_capacity)
         return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < merged body size %llu",

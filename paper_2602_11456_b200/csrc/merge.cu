@@ -245,8 +245,18 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
     __shared__ uint32_t s_src[WRITE ? kMpTile : 1];  // kept entry -> source (bit 31: from b)
     __shared__ uint32_t s_w[8];
     __shared__ unsigned long long s_prev;
+    __shared__ unsigned long long s_t, s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (unsigned long long t = blockIdx.x; t < m.ntiles; t += gridDim.x) {
+    // WRITE: one pass — tiles are claimed in order from a ticket and each finds its output
+    // offset by decoupled look-back over its predecessors' published counts (tile_off is
+    // the status array, zeroed: flag 1 = the tile's own count, 2 = inclusive prefix)
+    for (unsigned long long t0 = blockIdx.x;; t0 += gridDim.x) {
+        if constexpr (WRITE) {
+            if (tid == 0) s_t = atomicAdd(reinterpret_cast<unsigned long long *>(m.tile_cnt), 1ull);
+            __syncthreads();
+        }
+        const unsigned long long t = WRITE ? s_t : t0;
+        if (t >= m.ntiles) break;
         const unsigned long long d0 = t * kMpTile, d1 = min(d0 + kMpTile, m.ma + m.mb);
         const unsigned long long i0 = m.split[t], j0 = d0 - i0;
         const uint32_t na = (uint32_t)(m.split[t + 1] - i0), nb = (uint32_t)(d1 - m.split[t + 1] - j0);
@@ -288,6 +298,25 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
         if constexpr (!WRITE) {
             if (tid == 0) m.tile_cnt[t] = tot;
         } else {
+            if (tid == 0) {
+                constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
+                unsigned long long excl = 0;
+                if (t == 0) {
+                    st_release_u64(m.tile_off, kInc | tot);
+                } else {
+                    st_release_u64(m.tile_off + t, kAgg | tot);
+                    for (unsigned long long q = t - 1;; --q) {
+                        unsigned long long v;
+                        while (((v = ld_acquire_u64(m.tile_off + q)) >> 62) == 0) {
+                        }
+                        excl += v & kVal;
+                        if ((v >> 62) == 2) break;
+                    }
+                    st_release_u64(m.tile_off + t, kInc | (excl + tot));
+                }
+                if (t == m.ntiles - 1) m.tile_off[m.ntiles] = excl + tot;  // the union's size
+                s_base = excl;
+            }
             uint32_t q = pre + inc - keep;
             uint32_t i = i_start, j = e0 - i_start;
             for (uint32_t e = e0; e < e1; ++e) {
@@ -311,7 +340,7 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
             __syncthreads();
             const LT *va = static_cast<const LT *>(m.va), *vb = static_cast<const LT *>(m.vb);
             LT *uv = static_cast<LT *>(m.uv);
-            const unsigned long long base = m.tile_off[t];
+            const unsigned long long base = s_base;
             for (uint32_t x = tid; x < tot; x += blockDim.x) {
                 const uint32_t src = s_src[x], k = src & 0x7FFFFFFFu;
                 const bool fb = src >> 31;
@@ -429,25 +458,24 @@ cudaError_t launch_merge_walk(const MergeArgs &m, cudaStream_t s) {
 }
 
 cudaError_t launch_merge_count(const MergeArgs &m, cudaStream_t s) {
+    // splits, then the single merge-path pass (look-back offsets); tile_off[ntiles] = the
+    // union's size.  tile_cnt[0..1] is the tile ticket, tile_off the look-back status.
     k_merge_splits<<<(uint32_t)((m.ntiles + 1 + 255) / 256), 256, 0, s>>>(m);
-    if (m.ntiles) {
-        const uint32_t g = (uint32_t)(m.ntiles < 148ull * 8 ? m.ntiles : 148ull * 8);
-        if (m.width == 2) k_merge_path<2, false><<<g, 256, 0, s>>>(m);
-        else k_merge_path<4, false><<<g, 256, 0, s>>>(m);
-    }
-    return scan_u32(m.tile_cnt, m.ntiles, m.tile_off, m.blk, s);
-}
-
-cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(m.eu, 0xFF, (size_t)(m.n + 1) * 8, s);  // record starts: set by the write pass
+    cudaError_t e = cudaMemsetAsync(m.tile_off, 0, (size_t)(m.ntiles + 1) * 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(m.tile_cnt, 0, 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(m.eu, 0xFF, (size_t)(m.n + 1) * 8, s);  // record starts
     if (e != cudaSuccess) return e;
     if (m.ntiles) {
         const uint32_t g = (uint32_t)(m.ntiles < 148ull * 8 ? m.ntiles : 148ull * 8);
         if (m.width == 2) k_merge_path<2, true><<<g, 256, 0, s>>>(m);
         else k_merge_path<4, true><<<g, 256, 0, s>>>(m);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s) {
     k_merge_bounds_fill<<<1, 32, 0, s>>>(m);
-    e = scan_u32(m.len, m.mu, m.lo, m.blk, s);
+    cudaError_t e = scan_u32(m.len, m.mu, m.lo, m.blk, s);
     if (e != cudaSuccess) return e;
     k_merge_table<<<1, 1024, 0, s>>>(m);
     return cudaGetLastError();
