@@ -87,7 +87,7 @@ struct delta_ctx {
     uint32_t *h_asm = nullptr;  // pinned
     ApplyState *h_state = nullptr;  // pinned
     // ---- delta_merge workspace
-    DevBuf m_ha, m_hb, m_targets, m_name_len, m_name_off, m_numel, m_ea, m_eb, m_eu, m_status, m_ia, m_ib, m_va, m_vb, m_lb,
+    DevBuf m_bstat, m_ha, m_hb, m_targets, m_name_len, m_name_off, m_numel, m_ea, m_eb, m_eu, m_status, m_ia, m_ib, m_va, m_vb, m_lb,
         m_dup, m_ds, m_u, m_uv, m_len, m_lo, m_blk, m_table, m_size;
     // pinned staging ring for the per-call apply uploads (targets, hint, names): with a
     // pinned source cudaMemcpyAsync does not wait for earlier work on the stream, so
@@ -190,7 +190,7 @@ void delta_ctx_destroy(delta_ctx *c) {
     if (c && c->ev_extract) cudaEventDestroy(c->ev_extract);
     if (!c) return;
     cudaSetDevice(c->device);
-    DevBuf *mbufs[] = {&c->m_ha, &c->m_hb, &c->m_targets, &c->m_name_len, &c->m_name_off, &c->m_numel, &c->m_ea, &c->m_eb, &c->m_eu,
+    DevBuf *mbufs[] = {&c->m_bstat, &c->m_ha, &c->m_hb, &c->m_targets, &c->m_name_len, &c->m_name_off, &c->m_numel, &c->m_ea, &c->m_eb, &c->m_eu,
                        &c->m_status, &c->m_ia, &c->m_ib, &c->m_va, &c->m_vb, &c->m_lb, &c->m_dup, &c->m_ds,
                        &c->m_u, &c->m_uv, &c->m_len, &c->m_lo, &c->m_blk, &c->m_table, &c->m_size};
     for (DevBuf *b : mbufs) b->release();
@@ -1202,6 +1202,8 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     GROW(ctx->m_ds, (m.ntiles + 1) * 8);
     GROW(ctx->m_blk, ((mx + 4095) / 4096 + 1) * 8);
     GROW(ctx->m_lb, (m.ntiles + 1) * 8);
+    GROW(ctx->m_bstat, (m.ntiles + 1) * 8);
+    m.bstat = ctx->m_bstat.as<unsigned long long>();
     GROW(ctx->m_u, mx * 8);
     GROW(ctx->m_uv, mx * w);
     GROW(ctx->m_len, mx * 4);
@@ -1223,7 +1225,7 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
     unsigned long long size = 0;
     CK(cudaMemcpyAsync(&size, m.body_size, 8, cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaStreamSynchronize(s), "merge place");
-    mt.mark("scan of lengths + table");
+    mt.mark("record bounds + table");
     *out_bytes = size;
     if (size > out_capacity)
         return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < merged body size %llu",

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
     __shared__ uint32_t s_src[WRITE ? kMpTile : 1];  // kept entry -> source (bit 31: from b)
     __shared__ uint32_t s_w[8];
     __shared__ unsigned long long s_prev;
-    __shared__ unsigned long long s_t, s_base;
+    __shared__ unsigned long long s_t, s_base, s_bbase;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // WRITE: one pass — tiles are claimed in order from a ticket and each finds its output
     // offset by decoupled look-back over its predecessors' published counts (tile_off is
@@ -341,7 +341,12 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
             const LT *va = static_cast<const LT *>(m.va), *vb = static_cast<const LT *>(m.vb);
             LT *uv = static_cast<LT *>(m.uv);
             const unsigned long long base = s_base;
-            for (uint32_t x = tid; x < tot; x += blockDim.x) {
+            uint32_t lens[kMpTile / 256];
+#pragma unroll
+            for (int r = 0; r < kMpTile / 256; ++r) {
+                const uint32_t x = tid + 256u * r;
+                lens[r] = 0;
+                if (x >= tot) continue;
                 const uint32_t src = s_src[x], k = src & 0x7FFFFFFFu;
                 const bool fb = src >> 31;
                 const unsigned long long key = fb ? sb[k] : sa[k];
@@ -355,8 +360,59 @@ __global__ void __launch_bounds__(256) k_merge_path(MergeArgs m) {
                 }
                 const bool first = prev == ~0ull || (prev >> kKeyShift) != (key >> kKeyShift);
                 if (first) m.eu[key >> kKeyShift] = base + x;
-                m.len[base + x] = leb_len(first ? (key & kIdxMask) : key - prev);
+                lens[r] = leb_len(first ? (key & kIdxMask) : key - prev);
             }
+            // the entries' byte offsets: block scan of the lengths (in sa's space, free now)
+            // plus the tile's byte base from a second look-back; no separate scan pass
+            __syncthreads();
+            uint32_t *sl = reinterpret_cast<uint32_t *>(sa);
+#pragma unroll
+            for (int r = 0; r < kMpTile / 256; ++r) sl[tid + 256u * r] = lens[r];
+            __syncthreads();
+            uint32_t loc[8], run = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                loc[e] = run;
+                run += sl[tid * 8 + e];
+            }
+            uint32_t binc = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, binc, o);
+                if (lane >= o) binc += y;
+            }
+            __syncthreads();
+            if (lane == 31) s_w[warp] = binc;
+            __syncthreads();
+            uint32_t bpre = 0, btot = 0;
+            for (int w = 0; w < 8; ++w) {
+                if (w < warp) bpre += s_w[w];
+                btot += s_w[w];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) sl[tid * 8 + e] = bpre + binc - run + loc[e];
+            if (tid == 0) {
+                constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
+                unsigned long long excl = 0;
+                if (t == 0) {
+                    st_release_u64(m.bstat, kInc | btot);
+                } else {
+                    st_release_u64(m.bstat + t, kAgg | btot);
+                    for (unsigned long long q = t - 1;; --q) {
+                        unsigned long long v;
+                        while (((v = ld_acquire_u64(m.bstat + q)) >> 62) == 0) {
+                        }
+                        excl += v & kVal;
+                        if ((v >> 62) == 2) break;
+                    }
+                    st_release_u64(m.bstat + t, kInc | (excl + btot));
+                }
+                if (t == m.ntiles - 1) m.lo[base + tot] = excl + btot;  // lo[union size] = total bytes
+                s_bbase = excl;
+            }
+            __syncthreads();
+            const unsigned long long bbase = s_bbase;
+            for (uint32_t x = tid; x < tot; x += blockDim.x) m.lo[base + x] = bbase + sl[x];
         }
         __syncthreads();  // shared staging reused by the next tile
     }
@@ -412,7 +468,7 @@ __global__ void __launch_bounds__(256) k_merge_emit(MergeArgs m, uint8_t *__rest
         const unsigned long long e0 = m.eu[k];
         unsigned long long g = p == e0 ? x : x - (m.u[p - 1] & kIdxMask);
         uint8_t *q = out + r.index_offset + (m.lo[p] - m.lo[e0]);
-        const uint32_t L = m.len[p];
+        const uint32_t L = leb_len(g);
         for (uint32_t j = 0; j + 1 < L; ++j) {
             q[j] = (uint8_t)(g | 0x80);
             g >>= 7;
@@ -462,6 +518,7 @@ cudaError_t launch_merge_count(const MergeArgs &m, cudaStream_t s) {
     // union's size.  tile_cnt[0..1] is the tile ticket, tile_off the look-back status.
     k_merge_splits<<<(uint32_t)((m.ntiles + 1 + 255) / 256), 256, 0, s>>>(m);
     cudaError_t e = cudaMemsetAsync(m.tile_off, 0, (size_t)(m.ntiles + 1) * 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(m.bstat, 0, (size_t)(m.ntiles + 1) * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(m.tile_cnt, 0, 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(m.eu, 0xFF, (size_t)(m.n + 1) * 8, s);  // record starts
     if (e != cudaSuccess) return e;
@@ -474,9 +531,11 @@ cudaError_t launch_merge_count(const MergeArgs &m, cudaStream_t s) {
 }
 
 cudaError_t launch_merge_place(const MergeArgs &m, cudaStream_t s) {
+    if (m.mu == 0) {  // no entry at all: lo[0] = 0 bytes
+        cudaError_t e = cudaMemsetAsync(m.lo, 0, 8, s);
+        if (e != cudaSuccess) return e;
+    }
     k_merge_bounds_fill<<<1, 32, 0, s>>>(m);
-    cudaError_t e = scan_u32(m.len, m.mu, m.lo, m.blk, s);
-    if (e != cudaSuccess) return e;
     k_merge_table<<<1, 1024, 0, s>>>(m);
     return cudaGetLastError();
 }

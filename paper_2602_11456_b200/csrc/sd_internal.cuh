@@ -220,6 +220,7 @@ struct MergeArgs {
     unsigned long long *tile_off;         // tiles + 1: exclusive scan of tile_cnt
     unsigned long long ntiles;
     unsigned long long *split;            // ntiles + 1: a-entries before each tile boundary
+    unsigned long long *bstat;            // ntiles + 1: look-back status of the tiles' LEB128 bytes
     unsigned long long *u;                // mu merged keys
     void *uv;                             // mu merged values
     uint32_t *len;                        // mu LEB128 lengths
