@@ -15,11 +15,12 @@
 //                       splits by one binary search per boundary (k_merge_splits, all in
 //                       parallel), tiles staged in shared memory, 8 positions per thread (a
 //                       second binary search in shared memory); an a-entry is dropped when
-//                       the b head equals it (b's value wins).  Pass 1 counts the kept
-//                       entries per tile, pass 2 stages them and writes them coalesced at
-//                       the scanned offsets.
-//   M3 (fused into the write pass) record starts of the union and the LEB128 length of
-//                       every gap; then their exclusive scan, the offset table, body size.
+//                       the b head equals it (b's value wins).  One pass: tiles are
+//                       claimed in order from a ticket; each finds the offset of its kept
+//                       entries and of their LEB128 bytes by decoupled look-back over its
+//                       predecessors, marks record starts and writes keys, values and byte
+//                       offsets coalesced (via shared memory).
+//   M3 k_merge_bounds_fill / k_merge_table: empty records, the offset table, body size.
 //   M4 k_merge_emit     LEB128 bytes + values per entry; k_merge_headers per record.
 //
 // Product code; shares nothing with oracle/.
