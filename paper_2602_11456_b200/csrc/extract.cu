@@ -338,15 +338,13 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
                     for (int k = 0; k < 4; ++k)
                         if (mm & (0x80u << (8 * k))) put(k, 0x22u * k + 0x10u);
                 } else {
-                    // highest change first (FLO, no bit reverse) into descending slot
-                    // positions: 32-bit indices off the slot bases, no pointer chains
-                    uint32_t pos = (uint32_t)(so - sg) + __popc(mm);
+                    // 32-bit slot indices off the slot bases (no 64-bit pointer chains)
+                    uint32_t pos = (uint32_t)(so - sg);
                     so += __popc(mm);
                     vp += __popc(mm);
                     while (mm) {
-                        const uint32_t b = 31u - __clz(mm);  // 8k + 7
-                        mm ^= 1u << b;
-                        --pos;
+                        const uint32_t b = (uint32_t)__ffs(mm) - 1;  // 8k + 7
+                        mm &= mm - 1;
                         const uint32_t k = b >> 3;
                         const uint32_t sel = __funnelshift_r(0x76543210u, 0u, b - 7);
                         const uint32_t nv = prmt(na, nb, sel);
@@ -355,6 +353,7 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
                             sv[pos] = (LT)lane_combine<W>(nv & 0xFFFFu, prmt(oa, ob, sel) & 0xFFFFu, true);
                         else
                             sv[pos] = (LT)nv;
+                        ++pos;
                     }
                 }
             }
