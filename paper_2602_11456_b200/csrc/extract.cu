@@ -359,14 +359,16 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
             }
         } else {
             uint32_t mm = m[r];
+            uint32_t pos = (uint32_t)(so - sg);  // 32-bit slot indices (no pointer chains)
             while (mm) {
                 const int j = __ffs(mm) - 1;
                 mm &= mm - 1;
-                *so++ = (uint16_t)((r * THREADS + tid) * LPV + j);
+                sg[pos] = (uint16_t)((r * THREADS + tid) * LPV + j);
                 if constexpr (ADDITIVE)
-                    *vp++ = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
+                    sv[pos] = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
                 else
-                    *vp++ = (LT)lane_of<W>(vn[r], j);
+                    sv[pos] = (LT)lane_of<W>(vn[r], j);
+                ++pos;
             }
         }
     }
