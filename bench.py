@@ -273,6 +273,39 @@ def ops_view(k, lanes, width, nnz, idx_bytes, body, peak, value, scanned_total, 
                            "scanned_frac_of_measured_peak": round(value / peak, 4)}}
 
 
+def host_info() -> dict:
+    """CPU model, logical CPUs, affinity and RAM of the host the oracle ran on."""
+    info = {"cpu_count": os.cpu_count(), "affinity": host_cores()}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                info["ram_gb"] = round(int(ln.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return info
+
+
+def brute_m1(smp) -> dict:
+    """oracle.brute (pure Python, per element / per byte) extract + apply of the M1 tensor,
+    one thread; GB/s of old+new scanned."""
+    import oracle
+    name, on, wn = smp.items[0]
+    old, new = on.tolist(), wn.tolist()
+    t0 = time.perf_counter()
+    body, _ = oracle.brute.extract([(name, [old], [new])], on.dtype.itemsize)
+    got = oracle.brute.apply([(name, old)], body, on.dtype.itemsize)[0]
+    secs = time.perf_counter() - t0
+    if got != new:
+        raise SystemExit("brute-force oracle round trip mismatch")
+    return {"value": round(2 * len(old) * on.dtype.itemsize / secs / 1e9, 5), "unit": "GB/s", "cores": 1,
+            "seconds": round(secs, 2), "kind": "oracle.brute (pure Python)"}
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -308,7 +341,8 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": desc, "config": args.config, "rho": rho,
                                         "pattern": pattern},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
-                         "sample": smp.sample + f"; {cores} worker processes (one tensor per task)"},
+                         "sample": smp.sample + f"; {cores} worker processes (one tensor per task)",
+                         "host": host_info()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -697,7 +731,10 @@ def main():
         result["cpu_baseline"] = {"value": round(vp, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
                                   "sample": smp.sample + f"; {cores} worker processes (one tensor per task)",
                                   "seconds": round(secsp, 2), "host_cpus": os.cpu_count(),
-                                  "single_core": {"value": round(v1, 4), "seconds": round(secs1, 2)}}
+                                  "single_core": {"value": round(v1, 4), "seconds": round(secs1, 2)},
+                                  "host": host_info()}
+        if args.config == "M1":  # the pure-Python definition on configs[0]
+            result["cpu_baseline"]["brute_force"] = brute_m1(smp)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if nvasm is not None:  # drop the CUDA IPC mapping of rank 0's buffer before rank 0 exits
