@@ -728,8 +728,11 @@ def main():
         v1, secs1 = smp.run()
         cores = host_cores()
         vp, secsp = smp.run(cores) if cores > 1 else (v1, secs1)
+        if vp < v1:  # e.g. a single-tensor sample: the pool cannot help, report one core
+            vp, secsp, cores = v1, secs1, 1
         result["cpu_baseline"] = {"value": round(vp, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
-                                  "sample": smp.sample + f"; {cores} worker processes (one tensor per task)",
+                                  "sample": smp.sample + (f"; {cores} worker processes (one tensor per task)"
+                                                          if cores > 1 else "; one process"),
                                   "seconds": round(secsp, 2), "host_cpus": os.cpu_count(),
                                   "single_core": {"value": round(v1, 4), "seconds": round(secs1, 2)},
                                   "host": host_info()}
