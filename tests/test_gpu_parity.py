@@ -883,3 +883,29 @@ def test_merge_degenerate(sd):
     empty = torch.empty(0, dtype=torch.uint8, device=DEV)
     assert ctx.delta_merge(empty, empty, 0).numel() == 0
     ctx.close()
+
+
+def test_pipelined_round_trips_and_accumulated_timing(sd):
+    """round_trip(wait=False) back to back (the host never waits between steps) ends in the
+    same state as waited steps, and profiling mode 2 accumulates every step's kernel times
+    (delta_timing_totals) without host synchronisation."""
+    spec = m1_specs()[0]
+    o, w = generate_pair(spec, 0, 5, rho=0.01, device=DEV)
+    ref_body, _ = oracle_extract([(spec.name, o, w)])
+    ctx = sd.DeltaContext(DEV)
+    tl = sd.TensorList([(spec.name, o, w)])
+    target = o.clone()
+    tg = sd.TargetList([(spec.name, target)])
+    out = torch.empty(len(ref_body) * 2 + 4096, dtype=torch.uint8, device=DEV)
+    size = torch.zeros(1, dtype=torch.int64, device=DEV)
+    assert ctx.round_trip(tl, tg, out, size) == len(ref_body)  # first call sizes the workspace
+    ctx.set_profiling(2)
+    for _ in range(5):
+        assert ctx.round_trip(tl, tg, out, size, wait=False) is None
+    assert ctx.extract_wait() == len(ref_body)
+    ctx.apply_wait()
+    tot, calls = ctx.timing_totals()
+    assert calls == 5 and tot["scan_ms"] > 0 and tot["scatter_ms"] > 0
+    assert_body_equal(out[:len(ref_body)], ref_body)
+    assert_lanes_equal(target, w)
+    ctx.close()
