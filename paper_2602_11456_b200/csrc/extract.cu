@@ -775,8 +775,11 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
 // (differences of the slot's u16 lane offsets, < 2^14: one or two bytes each) encoded 32 at
 // a time — byte positions from a ballot of the two-byte ones — and the raw values copied
 // to their final offsets in the body.
-template <int W, bool FIXED>
-__global__ void __launch_bounds__(256, 8)
+// BATCHED (chosen on the host when some tile has > 1024 changes): every tile's gaps in
+// batches of 256 with the offsets loaded up front; 40 registers at 6 CTAs per SM, where
+// the sparse variant keeps 32 registers at 8 CTAs per SM.
+template <int W, bool FIXED, bool BATCHED = false>
+__global__ void __launch_bounds__(256, BATCHED ? 6 : 8)
 k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
@@ -824,6 +827,42 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
         const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
         uint8_t *p = ib + L0;
         const uint32_t c = e.count;
+        if constexpr (BATCHED) {  // dense regime: the values first, then batches of 256 gaps
+            warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
+            uint32_t last = 0;  // offset of the entry before the batch
+            for (uint32_t b0 = 0; b0 < c; b0 += 256) {
+                uint32_t o[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const uint32_t i = b0 + r * 32 + lane;
+                    o[r] = i < c ? (uint32_t)so[i] : 0u;
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    if (b0 + (uint32_t)r * 32u >= c) break;
+                    const uint32_t i = b0 + r * 32 + lane;
+                    uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
+                    const uint32_t carry = r ? __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31) : last;
+                    if (lane == 0) prev = carry;
+                    const bool act = i >= 1 && i < c;
+                    const uint32_t gi = act ? o[r] - prev : 0u;
+                    const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
+                    const uint32_t skip = (b0 == 0 && r == 0) ? 1u : 0u;  // entry 0 has no in-tile gap
+                    if (act) {
+                        uint8_t *q = p + (lane - skip) + __popc(two & lt_mask);
+                        if (gi < 128u) {
+                            q[0] = (uint8_t)gi;
+                        } else {
+                            q[0] = (uint8_t)(gi | 0x80u);
+                            q[1] = (uint8_t)(gi >> 7);
+                        }
+                    }
+                    p += min(32u, c - b0 - r * 32u) - skip + __popc(two);
+                }
+                last = __shfl_sync(0xffffffffu, o[7], 31);
+            }
+            continue;
+        }
         if (c <= 256) {  // ~all tiles up to a few % density: every load of the tile issued up front
             uint32_t o[8];
 #pragma unroll
@@ -964,8 +1003,18 @@ template <int W>
 static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
-    (a.index_codec ? k_emit_tiles<W, true> : k_emit_tiles<W, false>)<<<a.persist_ctas, 256, 0, s>>>(
-        a.plan, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<const LT *>(a.slot_val), out, a.summary, a.out_cap);
+    if (a.index_codec)
+        k_emit_tiles<W, true><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
+                                                            static_cast<const LT *>(a.slot_val), out, a.summary,
+                                                            a.out_cap);
+    else if (a.slot_cap > kDenseEmitSlot)  // some tile has > kDenseEmitSlot changes
+        k_emit_tiles<W, false, true><<<a.sm_count * 6, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
+                                                                   static_cast<const LT *>(a.slot_val), out,
+                                                                   a.summary, a.out_cap);
+    else
+        k_emit_tiles<W, false><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
+                                                             static_cast<const LT *>(a.slot_val), out, a.summary,
+                                                             a.out_cap);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
     k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode, a.summary,
