@@ -465,8 +465,24 @@ k_tiles_gaps(TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t slot_cap,
                 if (lane == 0) prev = carry;
                 big += (i >= 1 && i < c && o[r] - prev >= 128u);
             }
-        } else {
-            for (uint32_t i = 1 + lane; i < c; i += 32) big += (uint32_t)(so[i] - so[i - 1]) >= 128u;
+        } else {  // dense tile: 8 consecutive offsets per lane (one 16-byte load; slots hold a
+                  // power of two >= 512 entries, so the load stays inside), 256 per round
+            uint32_t carry = 0;
+            for (uint32_t b = 0; b < c; b += 256) {
+                const uint32_t i0 = b + 8 * lane;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (i0 < c) v = *reinterpret_cast<const uint4 *>(so + i0);
+                const uint32_t o[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                                       v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+                uint32_t prev = __shfl_up_sync(0xffffffffu, o[7], 1);
+                if (lane == 0) prev = carry;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t i = i0 + k;
+                    big += (i >= 1 && i < c && o[k] - (k ? o[k - 1] : prev) >= 128u);
+                }
+                carry = __shfl_sync(0xffffffffu, o[7], 31);
+            }
         }
         big = __reduce_add_sync(0xffffffffu, big);
         if (lane == 0) {
