@@ -437,6 +437,9 @@ k_scan_tiles_persist(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32
 // One warp per tile over the u16 lane offsets K1 left in the slot: the tile's first and
 // last change offsets and the LEB128 bytes of its internal gaps (each gap < 2^14 lanes:
 // 1 byte if < 128, else 2), i.e. (count - 1) + #{gaps >= 128}.
+// DENSE (chosen on the host when some tile has > 1024 changes): dense tiles read 8
+// consecutive offsets per lane; the sparse variant keeps its lean register budget.
+template <bool DENSE>
 __global__ void __launch_bounds__(256)
 k_tiles_gaps(TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const ExtractSummary *summary) {
@@ -465,6 +468,8 @@ k_tiles_gaps(TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t slot_cap,
                 if (lane == 0) prev = carry;
                 big += (i >= 1 && i < c && o[r] - prev >= 128u);
             }
+        } else if constexpr (!DENSE) {
+            for (uint32_t i = 1 + lane; i < c; i += 32) big += (uint32_t)(so[i] - so[i - 1]) >= 128u;
         } else {  // dense tile: 8 consecutive offsets per lane (one 16-byte load; slots hold a
                   // power of two >= 512 entries, so the load stays inside), 256 per round
             uint32_t carry = 0;
@@ -990,7 +995,8 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     }
     if (ev) cudaEventRecord(ev[1], s);
     if (!a.index_codec)  // the fixed-width codec needs no gap statistics
-        k_tiles_gaps<<<a.persist_ctas, 256, 0, s>>>(a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
+        (a.slot_cap > kDenseEmitSlot ? k_tiles_gaps<true> : k_tiles_gaps<false>)<<<a.persist_ctas, 256, 0, s>>>(
+            a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
     k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);
