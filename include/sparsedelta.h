@@ -363,7 +363,7 @@ enum {
                                         5 = as 1, persistent (3 CTAs per SM loop over tiles).
                                         2 and 3 (TMA pipeline, 128-byte runs) were measured slower
                                         and retired: DELTA_EINVAL */
-    DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 4) */
+    DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 5: one full wave at its shared-memory limit) */
     DELTA_OPT_PREFETCH_TILES = 5,     /* 1 + distance, in tiles, of the L2 bulk prefetch issued by
                                          the default compare kernel (1 = off; default: one wave of
                                          resident tiles, 3 x SMs) */
