@@ -349,57 +349,22 @@ __device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cn
 }
 
 // ------------------------------------------------------------------------------ A2
-// Asynchronous form of stage_chunk (cp.async 16-byte copies into shared memory, one
-// commit group): A2 stages the next chunk while it validates the current one.
-__device__ __forceinline__ ChunkView stage_chunk_async(const uint8_t *body, const ApplyRec &R,
-                                                       unsigned long long j, uint8_t *buf) {
-    ChunkView v;
-    v.cs = j * kByteChunk;
-    const unsigned long long ce = min(R.idx_len, v.cs + kByteChunk);
-    v.len = (uint32_t)(ce - v.cs);
-    v.last = (ce == R.idx_len);
-    const uint32_t hs = (uint32_t)min(v.cs, (unsigned long long)kHalo);
-    const uint8_t *src = body + R.idx_off + v.cs - hs;
-    const uint4 *a = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-    const uint32_t o = (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15);
-    const uint32_t nv = (o + hs + v.len + 15) / 16;
-    for (uint32_t q = threadIdx.x; q < nv; q += blockDim.x) {
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + 16 * q);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a + q) : "memory");
-    }
-    v.b = buf + o + hs;
-    return v;
-}
-
-__global__ void __launch_bounds__(256, 8)
+__global__ void __launch_bounds__(256)
 k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
                const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
                unsigned int *__restrict__ chunk_count,
                unsigned long long *__restrict__ chunk_sum, ApplyState *st) {
     if (st->status != kOk) return;
     const unsigned long long nch = st->n_chunks;
-    __shared__ __align__(16) uint8_t sb[2][kStageBytes];
+    __shared__ __align__(16) uint8_t sb[kStageBytes];
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int cur = 0;
-    ChunkView vn{};
-    if (blockIdx.x < nch) {
-        const uint32_t k = __ldg(chunk_rec + blockIdx.x);
-        vn = stage_chunk_async(body, recs[k], blockIdx.x - __ldg(rcb + k), sb[0]);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
-        const ChunkView v = vn;
-        const unsigned long long cn = c + gridDim.x;  // stage the next chunk into the other buffer
-        if (cn < nch) {
-            const uint32_t k = __ldg(chunk_rec + cn);
-            vn = stage_chunk_async(body, recs[k], cn - __ldg(rcb + k), sb[cur ^ 1]);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");  // the current chunk has landed
+        const uint32_t k = __ldg(chunk_rec + c);
+        const ApplyRec R = recs[k];
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
         __syncthreads();
-        cur ^= 1;
         uint32_t cnt = 0, err = kOk;
         unsigned long long sum = 0;
         validate_thread(v, cnt, sum, err);
