@@ -151,6 +151,18 @@ const char *delta_version(void);
 int delta_size(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int elem,
                void *stream, uint64_t *body_bytes);
 
+/* delta_size_table — the offset table of the compaction the last delta_size on ctx left
+ * cached, without writing a body (E6 table rows, E7 per-tensor readback).
+ *
+ * Rows (host, n entries, descriptor order) carry element_count N_k and nnz_k = ||ΔW^(k)||_0
+ * under the bitwise-inequality reading (Eq. 1
+ * compute_rho: rho = Σ nnz_k / Σ N_k), plus the offsets the body would have.  Synchronises
+ * `stream` once.  The cached compaction stays valid for a following delta_extract.
+ *   n: must equal the tensor count of that delta_size call.
+ * Errors: DELTA_EINVAL (no cached delta_size result — e.g. a delta_extract consumed it —,
+ * n mismatch, NULL table with n > 0), DELTA_ECUDA. */
+int delta_size_table(delta_ctx *ctx, uint32_t n, delta_record_info *table, void *stream);
+
 /* delta_extract — write the packed body (records in descriptor order) to out_dev.
  *
  * If the previous call on ctx was delta_size with identical descriptors, its cached

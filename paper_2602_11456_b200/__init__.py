@@ -9,5 +9,5 @@ multi-GPU orchestration (``dist``); see DESIGN.md.
 """
 
 from .binding import (DeltaContext, DeltaError, DeviceTable, Table, TargetList, TensorList, TABLE_FIELDS,  # noqa: F401
-                      context, delta_apply, delta_extract, delta_size, version)
+                      compute_rho, context, delta_apply, delta_extract, delta_size, version)
 from .container import pack_container, unpack_container  # noqa: F401

@@ -30,7 +30,8 @@ EXPORTS = ("delta_ctx_create", "delta_ctx_destroy", "delta_last_error", "delta_l
            "delta_apply_async_dev", "delta_table_dev", "delta_assemble", "delta_assemble_wait",
            "delta_digest", "delta_extract_async", "delta_extract_wait", "delta_apply_async_chain",
            "delta_merge", "delta_timing_totals", "delta_record_sizes", "delta_assemble_records",
-           "delta_assemble_flags", "delta_assemble_flags_wait", "delta_assemble_records_flags")
+           "delta_assemble_flags", "delta_assemble_flags_wait", "delta_assemble_records_flags",
+           "delta_size_table")
 DELTA_OPT_APPLY_CTAS_PER_SM, DELTA_OPT_EMIT_CTAS_PER_SM, DELTA_OPT_SCAN_KERNEL = 1, 2, 3
 DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER, DELTA_OPT_MODE = 4, 5, 6, 7
 DELTA_OPT_INDEX_CODEC = 8  # 1 LEB128 gaps (default), 2 fixed-width absolute indices (reading R18)
@@ -86,6 +87,8 @@ def lib():
         L.delta_version.restype = c_char_p
         L.delta_size.argtypes = [c_void_p, POINTER(Tensor), c_uint32, c_int, c_void_p, POINTER(c_uint64)]
         L.delta_size.restype = c_int
+        L.delta_size_table.argtypes = [c_void_p, c_uint32, POINTER(RecordInfo), c_void_p]
+        L.delta_size_table.restype = c_int
         L.delta_extract.argtypes = [c_void_p, POINTER(Tensor), c_uint32, c_int, c_void_p, c_uint64,
                                     POINTER(RecordInfo), c_void_p, POINTER(c_uint64)]
         L.delta_extract.restype = c_int

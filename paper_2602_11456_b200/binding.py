@@ -227,6 +227,25 @@ class DeltaContext:
                                          _stream_handle(stream), byref(out)))
         return out.value
 
+    def size_table(self, n: int, stream=None) -> "Table":
+        """Offset-table rows of the compaction the last ``delta_size`` left cached (host
+        Table, no body written; the cache stays valid for a following ``delta_extract``)."""
+        rows = (RecordInfo * max(n, 1))()
+        self._check(self._lib.delta_size_table(self._h, n, rows, _stream_handle(stream)))
+        return Table(rows, n)
+
+    def compute_rho(self, tensors, stream=None):
+        """SPEC.md:116-119 ``compute_rho`` / PAPER.md:294-297 Eq. 1 on the GPU:
+        rho = sum_k nnz_k / sum_k N_k, nnz_k = lanes whose bits differ (reading R2).
+        Returns ``(rho, nnz)``: the float ratio and the per-tensor counts (descriptor
+        order).  Runs the compare + compaction (K1-K3) once; its result stays cached."""
+        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        self.delta_size(tl, stream=stream)
+        rows = self.size_table(tl.n, stream=stream)
+        nnz = [r[2] for r in rows]
+        total = sum(r[1] for r in rows)
+        return (sum(nnz) / total if total else 0.0), nnz
+
     def delta_extract(self, tensors, out=None, stream=None, table=True):
         """Pack the delta.  Returns ``(body, table)``: ``body`` a uint8 CUDA tensor view of
         exactly the body bytes (``out``'s prefix if ``out`` is given); ``table``: True -> a
@@ -444,6 +463,10 @@ def context(device=None) -> DeltaContext:
 
 def delta_size(tensors, stream=None) -> int:
     return context().delta_size(tensors, stream=stream)
+
+
+def compute_rho(tensors, stream=None):
+    return context().compute_rho(tensors, stream=stream)
 
 
 def delta_extract(tensors, out=None, stream=None, table=True):

@@ -620,6 +620,24 @@ extern "C" int delta_size(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int
     return DELTA_OK;
 }
 
+// The offset table of the compaction the last delta_size left cached (K3 wrote it on the
+// device), copied to the host without emitting a body; the cache stays valid.
+extern "C" int delta_size_table(delta_ctx *ctx, uint32_t n, delta_record_info *table, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!ctx->scan_cached || !ctx->plan_valid)
+        return fail(ctx, DELTA_EINVAL, 0, "no cached delta_size result on this context");
+    if (n != ctx->ntensors) return fail(ctx, DELTA_EINVAL, 0, "n = %u but delta_size ran on %u tensors", n, ctx->ntensors);
+    if (n && !table) return fail(ctx, DELTA_EINVAL, 0, "table is NULL");
+    if (!n) return DELTA_OK;
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaMemcpyAsync(table, ctx->table.p, (size_t)n * sizeof(RecordRow), cudaMemcpyDeviceToHost, s), "table readback");
+    CK(cudaStreamSynchronize(s), "table readback");
+    return DELTA_OK;
+}
+
 extern "C" int delta_extract(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *out,
                              uint64_t cap, delta_record_info *table, void *stream,
                              uint64_t *body_bytes) {

@@ -71,6 +71,7 @@ def test_null_context_is_einval(built):
     assert lib.delta_set_profiling(None, 1) == E
     assert lib.delta_last_timing(None, byref(built.Timing())) == E
     assert lib.delta_table_dev(None) is None
+    assert lib.delta_size_table(None, 0, rows, None) == E
     assert lib.delta_assemble(None, None, None, 0, None, 1, 0, None) == E
     assert lib.delta_assemble_wait(None, None) == E
     assert lib.delta_digest(None, None, 0, None, None) == E

@@ -170,6 +170,33 @@ def test_size_then_extract_and_capacity(sd):
     assert e.value.status == -3  # DELTA_ECAPACITY
 
 
+def test_compute_rho_and_size_table(sd):
+    """SPEC.md:116-119 compute_rho (Eq. 1): per-tensor nnz and rho from the GPU compaction
+    equal the oracle's; the cached compaction still serves the following extract."""
+    specs = [TensorSpec("a", (4096, 33), "matrix"), TensorSpec("b", (70_001,), "matrix"),
+             TensorSpec("c", (257,), "norm")]
+    tensors = []
+    for i, (spec, r) in enumerate(zip(specs, (0.01, 0.3, 0.0))):
+        o, w = generate_pair(spec, 0, i, rho=r, device=DEV)
+        tensors.append((spec.name, o, w))
+    pairs = [(to_np(o), to_np(w)) for _, o, w in tensors]
+    ctx = sd.context()
+    tl = sd.TensorList(tensors)
+    rho, nnz = ctx.compute_rho(tl)
+    ref_body, ref_table = oracle_extract(tensors)
+    assert nnz == [r[2] for r in ref_table]
+    assert nnz[2] == 0
+    assert rho == oracle.codec.rho(pairs)
+    assert [tuple(r) for r in ctx.size_table(len(tensors))] == [tuple(r) for r in ref_table]
+    body, _ = ctx.delta_extract(tl)  # consumes the cached compaction
+    assert_body_equal(body, ref_body)
+    with pytest.raises(sd.DeltaError):
+        ctx.size_table(len(tensors))  # nothing cached any more
+    ctx.delta_size(tl)
+    with pytest.raises(sd.DeltaError):
+        ctx.size_table(len(tensors) + 1)  # n mismatch
+
+
 def test_fp32_m1_shape(sd):
     spec = m1_specs()[0]
     o, w = generate_pair(spec, 0, 4, rho=0.01, dtype=torch.float32, device=DEV)
