@@ -197,6 +197,20 @@ def test_compute_rho_and_size_table(sd):
         ctx.size_table(len(tensors) + 1)  # n mismatch
 
 
+def test_compute_rho_spec_example(sd):
+    """SPEC.md:121 worked example: tensors of 4 and 6 lanes with 1 and 2 changed -> 0.3."""
+    a_old = torch.tensor([1.0, 2.0, 3.0, 4.0], dtype=torch.bfloat16, device=DEV)
+    a_new = a_old.clone()
+    a_new[2] = 5.0
+    b_old = torch.arange(6, dtype=torch.float32, device=DEV).to(torch.bfloat16)
+    b_new = b_old.clone()
+    b_new[0] = -0.0  # +0.0 -> -0.0 is a change (bitwise, reading R2)
+    b_new[5] = 7.0
+    rho, nnz = sd.compute_rho([("a", a_old, a_new), ("b", b_old, b_new)])
+    assert nnz == [1, 2]
+    assert rho == 3 / 10
+
+
 def test_fp32_m1_shape(sd):
     spec = m1_specs()[0]
     o, w = generate_pair(spec, 0, 4, rho=0.01, dtype=torch.float32, device=DEV)
