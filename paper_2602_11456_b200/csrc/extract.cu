@@ -812,6 +812,15 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
     // FIXED: absolute indices staged per warp in shared memory, then copied to the body
     __shared__ __align__(16) unsigned long long s_fix[FIXED ? 8 * 256 + 2 : 1];
     for (uint32_t t = wg; t < ntiles; t += nw) {
+        // sparse variant: the first 256 slot offsets are loaded before the plan entry arrives
+        // (every tile's slot region holds slot_cap >= 512 entries, so the unguarded loads
+        // stay inside it; entries past the count are never used)
+        uint32_t o[8];
+        if constexpr (!FIXED && !BATCHED) {
+            const uint16_t *so0 = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) o[r] = so0[r * 32 + lane];
+        }
         const TileEmit e = plan[t];
         if (e.count == 0) continue;
         if constexpr (FIXED) {  // reading R18: lane_base + offset as u32 / u64, little-endian
@@ -885,12 +894,6 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
             continue;
         }
         if (c <= 256) {  // ~all tiles up to a few % density: every load of the tile issued up front
-            uint32_t o[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const uint32_t i = r * 32 + lane;
-                o[r] = i < c ? (uint32_t)so[i] : 0u;
-            }
             warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
