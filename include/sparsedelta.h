@@ -72,7 +72,7 @@ enum {
     DELTA_D_COUNT = 6,         /* number of varints != nnz */
     DELTA_D_NAME = 7,          /* record name != target name */
     DELTA_D_NUMEL = 8,         /* record element_count != target numel */
-    DELTA_D_MODE = 9,          /* mode byte not 0 (replace) or 1 (additive); delta_merge: not 0 */
+    DELTA_D_MODE = 9,          /* mode byte not in {0 (replace), 1 (additive)}; delta_merge: not 0 */
     DELTA_D_LAYOUT = 10        /* record past the body end, trailing bytes, record count != n */
 };
 
@@ -145,6 +145,10 @@ const char *delta_version(void);
  * a following delta_extract with identical descriptors (same pointers, sizes, names,
  * elem) reuses it without re-reading old/new — the caller must not modify old/new in
  * between (two-phase, as CUB's temp-storage query).
+ * With DELTA_OPT_ADVANCE the compare also overwrites old with new: call delta_size at most
+ * once per step (a second call compares old against itself and finds nothing) and follow it
+ * with delta_extract, which consumes the cached compaction — also after a DELTA_ECAPACITY
+ * return, so the retry with a larger buffer emits the same body.
  *   tensors: n descriptors (host); elem: DELTA_ELEM16 or DELTA_ELEM32.
  * Errors: DELTA_EINVAL, DELTA_ESHAPE (a span with numel but NULL pointers), DELTA_ECUDA,
  * DELTA_ENOMEM. */
@@ -162,6 +166,25 @@ int delta_size(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int elem
  * Errors: DELTA_EINVAL (no cached delta_size result — e.g. a delta_extract consumed it —,
  * n mismatch, NULL table with n > 0), DELTA_ECUDA. */
 int delta_size_table(delta_ctx *ctx, uint32_t n, delta_record_info *table, void *stream);
+
+/* delta_compute_rho — SPEC.md:116-119 compute_rho, Eq. 1:
+ *     rho = sum_k ||dW^(k)||_0 / sum_k N_k,
+ * with ||dW^(k)||_0 = nnz_k, the lanes of tensor k whose bits differ (reading R2).  Runs the
+ * compare + compaction of delta_size (cached on ctx for a following delta_extract) and sums
+ * the offset-table rows on the host side of the library.  Synchronises `stream` twice.
+ *   nnz:         host array of n uint64 (per-tensor nnz_k, descriptor order) or NULL;
+ *   nnz_total, numel_total, rho: host, required (rho = 0 when numel_total == 0).
+ * Errors: as delta_size; DELTA_EINVAL on a context with DELTA_OPT_ADVANCE set (the advancing
+ * compare would overwrite old — compute_rho is a pure function). */
+int delta_compute_rho(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int elem, void *stream,
+                      uint64_t *nnz, uint64_t *nnz_total, uint64_t *numel_total, double *rho);
+
+/* delta_table_rebase — host-only (no device, no context): shift n offset-table rows (host) of a
+ * body that is placed `offset` bytes into a larger body, e.g. a group's or a rank's records
+ * after the earlier ones (R15): record_offset, index_offset and values_offset += offset.
+ * DELTA_EINVAL for NULL rows with n > 0 or an offset that overflows 64 bits (rows untouched
+ * from the failing row on). */
+int delta_table_rebase(delta_record_info *rows, uint32_t n, uint64_t offset);
 
 /* delta_extract — write the packed body (records in descriptor order) to out_dev.
  *
@@ -190,7 +213,9 @@ int delta_extract_async(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n,
                         void *stream);
 
 /* delta_extract_wait — wait for the last delta_extract_async on ctx (an event, not the
- * whole stream) and report its outcome; *body_bytes (host, may be NULL) = body size.
+ * whole stream) and report the outcome of EVERY delta_extract_async since the previous wait
+ * (a closed emit gate in any of them is reported, not only in the last); *body_bytes (host,
+ * may be NULL) = the last body's size (on DELTA_ECAPACITY: the largest size needed).
  * DELTA_EAGAIN: a tile held more changes than the slots (first call at a higher density);
  * the slots have been grown, no body was written, repeat the extract (and anything
  * chained on it, which refused to run: see delta_apply_async_chain).  DELTA_ECAPACITY:

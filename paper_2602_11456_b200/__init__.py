@@ -8,6 +8,6 @@ scatter-store into resident weights), as hand-written sm_100a CUDA kernels behin
 multi-GPU orchestration (``dist``); see DESIGN.md.
 """
 
-from .binding import (DeltaContext, DeltaError, DeviceTable, Table, TargetList, TensorList, TABLE_FIELDS,  # noqa: F401
+from .binding import (DeltaContext, DeltaError, DeviceTable, Table, TargetList, TensorList, TABLE_FIELDS, rebase,  # noqa: F401
                       compute_rho, context, delta_apply, delta_extract, delta_size, version)
 from .container import pack_container, unpack_container  # noqa: F401

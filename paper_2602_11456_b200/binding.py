@@ -120,7 +120,9 @@ class TensorList:
                     self.width = ww
                 elif self.width != ww:
                     raise ValueError("all tensors must have the same lane width (SPEC.md:34)")
-                self.device = o.device if self.device is None else self.device
+                if o.device != w.device or (self.device is not None and o.device != self.device):
+                    raise ValueError(f"tensor {name!r} span {s}: all spans must be on one device")
+                self.device = o.device
                 spans[s].old_dev = o.data_ptr()
                 spans[s].new_dev = w.data_ptr()
                 spans[s].numel = o.numel()
@@ -147,9 +149,13 @@ class TargetList:
         self.n = n
         self._keep = []
         self.width = None
+        self.device = None
         for k, (name, w) in enumerate(targets):
             if not w.is_cuda or not w.is_contiguous():
                 raise ValueError(f"target {name!r} must be a contiguous CUDA tensor")
+            if self.device is not None and w.device != self.device:
+                raise ValueError(f"target {name!r}: all targets must be on one device")
+            self.device = w.device
             ww = _width(w)
             if self.width is None:
                 self.width = ww
@@ -218,10 +224,22 @@ class DeltaContext:
         self._check(self._lib.delta_last_timing(self._h, byref(t)))
         return {f: getattr(t, f) for f, _ in _abi.Timing._fields_}
 
+    def _tensors(self, tensors) -> "TensorList":
+        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        if tl.device is not None and tl.device != self.device:
+            raise ValueError(f"tensors are on {tl.device}, the context on {self.device}")
+        return tl
+
+    def _targets(self, targets) -> "TargetList":
+        tg = targets if isinstance(targets, TargetList) else TargetList(targets)
+        if tg.device is not None and tg.device != self.device:
+            raise ValueError(f"targets are on {tg.device}, the context on {self.device}")
+        return tg
+
     # --------------------------------------------------------------- C-ABI mirrors
     def delta_size(self, tensors, stream=None) -> int:
         """Body size in bytes (runs and caches the compare + compaction)."""
-        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        tl = self._tensors(tensors)
         out = c_uint64()
         self._check(self._lib.delta_size(self._h, tl.arr, tl.n, _ELEM[tl.width],
                                          _stream_handle(stream), byref(out)))
@@ -235,23 +253,24 @@ class DeltaContext:
         return Table(rows, n)
 
     def compute_rho(self, tensors, stream=None):
-        """SPEC.md:116-119 ``compute_rho`` / PAPER.md:294-297 Eq. 1 on the GPU:
+        """SPEC.md:116-119 ``compute_rho`` / PAPER.md:294-297 Eq. 1 (delta_compute_rho):
         rho = sum_k nnz_k / sum_k N_k, nnz_k = lanes whose bits differ (reading R2).
-        Returns ``(rho, nnz)``: the float ratio and the per-tensor counts (descriptor
-        order).  Runs the compare + compaction (K1-K3) once; its result stays cached."""
-        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
-        self.delta_size(tl, stream=stream)
-        rows = self.size_table(tl.n, stream=stream)
-        nnz = [r[2] for r in rows]
-        total = sum(r[1] for r in rows)
-        return (sum(nnz) / total if total else 0.0), nnz
+        Returns ``(rho, nnz)``: the ratio and the per-tensor counts (descriptor order), both
+        computed by the library.  Refused (DeltaError EINVAL) on an extract-and-advance
+        context: its compare overwrites old."""
+        tl = self._tensors(tensors)
+        nnz = (c_uint64 * max(tl.n, 1))()
+        tot, numel, rho = c_uint64(), c_uint64(), ctypes.c_double()
+        self._check(self._lib.delta_compute_rho(self._h, tl.arr, tl.n, _ELEM[tl.width], _stream_handle(stream),
+                                                nnz, byref(tot), byref(numel), byref(rho)))
+        return rho.value, list(nnz[:tl.n])
 
     def delta_extract(self, tensors, out=None, stream=None, table=True):
         """Pack the delta.  Returns ``(body, table)``: ``body`` a uint8 CUDA tensor view of
         exactly the body bytes (``out``'s prefix if ``out`` is given); ``table``: True -> a
         host Table of offset-table rows (TABLE_FIELDS order; one extra synchronisation),
         "device" -> a DeviceTable (no extra synchronisation), False -> None."""
-        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        tl = self._tensors(tensors)
         st = _stream_handle(stream)
         nbytes = c_uint64()
         rows = (RecordInfo * max(tl.n, 1))() if table is True else None
@@ -274,7 +293,7 @@ class DeltaContext:
         with no host synchronisation; ``size`` (int64 CUDA tensor, 1 element) receives the
         body size on the device (or -1 = UINT64_MAX if nothing was written).  Returns the
         device-resident offset table.  Pair with ``extract_wait``."""
-        tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+        tl = self._tensors(tensors)
         if out.dtype != torch.uint8 or not out.is_contiguous() or not out.is_cuda:
             raise ValueError("out must be a contiguous uint8 CUDA tensor")
         if size.dtype != torch.int64 or not size.is_cuda or size.numel() != 1:
@@ -329,7 +348,7 @@ class DeltaContext:
         """Validate ``body`` fully, then scatter its values into ``targets`` in place
         (all-or-nothing).  ``table``: optional offset-table rows from delta_extract.
         ``wait=False`` enqueues only (delta_apply_async); call ``apply_wait`` later."""
-        tg = targets if isinstance(targets, TargetList) else TargetList(targets)
+        tg = self._targets(targets)
         if body.dtype != torch.uint8 or not body.is_contiguous() or not body.is_cuda:
             raise ValueError("body must be a contiguous uint8 CUDA tensor")
         hint = None
@@ -441,6 +460,20 @@ class DeltaContext:
     def apply_wait(self, stream=None):
         """Synchronise and raise the first error of the async applies since the last wait."""
         self._check(self._lib.delta_apply_wait(self._h, _stream_handle(stream)))
+
+
+def rebase(rows, offset: int) -> "Table":
+    """Offset-table rows of a body placed ``offset`` bytes into a larger body (the library's
+    delta_table_rebase; host only).  ``rows``: a Table or a sequence of TABLE_FIELDS tuples;
+    returns a new Table."""
+    src = rows.arr if isinstance(rows, Table) else _rows_to_ctypes(rows)
+    n = len(rows)
+    arr = (RecordInfo * max(n, 1))()
+    ctypes.memmove(arr, src, ctypes.sizeof(RecordInfo) * n)
+    rc = _abi.lib().delta_table_rebase(arr, n, offset)
+    if rc != 0:
+        raise DeltaError(rc, 0, f"delta_table_rebase(offset={offset}) failed")
+    return Table(arr, n)
 
 
 def _rows_to_ctypes(rows):

@@ -73,7 +73,7 @@ struct delta_ctx {
     DevBuf tiles, name_len, name_off, names, numel, tensor_first_tile;
     // ---- extract workspace
     DevBuf slot_bytes, slot_val, meta, tile_entry, tile_byte, tile_pred, tile_bytes, tile_plan, blk_a, blk_key,
-        entry_begin, tensor_byte_begin, table, summary;
+        entry_begin, tensor_byte_begin, table, summary, sticky;
     uint32_t slot_cap = 0;          // entries per tile slot (grows on overflow)
     bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
     // delta_extract_async: readback of the summary lands in h_summary when ev_extract fires
@@ -81,6 +81,8 @@ struct delta_ctx {
     unsigned long long async_cap = 0;
     cudaEvent_t ev_extract = nullptr;
     ExtractSummary *h_summary = nullptr;  // pinned
+    ExtractSticky *h_sticky = nullptr;    // pinned: outcome of every async extract since the last wait
+    cudaStream_t async_stream = nullptr;
 
     // ---- apply workspace
     DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status, asm_off, dg_ws;
@@ -177,6 +179,7 @@ int delta_ctx_create(delta_ctx **out, int device) {
     c->device = device;
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (cudaMallocHost(&c->h_summary, sizeof(ExtractSummary)) != cudaSuccess ||
+        cudaMallocHost(&c->h_sticky, sizeof(ExtractSticky)) != cudaSuccess ||
         cudaMallocHost(&c->h_state, sizeof(ApplyState)) != cudaSuccess) {
         cudaGetLastError();
         delete c;
@@ -198,7 +201,7 @@ void delta_ctx_destroy(delta_ctx *c) {
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->tile_plan, &c->blk_a,
                       &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
-                      &c->summary, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->asm_off, &c->dg_ws, &c->a_cnt, &c->a_sum,
+                      &c->summary, &c->sticky, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->asm_off, &c->dg_ws, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
     if (c->profiling) {
@@ -212,6 +215,7 @@ void delta_ctx_destroy(delta_ctx *c) {
         }
     }
     if (c->h_summary) cudaFreeHost(c->h_summary);
+    if (c->h_sticky) cudaFreeHost(c->h_sticky);
     if (c->h_state) cudaFreeHost(c->h_state);
     if (c->h_asm) cudaFreeHost(c->h_asm);
     for (int i = 0; i < delta_ctx::kRing; ++i) {
@@ -638,6 +642,50 @@ extern "C" int delta_size_table(delta_ctx *ctx, uint32_t n, delta_record_info *t
     return DELTA_OK;
 }
 
+// compute_rho (Eq. 1): rho = sum_k nnz_k / sum_k N_k with
+// nnz_k the changed lanes under the bitwise reading R2.  One compare + compaction (cached for a
+// following delta_extract, like delta_size); the sums are taken over the offset-table rows.
+extern "C" int delta_compute_rho(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *stream,
+                                 uint64_t *nnz, uint64_t *nnz_total, uint64_t *numel_total, double *rho) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (!nnz_total || !numel_total || !rho) return fail(ctx, DELTA_EINVAL, 0, "NULL result pointer");
+    if (ctx->advance)  // the advancing compare overwrites old: compute_rho is a pure function
+        return fail(ctx, DELTA_EINVAL, 0, "compute_rho on a context with DELTA_OPT_ADVANCE set");
+    uint64_t body = 0;
+    int rc = delta_size(ctx, t, n, elem, stream, &body);
+    if (rc) return rc;
+    std::vector<delta_record_info> rows(std::max<uint32_t>(n, 1));
+    if (n) {
+        rc = delta_size_table(ctx, n, rows.data(), stream);
+        if (rc) return rc;
+    }
+    uint64_t sn = 0, sN = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+        if (nnz) nnz[k] = rows[k].nnz;
+        sn += rows[k].nnz;
+        sN += rows[k].element_count;
+    }
+    *nnz_total = sn;
+    *numel_total = sN;
+    *rho = sN ? (double)sn / (double)sN : 0.0;
+    return DELTA_OK;
+}
+
+// Host-only: offset-table rows of a body that starts `offset` bytes into a larger body
+// (a group's or a rank's records placed after the earlier ones, reading R15).
+extern "C" int delta_table_rebase(delta_record_info *rows, uint32_t n, uint64_t offset) {
+    if (n && !rows) return DELTA_EINVAL;
+    for (uint32_t k = 0; k < n; ++k) {
+        if (rows[k].record_offset + rows[k].record_bytes > UINT64_MAX - offset) return DELTA_EINVAL;
+        rows[k].record_offset += offset;
+        rows[k].index_offset += offset;
+        rows[k].values_offset += offset;
+    }
+    return DELTA_OK;
+}
+
 extern "C" int delta_extract(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *out,
                              uint64_t cap, delta_record_info *table, void *stream,
                              uint64_t *body_bytes) {
@@ -659,13 +707,17 @@ extern "C" int delta_extract(delta_ctx *ctx, const delta_tensor *t, uint32_t n, 
         rc = run_scan(ctx, s);
         if (rc) return rc;
     }
-    ctx->scan_cached = false;  // consumed
+    // The compaction stays cached across DELTA_ECAPACITY / a NULL out_dev: with
+    // extract-and-advance, old already equals new, so a retry with a larger buffer must
+    // emit from this scan rather than compare again (it would find nothing).
+    ctx->scan_cached = true;
     const unsigned long long need = ctx->h_summary->body_bytes;
     *body_bytes = need;
     if (need > cap)
         return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < body size %llu",
                     (unsigned long long)cap, need);
     if (need && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
+    ctx->scan_cached = false;  // consumed
     if (n)
         CK(launch_extract_emit(extract_args(ctx), static_cast<uint8_t *>(out), s,
                                prof_emit(ctx)),
@@ -707,10 +759,13 @@ extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32
     if (rc) return rc;
     ctx->scan_cached = false;
     if (!ctx->ev_extract) CK(cudaEventCreateWithFlags(&ctx->ev_extract, cudaEventDisableTiming), "event");
+    GROW(ctx->sticky, sizeof(ExtractSticky));
+    if (!ctx->async_pending) CK(cudaMemsetAsync(ctx->sticky.p, 0, sizeof(ExtractSticky), s), "memset");
     CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
     ExtractArgs a = extract_args(ctx);
     a.out_cap = cap;
     a.size_out = reinterpret_cast<unsigned long long *>(body_bytes_dev);
+    a.sticky = ctx->sticky.as<ExtractSticky>();
     CK(launch_extract_scan(a, s, prof_scan(ctx)), "extract scan launch");
     if (n) {
         CK(launch_extract_emit(a, static_cast<uint8_t *>(out), s, prof_emit(ctx)),
@@ -719,8 +774,10 @@ extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32
         CK(cudaMemsetAsync(body_bytes_dev, 0, 8, s), "memset");
     }
     CK(cudaMemcpyAsync(ctx->h_summary, ctx->summary.p, sizeof(ExtractSummary), cudaMemcpyDeviceToHost, s), "readback");
+    CK(cudaMemcpyAsync(ctx->h_sticky, ctx->sticky.p, sizeof(ExtractSticky), cudaMemcpyDeviceToHost, s), "readback");
     CK(cudaEventRecord(ctx->ev_extract, s), "event");
     ctx->async_pending = true;
+    ctx->async_stream = s;
     ctx->async_cap = cap;
     return DELTA_OK;
 }
@@ -740,21 +797,24 @@ extern "C" int delta_extract_wait(delta_ctx *ctx, uint64_t *body_bytes) {
             ctx->timing.headers_ms = ev_ms(ctx->ev_emit[1], ctx->ev_emit[2]);
         }
     }
+    // the sticky record covers every async extract since the last wait (the summary only
+    // the last one): an earlier call's closed gate is reported here, not lost
     const ExtractSummary &sm = *ctx->h_summary;
-    if (sm.overflow) {
+    const ExtractSticky sk = *ctx->h_sticky;
+    if (sk.overflow) {
         const uint32_t lanes_per_tile = kTileBytes / ctx->width;
         uint32_t need = 2;
-        while (need < sm.max_count) need <<= 1;
+        while (need < sk.max_count) need <<= 1;
         int rc = reserve_slots(ctx, std::min(need, lanes_per_tile));
         if (rc) return rc;
         return fail(ctx, DELTA_EAGAIN, 0,
                     "tile slots overflowed (largest tile count %llu); workspace grown, issue the call again",
-                    (unsigned long long)sm.max_count);
+                    (unsigned long long)sk.max_count);
     }
-    if (body_bytes) *body_bytes = sm.body_bytes;
-    if (sm.body_bytes > ctx->async_cap)
+    if (body_bytes) *body_bytes = sk.over_cap ? sk.need : sm.body_bytes;
+    if (sk.over_cap)
         return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < body size %llu",
-                    (unsigned long long)ctx->async_cap, (unsigned long long)sm.body_bytes);
+                    (unsigned long long)ctx->async_cap, (unsigned long long)sk.need);
     return DELTA_OK;
 }
 
@@ -765,7 +825,7 @@ static const int kDetailToStatus[] = {
 static const char *kDetailName[] = {"ok", "truncated varint", "overlong varint", "varint exceeds 64 bits",
                                     "non-increasing index", "index >= element_count", "index count != nnz",
                                     "record name != target name", "record element_count != target numel",
-                                    "mode byte != 0", "record layout"};
+                                    "mode byte not in {0, 1}", "record layout"};
 
 static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int elem, const void *body,
                          uint64_t body_bytes, const delta_record_info *hint, cudaStream_t s,

@@ -948,9 +948,20 @@ __global__ void __launch_bounds__(128)
 k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__restrict__ name_len,
           const uint32_t *__restrict__ name_off, const uint8_t *__restrict__ names,
           uint8_t *__restrict__ out, int mode, const ExtractSummary *summary, unsigned long long cap,
-          unsigned long long *size_out) {
+          unsigned long long *size_out, ExtractSticky *sticky) {
     const bool open = !summary->overflow && summary->body_bytes <= cap;
-    if (size_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *size_out = open ? summary->body_bytes : ~0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (size_out != nullptr) *size_out = open ? summary->body_bytes : ~0ull;
+        if (sticky != nullptr && !open) {  // delta_extract_wait reports every closed gate, not just the last
+            if (summary->overflow) {
+                sticky->overflow = 1;
+                sticky->max_count = max(sticky->max_count, summary->max_count);
+            } else {
+                sticky->over_cap = 1;
+                sticky->need = max(sticky->need, summary->body_bytes);
+            }
+        }
+    }
     if (!open) return;
     for (uint32_t k = blockIdx.x; k < T; k += gridDim.x) {
         const RecordRow r = table[k];
@@ -1043,7 +1054,7 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
     k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode, a.summary,
-                                 a.out_cap, a.size_out);
+                                 a.out_cap, a.size_out, a.sticky);
     if (ev) cudaEventRecord(ev[2], s);
     return cudaGetLastError();
 }

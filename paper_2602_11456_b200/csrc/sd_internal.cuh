@@ -61,6 +61,15 @@ struct ExtractSummary {
     unsigned long long body_bytes;  // packed body size
 };
 
+// Sticky outcome of the delta_extract_async calls since the last delta_extract_wait (folded
+// in by K5 of every async extract; the per-call summary is reset by each call).
+struct ExtractSticky {
+    unsigned long long overflow;    // some call's tiles overflowed their slots
+    unsigned long long max_count;   // largest per-tile count over those calls
+    unsigned long long over_cap;    // some call's body exceeded its capacity
+    unsigned long long need;        // largest such body
+};
+
 // Per-tensor row of the device offset table (same field order as delta_record_info).
 struct RecordRow {
     unsigned long long record_offset, element_count, nnz, index_offset, index_bytes,
@@ -137,6 +146,7 @@ struct ExtractArgs {
     // size_out (device, may be NULL) receives the body size, or ~0 when the gate is closed
     unsigned long long out_cap = ~0ull;
     unsigned long long *size_out = nullptr;
+    ExtractSticky *sticky = nullptr;  // async extracts: outcome folded in by K5
 };
 
 // ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1,

@@ -15,6 +15,7 @@ S3  ``assemble``: the rank bodies are sent to the root into their final offsets
 import torch
 import torch.distributed as dist
 from torch.multiprocessing.reductions import reduce_tensor
+from .binding import rebase
 
 
 def shard_plan(numels, world: int):
@@ -103,7 +104,7 @@ def assemble(local_body: torch.Tensor, sizes, root_out: torch.Tensor = None, roo
 
 def shift_table(rows, offset: int):
     """Offset-table rows of a rank's body, shifted to the global body's byte offsets."""
-    return [(r[0] + offset, r[1], r[2], r[3] + offset, r[4], r[5] + offset, r[6]) for r in rows]
+    return list(rebase(rows, offset))
 
 
 class NvlinkAssembler:

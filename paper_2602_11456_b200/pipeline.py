@@ -15,7 +15,7 @@ Everything still runs in the library's kernels; this module only orders calls on
 import torch
 
 from . import _abi
-from .binding import DeltaContext, TargetList, TensorList
+from .binding import DeltaContext, TargetList, TensorList, rebase
 from .dist import shard_plan
 
 
@@ -91,7 +91,7 @@ class RoundTrip:
         """Offset table of the whole body (rows shifted to global offsets)."""
         rows = []
         for off, tab in self.tables or []:
-            rows += [(r[0] + off, r[1], r[2], r[3] + off, r[4], r[5] + off, r[6]) for r in tab]
+            rows += list(rebase(tab, off))
         return rows
 
     def close(self):

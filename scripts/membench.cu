@@ -155,6 +155,62 @@ __global__ void k_scatter_hint(uint16_t *w, const unsigned long long *pos, const
 // v7: plain, one warp per 32 consecutive entries but the grid sweeps the entries in narrow
 // windows: CTA b handles entries [k*S + b*256, ...) for k = 0.. (S = grid*256) — same as plain
 // with a grid of 148 CTAs (small window in flight)
+
+// v7: windowed plain stores — the whole grid sweeps the entries together: warp w of W handles
+// entries [(k W + w) 32, +32) at iteration k, so the stores in flight span ~W x 32 entries of
+// address space (the DRAM row-locality window); UNROLL iterations' loads are issued first.
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k_scatter_window(uint16_t *w, const unsigned long long *pos, const uint16_t *val, size_t n) {
+    const int lane = threadIdx.x & 31;
+    const size_t W = (size_t)gridDim.x * (blockDim.x >> 5);
+    const size_t wid = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (size_t k = 0;; k += UNROLL) {
+        unsigned long long p[UNROLL];
+        uint16_t v[UNROLL];
+        bool any = false;
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const size_t i = ((k + u) * W + wid) * 32 + lane;
+            p[u] = i < n ? pos[i] : ~0ull;
+            v[u] = i < n ? val[i] : 0;
+            any |= ((k + u) * W + wid) * 32 < n;
+        }
+        if (!__any_sync(0xffffffffu, any)) break;
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+            if (p[u] != ~0ull) w[p[u]] = v[u];
+    }
+}
+
+// v8: read-only gather of the same lanes (the L2 fills alone): XOR of w[pos[i]]
+__global__ void __launch_bounds__(256) k_gather(const uint16_t *w, const unsigned long long *pos, size_t n, unsigned long long *out) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) acc ^= w[pos[i]];
+    if (acc == 0x12345u) atomicAdd(out, 1ull);
+}
+
+// v9: full 32-byte sector writes of every touched sector (the write-backs alone, no fill):
+// thread pair (2j, 2j+1) writes the two 16-byte halves of sector sec[j]
+__global__ void __launch_bounds__(256) k_sector_write(uint16_t *w, const unsigned long long *sec, size_t ns) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * ns; t += stride) {
+        uint4 *p = reinterpret_cast<uint4 *>(w + (sec[t >> 1] << 4)) + (t & 1);
+        *p = make_uint4((uint32_t)t, 1u, 2u, 3u);
+    }
+}
+
+// v10: full 32-byte sector read of every touched sector (the fills as whole-sector loads)
+__global__ void __launch_bounds__(256) k_sector_read(const uint16_t *w, const unsigned long long *sec, size_t ns, unsigned long long *out) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * ns; t += stride) {
+        const uint4 x = *(reinterpret_cast<const uint4 *>(w + (sec[t >> 1] << 4)) + (t & 1));
+        acc ^= x.x ^ x.y ^ x.z ^ x.w;
+    }
+    if (acc == 0x12345u) atomicAdd(out, 1ull);
+}
+
 extern "C" {
 int mb_read(const void *p, size_t bytes, void *out, int grid, int block, cudaStream_t s) {
     k_read<<<grid, block, 0, s>>>(static_cast<const uint4 *>(p), bytes / 16, static_cast<unsigned long long *>(out));
@@ -171,6 +227,20 @@ int mb_scatter(int variant, void *w, const void *pos, const void *val, size_t n,
     else if (variant == 4) k_scatter_batch<1><<<grid, 128, 0, s>>>(W, P, V, n);
     else if (variant == 5) k_scatter_hint<0><<<grid, block, 0, s>>>(W, P, V, n);
     else if (variant == 6) k_scatter_hint<1><<<grid, block, 0, s>>>(W, P, V, n);
+    else if (variant == 7) k_scatter_window<4><<<grid, block, 0, s>>>(W, P, V, n);
+    else if (variant == 8) k_scatter_window<1><<<grid, block, 0, s>>>(W, P, V, n);
+    return (int)cudaGetLastError();
+}
+
+int mb_gather(const void *w, const void *pos, size_t n, void *out, int grid, int block, cudaStream_t s) {
+    k_gather<<<grid, block, 0, s>>>(static_cast<const uint16_t *>(w), static_cast<const unsigned long long *>(pos), n,
+                                    static_cast<unsigned long long *>(out));
+    return (int)cudaGetLastError();
+}
+int mb_sector(int write, void *w, const void *sec, size_t ns, void *out, int grid, int block, cudaStream_t s) {
+    if (write) k_sector_write<<<grid, block, 0, s>>>(static_cast<uint16_t *>(w), static_cast<const unsigned long long *>(sec), ns);
+    else k_sector_read<<<grid, block, 0, s>>>(static_cast<const uint16_t *>(w), static_cast<const unsigned long long *>(sec), ns,
+                                             static_cast<unsigned long long *>(out));
     return (int)cudaGetLastError();
 }
 }

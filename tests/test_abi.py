@@ -78,6 +78,7 @@ def test_null_context_is_einval(built):
     assert lib.delta_extract_async(None, tl, 0, 0, None, 0, c_void_p(0), None) == E
     assert lib.delta_extract_wait(None, byref(n)) == E
     assert lib.delta_apply_async_chain(None, tg, 0, 0, None, 0, c_void_p(0), c_void_p(0), None) == E
+    assert lib.delta_compute_rho(None, tl, 0, 0, None, None, byref(n), byref(n), None) == E
     assert lib.delta_last_detail(None) == 0
     assert lib.delta_last_error(None) == b"no context"
     assert b"sm_100a" in lib.delta_version()
@@ -107,3 +108,25 @@ def test_product_container_reader_matches_oracle():
     body = bytes(range(200)) * 3
     b = oracle.container.pack(body, 8, 7, 2, 5)
     assert sd.unpack_container(b) == oracle.container.unpack(b)
+
+
+def test_table_rebase_host_only(built):
+    """delta_table_rebase (host code, no device): rows of a body placed `off` bytes into a
+    larger body move by `off` in record/index/values offsets; sizes and counts stay (O7)."""
+    import oracle
+    import numpy as np
+    import paper_2602_11456_b200 as sd
+    rng = np.random.default_rng(3)
+    tensors = [(f"t{k}", [rng.integers(0, 65536, 50, dtype=np.uint16)], [rng.integers(0, 65536, 50, dtype=np.uint16)])
+               for k in range(4)]
+    body, table = oracle.codec.extract(tensors)
+    # the records of tensors 2..3 extracted alone, placed after those of 0..1
+    _, tail = oracle.codec.extract(tensors[2:])
+    off = table[2][0]
+    assert list(sd.rebase(tail, off)) == [tuple(r) for r in table[2:]]
+    assert list(sd.rebase(tail, 0)) == [tuple(r) for r in tail]
+    rows = (built.RecordInfo * 1)()
+    rows[0].record_offset, rows[0].record_bytes = 10, 20
+    assert built.lib().delta_table_rebase(rows, 1, 2 ** 64 - 25) == built.DELTA_EINVAL
+    assert built.lib().delta_table_rebase(None, 1, 5) == built.DELTA_EINVAL
+    assert built.lib().delta_table_rebase(None, 0, 5) == 0

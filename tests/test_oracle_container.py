@@ -52,3 +52,29 @@ def test_fixed_codec_container_version():
     assert container.unpack(blob, index_codec="fixed") == (2, 1, 2, 1, body)
     with pytest.raises(DeltaError):
         container.unpack(blob)
+
+
+def _kat():
+    out = []
+    for ln in golden_lines("blake3_kat.txt"):
+        n, h = ln.split()
+        out.append((int(n), bytes.fromhex(h)))
+    return out
+
+
+def test_digest_blake3_known_answers():
+    """container.digest against the official BLAKE3 vectors (tests/golden/blake3_kat.txt): the
+    empty input, 1 byte, chunk boundaries 1023/1024/1025 and multi-chunk trees."""
+    kat = _kat()
+    assert [n for n, _ in kat][:5] == [0, 1, 1023, 1024, 1025]
+    for n, h in kat:
+        assert container.digest(bytes(i % 251 for i in range(n))) == h, n
+
+
+def test_header_digest_field_is_the_body_hash():
+    """The 32 header bytes 35..67 are the BLAKE3 of exactly the body, pinned
+    through a KAT body: a 1025-byte body of i mod 251 carries the 1025-byte vector."""
+    n, h = _kat()[4]
+    body = bytes(i % 251 for i in range(n))
+    blob = container.pack(body, version=2, base_version=1, width=2, n_tensors=0)
+    assert blob[35:67] == h

@@ -101,3 +101,32 @@ def test_shape_mismatch():
     with pytest.raises(DeltaError) as e:
         brute.extract([("x", [[0, 0]], [[0, 0], [1]])], 2)
     assert e.value.kind == "shape"
+
+
+def test_record_from_sparse_equals_record_on_dense():
+    """brute.record_from_sparse (the expected value of the >2^32-lane GPU test) is the same
+    O3-O6 record as brute.record when the change set comes from dense lists."""
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        n = int(rng.integers(0, 400))
+        width = 2 if trial % 2 else 4
+        old = rng.integers(0, 1 << (8 * width), n, dtype=np.uint64).tolist()
+        new = list(old)
+        for j in rng.choice(n, size=int(rng.integers(0, n + 1)) if n else 0, replace=False).tolist():
+            new[j] = (new[j] + int(rng.integers(1, 1 << (8 * width)))) % (1 << (8 * width))
+        idx = [j for j in range(n) if old[j] != new[j]]
+        name = f"t{trial}.weight" + ("é" if trial % 3 == 0 else "")
+        assert brute.record_from_sparse(name, n, idx, [new[j] for j in idx], width) == \
+            brute.record(name, old, new, width)
+
+
+def test_record_from_sparse_golden_2p32():
+    """Hand-derived record of a tensor with 2^32 + 1000 lanes (tests/golden/record_sparse_2p32.txt):
+    u64 element count above 2^32, a 5-byte LEB128 gap (reading R13)."""
+    g = _kv("record_sparse_2p32.txt")
+    want = hexbytes(g["record"])
+    n = int(g["numel"])
+    assert n == 2 ** 32 + 1000 and len(want) == 40
+    got = brute.record_from_sparse(g["name"], n, [int(t) for t in g["idx"].split()],
+                                   [int(t, 16) for t in g["vals"].split()], int(g["width"]))
+    assert got == want
