@@ -352,8 +352,33 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def launch_ranks(args):
+    """--gpus N with no WORLD_SIZE in the environment: re-exec this command under
+    torch.distributed.run, one rank per GPU (rendezvous on 127.0.0.1).  Under a launcher,
+    WORLD_SIZE must equal --gpus.  Returns an exit code, or None to run in this process."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus <= 1:
+            return None
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        print(f"bench: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+        return subprocess.call(cmd)
+    if int(world) != args.gpus:
+        print(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
+        return 2
+    return None
+
+
 def main():
     args = parse()
+    rc = launch_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -370,8 +395,18 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm_info = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        # the communicator as NCCL sees it (one all-reduce over it), logged per rank
+        probe = torch.ones(1, dtype=torch.int64, device=dev)
+        dist.all_reduce(probe)
+        comm_info = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+                     "ranks_seen_by_allreduce": int(probe.item()),
+                     "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
+        print(f"bench: rank {rank}/{world} on cuda:{local} {comm_info}", file=sys.stderr, flush=True)
+        if comm_info["ranks_seen_by_allreduce"] != world:
+            raise SystemExit(f"bench: NCCL all-reduce saw {comm_info['ranks_seen_by_allreduce']} ranks, expected {world}")
 
     specs, rho, pattern, desc = workload(args)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
@@ -621,7 +656,7 @@ def main():
     else:
         body_total, nnz_total, idx_total, naive_total = body_local, nnz_local, idx_local, naive_local
     k1_ms = acc.get("scan_ms", 0.0) / args.steps
-    k1_bytes = 2 * local_lanes * width + nnz_local * (2 + width)  # reads + slot writes
+    k1_bytes = 2 * local_lanes * width  # K1's algorithmic bytes = the 2wN it compares
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -689,6 +724,8 @@ def main():
         result["roofline"]["k1_share_of_step"] = round(k1_ms / ms_step, 4)
     if rank_view is not None:
         result["per_rank"] = rank_view
+    if comm_info is not None:
+        result["comm"] = comm_info
     result["config"]["host_sync"] = "end (steps enqueued back to back)" if pipelined else "every step"
     if world > 1:
         result["config"]["assembly"] = {"nvlink": "delta_assemble over NVLink (CUDA IPC), 2 body buffers",

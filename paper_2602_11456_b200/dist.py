@@ -107,6 +107,19 @@ def shift_table(rows, offset: int):
     return list(rebase(rows, offset))
 
 
+def _ipc_teardown(device, group):
+    """Release order for CUDA IPC mappings: every consumer drops its mappings (and lets the
+    garbage collector free the rebuilt tensors), then the producer reclaims what the
+    consumers released (torch.cuda.ipc_collect) before anything is freed or the process
+    exits — so no rank exits while a peer still maps its memory."""
+    import gc
+    gc.collect()
+    torch.cuda.synchronize(device)
+    dist.barrier(group=group)
+    torch.cuda.ipc_collect()
+    dist.barrier(group=group)
+
+
 class NvlinkAssembler:
     """S3 as one kernel over NVLink peer memory (delta_assemble): the root owns the
     assembled-body buffer ``buf``; every other rank maps it into its own address space with
@@ -161,7 +174,7 @@ class NvlinkAssembler:
         torch.cuda.synchronize(self.device)
         self.peer = None
         self.peers = []
-        dist.barrier(group=self.group)
+        _ipc_teardown(self.device, self.group)
 
 
 class RecordAssembler:
@@ -232,7 +245,7 @@ class RecordAssembler:
         torch.cuda.synchronize(self.device)
         self.peers = []
         self.pboard = self.proot_sizes = None
-        dist.barrier(group=self.group)
+        _ipc_teardown(self.device, self.group)
 
 
 class FlagAssembler:
@@ -283,5 +296,5 @@ class FlagAssembler:
     def close(self):
         torch.cuda.synchronize(self.device)
         self.peers, self.pboard = [], None
-        dist.barrier(group=self.group)
+        _ipc_teardown(self.device, self.group)
 

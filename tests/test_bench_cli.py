@@ -25,3 +25,27 @@ def test_reference_arm_json_line():
     for key in ("metric", "n_gpus", "steps", "warmup", "ms_per_step", "scaling", "vs_baseline",
                 "dtype", "data", "config"):
         assert key in line
+
+
+def test_gpus_flag_launches_ranks():
+    """--gpus N with no WORLD_SIZE re-execs under torch.distributed.run (N ranks on
+    127.0.0.1); the reference arm then prints one line from rank 0 with n_gpus == N."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--config", "M1", "--steps", "1", "--warmup", "0", "--cpu-seconds", "0.5"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "launching 2 ranks" in r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_world_size_mismatch_fails():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0", CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "1",
+                        "--config", "M1", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode != 0
+    assert "WORLD_SIZE=2 but --gpus 1" in r.stderr
