@@ -150,16 +150,32 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long acc = 0;
-        if (st->status == kOk) {
-            for (uint32_t k = 0; k < n; ++k) {
-                rec_chunk_begin[k] = acc;
-                acc += (recs[k].idx_len + kByteChunk - 1) / kByteChunk;
+    {   // chunk prefix over the records: block-wide exclusive scan, 256 records per round
+        __shared__ unsigned long long s_w[8];
+        const bool okst = st->status == kOk;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        unsigned long long carry = 0;
+        for (uint32_t b = 0; b < n; b += blockDim.x) {
+            const uint32_t k = b + threadIdx.x;
+            const unsigned long long x = (okst && k < n) ? (recs[k].idx_len + kByteChunk - 1) / kByteChunk : 0ull;
+            const unsigned long long inc = warp_inclusive_sum(x);
+            if (lane == 31) s_w[warp] = inc;
+            __syncthreads();
+            unsigned long long pre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const unsigned long long y = s_w[w];
+                if (w < warp) pre += y;
+                tot += y;
             }
+            if (k < n) rec_chunk_begin[k] = carry + pre + inc - x;
+            carry += tot;
+            __syncthreads();
         }
-        rec_chunk_begin[n] = acc;
-        st->n_chunks = acc;
+        if (threadIdx.x == 0) {
+            rec_chunk_begin[n] = carry;
+            st->n_chunks = carry;
+        }
     }
     __syncthreads();
     // chunk -> record map (one load per chunk in A2/A4 instead of a binary search)

@@ -7,8 +7,9 @@
 //                       straight into the tile's workspace slot (u16 lane offsets + raw
 //                       values) and the tile's change count.  No inter-CTA communication
 //                       and no shared-memory staging: a pure streaming pass.
-//   K1b k_tiles_gaps    warp per tile: first / last offset and the LEB128 byte count of the
-//                       gaps inside the tile (< 2^14 lanes: 1-2 bytes each).
+//                       From the tile's change bitmap (shared memory) K1 also derives the
+//                       first / last changed lane and the LEB128 bytes of the gaps inside the
+//                       tile (< 2^14 lanes: 1-2 bytes each).
 //   K2  k_tiles_reduce / k_blocks_scan / k_tiles_bytes / k_tiles_place
 //                       E3+E4+E5 sizes: scans over the (small) per-tile metadata — entry
 //                       prefix, nearest earlier non-empty tile (its last change is the
@@ -173,6 +174,12 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     __shared__ uint32_t s_warp[NWARP][NQ];
     __shared__ uint32_t s_pre[NWARP][NQ];
     __shared__ uint32_t s_tot[NQ];
+    // the tile's change bitmap in lane order (bit L & 63 of word L >> 6) and per-warp gap
+    // statistics: K1 derives the tile's first / last change and the LEB128 bytes of its
+    // in-tile gaps itself (no second pass over the slot offsets)
+    constexpr int NWORDS = LANES / 64;
+    __shared__ __align__(8) unsigned long long s_bits[NWORDS];
+    __shared__ uint32_t s_big[NWARP], s_first[NWARP], s_last[NWARP];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if constexpr (ADVANCE) {
@@ -244,6 +251,21 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
+    // bitmap: vector v = r THREADS + tid holds lanes [v LPV, v LPV + LPV) -> lane-order bits
+    {
+        uint8_t *sb8 = reinterpret_cast<uint8_t *>(s_bits);
+#pragma unroll
+        for (int r = 0; r < VECS; ++r) {
+            const uint32_t v = r * THREADS + tid;
+            if constexpr (H16) {  // lanes 0-3 at bits 8k+7, lanes 4-7 at bits 8k+3 -> one byte
+                const uint32_t u = (m[r] >> 7) & 0x01010101u, w = (m[r] >> 3) & 0x01010101u;
+                sb8[v] = (uint8_t)(((u * 0x01020408u) >> 24) | (((w * 0x01020408u) >> 20) & 0xF0u));
+            } else {  // 4 lanes per vector: an even/odd thread pair shares one byte
+                const uint32_t other = __shfl_xor_sync(0xffffffffu, m[r], 1);
+                if (!(tid & 1)) sb8[v >> 1] = (uint8_t)(m[r] | (other << 4));
+            }
+        }
+    }
     uint32_t inc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) inc[q] = warp_inclusive_sum(pk[q]);
@@ -252,6 +274,34 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         for (int q = 0; q < NQ; ++q) s_warp[warp][q] = inc[q];
     }
     __syncthreads();
+    // In-tile gap statistics from the bitmap: thread i owns word i (64 lanes).  Only the
+    // first change of a word can sit >= 64 lanes after its predecessor; it is a two-byte
+    // (>= 128-lane) gap iff the previous word is empty and either the word before it is
+    // empty too or 128 + b - (its highest lane) >= 128.  The tile's very first change also
+    // passes that test (no change before it): it is subtracted once below — its gap to the
+    // previous tile is K2's.
+    {
+        uint32_t big = 0, first = 0xFFFFFFFFu, last = 0;
+        if (tid < NWORDS) {
+            const unsigned long long X = s_bits[tid];
+            if (X) {
+                const unsigned long long p1 = tid >= 1 ? s_bits[tid - 1] : 0ull;
+                const unsigned long long p2 = tid >= 2 ? s_bits[tid - 2] : 0ull;
+                const uint32_t b = (uint32_t)__ffsll((long long)X) - 1u;
+                big = p1 ? 0u : (p2 ? (uint32_t)(b + __clzll((long long)p2) >= 63) : 1u);
+                first = 64u * tid + b;
+                last = 64u * tid + 63u - (uint32_t)__clzll((long long)X);
+            }
+        }
+        big = __reduce_add_sync(0xffffffffu, big);
+        first = __reduce_min_sync(0xffffffffu, first);
+        last = __reduce_max_sync(0xffffffffu, last);
+        if (lane == 0) {
+            s_big[warp] = big;
+            s_first[warp] = first;
+            s_last[warp] = last;
+        }
+    }
     // warp 0 scans the NWARP x NQ warp totals across warps (lane = NQ * warp + word)
     if (warp == 0) {
         const uint32_t x = s_warp[lane / NQ][lane % NQ];
@@ -280,7 +330,16 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
     // slot; lane offsets to shared memory (for the in-tile gaps below).
     const bool fits = c <= slot_cap;  // CTA-uniform; an overflowing tile is redone after regrowth
     if (tid == 0) {
-        meta[t] = TileMeta{c, 0, 0, 0, 0};  // first/last offsets and gap bytes: k_tiles_gaps
+        uint32_t big = 0, first = 0xFFFFFFFFu, last = 0;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) {
+            big += s_big[w];
+            first = min(first, s_first[w]);
+            last = max(last, s_last[w]);
+        }
+        // internal bytes = one per in-tile gap plus one more per gap >= 128 lanes (< 2^14 lanes:
+        // at most two LEB128 bytes); `big` counted the tile's first change once
+        meta[t] = c ? TileMeta{c, (uint16_t)first, (uint16_t)last, c - 1 + big - 1, 0} : TileMeta{0, 0, 0, 0, 0};
         if (!fits) {
             summary->overflow = 1;
             atomicMax(&summary->max_count, (unsigned long long)c);
@@ -430,71 +489,6 @@ k_scan_tiles_persist(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         scan_tile<W, 256, 8, false>(t, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val, meta, summary);
         __syncthreads();  // shared scratch is reused by the next tile
-    }
-}
-
-// ------------------------------------------------------------------------------ K1b
-// One warp per tile over the u16 lane offsets K1 left in the slot: the tile's first and
-// last change offsets and the LEB128 bytes of its internal gaps (each gap < 2^14 lanes:
-// 1 byte if < 128, else 2), i.e. (count - 1) + #{gaps >= 128}.
-// DENSE (chosen on the host when some tile has > 1024 changes): dense tiles read 8
-// consecutive offsets per lane; the sparse variant keeps its lean register budget.
-template <bool DENSE>
-__global__ void __launch_bounds__(256)
-k_tiles_gaps(TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t slot_cap,
-             const uint8_t *__restrict__ slot_bytes, const ExtractSummary *summary) {
-    if (summary->overflow) return;
-    const int lane = threadIdx.x & 31;
-    const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t t = wg; t < ntiles; t += nw) {
-        const uint32_t c = meta[t].count;
-        if (c == 0) continue;
-        const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
-        uint32_t big = 0;
-        if (c <= 256) {  // every offset of the tile loaded up front, predecessors by shuffle
-            uint32_t o[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const uint32_t i = r * 32 + lane;
-                o[r] = i < c ? (uint32_t)so[i] : 0u;
-            }
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                if ((uint32_t)r * 32u >= c) break;
-                const uint32_t i = r * 32 + lane;
-                uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
-                const uint32_t carry = __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31);
-                if (lane == 0) prev = carry;
-                big += (i >= 1 && i < c && o[r] - prev >= 128u);
-            }
-        } else if constexpr (!DENSE) {
-            for (uint32_t i = 1 + lane; i < c; i += 32) big += (uint32_t)(so[i] - so[i - 1]) >= 128u;
-        } else {  // dense tile: 8 consecutive offsets per lane (one 16-byte load; slots hold a
-                  // power of two >= 512 entries, so the load stays inside), 256 per round
-            uint32_t carry = 0;
-            for (uint32_t b = 0; b < c; b += 256) {
-                const uint32_t i0 = b + 8 * lane;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (i0 < c) v = *reinterpret_cast<const uint4 *>(so + i0);
-                const uint32_t o[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
-                                       v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
-                uint32_t prev = __shfl_up_sync(0xffffffffu, o[7], 1);
-                if (lane == 0) prev = carry;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t i = i0 + k;
-                    big += (i >= 1 && i < c && o[k] - (k ? o[k - 1] : prev) >= 128u);
-                }
-                carry = __shfl_sync(0xffffffffu, o[7], 31);
-            }
-        }
-        big = __reduce_add_sync(0xffffffffu, big);
-        if (lane == 0) {
-            meta[t].first_off = so[0];
-            meta[t].last_off = so[c - 1];
-            meta[t].internal_bytes = c - 1 + big;
-        }
     }
 }
 
@@ -1008,9 +1002,6 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
                                       static_cast<LT *>(a.slot_val), a.meta, a.summary, a.redo_cap);
     }
     if (ev) cudaEventRecord(ev[1], s);
-    if (!a.index_codec)  // the fixed-width codec needs no gap statistics
-        (a.slot_cap > kDenseEmitSlot ? k_tiles_gaps<true> : k_tiles_gaps<false>)<<<a.persist_ctas, 256, 0, s>>>(
-            a.meta, a.ntiles, a.slot_cap, a.slot_bytes, a.summary);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
     k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);

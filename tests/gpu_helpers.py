@@ -72,6 +72,7 @@ def oracle_check_all(tensors, body: torch.Tensor, table, group_bytes: int = 12 <
     checked; raises AssertionError listing the first mismatches."""
     import multiprocessing as mp
     import os
+    import warnings
     global _FULL
     rows = [tuple(r) for r in table]
     assert len(rows) == len(tensors)
@@ -92,11 +93,13 @@ def oracle_check_all(tensors, body: torch.Tensor, table, group_bytes: int = 12 <
         olds = {k: to_np(fused(tensors[k][1])) for k in range(k0, k1)}
         news = {k: to_np(fused(tensors[k][2])) for k in range(k0, k1)}
         _FULL = (names, olds, news, body_np, rows, mode)
-        with mp.get_context("fork").Pool(min(procs, k1 - k0)) as pool:
-            for k, err in pool.imap_unordered(_full_task, range(k0, k1)):
-                checked += 1
-                if err:
-                    errors.append(err)
+        with warnings.catch_warnings():  # the forked workers run numpy only (no CUDA, no threads)
+            warnings.simplefilter("ignore", DeprecationWarning)
+            with mp.get_context("fork").Pool(min(procs, k1 - k0)) as pool:
+                for k, err in pool.imap_unordered(_full_task, range(k0, k1)):
+                    checked += 1
+                    if err:
+                        errors.append(err)
         _FULL = None
         del olds, news
         k0 = k1
