@@ -83,7 +83,7 @@ def parse():
     p.add_argument("--prefetch-tiles", type=int, default=0, help="K1 L2 prefetch distance in tiles + 1 (0 = default)")
     p.add_argument("--scatter-order", type=int, default=0, help="1 thread-major, 2 entry-major (0 = default)")
     p.add_argument("--scan-kernel", type=int, default=0,
-                   help="1 = one CTA per tile, 2 = persistent TMA pipeline (0 = library default)")
+                   help="compare kernel form: 1 (the only one; 0 = library default)")
     p.add_argument("--tensors", type=int, default=0,
                    help="profiling only: keep the first N tensors of the config")
     return p.parse_args()

@@ -396,10 +396,9 @@ enum {
     DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode kernel, CTAs per SM (default 8) */
     DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 8) */
     DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
-                                        vectors (default); 4 = as 1 with 512 threads x 4 vectors;
-                                        5 = as 1, persistent (3 CTAs per SM loop over tiles).
-                                        2 and 3 (TMA pipeline, 128-byte runs) were measured slower
-                                        and retired: DELTA_EINVAL */
+                                        vectors, bitmap compaction (the only form; the retired
+                                        variants 2-5 — TMA pipeline, 128-byte runs, 512 x 4,
+                                        persistent — were measured slower): DELTA_EINVAL */
     DELTA_OPT_SCATTER_CTAS_PER_SM = 4, /* grid of the apply scatter kernel, CTAs per SM (default 5: one full wave at its shared-memory limit) */
     DELTA_OPT_PREFETCH_TILES = 5,     /* 1 + distance, in tiles, of the L2 bulk prefetch issued by
                                          the default compare kernel (1 = off; default: one wave of

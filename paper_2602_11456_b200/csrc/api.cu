@@ -72,8 +72,8 @@ struct delta_ctx {
     unsigned long long total_lanes = 0;
     DevBuf tiles, name_len, name_off, names, numel, tensor_first_tile;
     // ---- extract workspace
-    DevBuf slot_bytes, slot_val, meta, tile_entry, tile_byte, tile_pred, tile_bytes, tile_plan, blk_a, blk_key,
-        entry_begin, tensor_byte_begin, table, summary, sticky;
+    DevBuf slot_bytes, slot_val, meta, tile_plan, blk_agg, tensor_bases, entry_begin, tensor_byte_begin, table,
+        summary, sticky;
     uint32_t slot_cap = 0;          // entries per tile slot (grows on overflow)
     bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
     // delta_extract_async: readback of the summary lands in h_summary when ev_extract fires
@@ -199,8 +199,7 @@ void delta_ctx_destroy(delta_ctx *c) {
     for (DevBuf *b : mbufs) b->release();
     DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
-                      &c->tile_entry, &c->tile_byte, &c->tile_pred, &c->tile_bytes, &c->tile_plan, &c->blk_a,
-                      &c->blk_key, &c->entry_begin, &c->tensor_byte_begin, &c->table,
+                      &c->tile_plan, &c->blk_agg, &c->tensor_bases, &c->entry_begin, &c->tensor_byte_begin, &c->table,
                       &c->summary, &c->sticky, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->asm_off, &c->dg_ws, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
@@ -234,8 +233,8 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
     if (option == DELTA_OPT_APPLY_CTAS_PER_SM) c->apply_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_EMIT_CTAS_PER_SM) c->emit_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_SCAN_KERNEL) {
-        if (value == 2 || value == 3 || value > 5) return DELTA_EINVAL;  // 2, 3: retired variants
-        c->scan_kernel = (int)value - 1;
+        if (value != 1) return DELTA_EINVAL;  // 2-5: retired variants (measured slower)
+        c->scan_kernel = 0;
     }
     else if (option == DELTA_OPT_SCATTER_CTAS_PER_SM) c->scatter_ctas_per_sm = (int)value;
     else if (option == DELTA_OPT_PREFETCH_TILES) c->prefetch_tiles = (int)value - 1;
@@ -492,13 +491,9 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.slot_bytes = ctx->slot_bytes.as<uint8_t>();
     a.slot_val = ctx->slot_val.p;
     a.meta = ctx->meta.as<TileMeta>();
-    a.tile_entry = ctx->tile_entry.as<unsigned long long>();
-    a.tile_byte = ctx->tile_byte.as<unsigned long long>();
-    a.tile_pred = ctx->tile_pred.as<unsigned long long>();
-    a.tile_bytes_tmp = ctx->tile_bytes.as<unsigned int>();
     a.plan = ctx->tile_plan.as<TileEmit>();
-    a.blk_a = ctx->blk_a.as<unsigned long long>();
-    a.blk_key = ctx->blk_key.as<long long>();
+    a.agg = ctx->blk_agg.as<BlockAgg>();
+    a.bases = ctx->tensor_bases.as<TensorBase>();
     a.tensor_first_tile = ctx->tensor_first_tile.as<uint32_t>();
     a.entry_begin = ctx->entry_begin.as<unsigned long long>();
     a.tensor_byte_begin = ctx->tensor_byte_begin.as<unsigned long long>();
@@ -511,7 +506,6 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.width = ctx->width;
     a.persist_ctas = ctx->sm_count * ctx->emit_ctas_per_sm;
     a.sm_count = ctx->sm_count;
-    a.scan_kernel = ctx->scan_kernel;
     a.prefetch_dist = (uint32_t)(ctx->prefetch_tiles < 0 ? ctx->sm_count * 3 : ctx->prefetch_tiles);
     a.mode = ctx->mode;
     a.index_codec = ctx->index_codec;
@@ -533,13 +527,9 @@ static int prepare_scan(delta_ctx *ctx) {
     const uint32_t nblk = (nt + kTileBlock - 1) / kTileBlock;
     const uint32_t lanes_per_tile = kTileBytes / ctx->width;
     GROW(ctx->meta, (size_t)nt * sizeof(TileMeta));
-    GROW(ctx->tile_entry, (size_t)nt * 8);
-    GROW(ctx->tile_byte, (size_t)nt * 8);
-    GROW(ctx->tile_pred, (size_t)nt * 8);
-    GROW(ctx->tile_bytes, (size_t)nt * 4);
     GROW(ctx->tile_plan, (size_t)nt * sizeof(TileEmit));
-    GROW(ctx->blk_a, (size_t)nblk * 2 * 8);
-    GROW(ctx->blk_key, (size_t)nblk * 8);
+    GROW(ctx->blk_agg, (size_t)std::max<uint32_t>(nblk, 1) * sizeof(BlockAgg));
+    GROW(ctx->tensor_bases, (size_t)std::max<uint32_t>(T, 1) * sizeof(TensorBase));
     GROW(ctx->entry_begin, (size_t)(T + 1) * 8);
     GROW(ctx->tensor_byte_begin, (size_t)(T + 1) * 8);
     GROW(ctx->table, (size_t)std::max<uint32_t>(T, 1) * sizeof(RecordRow));

@@ -67,65 +67,15 @@ __device__ __forceinline__ void set_lane(uint4 &v, int j, uint32_t x) {
     }
 }
 
-// Bit j set iff lane j of the two vectors differs as an unsigned integer (reading R2).
-// 16-bit lanes without compares: for x = a ^ b, ((x & 0x7FFF7FFF) + 0x7FFF7FFF) | x has
-// bit 15 (31) set iff the low (high) half of x is nonzero; PRMT gathers those bytes and a
-// multiply packs their top bits into lane order.
-template <int W>
-__device__ __forceinline__ uint32_t diff_mask(const uint4 &a, const uint4 &b) {
-    const uint32_t x0 = a.x ^ b.x, x1 = a.y ^ b.y, x2 = a.z ^ b.z, x3 = a.w ^ b.w;
-    if constexpr (W == 2) {
-        const uint32_t f0 = ((x0 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x0;
-        const uint32_t f1 = ((x1 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x1;
-        const uint32_t f2 = ((x2 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x2;
-        const uint32_t f3 = ((x3 & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x3;
-        const uint32_t u = (__byte_perm(f0, f1, 0x7531) >> 7) & 0x01010101u;  // lanes 0..3
-        const uint32_t v = (__byte_perm(f2, f3, 0x7531) >> 7) & 0x01010101u;  // lanes 4..7
-        return ((u * 0x01020408u) >> 24) | (((v * 0x01020408u) >> 20) & 0xF0u);
-    } else {
-        return (uint32_t)(x0 != 0) | ((uint32_t)(x1 != 0) << 1) | ((uint32_t)(x2 != 0) << 2) |
-               ((uint32_t)(x3 != 0) << 3);
-    }
-}
-
-// 16-bit lanes: two masks per vector, lanes 0-3 (words x, y) and lanes 4-7 (words z, w),
-// lane k of a half at bit 8k + 7 — ascending bit order is lane order, and the pair of
-// words holding the half is what PRMT extracts lane k from (selector 0x22 k + 0x10).
-// f = ((x & 0x7FFF7FFF) + 0x7FFF7FFF) | x has bit 15 (31) set iff the low (high) 16-bit
-// half of x = a ^ b is nonzero; PRMT gathers the four high bytes of a half.
+// f = ((x & 0x7FFF7FFF) + 0x7FFF7FFF) | x, x = a ^ b, has bit 15 (31) set iff the low (high)
+// 16-bit half of x is nonzero, i.e. iff that bf16 lane differs bitwise (reading R2): two LOP3
+// and an add, no compares.
 __device__ __forceinline__ uint32_t nz16_hi(uint32_t a, uint32_t b) {
     uint32_t t, f;
     asm("lop3.b32 %0, %1, %2, 0x7FFF7FFF, 0x28;" : "=r"(t) : "r"(a), "r"(b));  // (a ^ b) & C
     t += 0x7FFF7FFFu;
     asm("lop3.b32 %0, %1, %2, %3, 0xF6;" : "=r"(f) : "r"(t), "r"(a), "r"(b));  // t | (a ^ b)
     return f;
-}
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-    return d;
-}
-__device__ __forceinline__ void diff_mask16(const uint4 &a, const uint4 &b, uint32_t &lo, uint32_t &hi) {
-    lo = __byte_perm(nz16_hi(a.x, b.x), nz16_hi(a.y, b.y), 0x7531) & 0x80808080u;
-    hi = __byte_perm(nz16_hi(a.z, b.z), nz16_hi(a.w, b.w), 0x7531) & 0x80808080u;
-}
-
-template <int NW, typename T>
-__device__ __forceinline__ T block_excl_scan(T v, T *s_warp, T &total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const T inc = warp_inclusive_sum(v);
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    T pre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        const T x = s_warp[w];
-        if (w < warp) pre += x;
-        tot += x;
-    }
-    __syncthreads();
-    total = tot;
-    return pre + inc - v;
 }
 
 template <typename T>
@@ -150,37 +100,59 @@ __device__ __forceinline__ T warp_inclusive_max(T v) {
 }
 
 // ------------------------------------------------------------------------------ K1
-// THREADS x VECS = 2048 16-byte vectors per operand per tile (32 KiB); instantiated as
-// 256 x 8 (3 CTAs / SM) and 512 x 4 (2 CTAs / SM, more warps, fewer registers each).
-// ADVANCE (extract-and-advance, NEXT f3): every changed lane of old is overwritten with the
-// new lane while the tile's sectors are still in L2, so old == new afterwards (the trainer's
-// shadow copy advances to the new version without a second pass).  Old is then read with
-// coherent loads, and on a retry after slot regrowth (redo_cap != 0) only the tiles that
-// overflowed a redo_cap-entry slot run again (the others were compacted AND advanced).
-template <int W, int THREADS, int VECS, bool DENSE, bool ADDITIVE = false, bool ADVANCE = false>
-__device__ __forceinline__ void
-scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
-          uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
-          typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
-          ExtractSummary *summary, uint32_t redo_cap = 0) {
+// One CTA per tile: THREADS x VECS = 2048 16-byte vectors per operand (32 KiB of old + 32
+// KiB of new), streaming loads into registers, then everything else from shared memory:
+//   1. each thread turns its 8 vector pairs into lane-order change masks (bitwise lane
+//      inequality, reading R2) and writes them into the tile's change bitmap (lane L is bit
+//      L & 63 of word L >> 6), and stages the new vectors that hold a change;
+//   2. thread i owns bitmap word i (64 consecutive lanes): one block scan of its change
+//      count (packed with its "two-byte gap" flag) gives every change its rank in lane order
+//      (the ordered compaction) and the tile's totals;
+//   3. thread i emits its word's changes in order: u16 lane offset + value into the tile's
+//      slot.  One loop per thread over set bits (instead of one per half-vector), so a warp
+//      iterates about as often as its busiest word has changes.
+// Gap statistics for the LEB128 byte count come from the same bitmap: only the first change
+// of a word can sit >= 64 lanes after its predecessor, and it is a two-byte (>= 128-lane) gap
+// iff the previous word is empty and the word before it is empty too or its highest change
+// is far enough back.  The tile's very first change also passes that test (nothing before it
+// in the tile): it is subtracted once — its gap to the previous tile is K2's.
+// ADVANCE (extract-and-advance, NEXT f3): every 32-byte sector of old holding a change is
+// rewritten with the new lanes while the tile is in registers, so old == new afterwards; a
+// retry after slot regrowth (redo_cap != 0) re-runs only the tiles that overflowed.
+// ADDITIVE (reading R17): the staged vectors hold new - old in the lane's float type.
+template <int W>
+__device__ __forceinline__ uint32_t lane_mask(const uint4 &a, const uint4 &b) {
+    if constexpr (W == 2) {  // bit j (lane order) iff 16-bit lane j differs: nz16_hi marks
+                             // nonzero halves in bits 15 / 31, PRMT gathers those bytes
+        const uint32_t p = __byte_perm(nz16_hi(a.x, b.x), nz16_hi(a.y, b.y), 0x7531);  // lanes 0..3
+        const uint32_t q = __byte_perm(nz16_hi(a.z, b.z), nz16_hi(a.w, b.w), 0x7531);  // lanes 4..7
+        const uint32_t u = (p >> 7) & 0x01010101u, v = (q >> 7) & 0x01010101u;
+        return ((u * 0x01020408u) >> 24) | (((v * 0x01020408u) >> 20) & 0xF0u);
+    } else {
+        return (uint32_t)(a.x != b.x) | ((uint32_t)(a.y != b.y) << 1) | ((uint32_t)(a.z != b.z) << 2) |
+               ((uint32_t)(a.w != b.w) << 3);
+    }
+}
+
+template <int W, bool ADDITIVE = false, bool ADVANCE = false>
+__global__ void __launch_bounds__(256, 3)
+k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist, uint32_t slot_cap,
+             uint8_t *__restrict__ slot_bytes, typename LaneOf<W>::T *__restrict__ slot_val,
+             TileMeta *__restrict__ meta, ExtractSummary *summary, uint32_t redo_cap) {
     using LT = typename LaneOf<W>::T;
+    constexpr int THREADS = 256, VECS = 8;
     constexpr int LPV = 16 / W;                  // lanes per 16-byte vector
     constexpr int LANES = THREADS * VECS * LPV;  // lanes per tile
     constexpr int NWARP = THREADS / 32;
-    constexpr int NQ = VECS / 2;                 // packed count words (two 16-bit fields each)
+    constexpr int NWORDS = LANES / 64;           // bitmap words = threads that emit
     static_assert(THREADS * VECS * 16 == kTileBytes, "tile geometry is fixed by the plan");
     static_assert(LANES <= 65536, "lane offsets are u16");
-    static_assert(NWARP * NQ == 32, "warp-0 scan covers NWARP warps x NQ words");
-    __shared__ uint32_t s_warp[NWARP][NQ];
-    __shared__ uint32_t s_pre[NWARP][NQ];
-    __shared__ uint32_t s_tot[NQ];
-    // the tile's change bitmap in lane order (bit L & 63 of word L >> 6) and per-warp gap
-    // statistics: K1 derives the tile's first / last change and the LEB128 bytes of its
-    // in-tile gaps itself (no second pass over the slot offsets)
-    constexpr int NWORDS = LANES / 64;
+    __shared__ __align__(16) uint4 s_new[THREADS * VECS];  // changed vectors (new, or new - old)
     __shared__ __align__(8) unsigned long long s_bits[NWORDS];
-    __shared__ uint32_t s_big[NWARP], s_first[NWARP], s_last[NWARP];
+    __shared__ uint32_t s_wsum[NWARP];
+    __shared__ int s_wfirst[NWARP], s_wlast[NWARP];
 
+    const uint32_t t = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if constexpr (ADVANCE) {
         if (redo_cap && meta[t].count <= redo_cap) return;  // done (and advanced) by the first pass
@@ -221,8 +193,9 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         }
     }
 
-    // (after this tile's loads are in flight) L2 prefetch of a tile about prefetch_dist tiles ahead (CTAs run roughly in blockIdx
-    // order): the TMA engine keeps DRAM streaming while this CTA's loads hit L2.
+    // (after this tile's loads are in flight) L2 prefetch of a tile about prefetch_dist tiles
+    // ahead (CTAs run roughly in blockIdx order): the TMA engine keeps DRAM streaming while
+    // this CTA's loads hit L2.
     if (prefetch_dist && tid == 0 && t + prefetch_dist < ntiles) {
         const TileDesc p = tiles[t + prefetch_dist];
         if (p.flags_tensor & kTileAligned) {
@@ -234,118 +207,29 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
         }
     }
 
-    // Per-vector change masks; VECS counts (<= LPV each) packed as 16-bit fields into NQ
-    // words so one block scan yields every vector's rank base.
-    constexpr bool H16 = (W == 2);  // 16-bit lanes: lanes 0-3 at bits 8k+7, lanes 4-7 at bits 8k+3
+    // ---- 1. change masks -> bitmap; stage the vectors that hold a change
     uint32_t m[VECS];
-    uint32_t pk[NQ];
+    uint8_t *sb8 = reinterpret_cast<uint8_t *>(s_bits);
 #pragma unroll
     for (int r = 0; r < VECS; ++r) {
-        if constexpr (H16) {
-            uint32_t lo, hi;
-            diff_mask16(vo[r], vn[r], lo, hi);
-            m[r] = lo | (hi >> 4);
-        } else {
-            m[r] = diff_mask<W>(vo[r], vn[r]);
+        const uint32_t v = r * THREADS + tid;
+        m[r] = lane_mask<W>(vo[r], vn[r]);
+        if constexpr (W == 2) {
+            sb8[v] = (uint8_t)m[r];
+        } else {  // 4 lanes per vector: an even/odd thread pair shares one byte
+            const uint32_t other = __shfl_xor_sync(0xffffffffu, m[r], 1);
+            if (!(tid & 1)) sb8[v >> 1] = (uint8_t)(m[r] | (other << 4));
         }
-    }
+        if (m[r]) {
+            uint4 x = vn[r];
+            if constexpr (ADDITIVE) {  // the arithmetic difference new - old, changed lanes
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) pk[q] = __popc(m[2 * q]) | (__popc(m[2 * q + 1]) << 16);
-    // bitmap: vector v = r THREADS + tid holds lanes [v LPV, v LPV + LPV) -> lane-order bits
-    {
-        uint8_t *sb8 = reinterpret_cast<uint8_t *>(s_bits);
-#pragma unroll
-        for (int r = 0; r < VECS; ++r) {
-            const uint32_t v = r * THREADS + tid;
-            if constexpr (H16) {  // lanes 0-3 at bits 8k+7, lanes 4-7 at bits 8k+3 -> one byte
-                const uint32_t u = (m[r] >> 7) & 0x01010101u, w = (m[r] >> 3) & 0x01010101u;
-                sb8[v] = (uint8_t)(((u * 0x01020408u) >> 24) | (((w * 0x01020408u) >> 20) & 0xF0u));
-            } else {  // 4 lanes per vector: an even/odd thread pair shares one byte
-                const uint32_t other = __shfl_xor_sync(0xffffffffu, m[r], 1);
-                if (!(tid & 1)) sb8[v >> 1] = (uint8_t)(m[r] | (other << 4));
+                for (int j = 0; j < LPV; ++j)
+                    if ((m[r] >> j) & 1u) set_lane<W>(x, j, lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true));
             }
+            s_new[v] = x;
         }
     }
-    uint32_t inc[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) inc[q] = warp_inclusive_sum(pk[q]);
-    if (lane == 31) {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) s_warp[warp][q] = inc[q];
-    }
-    __syncthreads();
-    // In-tile gap statistics from the bitmap: thread i owns word i (64 lanes).  Only the
-    // first change of a word can sit >= 64 lanes after its predecessor; it is a two-byte
-    // (>= 128-lane) gap iff the previous word is empty and either the word before it is
-    // empty too or 128 + b - (its highest lane) >= 128.  The tile's very first change also
-    // passes that test (no change before it): it is subtracted once below — its gap to the
-    // previous tile is K2's.
-    {
-        uint32_t big = 0, first = 0xFFFFFFFFu, last = 0;
-        if (tid < NWORDS) {
-            const unsigned long long X = s_bits[tid];
-            if (X) {
-                const unsigned long long p1 = tid >= 1 ? s_bits[tid - 1] : 0ull;
-                const unsigned long long p2 = tid >= 2 ? s_bits[tid - 2] : 0ull;
-                const uint32_t b = (uint32_t)__ffsll((long long)X) - 1u;
-                big = p1 ? 0u : (p2 ? (uint32_t)(b + __clzll((long long)p2) >= 63) : 1u);
-                first = 64u * tid + b;
-                last = 64u * tid + 63u - (uint32_t)__clzll((long long)X);
-            }
-        }
-        big = __reduce_add_sync(0xffffffffu, big);
-        first = __reduce_min_sync(0xffffffffu, first);
-        last = __reduce_max_sync(0xffffffffu, last);
-        if (lane == 0) {
-            s_big[warp] = big;
-            s_first[warp] = first;
-            s_last[warp] = last;
-        }
-    }
-    // warp 0 scans the NWARP x NQ warp totals across warps (lane = NQ * warp + word)
-    if (warp == 0) {
-        const uint32_t x = s_warp[lane / NQ][lane % NQ];
-        uint32_t y = x;
-#pragma unroll
-        for (int o = NQ; o < 32; o <<= 1) {
-            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += z;
-        }
-        s_pre[lane / NQ][lane % NQ] = y - x;
-        if (lane >= 32 - NQ) s_tot[lane % NQ] = y;
-    }
-    __syncthreads();
-    uint32_t pre[NQ], tot[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        pre[q] = s_pre[warp][q];
-        tot[q] = s_tot[q];
-    }
-    uint32_t c = 0;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) c += (tot[q] & 0xFFFFu) + (tot[q] >> 16);
-
-    // Ordered compaction: entry (r, tid, j) gets rank sum_{r'<r} tot_r' + prefix_r(tid) +
-    // popc(mask below j) — lane order.  Values go straight from registers to the tile's
-    // slot; lane offsets to shared memory (for the in-tile gaps below).
-    const bool fits = c <= slot_cap;  // CTA-uniform; an overflowing tile is redone after regrowth
-    if (tid == 0) {
-        uint32_t big = 0, first = 0xFFFFFFFFu, last = 0;
-#pragma unroll
-        for (int w = 0; w < NWARP; ++w) {
-            big += s_big[w];
-            first = min(first, s_first[w]);
-            last = max(last, s_last[w]);
-        }
-        // internal bytes = one per in-tile gap plus one more per gap >= 128 lanes (< 2^14 lanes:
-        // at most two LEB128 bytes); `big` counted the tile's first change once
-        meta[t] = c ? TileMeta{c, (uint16_t)first, (uint16_t)last, c - 1 + big - 1, 0} : TileMeta{0, 0, 0, 0, 0};
-        if (!fits) {
-            summary->overflow = 1;
-            atomicMax(&summary->max_count, (unsigned long long)c);
-        }
-    }
-    if (!fits) return;
     if constexpr (ADVANCE) {
         // old <- new where anything changed: a thread pair (tid, tid ^ 1) holds one 32-byte
         // sector; if either half changed both store their whole 16-byte vector (a full-sector
@@ -360,87 +244,77 @@ scan_tile(const uint32_t t, const TileDesc *__restrict__ tiles, uint32_t ntiles,
             if (aligned && any && (v + 1) * LPV <= nl) {
                 reinterpret_cast<uint4 *>(op)[v] = vn[r];
             } else if (m[r]) {
-                for (int j = 0; j < LPV && v * LPV + j < nl; ++j) {
-                    const uint32_t bit = (W == 2) ? (j < 4 ? 8 * j + 7 : 8 * (j - 4) + 3) : j;
-                    if ((m[r] >> bit) & 1u) op[v * LPV + j] = (LT)lane_of<W>(vn[r], j);
-                }
+                for (int j = 0; j < LPV && v * LPV + j < nl; ++j)
+                    if ((m[r] >> j) & 1u) op[v * LPV + j] = (LT)lane_of<W>(vn[r], j);
             }
         }
     }
+    __syncthreads();
+
+    // ---- 2. word i: change count + two-byte-gap flag, block scan -> ranks and tile totals
+    unsigned long long X = 0;
+    uint32_t val = 0;
+    if (tid < NWORDS) {
+        X = s_bits[tid];
+        if (X) {
+            const unsigned long long p1 = tid >= 1 ? s_bits[tid - 1] : 0ull;
+            const unsigned long long p2 = tid >= 2 ? s_bits[tid - 2] : 0ull;
+            const uint32_t b = (uint32_t)__ffsll((long long)X) - 1u;
+            const uint32_t big = p1 ? 0u : (p2 ? (uint32_t)(b + __clzll((long long)p2) >= 63) : 1u);
+            val = (uint32_t)__popcll((long long)X) | (big << 16);  // counts <= 16384, flags <= 256
+        }
+    }
+    const uint32_t inc = warp_inclusive_sum(val);
+    const uint32_t bw = __ballot_sync(0xffffffffu, X != 0);
+    if (lane == 31) s_wsum[warp] = inc;
+    if (lane == 0) {
+        s_wfirst[warp] = bw ? 32 * warp + __ffs(bw) - 1 : -1;
+        s_wlast[warp] = bw ? 32 * warp + 31 - __clz(bw) : -1;
+    }
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) {
+        const uint32_t y = s_wsum[w];
+        pre += w < warp ? y : 0u;
+        tot += y;
+    }
+    const uint32_t c = tot & 0xFFFFu;
+    const bool fits = c <= slot_cap;  // CTA-uniform; an overflowing tile is redone after regrowth
+    if (tid == 0) {
+        TileMeta mt{0, 0, 0, 0, 0};
+        if (c) {
+            int fw = -1, lw = -1;
+#pragma unroll
+            for (int w = 0; w < NWARP; ++w) {
+                if (fw < 0) fw = s_wfirst[w];
+                if (s_wlast[w] >= 0) lw = s_wlast[w];
+            }
+            // internal bytes = one per in-tile gap, one more per gap >= 128 lanes (< 2^14
+            // lanes: at most two LEB128 bytes); the flag total counted the first change once
+            mt = TileMeta{c, (uint16_t)(64 * fw + __ffsll((long long)s_bits[fw]) - 1),
+                          (uint16_t)(64 * lw + 63 - __clzll((long long)s_bits[lw])), c - 1 + (tot >> 16) - 1, 0};
+        }
+        meta[t] = mt;
+        if (!fits) {
+            summary->overflow = 1;
+            atomicMax(&summary->max_count, (unsigned long long)c);
+        }
+    }
+    if (!fits) return;
+
+    // ---- 3. ordered emission of word tid's changes
+    uint32_t pos = (pre + inc - val) & 0xFFFFu;
     LT *sv = slot_val + (size_t)t * slot_cap;
     uint16_t *sg = reinterpret_cast<uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
-    uint32_t rbase = 0;
-#pragma unroll
-    for (int r = 0; r < VECS; ++r) {
-        const int q = r >> 1, sh = (r & 1) * 16;
-        const uint32_t p0 = rbase + (((pre[q] + inc[q] - pk[q]) >> sh) & 0xFFFFu);
-        rbase += (tot[q] >> sh) & 0xFFFFu;
-        uint16_t *so = sg + p0;
-        LT *vp = sv + p0;
-        if constexpr (H16) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t mm = (h ? m[r] << 4 : m[r]) & 0x80808080u;
-                const uint32_t na = h ? vn[r].z : vn[r].x, nb = h ? vn[r].w : vn[r].y;
-                const uint32_t oa = h ? vo[r].z : vo[r].x, ob = h ? vo[r].w : vo[r].y;
-                const uint32_t obase = (r * THREADS + tid) * LPV + 4 * h;
-                auto put = [&](uint32_t k, uint32_t sel) {
-                    *so++ = (uint16_t)(obase + k);
-                    const uint32_t nv = prmt(na, nb, sel);
-                    if constexpr (ADDITIVE)  // the arithmetic difference new - old
-                        *vp++ = (LT)lane_combine<W>(nv & 0xFFFFu, prmt(oa, ob, sel) & 0xFFFFu, true);
-                    else
-                        *vp++ = (LT)nv;
-                };
-                if constexpr (DENSE) {  // four predicated steps, no divergent loop
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (mm & (0x80u << (8 * k))) put(k, 0x22u * k + 0x10u);
-                } else {
-                    // 32-bit slot indices off the slot bases (no 64-bit pointer chains)
-                    uint32_t pos = (uint32_t)(so - sg);
-                    so += __popc(mm);
-                    vp += __popc(mm);
-                    while (mm) {
-                        const uint32_t b = (uint32_t)__ffs(mm) - 1;  // 8k + 7
-                        mm &= mm - 1;
-                        const uint32_t k = b >> 3;
-                        const uint32_t sel = __funnelshift_r(0x76543210u, 0u, b - 7);
-                        const uint32_t nv = prmt(na, nb, sel);
-                        sg[pos] = (uint16_t)(obase + k);
-                        if constexpr (ADDITIVE)
-                            sv[pos] = (LT)lane_combine<W>(nv & 0xFFFFu, prmt(oa, ob, sel) & 0xFFFFu, true);
-                        else
-                            sv[pos] = (LT)nv;
-                        ++pos;
-                    }
-                }
-            }
-        } else {
-            uint32_t mm = m[r];
-            uint32_t pos = (uint32_t)(so - sg);  // 32-bit slot indices (no pointer chains)
-            while (mm) {
-                const int j = __ffs(mm) - 1;
-                mm &= mm - 1;
-                sg[pos] = (uint16_t)((r * THREADS + tid) * LPV + j);
-                if constexpr (ADDITIVE)
-                    sv[pos] = (LT)lane_combine<W>(lane_of<W>(vn[r], j), lane_of<W>(vo[r], j), true);
-                else
-                    sv[pos] = (LT)lane_of<W>(vn[r], j);
-                ++pos;
-            }
-        }
+    const LT *sn = reinterpret_cast<const LT *>(s_new);
+    while (X) {
+        const uint32_t L = 64u * tid + (uint32_t)__ffsll((long long)X) - 1u;
+        X &= X - 1;
+        sg[pos] = (uint16_t)L;
+        sv[pos] = sn[L];
+        ++pos;
     }
-}
-
-template <int W, int THREADS, int VECS, int MINB, bool DENSE, bool ADDITIVE = false, bool ADVANCE = false>
-__global__ void __launch_bounds__(THREADS, MINB)
-k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
-             uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
-             typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
-             ExtractSummary *summary, uint32_t redo_cap) {
-    scan_tile<W, THREADS, VECS, DENSE, ADDITIVE, ADVANCE>(blockIdx.x, tiles, ntiles, prefetch_dist, slot_cap,
-                                                          slot_bytes, slot_val, meta, summary, redo_cap);
 }
 
 // Slot regrowth that keeps the compaction of the tiles that fitted (extract-and-advance:
@@ -478,224 +352,239 @@ cudaError_t launch_slots_regrow(const TileMeta *meta, uint32_t ntiles, int width
     return cudaGetLastError();
 }
 
-// Persistent form: 3 CTAs per SM loop over the tiles (t = CTA, CTA + grid, ...), no
-// per-tile CTA launch.
-template <int W>
-__global__ void __launch_bounds__(256, 3)
-k_scan_tiles_persist(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist,
-                     uint32_t slot_cap, uint8_t *__restrict__ slot_bytes,
-                     typename LaneOf<W>::T *__restrict__ slot_val, TileMeta *__restrict__ meta,
-                     ExtractSummary *summary) {
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        scan_tile<W, 256, 8, false>(t, tiles, ntiles, prefetch_dist, slot_cap, slot_bytes, slot_val, meta, summary);
-        __syncthreads();  // shared scratch is reused by the next tile
-    }
+// ------------------------------------------------------------------------------ K2 / K3
+// The tile-level prefixes in two launches over blocks of kTileBlock tiles (1024 threads x 4
+// tiles): K2a reduces each block (entries, LEB128 bytes but the block's first non-empty
+// tile's first gap, first / last non-empty tile); K2b — every CTA re-scans the (few hundred)
+// block aggregates itself, so no single-CTA scan launch sits between them — places every
+// tile (entry and byte prefix, first gap) into K4's plan, records each tensor's E_k / B_k at
+// its first tile, and the last CTA to finish (ticket after a fence) writes the offset table
+// (K3: record sizes and offsets, PAPER.md:382 + SPEC.md:148) and the per-tensor emit bases.
+
+// Absolute lane index (within its fused tensor) of the last change of non-empty tile p, if p
+// is in tensor k; otherwise 0 — the tile after it then starts its tensor's gap chain with the
+// first index as-is (reading R3/R4).
+__device__ __forceinline__ unsigned long long pred_abs(const TileDesc *__restrict__ tiles,
+                                                       const TileMeta *__restrict__ meta, long long p, uint32_t k) {
+    if (p < 0) return 0;
+    const TileDesc d = tiles[p];
+    if ((d.flags_tensor & kTileTensorMask) != k) return 0;
+    return d.lane_base + meta[p].last_off;
 }
 
-// ------------------------------------------------------------------------------ K2
-// Tile-level scans over blocks of kTileBlock tiles (1024 threads x 4 tiles).
-__global__ void __launch_bounds__(1024)
-k_tiles_reduce(const TileMeta *__restrict__ meta, uint32_t ntiles, unsigned long long *__restrict__ blk_cnt,
-               long long *__restrict__ blk_key, const ExtractSummary *summary) {
-    if (summary->overflow) return;
-    __shared__ unsigned long long s_c[32];
-    __shared__ long long s_k[32];
-    const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
-    unsigned long long c = 0;
-    long long key = -1;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const uint32_t t = t0 + e;
-        if (t < ntiles) {
-            const uint32_t n = meta[t].count;
-            c += n;
-            if (n) key = t;
-        }
+// LEB128 bytes of non-empty tile t given its predecessor tile p (-1: none): the first gap
+// plus the in-tile gaps; fixed-width codec (reading R18): count x index width.  Also its
+// first gap g0 (fixed: the tile's lane base, i.e. the absolute index base).
+__device__ __forceinline__ unsigned long long tile_bytes(const TileDesc &d, const TileMeta &m, const TileDesc *tiles,
+                                                         const TileMeta *meta, long long p,
+                                                         const unsigned long long *numel, int fixed,
+                                                         unsigned long long &g0) {
+    const uint32_t k = d.flags_tensor & kTileTensorMask;
+    if (fixed) {
+        g0 = d.lane_base;
+        return (unsigned long long)m.count * fixed_index_width(numel[k]);
     }
-    c = warp_sum(c);
-    key = warp_max(key);
+    g0 = d.lane_base + m.first_off - pred_abs(tiles, meta, p, k);
+    return m.internal_bytes + leb_len(g0);
+}
+
+// Block-wide (1024 threads) exclusive scans: sum of x, max of key (identity -1).
+__device__ __forceinline__ void block_scan_sum_max(unsigned long long x, long long key, unsigned long long &xex,
+                                                   unsigned long long &xtot, long long &kex, long long &ktot) {
+    __shared__ unsigned long long s_x[32];
+    __shared__ long long s_k[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        s_c[warp] = c;
-        s_k[warp] = key;
+    const unsigned long long xi = warp_inclusive_sum(x);
+    const long long ki = warp_inclusive_max(key);
+    if (lane == 31) {
+        s_x[warp] = xi;
+        s_k[warp] = ki;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long tc = 0;
-        long long tk = -1;
-        for (int w = 0; w < 32; ++w) {
-            tc += s_c[w];
-            tk = s_k[w] > tk ? s_k[w] : tk;
+    unsigned long long px = 0, tx = 0;
+    long long pk = -1, tk = -1;
+#pragma unroll 8
+    for (int w = 0; w < 32; ++w) {
+        const unsigned long long a = s_x[w];
+        const long long b = s_k[w];
+        if (w < warp) {
+            px += a;
+            pk = b > pk ? b : pk;
         }
-        blk_cnt[blockIdx.x] = tc;
-        blk_key[blockIdx.x] = tk;
+        tx += a;
+        tk = b > tk ? b : tk;
     }
+    __syncthreads();
+    long long ke = __shfl_up_sync(0xffffffffu, ki, 1);
+    if (lane == 0) ke = -1;
+    xex = px + xi - x;
+    xtot = tx;
+    kex = pk > ke ? pk : ke;
+    ktot = tk;
 }
 
-// One CTA: exclusive sum-scan of blk_a (in place) and, if blk_key != nullptr, exclusive
-// max-scan of blk_key (in place, identity -1).
 __global__ void __launch_bounds__(1024)
-k_blocks_scan(unsigned long long *__restrict__ blk_a, long long *__restrict__ blk_key, uint32_t nblk,
-              const ExtractSummary *summary) {
+k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
+            BlockAgg *__restrict__ agg, const unsigned long long *__restrict__ numel, int fixed,
+            const ExtractSummary *summary) {
     if (summary->overflow) return;
-    __shared__ unsigned long long s_w[32];
-    __shared__ long long s_m[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long carry = 0;
-    long long mcarry = -1;
-    for (uint32_t b = 0; b < nblk; b += 1024) {
-        const uint32_t i = b + threadIdx.x;
-        const unsigned long long x = i < nblk ? blk_a[i] : 0;
-        unsigned long long tot;
-        const unsigned long long ex = block_excl_scan<32, unsigned long long>(x, s_w, tot);
-        if (blk_key) {
-            const long long k = i < nblk ? blk_key[i] : -1;
-            const long long inc = warp_inclusive_max(k);
-            if (lane == 31) s_m[warp] = inc;
-            __syncthreads();
-            long long pre = -1, all = -1;
-            for (int w = 0; w < 32; ++w) {
-                if (w < warp && s_m[w] > pre) pre = s_m[w];
-                if (s_m[w] > all) all = s_m[w];
-            }
-            long long exm = __shfl_up_sync(0xffffffffu, inc, 1);
-            if (lane == 0) exm = -1;
-            if (pre > exm) exm = pre;
-            if (mcarry > exm) exm = mcarry;
-            __syncthreads();
-            if (i < nblk) blk_key[i] = exm;
-            if (all > mcarry) mcarry = all;
-        }
-        if (i < nblk) blk_a[i] = carry + ex;
-        carry += tot;
-    }
-}
-
-// Per tile: entry prefix E_t, predecessor of its first change, its LEB128 bytes.
-__global__ void __launch_bounds__(1024)
-k_tiles_bytes(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
-              const unsigned long long *__restrict__ blk_cnt, const long long *__restrict__ blk_key,
-              const uint32_t *__restrict__ tensor_first_tile, unsigned long long *__restrict__ tile_entry,
-              unsigned long long *__restrict__ tile_pred, unsigned int *__restrict__ tile_bytes,
-              unsigned long long *__restrict__ blk_bytes, const unsigned long long *__restrict__ numel,
-              int fixed, const ExtractSummary *summary) {
-    if (summary->overflow) return;
-    __shared__ unsigned long long s_w[32];
-    __shared__ long long s_m[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
     TileMeta mt[4];
     unsigned long long c = 0;
-    long long key = -1;
+    long long klast = -1, kfirst = -1;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         mt[e] = t0 + e < ntiles ? meta[t0 + e] : TileMeta{0, 0, 0, 0, 0};
         c += mt[e].count;
-        if (mt[e].count) key = t0 + e;
+        if (mt[e].count) {
+            klast = t0 + e;
+            if (kfirst < 0) kfirst = t0 + e;
+        }
     }
-    unsigned long long tot;
-    unsigned long long cex = block_excl_scan<32, unsigned long long>(c, s_w, tot) + blk_cnt[blockIdx.x];
-    const long long kinc = warp_inclusive_max(key);
-    if (lane == 31) s_m[warp] = kinc;
-    __syncthreads();
-    long long kex = __shfl_up_sync(0xffffffffu, kinc, 1);
-    if (lane == 0) kex = -1;
-    for (int w = 0; w < warp; ++w)
-        if (s_m[w] > kex) kex = s_m[w];
-    if (blk_key[blockIdx.x] > kex) kex = blk_key[blockIdx.x];
-    unsigned int mybytes = 0;
+    unsigned long long cex, ctot;
+    long long kex, ktot;
+    block_scan_sum_max(c, klast, cex, ctot, kex, ktot);
+    unsigned long long b = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const uint32_t t = t0 + e;
-        if (t >= ntiles) break;
-        unsigned long long pred = 0;
-        unsigned int b = 0;
-        if (mt[e].count) {
-            const TileDesc d = tiles[t];
-            const uint32_t k = d.flags_tensor & kTileTensorMask;
-            if (kex >= 0 && (unsigned long long)kex >= tensor_first_tile[k]) {
-                pred = tiles[kex].lane_base + meta[kex].last_off;  // last change before this tile
-            }
-            const unsigned long long first = d.lane_base + mt[e].first_off;
-            b = fixed ? mt[e].count * fixed_index_width(numel[k])  // reading R18: absolute indices
-                      : mt[e].internal_bytes + leb_len(first - pred);
-            kex = t;
-        }
-        tile_entry[t] = cex;
-        tile_pred[t] = pred;
-        tile_bytes[t] = b;
-        cex += mt[e].count;
-        mybytes += b;
+        if (t >= ntiles || !mt[e].count) continue;
+        unsigned long long g0;
+        if (kex >= 0 || fixed) b += tile_bytes(tiles[t], mt[e], tiles, meta, kex, numel, fixed, g0);
+        else b += mt[e].internal_bytes;  // the block's first non-empty tile: first gap in K2b
+        kex = t;
     }
-    __syncthreads();  // s_w reuse
-    unsigned long long bs = warp_sum((unsigned long long)mybytes);
-    if (lane == 0) s_w[warp] = bs;
+    const unsigned long long bs = warp_sum(b);
+    const long long kf = -warp_max(kfirst < 0 ? -(long long)0x7FFFFFFFFFFFFFFF : -kfirst);
+    __shared__ unsigned long long s_b[32];
+    __shared__ long long s_f[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_b[warp] = bs;
+        s_f[warp] = kf;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long x = 0;
-        for (int w = 0; w < 32; ++w) x += s_w[w];
-        blk_bytes[blockIdx.x] = x;
+        unsigned long long tb = 0;
+        long long f = 0x7FFFFFFFFFFFFFFF;
+        for (int w = 0; w < 32; ++w) {
+            tb += s_b[w];
+            f = s_f[w] < f ? s_f[w] : f;
+        }
+        agg[blockIdx.x] = BlockAgg{ctot, tb, f == 0x7FFFFFFFFFFFFFFF ? -1 : f, ktot};
     }
 }
 
-// Per tile: byte prefix; per tensor: E_k and B_k at its first tile; totals.
 __global__ void __launch_bounds__(1024)
-k_tiles_place(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
-              uint32_t ntensors, const unsigned long long *__restrict__ tile_entry,
-              const unsigned int *__restrict__ tile_bytes, const unsigned long long *__restrict__ blk_bytes,
-              unsigned long long *__restrict__ tile_byte, unsigned long long *__restrict__ entry_begin,
-              unsigned long long *__restrict__ tensor_byte_begin, ExtractSummary *summary) {
+k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
+               uint32_t nblk, const BlockAgg *__restrict__ agg, TileEmit *__restrict__ plan,
+               unsigned long long *__restrict__ E, unsigned long long *__restrict__ Bk, uint32_t T,
+               const uint32_t *__restrict__ name_len, const unsigned long long *__restrict__ numel,
+               RecordRow *__restrict__ table, TensorBase *__restrict__ bases, int width, int fixed,
+               ExtractSummary *summary) {
     if (summary->overflow) return;
-    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_e0, s_b0;
+    __shared__ long long s_p0;
+    __shared__ bool s_last;
+    // ---- this block's entry / byte prefix and the last non-empty tile before it, from the
+    // block aggregates (scanned by every CTA; nblk is a few hundred)
+    {
+        unsigned long long ecarry = 0, bcarry = 0;
+        long long pcarry = -1;
+        for (uint32_t j0 = 0; j0 < nblk; j0 += 1024) {
+            const uint32_t j = j0 + threadIdx.x;
+            BlockAgg a = j < nblk ? agg[j] : BlockAgg{0, 0, -1, -1};
+            unsigned long long cex, ctot;
+            long long pex, ptot;
+            block_scan_sum_max(a.cnt, a.last, cex, ctot, pex, ptot);
+            if (pcarry > pex) pex = pcarry;
+            unsigned long long fb = 0, g0;  // the first gap of the block's first non-empty tile
+            if (a.first >= 0 && !fixed) {
+                const TileMeta m = meta[a.first];
+                fb = tile_bytes(tiles[a.first], m, tiles, meta, pex, numel, 0, g0) - m.internal_bytes;
+            }
+            unsigned long long bex, btot;
+            long long d0, d1;
+            block_scan_sum_max(a.bytes + fb, -1, bex, btot, d0, d1);
+            if (j == blockIdx.x) {
+                s_e0 = ecarry + cex;
+                s_b0 = bcarry + bex;
+                s_p0 = pex;
+            }
+            ecarry += ctot;
+            bcarry += btot;
+            if (ptot > pcarry) pcarry = ptot;
+        }
+    }
+    __syncthreads();
+    // ---- the block's tiles
     const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
-    unsigned int b[4];
-    unsigned long long mine = 0;
+    TileMeta mt[4];
+    unsigned long long c = 0;
+    long long klast = -1;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        b[e] = t0 + e < ntiles ? tile_bytes[t0 + e] : 0;
-        mine += b[e];
+        mt[e] = t0 + e < ntiles ? meta[t0 + e] : TileMeta{0, 0, 0, 0, 0};
+        c += mt[e].count;
+        if (mt[e].count) klast = t0 + e;
     }
-    unsigned long long tot;
-    unsigned long long ex = block_excl_scan<32, unsigned long long>(mine, s_w, tot) + blk_bytes[blockIdx.x];
+    unsigned long long cex, ctot;
+    long long kex, ktot;
+    block_scan_sum_max(c, klast, cex, ctot, kex, ktot);
+    if (kex < 0) kex = s_p0;
+    unsigned long long bt[4], g0[4], mine = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        bt[e] = 0;
+        g0[e] = 0;
+        const uint32_t t = t0 + e;
+        if (t >= ntiles || !mt[e].count) continue;
+        bt[e] = tile_bytes(tiles[t], mt[e], tiles, meta, kex, numel, fixed, g0[e]);
+        mine += bt[e];
+        kex = t;
+    }
+    unsigned long long bex, btot;
+    long long d0, d1;
+    block_scan_sum_max(mine, -1, bex, btot, d0, d1);
+    unsigned long long ent = s_e0 + cex, byt = s_b0 + bex;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const uint32_t t = t0 + e;
         if (t >= ntiles) break;
-        tile_byte[t] = ex;
-        const uint32_t f = tiles[t].flags_tensor;
+        const uint32_t f = tiles[t].flags_tensor, k = f & kTileTensorMask;
+        plan[t] = TileEmit{byt, ent, g0[e], mt[e].count | (fixed ? fixed_index_width(numel[k]) : mt[e].internal_bytes) << 16, k};
         if (f & kTileFirstOfTensor) {
-            entry_begin[f & kTileTensorMask] = tile_entry[t];
-            tensor_byte_begin[f & kTileTensorMask] = ex;
+            E[k] = ent;
+            Bk[k] = byt;
         }
+        ent += mt[e].count;
+        byt += bt[e];
         if (t == ntiles - 1) {
-            const unsigned long long M = tile_entry[t] + meta[t].count;
-            entry_begin[ntensors] = M;
-            tensor_byte_begin[ntensors] = ex + b[e];
-            summary->M = M;
-            summary->idx_bytes = ex + b[e];
+            E[T] = ent;
+            Bk[T] = byt;
         }
-        ex += b[e];
     }
-}
-
-// ------------------------------------------------------------------------------ K3
-__global__ void __launch_bounds__(1024)
-k_finalize(const unsigned long long *__restrict__ E, const unsigned long long *__restrict__ Bk, uint32_t T,
-           const uint32_t *__restrict__ name_len, const unsigned long long *__restrict__ numel,
-           RecordRow *__restrict__ table, int width, ExtractSummary *summary) {
-    if (summary->overflow) return;
-    __shared__ unsigned long long s_warp[32];
+    // ---- K3, by the last CTA to finish: the offset table and the per-tensor emit bases
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&summary->blocks_done, 1ull) == nblk - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     unsigned long long carry = 0;
     for (uint32_t b = 0; b < T; b += 1024) {
         const uint32_t k = b + threadIdx.x;
-        unsigned long long rb = 0, nnz = 0, ilen = 0;
+        unsigned long long rb = 0, nnz = 0, ilen = 0, ek = 0, bk = 0;
         if (k < T) {
-            nnz = E[k + 1] - E[k];
-            ilen = Bk[k + 1] - Bk[k];
+            ek = __ldcg(E + k);
+            bk = __ldcg(Bk + k);
+            nnz = __ldcg(E + k + 1) - ek;
+            ilen = __ldcg(Bk + k + 1) - bk;
             rb = 27ull + name_len[k] + ilen + (unsigned long long)width * nnz;
         }
-        unsigned long long tot;
-        const unsigned long long ex = block_excl_scan<32, unsigned long long>(rb, s_warp, tot);
+        unsigned long long ex, tot;
+        long long d2, d3;
+        block_scan_sum_max(rb, -1, ex, tot, d2, d3);
         if (k < T) {
             RecordRow r;
             r.record_offset = carry + ex;
@@ -706,10 +595,15 @@ k_finalize(const unsigned long long *__restrict__ E, const unsigned long long *_
             r.values_offset = r.index_offset + ilen;
             r.record_bytes = rb;
             table[k] = r;
+            bases[k] = TensorBase{r.index_offset - bk, r.values_offset - ek * (unsigned long long)width};
         }
         carry += tot;
     }
-    if (threadIdx.x == 0) summary->body_bytes = carry;
+    if (threadIdx.x == 0) {
+        summary->M = __ldcg(E + T);
+        summary->idx_bytes = __ldcg(Bk + T);
+        summary->body_bytes = carry;
+    }
 }
 
 // ------------------------------------------------------------------------------ K4
@@ -760,32 +654,6 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
     for (uint32_t b = (nv << 4) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
 }
 
-// K3b: per tile, the final body offsets of its index bytes and values and its first gap
-// (one thread per tile; turns K4's chain of dependent loads into one 32-byte load).
-template <int W>
-__global__ void __launch_bounds__(256)
-k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
-                 const unsigned long long *__restrict__ tile_entry, const unsigned long long *__restrict__ tile_byte,
-                 const unsigned long long *__restrict__ tile_pred, const unsigned long long *__restrict__ E,
-                 const unsigned long long *__restrict__ Bk, const RecordRow *__restrict__ table,
-                 TileEmit *__restrict__ plan, const unsigned long long *__restrict__ numel, int fixed,
-                 const ExtractSummary *summary) {
-    if (summary->overflow) return;
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
-        const TileMeta m = meta[t];
-        TileEmit e{0, 0, 0, m.count, m.internal_bytes};
-        if (m.count) {
-            const TileDesc d = tiles[t];
-            const uint32_t k = d.flags_tensor & kTileTensorMask;
-            e.ib = table[k].index_offset + (tile_byte[t] - Bk[k]);
-            e.vb = table[k].values_offset + (tile_entry[t] - E[k]) * W;
-            e.g0 = fixed ? d.lane_base : d.lane_base + m.first_off - tile_pred[t];
-            if (fixed) e.internal_bytes = fixed_index_width(numel[k]);
-        }
-        plan[t] = e;
-    }
-}
-
 // One warp per tile: the LEB128 bytes of the tile's first gap, then the in-tile gaps
 // (differences of the slot's u16 lane offsets, < 2^14: one or two bytes each) encoded 32 at
 // a time — byte positions from a ballot of the two-byte ones — and the raw values copied
@@ -795,7 +663,7 @@ k_tiles_emitplan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict_
 // the sparse variant keeps 32 registers at 8 CTAs per SM.
 template <int W, bool FIXED, bool BATCHED = false>
 __global__ void __launch_bounds__(256, BATCHED ? 6 : 8)
-k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_cap,
+k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
     if (summary->overflow || summary->body_bytes > cap) return;  // emit gate (async extract)
@@ -815,10 +683,16 @@ k_emit_tiles(const TileEmit *__restrict__ plan, uint32_t ntiles, uint32_t slot_c
 #pragma unroll
             for (int r = 0; r < 8; ++r) o[r] = so0[r * 32 + lane];
         }
-        const TileEmit e = plan[t];
-        if (e.count == 0) continue;
+        const TileEmit pe = plan[t];
+        const uint32_t ecount = pe.count_internal & 0xFFFFu;
+        if (ecount == 0) continue;
+        const TensorBase tb = bases[pe.k];
+        const struct {
+            unsigned long long ib, vb, g0;
+            uint32_t count, internal_bytes;
+        } e{tb.ib + pe.ib, tb.vb + pe.eb * W, pe.g0, ecount, pe.count_internal >> 16};
         if constexpr (FIXED) {  // reading R18: lane_base + offset as u32 / u64, little-endian
-            const uint32_t iw = e.internal_bytes;  // the index width (set by K3b for FIXED)
+            const uint32_t iw = e.internal_bytes;  // the index width (set by K2b for FIXED)
             const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
             unsigned long long *buf = s_fix + 256 * (threadIdx.x >> 5);
             uint8_t *dst = out + e.ib;
@@ -977,50 +851,21 @@ k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__res
 template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
-    // The ffs loop beats four predicated steps per half-vector at every density measured
-    // (check 56: 10 % K1 6.46 vs 7.80 ms, 50 % 19.99 vs 24.29 ms), so the predicated
-    // (DENSE) compaction is only a diagnostic: DELTA_K1_DENSE=1.
-    static const bool dense = [] {
-        const char *e = getenv("DELTA_K1_DENSE");
-        return e != nullptr && atoi(e) == 1;
-    }();
     if (ev) cudaEventRecord(ev[0], s);
-    const bool variant_ok = !a.advance && a.mode == 0;  // the variants implement plain replace extraction
-    if (a.scan_kernel == 4 && variant_ok) {
-        const uint32_t grid = a.ntiles < 3u * a.sm_count ? a.ntiles : 3u * a.sm_count;
-        k_scan_tiles_persist<W><<<grid, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
-                                                    static_cast<LT *>(a.slot_val), a.meta, a.summary);
-    } else if (a.scan_kernel == 3 && variant_ok) {
-        k_scan_tiles<W, 512, 4, 2, false><<<a.ntiles, 512, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap,
-                                                                  a.slot_bytes, static_cast<LT *>(a.slot_val),
-                                                                  a.meta, a.summary, 0u);
-    } else {
-        (a.advance ? (dense ? k_scan_tiles<W, 256, 8, 3, true, false, true> : k_scan_tiles<W, 256, 8, 3, false, false, true>)
-         : a.mode == 1 ? (dense ? k_scan_tiles<W, 256, 8, 2, true, true> : k_scan_tiles<W, 256, 8, 2, false, true>)
-                       : (dense ? k_scan_tiles<W, 256, 8, 3, true> : k_scan_tiles<W, 256, 8, 3, false>))
+    if (a.ntiles)
+        (a.advance ? k_scan_tiles<W, false, true> : a.mode == 1 ? k_scan_tiles<W, true> : k_scan_tiles<W>)
             <<<a.ntiles, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
                                       static_cast<LT *>(a.slot_val), a.meta, a.summary, a.redo_cap);
-    }
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
-    k_tiles_reduce<<<nblk, 1024, 0, s>>>(a.meta, a.ntiles, a.blk_a, a.blk_key, a.summary);
-    k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a, a.blk_key, nblk, a.summary);
-    k_tiles_bytes<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.blk_a, a.blk_key, a.tensor_first_tile,
-                                        a.tile_entry, a.tile_pred, a.tile_bytes_tmp, a.blk_a + nblk,
-                                        a.numel, a.index_codec, a.summary);
-    k_blocks_scan<<<1, 1024, 0, s>>>(a.blk_a + nblk, nullptr, nblk, a.summary);
-    k_tiles_place<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.ntensors, a.tile_entry,
-                                        a.tile_bytes_tmp, a.blk_a + nblk, a.tile_byte, a.entry_begin,
-                                        a.tensor_byte_begin, a.summary);
-    if (ev) cudaEventRecord(ev[2], s);
-    k_finalize<<<1, 1024, 0, s>>>(a.entry_begin, a.tensor_byte_begin, a.ntensors, a.name_len, a.numel,
-                                  a.table, a.width, a.summary);
-    {
-        const uint32_t g = (a.ntiles + 255) / 256;
-        k_tiles_emitplan<W><<<g < 65535u ? g : 65535u, 256, 0, s>>>(a.tiles, a.meta, a.ntiles, a.tile_entry,
-                                                                   a.tile_byte, a.tile_pred, a.entry_begin,
-                                                                   a.tensor_byte_begin, a.table, a.plan,
-                                                                   a.numel, a.index_codec, a.summary);
+    if (nblk) {
+        k_tiles_agg<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.agg, a.numel, a.index_codec, a.summary);
+        if (ev) cudaEventRecord(ev[2], s);
+        k_tiles_prefix<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.plan, a.entry_begin,
+                                             a.tensor_byte_begin, a.ntensors, a.name_len, a.numel, a.table, a.bases,
+                                             a.width, a.index_codec, a.summary);
+    } else if (ev) {
+        cudaEventRecord(ev[2], s);
     }
     if (ev) cudaEventRecord(ev[3], s);
     return cudaGetLastError();
@@ -1031,15 +876,15 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
     if (a.index_codec)
-        k_emit_tiles<W, true><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
+        k_emit_tiles<W, true><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                             static_cast<const LT *>(a.slot_val), out, a.summary,
                                                             a.out_cap);
     else if (a.slot_cap > kDenseEmitSlot)  // some tile has > kDenseEmitSlot changes
-        k_emit_tiles<W, false, true><<<a.sm_count * 6, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
+        k_emit_tiles<W, false, true><<<a.sm_count * 6, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                                    static_cast<const LT *>(a.slot_val), out,
                                                                    a.summary, a.out_cap);
     else
-        k_emit_tiles<W, false><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.ntiles, a.slot_cap, a.slot_bytes,
+        k_emit_tiles<W, false><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                              static_cast<const LT *>(a.slot_val), out, a.summary,
                                                              a.out_cap);
     if (ev) cudaEventRecord(ev[1], s);

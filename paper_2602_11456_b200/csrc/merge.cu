@@ -46,8 +46,7 @@ __device__ __forceinline__ unsigned long long rd_u(const uint8_t *p, int nbytes)
 
 constexpr unsigned long long kIdxMask = (1ull << kKeyShift) - 1;
 
-// ---------------------------------------------------------------- exclusive scan u32 -> u64
-constexpr int kScanPer = 4096;  // elements per block (1024 threads x 4)
+// ---------------------------------------------------------------- block-wide exclusive scan (u64)
 
 __device__ __forceinline__ unsigned long long block_scan_excl(unsigned long long v, unsigned long long *s_w,
                                                               unsigned long long &total) {
@@ -68,64 +67,6 @@ __device__ __forceinline__ unsigned long long block_scan_excl(unsigned long long
     __syncthreads();
     total = tot;
     return pre + inc - v;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_reduce(const uint32_t *__restrict__ x, unsigned long long m,
-                                                      unsigned long long *__restrict__ blk) {
-    __shared__ unsigned long long s_w[32];
-    const unsigned long long i0 = (unsigned long long)blockIdx.x * kScanPer + threadIdx.x * 4;
-    unsigned long long v = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-        if (i0 + e < m) v += x[i0 + e];
-    unsigned long long tot;
-    block_scan_excl(v, s_w, tot);
-    if (threadIdx.x == 0) blk[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_blocks(unsigned long long *__restrict__ blk, uint32_t nblk) {
-    __shared__ unsigned long long s_w[32];
-    unsigned long long carry = 0;
-    for (uint32_t b = 0; b < nblk; b += 1024) {
-        const uint32_t i = b + threadIdx.x;
-        const unsigned long long v = i < nblk ? blk[i] : 0;
-        unsigned long long tot;
-        const unsigned long long ex = block_scan_excl(v, s_w, tot);
-        if (i < nblk) blk[i] = carry + ex;
-        carry += tot;
-    }
-}
-
-__global__ void __launch_bounds__(1024) k_scan_down(const uint32_t *__restrict__ x, unsigned long long m,
-                                                    const unsigned long long *__restrict__ blk,
-                                                    unsigned long long *__restrict__ y) {
-    __shared__ unsigned long long s_w[32];
-    const unsigned long long i0 = (unsigned long long)blockIdx.x * kScanPer + threadIdx.x * 4;
-    uint32_t v[4];
-    unsigned long long mine = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        v[e] = i0 + e < m ? x[i0 + e] : 0u;
-        mine += v[e];
-    }
-    unsigned long long tot;
-    unsigned long long ex = block_scan_excl(mine, s_w, tot) + blk[blockIdx.x];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        if (i0 + e < m) y[i0 + e] = ex;
-        if (i0 + e == m - 1) y[m] = ex + v[e];
-        ex += v[e];
-    }
-}
-
-cudaError_t scan_u32(const uint32_t *x, unsigned long long m, unsigned long long *y, unsigned long long *blk,
-                     cudaStream_t s) {
-    if (m == 0) return cudaMemsetAsync(y, 0, 8, s);
-    const uint32_t nblk = (uint32_t)((m + kScanPer - 1) / kScanPer);
-    k_scan_reduce<<<nblk, 1024, 0, s>>>(x, m, blk);
-    k_scan_blocks<<<1, 1024, 0, s>>>(blk, nblk);
-    k_scan_down<<<nblk, 1024, 0, s>>>(x, m, blk, y);
-    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- M1

@@ -42,13 +42,25 @@ struct TileMeta {
 };
 static_assert(sizeof(TileMeta) == 16, "TileMeta is 16 bytes");
 
-// K3b output per tile: everything K4 needs in one 32-byte load.
+// K2b output per tile: everything K4 needs besides its tensor's bases, in one 32-byte load.
 struct TileEmit {
-    unsigned long long ib;   // body offset of the tile's first LEB128 byte
-    unsigned long long vb;   // body offset of the tile's first value
+    unsigned long long ib;   // LEB128 bytes of all tiles before this one (all tensors)
+    unsigned long long eb;   // entries of all tiles before this one (all tensors)
     unsigned long long g0;   // gap of the tile's first change (to the previous change, or absolute)
-    uint32_t count;          // changes in the tile
-    uint32_t internal_bytes; // LEB128 bytes of the gaps inside the tile (encoded by K4)
+    uint32_t count_internal; // changes in the tile | in-tile gap bytes (FIXED: index width) << 16
+    uint32_t k;              // tensor
+};
+// K2a output per block of kTileBlock tiles.
+struct BlockAgg {
+    unsigned long long cnt;    // entries in the block
+    unsigned long long bytes;  // LEB128 bytes, except the first gap of the block's first non-empty tile
+    long long first, last;     // first / last non-empty tile of the block, -1 if none
+};
+
+// Per tensor (written with the offset table): body offset of a tile's first index byte =
+// ib + TileEmit::ib, of its first value = vb + TileEmit::eb * w.
+struct TensorBase {
+    unsigned long long ib, vb;
 };
 static_assert(sizeof(TileEmit) == 32, "TileEmit is 32 bytes");
 
@@ -59,6 +71,7 @@ struct ExtractSummary {
     unsigned long long max_count;   // largest per-tile count seen (sizes the slots on retry)
     unsigned long long idx_bytes;   // total LEB128 bytes over all tensors
     unsigned long long body_bytes;  // packed body size
+    unsigned long long blocks_done; // K2b tickets (the last CTA writes the offset table)
 };
 
 // Sticky outcome of the delta_extract_async calls since the last delta_extract_wait (folded
@@ -117,13 +130,9 @@ struct ExtractArgs {
     uint8_t *slot_bytes;              // ntiles x 2C LEB128 bytes of the gaps inside the tile
     void *slot_val;                   // ntiles x C lanes
     TileMeta *meta;                   // ntiles
-    unsigned long long *tile_entry;   // ntiles: entries before the tile (all tensors)
-    unsigned long long *tile_byte;    // ntiles: LEB128 bytes before the tile (all tensors)
-    unsigned long long *tile_pred;    // ntiles: absolute index of the previous change in the tensor, or 0
-    unsigned int *tile_bytes_tmp;     // ntiles: the tile's own LEB128 bytes
     TileEmit *plan;                   // ntiles: K4's per-tile plan
-    unsigned long long *blk_a;        // per tile block: entry count, then LEB128 bytes
-    long long *blk_key;               // per tile block: last non-empty tile
+    BlockAgg *agg;                    // per tile block (kTileBlock tiles): K2a aggregates
+    TensorBase *bases;                // ntensors: K4's per-tensor body bases
     const uint32_t *tensor_first_tile;  // ntensors
     unsigned long long *entry_begin;  // ntensors + 1 (E_k)
     unsigned long long *tensor_byte_begin;  // ntensors + 1 (B_k)
@@ -136,7 +145,6 @@ struct ExtractArgs {
     int width;                        // 2 or 4
     int persist_ctas;                 // grid for grid-stride kernels
     int sm_count;
-    int scan_kernel;                  // 0: one CTA per tile; 1: persistent TMA pipeline; 2: runs
     uint32_t prefetch_dist;           // K1 (0): L2 bulk prefetch distance in tiles (0 = off)
     int mode;                         // record mode: 0 replace, 1 additive
     int index_codec;                  // 0 LEB128 gaps, 1 fixed-width absolute (R18)

@@ -416,16 +416,15 @@ def test_async_apply_error_is_reported_at_wait(sd):
 
 
 # ------------------------------------------------------------------ K1 launch variants
-@pytest.mark.parametrize("kernel", [1, 4, 5])
+@pytest.mark.parametrize("kernel", [1])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_scan_kernel_variants_parity(sd, dtype, kernel):
-    """The compare+compaction kernel's launch forms (DELTA_OPT_SCAN_KERNEL = 1: CTA per
-    tile, 256 x 8; 4: 512 threads x 4 vectors; 5: persistent) on ragged / unaligned /
-    multi-tile / dense inputs, byte-exact against the oracle; the retired forms 2, 3 are
-    rejected."""
+    """The compare+compaction kernel (DELTA_OPT_SCAN_KERNEL = 1, the only form) on ragged /
+    unaligned / multi-tile / dense inputs, byte-exact against the oracle; the retired forms
+    2-5 are rejected."""
     from paper_2602_11456_b200 import _abi
     ctx = sd.DeltaContext(DEV)
-    for bad in (2, 3, 6):
+    for bad in (2, 3, 4, 5, 6):
         with pytest.raises(sd.DeltaError):
             ctx.set_option(_abi.DELTA_OPT_SCAN_KERNEL, bad)
     ctx.set_option(_abi.DELTA_OPT_SCAN_KERNEL, kernel)
