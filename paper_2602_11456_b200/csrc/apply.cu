@@ -208,7 +208,8 @@ __device__ __forceinline__ const uint8_t *stage_bytes(uint8_t *buf, const uint8_
     return buf + o;
 }
 
-constexpr int kStageBytes = kHalo + kByteChunk + 32;
+constexpr int kStagePad = 16;  // bytes below the staged data that validate_fast may read (never used)
+constexpr int kStageBytes = kStagePad + kHalo + kByteChunk + 32;
 
 // Stage bytes [cs - halo, cs + len) of the record's stream.  The caller synchronises
 // before reading.
@@ -268,66 +269,63 @@ __device__ __forceinline__ void decode_thread(const ChunkView &v, F &&f) {
 //   a 0x00 byte ending a multi-byte varint                -> overlong
 //   a lone 0x00 byte (gap 0) that is not the record's first -> non-increasing
 // Indices >= N are caught by A3 (last index = total sum, gaps >= 1).
-// Bit 7 of byte i of the result is set iff byte i of w is nonzero (exact, no borrows).
-__device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
-    return (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
-}
-
-// The top bits of the four bytes of x (bits 7, 15, 23, 31) as a 4-bit value.
-__device__ __forceinline__ uint32_t gather_top_bits(uint32_t x) {
-    return (((x >> 7) & 0x01010101u) * 0x01020408u) >> 24;
-}
-
-// A 4-bit mask expanded to a byte mask (0xFF in byte i iff bit i).
-__device__ __forceinline__ uint32_t expand_nibble(uint32_t nib) {
-    return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
-}
-
 // Fast path of validate_thread for a full 16-byte window whose varints are all 1-3 bytes
-// long and contain no 0x00 byte (the common case at any density): the terminator mask
-// (MSB clear) gives every byte's position d in its varint, and the sum of the window's
-// varint values is sum_d 128^d * (sum of the payloads at position d), three byte-masked
-// dot products.  Returns false if the window needs the byte loop.
+// long and contain no 0x00 byte (the common case at any density), SIMD within 32-bit words:
+// with C the continuation bits (byte MSBs), a byte's position d in its varint is >= 1 iff the
+// byte before it continues, >= 2 iff the two before it do, so the window's sum of varint
+// values is  S_all + 127 S_1 + 16256 S_2  (S_j: payload bytes with d >= j, each a dp4a of the
+// payloads masked by those funnel-shifted bits).  Bytes after the window's last terminator
+// belong to the next window's varint; the continuation run just before p0 (at most two bytes)
+// belongs to this window's first varint.  Returns false if the window needs the byte loop.
 __device__ __forceinline__ bool validate_fast(const ChunkView &v, int p0, uint32_t &cnt,
                                               unsigned long long &sum, bool *ones = nullptr) {
-    int c_in = 0;  // continuation bytes of a varint that started before p0
-    while (c_in < 3 && (long long)v.cs + p0 - c_in > 0 && (v.b[p0 - c_in - 1] & 0x80)) ++c_in;
-    if (c_in >= 3) return false;
-    const uint8_t *ptr = v.b + p0;
+    const uint8_t *ptr = v.b + p0 - 4;  // 4 bytes before the window: the straddling varint
     const uint32_t *a4 = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(ptr) & ~uintptr_t(3));
     const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(ptr) & 3) * 8;
-    uint32_t W[5], w[4];
+    uint32_t W[6], w[5];  // w[0] = bytes p0-4 .. p0-1, w[1..4] = the window
 #pragma unroll
-    for (int j = 0; j < 5; ++j) W[j] = a4[j];
-    uint32_t T = 0, Z = 0;  // terminator / zero-byte masks, bit i = byte i of the window
+    for (int j = 0; j < 6; ++j) W[j] = a4[j];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        w[k] = sh ? __funnelshift_r(W[k], W[k + 1], sh) : W[k];
-        T |= gather_top_bits(~w[k] & 0x80808080u) << (4 * k);
-        Z |= gather_top_bits(~nonzero_bytes(w[k]) & 0x80808080u) << (4 * k);
+    for (int k = 0; k < 5; ++k) w[k] = sh ? __funnelshift_r(W[k], W[k + 1], sh) : W[k];
+    if ((long long)v.cs + p0 == 0) w[0] = 0;  // the stream's first byte: nothing before it
+    uint32_t C[5], t[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        C[k] = w[k] & 0x80808080u;
+        t[k] = C[k] ^ 0x80808080u;  // terminators
     }
-    if (T == 0) return true;  // no varint ends in this window (a long one is its owner's concern)
-    const uint32_t valid = (2u << (31 - __clz(T))) - 1u;  // bytes up to the last terminator
-    // E: terminator flags at positions -3..15 (bits 0..18); positions before p0 from c_in
-    const uint32_t E = (T << 3) | (0x7u & ((1u << (3 - c_in)) - 1u));
-    const uint32_t D0 = (E >> 2) & valid;
-    const uint32_t D1 = ~(E >> 2) & (E >> 1) & valid;
-    const uint32_t D2 = ~(E >> 2) & ~(E >> 1) & E & valid;
-    if ((~(E >> 2) & ~(E >> 1) & ~E & valid) || (Z & valid)) return false;
-    uint32_t s0 = 0, s1 = 0, s2 = 0;
+    const uint32_t n = __popc(t[1]) + __popc(t[2]) + __popc(t[3]) + __popc(t[4]);
+    if (n == 0) return true;  // no varint ends in this window (a long one is its owner's concern)
+    // valid bytes: up to and including the last terminator
+    const int kl = t[4] ? 4 : t[3] ? 3 : t[2] ? 2 : 1;
+    const uint32_t lastmask = 0xFFFFFFFFu >> __clz(t[kl]);  // bits up to the terminator's MSB
+    uint32_t V[5];
+    // bytes before p0 that belong to the first varint: the continuation run ending at p0-1
+    V[0] = (C[0] & 0x80000000u) ? ((C[0] & 0x00800000u) ? 0xFFFF0000u : 0xFF000000u) : 0u;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint32_t pw = w[k] & 0x7F7F7F7Fu;
-        s0 = __dp4a(pw & expand_nibble((D0 >> (4 * k)) & 0xF), 0x01010101u, s0);
-        s1 = __dp4a(pw & expand_nibble((D1 >> (4 * k)) & 0xF), 0x01010101u, s1);
-        s2 = __dp4a(pw & expand_nibble((D2 >> (4 * k)) & 0xF), 0x01010101u, s2);
+    for (int k = 1; k < 5; ++k) V[k] = k < kl ? 0xFFFFFFFFu : (k == kl ? lastmask : 0u);
+    uint32_t s_all = 0, s1 = 0, s2 = 0, bad = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint32_t Cp = k ? C[k - 1] : 0u;
+        const uint32_t P1 = __funnelshift_l(Cp, C[k], 8), P2 = __funnelshift_l(Cp, C[k], 16),
+                       P3 = __funnelshift_l(Cp, C[k], 24);
+        const uint32_t M2 = P1 & P2;
+        if (k) {  // > 3-byte varint, or a 0x00 byte (overlong / zero gap / a first index of 0)
+            // bit 7 of byte i of nz is set iff byte i of w is nonzero (exact, no borrows)
+            const uint32_t nz = ((w[k] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w[k];
+            bad |= ((M2 & P3) | (~nz & 0x80808080u)) & V[k];
+        }
+        const uint32_t pw = w[k] & 0x7F7F7F7Fu & V[k];
+        s_all = __dp4a(pw, 0x01010101u, s_all);
+        s1 = __dp4a(pw & ((P1 >> 7) * 0xFFu), 0x01010101u, s1);
+        s2 = __dp4a(pw & ((M2 >> 7) * 0xFFu), 0x01010101u, s2);
     }
-    if (ones) *ones = (T == 0xFFFFu && c_in == 0);  // 16 one-byte varints
-    uint32_t carry = 0;  // low bits of the straddling varint, from the bytes before p0
-    if (c_in == 1) carry = v.b[p0 - 1] & 0x7F;
-    else if (c_in == 2) carry = (v.b[p0 - 2] & 0x7F) | ((uint32_t)(v.b[p0 - 1] & 0x7F) << 7);
-    cnt += __popc(T);
-    sum = sat_add(sum, (unsigned long long)carry + s0 + (s1 << 7) + (s2 << 14));
+    if (bad) return false;
+    if (V[0] == 0xFFFF0000u && (C[0] & 0x00008000u)) return false;  // > 3 bytes into the window
+    if (ones) *ones = (n == 16 && V[0] == 0);  // 16 one-byte varints
+    cnt += n;
+    sum = sat_add(sum, (unsigned long long)s_all + 127ull * s1 + 16256ull * s2);
     return true;
 }
 
@@ -379,7 +377,7 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = __ldg(chunk_rec + c);
         const ApplyRec R = recs[k];
-        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb + kStagePad);
         __syncthreads();
         uint32_t cnt = 0, err = kOk;
         unsigned long long sum = 0;
@@ -507,7 +505,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = __ldg(chunk_rec + c);
         const ApplyRec R = recs[k];
-        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb + kStagePad);
         const unsigned long long ob = ord_base[c];
         const uint32_t cn = chunk_count[c];
         // this chunk's values (cn lanes, any alignment in the body)
@@ -655,7 +653,7 @@ k_decode_write(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = __ldg(chunk_rec + c);
         const ApplyRec R = recs[k];
-        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb);
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb + kStagePad);
         const unsigned long long ob = ord_base[c];
         const uint32_t cn = chunk_count[c];
         const uint8_t *vals = stage_bytes(svb, body + R.val_off + ob * W, cn * W);

@@ -134,7 +134,7 @@ __device__ __forceinline__ uint32_t lane_mask(const uint4 &a, const uint4 &b) {
     }
 }
 
-template <int W, bool ADDITIVE = false, bool ADVANCE = false>
+template <int W, bool ADDITIVE = false, bool ADVANCE = false, bool OFFSETS = false>
 __global__ void __launch_bounds__(256, 3)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist, uint32_t slot_cap,
              uint8_t *__restrict__ slot_bytes, typename LaneOf<W>::T *__restrict__ slot_val,
@@ -230,25 +230,6 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
             s_new[v] = x;
         }
     }
-    if constexpr (ADVANCE) {
-        // old <- new where anything changed: a thread pair (tid, tid ^ 1) holds one 32-byte
-        // sector; if either half changed both store their whole 16-byte vector (a full-sector
-        // write needs no DRAM fill; unchanged lanes are rewritten with their own value).
-        // Partial vectors at the end of a tile and unaligned tiles: changed lanes only.
-        LT *op = const_cast<LT *>(reinterpret_cast<const LT *>(d.old_p));
-        const bool aligned = d.flags_tensor & kTileAligned;
-#pragma unroll
-        for (int r = 0; r < VECS; ++r) {
-            const uint32_t v = r * THREADS + tid;
-            const bool any = (m[r] | __shfl_xor_sync(0xffffffffu, m[r], 1)) != 0;
-            if (aligned && any && (v + 1) * LPV <= nl) {
-                reinterpret_cast<uint4 *>(op)[v] = vn[r];
-            } else if (m[r]) {
-                for (int j = 0; j < LPV && v * LPV + j < nl; ++j)
-                    if ((m[r] >> j) & 1u) op[v * LPV + j] = (LT)lane_of<W>(vn[r], j);
-            }
-        }
-    }
     __syncthreads();
 
     // ---- 2. word i: change count + two-byte-gap flag, block scan -> ranks and tile totals
@@ -302,18 +283,90 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         }
     }
     if (!fits) return;
+    if constexpr (ADVANCE) {
+        // old <- new where anything changed (only for tiles that fit their slot: an overflowed
+        // tile is compared again after the regrowth): a thread pair (tid, tid ^ 1) holds one 32-byte
+        // sector; if either half changed both store their whole 16-byte vector (a full-sector
+        // write needs no DRAM fill; unchanged lanes are rewritten with their own value).
+        // Partial vectors at the end of a tile and unaligned tiles: changed lanes only.
+        LT *op = const_cast<LT *>(reinterpret_cast<const LT *>(d.old_p));
+        const bool aligned = d.flags_tensor & kTileAligned;
+#pragma unroll
+        for (int r = 0; r < VECS; ++r) {
+            const uint32_t v = r * THREADS + tid;
+            const bool any = (m[r] | __shfl_xor_sync(0xffffffffu, m[r], 1)) != 0;
+            if (aligned && any && (v + 1) * LPV <= nl) {
+                reinterpret_cast<uint4 *>(op)[v] = vn[r];
+            } else if (m[r]) {
+                for (int j = 0; j < LPV && v * LPV + j < nl; ++j)
+                    if ((m[r] >> j) & 1u) op[v * LPV + j] = (LT)lane_of<W>(vn[r], j);
+            }
+        }
+    }
 
-    // ---- 3. ordered emission of word tid's changes
-    uint32_t pos = (pre + inc - val) & 0xFFFFu;
+    // ---- 3. ordered emission of word tid's changes: the value at its rank; the gap to the
+    // previous change as LEB128 bytes at its position in the tile's internal index stream
+    // (OFFSETS, for the fixed-width codec: the u16 lane offset at its rank instead).
+    // Entry e >= 1 of the tile starts at byte (e - 1) + #{two-byte gaps before e}; two-byte
+    // gaps are first entries of flagged words other than the tile's first word fw.
+    const uint32_t ex = pre + inc - val;
+    uint32_t pos = ex & 0xFFFFu;
     LT *sv = slot_val + (size_t)t * slot_cap;
-    uint16_t *sg = reinterpret_cast<uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
     const LT *sn = reinterpret_cast<const LT *>(s_new);
-    while (X) {
-        const uint32_t L = 64u * tid + (uint32_t)__ffsll((long long)X) - 1u;
-        X &= X - 1;
-        sg[pos] = (uint16_t)L;
-        sv[pos] = sn[L];
-        ++pos;
+    if constexpr (OFFSETS) {
+        uint16_t *sg = reinterpret_cast<uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
+        while (X) {
+            const uint32_t L = 64u * tid + (uint32_t)__ffsll((long long)X) - 1u;
+            X &= X - 1;
+            sg[pos] = (uint16_t)L;
+            sv[pos] = sn[L];
+            ++pos;
+        }
+    } else {
+        // the last change before this word: in an earlier word of this warp (ballot + shuffle of
+        // that word's last lane), else in the last non-empty word of an earlier warp
+        const uint32_t mylast = X ? 64u * tid + 63u - (uint32_t)__clzll((long long)X) : 0u;
+        const uint32_t lower = bw & ((1u << lane) - 1u);
+        uint32_t prev = __shfl_sync(0xffffffffu, mylast, lower ? 31 - __clz(lower) : 0);
+        bool has_prev = lower != 0;
+        if (X && !lower) {
+            int lw = -1;
+#pragma unroll
+            for (int w = 0; w < NWARP; ++w)
+                if (w < warp && s_wlast[w] >= 0) lw = s_wlast[w];
+            if (lw >= 0) {
+                prev = 64u * lw + 63u - (uint32_t)__clzll((long long)s_bits[lw]);
+                has_prev = true;
+            }
+        }
+        uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
+        // two-byte flags before this word, without the tile's first word's (it has no gap)
+        const uint32_t bigs = (ex >> 16) - (has_prev && (ex >> 16) ? 1u : 0u);
+        const bool rbig = has_prev && (val >> 16);  // this word's first gap takes two bytes
+        uint32_t bp = pos + bigs - 1u;               // byte position of this word's first gap
+        bool first = true;
+        while (X) {
+            const uint32_t L = 64u * tid + (uint32_t)__ffsll((long long)X) - 1u;
+            X &= X - 1;
+            sv[pos] = sn[L];
+            if (has_prev) {  // every entry but the tile's first has an in-tile gap
+                const uint32_t g = L - prev;
+                if (first && rbig) {
+                    sb[bp] = (uint8_t)(g | 0x80u);
+                    sb[bp + 1] = (uint8_t)(g >> 7);
+                    bp += 2;
+                } else {
+                    sb[bp] = (uint8_t)g;
+                    bp += 1;
+                }
+            } else {
+                bp += 1;  // the tile's first entry: its gap is the plan's first gap (K2)
+            }
+            has_prev = true;
+            first = false;
+            prev = L;
+            ++pos;
+        }
     }
 }
 
@@ -654,52 +707,38 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
     for (uint32_t b = (nv << 4) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
 }
 
-// One warp per tile: the LEB128 bytes of the tile's first gap, then the in-tile gaps
-// (differences of the slot's u16 lane offsets, < 2^14: one or two bytes each) encoded 32 at
-// a time — byte positions from a ballot of the two-byte ones — and the raw values copied
-// to their final offsets in the body.
-// BATCHED (chosen on the host when some tile has > 1024 changes): every tile's gaps in
-// batches of 256 with the offsets loaded up front; 40 registers at 6 CTAs per SM, where
-// the sparse variant keeps 32 registers at 8 CTAs per SM.
-template <int W, bool FIXED, bool BATCHED = false>
-__global__ void __launch_bounds__(256, BATCHED ? 6 : 8)
+// One warp per tile.  LEB128 codec: K1 left the tile's in-tile gaps already encoded in its
+// slot, so the warp writes the first gap's bytes (one lane per byte), then copies the in-tile
+// bytes and the raw values to their final offsets — two warp-wide copies, no per-entry work.
+// FIXED (reading R18): absolute indices lane_base + offset as u32 / u64, via shared memory.
+template <int W, bool FIXED>
+__global__ void __launch_bounds__(256, 6)
 k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
     if (summary->overflow || summary->body_bytes > cap) return;  // emit gate (async extract)
     const int lane = threadIdx.x & 31;
-    const uint32_t lt_mask = (1u << lane) - 1u;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    // FIXED: absolute indices staged per warp in shared memory, then copied to the body
     __shared__ __align__(16) unsigned long long s_fix[FIXED ? 8 * 256 + 2 : 1];
     for (uint32_t t = wg; t < ntiles; t += nw) {
-        // sparse variant: the first 256 slot offsets are loaded before the plan entry arrives
-        // (every tile's slot region holds slot_cap >= 512 entries, so the unguarded loads
-        // stay inside it; entries past the count are never used)
-        uint32_t o[8];
-        if constexpr (!FIXED && !BATCHED) {
-            const uint16_t *so0 = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
-#pragma unroll
-            for (int r = 0; r < 8; ++r) o[r] = so0[r * 32 + lane];
-        }
         const TileEmit pe = plan[t];
-        const uint32_t ecount = pe.count_internal & 0xFFFFu;
-        if (ecount == 0) continue;
+        const uint32_t count = pe.count_internal & 0xFFFFu;
+        if (count == 0) continue;
         const TensorBase tb = bases[pe.k];
-        const struct {
-            unsigned long long ib, vb, g0;
-            uint32_t count, internal_bytes;
-        } e{tb.ib + pe.ib, tb.vb + pe.eb * W, pe.g0, ecount, pe.count_internal >> 16};
-        if constexpr (FIXED) {  // reading R18: lane_base + offset as u32 / u64, little-endian
-            const uint32_t iw = e.internal_bytes;  // the index width (set by K2b for FIXED)
-            const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
+        uint8_t *ib = out + (tb.ib + pe.ib);
+        uint8_t *vb = out + (tb.vb + pe.eb * W);
+        const uint8_t *sv = reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap);
+        const uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
+        if constexpr (FIXED) {
+            const uint32_t iw = pe.count_internal >> 16;  // the index width (set by K2b for FIXED)
+            const uint16_t *so = reinterpret_cast<const uint16_t *>(sb);
             unsigned long long *buf = s_fix + 256 * (threadIdx.x >> 5);
-            uint8_t *dst = out + e.ib;
-            for (uint32_t b = 0; b < e.count; b += 256) {
-                const uint32_t n = min(256u, e.count - b);
+            uint8_t *dst = ib;
+            for (uint32_t b = 0; b < count; b += 256) {
+                const uint32_t n = min(256u, count - b);
                 for (uint32_t i = lane; i < n; i += 32) {
-                    const unsigned long long x = e.g0 + so[b + i];
+                    const unsigned long long x = pe.g0 + so[b + i];
                     if (iw == 4) reinterpret_cast<uint32_t *>(buf)[i] = (uint32_t)x;
                     else buf[i] = x;
                 }
@@ -708,101 +747,16 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
                 __syncwarp();
                 dst += (size_t)n * iw;
             }
-            warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), e.count * W,
-                      lane);
+            warp_copy(vb, sv, count * W, lane);
             continue;
         }
-        uint8_t *ib = out + e.ib;
-        unsigned long long g = e.g0;
+        // the first gap: byte n = 7-bit group n, continuation bit on all but the last
+        const unsigned long long g = pe.g0;
         const uint32_t L0 = leb_len(g);
-        if (lane == 0) {
-            for (uint32_t n = 0; n + 1 < L0; ++n) {
-                ib[n] = (uint8_t)(g | 0x80);
-                g >>= 7;
-            }
-            ib[L0 - 1] = (uint8_t)g;
-        }
-        const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
-        uint8_t *p = ib + L0;
-        const uint32_t c = e.count;
-        if constexpr (BATCHED) {  // dense regime: the values first, then batches of 256 gaps
-            warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
-            uint32_t last = 0;  // offset of the entry before the batch
-            for (uint32_t b0 = 0; b0 < c; b0 += 256) {
-                uint32_t o[8];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const uint32_t i = b0 + r * 32 + lane;
-                    o[r] = i < c ? (uint32_t)so[i] : 0u;
-                }
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    if (b0 + (uint32_t)r * 32u >= c) break;
-                    const uint32_t i = b0 + r * 32 + lane;
-                    uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
-                    const uint32_t carry = r ? __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31) : last;
-                    if (lane == 0) prev = carry;
-                    const bool act = i >= 1 && i < c;
-                    const uint32_t gi = act ? o[r] - prev : 0u;
-                    const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
-                    const uint32_t skip = (b0 == 0 && r == 0) ? 1u : 0u;  // entry 0 has no in-tile gap
-                    if (act) {
-                        uint8_t *q = p + (lane - skip) + __popc(two & lt_mask);
-                        if (gi < 128u) {
-                            q[0] = (uint8_t)gi;
-                        } else {
-                            q[0] = (uint8_t)(gi | 0x80u);
-                            q[1] = (uint8_t)(gi >> 7);
-                        }
-                    }
-                    p += min(32u, c - b0 - r * 32u) - skip + __popc(two);
-                }
-                last = __shfl_sync(0xffffffffu, o[7], 31);
-            }
-            continue;
-        }
-        if (c <= 256) {  // ~all tiles up to a few % density: every load of the tile issued up front
-            warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), c * W, lane);
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                if ((uint32_t)r * 32u >= c) break;
-                const uint32_t i = r * 32 + lane;
-                uint32_t prev = __shfl_up_sync(0xffffffffu, o[r], 1);
-                const uint32_t carry = __shfl_sync(0xffffffffu, o[r ? r - 1 : 0], 31);
-                if (lane == 0) prev = carry;
-                const bool act = i >= 1 && i < c;
-                const uint32_t gi = act ? o[r] - prev : 0u;
-                const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
-                if (act) {
-                    uint8_t *q = p + (lane - (r == 0 ? 1 : 0)) + __popc(two & lt_mask);
-                    if (gi < 128u) {
-                        q[0] = (uint8_t)gi;
-                    } else {
-                        q[0] = (uint8_t)(gi | 0x80u);
-                        q[1] = (uint8_t)(gi >> 7);
-                    }
-                }
-                p += min(32u, c - r * 32u) - (r == 0 ? 1u : 0u) + __popc(two);
-            }
-            continue;
-        }
-        for (uint32_t i0 = 1; i0 < e.count; i0 += 32) {
-            const uint32_t i = i0 + lane;
-            const bool act = i < e.count;
-            const uint32_t gi = act ? (uint32_t)(so[i] - so[i - 1]) : 0u;
-            const uint32_t two = __ballot_sync(0xffffffffu, act && gi >= 128u);
-            if (act) {
-                uint8_t *q = p + lane + __popc(two & lt_mask);
-                if (gi < 128u) {
-                    q[0] = (uint8_t)gi;
-                } else {
-                    q[0] = (uint8_t)(gi | 0x80u);
-                    q[1] = (uint8_t)(gi >> 7);
-                }
-            }
-            p += min(32u, e.count - i0) + __popc(two);
-        }
-        warp_copy(out + e.vb, reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap), e.count * W, lane);
+        if ((uint32_t)lane < L0)
+            ib[lane] = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
+        warp_copy(ib + L0, sb, pe.count_internal >> 16, lane);
+        warp_copy(vb, sv, count * W, lane);
     }
 }
 
@@ -853,7 +807,9 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
     if (a.ntiles)
-        (a.advance ? k_scan_tiles<W, false, true> : a.mode == 1 ? k_scan_tiles<W, true> : k_scan_tiles<W>)
+        (a.index_codec ? (a.advance ? k_scan_tiles<W, false, true, true>
+                                    : a.mode == 1 ? k_scan_tiles<W, true, false, true> : k_scan_tiles<W, false, false, true>)
+                       : (a.advance ? k_scan_tiles<W, false, true> : a.mode == 1 ? k_scan_tiles<W, true> : k_scan_tiles<W>))
             <<<a.ntiles, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
                                       static_cast<LT *>(a.slot_val), a.meta, a.summary, a.redo_cap);
     if (ev) cudaEventRecord(ev[1], s);
@@ -879,10 +835,6 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
         k_emit_tiles<W, true><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                             static_cast<const LT *>(a.slot_val), out, a.summary,
                                                             a.out_cap);
-    else if (a.slot_cap > kDenseEmitSlot)  // some tile has > kDenseEmitSlot changes
-        k_emit_tiles<W, false, true><<<a.sm_count * 6, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
-                                                                   static_cast<const LT *>(a.slot_val), out,
-                                                                   a.summary, a.out_cap);
     else
         k_emit_tiles<W, false><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                              static_cast<const LT *>(a.slot_val), out, a.summary,

@@ -15,7 +15,6 @@ constexpr int kTileBlock = 4096;   // tiles per block of the tile-level scans (1
 constexpr int kByteChunk = 4096;   // index-stream bytes per A2/A4 chunk (256 threads x 16)
 constexpr int kHalo = 16;          // bytes before a chunk kept for varints that straddle it
 constexpr uint32_t kStageGapBytes = 2048;
-constexpr uint32_t kDenseEmitSlot = 1024;  // slots above this (a tile with > 1024 changes): batched K4  // slot sizes above this: K1's predicated (dense) compaction
 
 constexpr uint32_t kTileFirstOfTensor = 1u << 31;
 constexpr uint32_t kTileAligned = 1u << 30;
