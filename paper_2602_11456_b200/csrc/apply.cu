@@ -386,10 +386,12 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
         if (v.last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (v.b[pl] & 0x80))
             err = err ? err : kTruncated;
         if (err != kOk) set_status(st, err);
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (__all_sync(0xffffffffu, sum < (1ull << 26))) {  // 32 lanes x 2^26 < 2^32: no overflow
+            sum = __reduce_add_sync(0xffffffffu, (uint32_t)sum);
+        } else {  // saturating (a malformed stream can decode to gaps up to 2^64 - 1)
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-            sum = sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+            for (int o = 16; o > 0; o >>= 1) sum = sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
         }
         if (lane == 0) {
             s_cnt[warp] = cnt;

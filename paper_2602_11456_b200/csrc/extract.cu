@@ -707,12 +707,51 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
     for (uint32_t b = (nv << 4) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
 }
 
+// Up to 1 KiB of a 4-byte aligned source copied by a warp to any destination, with every
+// load issued before any store (one memory round trip): destination words assembled from
+// funnel-shifted source words (8 per lane), plus the < 4 head and < 4 tail bytes.  Reads at
+// most 4 bytes past the source range (slots are padded).
+struct CopyBatch {
+    uint32_t w[9];    // source words lane + 32 i (the word after each comes from the next lane)
+    uint32_t hb, tb;  // this lane's head / tail byte
+};
+__device__ __forceinline__ void copy_load(CopyBatch &c, uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
+    const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
+    const uint32_t nw = (n - head) >> 2;
+    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        const uint32_t j = lane + 32 * i;
+        c.w[i] = j <= nw ? __ldg(s32 + j) : 0u;  // word nw: the last word's successor
+    }
+    const uint32_t tail0 = head + 4 * nw;
+    c.hb = (uint32_t)lane < head ? src[lane] : 0u;
+    c.tb = (uint32_t)lane < n - tail0 ? src[tail0 + lane] : 0u;
+}
+__device__ __forceinline__ void copy_store(const CopyBatch &c, uint8_t *dst, uint32_t n, int lane) {
+    const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
+    const uint32_t nw = (n - head) >> 2;
+    const uint32_t sh = 8u * head;
+    uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + head);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t j = lane + 32 * i;
+        const uint32_t up = __shfl_down_sync(0xffffffffu, c.w[i], 1);
+        const uint32_t wrap = __shfl_sync(0xffffffffu, c.w[i + 1], 0);
+        const uint32_t nxt = lane == 31 ? wrap : up;
+        if (j < nw) d32[j] = sh ? __funnelshift_r(c.w[i], nxt, sh) : c.w[i];
+    }
+    const uint32_t tail0 = head + 4 * nw;
+    if ((uint32_t)lane < head) dst[lane] = (uint8_t)c.hb;
+    if ((uint32_t)lane < n - tail0) dst[tail0 + lane] = (uint8_t)c.tb;
+}
+
 // One warp per tile.  LEB128 codec: K1 left the tile's in-tile gaps already encoded in its
 // slot, so the warp writes the first gap's bytes (one lane per byte), then copies the in-tile
 // bytes and the raw values to their final offsets — two warp-wide copies, no per-entry work.
 // FIXED (reading R18): absolute indices lane_base + offset as u32 / u64, via shared memory.
 template <int W, bool FIXED>
-__global__ void __launch_bounds__(256, 6)
+__global__ void __launch_bounds__(256, 4)
 k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
@@ -721,8 +760,10 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
     __shared__ __align__(16) unsigned long long s_fix[FIXED ? 8 * 256 + 2 : 1];
+    TileEmit pnext = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
     for (uint32_t t = wg; t < ntiles; t += nw) {
-        const TileEmit pe = plan[t];
+        const TileEmit pe = pnext;  // this tile's plan, loaded one iteration ahead
+        if (t + nw < ntiles) pnext = plan[t + nw];
         const uint32_t count = pe.count_internal & 0xFFFFu;
         if (count == 0) continue;
         const TensorBase tb = bases[pe.k];
@@ -755,8 +796,17 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
         const uint32_t L0 = leb_len(g);
         if ((uint32_t)lane < L0)
             ib[lane] = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
-        warp_copy(ib + L0, sb, pe.count_internal >> 16, lane);
-        warp_copy(vb, sv, count * W, lane);
+        const uint32_t ni = pe.count_internal >> 16, nv = count * W;
+        if (ni <= 1024 && nv <= 1024) {  // ~every tile up to a few % density: one round trip
+            CopyBatch ci, cv;
+            copy_load(ci, ib + L0, sb, ni, lane);
+            copy_load(cv, vb, sv, nv, lane);
+            copy_store(ci, ib + L0, ni, lane);
+            copy_store(cv, vb, nv, lane);
+        } else {
+            warp_copy(ib + L0, sb, ni, lane);
+            warp_copy(vb, sv, nv, lane);
+        }
     }
 }
 
