@@ -212,6 +212,35 @@ int delta_extract_async(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n,
                         void *out_dev, uint64_t out_capacity, uint64_t *body_bytes_dev,
                         void *stream);
 
+/* delta_extract_scan_async + delta_extract_emit_async — delta_extract_async in its two
+ * phases, for the fused multi-GPU emit + assembly (the
+ * in-box analog of the paper's cut-through emission).
+ *
+ * delta_extract_scan_async: compare, compaction and offset table (K1-K3) on `stream`; writes
+ * this rank's body size to size_dev (device, 8-byte aligned u64; UINT64_MAX if a tile
+ * overflowed its slot; may be NULL).  No host synchronisation.  Must be followed by exactly
+ * one delta_extract_emit_async on the same ctx and stream (DELTA_EINVAL otherwise).
+ *
+ * delta_extract_emit_async: writes the body to out_dev (out_capacity bytes) and, if peer_dev
+ * is not NULL, the same bytes to peer_dev (peer_capacity bytes; e.g. the root's assembled-body
+ * buffer mapped into this process with CUDA IPC, so the stores go over NVLink) at byte offset
+ * sum(sizes_dev[q], q < rank) — every record lands at its global offset straight from the
+ * compaction, with no separate copy of the body.  sizes_dev: n_ranks u64 on this device (e.g. an
+ * NCCL all-gather of every rank's size_dev); rank < n_ranks.  body_bytes_dev (may be NULL)
+ * receives the size, or UINT64_MAX if the local gate is closed.  The local body is written iff
+ * the scan fitted and the body fits out_capacity; the peer copy iff, in addition, no size is
+ * UINT64_MAX and the records fit peer_capacity.  delta_extract_wait reports the outcome of both:
+ * DELTA_EAGAIN (a tile overflowed here, or another rank's size was UINT64_MAX: nothing was
+ * assembled), DELTA_ECAPACITY (out or peer too small).  The caller orders the peer stores
+ * before the root's readers (e.g. an NCCL all-reduce on this stream after the call).
+ * Errors (immediate): as delta_size; DELTA_EINVAL for a missing scan phase, misaligned size
+ * pointers, NULL sizes_dev with a peer, or rank >= n_ranks. */
+int delta_extract_scan_async(delta_ctx *ctx, const delta_tensor *tensors, uint32_t n, int elem,
+                             uint64_t *size_dev, void *stream);
+int delta_extract_emit_async(delta_ctx *ctx, void *out_dev, uint64_t out_capacity, uint64_t *body_bytes_dev,
+                             void *peer_dev, uint64_t peer_capacity, const uint64_t *sizes_dev, uint32_t n_ranks,
+                             uint32_t rank, void *stream);
+
 /* delta_extract_wait — wait for the last delta_extract_async on ctx (an event, not the
  * whole stream) and report the outcome of EVERY delta_extract_async since the previous wait
  * (a closed emit gate in any of them is reported, not only in the last); *body_bytes (host,
@@ -285,37 +314,6 @@ int delta_apply_wait(delta_ctx *ctx, void *stream);
  * root's readers (e.g. an NCCL all-reduce on the same stream after it). */
 int delta_assemble(delta_ctx *ctx, const void *src_dev, void *dst_peer_dev, uint64_t dst_capacity,
                    const uint64_t *sizes_dev, uint32_t n_ranks, uint32_t rank, void *stream);
-
-/* Flag-based assembly for contiguous shards — the S2 + S3 exchange with no collective on the
- * data path.  board_root_dev: n_ranks entries of 32 bytes {u64 size, u64 tag, u64 done, pad}
- * in the ROOT's memory (zero-initialised once; mapped into every rank with CUDA IPC; one
- * board per body buffer when buffers alternate).  delta_assemble_flags (every rank, rank 0
- * included): publishes *size_dev (this rank's body size, device) and `tag` in board[rank]
- * with release stores, waits (acquire loads over NVLink) until board[q].tag == tag for every
- * q < rank, then copies src_dev (16-byte aligned; rank 0: nothing, its records are extracted
- * in place) into dst_root_dev at sum(board[q].size, q < rank) and finally sets
- * board[rank].done = tag.  delta_assemble_flags_wait (the root): waits until every rank's
- * done == tag, ordering the root's readers after the copies.  `tag`: the step number, > 0,
- * the same on every rank and increasing per board.  Waits are bounded (~10 s); a peer that
- * never arrives, or an overflowing destination, is reported by delta_assemble_wait
- * (DELTA_ECAPACITY).  Asynchronous on `stream`. */
-int delta_assemble_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *size_dev, void *dst_root_dev,
-                         uint64_t dst_capacity, void *board_root_dev, uint32_t n_ranks, uint32_t rank,
-                         uint64_t tag, void *stream);
-int delta_assemble_flags_wait(delta_ctx *ctx, const void *board_root_dev, uint32_t n_ranks, uint64_t tag,
-                              void *stream);
-
-/* delta_assemble_records_flags — the flag-based exchange for any partition (LPT): this rank's
- * entries of local_sizes_dev (n_global uint64 in global order, from delta_record_sizes) are
- * stored into root_sizes_dev (the root's global-order array, n_global uint64, IPC-mapped),
- * then board[rank].tag = tag; once every rank's tag is there, each local record j is copied
- * from src_dev (this rank's body, records back to back in local order) to dst_root_dev at
- * the global offset sum(root_sizes_dev[0 .. gidx_dev[j] - 1]), and board[rank].done = tag.
- * The root waits with delta_assemble_flags_wait.  Errors as delta_assemble_flags. */
-int delta_assemble_records_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *local_sizes_dev,
-                                 const uint32_t *gidx_dev, uint32_t n_local, uint32_t n_global, void *dst_root_dev,
-                                 uint64_t dst_capacity, void *board_root_dev, uint64_t *root_sizes_dev,
-                                 uint32_t n_ranks, uint32_t rank, uint64_t tag, void *stream);
 
 /* Record-granular assembly, for any tensor partition (LPT balances the
  * shards better than contiguous ranges, but then a rank's records are not one byte range of

@@ -302,6 +302,32 @@ class DeltaContext:
                                                   out.numel(), c_void_p(size.data_ptr()), _stream_handle(stream)))
         return DeviceTable(self._lib.delta_table_dev(self._h), tl.n, self)
 
+    def delta_extract_scan_async(self, tensors, size, stream=None):
+        """Phase 1 of the async extract (compare, compaction, offset table): ``size`` (int64
+        CUDA tensor, 1 element) receives this rank's body size on the device (-1 if a tile
+        overflowed).  Follow with ``delta_extract_emit_async``."""
+        tl = self._tensors(tensors)
+        self._ntensors_last = tl.n
+        if size is not None and (size.dtype != torch.int64 or not size.is_cuda or size.numel() != 1):
+            raise ValueError("size must be a one-element int64 CUDA tensor")
+        self._check(self._lib.delta_extract_scan_async(self._h, tl.arr, tl.n, _ELEM[tl.width],
+                                                       c_void_p(size.data_ptr() if size is not None else 0),
+                                                       _stream_handle(stream)))
+
+    def delta_extract_emit_async(self, out, size, peer=None, sizes=None, rank: int = 0, stream=None) -> "DeviceTable":
+        """Phase 2: the body into ``out`` (uint8 CUDA tensor) and, with ``peer`` (uint8 CUDA
+        tensor, e.g. the root's buffer mapped by CUDA IPC), the same bytes into ``peer`` at
+        sum(sizes[:rank]) — the fused emit + assembly.  ``sizes``: int64 CUDA tensor of every
+        rank's size.  ``size`` receives the body size.  Pair with ``extract_wait``."""
+        if out.dtype != torch.uint8 or not out.is_contiguous() or not out.is_cuda:
+            raise ValueError("out must be a contiguous uint8 CUDA tensor")
+        pp = c_void_p(peer.data_ptr()) if peer is not None else c_void_p(0)
+        self._check(self._lib.delta_extract_emit_async(
+            self._h, out.data_ptr(), out.numel(), c_void_p(size.data_ptr() if size is not None else 0), pp,
+            peer.numel() if peer is not None else 0, c_void_p(sizes.data_ptr() if sizes is not None else 0),
+            sizes.numel() if sizes is not None else 0, rank, _stream_handle(stream)))
+        return DeviceTable(self._lib.delta_table_dev(self._h), self._ntensors_last, self)
+
     def extract_wait(self) -> int:
         """Wait for the last delta_extract_async; returns the body size.  Raises DeltaError
         with status EAGAIN after a slot overflow (workspace grown: issue the extract, and
@@ -310,23 +336,26 @@ class DeltaContext:
         self._check(self._lib.delta_extract_wait(self._h, byref(nbytes)))
         return nbytes.value
 
-    def round_trip(self, tensors, targets, out, size, stream=None, before_apply=None, wait=True):
+    def round_trip(self, tensors, targets, out, size, stream=None, before_apply=None, wait=True, extract=None):
         """extract(tensors) -> apply into ``targets`` as one stream of kernels: the apply
         reads the body size and offset table on the device (delta_apply_async_chain), so
         the host waits once, at the end.  ``before_apply(out, size)`` may enqueue work
-        between the two (e.g. the multi-GPU body assembly).  A first call at a higher
-        density that overflows the tile slots (EAGAIN) is re-issued once.  Returns the
-        body size.  ``wait=False``: enqueue only and return None — the host never waits, an
-        overflow leaves the apply's gate closed (targets untouched) and is reported by the
-        next extract_wait / apply_wait (steady-state loops after a first waited call)."""
+        between the two (e.g. the multi-GPU body assembly).  ``extract(tensors, out, size,
+        stream) -> DeviceTable`` replaces the plain async extract (e.g. the fused multi-GPU
+        emit, dist.FusedAssembler).  A first call at a higher density that overflows the tile
+        slots (EAGAIN) is re-issued once.  Returns the body size.  ``wait=False``: enqueue
+        only and return None — the host never waits, an overflow leaves the apply's gate
+        closed (targets untouched) and is reported by the next extract_wait / apply_wait
+        (steady-state loops after a first waited call)."""
+        ex = extract or (lambda tl, o, sz, st: self.delta_extract_async(tl, o, sz, st))
         if not wait:  # enqueue only; errors surface at the next extract_wait / apply_wait
-            table = self.delta_extract_async(tensors, out, size, stream)
+            table = ex(tensors, out, size, stream)
             if before_apply is not None:
                 before_apply(out, size)
             self.delta_apply(targets, out, table=table, size=size, stream=stream, wait=False)
             return None
         for attempt in range(2):
-            table = self.delta_extract_async(tensors, out, size, stream)
+            table = ex(tensors, out, size, stream)
             if before_apply is not None:
                 before_apply(out, size)
             self.delta_apply(targets, out, table=table, size=size, stream=stream, wait=False)
@@ -386,27 +415,6 @@ class DeltaContext:
                                              c_void_p(dst_peer.data_ptr()), dst_peer.numel(),
                                              c_void_p(sizes.data_ptr()), sizes.numel(), rank,
                                              _stream_handle(stream)))
-
-    def assemble_flags(self, src, size, dst, board, n_ranks: int, rank: int, tag: int, stream=None):
-        """delta_assemble_flags: ``size`` one-element int64 CUDA tensor (this rank's body
-        size), ``dst`` the root's body buffer and ``board`` the root's board slice
-        (int64 CUDA tensor of 4 x n_ranks), both local or IPC-mapped."""
-        self._check(self._lib.delta_assemble_flags(self._h, c_void_p(src.data_ptr() if src.numel() else 0),
-                                                   c_void_p(size.data_ptr()), c_void_p(dst.data_ptr()), dst.numel(),
-                                                   c_void_p(board.data_ptr()), n_ranks, rank, tag,
-                                                   _stream_handle(stream)))
-
-    def assemble_records_flags(self, src, local_sizes, gidx, dst, board, root_sizes, n_ranks: int, rank: int,
-                               tag: int, stream=None):
-        """delta_assemble_records_flags (any partition, no collective)."""
-        self._check(self._lib.delta_assemble_records_flags(
-            self._h, c_void_p(src.data_ptr() if src.numel() else 0), c_void_p(local_sizes.data_ptr()),
-            c_void_p(gidx.data_ptr()), gidx.numel(), local_sizes.numel(), c_void_p(dst.data_ptr()), dst.numel(),
-            c_void_p(board.data_ptr()), c_void_p(root_sizes.data_ptr()), n_ranks, rank, tag, _stream_handle(stream)))
-
-    def assemble_flags_wait(self, board, n_ranks: int, tag: int, stream=None):
-        self._check(self._lib.delta_assemble_flags_wait(self._h, c_void_p(board.data_ptr()), n_ranks, tag,
-                                                        _stream_handle(stream)))
 
     def table_dev_ptr(self) -> int:
         """Device pointer of this context's offset table (delta_table_dev): valid after an

@@ -83,6 +83,7 @@ struct delta_ctx {
     ExtractSummary *h_summary = nullptr;  // pinned
     ExtractSticky *h_sticky = nullptr;    // pinned: outcome of every async extract since the last wait
     cudaStream_t async_stream = nullptr;
+    bool scan_phase = false;  // a delta_extract_scan_async awaits its emit
 
     // ---- apply workspace
     DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status, asm_off, dg_ws;
@@ -727,22 +728,20 @@ extern "C" int delta_extract(delta_ctx *ctx, const delta_tensor *t, uint32_t n, 
 // back to back; K4/K5 write the body only if the scan fitted its tile slots and the body
 // fits `cap`, and write the size (or ~0) to body_bytes_dev.  delta_extract_wait reports
 // the outcome.
-extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *out,
-                                   uint64_t cap, uint64_t *body_bytes_dev, void *stream) {
-    if (!ctx) return DELTA_EINVAL;
-    ctx->err.clear();
-    ctx->detail = 0;
+// Enqueue-only extract in two phases (no host synchronisation when the plan is cached).
+// Phase 1 (scan, K1-K3) on the context's cached plan; phase 2 (emit, K4-K5) writes the body
+// only if the scan fitted its tile slots and the body fits `cap` (and, fused assembly, the
+// peer copy only if every rank's size is known and the records fit the peer buffer).
+static int extract_scan_async(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem,
+                              uint64_t *size_dev, cudaStream_t s) {
     const int w = elem_width(elem);
     if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
-    if (cap && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
     if (ctx->advance)  // an overflow retry needs the host: extract-and-advance is synchronous only
         return fail(ctx, DELTA_EINVAL, 0, "DELTA_OPT_ADVANCE needs delta_size / delta_extract");
-    if (reinterpret_cast<uintptr_t>(body_bytes_dev) % 8)
-        return fail(ctx, DELTA_EINVAL, 0, "body_bytes_dev not 8-byte aligned");
+    if (reinterpret_cast<uintptr_t>(size_dev) % 8) return fail(ctx, DELTA_EINVAL, 0, "size not 8-byte aligned");
     int rc = validate_tensors(ctx, t, n, w);
     if (rc) return rc;
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     rc = build_plan(ctx, t, n, w, s);
     if (rc) return rc;
     rc = prepare_scan(ctx);
@@ -753,13 +752,36 @@ extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32
     if (!ctx->async_pending) CK(cudaMemsetAsync(ctx->sticky.p, 0, sizeof(ExtractSticky), s), "memset");
     CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
     ExtractArgs a = extract_args(ctx);
+    a.scan_size_out = reinterpret_cast<unsigned long long *>(size_dev);
+    CK(launch_extract_scan(a, s, prof_scan(ctx)), "extract scan launch");
+    if (!n && size_dev) CK(cudaMemsetAsync(size_dev, 0, 8, s), "memset");
+    ctx->scan_phase = true;
+    return DELTA_OK;
+}
+
+static int extract_emit_async(delta_ctx *ctx, void *out, uint64_t cap, uint64_t *body_bytes_dev, void *peer,
+                              uint64_t peer_cap, const uint64_t *sizes_dev, uint32_t n_ranks, uint32_t rank,
+                              cudaStream_t s) {
+    if (!ctx->scan_phase) return fail(ctx, DELTA_EINVAL, 0, "no delta_extract_scan_async to emit");
+    if (cap && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
+    if (reinterpret_cast<uintptr_t>(body_bytes_dev) % 8)
+        return fail(ctx, DELTA_EINVAL, 0, "body_bytes_dev not 8-byte aligned");
+    if (peer && (!sizes_dev || rank >= n_ranks))
+        return fail(ctx, DELTA_EINVAL, 0, "peer destination needs sizes_dev and rank < n_ranks");
+    ctx->scan_phase = false;
+    ExtractArgs a = extract_args(ctx);
     a.out_cap = cap;
     a.size_out = reinterpret_cast<unsigned long long *>(body_bytes_dev);
     a.sticky = ctx->sticky.as<ExtractSticky>();
-    CK(launch_extract_scan(a, s, prof_scan(ctx)), "extract scan launch");
-    if (n) {
-        CK(launch_extract_emit(a, static_cast<uint8_t *>(out), s, prof_emit(ctx)),
-           "extract emit launch");
+    if (peer) {
+        a.peer.base = static_cast<uint8_t *>(peer);
+        a.peer.cap = peer_cap;
+        a.peer.sizes = reinterpret_cast<const unsigned long long *>(sizes_dev);
+        a.peer.n_ranks = n_ranks;
+        a.peer.rank = rank;
+    }
+    if (ctx->ntensors) {
+        CK(launch_extract_emit(a, static_cast<uint8_t *>(out), s, prof_emit(ctx)), "extract emit launch");
     } else if (body_bytes_dev) {
         CK(cudaMemsetAsync(body_bytes_dev, 0, 8, s), "memset");
     }
@@ -770,6 +792,38 @@ extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32
     ctx->async_stream = s;
     ctx->async_cap = cap;
     return DELTA_OK;
+}
+
+extern "C" int delta_extract_async(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem, void *out,
+                                   uint64_t cap, uint64_t *body_bytes_dev, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    if (cap && !out) return fail(ctx, DELTA_EINVAL, 0, "out_dev is NULL");
+    if (reinterpret_cast<uintptr_t>(body_bytes_dev) % 8)
+        return fail(ctx, DELTA_EINVAL, 0, "body_bytes_dev not 8-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = extract_scan_async(ctx, t, n, elem, nullptr, s);
+    if (rc) return rc;
+    return extract_emit_async(ctx, out, cap, body_bytes_dev, nullptr, 0, nullptr, 0, 0, s);
+}
+
+extern "C" int delta_extract_scan_async(delta_ctx *ctx, const delta_tensor *t, uint32_t n, int elem,
+                                        uint64_t *size_dev, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    return extract_scan_async(ctx, t, n, elem, size_dev, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int delta_extract_emit_async(delta_ctx *ctx, void *out, uint64_t cap, uint64_t *body_bytes_dev,
+                                        void *peer, uint64_t peer_cap, const uint64_t *sizes_dev, uint32_t n_ranks,
+                                        uint32_t rank, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    return extract_emit_async(ctx, out, cap, body_bytes_dev, peer, peer_cap, sizes_dev, n_ranks, rank,
+                              static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int delta_extract_wait(delta_ctx *ctx, uint64_t *body_bytes) {
@@ -805,6 +859,10 @@ extern "C" int delta_extract_wait(delta_ctx *ctx, uint64_t *body_bytes) {
     if (sk.over_cap)
         return fail(ctx, DELTA_ECAPACITY, 0, "output capacity %llu < body size %llu",
                     (unsigned long long)ctx->async_cap, (unsigned long long)sk.need);
+    if (sk.peer_fail == 1)
+        return fail(ctx, DELTA_EAGAIN, 0, "fused assembly skipped: a rank's extract did not complete (size ~0)");
+    if (sk.peer_fail == 2)
+        return fail(ctx, DELTA_ECAPACITY, 0, "fused assembly skipped: the records do not fit the peer buffer");
     return DELTA_OK;
 }
 
@@ -988,71 +1046,8 @@ extern "C" int delta_assemble(delta_ctx *ctx, const void *src, void *dst, uint64
     return DELTA_OK;
 }
 
-extern "C" int delta_assemble_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *size_dev, void *dst_root_dev,
-                                    uint64_t dst_capacity, void *board_root_dev, uint32_t n_ranks, uint32_t rank,
-                                    uint64_t tag, void *stream) {
-    if (!ctx) return DELTA_EINVAL;
-    ctx->err.clear();
-    ctx->detail = 0;
-    if (!size_dev || !dst_root_dev || !board_root_dev || rank >= n_ranks || tag == 0 || (rank && !src_dev))
-        return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_flags: bad arguments");
-    if (reinterpret_cast<uintptr_t>(src_dev) % 16) return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_flags: src not 16-byte aligned");
-    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!ctx->asm_status.p) {
-        GROW(ctx->asm_status, 16);
-        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
-    }
-    uint32_t *counter = ctx->asm_status.as<uint32_t>() + 2;  // zero-initialised, reset by the last CTA
-    CK(launch_assemble_flags(static_cast<const uint8_t *>(src_dev), reinterpret_cast<const unsigned long long *>(size_dev),
-                             static_cast<uint8_t *>(dst_root_dev), dst_capacity,
-                             static_cast<uint8_t *>(board_root_dev) + (size_t)0, rank, tag, counter,
-                             ctx->asm_status.as<uint32_t>(), ctx->assemble_ctas, s),
-       "assemble flags launch");
-    return DELTA_OK;
-}
 
-extern "C" int delta_assemble_records_flags(delta_ctx *ctx, const void *src_dev, const uint64_t *local_sizes_dev,
-                                            const uint32_t *gidx_dev, uint32_t n_local, uint32_t n_global,
-                                            void *dst_root_dev, uint64_t dst_capacity, void *board_root_dev,
-                                            uint64_t *root_sizes_dev, uint32_t n_ranks, uint32_t rank, uint64_t tag,
-                                            void *stream) {
-    if (!ctx) return DELTA_EINVAL;
-    ctx->err.clear();
-    ctx->detail = 0;
-    if (!local_sizes_dev || !dst_root_dev || !board_root_dev || !root_sizes_dev || rank >= n_ranks || tag == 0 ||
-        n_local > n_global || (n_local && (!src_dev || !gidx_dev)))
-        return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_records_flags: bad arguments");
-    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!ctx->asm_status.p) {
-        GROW(ctx->asm_status, 16);
-        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
-    }
-    CK(launch_assemble_records_flags(static_cast<const uint8_t *>(src_dev),
-                                     reinterpret_cast<const unsigned long long *>(local_sizes_dev), gidx_dev, n_local,
-                                     n_global, static_cast<uint8_t *>(dst_root_dev), dst_capacity, board_root_dev,
-                                     reinterpret_cast<unsigned long long *>(root_sizes_dev), rank, n_ranks, tag,
-                                     ctx->asm_status.as<uint32_t>() + 2, ctx->asm_status.as<uint32_t>(),
-                                     ctx->assemble_ctas, s),
-       "assemble records flags launch");
-    return DELTA_OK;
-}
 
-extern "C" int delta_assemble_flags_wait(delta_ctx *ctx, const void *board_root_dev, uint32_t n_ranks, uint64_t tag,
-                                         void *stream) {
-    if (!ctx) return DELTA_EINVAL;
-    if (!board_root_dev || tag == 0) return fail(ctx, DELTA_EINVAL, 0, "delta_assemble_flags_wait: bad arguments");
-    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!ctx->asm_status.p) {
-        GROW(ctx->asm_status, 16);
-        CK(cudaMemsetAsync(ctx->asm_status.p, 0, 16, s), "memset");
-    }
-    CK(launch_assemble_flags_wait(board_root_dev, n_ranks, tag, ctx->asm_status.as<uint32_t>(), s),
-       "assemble flags wait launch");
-    return DELTA_OK;
-}
 
 extern "C" int delta_record_sizes(delta_ctx *ctx, const delta_record_info *table_dev, uint32_t n_local,
                                   const uint32_t *gidx_dev, uint64_t *sizes_dev, uint32_t n_global, void *stream) {

@@ -7,13 +7,11 @@
 //                between the size exchange and the transfer.  Records are self-contained
 //                and in list order (R4, R15): the concatenation of the rank bodies
 //                in rank order IS the body of the whole tensor list.
-//   k_assemble_flags / k_assemble_flags_wait
-//                the contiguous-shard exchange with no collective: sizes, tags and
-//                completion through flags in the root's memory (release / acquire over
-//                NVLink).
 //   k_record_sizes / k_record_offsets / k_assemble_records
 //                the same for any tensor partition (LPT): each record to its own global
 //                offset, computed on the device from the all-reduced record sizes.
+// The default multi-GPU path no longer runs a separate copy: K4/K5 store each rank's records
+// at their global offsets directly (delta_extract_emit_async with a peer destination).
 //
 // Product code; shares nothing with the test oracle.
 #include <cstdint>
@@ -152,240 +150,6 @@ k_assemble_records(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, u
         }
         for (unsigned long long b = (nv << 4) + gtid; b < rest; b += nthreads) d[head + b] = sh0[b];
     }
-}
-
-// ---------------------------------------------------------------- flag-based assembly
-// The same S2 + S3 with no collective on the data path: the root's "board" (CUDA IPC
-// mapped by every rank) holds, per buffer slot and rank, {size, tag, done}.  Each rank's
-// kernel publishes its body size with a release store, waits (acquire loads over NVLink)
-// for the tags of the lower ranks, copies its body to the offset their sizes give, and the
-// last CTA to finish publishes `done`.  The root waits for every rank's `done` with
-// k_assemble_flags_wait.  `tag` is the caller's step number (identical on all ranks,
-// strictly increasing, > 0).  Waits are bounded: a peer that never arrives sets *status.
-struct BoardEntry {
-    unsigned long long size, tag, done, pad;
-};
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-// spin until *p == want (bounded: ~10 s); false on timeout
-__device__ __forceinline__ bool wait_tag(const unsigned long long *p, unsigned long long want) {
-    for (unsigned long long it = 0; it < (1ull << 26); ++it) {
-        if (ld_acquire_sys(p) == want) return true;
-        __nanosleep(128);
-    }
-    return false;
-}
-
-__global__ void __launch_bounds__(256)
-k_assemble_flags(const uint8_t *__restrict__ src, const unsigned long long *__restrict__ size_dev,
-                 uint8_t *__restrict__ dst_base, unsigned long long capacity, BoardEntry *board, uint32_t rank,
-                 unsigned long long tag, uint32_t *counter, uint32_t *status) {
-    __shared__ unsigned long long s_off, s_n;
-    __shared__ bool s_ok;
-    if (threadIdx.x == 0) {
-        const unsigned long long n = *size_dev;
-        if (blockIdx.x == 0) {  // publish this rank's size, then its tag
-            board[rank].size = n;
-            __threadfence_system();
-            st_release_sys(&board[rank].tag, tag);
-        }
-        unsigned long long off = 0;
-        bool ok = n <= capacity;  // ~0: the extract's gate was closed
-        for (uint32_t q = 0; q < rank && ok; ++q) {
-            ok = wait_tag(&board[q].tag, tag);
-            const unsigned long long sq = ok ? board[q].size : 0ull;
-            ok = ok && sq <= capacity;
-            off += ok ? sq : 0ull;
-        }
-        ok = ok && off + n <= capacity;
-        s_off = off;
-        s_n = n;
-        s_ok = ok;
-        if (!ok && blockIdx.x == 0) atomicExch(status, 1u);
-    }
-    __syncthreads();
-    if (s_ok && rank != 0) {  // rank 0's records were extracted in place at offset 0
-        const unsigned long long n = s_n;
-        uint8_t *dst = dst_base + s_off;
-        const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-        const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-        const uint32_t head = (uint32_t)min(n, (unsigned long long)((16u - ((uintptr_t)dst & 15u)) & 15u));
-        if (gtid < head) dst[gtid] = src[gtid];
-        const unsigned long long rest = n - head, nv = rest >> 4;
-        uint4 *d16 = reinterpret_cast<uint4 *>(dst + head);
-        const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-        const uint32_t q0 = head >> 2, sh = 8u * (head & 3u);
-        for (unsigned long long j = gtid; j < nv; j += nthreads) {
-            const unsigned long long q = q0 + 4 * j;
-            const uint32_t a0 = __ldg(s32 + q), a1 = __ldg(s32 + q + 1), a2 = __ldg(s32 + q + 2),
-                           a3 = __ldg(s32 + q + 3), a4 = __ldg(s32 + q + 4);
-            uint4 o;
-            o.x = __funnelshift_r(a0, a1, sh);
-            o.y = __funnelshift_r(a1, a2, sh);
-            o.z = __funnelshift_r(a2, a3, sh);
-            o.w = __funnelshift_r(a3, a4, sh);
-            d16[j] = o;
-        }
-        for (unsigned long long b = (nv << 4) + gtid; b < rest; b += nthreads) dst[head + b] = src[head + b];
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {  // the last CTA publishes `done`
-        if (atomicAdd(counter, 1u) == gridDim.x - 1) {
-            *counter = 0;
-            __threadfence_system();
-            st_release_sys(&board[rank].done, tag);
-        }
-    }
-}
-
-__global__ void k_assemble_flags_wait(const BoardEntry *board, uint32_t n_ranks, unsigned long long tag,
-                                      uint32_t *status) {
-    if (blockIdx.x || threadIdx.x) return;
-    for (uint32_t q = 0; q < n_ranks; ++q)
-        if (!wait_tag(&board[q].done, tag)) atomicExch(status, 2u);
-}
-
-// Record-granular variant (any partition, e.g. LPT) with the same flags: each rank stores its
-// records' sizes into the root's global-order size array (its own entries only), publishes
-// its tag, waits for every rank's tag, derives all global offsets from that array (each CTA
-// scans it in shared memory), copies its records, and the last CTA publishes `done`.
-// local_sizes: this rank's global-order array from k_record_sizes (stable per slot).
-__global__ void __launch_bounds__(256)
-k_assemble_records_flags(const uint8_t *__restrict__ src, const unsigned long long *__restrict__ local_sizes,
-                         const uint32_t *__restrict__ gidx, uint32_t n_local, uint32_t n_global,
-                         uint8_t *__restrict__ dst, unsigned long long capacity, BoardEntry *board,
-                         unsigned long long *root_sizes, uint32_t rank, uint32_t n_ranks, unsigned long long tag,
-                         uint32_t *counter, uint32_t *status) {
-    extern __shared__ unsigned long long s_dyn[];  // n_global global offsets, then n_local local
-    unsigned long long *s_goff = s_dyn, *s_loff = s_dyn + n_global;
-    __shared__ bool s_ok;
-    __shared__ unsigned long long s_w[8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (blockIdx.x == 0) {
-        for (uint32_t j = threadIdx.x; j < n_local; j += blockDim.x) root_sizes[gidx[j]] = local_sizes[gidx[j]];
-        __threadfence_system();
-        __syncthreads();
-        if (threadIdx.x == 0) st_release_sys(&board[rank].tag, tag);
-    }
-    if (threadIdx.x == 0) {
-        bool ok = true;
-        for (uint32_t q = 0; q < n_ranks && ok; ++q) ok = wait_tag(&board[q].tag, tag);
-        s_ok = ok;
-        if (!ok) atomicExch(status, 1u);
-    }
-    __syncthreads();
-    if (s_ok) {
-        // exclusive scans: global sizes (from the root) -> offsets; local record sizes -> offsets
-        for (int pass = 0; pass < 2; ++pass) {
-            const uint32_t n = pass ? n_local : n_global;
-            unsigned long long *out = pass ? s_loff : s_goff;
-            unsigned long long carry = 0;
-            for (uint32_t b = 0; b < n; b += blockDim.x) {
-                const uint32_t i = b + threadIdx.x;
-                unsigned long long v = 0;
-                if (i < n) v = pass ? local_sizes[gidx[i]] : *(volatile unsigned long long *)&root_sizes[i];
-                unsigned long long inc = v;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += y;
-                }
-                if (lane == 31) s_w[warp] = inc;
-                __syncthreads();
-                unsigned long long pre = 0, tot = 0;
-                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-                    if (w < warp) pre += s_w[w];
-                    tot += s_w[w];
-                }
-                __syncthreads();
-                if (i < n) out[i] = carry + pre + inc - v;
-                carry += tot;
-            }
-            if (pass == 0 && carry > capacity) {  // incl. ~0 sizes from a closed extract gate
-                if (threadIdx.x == 0) {
-                    s_ok = false;
-                    if (blockIdx.x == 0) atomicExch(status, 1u);
-                }
-            }
-            __syncthreads();
-        }
-    }
-    if (s_ok) {
-        const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-        const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-        for (uint32_t j = 0; j < n_local; ++j) {
-            const uint32_t k = gidx[j];
-            const unsigned long long n = local_sizes[k];
-            const uint8_t *sp = src + s_loff[j];
-            uint8_t *d = dst + s_goff[k];
-            const uint32_t head = (uint32_t)min(n, (unsigned long long)((16u - ((uintptr_t)d & 15u)) & 15u));
-            if (gtid < head) d[gtid] = sp[gtid];
-            const unsigned long long rest = n - head, nv = rest >> 4;
-            const uint8_t *sh0 = sp + head;
-            const uint32_t *w = reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(sh0) & ~uintptr_t(3));
-            const uint32_t sh = 8u * (uint32_t)(reinterpret_cast<uintptr_t>(sh0) & 3u);
-            uint4 *d16 = reinterpret_cast<uint4 *>(d + head);
-            for (unsigned long long v = gtid; v < nv; v += nthreads) {
-                const uint32_t *q = w + 4 * v;
-                const uint32_t a0 = __ldg(q), a1 = __ldg(q + 1), a2 = __ldg(q + 2), a3 = __ldg(q + 3), a4 = __ldg(q + 4);
-                uint4 o;
-                o.x = __funnelshift_r(a0, a1, sh);
-                o.y = __funnelshift_r(a1, a2, sh);
-                o.z = __funnelshift_r(a2, a3, sh);
-                o.w = __funnelshift_r(a3, a4, sh);
-                d16[v] = o;
-            }
-            for (unsigned long long b = (nv << 4) + gtid; b < rest; b += nthreads) d[head + b] = sh0[b];
-        }
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (atomicAdd(counter, 1u) == gridDim.x - 1) {
-            *counter = 0;
-            __threadfence_system();
-            st_release_sys(&board[rank].done, tag);
-        }
-    }
-}
-
-cudaError_t launch_assemble_records_flags(const uint8_t *src, const unsigned long long *local_sizes,
-                                          const uint32_t *gidx, uint32_t n_local, uint32_t n_global, uint8_t *dst,
-                                          unsigned long long capacity, void *board, unsigned long long *root_sizes,
-                                          uint32_t rank, uint32_t n_ranks, unsigned long long tag, uint32_t *counter,
-                                          uint32_t *status, int ctas, cudaStream_t s) {
-    const size_t smem = ((size_t)n_global + n_local) * 8;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_assemble_records_flags, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    k_assemble_records_flags<<<ctas, 256, smem, s>>>(src, local_sizes, gidx, n_local, n_global, dst, capacity,
-                                                     static_cast<BoardEntry *>(board), root_sizes, rank, n_ranks, tag,
-                                                     counter, status);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_assemble_flags(const uint8_t *src, const unsigned long long *size_dev, uint8_t *dst,
-                                  unsigned long long capacity, void *board, uint32_t rank, unsigned long long tag,
-                                  uint32_t *counter, uint32_t *status, int ctas, cudaStream_t s) {
-    k_assemble_flags<<<ctas, 256, 0, s>>>(src, size_dev, dst, capacity, static_cast<BoardEntry *>(board), rank, tag,
-                                         counter, status);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_assemble_flags_wait(const void *board, uint32_t n_ranks, unsigned long long tag, uint32_t *status,
-                                       cudaStream_t s) {
-    k_assemble_flags_wait<<<1, 32, 0, s>>>(static_cast<const BoardEntry *>(board), n_ranks, tag, status);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_record_sizes(const RecordRow *table, uint32_t n_local, const uint32_t *gidx,

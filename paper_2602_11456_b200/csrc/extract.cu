@@ -534,8 +534,11 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
                unsigned long long *__restrict__ E, unsigned long long *__restrict__ Bk, uint32_t T,
                const uint32_t *__restrict__ name_len, const unsigned long long *__restrict__ numel,
                RecordRow *__restrict__ table, TensorBase *__restrict__ bases, int width, int fixed,
-               ExtractSummary *summary) {
-    if (summary->overflow) return;
+               ExtractSummary *summary, unsigned long long *size_out) {
+    if (summary->overflow) {
+        if (size_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *size_out = ~0ull;
+        return;
+    }
     __shared__ unsigned long long s_e0, s_b0;
     __shared__ long long s_p0;
     __shared__ bool s_last;
@@ -656,6 +659,7 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
         summary->M = __ldcg(E + T);
         summary->idx_bytes = __ldcg(Bk + T);
         summary->body_bytes = carry;
+        if (size_out != nullptr) *size_out = carry;
     }
 }
 
@@ -707,6 +711,31 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
     for (uint32_t b = (nv << 4) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
 }
 
+// The emit gate (K4/K5): the local body is written iff every tile fitted its slot and the body
+// fits `cap`; the fused-assembly copy (peer.base) iff, in addition, no rank's size is ~0 (its
+// extract did not complete) and this rank's records fit the peer buffer at sum(sizes[q < rank]).
+struct EmitGate {
+    bool local, peer;
+    unsigned long long off;  // this rank's byte offset in the peer buffer
+    unsigned long long fail; // ExtractSticky::peer_fail code when the peer copy is skipped
+};
+__device__ __forceinline__ EmitGate emit_gate(const ExtractSummary *summary, unsigned long long cap,
+                                              const PeerDst &peer) {
+    EmitGate g{!summary->overflow && summary->body_bytes <= cap, false, 0, 0};
+    if (peer.base != nullptr && g.local) {
+        bool ok = true;
+        for (uint32_t q = 0; q < peer.n_ranks; ++q) {
+            const unsigned long long z = peer.sizes[q];
+            if (z == ~0ull) ok = false;
+            else if (q < peer.rank) g.off += z;
+        }
+        if (!ok) g.fail = 1;
+        else if (g.off > peer.cap || summary->body_bytes > peer.cap - g.off) g.fail = 2;
+        g.peer = g.fail == 0;
+    }
+    return g;
+}
+
 // Up to 1 KiB of a 4-byte aligned source copied by a warp to any destination, with every
 // load issued before any store (one memory round trip): destination words assembled from
 // funnel-shifted source words (8 per lane), plus the < 4 head and < 4 tail bytes.  Reads at
@@ -719,10 +748,13 @@ __device__ __forceinline__ void copy_load(CopyBatch &c, uint8_t *dst, const uint
     const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
     const uint32_t nw = (n - head) >> 2;
     const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+    const uint32_t rounds = (nw + 32) >> 5;  // words 0 .. nw (word nw: the last word's successor)
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
         const uint32_t j = lane + 32 * i;
-        c.w[i] = j <= nw ? __ldg(s32 + j) : 0u;  // word nw: the last word's successor
+        c.w[i] = 0u;
+        if ((uint32_t)i >= rounds) continue;  // warp-uniform: only the rounds the copy needs
+        if (j <= nw) c.w[i] = __ldg(s32 + j);
     }
     const uint32_t tail0 = head + 4 * nw;
     c.hb = (uint32_t)lane < head ? src[lane] : 0u;
@@ -733,8 +765,10 @@ __device__ __forceinline__ void copy_store(const CopyBatch &c, uint8_t *dst, uin
     const uint32_t nw = (n - head) >> 2;
     const uint32_t sh = 8u * head;
     uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + head);
+    const uint32_t rounds = (nw + 31) >> 5;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
+        if ((uint32_t)i >= rounds) break;  // warp-uniform
         const uint32_t j = lane + 32 * i;
         const uint32_t up = __shfl_down_sync(0xffffffffu, c.w[i], 1);
         const uint32_t wrap = __shfl_sync(0xffffffffu, c.w[i + 1], 0);
@@ -754,8 +788,10 @@ template <int W, bool FIXED>
 __global__ void __launch_bounds__(256, 4)
 k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
-             uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap) {
-    if (summary->overflow || summary->body_bytes > cap) return;  // emit gate (async extract)
+             uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
+    const EmitGate gate = emit_gate(summary, cap, peer);
+    if (!gate.local) return;  // emit gate (async extract)
+    uint8_t *const pout = gate.peer ? peer.base + gate.off : nullptr;  // fused assembly: the same bytes there too
     const int lane = threadIdx.x & 31;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
@@ -775,7 +811,7 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
             const uint32_t iw = pe.count_internal >> 16;  // the index width (set by K2b for FIXED)
             const uint16_t *so = reinterpret_cast<const uint16_t *>(sb);
             unsigned long long *buf = s_fix + 256 * (threadIdx.x >> 5);
-            uint8_t *dst = ib;
+            uint8_t *dst = ib, *pdst = pout ? pout + (ib - out) : nullptr;
             for (uint32_t b = 0; b < count; b += 256) {
                 const uint32_t n = min(256u, count - b);
                 for (uint32_t i = lane; i < n; i += 32) {
@@ -785,17 +821,22 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
                 }
                 __syncwarp();
                 warp_copy4<false>(dst, reinterpret_cast<const uint8_t *>(buf), n * iw, lane);
+                if (pdst) {  // fused assembly: the same bytes at their global offset
+                    warp_copy4<false>(pdst, reinterpret_cast<const uint8_t *>(buf), n * iw, lane);
+                    pdst += (size_t)n * iw;
+                }
                 __syncwarp();
                 dst += (size_t)n * iw;
             }
             warp_copy(vb, sv, count * W, lane);
+            if (pout) warp_copy(pout + (vb - out), sv, count * W, lane);
             continue;
         }
         // the first gap: byte n = 7-bit group n, continuation bit on all but the last
         const unsigned long long g = pe.g0;
         const uint32_t L0 = leb_len(g);
-        if ((uint32_t)lane < L0)
-            ib[lane] = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
+        const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
+        if ((uint32_t)lane < L0) ib[lane] = g_byte;
         const uint32_t ni = pe.count_internal >> 16, nv = count * W;
         if (ni <= 1024 && nv <= 1024) {  // ~every tile up to a few % density: one round trip
             CopyBatch ci, cv;
@@ -803,9 +844,21 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
             copy_load(cv, vb, sv, nv, lane);
             copy_store(ci, ib + L0, ni, lane);
             copy_store(cv, vb, nv, lane);
+            if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
+                uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
+                if ((uint32_t)lane < L0) pi[lane] = g_byte;
+                copy_store(ci, pi + L0, ni, lane);
+                copy_store(cv, pv, nv, lane);
+            }
         } else {
             warp_copy(ib + L0, sb, ni, lane);
             warp_copy(vb, sv, nv, lane);
+            if (pout) {
+                uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
+                if ((uint32_t)lane < L0) pi[lane] = g_byte;
+                warp_copy(pi + L0, sb, ni, lane);
+                warp_copy(pv, sv, nv, lane);
+            }
         }
     }
 }
@@ -820,8 +873,9 @@ __global__ void __launch_bounds__(128)
 k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__restrict__ name_len,
           const uint32_t *__restrict__ name_off, const uint8_t *__restrict__ names,
           uint8_t *__restrict__ out, int mode, const ExtractSummary *summary, unsigned long long cap,
-          unsigned long long *size_out, ExtractSticky *sticky) {
-    const bool open = !summary->overflow && summary->body_bytes <= cap;
+          unsigned long long *size_out, ExtractSticky *sticky, PeerDst peer) {
+    const EmitGate gate = emit_gate(summary, cap, peer);
+    const bool open = gate.local;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (size_out != nullptr) *size_out = open ? summary->body_bytes : ~0ull;
         if (sticky != nullptr && !open) {  // delta_extract_wait reports every closed gate, not just the last
@@ -833,11 +887,13 @@ k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__res
                 sticky->need = max(sticky->need, summary->body_bytes);
             }
         }
+        if (sticky != nullptr && gate.fail) sticky->peer_fail = max(sticky->peer_fail, gate.fail);
     }
     if (!open) return;
+    for (int dst = 0; dst < (gate.peer ? 2 : 1); ++dst)
     for (uint32_t k = blockIdx.x; k < T; k += gridDim.x) {
         const RecordRow r = table[k];
-        uint8_t *o = out + r.record_offset;
+        uint8_t *o = (dst ? peer.base + gate.off : out) + r.record_offset;
         const uint32_t nl = name_len[k];
         for (uint32_t b = threadIdx.x; b < nl; b += blockDim.x) o[2 + b] = names[name_off[k] + b];
         if (threadIdx.x == 0) {
@@ -869,7 +925,7 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
         if (ev) cudaEventRecord(ev[2], s);
         k_tiles_prefix<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.plan, a.entry_begin,
                                              a.tensor_byte_begin, a.ntensors, a.name_len, a.numel, a.table, a.bases,
-                                             a.width, a.index_codec, a.summary);
+                                             a.width, a.index_codec, a.summary, a.scan_size_out);
     } else if (ev) {
         cudaEventRecord(ev[2], s);
     }
@@ -884,15 +940,15 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
     if (a.index_codec)
         k_emit_tiles<W, true><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                             static_cast<const LT *>(a.slot_val), out, a.summary,
-                                                            a.out_cap);
+                                                            a.out_cap, a.peer);
     else
         k_emit_tiles<W, false><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                              static_cast<const LT *>(a.slot_val), out, a.summary,
-                                                             a.out_cap);
+                                                             a.out_cap, a.peer);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
     k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode, a.summary,
-                                 a.out_cap, a.size_out, a.sticky);
+                                 a.out_cap, a.size_out, a.sticky, a.peer);
     if (ev) cudaEventRecord(ev[2], s);
     return cudaGetLastError();
 }

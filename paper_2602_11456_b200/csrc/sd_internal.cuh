@@ -80,6 +80,16 @@ struct ExtractSticky {
     unsigned long long max_count;   // largest per-tile count over those calls
     unsigned long long over_cap;    // some call's body exceeded its capacity
     unsigned long long need;        // largest such body
+    unsigned long long peer_fail;   // fused assembly skipped: 1 a rank's size was ~0, 2 no room
+};
+
+// Fused emit + assembly (delta_extract_emit_async): a second destination for the body, e.g.
+// the root's assembled-body buffer mapped with CUDA IPC, at the offset sum(sizes[q < rank]).
+struct PeerDst {
+    uint8_t *base = nullptr;               // nullptr: no second destination
+    unsigned long long cap = 0;
+    const unsigned long long *sizes = nullptr;  // n_ranks body sizes (device)
+    uint32_t n_ranks = 0, rank = 0;
 };
 
 // Per-tensor row of the device offset table (same field order as delta_record_info).
@@ -154,6 +164,8 @@ struct ExtractArgs {
     unsigned long long out_cap = ~0ull;
     unsigned long long *size_out = nullptr;
     ExtractSticky *sticky = nullptr;  // async extracts: outcome folded in by K5
+    unsigned long long *scan_size_out = nullptr;  // K2b: the body size, or ~0 if a tile overflowed
+    PeerDst peer;                     // K4/K5: fused assembly destination
 };
 
 // ev: nullptr, or events recorded around the kernels (scan: 4 = before K1, after K1,
@@ -190,16 +202,6 @@ struct ApplyArgs {
 
 cudaError_t launch_blake3(const uint8_t *in, unsigned long long n, uint32_t *ws, uint32_t *out32, cudaStream_t s);
 
-cudaError_t launch_assemble_flags(const uint8_t *src, const unsigned long long *size_dev, uint8_t *dst,
-                                  unsigned long long capacity, void *board, uint32_t rank, unsigned long long tag,
-                                  uint32_t *counter, uint32_t *status, int ctas, cudaStream_t s);
-cudaError_t launch_assemble_records_flags(const uint8_t *src, const unsigned long long *local_sizes,
-                                          const uint32_t *gidx, uint32_t n_local, uint32_t n_global, uint8_t *dst,
-                                          unsigned long long capacity, void *board, unsigned long long *root_sizes,
-                                          uint32_t rank, uint32_t n_ranks, unsigned long long tag, uint32_t *counter,
-                                          uint32_t *status, int ctas, cudaStream_t s);
-cudaError_t launch_assemble_flags_wait(const void *board, uint32_t n_ranks, unsigned long long tag, uint32_t *status,
-                                       cudaStream_t s);
 cudaError_t launch_record_sizes(const RecordRow *table, uint32_t n_local, const uint32_t *gidx,
                                 unsigned long long *sizes, uint32_t n_global, cudaStream_t s);
 cudaError_t launch_assemble_records(const uint8_t *src, uint8_t *dst, unsigned long long capacity,

@@ -177,124 +177,59 @@ class NvlinkAssembler:
         _ipc_teardown(self.device, self.group)
 
 
-class RecordAssembler:
-    """S2 + S3 for any partition (LPT): every rank's records go to their own global offsets
-    in the root's assembled-body buffer.  Per step: ``record_sizes(slot)`` on the extract's
-    stream (right after the extract: this rank's record sizes into a global-order array),
-    then ``assemble(body, slot)`` on a comm stream — an all-reduce (sum) of that array and
-    one delta_assemble_records kernel writing the records over NVLink (CUDA IPC mapping of
-    the root's buffer; the root copies its own records locally) — and a one-element
-    all-reduce as the completion token.  ``nbuf`` root buffers / size arrays: step t's copy
-    overlaps step t+1."""
-
-    def __init__(self, ctx, capacity: int, device, mine, n_global: int, group=None, root: int = 0,
-                 nbuf: int = 2, mode: str = "nccl"):
-        self.ctx, self.group, self.root, self.mode = ctx, group, root, mode
-        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
-        self.device = torch.device(device)
-        self.n_global = n_global
-        self.gidx = torch.tensor(list(mine), dtype=torch.int32, device=self.device)
-        self.sizes = [torch.zeros(n_global, dtype=torch.int64, device=self.device) for _ in range(nbuf)]
-        shared = []
-        if self.rank == root:
-            self.bufs = [torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
-            shared = list(self.bufs)
-            if mode == "flags":  # boards and the global-order size arrays live on the root
-                self.board = torch.zeros(nbuf, self.world, 4, dtype=torch.int64, device=self.device)
-                self.root_sizes = torch.zeros(nbuf, n_global, dtype=torch.int64, device=self.device)
-                shared += [self.board, self.root_sizes]
-            torch.cuda.synchronize(self.device)
-        else:
-            self.bufs = [None] * nbuf
-        handles = [None] * self.world
-        dist.all_gather_object(handles, [reduce_tensor(b) for b in shared] if self.rank == root else None,
-                               group=group)
-        if self.rank == root:
-            mapped = shared
-        else:
-            mapped = []
-            for fn, args in handles[root]:
-                args = list(args)
-                args[6] = self.device.index  # rebuild on this process's device (peer mapping)
-                mapped.append(fn(*args))
-        self.peers = mapped[:nbuf]
-        if mode == "flags":
-            self.pboard, self.proot_sizes = mapped[nbuf], mapped[nbuf + 1]
-        self.token = torch.zeros(1, dtype=torch.float32, device=self.device)
-        self.tag = 0
-
-    def record_sizes(self, table_ptr: int, slot: int = 0, stream=None):
-        self.ctx.record_sizes(table_ptr, self.gidx.numel(), self.gidx, self.sizes[slot], stream=stream)
-
-    def assemble(self, body: torch.Tensor, slot: int = 0, stream=None):
-        stream = stream or torch.cuda.current_stream(self.device)
-        if self.mode == "flags":  # sizes, tags and completion through the root's board
-            self.tag += 1
-            self.ctx.assemble_records_flags(body, self.sizes[slot], self.gidx, self.peers[slot], self.pboard[slot],
-                                            self.proot_sizes[slot], self.world, self.rank, self.tag, stream=stream)
-            if self.rank == self.root:
-                self.ctx.assemble_flags_wait(self.pboard[slot], self.world, self.tag, stream=stream)
-            return self.bufs[slot] if self.rank == self.root else None
-        with torch.cuda.stream(stream):
-            dist.all_reduce(self.sizes[slot], group=self.group)
-            self.ctx.assemble_records(body, self.gidx, self.sizes[slot], self.peers[slot], stream=stream)
-            dist.all_reduce(self.token, group=self.group)
-        return self.bufs[slot] if self.rank == self.root else None
-
-    def close(self):
-        torch.cuda.synchronize(self.device)
-        self.peers = []
-        self.pboard = self.proot_sizes = None
-        _ipc_teardown(self.device, self.group)
-
-
-class FlagAssembler:
-    """S2 + S3 for contiguous shards with no collective on the data path
-    (delta_assemble_flags): rank 0 owns ``nbuf`` assembled-body buffers and one board per
-    buffer (sizes, step tags, completion flags), all shared by CUDA IPC; each step every
-    rank publishes its size and copies its body over NVLink once the lower ranks' sizes are
-    on the board, and the root waits for every rank's completion flag on its comm stream.
-    Rank 0's records are extracted in place at the head of its buffer."""
+class FusedAssembler:
+    """S2 + S3 fused into the emit (NEXT f2; PAPER.md:405-409 cut-through): the root owns
+    ``nbuf`` assembled-body buffers, mapped into every other rank with CUDA IPC once.  Per step
+    each rank runs the scan phase (its body size lands on the device), one NCCL all-gather of
+    the sizes on the same stream, then the emit phase: K4/K5 store this rank's records into its
+    local body (for its own apply) AND straight into the root's buffer at their global offset
+    (delta_extract_emit_async with a peer destination) — no separate copy kernel.  Rank 0 emits
+    directly into the root buffer (its records head the body).  ``token()`` enqueues the
+    completion all-reduce on a comm stream: the root's readers wait for it."""
 
     def __init__(self, ctx, capacity: int, device, group=None, root: int = 0, nbuf: int = 2):
         assert root == 0, "the assembled body starts with rank 0's records"
         self.ctx, self.group, self.root = ctx, group, root
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.device = torch.device(device)
-        if self.rank == root:
-            self.bufs = [torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
-            self.board = torch.zeros(nbuf, self.world, 4, dtype=torch.int64, device=self.device)
-            torch.cuda.synchronize(self.device)
-            share = [reduce_tensor(b) for b in self.bufs] + [reduce_tensor(self.board)]
-        else:
-            self.bufs, share = [None] * nbuf, None
+        self.bufs = ([torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
+                     if self.rank == root else [None] * nbuf)
         handles = [None] * self.world
-        dist.all_gather_object(handles, share, group=group)
-        if self.rank == root:
-            self.peers, self.pboard = list(self.bufs), self.board
-        else:
-            mapped = []
+        dist.all_gather_object(handles, [reduce_tensor(b) for b in self.bufs] if self.rank == root else None,
+                               group=group)
+        self.peers = []
+        if self.rank != root:
             for fn, args in handles[root]:
                 args = list(args)
                 args[6] = self.device.index  # rebuild on this process's device (peer mapping)
-                mapped.append(fn(*args))
-            self.peers, self.pboard = mapped[:-1], mapped[-1]
-        self.buf = self.bufs[0]
-        self.tag = 0
+                self.peers.append(fn(*args))
+        self.sizes = [torch.zeros(self.world, dtype=torch.int64, device=self.device) for _ in range(nbuf)]
+        self.token_t = torch.zeros(1, dtype=torch.float32, device=self.device)
 
-    def assemble(self, body: torch.Tensor, size, slot: int = 0, stream=None):
-        """Enqueue on ``stream``: publish + copy (+ on the root: wait for every rank).
-        ``size``: one-element int64 CUDA tensor with this rank's body size."""
-        self.tag += 1
+    def extract(self, tensors, out, size, slot: int = 0, stream=None):
+        """Scan, size all-gather, fused emit, all on ``stream`` (default: current).  ``out``:
+        this rank's local body buffer (ignored on the root, whose body is the root buffer);
+        ``size``: one-element int64 CUDA tensor.  Returns (body buffer, DeviceTable)."""
         stream = stream or torch.cuda.current_stream(self.device)
-        board = self.pboard[slot]
-        self.ctx.assemble_flags(body, size, self.peers[slot], board, self.world, self.rank, self.tag, stream=stream)
+        self.ctx.delta_extract_scan_async(tensors, size, stream=stream)
+        with torch.cuda.stream(stream):
+            dist.all_gather_into_tensor(self.sizes[slot], size, group=self.group)
         if self.rank == self.root:
-            self.ctx.assemble_flags_wait(board, self.world, self.tag, stream=stream)
-        return self.bufs[slot] if self.rank == self.root else None
+            dst = self.bufs[slot]
+            table = self.ctx.delta_extract_emit_async(dst, size, stream=stream)
+        else:
+            dst = out
+            table = self.ctx.delta_extract_emit_async(out, size, peer=self.peers[slot], sizes=self.sizes[slot],
+                                                      rank=self.rank, stream=stream)
+        return dst, table
+
+    def token(self, stream):
+        """The completion token: one all-reduce on ``stream`` after the emit (the caller makes
+        ``stream`` wait for the emit first).  The root's body is complete once it returns."""
+        with torch.cuda.stream(stream):
+            dist.all_reduce(self.token_t, group=self.group)
 
     def close(self):
         torch.cuda.synchronize(self.device)
-        self.peers, self.pboard = [], None
+        self.peers = []
         _ipc_teardown(self.device, self.group)
-

@@ -1,8 +1,10 @@
 """Multi-GPU check (run under torchrun on >= 2 GPUs): every rank extracts its contiguous
 shard of a small Qwen-shaped tensor set, sizes are all-gathered over NCCL, the bodies are
-assembled on rank 0 and compared byte-for-byte with (a) the single-GPU body of the whole
-list and (b) the CPU oracle; every rank then applies its own records and checks the
-round trip.  Exit code 0 iff all checks pass on all ranks."""
+assembled on rank 0 — NCCL P2P, the delta_assemble copy kernel over NVLink, and the fused
+emit (K4/K5 storing each rank's records at their global offsets in rank 0's buffer) — and
+compared byte-for-byte with (a) the single-GPU body of the whole list and (b) the CPU oracle;
+every rank then applies its own records and checks the round trip.  Exit code 0 iff all
+checks pass on all ranks."""
 import os
 import sys
 
@@ -58,74 +60,51 @@ def main():
         ok2 = torch.equal(got2[:tot].cpu(), full_body.cpu())
         print(f"[rank0] NVLink delta_assemble: match = {ok2}", flush=True)
         ok &= ok2
-    # flag-based assembly (no collective): three steps over two buffers
-    fasm = sdist.FlagAssembler(ctx, tot + 4096, dev, nbuf=2)
+    # the fused emit + assembly: scan, size all-gather, emit into the local body AND straight
+    # into rank 0's buffer at the global offset (three steps over two root buffers)
+    fu = sdist.FusedAssembler(ctx, tot + 4096, dev, nbuf=2)
+    comm = torch.cuda.Stream(dev)
+    local = torch.empty(max(body.numel(), 1) + 4096, dtype=torch.uint8, device=dev)
+    size = torch.zeros(1, dtype=torch.int64, device=dev)
     for step in range(3):
         slot = step % 2
-        if rank == 0 and mine:
-            bf, _ = ctx.delta_extract(mine, out=fasm.bufs[slot])
-        elif mine:
-            bf, _ = ctx.delta_extract(mine)
-        else:
-            bf = torch.empty(0, dtype=torch.uint8, device=dev)
-        sz = torch.tensor([bf.numel()], dtype=torch.int64, device=dev)
-        got4 = fasm.assemble(bf, sz, slot=slot)
+        if rank == 0:
+            fu.bufs[slot].fill_(0xEE)
+        dist.barrier()
+        buf, dtab = fu.extract(mine, local, size, slot=slot)
+        comm.wait_stream(torch.cuda.current_stream())
+        fu.token(comm)
+        torch.cuda.current_stream().wait_stream(comm)
         torch.cuda.synchronize()
-        rc4 = 0
+        rc6 = 0
         try:
-            ctx.assemble_wait()
-        except Exception:
-            rc4 = 1
+            n6 = ctx.extract_wait()
+        except Exception as e:  # noqa: BLE001
+            print(f"[rank{rank}] fused extract_wait: {e}", flush=True)
+            rc6, n6 = 1, -1
+        ok &= rc6 == 0 and n6 == body.numel() and torch.equal(buf[:n6], body[:n6])
         if rank == 0:
-            ok4 = rc4 == 0 and torch.equal(got4[:tot].cpu(), full_body.cpu())
-            print(f"[rank0] flag assembly step {step} slot {slot}: match = {ok4}", flush=True)
-            ok &= ok4
-        ok &= rc4 == 0
-    fasm.close()
-    # LPT partition + record-granular assembly (delta_record_sizes / delta_assemble_records)
-    lpt = sdist.shard_lpt([s.numel for s in specs], world)[rank]
-    mine_l = [(specs[k].name, pairs[k][0], pairs[k][1]) for k in lpt]
-    rasm = sdist.RecordAssembler(ctx, tot + 4096, dev, lpt, len(specs))
-    for slot in (0, 1):
-        if mine_l:
-            bl, _ = ctx.delta_extract(mine_l, table="device")
-        else:
-            bl = torch.empty(0, dtype=torch.uint8, device=dev)
-            rasm.sizes[slot].zero_()
-        if mine_l:
-            rasm.record_sizes(ctx.table_dev_ptr(), slot=slot)
-        got3 = rasm.assemble(bl, slot=slot)
-        torch.cuda.synchronize()
-        ctx.assemble_wait()
-        if rank == 0:
-            ok3 = torch.equal(got3[:tot].cpu(), full_body.cpu())
-            print(f"[rank0] LPT {[len(p) for p in sdist.shard_lpt([s.numel for s in specs], world)]} "
-                  f"record assembly slot {slot}: match = {ok3}", flush=True)
-            ok &= ok3
-    rasm.close()
-    # LPT + record assembly through the root's board (no collective)
-    rfa = sdist.RecordAssembler(ctx, tot + 4096, dev, lpt, len(specs), mode="flags")
-    for step in range(3):
-        slot = step % 2
-        if mine_l:
-            bl, _ = ctx.delta_extract(mine_l, table="device")
-            rfa.record_sizes(ctx.table_dev_ptr(), slot=slot)
-        else:
-            bl = torch.empty(0, dtype=torch.uint8, device=dev)
-            rfa.sizes[slot].zero_()
-        got5 = rfa.assemble(bl, slot=slot)
-        torch.cuda.synchronize()
-        rc5 = 0
-        try:
-            ctx.assemble_wait()
-        except Exception:
-            rc5 = 1
-        if rank == 0:
-            ok5 = rc5 == 0 and torch.equal(got5[:tot].cpu(), full_body.cpu())
-            print(f"[rank0] LPT record flags assembly step {step} slot {slot}: match = {ok5}", flush=True)
-            ok &= ok5
-        ok &= rc5 == 0
-    rfa.close()
+            ok6 = rc6 == 0 and torch.equal(fu.bufs[slot][:tot].cpu(), full_body.cpu())
+            print(f"[rank0] fused emit + NVLink assembly step {step} slot {slot}: match = {ok6}", flush=True)
+            ok &= ok6
+    fu.close()
+    # a destination too small for the last rank: the peer copy is skipped and reported
+    fu2 = sdist.FusedAssembler(ctx, max(tot - 1, 1), dev, nbuf=1)
+    if rank == 0:
+        fu2.bufs[0].fill_(0x11)
+    dist.barrier()
+    fu2.extract(mine, local, size, slot=0)
+    fu2.token(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    failed = False
+    try:
+        ctx.extract_wait()
+    except Exception:  # noqa: BLE001
+        failed = True
+    if rank == world - 1:
+        ok &= failed or not mine  # the last rank's records end past tot - 1
+        print(f"[rank{rank}] fused assembly into a short buffer reported: {failed}", flush=True)
+    fu2.close()
     if mine:
         targets = [(n, o.clone()) for n, o, _ in mine]
         ctx.delta_apply(targets, body, table=table)
