@@ -349,6 +349,20 @@ int delta_assemble_wait(delta_ctx *ctx, void *stream);
  * `stream` once. */
 int delta_digest(delta_ctx *ctx, const void *body_dev, uint64_t bytes, uint8_t *out32, void *stream);
 
+/* delta_container_header — the SPDC container header written on the device (NEXT f1;
+ * PAPER.md:368-370 "versioned, immutable ... integrity hash"):
+ *     "SPDC" | u16 format_version | u64 version | u64 base_version | u8 element code
+ *     (0 = 16-bit lanes, 1 = 32-bit) | u32 n_tensors | u64 body length | BLAKE3-256(body)
+ * = 67 bytes, little-endian, to out_dev (device, any alignment; e.g. the 67 bytes ahead of the
+ * body in one buffer, so the container never passes through host memory).  The digest covers
+ * exactly the body bytes (reading R10); format_version = index_codec: 1 LEB128, 2 fixed-width
+ * (reading R18).  Asynchronous on `stream` (no host synchronisation).
+ * Errors: DELTA_EINVAL (NULL pointers, elem, index_codec not 1/2, version != base_version + 1),
+ * DELTA_ECUDA, DELTA_ENOMEM. */
+int delta_container_header(delta_ctx *ctx, const void *body_dev, uint64_t body_bytes, uint64_t version,
+                           uint64_t base_version, int elem, uint32_t n_tensors, int index_codec, void *out_dev,
+                           void *stream);
+
 /* ---------------------------------------------------------------------------------------
  * delta_merge — NEXT f4 (reading R19): two consecutive bodies D_a (version v-1 ->
  * v) and D_b (v -> v+1) over the same n tensors become ONE body (v-1 -> v+1) that a laggard

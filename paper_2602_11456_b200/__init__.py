@@ -10,4 +10,4 @@ multi-GPU orchestration (``dist``); see DESIGN.md.
 
 from .binding import (DeltaContext, DeltaError, DeviceTable, Table, TargetList, TensorList, TABLE_FIELDS, rebase,  # noqa: F401
                       compute_rho, context, delta_apply, delta_extract, delta_size, version)
-from .container import pack_container, unpack_container  # noqa: F401
+from .container import pack_container, pack_container_device, unpack_container  # noqa: F401

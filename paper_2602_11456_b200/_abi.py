@@ -31,7 +31,8 @@ EXPORTS = ("delta_ctx_create", "delta_ctx_destroy", "delta_last_error", "delta_l
            "delta_digest", "delta_extract_async", "delta_extract_wait", "delta_apply_async_chain",
            "delta_merge", "delta_timing_totals", "delta_record_sizes", "delta_assemble_records",
            "delta_size_table", "delta_compute_rho", "delta_table_rebase",
-           "delta_extract_scan_async", "delta_extract_emit_async")
+           "delta_extract_scan_async", "delta_extract_emit_async",
+           "delta_container_header")
 DELTA_OPT_APPLY_CTAS_PER_SM, DELTA_OPT_EMIT_CTAS_PER_SM, DELTA_OPT_SCAN_KERNEL = 1, 2, 3
 DELTA_OPT_SCATTER_CTAS_PER_SM, DELTA_OPT_PREFETCH_TILES, DELTA_OPT_SCATTER_ORDER, DELTA_OPT_MODE = 4, 5, 6, 7
 DELTA_OPT_INDEX_CODEC = 8  # 1 LEB128 gaps (default), 2 fixed-width absolute indices (reading R18)
@@ -99,6 +100,9 @@ def lib():
         L.delta_extract_emit_async.argtypes = [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_uint64, c_void_p,
                                                c_uint32, c_uint32, c_void_p]
         L.delta_extract_emit_async.restype = c_int
+        L.delta_container_header.argtypes = [c_void_p, c_void_p, c_uint64, c_uint64, c_uint64, c_int, c_uint32, c_int,
+                                             c_void_p, c_void_p]
+        L.delta_container_header.restype = c_int
         L.delta_extract.argtypes = [c_void_p, POINTER(Tensor), c_uint32, c_int, c_void_p, c_uint64,
                                     POINTER(RecordInfo), c_void_p, POINTER(c_uint64)]
         L.delta_extract.restype = c_int

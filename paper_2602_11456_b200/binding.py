@@ -462,6 +462,16 @@ class DeltaContext:
         self._check(call(out, out.numel()))
         return out[:nbytes.value]
 
+    def container_header(self, body, version: int, base_version: int, width: int, n_tensors: int, out,
+                         index_codec: str = "leb128", stream=None):
+        """delta_container_header: the 67-byte SPDC header of ``body`` (uint8 CUDA tensor),
+        digest included, written on the device into ``out`` (uint8 CUDA tensor, first 67
+        bytes)."""
+        self._check(self._lib.delta_container_header(
+            self._h, c_void_p(body.data_ptr() if body.numel() else 0), body.numel(), version, base_version,
+            _ELEM[width], n_tensors, {"leb128": 1, "fixed": 2}[index_codec], c_void_p(out.data_ptr()),
+            _stream_handle(stream)))
+
     def assemble_wait(self, stream=None):
         self._check(self._lib.delta_assemble_wait(self._h, _stream_handle(stream)))
 

@@ -1119,6 +1119,33 @@ extern "C" int delta_digest(delta_ctx *ctx, const void *body, uint64_t bytes, ui
     return DELTA_OK;
 }
 
+// SPDC container header on the device (NEXT f1): the BLAKE3-256 of exactly
+// the body (reading R10) and the 67 header bytes, written to out_dev — e.g. the 67 bytes just
+// ahead of the body in one buffer, so a container never passes through host memory.
+extern "C" int delta_container_header(delta_ctx *ctx, const void *body_dev, uint64_t body_bytes, uint64_t version,
+                                      uint64_t base_version, int elem, uint32_t n_tensors, int index_codec,
+                                      void *out_dev, void *stream) {
+    if (!ctx) return DELTA_EINVAL;
+    ctx->err.clear();
+    ctx->detail = 0;
+    const int w = elem_width(elem);
+    if (!w) return fail(ctx, DELTA_EINVAL, 0, "unknown elem %d", elem);
+    if (!out_dev || (body_bytes && !body_dev)) return fail(ctx, DELTA_EINVAL, 0, "delta_container_header: NULL pointer");
+    if (index_codec != 1 && index_codec != 2) return fail(ctx, DELTA_EINVAL, 0, "index_codec must be 1 or 2");
+    if (version != base_version + 1) return fail(ctx, DELTA_EINVAL, 0, "version must be base_version + 1 (SPEC.md:46)");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned long long nch = body_bytes == 0 ? 1 : (body_bytes + 1023) / 1024;
+    GROW(ctx->dg_ws, (size_t)(2 * nch * 32 + 64));
+    uint32_t *ws = ctx->dg_ws.as<uint32_t>();
+    uint32_t *dout = ws + 2 * nch * 8;
+    CK(launch_blake3(static_cast<const uint8_t *>(body_dev), body_bytes, ws, dout, s), "digest launch");
+    CK(launch_spdc_header(static_cast<uint8_t *>(out_dev), dout, (uint32_t)index_codec, version, base_version,
+                          w == 2 ? 0u : 1u, n_tensors, body_bytes, s),
+       "header launch");
+    return DELTA_OK;
+}
+
 // --------------------------------------------------------------------------- merge
 // DELTA_MERGE_TIMING=1: host wall time of each delta_merge phase (each ends in a stream
 // synchronisation) printed to stderr — diagnostics for scripts/merge_bench.py.

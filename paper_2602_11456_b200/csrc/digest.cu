@@ -142,4 +142,34 @@ cudaError_t launch_blake3(const uint8_t *in, unsigned long long n, uint32_t *ws,
     return cudaMemcpyAsync(out32, a, 32, cudaMemcpyDeviceToDevice, s);
 }
 
+// SPDC header (readings R9, R10, R18), written on the device from the digest the
+// tree above left in `digest` (device, 32 bytes): "SPDC" | u16 format_version | u64 version |
+// u64 base_version | u8 element code | u32 tensor count | u64 body length | 32-byte BLAKE3.
+// 67 bytes, little-endian, to `out` (any alignment).
+__global__ void k_spdc_header(uint8_t *out, const uint32_t *digest, uint32_t format_version,
+                              unsigned long long version, unsigned long long base_version, uint32_t elem_code,
+                              uint32_t n_tensors, unsigned long long body_bytes) {
+    const int i = threadIdx.x;
+    if (i >= 67) return;
+    uint8_t b;
+    auto le = [](unsigned long long x, int k) { return (uint8_t)(x >> (8 * k)); };
+    if (i < 4) b = (uint8_t)"SPDC"[i];
+    else if (i < 6) b = le(format_version, i - 4);
+    else if (i < 14) b = le(version, i - 6);
+    else if (i < 22) b = le(base_version, i - 14);
+    else if (i < 23) b = (uint8_t)elem_code;
+    else if (i < 27) b = le(n_tensors, i - 23);
+    else if (i < 35) b = le(body_bytes, i - 27);
+    else b = (uint8_t)(digest[(i - 35) >> 2] >> (8 * ((i - 35) & 3)));
+    out[i] = b;
+}
+
+cudaError_t launch_spdc_header(uint8_t *out, const uint32_t *digest, uint32_t format_version,
+                               unsigned long long version, unsigned long long base_version, uint32_t elem_code,
+                               uint32_t n_tensors, unsigned long long body_bytes, cudaStream_t s) {
+    k_spdc_header<<<1, 96, 0, s>>>(out, digest, format_version, version, base_version, elem_code, n_tensors,
+                                   body_bytes);
+    return cudaGetLastError();
+}
+
 }  // namespace sd

@@ -200,6 +200,9 @@ struct ApplyArgs {
     int index_codec;                  // 0 LEB128 gaps, 1 fixed-width absolute indices (R18)
 };
 
+cudaError_t launch_spdc_header(uint8_t *out, const uint32_t *digest, uint32_t format_version,
+                               unsigned long long version, unsigned long long base_version, uint32_t elem_code,
+                               uint32_t n_tensors, unsigned long long body_bytes, cudaStream_t s);
 cudaError_t launch_blake3(const uint8_t *in, unsigned long long n, uint32_t *ws, uint32_t *out32, cudaStream_t s);
 
 cudaError_t launch_record_sizes(const RecordRow *table, uint32_t n_local, const uint32_t *gidx,

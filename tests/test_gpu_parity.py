@@ -504,6 +504,19 @@ def test_gpu_digest_and_container(sd):
     blob = sd.pack_container(body, 9, 8, 2, 1, ctx=ctx)
     ref = oracle.container.pack(body.cpu().numpy().tobytes(), 9, 8, 2, 1)
     assert blob == ref
+    # the container built on the device: the extract writes straight into it, the header
+    # (digest included) is written by the library's kernel — no host copy of the body
+    cont = torch.empty(sd.container.HEADER_BYTES + body.numel(), dtype=torch.uint8, device=DEV)
+    b2, _ = ctx.delta_extract([(spec.name, o, w)], out=cont[sd.container.HEADER_BYTES:], table=False)
+    dev_blob = sd.pack_container_device(b2, 9, 8, 2, 1, ctx=ctx, out=cont)
+    assert dev_blob.data_ptr() == cont.data_ptr()
+    assert dev_blob.cpu().numpy().tobytes() == ref
+    # fixed-width codec: format_version 2 in the header
+    ref_f = oracle.container.pack(body.cpu().numpy().tobytes(), 9, 8, 2, 1, index_codec="fixed")
+    dev_f = sd.pack_container_device(body, 9, 8, 2, 1, ctx=ctx, index_codec="fixed")
+    assert dev_f.cpu().numpy().tobytes() == ref_f
+    with pytest.raises(sd.DeltaError):
+        ctx.container_header(body, 9, 7, 2, 1, cont)  # version != base_version + 1
     ctx.close()
 
 
