@@ -32,6 +32,14 @@ __device__ __forceinline__ void set_status(ApplyState *st, uint32_t code) {
 
 __device__ __forceinline__ unsigned long long rd_le(const uint8_t *p, int nbytes) {
     unsigned long long x = 0;
+    if (nbytes == 8) {  // all eight loads in flight at once
+        uint8_t b[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) b[i] = p[i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x |= (unsigned long long)b[i] << (8 * i);
+        return x;
+    }
     for (int b = 0; b < nbytes; ++b) x |= (unsigned long long)p[b] << (8 * b);
     return x;
 }
@@ -58,8 +66,13 @@ __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_by
     const uint8_t mode = body[end - 1];
     if (mode > 1) return kMode;  // 0 replace, 1 additive
     if (nl != tg.name_len) return kName;
-    uint32_t diff = 0;  // no early exit: the byte loads are independent
-    for (unsigned long long b = 0; b < nl; ++b) diff |= body[ro + 2 + b] ^ names[tg.name_off + b];
+    uint32_t diff = 0;  // no early exit: the byte loads are independent (4 in flight per step)
+    unsigned long long b = 0;
+    for (; b + 4 <= nl; b += 4) {
+        const uint8_t *x = body + ro + 2 + b, *y = names + tg.name_off + b;
+        diff |= (x[0] ^ y[0]) | (x[1] ^ y[1]) | (x[2] ^ y[2]) | (x[3] ^ y[3]);
+    }
+    for (; b < nl; ++b) diff |= body[ro + 2 + b] ^ names[tg.name_off + b];
     if (diff) return kName;
     if (N != tg.numel) return kNumel;
     if (fixed) {  // reading R18: a whole number of fixed-width indices, one per entry

@@ -406,7 +406,7 @@ cudaError_t launch_slots_regrow(const TileMeta *meta, uint32_t ntiles, int width
 }
 
 // ------------------------------------------------------------------------------ K2 / K3
-// The tile-level prefixes in two launches over blocks of kTileBlock tiles (1024 threads x 4
+// The tile-level prefixes in two launches over blocks of kTileBlock tiles (256 threads x 4
 // tiles): K2a reduces each block (entries, LEB128 bytes but the block's first non-empty
 // tile's first gap, first / last non-empty tile); K2b — every CTA re-scans the (few hundred)
 // block aggregates itself, so no single-CTA scan launch sits between them — places every
@@ -441,11 +441,12 @@ __device__ __forceinline__ unsigned long long tile_bytes(const TileDesc &d, cons
     return m.internal_bytes + leb_len(g0);
 }
 
-// Block-wide (1024 threads) exclusive scans: sum of x, max of key (identity -1).
+// Block-wide (kTileThreads threads) exclusive scans: sum of x, max of key (identity -1).
 __device__ __forceinline__ void block_scan_sum_max(unsigned long long x, long long key, unsigned long long &xex,
                                                    unsigned long long &xtot, long long &kex, long long &ktot) {
-    __shared__ unsigned long long s_x[32];
-    __shared__ long long s_k[32];
+    constexpr int NW = kTileThreads / 32;
+    __shared__ unsigned long long s_x[NW];
+    __shared__ long long s_k[NW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned long long xi = warp_inclusive_sum(x);
     const long long ki = warp_inclusive_max(key);
@@ -456,8 +457,8 @@ __device__ __forceinline__ void block_scan_sum_max(unsigned long long x, long lo
     __syncthreads();
     unsigned long long px = 0, tx = 0;
     long long pk = -1, tk = -1;
-#pragma unroll 8
-    for (int w = 0; w < 32; ++w) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
         const unsigned long long a = s_x[w];
         const long long b = s_k[w];
         if (w < warp) {
@@ -476,7 +477,7 @@ __device__ __forceinline__ void block_scan_sum_max(unsigned long long x, long lo
     ktot = tk;
 }
 
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kTileThreads)
 k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
             BlockAgg *__restrict__ agg, const unsigned long long *__restrict__ numel, int fixed,
             const ExtractSummary *summary) {
@@ -509,8 +510,8 @@ k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ met
     }
     const unsigned long long bs = warp_sum(b);
     const long long kf = -warp_max(kfirst < 0 ? -(long long)0x7FFFFFFFFFFFFFFF : -kfirst);
-    __shared__ unsigned long long s_b[32];
-    __shared__ long long s_f[32];
+    __shared__ unsigned long long s_b[kTileThreads / 32];
+    __shared__ long long s_f[kTileThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) {
         s_b[warp] = bs;
@@ -520,7 +521,7 @@ k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ met
     if (threadIdx.x == 0) {
         unsigned long long tb = 0;
         long long f = 0x7FFFFFFFFFFFFFFF;
-        for (int w = 0; w < 32; ++w) {
+        for (int w = 0; w < kTileThreads / 32; ++w) {
             tb += s_b[w];
             f = s_f[w] < f ? s_f[w] : f;
         }
@@ -528,7 +529,7 @@ k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ met
     }
 }
 
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kTileThreads)
 k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
                uint32_t nblk, const BlockAgg *__restrict__ agg, TileEmit *__restrict__ plan,
                unsigned long long *__restrict__ E, unsigned long long *__restrict__ Bk, uint32_t T,
@@ -547,7 +548,7 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
     {
         unsigned long long ecarry = 0, bcarry = 0;
         long long pcarry = -1;
-        for (uint32_t j0 = 0; j0 < nblk; j0 += 1024) {
+        for (uint32_t j0 = 0; j0 < nblk; j0 += kTileThreads) {
             const uint32_t j = j0 + threadIdx.x;
             BlockAgg a = j < nblk ? agg[j] : BlockAgg{0, 0, -1, -1};
             unsigned long long cex, ctot;
@@ -628,7 +629,7 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
     if (!s_last) return;
     __threadfence();
     unsigned long long carry = 0;
-    for (uint32_t b = 0; b < T; b += 1024) {
+    for (uint32_t b = 0; b < T; b += kTileThreads) {
         const uint32_t k = b + threadIdx.x;
         unsigned long long rb = 0, nnz = 0, ilen = 0, ek = 0, bk = 0;
         if (k < T) {
@@ -741,24 +742,25 @@ __device__ __forceinline__ EmitGate emit_gate(const ExtractSummary *summary, uns
 // funnel-shifted source words (8 per lane), plus the < 4 head and < 4 tail bytes.  Reads at
 // most 4 bytes past the source range (slots are padded).
 struct CopyBatch {
-    uint32_t w[9];    // source words lane + 32 i (the word after each comes from the next lane)
-    uint32_t hb, tb;  // this lane's head / tail byte
+    uint32_t w[9];    // source words lane + 32 i, i.e. words 0 .. n / 4 (each word's successor
+                      // comes from the next lane)
+    uint32_t hb, tb;  // lanes 0-2: the source's first / last three bytes
 };
-__device__ __forceinline__ void copy_load(CopyBatch &c, uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
-    const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
-    const uint32_t nw = (n - head) >> 2;
+// The loads do not depend on the destination, so one batch can be stored to several
+// destinations of any alignment (the fused assembly stores it locally and into the peer).
+__device__ __forceinline__ void copy_load(CopyBatch &c, const uint8_t *src, uint32_t n, int lane) {
     const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-    const uint32_t rounds = (nw + 32) >> 5;  // words 0 .. nw (word nw: the last word's successor)
+    const uint32_t last = n >> 2;  // words 0 .. last cover every destination word + successor
+    const uint32_t rounds = (last + 32) >> 5;
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
         const uint32_t j = lane + 32 * i;
         c.w[i] = 0u;
         if ((uint32_t)i >= rounds) continue;  // warp-uniform: only the rounds the copy needs
-        if (j <= nw) c.w[i] = __ldg(s32 + j);
+        if (j <= last) c.w[i] = __ldg(s32 + j);
     }
-    const uint32_t tail0 = head + 4 * nw;
-    c.hb = (uint32_t)lane < head ? src[lane] : 0u;
-    c.tb = (uint32_t)lane < n - tail0 ? src[tail0 + lane] : 0u;
+    c.hb = (lane < 3 && (uint32_t)lane < n) ? src[lane] : 0u;
+    c.tb = (lane < 3 && n + lane >= 3) ? src[n + lane - 3] : 0u;
 }
 __device__ __forceinline__ void copy_store(const CopyBatch &c, uint8_t *dst, uint32_t n, int lane) {
     const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
@@ -775,9 +777,12 @@ __device__ __forceinline__ void copy_store(const CopyBatch &c, uint8_t *dst, uin
         const uint32_t nxt = lane == 31 ? wrap : up;
         if (j < nw) d32[j] = sh ? __funnelshift_r(c.w[i], nxt, sh) : c.w[i];
     }
-    const uint32_t tail0 = head + 4 * nw;
-    if ((uint32_t)lane < head) dst[lane] = (uint8_t)c.hb;
-    if ((uint32_t)lane < n - tail0) dst[tail0 + lane] = (uint8_t)c.tb;
+    // head bytes 0 .. head-1 and tail bytes n - ntail .. n-1 (< 4 each) from lanes 0-2
+    const uint32_t ntail = n - head - 4 * nw;
+    const uint32_t hbyte = __shfl_sync(0xffffffffu, c.hb, lane & 3);
+    const uint32_t tbyte = __shfl_sync(0xffffffffu, c.tb, (3 - ntail + lane) & 31);
+    if ((uint32_t)lane < head) dst[lane] = (uint8_t)hbyte;
+    if ((uint32_t)lane < ntail) dst[n - ntail + lane] = (uint8_t)tbyte;
 }
 
 // One warp per tile.  LEB128 codec: K1 left the tile's in-tile gaps already encoded in its
@@ -840,8 +845,8 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
         const uint32_t ni = pe.count_internal >> 16, nv = count * W;
         if (ni <= 1024 && nv <= 1024) {  // ~every tile up to a few % density: one round trip
             CopyBatch ci, cv;
-            copy_load(ci, ib + L0, sb, ni, lane);
-            copy_load(cv, vb, sv, nv, lane);
+            copy_load(ci, sb, ni, lane);
+            copy_load(cv, sv, nv, lane);
             copy_store(ci, ib + L0, ni, lane);
             copy_store(cv, vb, nv, lane);
             if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
@@ -921,9 +926,9 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     if (nblk) {
-        k_tiles_agg<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, a.agg, a.numel, a.index_codec, a.summary);
+        k_tiles_agg<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, a.agg, a.numel, a.index_codec, a.summary);
         if (ev) cudaEventRecord(ev[2], s);
-        k_tiles_prefix<<<nblk, 1024, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.plan, a.entry_begin,
+        k_tiles_prefix<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.plan, a.entry_begin,
                                              a.tensor_byte_begin, a.ntensors, a.name_len, a.numel, a.table, a.bases,
                                              a.width, a.index_codec, a.summary, a.scan_size_out);
     } else if (ev) {

@@ -70,6 +70,7 @@ def main():
         slot = step % 2
         if rank == 0:
             fu.bufs[slot].fill_(0xEE)
+            torch.cuda.synchronize()
         dist.barrier()
         buf, dtab = fu.extract(mine, local, size, slot=slot)
         comm.wait_stream(torch.cuda.current_stream())
@@ -92,6 +93,7 @@ def main():
     fu2 = sdist.FusedAssembler(ctx, max(tot - 1, 1), dev, nbuf=1)
     if rank == 0:
         fu2.bufs[0].fill_(0x11)
+        torch.cuda.synchronize()
     dist.barrier()
     fu2.extract(mine, local, size, slot=0)
     fu2.token(torch.cuda.current_stream())

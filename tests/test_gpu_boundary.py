@@ -187,3 +187,48 @@ def test_async_extract_sticky_overflow(sd):
         ctx.extract_wait()
     assert e.value.status == _abi.DELTA_ECAPACITY
     ctx.close()
+
+
+@pytest.mark.parametrize("prefix", [0, 1, 2, 3, 5, 4096 + 7])
+def test_fused_emit_peer_destination(sd, prefix):
+    """delta_extract_scan_async + delta_extract_emit_async with a peer destination (here a
+    local buffer standing in for the root's IPC mapping): the body lands in out AND at
+    sum(sizes[:rank]) of the peer buffer, for every alignment of that offset; the bytes
+    around it are untouched; a ~0 size of another rank or a short peer buffer skips the peer
+    copy (local body still written) and is reported by extract_wait."""
+    from paper_2602_11456_b200 import _abi
+    tensors = _tensors([300_001, 17, 0, 65_536 * 3 + 5], seed=prefix + 40, rho=0.02)
+    want, _ = oracle_extract(tensors)
+    ctx = sd.DeltaContext(DEV)
+    out = torch.empty(len(want) + 64, dtype=torch.uint8, device=DEV)
+    size = torch.zeros(1, dtype=torch.int64, device=DEV)
+    peer = torch.full((prefix + len(want) + 99,), 0x5A, dtype=torch.uint8, device=DEV)
+    ctx.delta_extract_scan_async(tensors, size)
+    torch.cuda.synchronize()
+    assert int(size.item()) == len(want)
+    sizes = torch.tensor([prefix, len(want), 12345], dtype=torch.int64, device=DEV)
+    ctx.delta_extract_emit_async(out, size, peer=peer, sizes=sizes, rank=1)
+    assert ctx.extract_wait() == len(want)
+    assert_body_equal(out[:len(want)], want)
+    assert_body_equal(peer[prefix:prefix + len(want)], want)
+    assert bool((peer[:prefix] == 0x5A).all()) and bool((peer[prefix + len(want):] == 0x5A).all())
+    # another rank's extract did not complete (~0 size): no peer copy, EAGAIN at the wait
+    peer.fill_(0x5A)
+    bad = sizes.clone()
+    bad[2] = -1
+    ctx.delta_extract_scan_async(tensors, size)
+    ctx.delta_extract_emit_async(out, size, peer=peer, sizes=bad, rank=1)
+    with pytest.raises(sd.DeltaError) as e:
+        ctx.extract_wait()
+    assert e.value.status == _abi.DELTA_EAGAIN
+    assert bool((peer == 0x5A).all())
+    assert_body_equal(out[:len(want)], want)
+    # the peer buffer one byte short: no peer copy, ECAPACITY
+    short = peer[:prefix + len(want) - 1]
+    ctx.delta_extract_scan_async(tensors, size)
+    ctx.delta_extract_emit_async(out, size, peer=short, sizes=sizes, rank=1)
+    with pytest.raises(sd.DeltaError) as e:
+        ctx.extract_wait()
+    assert e.value.status == _abi.DELTA_ECAPACITY
+    assert bool((peer == 0x5A).all())
+    ctx.close()
