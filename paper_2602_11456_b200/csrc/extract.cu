@@ -408,10 +408,10 @@ cudaError_t launch_slots_regrow(const TileMeta *meta, uint32_t ntiles, int width
 // ------------------------------------------------------------------------------ K2 / K3
 // The tile-level prefixes in two launches over blocks of kTileBlock tiles (256 threads x 4
 // tiles): K2a reduces each block (entries, LEB128 bytes but the block's first non-empty
-// tile's first gap, first / last non-empty tile); K2b — every CTA re-scans the (few hundred)
-// block aggregates itself, so no single-CTA scan launch sits between them — places every
-// tile (entry and byte prefix, first gap) into K4's plan, records each tensor's E_k / B_k at
-// its first tile, and the last CTA to finish (ticket after a fence) writes the offset table
+// tile's first gap, first / last non-empty tile) and its last CTA to finish (ticket after a
+// fence) scans the block aggregates into block prefixes — no single-CTA scan launch sits
+// between the two; K2b places every tile (entry and byte prefix, first gap) into K4's plan,
+// records each tensor's E_k / B_k at its first tile, and its last CTA writes the offset table
 // (K3: record sizes and offsets, PAPER.md:382 + SPEC.md:148) and the per-tensor emit bases.
 
 // Absolute lane index (within its fused tensor) of the last change of non-empty tile p, if p
@@ -478,9 +478,9 @@ __device__ __forceinline__ void block_scan_sum_max(unsigned long long x, long lo
 }
 
 __global__ void __launch_bounds__(kTileThreads)
-k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
+k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t nblk,
             BlockAgg *__restrict__ agg, const unsigned long long *__restrict__ numel, int fixed,
-            const ExtractSummary *summary) {
+            ExtractSummary *summary) {
     if (summary->overflow) return;
     const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
     TileMeta mt[4];
@@ -525,8 +525,51 @@ k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ met
             tb += s_b[w];
             f = s_f[w] < f ? s_f[w] : f;
         }
-        agg[blockIdx.x] = BlockAgg{ctot, tb, f == 0x7FFFFFFFFFFFFFFF ? -1 : f, ktot};
+        agg[blockIdx.x] = BlockAgg{ctot, tb, f == 0x7FFFFFFFFFFFFFFF ? -1 : f, ktot, 0, 0, -1, 0};
     }
+    // ---- the last CTA to finish (ticket after a fence) scans the block aggregates once:
+    // every block's entry / byte prefix and the last non-empty tile before it (the first gap
+    // of the block's first non-empty tile needs that tile)
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&summary->blocks_done, 1ull) == nblk - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    unsigned long long ecarry = 0, bcarry = 0;
+    long long pcarry = -1;
+    for (uint32_t j0 = 0; j0 < nblk; j0 += kTileThreads) {
+        const uint32_t j = j0 + threadIdx.x;
+        BlockAgg a{0, 0, -1, -1, 0, 0, -1, 0};
+        if (j < nblk) {
+            a.cnt = __ldcg(&agg[j].cnt);
+            a.bytes = __ldcg(&agg[j].bytes);
+            a.first = __ldcg(&agg[j].first);
+            a.last = __ldcg(&agg[j].last);
+        }
+        unsigned long long cex2, ctot2;
+        long long pex, ptot;
+        block_scan_sum_max(a.cnt, a.last, cex2, ctot2, pex, ptot);
+        if (pcarry > pex) pex = pcarry;
+        unsigned long long fb = 0, g0;  // the first gap of the block's first non-empty tile
+        if (a.first >= 0 && !fixed) {
+            const TileMeta m = meta[a.first];
+            fb = tile_bytes(tiles[a.first], m, tiles, meta, pex, numel, 0, g0) - m.internal_bytes;
+        }
+        unsigned long long bex, btot;
+        long long d0, d1;
+        block_scan_sum_max(a.bytes + fb, -1, bex, btot, d0, d1);
+        if (j < nblk) {
+            agg[j].e0 = ecarry + cex2;
+            agg[j].b0 = bcarry + bex;
+            agg[j].p0 = pex;
+        }
+        ecarry += ctot2;
+        bcarry += btot;
+        if (ptot > pcarry) pcarry = ptot;
+    }
+    if (threadIdx.x == 0) summary->blocks_done = 0;  // K2b's tickets start from zero
 }
 
 __global__ void __launch_bounds__(kTileThreads)
@@ -543,35 +586,11 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
     __shared__ unsigned long long s_e0, s_b0;
     __shared__ long long s_p0;
     __shared__ bool s_last;
-    // ---- this block's entry / byte prefix and the last non-empty tile before it, from the
-    // block aggregates (scanned by every CTA; nblk is a few hundred)
-    {
-        unsigned long long ecarry = 0, bcarry = 0;
-        long long pcarry = -1;
-        for (uint32_t j0 = 0; j0 < nblk; j0 += kTileThreads) {
-            const uint32_t j = j0 + threadIdx.x;
-            BlockAgg a = j < nblk ? agg[j] : BlockAgg{0, 0, -1, -1};
-            unsigned long long cex, ctot;
-            long long pex, ptot;
-            block_scan_sum_max(a.cnt, a.last, cex, ctot, pex, ptot);
-            if (pcarry > pex) pex = pcarry;
-            unsigned long long fb = 0, g0;  // the first gap of the block's first non-empty tile
-            if (a.first >= 0 && !fixed) {
-                const TileMeta m = meta[a.first];
-                fb = tile_bytes(tiles[a.first], m, tiles, meta, pex, numel, 0, g0) - m.internal_bytes;
-            }
-            unsigned long long bex, btot;
-            long long d0, d1;
-            block_scan_sum_max(a.bytes + fb, -1, bex, btot, d0, d1);
-            if (j == blockIdx.x) {
-                s_e0 = ecarry + cex;
-                s_b0 = bcarry + bex;
-                s_p0 = pex;
-            }
-            ecarry += ctot;
-            bcarry += btot;
-            if (ptot > pcarry) pcarry = ptot;
-        }
+    // ---- this block's entry / byte prefix and the last non-empty tile before it (K2a's last CTA)
+    if (threadIdx.x == 0) {
+        s_e0 = agg[blockIdx.x].e0;
+        s_b0 = agg[blockIdx.x].b0;
+        s_p0 = agg[blockIdx.x].p0;
     }
     __syncthreads();
     // ---- the block's tiles
@@ -926,7 +945,8 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     if (nblk) {
-        k_tiles_agg<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, a.agg, a.numel, a.index_codec, a.summary);
+        k_tiles_agg<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.numel, a.index_codec,
+                                                  a.summary);
         if (ev) cudaEventRecord(ev[2], s);
         k_tiles_prefix<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.plan, a.entry_begin,
                                              a.tensor_byte_begin, a.ntensors, a.name_len, a.numel, a.table, a.bases,

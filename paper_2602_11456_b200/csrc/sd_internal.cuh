@@ -55,6 +55,11 @@ struct BlockAgg {
     unsigned long long cnt;    // entries in the block
     unsigned long long bytes;  // LEB128 bytes, except the first gap of the block's first non-empty tile
     long long first, last;     // first / last non-empty tile of the block, -1 if none
+    // written by K2a's last CTA: entries / LEB128 bytes before the block, last non-empty tile
+    // before it (-1: none)
+    unsigned long long e0, b0;
+    long long p0;
+    unsigned long long pad;
 };
 
 // Per tensor (written with the offset table): body offset of a tile's first index byte =
