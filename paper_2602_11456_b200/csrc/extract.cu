@@ -760,19 +760,21 @@ __device__ __forceinline__ EmitGate emit_gate(const ExtractSummary *summary, uns
 // load issued before any store (one memory round trip): destination words assembled from
 // funnel-shifted source words (8 per lane), plus the < 4 head and < 4 tail bytes.  Reads at
 // most 4 bytes past the source range (slots are padded).
+template <int NWL>
 struct CopyBatch {
-    uint32_t w[9];    // source words lane + 32 i, i.e. words 0 .. n / 4 (each word's successor
-                      // comes from the next lane)
-    uint32_t hb, tb;  // lanes 0-2: the source's first / last three bytes
+    uint32_t w[NWL + 1];  // source words lane + 32 i, i.e. words 0 .. n / 4 (each word's
+                          // successor comes from the next lane): up to 128 NWL - 4 bytes
+    uint32_t hb, tb;      // lanes 0-2: the source's first / last three bytes
 };
 // The loads do not depend on the destination, so one batch can be stored to several
 // destinations of any alignment (the fused assembly stores it locally and into the peer).
-__device__ __forceinline__ void copy_load(CopyBatch &c, const uint8_t *src, uint32_t n, int lane) {
+template <int NWL>
+__device__ __forceinline__ void copy_load(CopyBatch<NWL> &c, const uint8_t *src, uint32_t n, int lane) {
     const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
     const uint32_t last = n >> 2;  // words 0 .. last cover every destination word + successor
     const uint32_t rounds = (last + 32) >> 5;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
+    for (int i = 0; i <= NWL; ++i) {
         const uint32_t j = lane + 32 * i;
         c.w[i] = 0u;
         if ((uint32_t)i >= rounds) continue;  // warp-uniform: only the rounds the copy needs
@@ -781,14 +783,15 @@ __device__ __forceinline__ void copy_load(CopyBatch &c, const uint8_t *src, uint
     c.hb = (lane < 3 && (uint32_t)lane < n) ? src[lane] : 0u;
     c.tb = (lane < 3 && n + lane >= 3) ? src[n + lane - 3] : 0u;
 }
-__device__ __forceinline__ void copy_store(const CopyBatch &c, uint8_t *dst, uint32_t n, int lane) {
+template <int NWL>
+__device__ __forceinline__ void copy_store(const CopyBatch<NWL> &c, uint8_t *dst, uint32_t n, int lane) {
     const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
     const uint32_t nw = (n - head) >> 2;
     const uint32_t sh = 8u * head;
     uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + head);
     const uint32_t rounds = (nw + 31) >> 5;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < NWL; ++i) {
         if ((uint32_t)i >= rounds) break;  // warp-uniform
         const uint32_t j = lane + 32 * i;
         const uint32_t up = __shfl_down_sync(0xffffffffu, c.w[i], 1);
@@ -809,7 +812,7 @@ __device__ __forceinline__ void copy_store(const CopyBatch &c, uint8_t *dst, uin
 // bytes and the raw values to their final offsets — two warp-wide copies, no per-entry work.
 // FIXED (reading R18): absolute indices lane_base + offset as u32 / u64, via shared memory.
 template <int W, bool FIXED>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, 3)
 k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
@@ -819,21 +822,18 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
     const int lane = threadIdx.x & 31;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    __shared__ __align__(16) unsigned long long s_fix[FIXED ? 8 * 256 + 2 : 1];
-    TileEmit pnext = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
-    for (uint32_t t = wg; t < ntiles; t += nw) {
-        const TileEmit pe = pnext;  // this tile's plan, loaded one iteration ahead
-        if (t + nw < ntiles) pnext = plan[t + nw];
-        const uint32_t count = pe.count_internal & 0xFFFFu;
-        if (count == 0) continue;
-        const TensorBase tb = bases[pe.k];
-        uint8_t *ib = out + (tb.ib + pe.ib);
-        uint8_t *vb = out + (tb.vb + pe.eb * W);
-        const uint8_t *sv = reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap);
-        const uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
-        if constexpr (FIXED) {
+    if constexpr (FIXED) {
+        __shared__ __align__(16) unsigned long long s_fix[8 * 256 + 2];
+        for (uint32_t t = wg; t < ntiles; t += nw) {
+            const TileEmit pe = plan[t];
+            const uint32_t count = pe.count_internal & 0xFFFFu;
+            if (count == 0) continue;
+            const TensorBase tb = bases[pe.k];
+            uint8_t *ib = out + (tb.ib + pe.ib);
+            uint8_t *vb = out + (tb.vb + pe.eb * W);
+            const uint8_t *sv = reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap);
             const uint32_t iw = pe.count_internal >> 16;  // the index width (set by K2b for FIXED)
-            const uint16_t *so = reinterpret_cast<const uint16_t *>(sb);
+            const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
             unsigned long long *buf = s_fix + 256 * (threadIdx.x >> 5);
             uint8_t *dst = ib, *pdst = pout ? pout + (ib - out) : nullptr;
             for (uint32_t b = 0; b < count; b += 256) {
@@ -854,36 +854,73 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
             }
             warp_copy(vb, sv, count * W, lane);
             if (pout) warp_copy(pout + (vb - out), sv, count * W, lane);
-            continue;
         }
-        // the first gap: byte n = 7-bit group n, continuation bit on all but the last
-        const unsigned long long g = pe.g0;
-        const uint32_t L0 = leb_len(g);
-        const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
-        if ((uint32_t)lane < L0) ib[lane] = g_byte;
-        const uint32_t ni = pe.count_internal >> 16, nv = count * W;
-        if (ni <= 1024 && nv <= 1024) {  // ~every tile up to a few % density: one round trip
-            CopyBatch ci, cv;
-            copy_load(ci, sb, ni, lane);
-            copy_load(cv, sv, nv, lane);
-            copy_store(ci, ib + L0, ni, lane);
-            copy_store(cv, vb, nv, lane);
-            if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
-                uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
-                if ((uint32_t)lane < L0) pi[lane] = g_byte;
-                copy_store(ci, pi + L0, ni, lane);
-                copy_store(cv, pv, nv, lane);
+        return;
+    }
+    // LEB128: software pipeline over the warp's tiles — plans loaded two tiles ahead, a tile's
+    // slot bytes one tile ahead (into registers), so the stores of tile t overlap the loads of
+    // the next; tiles with more than kPipe bytes in either copy take a synchronous path.
+    constexpr int NWL = 3;  // 380 bytes: the in-tile bytes and values of a tile up to ~190 changes
+    constexpr uint32_t kPipe = 128 * NWL - 4;
+    auto slot_i = [&](uint32_t t) { return slot_bytes + (size_t)t * 2 * slot_cap; };
+    auto slot_v = [&](uint32_t t) { return reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap); };
+    auto small = [&](const TileEmit &p) {
+        return (p.count_internal >> 16) <= kPipe && (p.count_internal & 0xFFFFu) * W <= kPipe;
+    };
+    TileEmit p1 = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
+    TileEmit p2 = wg + nw < ntiles ? plan[wg + nw] : TileEmit{0, 0, 0, 0, 0};
+    CopyBatch<NWL> ci, cv;
+    bool pre = false;
+    if (wg < ntiles && (p1.count_internal & 0xFFFFu) && small(p1)) {
+        copy_load(ci, slot_i(wg), p1.count_internal >> 16, lane);
+        copy_load(cv, slot_v(wg), (p1.count_internal & 0xFFFFu) * W, lane);
+        pre = true;
+    }
+    for (uint32_t t = wg; t < ntiles; t += nw) {
+        const TileEmit pe = p1;
+        p1 = p2;
+        if (t + 2 * nw < ntiles) p2 = plan[t + 2 * nw];
+        CopyBatch<NWL> ci2, cv2;  // the next tile's bytes, in flight while this one is stored
+        bool pre2 = false;
+        if (t + nw < ntiles && (p1.count_internal & 0xFFFFu) && small(p1)) {
+            copy_load(ci2, slot_i(t + nw), p1.count_internal >> 16, lane);
+            copy_load(cv2, slot_v(t + nw), (p1.count_internal & 0xFFFFu) * W, lane);
+            pre2 = true;
+        }
+        const uint32_t count = pe.count_internal & 0xFFFFu;
+        if (count) {
+            const TensorBase tb = bases[pe.k];
+            uint8_t *ib = out + (tb.ib + pe.ib);
+            uint8_t *vb = out + (tb.vb + pe.eb * W);
+            // the first gap: byte n = 7-bit group n, continuation bit on all but the last
+            const unsigned long long g = pe.g0;
+            const uint32_t L0 = leb_len(g);
+            const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
+            const uint32_t ni = pe.count_internal >> 16, nv = count * W;
+            uint8_t *pi = pout ? pout + (ib - out) : nullptr, *pv = pout ? pout + (vb - out) : nullptr;
+            if ((uint32_t)lane < L0) {
+                ib[lane] = g_byte;
+                if (pi) pi[lane] = g_byte;
             }
-        } else {
-            warp_copy(ib + L0, sb, ni, lane);
-            warp_copy(vb, sv, nv, lane);
-            if (pout) {
-                uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
-                if ((uint32_t)lane < L0) pi[lane] = g_byte;
-                warp_copy(pi + L0, sb, ni, lane);
-                warp_copy(pv, sv, nv, lane);
+            if (pre) {
+                copy_store(ci, ib + L0, ni, lane);
+                copy_store(cv, vb, nv, lane);
+                if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
+                    copy_store(ci, pi + L0, ni, lane);
+                    copy_store(cv, pv, nv, lane);
+                }
+            } else {  // a dense tile: synchronous copies
+                warp_copy(ib + L0, slot_i(t), ni, lane);
+                warp_copy(vb, slot_v(t), nv, lane);
+                if (pout) {
+                    warp_copy(pi + L0, slot_i(t), ni, lane);
+                    warp_copy(pv, slot_v(t), nv, lane);
+                }
             }
         }
+        ci = ci2;
+        cv = cv2;
+        pre = pre2;
     }
 }
 
