@@ -13,7 +13,8 @@
 #   sections   ncu SpeedOfLight/Memory/Occupancy/WarpState/Scheduler sections, K4 / A2 / A4 / K1
 #   full       ncu --set full of the top kernels on a 40-tensor prefix of M3
 #   sanitizer  compute-sanitizer memcheck / racecheck / synccheck / initcheck over the
-#              small parity tests (M1 and the edge sets; apply, merge, assembly included)
+#              small parity tests — NOTE: closed on this GPU pool (runs left GPUs needing a
+#              reset); tests/test_gpu_guard.py (guard bands + fuzz) stands in for memcheck
 #   probe      scripts/scatter_probe.py (+ DRAM counters)
 #   scale      bench.py --gpus 2 / 4 (as many GPUs as the box has) + dist_check
 TAG=${1:?tag}; shift
