@@ -731,6 +731,32 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
     for (uint32_t b = (nv << 4) + lane; b < rest; b += 32) dst[head + b] = src[head + b];
 }
 
+// Warp-wide copy of n bytes from a 16-byte aligned source to any destination with 16-byte
+// stores: the < 16 head bytes (up to the destination's alignment) by lanes 0-15 and the < 16
+// tail bytes by lanes 16-31, one byte store each; every aligned destination vector j is source
+// bytes [head + 16 j, +16), i.e. 20 bytes of two aligned source vectors funnel-shifted by the
+// (warp-uniform) misalignment.  Reads at most 16 bytes past the source range (slots are padded).
+__device__ __forceinline__ void warp_copy16(uint8_t *dst, const uint8_t *src, uint32_t n, int lane) {
+    const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
+    const uint32_t rest = n - head, nv = rest >> 4, tail = rest & 15u;
+    if ((uint32_t)lane < head) dst[lane] = src[lane];
+    const uint32_t tb = head + 16u * nv + (uint32_t)(lane - 16);
+    if (lane >= 16 && (uint32_t)(lane - 16) < tail) dst[tb] = src[tb];
+    uint4 *d16 = reinterpret_cast<uint4 *>(dst + head);
+    const uint4 *s16 = reinterpret_cast<const uint4 *>(src);
+    const uint32_t qv = head >> 2, sh = 8u * (head & 3u);  // word offset into the vector pair, bit shift
+    for (uint32_t j = lane; j < nv; j += 32) {
+        const uint4 a = __ldg(s16 + j), b = __ldg(s16 + j + 1);
+        uint32_t w0, w1, w2, w3, w4;  // source words qv .. qv + 4 of the pair (a, b)
+        if (qv == 0) { w0 = a.x; w1 = a.y; w2 = a.z; w3 = a.w; w4 = b.x; }
+        else if (qv == 1) { w0 = a.y; w1 = a.z; w2 = a.w; w3 = b.x; w4 = b.y; }
+        else if (qv == 2) { w0 = a.z; w1 = a.w; w2 = b.x; w3 = b.y; w4 = b.z; }
+        else { w0 = a.w; w1 = b.x; w2 = b.y; w3 = b.z; w4 = b.w; }
+        d16[j] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                            __funnelshift_r(w3, w4, sh));
+    }
+}
+
 // The emit gate (K4/K5): the local body is written iff every tile fitted its slot and the body
 // fits `cap`; the fused-assembly copy (peer.base) iff, in addition, no rank's size is ~0 (its
 // extract did not complete) and this rank's records fit the peer buffer at sum(sizes[q < rank]).
@@ -756,63 +782,12 @@ __device__ __forceinline__ EmitGate emit_gate(const ExtractSummary *summary, uns
     return g;
 }
 
-// Up to 1 KiB of a 4-byte aligned source copied by a warp to any destination, with every
-// load issued before any store (one memory round trip): destination words assembled from
-// funnel-shifted source words (8 per lane), plus the < 4 head and < 4 tail bytes.  Reads at
-// most 4 bytes past the source range (slots are padded).
-template <int NWL>
-struct CopyBatch {
-    uint32_t w[NWL + 1];  // source words lane + 32 i, i.e. words 0 .. n / 4 (each word's
-                          // successor comes from the next lane): up to 128 NWL - 4 bytes
-    uint32_t hb, tb;      // lanes 0-2: the source's first / last three bytes
-};
-// The loads do not depend on the destination, so one batch can be stored to several
-// destinations of any alignment (the fused assembly stores it locally and into the peer).
-template <int NWL>
-__device__ __forceinline__ void copy_load(CopyBatch<NWL> &c, const uint8_t *src, uint32_t n, int lane) {
-    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-    const uint32_t last = n >> 2;  // words 0 .. last cover every destination word + successor
-    const uint32_t rounds = (last + 32) >> 5;
-#pragma unroll
-    for (int i = 0; i <= NWL; ++i) {
-        const uint32_t j = lane + 32 * i;
-        c.w[i] = 0u;
-        if ((uint32_t)i >= rounds) continue;  // warp-uniform: only the rounds the copy needs
-        if (j <= last) c.w[i] = __ldg(s32 + j);
-    }
-    c.hb = (lane < 3 && (uint32_t)lane < n) ? src[lane] : 0u;
-    c.tb = (lane < 3 && n + lane >= 3) ? src[n + lane - 3] : 0u;
-}
-template <int NWL>
-__device__ __forceinline__ void copy_store(const CopyBatch<NWL> &c, uint8_t *dst, uint32_t n, int lane) {
-    const uint32_t head = min(n, (uint32_t)((4u - ((uintptr_t)dst & 3u)) & 3u));
-    const uint32_t nw = (n - head) >> 2;
-    const uint32_t sh = 8u * head;
-    uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + head);
-    const uint32_t rounds = (nw + 31) >> 5;
-#pragma unroll
-    for (int i = 0; i < NWL; ++i) {
-        if ((uint32_t)i >= rounds) break;  // warp-uniform
-        const uint32_t j = lane + 32 * i;
-        const uint32_t up = __shfl_down_sync(0xffffffffu, c.w[i], 1);
-        const uint32_t wrap = __shfl_sync(0xffffffffu, c.w[i + 1], 0);
-        const uint32_t nxt = lane == 31 ? wrap : up;
-        if (j < nw) d32[j] = sh ? __funnelshift_r(c.w[i], nxt, sh) : c.w[i];
-    }
-    // head bytes 0 .. head-1 and tail bytes n - ntail .. n-1 (< 4 each) from lanes 0-2
-    const uint32_t ntail = n - head - 4 * nw;
-    const uint32_t hbyte = __shfl_sync(0xffffffffu, c.hb, lane & 3);
-    const uint32_t tbyte = __shfl_sync(0xffffffffu, c.tb, (3 - ntail + lane) & 31);
-    if ((uint32_t)lane < head) dst[lane] = (uint8_t)hbyte;
-    if ((uint32_t)lane < ntail) dst[n - ntail + lane] = (uint8_t)tbyte;
-}
-
 // One warp per tile.  LEB128 codec: K1 left the tile's in-tile gaps already encoded in its
 // slot, so the warp writes the first gap's bytes (one lane per byte), then copies the in-tile
 // bytes and the raw values to their final offsets — two warp-wide copies, no per-entry work.
 // FIXED (reading R18): absolute indices lane_base + offset as u32 / u64, via shared memory.
 template <int W, bool FIXED>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 5)
 k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
@@ -857,70 +832,33 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
         }
         return;
     }
-    // LEB128: software pipeline over the warp's tiles — plans loaded two tiles ahead, a tile's
-    // slot bytes one tile ahead (into registers), so the stores of tile t overlap the loads of
-    // the next; tiles with more than kPipe bytes in either copy take a synchronous path.
-    constexpr int NWL = 3;  // 380 bytes: the in-tile bytes and values of a tile up to ~190 changes
-    constexpr uint32_t kPipe = 128 * NWL - 4;
-    auto slot_i = [&](uint32_t t) { return slot_bytes + (size_t)t * 2 * slot_cap; };
-    auto slot_v = [&](uint32_t t) { return reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap); };
-    auto small = [&](const TileEmit &p) {
-        return (p.count_internal >> 16) <= kPipe && (p.count_internal & 0xFFFFu) * W <= kPipe;
-    };
-    TileEmit p1 = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
-    TileEmit p2 = wg + nw < ntiles ? plan[wg + nw] : TileEmit{0, 0, 0, 0, 0};
-    CopyBatch<NWL> ci, cv;
-    bool pre = false;
-    if (wg < ntiles && (p1.count_internal & 0xFFFFu) && small(p1)) {
-        copy_load(ci, slot_i(wg), p1.count_internal >> 16, lane);
-        copy_load(cv, slot_v(wg), (p1.count_internal & 0xFFFFu) * W, lane);
-        pre = true;
-    }
+    // LEB128: per tile the first-gap bytes (one lane per byte) and two warp-wide 16-byte copies
+    // (in-tile bytes, values); the next tile's plan is loaded one tile ahead.
+    TileEmit pnext = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
     for (uint32_t t = wg; t < ntiles; t += nw) {
-        const TileEmit pe = p1;
-        p1 = p2;
-        if (t + 2 * nw < ntiles) p2 = plan[t + 2 * nw];
-        CopyBatch<NWL> ci2, cv2;  // the next tile's bytes, in flight while this one is stored
-        bool pre2 = false;
-        if (t + nw < ntiles && (p1.count_internal & 0xFFFFu) && small(p1)) {
-            copy_load(ci2, slot_i(t + nw), p1.count_internal >> 16, lane);
-            copy_load(cv2, slot_v(t + nw), (p1.count_internal & 0xFFFFu) * W, lane);
-            pre2 = true;
-        }
+        const TileEmit pe = pnext;
+        if (t + nw < ntiles) pnext = plan[t + nw];
         const uint32_t count = pe.count_internal & 0xFFFFu;
-        if (count) {
-            const TensorBase tb = bases[pe.k];
-            uint8_t *ib = out + (tb.ib + pe.ib);
-            uint8_t *vb = out + (tb.vb + pe.eb * W);
-            // the first gap: byte n = 7-bit group n, continuation bit on all but the last
-            const unsigned long long g = pe.g0;
-            const uint32_t L0 = leb_len(g);
-            const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
-            const uint32_t ni = pe.count_internal >> 16, nv = count * W;
-            uint8_t *pi = pout ? pout + (ib - out) : nullptr, *pv = pout ? pout + (vb - out) : nullptr;
-            if ((uint32_t)lane < L0) {
-                ib[lane] = g_byte;
-                if (pi) pi[lane] = g_byte;
-            }
-            if (pre) {
-                copy_store(ci, ib + L0, ni, lane);
-                copy_store(cv, vb, nv, lane);
-                if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
-                    copy_store(ci, pi + L0, ni, lane);
-                    copy_store(cv, pv, nv, lane);
-                }
-            } else {  // a dense tile: synchronous copies
-                warp_copy(ib + L0, slot_i(t), ni, lane);
-                warp_copy(vb, slot_v(t), nv, lane);
-                if (pout) {
-                    warp_copy(pi + L0, slot_i(t), ni, lane);
-                    warp_copy(pv, slot_v(t), nv, lane);
-                }
-            }
+        if (count == 0) continue;
+        const TensorBase tb = bases[pe.k];
+        uint8_t *ib = out + (tb.ib + pe.ib);
+        uint8_t *vb = out + (tb.vb + pe.eb * W);
+        const uint8_t *si = slot_bytes + (size_t)t * 2 * slot_cap;
+        const uint8_t *sv = reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap);
+        // the first gap: byte n = 7-bit group n, continuation bit on all but the last
+        const unsigned long long g = pe.g0;
+        const uint32_t L0 = leb_len(g);
+        const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
+        const uint32_t ni = pe.count_internal >> 16, nv = count * W;
+        if ((uint32_t)lane < L0) ib[lane] = g_byte;
+        warp_copy16(ib + L0, si, ni, lane);
+        warp_copy16(vb, sv, nv, lane);
+        if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
+            uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
+            if ((uint32_t)lane < L0) pi[lane] = g_byte;
+            warp_copy16(pi + L0, si, ni, lane);
+            warp_copy16(pv, sv, nv, lane);
         }
-        ci = ci2;
-        cv = cv2;
-        pre = pre2;
     }
 }
 
