@@ -405,8 +405,8 @@ typedef struct {
 
 /* Launch-shape options (performance only; results never depend on them). */
 enum {
-    DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode kernel, CTAs per SM (default 4: its register limit) */
-    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 5: its register limit) */
+    DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode kernel, CTAs per SM (default 8) */
+    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 3: its register limit) */
     DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
                                         vectors, bitmap compaction (the only form; the retired
                                         variants 2-5 — TMA pipeline, 128-byte runs, 512 x 4,

@@ -376,73 +376,50 @@ __device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cn
 }
 
 // ------------------------------------------------------------------------------ A2
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256)
 k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
                const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
                unsigned int *__restrict__ chunk_count,
                unsigned long long *__restrict__ chunk_sum, ApplyState *st) {
-    // KG consecutive chunks per iteration: each thread validates one 16-byte window in each
-    // (independent work in flight), and the staging / reduction barriers are paid once per
-    // group instead of once per chunk.  Outputs stay per chunk (A3 / A4 unchanged).
-    constexpr int KG = 4;
     if (st->status != kOk) return;
     const unsigned long long nch = st->n_chunks;
-    __shared__ __align__(16) uint8_t sb[KG][kStageBytes];
-    __shared__ uint32_t s_cnt[KG][8];
-    __shared__ unsigned long long s_sum[KG][8];
+    __shared__ __align__(16) uint8_t sb[kStageBytes];
+    __shared__ uint32_t s_cnt[8];
+    __shared__ unsigned long long s_sum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned long long ngr = (nch + KG - 1) / KG;
-    for (unsigned long long gi = blockIdx.x; gi < ngr; gi += gridDim.x) {
-        ChunkView v[KG];
+    for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        const uint32_t k = __ldg(chunk_rec + c);
+        const ApplyRec R = recs[k];
+        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb + kStagePad);
+        __syncthreads();
+        uint32_t cnt = 0, err = kOk;
+        unsigned long long sum = 0;
+        validate_thread(v, cnt, sum, err);
+        const int pl = (int)v.len - 1;  // the stream's last byte must end a varint
+        if (v.last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (v.b[pl] & 0x80))
+            err = err ? err : kTruncated;
+        if (err != kOk) set_status(st, err);
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (__all_sync(0xffffffffu, sum < (1ull << 26))) {  // 32 lanes x 2^26 < 2^32: no overflow
+            sum = __reduce_add_sync(0xffffffffu, (uint32_t)sum);
+        } else {  // saturating (a malformed stream can decode to gaps up to 2^64 - 1)
 #pragma unroll
-        for (int g = 0; g < KG; ++g) {
-            const unsigned long long c = gi * KG + g;
-            if (c < nch) {
-                const uint32_t k = __ldg(chunk_rec + c);
-                v[g] = stage_chunk(body, recs[k], c - __ldg(rcb + k), sb[g] + kStagePad);
-            } else {
-                v[g].len = 0;
-                v[g].last = false;
-                v[g].cs = 0;
-                v[g].b = sb[g] + kStagePad;
-            }
+            for (int o = 16; o > 0; o >>= 1) sum = sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        }
+        if (lane == 0) {
+            s_cnt[warp] = cnt;
+            s_sum[warp] = sum;
         }
         __syncthreads();
-#pragma unroll
-        for (int g = 0; g < KG; ++g) {
-            uint32_t cnt = 0, err = kOk;
-            unsigned long long sum = 0;
-            validate_thread(v[g], cnt, sum, err);
-            const int pl = (int)v[g].len - 1;  // the stream's last byte must end a varint
-            if (v[g].last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (v[g].b[pl] & 0x80))
-                err = err ? err : kTruncated;
-            if (err != kOk) set_status(st, err);
-            cnt = __reduce_add_sync(0xffffffffu, cnt);
-            if (__all_sync(0xffffffffu, sum < (1ull << 26))) {  // 32 lanes x 2^26 < 2^32: no overflow
-                sum = __reduce_add_sync(0xffffffffu, (uint32_t)sum);
-            } else {  // saturating (a malformed stream can decode to gaps up to 2^64 - 1)
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sum = sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        if (threadIdx.x == 0) {
+            uint32_t tc = 0;
+            unsigned long long ts = 0;
+            for (int w = 0; w < 8; ++w) {
+                tc += s_cnt[w];
+                ts = sat_add(ts, s_sum[w]);
             }
-            if (lane == 0) {
-                s_cnt[g][warp] = cnt;
-                s_sum[g][warp] = sum;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < KG) {
-            const int g = threadIdx.x;
-            const unsigned long long c = gi * KG + g;
-            if (c < nch) {
-                uint32_t tc = 0;
-                unsigned long long ts = 0;
-                for (int w = 0; w < 8; ++w) {
-                    tc += s_cnt[g][w];
-                    ts = sat_add(ts, s_sum[g][w]);
-                }
-                chunk_count[c] = tc;
-                chunk_sum[c] = ts;
-            }
+            chunk_count[c] = tc;
+            chunk_sum[c] = ts;
         }
         __syncthreads();
     }

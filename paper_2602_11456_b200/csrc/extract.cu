@@ -757,6 +757,42 @@ __device__ __forceinline__ void warp_copy16(uint8_t *dst, const uint8_t *src, ui
     }
 }
 
+// The loads of one warp_copy16 of at most kPref bytes, taken before the destination is known
+// (so K4 can issue a tile's loads one tile ahead): lane j holds source vector j, lanes 0-15 the
+// first 16 source bytes, lanes 16-31 the last 16.  pref_store writes them to any destination.
+constexpr uint32_t kPref = 496;
+struct Pref16 {
+    uint4 a;         // source vector `lane` (vectors 0 .. n / 16)
+    uint32_t hb, tb; // lanes 0-15: src[lane]; lanes 16-31: src[n - 32 + lane]
+};
+__device__ __forceinline__ void pref_load(Pref16 &p, const uint8_t *src, uint32_t n, int lane) {
+    const uint4 *s16 = reinterpret_cast<const uint4 *>(src);
+    p.a = (uint32_t)lane <= (n >> 4) ? __ldg(s16 + lane) : make_uint4(0, 0, 0, 0);
+    p.hb = (lane < 16 && (uint32_t)lane < n) ? src[lane] : 0u;
+    p.tb = (lane >= 16 && n + lane >= 32) ? src[n + lane - 32] : 0u;
+}
+__device__ __forceinline__ void pref_store(const Pref16 &p, uint8_t *dst, uint32_t n, int lane) {
+    const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
+    const uint32_t rest = n - head, nv = rest >> 4, tail = rest & 15u;
+    // tail byte k (lane 16 + k) = src[n - tail + k], held by lane 32 - tail + k
+    const uint32_t tbyte = __shfl_sync(0xffffffffu, p.tb, (32u - tail + (uint32_t)lane - 16u) & 31u);
+    const uint4 b = make_uint4(__shfl_down_sync(0xffffffffu, p.a.x, 1), __shfl_down_sync(0xffffffffu, p.a.y, 1),
+                               __shfl_down_sync(0xffffffffu, p.a.z, 1), __shfl_down_sync(0xffffffffu, p.a.w, 1));
+    if ((uint32_t)lane < head) dst[lane] = (uint8_t)p.hb;
+    if (lane >= 16 && (uint32_t)(lane - 16) < tail) dst[head + 16u * nv + (uint32_t)(lane - 16)] = (uint8_t)tbyte;
+    if ((uint32_t)lane < nv) {
+        const uint32_t qv = head >> 2, sh = 8u * (head & 3u);
+        uint32_t w0, w1, w2, w3, w4;
+        if (qv == 0) { w0 = p.a.x; w1 = p.a.y; w2 = p.a.z; w3 = p.a.w; w4 = b.x; }
+        else if (qv == 1) { w0 = p.a.y; w1 = p.a.z; w2 = p.a.w; w3 = b.x; w4 = b.y; }
+        else if (qv == 2) { w0 = p.a.z; w1 = p.a.w; w2 = b.x; w3 = b.y; w4 = b.z; }
+        else { w0 = p.a.w; w1 = b.x; w2 = b.y; w3 = b.z; w4 = b.w; }
+        reinterpret_cast<uint4 *>(dst + head)[lane] =
+            make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                       __funnelshift_r(w3, w4, sh));
+    }
+}
+
 // The emit gate (K4/K5): the local body is written iff every tile fitted its slot and the body
 // fits `cap`; the fused-assembly copy (peer.base) iff, in addition, no rank's size is ~0 (its
 // extract did not complete) and this rank's records fit the peer buffer at sum(sizes[q < rank]).
@@ -787,7 +823,7 @@ __device__ __forceinline__ EmitGate emit_gate(const ExtractSummary *summary, uns
 // bytes and the raw values to their final offsets — two warp-wide copies, no per-entry work.
 // FIXED (reading R18): absolute indices lane_base + offset as u32 / u64, via shared memory.
 template <int W, bool FIXED>
-__global__ void __launch_bounds__(256, 5)
+__global__ void __launch_bounds__(256, 3)
 k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
@@ -833,32 +869,62 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
         return;
     }
     // LEB128: per tile the first-gap bytes (one lane per byte) and two warp-wide 16-byte copies
-    // (in-tile bytes, values); the next tile's plan is loaded one tile ahead.
-    TileEmit pnext = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
+    // (in-tile bytes, values).  Software pipeline over the warp's tiles: plans two tiles ahead,
+    // a tile's slot bytes one tile ahead (they do not depend on where they go), so the stores
+    // of tile t overlap the loads of the next; larger tiles take synchronous copies.
+    auto slot_i = [&](uint32_t t) { return slot_bytes + (size_t)t * 2 * slot_cap; };
+    auto slot_v = [&](uint32_t t) { return reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap); };
+    auto fast = [&](const TileEmit &p) {
+        return (p.count_internal >> 16) <= kPref && (p.count_internal & 0xFFFFu) * W <= kPref;
+    };
+    TileEmit p1 = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
+    TileEmit p2 = wg + nw < ntiles ? plan[wg + nw] : TileEmit{0, 0, 0, 0, 0};
+    Pref16 fi, fv;
+    if (wg < ntiles && fast(p1)) {
+        pref_load(fi, slot_i(wg), p1.count_internal >> 16, lane);
+        pref_load(fv, slot_v(wg), (p1.count_internal & 0xFFFFu) * W, lane);
+    }
     for (uint32_t t = wg; t < ntiles; t += nw) {
-        const TileEmit pe = pnext;
-        if (t + nw < ntiles) pnext = plan[t + nw];
-        const uint32_t count = pe.count_internal & 0xFFFFu;
-        if (count == 0) continue;
-        const TensorBase tb = bases[pe.k];
-        uint8_t *ib = out + (tb.ib + pe.ib);
-        uint8_t *vb = out + (tb.vb + pe.eb * W);
-        const uint8_t *si = slot_bytes + (size_t)t * 2 * slot_cap;
-        const uint8_t *sv = reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap);
-        // the first gap: byte n = 7-bit group n, continuation bit on all but the last
-        const unsigned long long g = pe.g0;
-        const uint32_t L0 = leb_len(g);
-        const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
-        const uint32_t ni = pe.count_internal >> 16, nv = count * W;
-        if ((uint32_t)lane < L0) ib[lane] = g_byte;
-        warp_copy16(ib + L0, si, ni, lane);
-        warp_copy16(vb, sv, nv, lane);
-        if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
-            uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
-            if ((uint32_t)lane < L0) pi[lane] = g_byte;
-            warp_copy16(pi + L0, si, ni, lane);
-            warp_copy16(pv, sv, nv, lane);
+        const TileEmit pe = p1;
+        p1 = p2;
+        if (t + 2 * nw < ntiles) p2 = plan[t + 2 * nw];
+        Pref16 ni_, nv_;  // the next tile's bytes, in flight while this tile is stored
+        if (t + nw < ntiles && fast(p1)) {
+            pref_load(ni_, slot_i(t + nw), p1.count_internal >> 16, lane);
+            pref_load(nv_, slot_v(t + nw), (p1.count_internal & 0xFFFFu) * W, lane);
         }
+        const uint32_t count = pe.count_internal & 0xFFFFu;
+        if (count) {
+            const TensorBase tb = bases[pe.k];
+            uint8_t *ib = out + (tb.ib + pe.ib);
+            uint8_t *vb = out + (tb.vb + pe.eb * W);
+            // the first gap: byte n = 7-bit group n, continuation bit on all but the last
+            const unsigned long long g = pe.g0;
+            const uint32_t L0 = leb_len(g);
+            const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
+            const uint32_t ni = pe.count_internal >> 16, nv = count * W;
+            if ((uint32_t)lane < L0) ib[lane] = g_byte;
+            if (fast(pe)) {
+                pref_store(fi, ib + L0, ni, lane);
+                pref_store(fv, vb, nv, lane);
+            } else {
+                warp_copy16(ib + L0, slot_i(t), ni, lane);
+                warp_copy16(vb, slot_v(t), nv, lane);
+            }
+            if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
+                uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
+                if ((uint32_t)lane < L0) pi[lane] = g_byte;
+                if (fast(pe)) {
+                    pref_store(fi, pi + L0, ni, lane);
+                    pref_store(fv, pv, nv, lane);
+                } else {
+                    warp_copy16(pi + L0, slot_i(t), ni, lane);
+                    warp_copy16(pv, slot_v(t), nv, lane);
+                }
+            }
+        }
+        fi = ni_;
+        fv = nv_;
     }
 }
 
