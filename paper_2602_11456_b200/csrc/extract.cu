@@ -877,54 +877,50 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
     auto fast = [&](const TileEmit &p) {
         return (p.count_internal >> 16) <= kPref && (p.count_internal & 0xFFFFu) * W <= kPref;
     };
-    TileEmit p1 = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
-    TileEmit p2 = wg + nw < ntiles ? plan[wg + nw] : TileEmit{0, 0, 0, 0, 0};
-    Pref16 fi, fv;
-    if (wg < ntiles && fast(p1)) {
-        pref_load(fi, slot_i(wg), p1.count_internal >> 16, lane);
-        pref_load(fv, slot_v(wg), (p1.count_internal & 0xFFFFu) * W, lane);
-    }
-    for (uint32_t t = wg; t < ntiles; t += nw) {
-        const TileEmit pe = p1;
-        p1 = p2;
-        if (t + 2 * nw < ntiles) p2 = plan[t + 2 * nw];
-        Pref16 ni_, nv_;  // the next tile's bytes, in flight while this tile is stored
-        if (t + nw < ntiles && fast(p1)) {
-            pref_load(ni_, slot_i(t + nw), p1.count_internal >> 16, lane);
-            pref_load(nv_, slot_v(t + nw), (p1.count_internal & 0xFFFFu) * W, lane);
+    // one pipeline step for tile t: issue the loads of tile t + nw (plan pn, into dn), store
+    // tile t (plan pc, data dc), then load the plan of tile t + 2 nw into pc.  Unrolled by two
+    // over fixed (A, B) slots so no registers rotate.
+    auto step = [&](uint32_t t, TileEmit &pc, const TileEmit &pn, Pref16 &ci, Pref16 &cv, Pref16 &ni_, Pref16 &nv_) {
+        if (t + nw < ntiles && fast(pn)) {
+            pref_load(ni_, slot_i(t + nw), pn.count_internal >> 16, lane);
+            pref_load(nv_, slot_v(t + nw), (pn.count_internal & 0xFFFFu) * W, lane);
         }
-        const uint32_t count = pe.count_internal & 0xFFFFu;
+        const uint32_t count = pc.count_internal & 0xFFFFu;
         if (count) {
-            const TensorBase tb = bases[pe.k];
-            uint8_t *ib = out + (tb.ib + pe.ib);
-            uint8_t *vb = out + (tb.vb + pe.eb * W);
+            const TensorBase tb = bases[pc.k];
+            uint8_t *ib = out + (tb.ib + pc.ib);
+            uint8_t *vb = out + (tb.vb + pc.eb * W);
             // the first gap: byte n = 7-bit group n, continuation bit on all but the last
-            const unsigned long long g = pe.g0;
+            const unsigned long long g = pc.g0;
             const uint32_t L0 = leb_len(g);
             const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
-            const uint32_t ni = pe.count_internal >> 16, nv = count * W;
-            if ((uint32_t)lane < L0) ib[lane] = g_byte;
-            if (fast(pe)) {
-                pref_store(fi, ib + L0, ni, lane);
-                pref_store(fv, vb, nv, lane);
-            } else {
-                warp_copy16(ib + L0, slot_i(t), ni, lane);
-                warp_copy16(vb, slot_v(t), nv, lane);
-            }
-            if (pout) {  // fused assembly: the same bytes at their global offsets (NVLink stores)
-                uint8_t *pi = pout + (ib - out), *pv = pout + (vb - out);
-                if ((uint32_t)lane < L0) pi[lane] = g_byte;
-                if (fast(pe)) {
-                    pref_store(fi, pi + L0, ni, lane);
-                    pref_store(fv, pv, nv, lane);
-                } else {
-                    warp_copy16(pi + L0, slot_i(t), ni, lane);
-                    warp_copy16(pv, slot_v(t), nv, lane);
+            const uint32_t ni = pc.count_internal >> 16, nv = count * W;
+            const bool f = fast(pc);
+            for (int d = 0; d < (pout ? 2 : 1); ++d) {  // d = 1: fused assembly, the same bytes at
+                uint8_t *di = d ? pout + (ib - out) : ib;   // their global offsets (NVLink stores)
+                uint8_t *dv = d ? pout + (vb - out) : vb;
+                if ((uint32_t)lane < L0) di[lane] = g_byte;
+                if (f) {
+                    pref_store(ci, di + L0, ni, lane);
+                    pref_store(cv, dv, nv, lane);
+                } else {  // a dense tile: synchronous copies
+                    warp_copy16(di + L0, slot_i(t), ni, lane);
+                    warp_copy16(dv, slot_v(t), nv, lane);
                 }
             }
         }
-        fi = ni_;
-        fv = nv_;
+        pc = t + 2 * nw < ntiles ? plan[t + 2 * nw] : TileEmit{0, 0, 0, 0, 0};
+    };
+    TileEmit pa = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
+    TileEmit pb = wg + nw < ntiles ? plan[wg + nw] : TileEmit{0, 0, 0, 0, 0};
+    Pref16 ai, av, bi, bv;
+    if (wg < ntiles && fast(pa)) {
+        pref_load(ai, slot_i(wg), pa.count_internal >> 16, lane);
+        pref_load(av, slot_v(wg), (pa.count_internal & 0xFFFFu) * W, lane);
+    }
+    for (uint32_t t = wg; t < ntiles; t += 2 * nw) {
+        step(t, pa, pb, ai, av, bi, bv);
+        if (t + nw < ntiles) step(t + nw, pb, pa, bi, bv, ai, av);
     }
 }
 
