@@ -102,7 +102,7 @@ struct delta_ctx {
     int ring_next = 0;
 
     // ---- launch options
-    int apply_ctas_per_sm = 8, emit_ctas_per_sm = 3, scatter_ctas_per_sm = 5, scan_kernel = 0;
+    int apply_ctas_per_sm = 32, emit_ctas_per_sm = 3, scatter_ctas_per_sm = 96, scan_kernel = 0;
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
     int assemble_ctas = 64;   // grid of the NVLink assembly kernels (peer stores; 64: measured best at N=4)
     bool entry_major = true;
