@@ -393,13 +393,13 @@ int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *body_a_dev, ui
  * most recent launch of that kernel; *_count fields say how many launches it covers. */
 typedef struct {
     float scan_ms;      /* K1 compare + ordered compaction (reads old and new) */
-    float lens_ms;      /* K2a tile-block aggregates + block prefixes */
-    float finalize_ms;  /* K2b tile placement + K3 offset table */
+    float lens_ms;      /* K2 gap LEB128 lengths */
+    float finalize_ms;  /* K3 offset table */
     float emit_ms;      /* K4 index bytes + values */
-    float headers_ms;   /* K5 record headers (0: written inside K4 since round 2) */
+    float headers_ms;   /* K5 record headers */
     float locate_ms;    /* A1 record headers located + verified */
     float decode_ms;    /* A2 LEB128 decode + validation */
-    float apply_scan_ms;/* A3 per-record scans + count/range checks (0: inside A2 since round 2) */
+    float apply_scan_ms;/* A3 per-record scans + count/range checks */
     float scatter_ms;   /* A4 gated scatter-store */
 } delta_timing;
 
@@ -441,7 +441,7 @@ enum {
                                          not strictly increasing -> DELTA_D_NONINCREASING, an index
                                          >= element_count -> DELTA_D_RANGE (all-or-nothing as ever). */
     DELTA_OPT_ASSEMBLE_CTAS = 10,     /* grid (CTAs, total) of delta_assemble / delta_assemble_records
-                                         (default 32): fewer CTAs take fewer SM slots from the
+                                         (default 64): fewer CTAs take fewer SM slots from the
                                          kernels the copy overlaps */
     DELTA_OPT_ADVANCE = 9             /* extract-and-advance (NEXT f3; the trainer keeps W_t only to
                                          diff it against W_{t+1}): 2 = the

@@ -86,7 +86,7 @@ struct delta_ctx {
     bool scan_phase = false;  // a delta_extract_scan_async awaits its emit
 
     // ---- apply workspace
-    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_done, a_state, asm_status, asm_off, dg_ws;
+    DevBuf a_upload, a_recs, a_rcb, a_crec, a_cnt, a_sum, a_ord, a_idx, a_state, asm_status, asm_off, dg_ws;
     uint32_t *h_asm = nullptr;  // pinned
     ApplyState *h_state = nullptr;  // pinned
     // ---- delta_merge workspace
@@ -104,7 +104,7 @@ struct delta_ctx {
     // ---- launch options
     int apply_ctas_per_sm = 32, emit_ctas_per_sm = 3, scatter_ctas_per_sm = 96, scan_kernel = 0;
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
-    int assemble_ctas = 32;   // grid of the NVLink assembly kernels (peer stores; 32: measured best at N=4, round 2)
+    int assemble_ctas = 64;   // grid of the NVLink assembly kernels (peer stores; 64: measured best at N=4)
     bool entry_major = true;
     int mode = 0;  // records written by extract: 0 replace, 1 additive
     int index_codec = 0;  // 0 LEB128 gaps, 1 fixed-width absolute indices (extract and apply)
@@ -202,7 +202,7 @@ void delta_ctx_destroy(delta_ctx *c) {
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
                       &c->tile_plan, &c->blk_agg, &c->tensor_bases, &c->entry_begin, &c->tensor_byte_begin, &c->table,
                       &c->summary, &c->sticky, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->asm_off, &c->dg_ws, &c->a_cnt, &c->a_sum,
-                      &c->a_ord, &c->a_idx, &c->a_done, &c->a_state};
+                      &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
     if (c->profiling) {
         for (auto &e : c->ev_scan) cudaEventDestroy(e);
@@ -907,7 +907,6 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     const size_t up_bytes = off_names + blob.size();
     GROW(ctx->a_upload, std::max<size_t>(up_bytes, 64));
     GROW(ctx->a_recs, nn * sizeof(ApplyRec));
-    GROW(ctx->a_done, nn * sizeof(unsigned int));
     GROW(ctx->a_rcb, (nn + 1) * 8);
     if (!ctx->a_state.p) {
         GROW(ctx->a_state, sizeof(ApplyState));
@@ -949,7 +948,6 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.hint = (hint && n) ? reinterpret_cast<const RecordRow *>(ctx->a_upload.as<uint8_t>() + off_hint) : nullptr;
     if (hint_dev && n) a.hint = reinterpret_cast<const RecordRow *>(hint_dev);
     a.recs = ctx->a_recs.as<ApplyRec>();
-    a.rec_done = ctx->a_done.as<unsigned int>();
     a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
     a.chunk_rec = ctx->a_crec.as<uint32_t>();
     a.chunk_count = ctx->a_cnt.as<unsigned int>();
@@ -1248,7 +1246,6 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
         CK(cudaMemsetAsync(ctx->a_state.p, 0, sizeof(ApplyState), s), "memset");
     }
     GROW(ctx->a_recs, nn * sizeof(ApplyRec));
-    GROW(ctx->a_done, nn * sizeof(unsigned int));
     GROW(ctx->a_rcb, (nn + 1) * 8);
     const size_t nch = std::max(a_bytes, b_bytes) / kByteChunk + n + 2;
     GROW(ctx->a_cnt, nch * 4);
@@ -1267,7 +1264,6 @@ extern "C" int delta_merge(delta_ctx *ctx, uint32_t n, int elem, const void *bod
         a.names = m.b;
         a.hint = x ? m.hb : m.ha;  // the walk's rows: A1 verifies all records in parallel
         a.recs = ctx->a_recs.as<ApplyRec>();
-        a.rec_done = ctx->a_done.as<unsigned int>();
         a.rec_chunk_begin = ctx->a_rcb.as<unsigned long long>();
         a.chunk_rec = ctx->a_crec.as<uint32_t>();
         a.chunk_count = ctx->a_cnt.as<unsigned int>();

@@ -10,7 +10,7 @@
 //                      back from its terminator; strict checks (truncated, overlong,
 //                      > 64-bit, zero gap after the first, gap >= N); per-chunk entry count
 //                      and gap sum.
-//   A3 record_scan     per record: scan of chunk (count, gap sum) -> each chunk's ordinal
+//   A3 k_apply_scan    per record: scan of chunk (count, gap sum) -> each chunk's ordinal
 //                      and index base; count == nnz and last index < N.
 //   A4 k_scatter       gated on the device status word (all-or-nothing):
 //                      decode again, absolute index = base + running gap sum, value read
@@ -96,7 +96,7 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
          const TargetDesc *__restrict__ tg, uint32_t n, const uint8_t *__restrict__ names,
          const RecordRow *__restrict__ hint, ApplyRec *__restrict__ recs,
          unsigned long long *__restrict__ rec_chunk_begin, uint32_t *__restrict__ chunk_rec, ApplyState *st,
-         int width, int fixed, unsigned int *__restrict__ rec_done) {
+         int width, int fixed) {
     if (body_bytes_dev != nullptr) {  // chained after delta_extract_async: size on the device
         const unsigned long long b = *body_bytes_dev;
         if (b > body_bytes) {  // ~0: the extract's gate was closed (no body was written)
@@ -191,14 +191,6 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
         }
     }
     __syncthreads();
-    // A2's per-record tickets start at zero; a record without index bytes gets no chunk, so its
-    // count check (nnz == 0) happens here
-    if (st->status == kOk) {
-        for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
-            rec_done[k] = 0;
-            if (rec_chunk_begin[k + 1] == rec_chunk_begin[k] && recs[k].nnz != 0) set_status(st, kCount);
-        }
-    }
     // chunk -> record map (one load per chunk in A2/A4 instead of a binary search)
     if (st->status == kOk) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -384,18 +376,11 @@ __device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cn
 }
 
 // ------------------------------------------------------------------------------ A2
-__device__ void record_scan(uint32_t k, const ApplyRec *__restrict__ recs, const unsigned long long *__restrict__ rcb,
-                            const unsigned int *chunk_count, const unsigned long long *chunk_sum,
-                            unsigned long long *__restrict__ ord_base, unsigned long long *__restrict__ idx_base,
-                            ApplyState *st);  // A3, below
 __global__ void __launch_bounds__(256)
 k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
                const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
                unsigned int *__restrict__ chunk_count,
-               unsigned long long *__restrict__ chunk_sum, unsigned int *__restrict__ rec_done,
-               unsigned long long *__restrict__ ord_base, unsigned long long *__restrict__ idx_base,
-               ApplyState *st) {
-    __shared__ bool s_last;
+               unsigned long long *__restrict__ chunk_sum, ApplyState *st) {
     if (st->status != kOk) return;
     const unsigned long long nch = st->n_chunks;
     __shared__ __align__(16) uint8_t sb[kStageBytes];
@@ -435,75 +420,71 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
             }
             chunk_count[c] = tc;
             chunk_sum[c] = ts;
-            __threadfence();  // the record's last CTA reads these
-            s_last = atomicAdd(rec_done + k, 1u) == (unsigned)(__ldg(rcb + k + 1) - __ldg(rcb + k)) - 1u;
-        }
-        __syncthreads();
-        if (s_last) {  // this CTA finished the record's last chunk: A3 for the record
-            __threadfence();
-            record_scan(k, recs, rcb, chunk_count, chunk_sum, ord_base, idx_base, st);
         }
         __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------------------ A3
-// Per record: exclusive scan of its chunks' (count, gap sum) -> ordinal and index base of
-// every chunk; count == nnz and last index (= total gap sum) < N.  Run by the CTA of A2 that
-// finishes the record's last chunk (a ticket per record), so it needs no launch of its own;
-// the counts and sums of the other CTAs are read with __ldcg (L2, after their fences).
-__device__ void record_scan(uint32_t k, const ApplyRec *__restrict__ recs, const unsigned long long *__restrict__ rcb,
-                            const unsigned int *chunk_count, const unsigned long long *chunk_sum,
-                            unsigned long long *__restrict__ ord_base, unsigned long long *__restrict__ idx_base,
-                            ApplyState *st) {
+// One CTA per record: exclusive scan of its chunks' (count, gap sum) -> ordinal and index
+// base of every chunk; count == nnz and last index (= total gap sum) < N.
+__global__ void __launch_bounds__(1024)
+k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long long *__restrict__ rcb,
+             const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
+             unsigned long long *__restrict__ ord_base, unsigned long long *__restrict__ idx_base,
+             ApplyState *st) {
+    if (st->status != kOk) return;
     __shared__ unsigned long long s_c[32], s_s[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    const unsigned long long c0 = rcb[k], c1 = rcb[k + 1];
-    unsigned long long cc = 0, cs = 0;
-    for (unsigned long long b = c0; b < c1; b += blockDim.x) {
-        const unsigned long long c = b + threadIdx.x;
-        unsigned long long x = c < c1 ? __ldcg(chunk_count + c) : 0;
-        unsigned long long y = c < c1 ? __ldcg(chunk_sum + c) : 0;
-        const unsigned long long x0 = x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+        const unsigned long long c0 = rcb[k], c1 = rcb[k + 1];
+        unsigned long long cc = 0, cs = 0;
+        for (unsigned long long b = c0; b < c1; b += 1024) {
+            const unsigned long long c = b + threadIdx.x;
+            unsigned long long x = c < c1 ? chunk_count[c] : 0;
+            unsigned long long y = c < c1 ? chunk_sum[c] : 0;
+            const unsigned long long x0 = x, y0 = y;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long xx = __shfl_up_sync(0xffffffffu, x, o);
-            const unsigned long long yy = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) {
-                x += xx;
-                y = sat_add(y, yy);
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long xx = __shfl_up_sync(0xffffffffu, x, o);
+                const unsigned long long yy = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) {
+                    x += xx;
+                    y = sat_add(y, yy);
+                }
             }
-        }
-        if (lane == 31) {
-            s_c[warp] = x;
-            s_s[warp] = y;
-        }
-        __syncthreads();
-        unsigned long long pc = 0, ps = 0, tc = 0, ts = 0;
-        for (int w = 0; w < nwarp; ++w) {
-            if (w < warp) {
-                pc += s_c[w];
-                ps = sat_add(ps, s_s[w]);
+            if (lane == 31) {
+                s_c[warp] = x;
+                s_s[warp] = y;
             }
-            tc += s_c[w];
-            ts = sat_add(ts, s_s[w]);
+            __syncthreads();
+            unsigned long long pc = 0, ps = 0, tc = 0, ts = 0;
+            for (int w = 0; w < 32; ++w) {
+                if (w < warp) {
+                    pc += s_c[w];
+                    ps = sat_add(ps, s_s[w]);
+                }
+                tc += s_c[w];
+                ts = sat_add(ts, s_s[w]);
+            }
+            __syncthreads();
+            // exclusive = prefix of earlier warps + inclusive within warp - own
+            // (the gap sum is saturating: recompute the exclusive part via a shuffle)
+            unsigned long long ye = __shfl_up_sync(0xffffffffu, y, 1);
+            if (lane == 0) ye = 0;
+            if (c < c1) {
+                ord_base[c] = cc + pc + (x - x0);
+                idx_base[c] = sat_add(cs, sat_add(ps, ye));
+            }
+            (void)y0;
+            cc += tc;
+            cs = sat_add(cs, ts);
         }
-        __syncthreads();
-        // exclusive = prefix of earlier warps + inclusive within warp - own
-        // (the gap sum is saturating: recompute the exclusive part via a shuffle)
-        unsigned long long ye = __shfl_up_sync(0xffffffffu, y, 1);
-        if (lane == 0) ye = 0;
-        if (c < c1) {
-            ord_base[c] = cc + pc + (x - x0);
-            idx_base[c] = sat_add(cs, sat_add(ps, ye));
+        if (threadIdx.x == 0) {
+            const ApplyRec R = recs[k];
+            if (cc != R.nnz) set_status(st, kCount);
+            else if (R.nnz > 0 && cs >= R.numel) set_status(st, kRange);
         }
-        cc += tc;
-        cs = sat_add(cs, ts);
-    }
-    if (threadIdx.x == 0) {
-        const ApplyRec R = recs[k];
-        if (cc != R.nnz) set_status(st, kCount);
-        else if (R.nnz > 0 && cs >= R.numel) set_status(st, kRange);
     }
 }
 
@@ -839,7 +820,7 @@ k_fixed_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ r
 cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], s);
     k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
-                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width, a.index_codec, a.rec_done);
+                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width, a.index_codec);
     if (ev) cudaEventRecord(ev[1], s);
     if (a.index_codec) {  // fixed-width indices: validate, then the gated scatter (no scans)
         k_fixed_validate<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.state);
@@ -855,12 +836,12 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
         return cudaGetLastError();
     }
     k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
-                                                  a.chunk_count, a.chunk_sum, a.rec_done, a.chunk_ord_base,
-                                                  a.chunk_idx_base, a.state);
-    if (ev) {  // A3 runs inside A2 (the CTA that finishes a record's last chunk)
-        cudaEventRecord(ev[2], s);
-        cudaEventRecord(ev[3], s);
-    }
+                                                  a.chunk_count, a.chunk_sum, a.state);
+    if (ev) cudaEventRecord(ev[2], s);
+    const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
+    k_apply_scan<<<nb, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
+                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
+    if (ev) cudaEventRecord(ev[3], s);
 #define SCATTER(WW, EM)                                                                                 \
     k_scatter<WW, EM><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec, a.chunk_count, a.chunk_sum, \
                                                      a.chunk_ord_base, a.chunk_idx_base, a.state)
@@ -878,10 +859,12 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
 cudaError_t launch_decode_only(const ApplyArgs &a, unsigned long long *idx_out, void *val_out,
                                const unsigned long long *entry_base, cudaStream_t s) {
     k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
-                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width, 0, a.rec_done);
+                               a.rec_chunk_begin, a.chunk_rec, a.state, a.width, 0);
     k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
-                                                  a.chunk_count, a.chunk_sum, a.rec_done, a.chunk_ord_base,
-                                                  a.chunk_idx_base, a.state);
+                                                  a.chunk_count, a.chunk_sum, a.state);
+    const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
+    k_apply_scan<<<nb, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
+                                     a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (a.width == 2)
         k_decode_write<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.chunk_count,
                                                          a.chunk_sum, a.chunk_ord_base, a.chunk_idx_base, entry_base, idx_out,

@@ -1,23 +1,25 @@
-// extract.cu — sm_100a kernels for delta extraction.  Four launches:
+// extract.cu — sm_100a kernels for delta extraction.
 //
-//   K1  k_scan_tiles    E2-E5: the only kernel that reads the 2W bytes of weights.  One CTA
-//                       per tile (16 Ki 16-bit lanes = 32 KiB of old + 32 KiB of new): 16-byte
-//                       streaming loads into registers, lane-order change masks (bitwise lane
-//                       compare, reading R2) into a shared-memory bitmap, changed vectors staged
-//                       in shared memory; one block scan over the bitmap words gives ranks and
-//                       the tile's count / LEB128 byte count; each thread then emits its word's
-//                       changes in order — values at their ranks, the in-tile gaps already as
-//                       LEB128 bytes — into the tile's workspace slot.
-//   K2a k_tiles_agg     per block of tiles: entries, LEB128 bytes, first / last non-empty tile;
-//                       the last CTA scans the block aggregates into block prefixes.
-//   K2b k_tiles_prefix  E3-E6 placement: per tile the entry / byte prefix and the first gap
-//                       (its predecessor is the last change of the nearest earlier non-empty
-//                       tile of the tensor) into K4's plan; the last CTA writes the
-//                       offset table (K3: record sizes and offsets) and per-tensor bases.
-//   K4  k_emit_tiles    E5+E6: one warp per tile writes the first gap's LEB128 bytes and copies
-//                       the slot's in-tile bytes and values to their final offsets (16-byte
-//                       stores, the next tile's loads in flight); the record headers (K5,
-//                       name_len, name, N, nnz, index_bytes, mode) are written by the same launch.
+//   K1  k_scan_tiles    E2+E3: the only kernel that reads the 2W bytes of weights.  One
+//                       CTA per tile (16 Ki 16-bit lanes = 32 KiB of old + 32 KiB of new),
+//                       16-byte streaming loads, bitwise lane compare, per-vector change
+//                       masks, one packed block scan for the ranks, ordered compaction
+//                       straight into the tile's workspace slot (u16 lane offsets + raw
+//                       values) and the tile's change count.  No inter-CTA communication
+//                       and no shared-memory staging: a pure streaming pass.
+//                       From the tile's change bitmap (shared memory) K1 also derives the
+//                       first / last changed lane and the LEB128 bytes of the gaps inside the
+//                       tile (< 2^14 lanes: 1-2 bytes each).
+//   K2  k_tiles_reduce / k_blocks_scan / k_tiles_bytes / k_tiles_place
+//                       E3+E4+E5 sizes: scans over the (small) per-tile metadata — entry
+//                       prefix, nearest earlier non-empty tile (its last change is the
+//                       predecessor of the tile's first change), each tile's
+//                       LEB128 bytes, byte prefix, per-tensor entry/byte begins.
+//   K3  k_finalize      E6: record sizes and offsets (the offset table), body size.
+//   K4  k_emit_tiles    E5+E6: one warp per tile writes the LEB128 bytes of the first gap
+//                       and of the in-tile gaps (ballot-placed, 32 at a time) and copies the
+//                       raw values to their final offsets (FIXED: absolute indices instead).
+//   K5  k_headers       E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
 //
 // Product code written for this library; none of it is shared with the test oracle.
 // Semantics: DESIGN.md §3 readings R1-R5, R12-R15.
@@ -816,45 +818,6 @@ __device__ __forceinline__ EmitGate emit_gate(const ExtractSummary *summary, uns
     return g;
 }
 
-// Record headers (E6) and the emit outcome, written by K4 (K5 folded in).
-struct HeaderArgs {
-    const RecordRow *table;
-    uint32_t T;
-    const uint32_t *name_len, *name_off;
-    const uint8_t *names;
-    int mode;                        // 0 replace (readings R1/R9), 1 additive
-    unsigned long long *size_out;    // device, may be NULL: the body size, or ~0 if the gate is closed
-    ExtractSticky *sticky;           // async extracts: every closed gate is reported at the wait
-};
-__device__ __forceinline__ void write_header(const HeaderArgs &h, uint32_t k, uint8_t *out, int lane) {
-    const RecordRow r = h.table[k];
-    uint8_t *o = out + r.record_offset;
-    const uint32_t nl = h.name_len[k];
-    for (uint32_t b = lane; b < nl; b += 32) o[2 + b] = h.names[h.name_off[k] + b];
-    // bytes 0-1 name_len, then 3 x u64 after the name: lanes 0-25 one byte each
-    if (lane < 2) o[lane] = (uint8_t)(nl >> (8 * lane));
-    else if (lane < 26) {
-        const int f = (lane - 2) >> 3, bb = (lane - 2) & 7;
-        const unsigned long long x = f == 0 ? r.element_count : (f == 1 ? r.nnz : r.index_bytes);
-        o[2 + nl + 8 * f + bb] = (uint8_t)(x >> (8 * bb));
-    } else if (lane == 26) {
-        o[r.record_bytes - 1] = (uint8_t)h.mode;
-    }
-}
-__device__ __forceinline__ void emit_outcome(const EmitGate &gate, const ExtractSummary *summary, const HeaderArgs &h) {
-    if (h.size_out != nullptr) *h.size_out = gate.local ? summary->body_bytes : ~0ull;
-    if (h.sticky != nullptr && !gate.local) {  // delta_extract_wait reports every closed gate, not just the last
-        if (summary->overflow) {
-            h.sticky->overflow = 1;
-            h.sticky->max_count = max(h.sticky->max_count, summary->max_count);
-        } else {
-            h.sticky->over_cap = 1;
-            h.sticky->need = max(h.sticky->need, summary->body_bytes);
-        }
-    }
-    if (h.sticky != nullptr && gate.fail) h.sticky->peer_fail = max(h.sticky->peer_fail, gate.fail);
-}
-
 // One warp per tile.  LEB128 codec: K1 left the tile's in-tile gaps already encoded in its
 // slot, so the warp writes the first gap's bytes (one lane per byte), then copies the in-tile
 // bytes and the raw values to their final offsets — two warp-wide copies, no per-entry work.
@@ -863,20 +826,13 @@ template <int W, bool FIXED>
 __global__ void __launch_bounds__(256, 3)
 k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
-             uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer,
-             HeaderArgs h) {
+             uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
     const EmitGate gate = emit_gate(summary, cap, peer);
-    if (blockIdx.x == 0 && threadIdx.x == 0) emit_outcome(gate, summary, h);
     if (!gate.local) return;  // emit gate (async extract)
     uint8_t *const pout = gate.peer ? peer.base + gate.off : nullptr;  // fused assembly: the same bytes there too
     const int lane = threadIdx.x & 31;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    // K5 folded in: one warp per record header (name_len, name, N, nnz, index_bytes, mode byte)
-    for (uint32_t k = wg; k < h.T; k += nw) {
-        write_header(h, k, out, lane);
-        if (pout) write_header(h, k, pout, lane);
-    }
     if constexpr (FIXED) {
         __shared__ __align__(16) unsigned long long s_fix[8 * 256 + 2];
         for (uint32_t t = wg; t < ntiles; t += nw) {
@@ -968,6 +924,50 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
     }
 }
 
+// ------------------------------------------------------------------------------ K5
+__device__ __forceinline__ void put_u64(uint8_t *p, unsigned long long x) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) p[b] = (uint8_t)(x >> (8 * b));
+}
+
+__global__ void __launch_bounds__(128)
+k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__restrict__ name_len,
+          const uint32_t *__restrict__ name_off, const uint8_t *__restrict__ names,
+          uint8_t *__restrict__ out, int mode, const ExtractSummary *summary, unsigned long long cap,
+          unsigned long long *size_out, ExtractSticky *sticky, PeerDst peer) {
+    const EmitGate gate = emit_gate(summary, cap, peer);
+    const bool open = gate.local;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (size_out != nullptr) *size_out = open ? summary->body_bytes : ~0ull;
+        if (sticky != nullptr && !open) {  // delta_extract_wait reports every closed gate, not just the last
+            if (summary->overflow) {
+                sticky->overflow = 1;
+                sticky->max_count = max(sticky->max_count, summary->max_count);
+            } else {
+                sticky->over_cap = 1;
+                sticky->need = max(sticky->need, summary->body_bytes);
+            }
+        }
+        if (sticky != nullptr && gate.fail) sticky->peer_fail = max(sticky->peer_fail, gate.fail);
+    }
+    if (!open) return;
+    for (int dst = 0; dst < (gate.peer ? 2 : 1); ++dst)
+    for (uint32_t k = blockIdx.x; k < T; k += gridDim.x) {
+        const RecordRow r = table[k];
+        uint8_t *o = (dst ? peer.base + gate.off : out) + r.record_offset;
+        const uint32_t nl = name_len[k];
+        for (uint32_t b = threadIdx.x; b < nl; b += blockDim.x) o[2 + b] = names[name_off[k] + b];
+        if (threadIdx.x == 0) {
+            o[0] = (uint8_t)nl;
+            o[1] = (uint8_t)(nl >> 8);
+            put_u64(o + 2 + nl, r.element_count);
+            put_u64(o + 2 + nl + 8, r.nnz);
+            put_u64(o + 2 + nl + 16, r.index_bytes);
+            o[r.record_bytes - 1] = (uint8_t)mode;  // 0 replace (reading R1/R9), 1 additive
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------ launchers
 template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
@@ -998,20 +998,20 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
 template <int W>
 static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
-    const HeaderArgs h{a.table, a.ntensors, a.name_len, a.name_off, a.names, a.mode, a.size_out, a.sticky};
     if (ev) cudaEventRecord(ev[0], s);
     if (a.index_codec)
         k_emit_tiles<W, true><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                             static_cast<const LT *>(a.slot_val), out, a.summary,
-                                                            a.out_cap, a.peer, h);
+                                                            a.out_cap, a.peer);
     else
         k_emit_tiles<W, false><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
                                                              static_cast<const LT *>(a.slot_val), out, a.summary,
-                                                             a.out_cap, a.peer, h);
-    if (ev) {  // K5 (headers) runs inside K4
-        cudaEventRecord(ev[1], s);
-        cudaEventRecord(ev[2], s);
-    }
+                                                             a.out_cap, a.peer);
+    if (ev) cudaEventRecord(ev[1], s);
+    const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
+    k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode, a.summary,
+                                 a.out_cap, a.size_out, a.sticky, a.peer);
+    if (ev) cudaEventRecord(ev[2], s);
     return cudaGetLastError();
 }
 

@@ -197,7 +197,6 @@ struct ApplyArgs {
     unsigned long long *chunk_sum;
     unsigned long long *chunk_ord_base;
     unsigned long long *chunk_idx_base;
-    unsigned int *rec_done;               // n: A2's per-record chunk tickets (zeroed by A1)
     unsigned long long chunk_cap;
     ApplyState *state;
     int width;
