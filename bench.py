@@ -698,361 +698,6 @@ def main():
                      "algorithmic_bytes_per_launch": k1_bytes},
         # per rank and step: K1, K2a, K2b (tile prefixes + offset table), K4, K5 + A1-A4
         # (fixed-width indices: A1, A2f, A4f) [+ delta_assemble with --assembly nvlink]
-        "gpu_launches": 0,
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-# ------------------------------------------------------------------ our arm
-def launch_ranks(args):
-    """--gpus N with no WORLD_SIZE in the environment: re-exec this command under
-    torch.distributed.run, one rank per GPU (rendezvous on 127.0.0.1).  Under a launcher,
-    WORLD_SIZE must equal --gpus.  Returns an exit code, or None to run in this process."""
-    world = os.environ.get("WORLD_SIZE")
-    if world is None:
-        if args.gpus <= 1:
-            return None
-        import socket
-        with socket.socket() as sk:
-            sk.bind(("127.0.0.1", 0))
-            port = sk.getsockname()[1]
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
-        print(f"bench: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
-        return subprocess.call(cmd)
-    if int(world) != args.gpus:
-        print(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
-        return 2
-    return None
-
-
-def main():
-    args = parse()
-    rc = launch_ranks(args)
-    if rc is not None:
-        return rc
-    if args.impl == "reference":
-        return run_reference(args)
-    import torch
-    import torch.distributed as dist
-
-    import __graft_entry__ as entry
-    entry.build()
-    import paper_2602_11456_b200 as sd
-    from paper_2602_11456_b200 import dist as sdist
-    from workload import generate_pair
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    comm_info = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        # the communicator as NCCL sees it (one all-reduce over it), logged per rank
-        probe = torch.ones(1, dtype=torch.int64, device=dev)
-        dist.all_reduce(probe)
-        comm_info = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
-                     "ranks_seen_by_allreduce": int(probe.item()),
-                     "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
-        print(f"bench: rank {rank}/{world} on cuda:{local} {comm_info}", file=sys.stderr, flush=True)
-        if comm_info["ranks_seen_by_allreduce"] != world:
-            raise SystemExit(f"bench: NCCL all-reduce saw {comm_info['ranks_seen_by_allreduce']} ranks, expected {world}")
-
-    specs, rho, pattern, desc = workload(args)
-    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
-    width = 2 if args.dtype == "bf16" else 4
-    # contiguous ranges: each rank's records are one byte range of the global body
-    b, e = sdist.shard_plan([s.numel for s in specs], world)[rank]
-    mine = list(range(b, e))
-
-    # ---- inputs resident in HBM before timing (per-tensor seeds: rank-independent data)
-    olds, news, targets = [], [], []
-    for k in mine:
-        o, w = generate_pair(specs[k], k, args.seed, rho=rho, pattern=pattern, dtype=dtype, device=dev)
-        olds.append(o)
-        news.append(w)
-        targets.append(o.clone())
-    torch.cuda.synchronize()
-    local_lanes = sum(specs[k].numel for k in mine)
-    total_lanes = sum(s.numel for s in specs)
-    scanned_total = 2 * total_lanes * width            # old + new bytes, all ranks
-    tensors = [(specs[k].name, o, w) for k, o, w in zip(mine, olds, news)]
-    tgts = [(specs[k].name, t) for k, t in zip(mine, targets)]
-    root_out = None
-    stream = torch.cuda.current_stream()
-
-    comm = torch.cuda.Stream(dev, priority=args.comm_priority) if world > 1 else None
-    nvasm = None
-    fuasm = None
-
-    slot = {"t": 0, "cur": 0}
-
-    def assemble(size, body):
-        """S2+S3 on a side stream: the transfer of the body to rank 0 overlaps this rank's
-        apply (which needs no collective) and, with two body buffers, the next step."""
-        nonlocal root_out
-        if args.assembly == "none":
-            return
-        comm.wait_stream(torch.cuda.current_stream())
-        if fuasm is not None:  # the body is already there (fused emit): completion token only
-            fuasm.token(comm)
-            return
-        if nvasm is not None:  # delta_assemble kernel over NVLink peer memory
-            nvasm.assemble(body, size, stream=comm, slot=slot["cur"])
-            return
-        with torch.cuda.stream(comm):
-            sizes, off, tot = sdist.gather_sizes(size, dev)
-            if rank == 0 and (root_out is None or root_out.numel() < tot):
-                root_out = torch.empty(tot + tot // 8, dtype=torch.uint8, device=dev)
-            sdist.assemble(body, sizes, root_out)
-
-    if args.pipeline > 1:
-        from paper_2602_11456_b200.pipeline import RoundTrip
-        rt = RoundTrip(tensors, tgts, groups=args.pipeline, device=dev,
-                       apply_ctas_per_sm=args.apply_ctas or None, scan_kernel=args.scan_kernel or None)
-        rt.set_profiling(True)
-        ctx = rt.cx
-
-        def step(acc=None):
-            body = rt.step(acc)
-            if world > 1:
-                assemble(body.numel(), body)
-                torch.cuda.current_stream().wait_stream(comm)
-            return body, rt.table()
-    else:
-        tl = sd.TensorList(tensors)
-        tg = sd.TargetList(tgts)
-        ctx = sd.DeltaContext(dev)
-        if args.apply_ctas:
-            ctx.set_option(1, args.apply_ctas)
-        if args.scan_kernel:
-            ctx.set_option(3, args.scan_kernel)
-        if args.scatter_ctas:
-            ctx.set_option(4, args.scatter_ctas)
-        if args.prefetch_tiles:
-            ctx.set_option(5, args.prefetch_tiles)
-        if args.scatter_order:
-            ctx.set_option(6, args.scatter_order)
-        if args.index_codec == "fixed":
-            ctx.set_option(8, 2)
-        if args.assemble_ctas:
-            ctx.set_option(10, args.assemble_ctas)
-        ctx.set_profiling(True)
-        size0 = ctx.delta_size(tl)
-        out = torch.empty(size0 + size0 // 8 + 4096, dtype=torch.uint8, device=dev)
-        if world > 1 and args.assembly in ("nvlink", "fused"):
-            tot0 = torch.tensor([size0], dtype=torch.int64, device=dev)
-            dist.all_reduce(tot0)
-            total0 = int(tot0.item())
-            if args.assembly == "fused":
-                fuasm = sdist.FusedAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
-                if rank == 0:
-                    out = fuasm.bufs[0]  # rank 0's records are the head of the assembled body
-            else:
-                nvasm = sdist.NvlinkAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
-                if rank == 0:
-                    out = nvasm.buf  # rank 0's records are the head of the assembled body
-
-        size_dev = torch.zeros(1, dtype=torch.int64, device=dev)
-        # two (body, size) slots when the NVLink assembly runs on the comm stream: step t+1
-        # extracts into the other slot while step t's body is still being copied to rank 0
-        nslots = 2 if (nvasm is not None or fuasm is not None) else 1
-        root_bufs = nvasm.bufs if nvasm is not None else (fuasm.bufs if fuasm is not None else None)
-        outs = [out] + ([root_bufs[1] if (rank == 0 and root_bufs is not None) else torch.empty_like(out)]
-                        if nslots == 2 else [])
-        size_devs = [size_dev] + ([torch.zeros(1, dtype=torch.int64, device=dev)] if nslots == 2 else [])
-        slot_free = [None] * nslots  # comm-stream event: the slot's last assembly is done
-
-        def record(acc):
-            t = ctx.last_timing()
-            if acc is not None:
-                for kname in ("scan_ms", "lens_ms", "finalize_ms", "emit_ms", "headers_ms",
-                              "locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
-                    acc[kname] = acc.get(kname, 0.0) + t[kname]
-
-        if args.sync_step or (world > 1 and nvasm is None and fuasm is None and args.assembly != "none"):
-            def step(acc=None):
-                # host-sized path: delta_extract reads the size back (sync), the apply takes
-                # the device table; 2 host syncs per step
-                body, table = ctx.delta_extract(tl, out=out, table="device")
-                if world > 1:
-                    assemble(body.numel(), body)
-                ctx.delta_apply(tg, body, table=table)
-                if world > 1:
-                    torch.cuda.current_stream().wait_stream(comm)
-                record(acc)
-                return body, table
-        else:
-            def before_apply(buf, size):
-                if world > 1:
-                    assemble(size, buf)
-
-            def step(acc=None, wait=True):
-                # one stream of kernels: extract (size + table stay on the device) -> [assembly
-                # on the comm stream] -> chained apply; the host waits once, at the end (or,
-                # wait=False, not at all: errors surface at the next extract_wait/apply_wait)
-                s = slot["t"] % nslots
-                slot["t"] += 1
-                slot["cur"] = s
-                if slot_free[s] is not None:  # the slot's previous body has reached rank 0
-                    torch.cuda.current_stream().wait_event(slot_free[s])
-                fx = None
-                if fuasm is not None:  # fused emit + assembly: scan, size all-gather, emit to both
-                    def fx(tl_, o_, sz_, st_, s=s):
-                        return fuasm.extract(tl_, o_, sz_, slot=s, stream=st_)[1]
-                n = ctx.round_trip(tl, tg, outs[s], size_devs[s], before_apply=before_apply, wait=wait, extract=fx)
-                if world > 1:
-                    if nslots == 1:
-                        torch.cuda.current_stream().wait_stream(comm)
-                    else:
-                        ev = torch.cuda.Event()
-                        ev.record(comm)
-                        slot_free[s] = ev
-                    if wait:
-                        torch.cuda.current_stream().wait_stream(comm)
-                if wait:
-                    record(acc)
-                return (outs[s][:n] if n is not None else None), None
-
-    chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None and fuasm is None
-                                                             and args.assembly != "none"))
-    pipelined = chained and args.host_sync == "end"
-    for _ in range(max(args.warmup, 0)):
-        body, table = step()
-    if pipelined:  # kernel times accumulated on the device over the timed region
-        ctx.set_profiling(2)
-        step()  # one more waited warm-up step with the accumulating event ring
-        ctx.timing_totals()
-    clocks = Clocks(local, enabled=not args.no_clocks)
-    acc = {}
-    clocks.start()
-    time.sleep(1.0)  # sampler up and running before the timed region
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    w0 = time.time()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        if pipelined:
-            step(wait=False)
-        else:
-            body, table = step(acc)
-    if comm is not None:  # the last step's assembly is part of the timed work
-        stream.wait_stream(comm)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if pipelined:
-        nb = ctx.extract_wait()   # raises if any step's extract overflowed (never after warm-up)
-        ctx.apply_wait()          # raises if any step's apply gate was closed
-        body, table = outs[(slot["t"] - 1) % nslots][:nb], None
-        tot, calls = ctx.timing_totals()
-        if calls != args.steps:
-            raise SystemExit(f"bench: {calls} extract scans timed for {args.steps} steps")
-        acc = {k: v for k, v in tot.items()}
-    w1 = time.time()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop(w0, w1)
-    # correctness guard on the timed configuration: apply(extract(old,new)) == new
-    ok = all(torch.equal(t.view(torch.int16 if width == 2 else torch.int32),
-                         w.view(torch.int16 if width == 2 else torch.int32))
-             for t, w in zip(targets, news))
-    if not ok:
-        raise SystemExit("bench: round trip mismatch")
-    ms = ev0.elapsed_time(ev1)
-    rank_view = None
-    if world > 1:  # max over ranks; every rank's time and K1 / scatter time for the record
-        k1_local = acc.get("scan_ms", 0.0) / args.steps
-        sc_local = acc.get("scatter_ms", 0.0) / args.steps
-        t = torch.tensor([ms, k1_local, sc_local], dtype=torch.float64, device=dev)
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(allt, t)
-        rank_view = {"ms_per_step": [round(float(x[0]) / args.steps, 4) for x in allt],
-                     "k1_ms": [round(float(x[1]), 4) for x in allt],
-                     "scatter_ms": [round(float(x[2]), 4) for x in allt]}
-        ms = max(float(x[0]) for x in allt)
-    ms_step = ms / args.steps
-    value = scanned_total * args.steps / (ms / 1e3) / 1e9
-
-    # ---- payload (global) and kernel-level roofline of the dominant kernel (K1)
-    if table is None or isinstance(table, sd.DeviceTable):  # host rows for the statistics (untimed)
-        body, table = ctx.delta_extract(tl, out=out, table=True)
-    body_local = body.numel()
-    nnz_local = sum(r[2] for r in table)
-    idx_local = sum(r[4] for r in table)
-    # the paper's "naive" fixed-width encoding of the same change set (PAPER.md:387: int32
-    # or int64 index "depending on tensor size" + the value; reading R6), for the
-    # naive-vs-varint payload ablation (PAPER.md:609: 414 MB -> 202 MB)
-    naive_local = sum((27 + len(specs[k].name.encode())) + r[2] * ((4 if r[1] - 1 <= 2**31 - 1 else 8) + width)
-                      for k, r in zip(mine, table))
-    if world > 1:
-        t = torch.tensor([body_local, nnz_local, idx_local, naive_local], dtype=torch.int64, device=dev)
-        dist.all_reduce(t)
-        body_total, nnz_total, idx_total, naive_total = (int(x) for x in t.tolist())
-    else:
-        body_total, nnz_total, idx_total, naive_total = body_local, nnz_local, idx_local, naive_local
-    k1_ms = acc.get("scan_ms", 0.0) / args.steps
-    k1_bytes = 2 * local_lanes * width  # DESIGN.md §6: K1's algorithmic bytes = the 2wN it compares
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except (OSError, ValueError):
-        pass
-    # DRAM traffic of one K1 launch from the committed ncu capture of this exact workload
-    # (profiles/ncu_traffic.json; null for other configurations)
-    k1_traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        c = tr["config"]
-        if (c["config"] == args.config and abs(c["rho"] - rho) < 1e-12 and c["pattern"] == pattern
-                and c["dtype"] == args.dtype and c["n_gpus"] == world):
-            k = tr["kernels"]["k_scan_tiles"]
-            k1_traffic = k["dram_read_bytes"] + k["dram_write_bytes"]
-    except (OSError, ValueError, KeyError):
-        pass
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None
-    kernel_ms = {k: round(v / args.steps, 4) for k, v in acc.items()}
-
-    result = {
-        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u16" if width == 2 else "u32", "data": "synthetic",
-        "config": {"workload": desc, "config": args.config, "tensors": len(specs),
-                   "lanes": total_lanes, "weights_bytes": total_lanes * width,
-                   "scanned_bytes_per_step": scanned_total, "rho": rho, "pattern": pattern,
-                   "seed": args.seed, "index_codec": args.index_codec,
-                   "shard": "contiguous balanced tensor ranges",
-                   "l2": f"inputs ({scanned_total / 1e9:.1f} GB per step) larger than L2 (126 MB); no flush"},
-        "payload": {"body_bytes": body_total, "ratio": round(total_lanes * width / body_total, 3),
-                    "nnz": nnz_total, "rho_measured": nnz_total / total_lanes,
-                    "index_bytes_per_entry": round(idx_total / max(nnz_total, 1), 4),
-                    "naive_fixed_width_bytes": naive_total,
-                    "varint_saving_vs_naive": round(naive_total / body_total, 3),
-                    "paper_context": PAPER_CPU},
-        "kernel_ms_per_step": kernel_ms,
-        # SURVEY §8(d): per-op time (this rank's kernels) and algorithmic bytes, and the round
-        # trip's algorithmic bytes per lane 2w + rho (3w + 2E) against the measured peak
-        "ops": ops_view(kernel_ms, local_lanes, width, nnz_local, idx_local, body_local,
-                        peaks.get("hbm_gbs", 6650.0), value, scanned_total, total_lanes, nnz_total,
-                        idx_total),
-        "roofline": {"kernel": "k_scan_tiles (K1)", "bound": "hbm",
-                     "achieved": round(achieved, 1) if achieved else None,
-                     "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": k1_traffic,
-                     "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write.sum, one launch)"
-                     if k1_traffic else None,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks
-                     else "fallback 6650 GB/s (B200_PROFILING.md)",
-                     "algorithmic_bytes_per_launch": k1_bytes},
-        # per rank and step: K1, K1b, 5 tile scans, K3, K3b (9; no K1b with fixed-width
-        # indices) + K4, K5 + A1-A4 (fixed-width: A1, A2f, A4f) [+ delta_assemble when N > 1]
         "gpu_launches": ((9 if args.index_codec == "leb128" else 8)
                          + (1 if world > 1 and nvasm is not None else 0)) * args.steps,
         "clocks": clk,

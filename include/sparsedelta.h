@@ -441,7 +441,7 @@ enum {
                                          not strictly increasing -> DELTA_D_NONINCREASING, an index
                                          >= element_count -> DELTA_D_RANGE (all-or-nothing as ever). */
     DELTA_OPT_ASSEMBLE_CTAS = 10,     /* grid (CTAs, total) of delta_assemble / delta_assemble_records
-                                         (default 64): fewer CTAs take fewer SM slots from the
+                                         (default 32): fewer CTAs take fewer SM slots from the
                                          kernels the copy overlaps */
     DELTA_OPT_ADVANCE = 9             /* extract-and-advance (NEXT f3; the trainer keeps W_t only to
                                          diff it against W_{t+1}): 2 = the

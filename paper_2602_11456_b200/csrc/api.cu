@@ -104,7 +104,7 @@ struct delta_ctx {
     // ---- launch options
     int apply_ctas_per_sm = 32, emit_ctas_per_sm = 3, scatter_ctas_per_sm = 96, scan_kernel = 0;
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
-    int assemble_ctas = 64;   // grid of the NVLink assembly kernels (peer stores; 64: measured best at N=4)
+    int assemble_ctas = 32;   // grid of the NVLink assembly kernels (peer stores; 32: measured best at N=4, round 2)
     bool entry_major = true;
     int mode = 0;  // records written by extract: 0 replace, 1 additive
     int index_codec = 0;  // 0 LEB128 gaps, 1 fixed-width absolute indices (extract and apply)
