@@ -304,6 +304,75 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         }
     }
 
+    // ---- 3'. dense tiles (>= kDenseTile changes): warp-cooperative emission in rank order.
+    // Round r of warp w emits the warp's entries 32 r .. 32 r + 31, one per lane: the owner
+    // word by bisection over the warp's word prefixes (shuffles), the lane by the j-th set bit
+    // (__fns), the previous entry's lane from the neighbour lane — so a round's value / offset
+    // stores are 32 consecutive slots and its gap bytes one contiguous run (coalesced), where
+    // the per-word loop below would scatter them over 32 runs.
+    if (c >= kDenseTile) {
+        const uint32_t wcnt = __shfl_sync(0xffffffffu, inc, 31) & 0xFFFFu;  // this warp's entries
+        const uint32_t wpre = pre & 0xFFFFu;                                 // entries before the warp
+        const uint32_t myex = (inc - val) & 0xFFFFu;  // entries before this lane's word, in the warp
+        int fw = -1, lwp = -1;  // the tile's first non-empty word; the last one before this warp
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) {
+            if (fw < 0) fw = s_wfirst[w];
+            if (w < warp && s_wlast[w] >= 0) lwp = s_wlast[w];
+        }
+        uint32_t prevL = lwp >= 0 ? 64u * lwp + 63u - (uint32_t)__clzll((long long)s_bits[lwp]) : 0u;
+        bool have_prev = lwp >= 0;
+        // LEB128 bytes before the warp's first entry: one per earlier in-tile gap plus the
+        // two-byte flags of earlier words, without the tile's first word's (it has no gap)
+        const uint32_t bigs = (pre >> 16) - ((fw >= 0 && fw < 32 * warp) ? 1u : 0u);
+        uint32_t boff = wpre ? wpre - 1u + bigs : 0u;
+        LT *sv = slot_val + (size_t)t * slot_cap;
+        const LT *sn = reinterpret_cast<const LT *>(s_new);
+        uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
+        const uint32_t lt = (1u << lane) - 1u;
+        for (uint32_t r0 = 0; r0 < wcnt; r0 += 32) {
+            const uint32_t k = r0 + lane;
+            const bool act = k < wcnt;
+            uint32_t o = 0;  // the largest lane whose word starts at or before entry k
+#pragma unroll
+            for (uint32_t st = 16; st; st >>= 1) {
+                const uint32_t e = __shfl_sync(0xffffffffu, myex, o + st);
+                if (e <= k) o += st;
+            }
+            const uint32_t jj = k - __shfl_sync(0xffffffffu, myex, o);
+            const uint32_t xlo = __shfl_sync(0xffffffffu, (uint32_t)X, o);
+            const uint32_t xhi = __shfl_sync(0xffffffffu, (uint32_t)(X >> 32), o);
+            const uint32_t plo = __popc(xlo);
+            const uint32_t bit = jj < plo ? __fns(xlo, 0, (int)jj + 1) : 32u + __fns(xhi, 0, (int)(jj - plo) + 1);
+            const uint32_t L = 64u * (32u * warp + o) + bit;
+            uint32_t Lp = __shfl_up_sync(0xffffffffu, L, 1);
+            bool hp = true;
+            if (lane == 0) {
+                Lp = prevL;
+                hp = have_prev;
+            }
+            const uint32_t g = L - Lp;
+            if (act) sv[wpre + k] = sn[L];
+            if constexpr (OFFSETS) {
+                if (act) reinterpret_cast<uint16_t *>(sb)[wpre + k] = (uint16_t)L;
+            } else {
+                const uint32_t len = (!act || !hp) ? 0u : (g >= 128u ? 2u : 1u);
+                const uint32_t b1 = __ballot_sync(0xffffffffu, len >= 1u), b2 = __ballot_sync(0xffffffffu, len == 2u);
+                const uint32_t my = boff + __popc(b1 & lt) + __popc(b2 & lt);
+                if (len == 1u) {
+                    sb[my] = (uint8_t)g;
+                } else if (len == 2u) {
+                    sb[my] = (uint8_t)(g | 0x80u);
+                    sb[my + 1] = (uint8_t)(g >> 7);
+                }
+                boff += __popc(b1) + __popc(b2);
+            }
+            prevL = __shfl_sync(0xffffffffu, L, min(31u, wcnt - 1u - r0));
+            have_prev = true;
+        }
+        return;
+    }
+
     // ---- 3. ordered emission of word tid's changes: the value at its rank; the gap to the
     // previous change as LEB128 bytes at its position in the tile's internal index stream
     // (OFFSETS, for the fixed-width codec: the u16 lane offset at its rank instead).
