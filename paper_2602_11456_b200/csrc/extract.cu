@@ -138,7 +138,7 @@ template <int W, bool ADDITIVE = false, bool ADVANCE = false, bool OFFSETS = fal
 __global__ void __launch_bounds__(256, 3)
 k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefetch_dist, uint32_t slot_cap,
              uint8_t *__restrict__ slot_bytes, typename LaneOf<W>::T *__restrict__ slot_val,
-             TileMeta *__restrict__ meta, ExtractSummary *summary, uint32_t redo_cap) {
+             TileMeta *__restrict__ meta, ExtractSummary *summary, uint32_t redo_cap, uint32_t dense_tile) {
     using LT = typename LaneOf<W>::T;
     constexpr int THREADS = 256, VECS = 8;
     constexpr int LPV = 16 / W;                  // lanes per 16-byte vector
@@ -304,71 +304,85 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         }
     }
 
-    // ---- 3'. dense tiles (>= kDenseTile changes): warp-cooperative emission in rank order.
-    // Round r of warp w emits the warp's entries 32 r .. 32 r + 31, one per lane: the owner
-    // word by bisection over the warp's word prefixes (shuffles), the lane by the j-th set bit
-    // (__fns), the previous entry's lane from the neighbour lane — so a round's value / offset
-    // stores are 32 consecutive slots and its gap bytes one contiguous run (coalesced), where
-    // the per-word loop below would scatter them over 32 runs.
-    if (c >= kDenseTile) {
-        const uint32_t wcnt = __shfl_sync(0xffffffffu, inc, 31) & 0xFFFFu;  // this warp's entries
-        const uint32_t wpre = pre & 0xFFFFu;                                 // entries before the warp
-        const uint32_t myex = (inc - val) & 0xFFFFu;  // entries before this lane's word, in the warp
-        int fw = -1, lwp = -1;  // the tile's first non-empty word; the last one before this warp
-#pragma unroll
-        for (int w = 0; w < NWARP; ++w) {
-            if (fw < 0) fw = s_wfirst[w];
-            if (w < warp && s_wlast[w] >= 0) lwp = s_wlast[w];
+    // ---- 3'. dense tiles (>= dense_tile changes, default kDenseTile): emission in vector order.  The owner of
+    // word w publishes its rank / two-byte-flag prefix and its first entry's predecessor; then
+    // thread tid emits the changes of ITS vectors v = r THREADS + tid (r = 0..7), whose 8 lanes
+    // are byte v & 7 of word v >> 3: a warp's lanes hold consecutive vectors, so each store
+    // instruction writes 32 nearby slots (the per-word loop below would write 32 runs 64
+    // entries apart).  Values come from the staged vectors, gap bytes at their stream positions.
+    if (c >= dense_tile) {
+        __shared__ uint32_t s_wex[NWORDS], s_wprv[NWORDS];
+        if (tid < NWORDS) {
+            s_wex[tid] = pre + inc - val;  // entries | two-byte flags before the word
+            s_wprv[tid] = 0;  // bits 0-15: predecessor lane; 16: first gap takes two bytes; 17: has one
         }
-        uint32_t prevL = lwp >= 0 ? 64u * lwp + 63u - (uint32_t)__clzll((long long)s_bits[lwp]) : 0u;
-        bool have_prev = lwp >= 0;
-        // LEB128 bytes before the warp's first entry: one per earlier in-tile gap plus the
-        // two-byte flags of earlier words, without the tile's first word's (it has no gap)
-        const uint32_t bigs = (pre >> 16) - ((fw >= 0 && fw < 32 * warp) ? 1u : 0u);
-        uint32_t boff = wpre ? wpre - 1u + bigs : 0u;
+        // the predecessor of each word's first entry (shuffles: all lanes take part)
+        {
+            const uint32_t mylast = X ? 64u * tid + 63u - (uint32_t)__clzll((long long)X) : 0u;
+            const uint32_t lower = bw & ((1u << lane) - 1u);
+            uint32_t prev = __shfl_sync(0xffffffffu, mylast, lower ? 31 - __clz(lower) : 0);
+            bool has_prev = lower != 0;
+            if (X && !lower) {
+                int lw = -1;
+#pragma unroll
+                for (int w = 0; w < NWARP; ++w)
+                    if (w < warp && s_wlast[w] >= 0) lw = s_wlast[w];
+                if (lw >= 0) {
+                    prev = 64u * lw + 63u - (uint32_t)__clzll((long long)s_bits[lw]);
+                    has_prev = true;
+                }
+            }
+            if (tid < NWORDS && X)
+                s_wprv[tid] = (has_prev ? (prev | (1u << 17) | ((val >> 16) ? (1u << 16) : 0u)) : 0u);
+        }
+        __syncthreads();
         LT *sv = slot_val + (size_t)t * slot_cap;
         const LT *sn = reinterpret_cast<const LT *>(s_new);
         uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
-        const uint32_t lt = (1u << lane) - 1u;
-        for (uint32_t r0 = 0; r0 < wcnt; r0 += 32) {
-            const uint32_t k = r0 + lane;
-            const bool act = k < wcnt;
-            uint32_t o = 0;  // the largest lane whose word starts at or before entry k
-#pragma unroll
-            for (uint32_t st = 16; st; st >>= 1) {
-                const uint32_t e = __shfl_sync(0xffffffffu, myex, o + st);
-                if (e <= k) o += st;
-            }
-            const uint32_t jj = k - __shfl_sync(0xffffffffu, myex, o);
-            const uint32_t xlo = __shfl_sync(0xffffffffu, (uint32_t)X, o);
-            const uint32_t xhi = __shfl_sync(0xffffffffu, (uint32_t)(X >> 32), o);
-            const uint32_t plo = __popc(xlo);
-            const uint32_t bit = jj < plo ? __fns(xlo, 0, (int)jj + 1) : 32u + __fns(xhi, 0, (int)(jj - plo) + 1);
-            const uint32_t L = 64u * (32u * warp + o) + bit;
-            uint32_t Lp = __shfl_up_sync(0xffffffffu, L, 1);
-            bool hp = true;
-            if (lane == 0) {
-                Lp = prevL;
-                hp = have_prev;
-            }
-            const uint32_t g = L - Lp;
-            if (act) sv[wpre + k] = sn[L];
-            if constexpr (OFFSETS) {
-                if (act) reinterpret_cast<uint16_t *>(sb)[wpre + k] = (uint16_t)L;
-            } else {
-                const uint32_t len = (!act || !hp) ? 0u : (g >= 128u ? 2u : 1u);
-                const uint32_t b1 = __ballot_sync(0xffffffffu, len >= 1u), b2 = __ballot_sync(0xffffffffu, len == 2u);
-                const uint32_t my = boff + __popc(b1 & lt) + __popc(b2 & lt);
-                if (len == 1u) {
-                    sb[my] = (uint8_t)g;
-                } else if (len == 2u) {
-                    sb[my] = (uint8_t)(g | 0x80u);
-                    sb[my + 1] = (uint8_t)(g >> 7);
+#pragma unroll 1
+        for (int r = 0; r < VECS; ++r) {
+            const uint32_t v = r * THREADS + tid;
+            const uint32_t w = v / (64 / LPV), sub = v % (64 / LPV);  // word, lane group in it
+            const unsigned long long Wb = s_bits[w];
+            uint32_t mb = (uint32_t)(Wb >> (sub * LPV)) & ((1u << LPV) - 1u);
+            if (!mb) continue;
+            const unsigned long long below = Wb & ((1ull << (sub * LPV)) - 1ull);
+            const uint32_t ex = s_wex[w], pv = s_wprv[w];
+            uint32_t rank = (ex & 0xFFFFu) + (uint32_t)__popcll((long long)below);
+            const bool hp_w = pv & (1u << 17);
+            const uint32_t bigs = (ex >> 16) - ((hp_w && (ex >> 16)) ? 1u : 0u);
+            // byte position: one per earlier in-tile gap + the earlier two-byte ones
+            uint32_t bp = rank - 1u + bigs + (below && (pv & (1u << 16)) ? 1u : 0u);
+            bool word_first = below == 0;
+            bool has_prev = below ? true : hp_w;
+            uint32_t prevL = below ? 64u * w + 63u - (uint32_t)__clzll((long long)below) : (pv & 0xFFFFu);
+            while (mb) {
+                const uint32_t jb = (uint32_t)__ffs(mb) - 1u;
+                mb &= mb - 1u;
+                const uint32_t L = v * LPV + jb;
+                sv[rank] = sn[L];
+                if constexpr (OFFSETS) {
+                    reinterpret_cast<uint16_t *>(sb)[rank] = (uint16_t)L;
+                } else {
+                    if (has_prev) {
+                        const uint32_t g = L - prevL;
+                        if (word_first && (pv & (1u << 16))) {
+                            sb[bp] = (uint8_t)(g | 0x80u);
+                            sb[bp + 1] = (uint8_t)(g >> 7);
+                            bp += 2;
+                        } else {
+                            sb[bp] = (uint8_t)g;
+                            bp += 1;
+                        }
+                    } else {
+                        bp += 1;  // the tile's first entry: its gap is the plan's first gap (K2)
+                    }
                 }
-                boff += __popc(b1) + __popc(b2);
+                has_prev = true;
+                word_first = false;
+                prevL = L;
+                ++rank;
             }
-            prevL = __shfl_sync(0xffffffffu, L, min(31u, wcnt - 1u - r0));
-            have_prev = true;
         }
         return;
     }
@@ -1041,13 +1055,19 @@ k_headers(const RecordRow *__restrict__ table, uint32_t T, const uint32_t *__res
 template <int W>
 static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     using LT = typename LaneOf<W>::T;
+    // K1's emission switches to vector order at this many changes per tile (DELTA_K1_DENSE_TILE
+    // overrides it for experiments; results never depend on it)
+    static const uint32_t dense_tile = [] {
+        const char *e = getenv("DELTA_K1_DENSE_TILE");
+        return e != nullptr ? (uint32_t)atoi(e) : kDenseTile;
+    }();
     if (ev) cudaEventRecord(ev[0], s);
     if (a.ntiles)
         (a.index_codec ? (a.advance ? k_scan_tiles<W, false, true, true>
                                     : a.mode == 1 ? k_scan_tiles<W, true, false, true> : k_scan_tiles<W, false, false, true>)
                        : (a.advance ? k_scan_tiles<W, false, true> : a.mode == 1 ? k_scan_tiles<W, true> : k_scan_tiles<W>))
             <<<a.ntiles, 256, 0, s>>>(a.tiles, a.ntiles, a.prefetch_dist, a.slot_cap, a.slot_bytes,
-                                      static_cast<LT *>(a.slot_val), a.meta, a.summary, a.redo_cap);
+                                      static_cast<LT *>(a.slot_val), a.meta, a.summary, a.redo_cap, dense_tile);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
     if (nblk) {
