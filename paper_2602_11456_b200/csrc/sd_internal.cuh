@@ -11,7 +11,7 @@ constexpr int kScanThreads = 256;  // K1 block
 constexpr int kScanVecs = 8;       // 16-byte vectors per thread per operand per tile
 constexpr int kTileBytes = kScanThreads * kScanVecs * 16;  // 32 KiB of old + 32 KiB of new
 // lanes per tile: 16384 (16-bit lanes) or 8192 (32-bit lanes) -> a lane offset fits a u16
-constexpr uint32_t kDenseTile = 1024;  // K1: tiles with this many changes emit in vector order
+constexpr uint32_t kDenseTile = 4096;  // K1: tiles with this many changes (25 %) emit in vector order
 constexpr int kTileThreads = 256;  // threads of the tile-level scan kernels (K2a, K2b)
 constexpr int kTileBlock = kTileThreads * 4;  // tiles per block of the tile-level scans (4 per thread)
 constexpr int kByteChunk = 4096;   // index-stream bytes per A2/A4 chunk (256 threads x 16)
