@@ -78,6 +78,7 @@ def parse():
                    help="G > 1: extract and apply in G pipelined groups on two streams")
     p.add_argument("--apply-ctas", type=int, default=0, help="apply kernels' CTAs per SM (0 = default)")
     p.add_argument("--scatter-ctas", type=int, default=0, help="scatter kernel CTAs per SM (0 = default)")
+    p.add_argument("--emit-ctas", type=int, default=0, help="extract emit kernel CTAs per SM (0 = default)")
     p.add_argument("--prefetch-tiles", type=int, default=0, help="K1 L2 prefetch distance in tiles + 1 (0 = default)")
     p.add_argument("--scatter-order", type=int, default=0, help="1 thread-major, 2 entry-major (0 = default)")
     p.add_argument("--scan-kernel", type=int, default=0,
@@ -473,6 +474,8 @@ def main():
         ctx = sd.DeltaContext(dev)
         if args.apply_ctas:
             ctx.set_option(1, args.apply_ctas)
+        if args.emit_ctas:
+            ctx.set_option(2, args.emit_ctas)
         if args.scan_kernel:
             ctx.set_option(3, args.scan_kernel)
         if args.scatter_ctas:
@@ -696,9 +699,9 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": k1_bytes},
-        # per rank and step: K1, K2a, K2b (tile prefixes + offset table), K4, K5 + A1-A4
+        # per rank and step: K1, K2 (tile prefixes + offset table), K4, K5 + A1-A4
         # (fixed-width indices: A1, A2f, A4f) [+ delta_assemble with --assembly nvlink]
-        "gpu_launches": ((9 if args.index_codec == "leb128" else 8)
+        "gpu_launches": ((8 if args.index_codec == "leb128" else 7)
                          + (1 if world > 1 and nvasm is not None else 0)) * args.steps,
         "clocks": clk,
     }

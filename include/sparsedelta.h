@@ -407,7 +407,8 @@ typedef struct {
 enum {
     DELTA_OPT_APPLY_CTAS_PER_SM = 1, /* grid of the apply decode kernel, CTAs per SM (default 32: many short
                                         CTAs, scheduled as slots free up, balance the chunks) */
-    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 3: its register limit) */
+    DELTA_OPT_EMIT_CTAS_PER_SM = 2,  /* grid of the extract emit kernel, CTAs per SM (default 24: ~5 resident,
+                                        the rest scheduled as slots free; measured 0.164 ms at 8, 0.153 at 24) */
     DELTA_OPT_SCAN_KERNEL = 3,       /* compare+compaction kernel: 1 = one CTA per tile, 16-byte
                                         vectors, bitmap compaction (the only form; the retired
                                         variants 2-5 — TMA pipeline, 128-byte runs, 512 x 4,

@@ -72,7 +72,7 @@ struct delta_ctx {
     unsigned long long total_lanes = 0;
     DevBuf tiles, name_len, name_off, names, numel, tensor_first_tile;
     // ---- extract workspace
-    DevBuf slot_bytes, slot_val, meta, tile_plan, blk_agg, tensor_bases, entry_begin, tensor_byte_begin, table,
+    DevBuf slot_bytes, slot_val, meta, tile_plan, lb_slots, tensor_bases, entry_begin, tensor_byte_begin, table,
         summary, sticky;
     uint32_t slot_cap = 0;          // entries per tile slot (grows on overflow)
     bool scan_cached = false;       // K1-K3 results valid for plan_key (delta_size)
@@ -102,7 +102,8 @@ struct delta_ctx {
     int ring_next = 0;
 
     // ---- launch options
-    int apply_ctas_per_sm = 32, emit_ctas_per_sm = 3, scatter_ctas_per_sm = 96, scan_kernel = 0;
+    uint32_t lb_epoch = 0;  // K2 look-back launch epoch
+    int apply_ctas_per_sm = 32, emit_ctas_per_sm = 24, scatter_ctas_per_sm = 96, scan_kernel = 0;
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
     int assemble_ctas = 32;   // grid of the NVLink assembly kernels (peer stores; 32: measured best at N=4, round 2)
     bool entry_major = true;
@@ -200,7 +201,7 @@ void delta_ctx_destroy(delta_ctx *c) {
     for (DevBuf *b : mbufs) b->release();
     DevBuf *bufs[] = {&c->tiles, &c->name_len, &c->name_off, &c->names, &c->numel,
                       &c->tensor_first_tile, &c->slot_bytes, &c->slot_val, &c->meta,
-                      &c->tile_plan, &c->blk_agg, &c->tensor_bases, &c->entry_begin, &c->tensor_byte_begin, &c->table,
+                      &c->tile_plan, &c->lb_slots, &c->tensor_bases, &c->entry_begin, &c->tensor_byte_begin, &c->table,
                       &c->summary, &c->sticky, &c->a_upload, &c->a_recs, &c->a_rcb, &c->a_crec, &c->asm_status, &c->asm_off, &c->dg_ws, &c->a_cnt, &c->a_sum,
                       &c->a_ord, &c->a_idx, &c->a_state};
     for (DevBuf *b : bufs) b->release();
@@ -493,7 +494,12 @@ static ExtractArgs extract_args(delta_ctx *ctx) {
     a.slot_val = ctx->slot_val.p;
     a.meta = ctx->meta.as<TileMeta>();
     a.plan = ctx->tile_plan.as<TileEmit>();
-    a.agg = ctx->blk_agg.as<BlockAgg>();
+    a.lb = ctx->lb_slots.as<LbSlot>();
+    if (++ctx->lb_epoch >= (1u << 30)) {  // the status words hold 30 epoch bits: start over
+        cudaMemset(ctx->lb_slots.p, 0, ctx->lb_slots.cap);
+        ctx->lb_epoch = 1;
+    }
+    a.epoch = ctx->lb_epoch;
     a.bases = ctx->tensor_bases.as<TensorBase>();
     a.tensor_first_tile = ctx->tensor_first_tile.as<uint32_t>();
     a.entry_begin = ctx->entry_begin.as<unsigned long long>();
@@ -529,7 +535,14 @@ static int prepare_scan(delta_ctx *ctx) {
     const uint32_t lanes_per_tile = kTileBytes / ctx->width;
     GROW(ctx->meta, (size_t)nt * sizeof(TileMeta));
     GROW(ctx->tile_plan, (size_t)nt * sizeof(TileEmit));
-    GROW(ctx->blk_agg, (size_t)std::max<uint32_t>(nblk, 1) * sizeof(BlockAgg));
+    {
+        void *old = ctx->lb_slots.p;
+        GROW(ctx->lb_slots, (size_t)std::max<uint32_t>(nblk, 1) * sizeof(LbSlot));
+        if (ctx->lb_slots.p != old) {  // fresh slots: no status word may carry a live epoch
+            CK(cudaMemset(ctx->lb_slots.p, 0, ctx->lb_slots.cap), "memset");
+            ctx->lb_epoch = 0;
+        }
+    }
     GROW(ctx->tensor_bases, (size_t)std::max<uint32_t>(T, 1) * sizeof(TensorBase));
     GROW(ctx->entry_begin, (size_t)(T + 1) * 8);
     GROW(ctx->tensor_byte_begin, (size_t)(T + 1) * 8);

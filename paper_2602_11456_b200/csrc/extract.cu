@@ -1,24 +1,21 @@
 // extract.cu — sm_100a kernels for delta extraction.
 //
-//   K1  k_scan_tiles    E2+E3: the only kernel that reads the 2W bytes of weights.  One
-//                       CTA per tile (16 Ki 16-bit lanes = 32 KiB of old + 32 KiB of new),
-//                       16-byte streaming loads, bitwise lane compare, per-vector change
-//                       masks, one packed block scan for the ranks, ordered compaction
-//                       straight into the tile's workspace slot (u16 lane offsets + raw
-//                       values) and the tile's change count.  No inter-CTA communication
-//                       and no shared-memory staging: a pure streaming pass.
-//                       From the tile's change bitmap (shared memory) K1 also derives the
-//                       first / last changed lane and the LEB128 bytes of the gaps inside the
-//                       tile (< 2^14 lanes: 1-2 bytes each).
-//   K2  k_tiles_reduce / k_blocks_scan / k_tiles_bytes / k_tiles_place
-//                       E3+E4+E5 sizes: scans over the (small) per-tile metadata — entry
-//                       prefix, nearest earlier non-empty tile (its last change is the
-//                       predecessor of the tile's first change), each tile's
-//                       LEB128 bytes, byte prefix, per-tensor entry/byte begins.
-//   K3  k_finalize      E6: record sizes and offsets (the offset table), body size.
-//   K4  k_emit_tiles    E5+E6: one warp per tile writes the LEB128 bytes of the first gap
-//                       and of the in-tile gaps (ballot-placed, 32 at a time) and copies the
-//                       raw values to their final offsets (FIXED: absolute indices instead).
+//   K1  k_scan_tiles    E2+E3(+E4/E5 inside a tile): the only kernel that reads the 2W bytes
+//                       of weights.  One CTA per tile (16 Ki 16-bit lanes = 32 KiB of old +
+//                       32 KiB of new), 16-byte streaming loads, bitwise lane compare, a change
+//                       bitmap in shared memory, one packed block scan for the ranks, ordered
+//                       compaction straight into the tile's workspace slot: the LEB128 bytes of
+//                       the gaps inside the tile (< 2^14 lanes: 1-2 bytes each; FIXED: u16 lane
+//                       offsets) and the raw new values; per tile its count, first / last
+//                       changed lane and in-tile LEB128 bytes.
+//   K2  k_tiles_scan    E3+E4+E5 sizes + E6 table, one launch: per block of 1024 tiles an
+//                       aggregate, folded in order across blocks (published aggregates), then
+//                       per tile its entry / byte prefix and first gap (the predecessor of the
+//                       tile's first change is the last change before it in its tensor,
+//                       PAPER.md:389) -> K4's plan; the last CTA writes the offset table (K3).
+//   K4  k_emit_ring     E5+E6: one warp per tile: the first gap's LEB128 bytes, then the in-tile
+//                       bytes and the values copied from the slot to their final offsets
+//                       through a cp.async shared-memory ring.  k_emit_fixed: FIXED codec.
 //   K5  k_headers       E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
 //
 // Product code written for this library; none of it is shared with the test oracle.
@@ -488,14 +485,7 @@ cudaError_t launch_slots_regrow(const TileMeta *meta, uint32_t ntiles, int width
     return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------------------ K2 / K3
-// The tile-level prefixes in two launches over blocks of kTileBlock tiles (256 threads x 4
-// tiles): K2a reduces each block (entries, LEB128 bytes but the block's first non-empty
-// tile's first gap, first / last non-empty tile) and its last CTA to finish (ticket after a
-// fence) scans the block aggregates into block prefixes — no single-CTA scan launch sits
-// between the two; K2b places every tile (entry and byte prefix, first gap) into K4's plan,
-// records each tensor's E_k / B_k at its first tile, and its last CTA writes the offset table
-// (K3: record sizes and offsets, PAPER.md:382 + SPEC.md:148) and the per-tensor emit bases.
+// ------------------------------------------------------------------------------ K2 / K3 helpers
 
 // Absolute lane index (within its fused tensor) of the last change of non-empty tile p, if p
 // is in tensor k; otherwise 0 — the tile after it then starts its tensor's gap chain with the
@@ -560,12 +550,73 @@ __device__ __forceinline__ void block_scan_sum_max(unsigned long long x, long lo
     ktot = tk;
 }
 
+// ------------------------------------------------------------------------------ K2 / K3
+// The tile-level prefixes and the offset table in ONE launch.  Each block of kTileBlock tiles publishes its aggregate
+// (entries, LEB128 bytes but its first tile's first gap, first / last change as (lane index,
+// tensor)) with a status word, then folds the aggregates of ALL its predecessors in order —
+// 256 threads in parallel, an ordered shuffle tree, one CTA-wide step — into its exclusive
+// prefix.  Between two blocks the first gap of the later one's first change is the LEB128
+// length of its distance to the earlier one's last change when they share a tensor, else of
+// its lane index.  Every tile is then placed (entry and byte prefix, first gap g0:
+// K4's plan), each tensor's E_k / B_k recorded at its first tile, and the last CTA to finish
+// writes the offset table (K3: record sizes and offsets, PAPER.md:382 + SPEC.md:148) and the
+// per-tensor emit bases.  Block ids come from a ticket, so a block only waits for blocks that
+// started before it (no deadlock whatever the residency); status words carry the launch's
+// epoch, so the slots are never cleared between launches.
+__device__ __forceinline__ LbAgg lb_combine(const LbAgg &a, const LbAgg &b, int fixed) {
+    if (!a.any) return LbAgg{a.cnt + b.cnt, a.bytes + b.bytes, b.fabs, b.labs, b.fk, b.lk, b.any, 0};
+    if (!b.any) return LbAgg{a.cnt + b.cnt, a.bytes + b.bytes, a.fabs, a.labs, a.fk, a.lk, a.any, 0};
+    const unsigned long long gap = b.fabs - (a.lk == b.fk ? a.labs : 0ull);
+    return LbAgg{a.cnt + b.cnt, a.bytes + b.bytes + (fixed ? 0ull : (unsigned long long)leb_len(gap)), a.fabs, b.labs,
+                 a.fk, b.lk, 1u, 0};
+}
+__device__ __forceinline__ uint32_t lb_status(const LbSlot *s) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&s->status) : "memory");
+    return v;
+}
+__device__ __forceinline__ LbAgg lb_load(const LbSlot *s) {
+    const unsigned long long *q = reinterpret_cast<const unsigned long long *>(&s->agg);
+    LbAgg x;
+    unsigned long long *o = reinterpret_cast<unsigned long long *>(&x);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(LbAgg) / 8); ++i) o[i] = __ldcg(q + i);
+    return x;
+}
+__device__ __forceinline__ LbAgg lb_shfl_down(const LbAgg &v, int off) {
+    LbAgg x;
+    const unsigned long long *i = reinterpret_cast<const unsigned long long *>(&v);
+    unsigned long long *o = reinterpret_cast<unsigned long long *>(&x);
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(LbAgg) / 8); ++k) o[k] = __shfl_down_sync(0xffffffffu, i[k], off);
+    return x;
+}
+__device__ __forceinline__ void lb_publish(LbSlot *s, const LbAgg &x, uint32_t epoch) {
+    s->agg = x;
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&s->status), "r"((epoch << 2) | 1u) : "memory");
+}
+
 __global__ void __launch_bounds__(kTileThreads)
-k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t nblk,
-            BlockAgg *__restrict__ agg, const unsigned long long *__restrict__ numel, int fixed,
-            ExtractSummary *summary) {
-    if (summary->overflow) return;
-    const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
+k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t nblk,
+             LbSlot *__restrict__ lb, uint32_t epoch, TileEmit *__restrict__ plan, unsigned long long *__restrict__ E,
+             unsigned long long *__restrict__ Bk, uint32_t T, const uint32_t *__restrict__ name_len,
+             const unsigned long long *__restrict__ numel, RecordRow *__restrict__ table,
+             TensorBase *__restrict__ bases, int width, int fixed, ExtractSummary *summary,
+             unsigned long long *size_out) {
+    if (summary->overflow) {
+        if (size_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *size_out = ~0ull;
+        return;
+    }
+    __shared__ uint32_t s_b;
+    __shared__ LbAgg s_excl;
+    __shared__ long long s_first;
+    __shared__ unsigned long long s_bytes[kTileThreads / 32];
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_b = atomicAdd(&summary->lb_ticket, 1ull);
+    __syncthreads();
+    const uint32_t b = s_b;
+    const uint32_t t0 = b * kTileBlock + threadIdx.x * 4;
     TileMeta mt[4];
     unsigned long long c = 0;
     long long klast = -1, kfirst = -1;
@@ -581,116 +632,72 @@ k_tiles_agg(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ met
     unsigned long long cex, ctot;
     long long kex, ktot;
     block_scan_sum_max(c, klast, cex, ctot, kex, ktot);
-    unsigned long long b = 0;
+    // this thread's tiles: LEB128 bytes with the predecessor inside the block where there is one
+    const long long kex_in = kex;
+    unsigned long long bloc = 0;
+    {
+        long long kp = kex;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const uint32_t t = t0 + e;
-        if (t >= ntiles || !mt[e].count) continue;
-        unsigned long long g0;
-        if (kex >= 0 || fixed) b += tile_bytes(tiles[t], mt[e], tiles, meta, kex, numel, fixed, g0);
-        else b += mt[e].internal_bytes;  // the block's first non-empty tile: first gap in K2b
-        kex = t;
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t t = t0 + e;
+            if (t >= ntiles || !mt[e].count) continue;
+            unsigned long long g0;
+            if (kp >= 0 || fixed) bloc += tile_bytes(tiles[t], mt[e], tiles, meta, kp, numel, fixed, g0);
+            else bloc += mt[e].internal_bytes;  // the block's first non-empty tile: its first gap after the fold
+            kp = t;
+        }
     }
-    const unsigned long long bs = warp_sum(b);
+    const unsigned long long bsum = warp_sum(bloc);
     const long long kf = -warp_max(kfirst < 0 ? -(long long)0x7FFFFFFFFFFFFFFF : -kfirst);
-    __shared__ unsigned long long s_b[kTileThreads / 32];
-    __shared__ long long s_f[kTileThreads / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        s_b[warp] = bs;
-        s_f[warp] = kf;
-    }
+    if (lane == 0) s_bytes[warp] = bsum;
+    if (threadIdx.x == 0) s_first = 0x7FFFFFFFFFFFFFFF;
     __syncthreads();
+    if (lane == 0) atomicMin(&s_first, kf);
+    __syncthreads();
+    // ---- publish the block's aggregate, then fold every predecessor's (all threads)
     if (threadIdx.x == 0) {
-        unsigned long long tb = 0;
-        long long f = 0x7FFFFFFFFFFFFFFF;
-        for (int w = 0; w < kTileThreads / 32; ++w) {
-            tb += s_b[w];
-            f = s_f[w] < f ? s_f[w] : f;
-        }
-        agg[blockIdx.x] = BlockAgg{ctot, tb, f == 0x7FFFFFFFFFFFFFFF ? -1 : f, ktot, 0, 0, -1, 0};
-    }
-    // ---- the last CTA to finish (ticket after a fence) scans the block aggregates once:
-    // every block's entry / byte prefix and the last non-empty tile before it (the first gap
-    // of the block's first non-empty tile needs that tile)
-    __shared__ bool s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&summary->blocks_done, 1ull) == nblk - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    unsigned long long ecarry = 0, bcarry = 0;
-    long long pcarry = -1;
-    for (uint32_t j0 = 0; j0 < nblk; j0 += kTileThreads) {
-        const uint32_t j = j0 + threadIdx.x;
-        BlockAgg a{0, 0, -1, -1, 0, 0, -1, 0};
-        if (j < nblk) {
-            a.cnt = __ldcg(&agg[j].cnt);
-            a.bytes = __ldcg(&agg[j].bytes);
-            a.first = __ldcg(&agg[j].first);
-            a.last = __ldcg(&agg[j].last);
-        }
-        unsigned long long cex2, ctot2;
-        long long pex, ptot;
-        block_scan_sum_max(a.cnt, a.last, cex2, ctot2, pex, ptot);
-        if (pcarry > pex) pex = pcarry;
-        unsigned long long fb = 0, g0;  // the first gap of the block's first non-empty tile
-        if (a.first >= 0 && !fixed) {
-            const TileMeta m = meta[a.first];
-            fb = tile_bytes(tiles[a.first], m, tiles, meta, pex, numel, 0, g0) - m.internal_bytes;
-        }
-        unsigned long long bex, btot;
-        long long d0, d1;
-        block_scan_sum_max(a.bytes + fb, -1, bex, btot, d0, d1);
-        if (j < nblk) {
-            agg[j].e0 = ecarry + cex2;
-            agg[j].b0 = bcarry + bex;
-            agg[j].p0 = pex;
-        }
-        ecarry += ctot2;
-        bcarry += btot;
-        if (ptot > pcarry) pcarry = ptot;
-    }
-    if (threadIdx.x == 0) summary->blocks_done = 0;  // K2b's tickets start from zero
-}
-
-__global__ void __launch_bounds__(kTileThreads)
-k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles,
-               uint32_t nblk, const BlockAgg *__restrict__ agg, TileEmit *__restrict__ plan,
-               unsigned long long *__restrict__ E, unsigned long long *__restrict__ Bk, uint32_t T,
-               const uint32_t *__restrict__ name_len, const unsigned long long *__restrict__ numel,
-               RecordRow *__restrict__ table, TensorBase *__restrict__ bases, int width, int fixed,
-               ExtractSummary *summary, unsigned long long *size_out) {
-    if (summary->overflow) {
-        if (size_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *size_out = ~0ull;
-        return;
-    }
-    __shared__ unsigned long long s_e0, s_b0;
-    __shared__ long long s_p0;
-    __shared__ bool s_last;
-    // ---- this block's entry / byte prefix and the last non-empty tile before it (K2a's last CTA)
-    if (threadIdx.x == 0) {
-        s_e0 = agg[blockIdx.x].e0;
-        s_b0 = agg[blockIdx.x].b0;
-        s_p0 = agg[blockIdx.x].p0;
-    }
-    __syncthreads();
-    // ---- the block's tiles
-    const uint32_t t0 = blockIdx.x * kTileBlock + threadIdx.x * 4;
-    TileMeta mt[4];
-    unsigned long long c = 0;
-    long long klast = -1;
+        LbAgg agg{ctot, 0, 0, 0, 0, 0, ctot ? 1u : 0u, 0};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        mt[e] = t0 + e < ntiles ? meta[t0 + e] : TileMeta{0, 0, 0, 0, 0};
-        c += mt[e].count;
-        if (mt[e].count) klast = t0 + e;
+        for (int w = 0; w < kTileThreads / 32; ++w) agg.bytes += s_bytes[w];
+        if (ctot) {
+            const long long f = s_first;
+            const TileDesc df = tiles[f], dl = tiles[ktot];
+            agg.fabs = df.lane_base + meta[f].first_off;
+            agg.fk = df.flags_tensor & kTileTensorMask;
+            agg.labs = dl.lane_base + meta[ktot].last_off;
+            agg.lk = dl.flags_tensor & kTileTensorMask;
+        }
+        lb_publish(lb + b, agg, epoch);
     }
-    unsigned long long cex, ctot;
-    long long kex, ktot;
-    block_scan_sum_max(c, klast, cex, ctot, kex, ktot);
-    if (kex < 0) kex = s_p0;
+    {
+        // thread i folds predecessors [i*c, (i+1)*c) in order once each is published, then an
+        // ordered tree over the lanes (older lanes first) and over the warps
+        const uint32_t c = (b + kTileThreads - 1) / kTileThreads;
+        LbAgg v{0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t j = threadIdx.x * c; j < min(b, (threadIdx.x + 1) * c); ++j) {
+            while ((lb_status(lb + j) >> 2) != epoch) {
+            }
+            v = lb_combine(v, lb_load(lb + j), fixed);
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const LbAgg o = lb_shfl_down(v, off);
+            if (lane + off < 32) v = lb_combine(v, o, fixed);
+        }
+        __shared__ LbAgg s_w[kTileThreads / 32];
+        if (lane == 0) s_w[warp] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            LbAgg e = s_w[0];
+#pragma unroll
+            for (int w = 1; w < kTileThreads / 32; ++w) e = lb_combine(e, s_w[w], fixed);
+            s_excl = e;
+        }
+    }
+    __syncthreads();
+    const LbAgg ex = s_excl;
+    // ---- place the block's tiles
+    long long kp = kex_in;
     unsigned long long bt[4], g0[4], mine = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -698,14 +705,22 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
         g0[e] = 0;
         const uint32_t t = t0 + e;
         if (t >= ntiles || !mt[e].count) continue;
-        bt[e] = tile_bytes(tiles[t], mt[e], tiles, meta, kex, numel, fixed, g0[e]);
+        const TileDesc d = tiles[t];
+        if (kp >= 0 || fixed) {
+            bt[e] = tile_bytes(d, mt[e], tiles, meta, kp, numel, fixed, g0[e]);
+        } else {  // the predecessor is the last change before the block (or none)
+            const uint32_t k = d.flags_tensor & kTileTensorMask;
+            g0[e] = d.lane_base + mt[e].first_off - ((ex.any && ex.lk == k) ? ex.labs : 0ull);
+            bt[e] = mt[e].internal_bytes + leb_len(g0[e]);
+        }
         mine += bt[e];
-        kex = t;
+        kp = t;
     }
     unsigned long long bex, btot;
     long long d0, d1;
     block_scan_sum_max(mine, -1, bex, btot, d0, d1);
-    unsigned long long ent = s_e0 + cex, byt = s_b0 + bex;
+    unsigned long long ent = ex.cnt + cex;
+    unsigned long long byt = (ex.any ? ex.bytes + (fixed ? 0ull : (unsigned long long)leb_len(ex.fabs)) : ex.bytes) + bex;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const uint32_t t = t0 + e;
@@ -731,8 +746,8 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
     if (!s_last) return;
     __threadfence();
     unsigned long long carry = 0;
-    for (uint32_t b = 0; b < T; b += kTileThreads) {
-        const uint32_t k = b + threadIdx.x;
+    for (uint32_t b0 = 0; b0 < T; b0 += kTileThreads) {
+        const uint32_t k = b0 + threadIdx.x;
         unsigned long long rb = 0, nnz = 0, ilen = 0, ek = 0, bk = 0;
         if (k < T) {
             ek = __ldcg(E + k);
@@ -741,12 +756,12 @@ k_tiles_prefix(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ 
             ilen = __ldcg(Bk + k + 1) - bk;
             rb = 27ull + name_len[k] + ilen + (unsigned long long)width * nnz;
         }
-        unsigned long long ex, tot;
+        unsigned long long exs, tot;
         long long d2, d3;
-        block_scan_sum_max(rb, -1, ex, tot, d2, d3);
+        block_scan_sum_max(rb, -1, exs, tot, d2, d3);
         if (k < T) {
             RecordRow r;
-            r.record_offset = carry + ex;
+            r.record_offset = carry + exs;
             r.element_count = numel[k];
             r.nnz = nnz;
             r.index_offset = r.record_offset + 2 + name_len[k] + 24;
@@ -840,41 +855,8 @@ __device__ __forceinline__ void warp_copy16(uint8_t *dst, const uint8_t *src, ui
     }
 }
 
-// The loads of one warp_copy16 of at most kPref bytes, taken before the destination is known
-// (so K4 can issue a tile's loads one tile ahead): lane j holds source vector j, lanes 0-15 the
-// first 16 source bytes, lanes 16-31 the last 16.  pref_store writes them to any destination.
+// Tiles whose in-tile bytes and values each fit kPref bytes go through K4's shared-memory ring.
 constexpr uint32_t kPref = 496;
-struct Pref16 {
-    uint4 a;         // source vector `lane` (vectors 0 .. n / 16)
-    uint32_t hb, tb; // lanes 0-15: src[lane]; lanes 16-31: src[n - 32 + lane]
-};
-__device__ __forceinline__ void pref_load(Pref16 &p, const uint8_t *src, uint32_t n, int lane) {
-    const uint4 *s16 = reinterpret_cast<const uint4 *>(src);
-    p.a = (uint32_t)lane <= (n >> 4) ? __ldg(s16 + lane) : make_uint4(0, 0, 0, 0);
-    p.hb = (lane < 16 && (uint32_t)lane < n) ? src[lane] : 0u;
-    p.tb = (lane >= 16 && n + lane >= 32) ? src[n + lane - 32] : 0u;
-}
-__device__ __forceinline__ void pref_store(const Pref16 &p, uint8_t *dst, uint32_t n, int lane) {
-    const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
-    const uint32_t rest = n - head, nv = rest >> 4, tail = rest & 15u;
-    // tail byte k (lane 16 + k) = src[n - tail + k], held by lane 32 - tail + k
-    const uint32_t tbyte = __shfl_sync(0xffffffffu, p.tb, (32u - tail + (uint32_t)lane - 16u) & 31u);
-    const uint4 b = make_uint4(__shfl_down_sync(0xffffffffu, p.a.x, 1), __shfl_down_sync(0xffffffffu, p.a.y, 1),
-                               __shfl_down_sync(0xffffffffu, p.a.z, 1), __shfl_down_sync(0xffffffffu, p.a.w, 1));
-    if ((uint32_t)lane < head) dst[lane] = (uint8_t)p.hb;
-    if (lane >= 16 && (uint32_t)(lane - 16) < tail) dst[head + 16u * nv + (uint32_t)(lane - 16)] = (uint8_t)tbyte;
-    if ((uint32_t)lane < nv) {
-        const uint32_t qv = head >> 2, sh = 8u * (head & 3u);
-        uint32_t w0, w1, w2, w3, w4;
-        if (qv == 0) { w0 = p.a.x; w1 = p.a.y; w2 = p.a.z; w3 = p.a.w; w4 = b.x; }
-        else if (qv == 1) { w0 = p.a.y; w1 = p.a.z; w2 = p.a.w; w3 = b.x; w4 = b.y; }
-        else if (qv == 2) { w0 = p.a.z; w1 = p.a.w; w2 = b.x; w3 = b.y; w4 = b.z; }
-        else { w0 = p.a.w; w1 = b.x; w2 = b.y; w3 = b.z; w4 = b.w; }
-        reinterpret_cast<uint4 *>(dst + head)[lane] =
-            make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
-                       __funnelshift_r(w3, w4, sh));
-    }
-}
 
 // The emit gate (K4/K5): the local body is written iff every tile fitted its slot and the body
 // fits `cap`; the fused-assembly copy (peer.base) iff, in addition, no rank's size is ~0 (its
@@ -901,13 +883,11 @@ __device__ __forceinline__ EmitGate emit_gate(const ExtractSummary *summary, uns
     return g;
 }
 
-// One warp per tile.  LEB128 codec: K1 left the tile's in-tile gaps already encoded in its
-// slot, so the warp writes the first gap's bytes (one lane per byte), then copies the in-tile
-// bytes and the raw values to their final offsets — two warp-wide copies, no per-entry work.
-// FIXED (reading R18): absolute indices lane_base + offset as u32 / u64, via shared memory.
-template <int W, bool FIXED>
+// FIXED codec K4 (reading R18): one warp per tile, absolute indices lane_base + offset as u32 /
+// u64 built in shared memory, then the values.
+template <int W>
 __global__ void __launch_bounds__(256, 3)
-k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
+k_emit_fixed(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
              const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
              uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
     const EmitGate gate = emit_gate(summary, cap, peer);
@@ -916,7 +896,7 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
     const int lane = threadIdx.x & 31;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    if constexpr (FIXED) {
+    {
         __shared__ __align__(16) unsigned long long s_fix[8 * 256 + 2];
         for (uint32_t t = wg; t < ntiles; t += nw) {
             const TileEmit pe = plan[t];
@@ -926,7 +906,7 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
             uint8_t *ib = out + (tb.ib + pe.ib);
             uint8_t *vb = out + (tb.vb + pe.eb * W);
             const uint8_t *sv = reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap);
-            const uint32_t iw = pe.count_internal >> 16;  // the index width (set by K2b for FIXED)
+            const uint32_t iw = pe.count_internal >> 16;  // the index width (set by K2 for FIXED)
             const uint16_t *so = reinterpret_cast<const uint16_t *>(slot_bytes + (size_t)t * 2 * slot_cap);
             unsigned long long *buf = s_fix + 256 * (threadIdx.x >> 5);
             uint8_t *dst = ib, *pdst = pout ? pout + (ib - out) : nullptr;
@@ -951,26 +931,116 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
         }
         return;
     }
-    // LEB128: per tile the first-gap bytes (one lane per byte) and two warp-wide 16-byte copies
-    // (in-tile bytes, values).  Software pipeline over the warp's tiles: plans two tiles ahead,
-    // a tile's slot bytes one tile ahead (they do not depend on where they go), so the stores
-    // of tile t overlap the loads of the next; larger tiles take synchronous copies.
+}
+
+// LEB128 K4 with a shared-memory ring: each warp keeps S tiles' slot bytes in flight through
+// cp.async (LDGSTS, no registers held), plans 2S tiles ahead, so a tile's DRAM latency overlaps
+// the stores of the S - 1 tiles before it (a register prefetch held one and ran 0.21 ms vs
+// 0.15 ms at M3; 1-D TMA bulk copies per tile, 0.24 ms, were slower still).  Per
+// warp and stage: 512 + 512 bytes of data (in-tile LEB128 bytes, values), the tensor's emit
+// bases; per warp 2S plans.  Tiles with a segment > kPref bytes take the synchronous copies.
+constexpr uint32_t kRingData = 1024;
+template <int S>
+__host__ __device__ constexpr uint32_t ring_warp_bytes() { return S * (kRingData + 16) + 2 * S * 32; }
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+// zero-fill form: src_bytes = 0 reads nothing and writes 16 zero bytes (no branch around it)
+__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *g, bool on) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(on ? 16u : 0u) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// n <= kPref bytes staged at s (16-byte aligned shared memory, vectors 0 .. n / 16 valid) to
+// any destination: head bytes (lanes 0-15), 16-byte vectors funnel-shifted from two staged
+// vectors, tail bytes (lanes 16-31) — the same split as warp_copy16.
+template <int QV>
+__device__ __forceinline__ void ring_vec(const uint8_t *s, uint8_t *dst, uint32_t head, uint32_t sh, int lane) {
+    const uint4 *s16 = reinterpret_cast<const uint4 *>(s);
+    const uint4 a = s16[lane], b = s16[lane + 1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    reinterpret_cast<uint4 *>(dst + head)[lane] =
+        make_uint4(__funnelshift_r(w[QV], w[QV + 1], sh), __funnelshift_r(w[QV + 1], w[QV + 2], sh),
+                   __funnelshift_r(w[QV + 2], w[QV + 3], sh), __funnelshift_r(w[QV + 3], w[QV + 4], sh));
+}
+__device__ __forceinline__ void ring_store(const uint8_t *s, uint8_t *dst, uint32_t n, int lane) {
+    const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
+    const uint32_t rest = n - head, nv = rest >> 4, tail = rest & 15u;
+    // head bytes on lanes 0-15, tail bytes on lanes 16-31: one predicated byte copy
+    const uint32_t bpos = lane < 16 ? (uint32_t)lane : head + 16u * nv + (uint32_t)(lane - 16);
+    if (lane < 16 ? (uint32_t)lane < head : (uint32_t)(lane - 16) < tail) dst[bpos] = s[bpos];
+    if ((uint32_t)lane < nv) {  // the word offset head / 4 is warp-uniform: one branch, no selects
+        const uint32_t sh = 8u * (head & 3u);
+        switch (head >> 2) {
+        case 0: ring_vec<0>(s, dst, head, sh, lane); break;
+        case 1: ring_vec<1>(s, dst, head, sh, lane); break;
+        case 2: ring_vec<2>(s, dst, head, sh, lane); break;
+        default: ring_vec<3>(s, dst, head, sh, lane); break;
+        }
+    }
+}
+
+template <int W, int S>
+__global__ void __launch_bounds__(256)
+k_emit_ring(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
+            const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
+            uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
+    const EmitGate gate = emit_gate(summary, cap, peer);
+    if (!gate.local) return;  // emit gate (async extract)
+    uint8_t *const pout = gate.peer ? peer.base + gate.off : nullptr;  // fused assembly: the same bytes there too
+    extern __shared__ __align__(16) uint8_t s_ring[];
+    const int lane = threadIdx.x & 31;
+    uint8_t *const sdata = s_ring + (threadIdx.x >> 5) * ring_warp_bytes<S>();
+    TensorBase *const sbase = reinterpret_cast<TensorBase *>(sdata + S * kRingData);
+    TileEmit *const splan = reinterpret_cast<TileEmit *>(sdata + S * (kRingData + 16));
+    const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    const uint32_t mine = wg < ntiles ? (ntiles - wg + nw - 1) / nw : 0;  // tiles of this warp: wg + m nw
     auto slot_i = [&](uint32_t t) { return slot_bytes + (size_t)t * 2 * slot_cap; };
     auto slot_v = [&](uint32_t t) { return reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap); };
     auto fast = [&](const TileEmit &p) {
         return (p.count_internal >> 16) <= kPref && (p.count_internal & 0xFFFFu) * W <= kPref;
     };
-    // one pipeline step for tile t: issue the loads of tile t + nw (plan pn, into dn), store
-    // tile t (plan pc, data dc), then load the plan of tile t + 2 nw into pc.  Unrolled by two
-    // over fixed (A, B) slots so no registers rotate.
-    auto step = [&](uint32_t t, TileEmit &pc, const TileEmit &pn, Pref16 &ci, Pref16 &cv, Pref16 &ni_, Pref16 &nv_) {
-        if (t + nw < ntiles && fast(pn)) {
-            pref_load(ni_, slot_i(t + nw), pn.count_internal >> 16, lane);
-            pref_load(nv_, slot_v(t + nw), (pn.count_internal & 0xFFFFu) * W, lane);
-        }
+    auto issue_plan = [&](uint32_t m) {  // plan of the warp's m-th tile -> plan slot m % 2S
+        if (m < mine && lane < 2)
+            cp_async16(reinterpret_cast<uint8_t *>(splan + m % (2 * S)) + 16 * lane,
+                       reinterpret_cast<const uint8_t *>(plan + (wg + m * nw)) + 16 * lane);
+    };
+    auto issue_data = [&](uint32_t m) {  // its slot bytes and emit bases -> stage m % S (plan m landed)
+        if (m >= mine) return;
+        const TileEmit p = splan[m % (2 * S)];
+        const uint32_t count = p.count_internal & 0xFFFFu, ni = p.count_internal >> 16, nv = count * W;
+        if (count == 0 || !fast(p)) return;
+        const uint32_t t = wg + m * nw;
+        uint8_t *d = sdata + (m % S) * kRingData;
+        cp_async16_zfill(d + 16 * lane, slot_i(t) + 16 * lane, (uint32_t)lane <= (ni >> 4));
+        cp_async16_zfill(d + 512 + 16 * lane, slot_v(t) + 16 * lane, (uint32_t)lane <= (nv >> 4));
+        if (lane == 0) cp_async16(sbase + m % S, bases + p.k);
+    };
+    for (uint32_t m = 0; m < 2 * S - 1; ++m) issue_plan(m);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    for (uint32_t m = 0; m < S - 1; ++m) {
+        issue_data(m);
+        cp_async_commit();
+    }
+    for (uint32_t n = 0; n < mine; ++n) {
+        issue_plan(n + 2 * S - 1);  // into the slot of tile n - 1 (stored last iteration)
+        issue_data(n + S - 1);      // into the stage of tile n - 1
+        cp_async_commit();
+        cp_async_wait<S - 1>();     // tile n's group (and the plan of n + S) landed
+        __syncwarp();
+        const TileEmit pc = splan[n % (2 * S)];
         const uint32_t count = pc.count_internal & 0xFFFFu;
         if (count) {
-            const TensorBase tb = bases[pc.k];
+            const bool f = fast(pc);
+            const TensorBase tb = f ? sbase[n % S] : bases[pc.k];
             uint8_t *ib = out + (tb.ib + pc.ib);
             uint8_t *vb = out + (tb.vb + pc.eb * W);
             // the first gap: byte n = 7-bit group n, continuation bit on all but the last
@@ -978,33 +1048,24 @@ k_emit_tiles(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
             const uint32_t L0 = leb_len(g);
             const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
             const uint32_t ni = pc.count_internal >> 16, nv = count * W;
-            const bool f = fast(pc);
-            for (int d = 0; d < (pout ? 2 : 1); ++d) {  // d = 1: fused assembly, the same bytes at
-                uint8_t *di = d ? pout + (ib - out) : ib;   // their global offsets (NVLink stores)
+            const uint8_t *sd = sdata + (n % S) * kRingData;
+            const uint32_t t = wg + n * nw;
+            for (int d = 0; d < (pout ? 2 : 1); ++d) {  // d = 1: fused assembly (NVLink stores)
+                uint8_t *di = d ? pout + (ib - out) : ib;
                 uint8_t *dv = d ? pout + (vb - out) : vb;
                 if ((uint32_t)lane < L0) di[lane] = g_byte;
                 if (f) {
-                    pref_store(ci, di + L0, ni, lane);
-                    pref_store(cv, dv, nv, lane);
+                    ring_store(sd, di + L0, ni, lane);
+                    ring_store(sd + 512, dv, nv, lane);
                 } else {  // a dense tile: synchronous copies
                     warp_copy16(di + L0, slot_i(t), ni, lane);
                     warp_copy16(dv, slot_v(t), nv, lane);
                 }
             }
         }
-        pc = t + 2 * nw < ntiles ? plan[t + 2 * nw] : TileEmit{0, 0, 0, 0, 0};
-    };
-    TileEmit pa = wg < ntiles ? plan[wg] : TileEmit{0, 0, 0, 0, 0};
-    TileEmit pb = wg + nw < ntiles ? plan[wg + nw] : TileEmit{0, 0, 0, 0, 0};
-    Pref16 ai, av, bi, bv;
-    if (wg < ntiles && fast(pa)) {
-        pref_load(ai, slot_i(wg), pa.count_internal >> 16, lane);
-        pref_load(av, slot_v(wg), (pa.count_internal & 0xFFFFu) * W, lane);
+        __syncwarp();  // stage n % S and plan slot n % 2S are refilled from the next iterations
     }
-    for (uint32_t t = wg; t < ntiles; t += 2 * nw) {
-        step(t, pa, pb, ai, av, bi, bv);
-        if (t + nw < ntiles) step(t + nw, pb, pa, bi, bv, ai, av);
-    }
+    cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------------ K5
@@ -1070,18 +1131,26 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
                                       static_cast<LT *>(a.slot_val), a.meta, a.summary, a.redo_cap, dense_tile);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t nblk = (a.ntiles + kTileBlock - 1) / kTileBlock;
-    if (nblk) {
-        k_tiles_agg<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.numel, a.index_codec,
-                                                  a.summary);
-        if (ev) cudaEventRecord(ev[2], s);
-        k_tiles_prefix<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.agg, a.plan, a.entry_begin,
-                                             a.tensor_byte_begin, a.ntensors, a.name_len, a.numel, a.table, a.bases,
-                                             a.width, a.index_codec, a.summary, a.scan_size_out);
-    } else if (ev) {
-        cudaEventRecord(ev[2], s);
-    }
+    if (nblk)
+        k_tiles_scan<<<nblk, kTileThreads, 0, s>>>(a.tiles, a.meta, a.ntiles, nblk, a.lb, a.epoch, a.plan,
+                                                   a.entry_begin, a.tensor_byte_begin, a.ntensors, a.name_len,
+                                                   a.numel, a.table, a.bases, a.width, a.index_codec, a.summary,
+                                                   a.scan_size_out);
+    if (ev) cudaEventRecord(ev[2], s);
     if (ev) cudaEventRecord(ev[3], s);
     return cudaGetLastError();
+}
+
+// K4's ring depth: 2 stages (measured: 3, 4, 6, 8 no faster, more shared memory per CTA)
+constexpr int kEmitStages = 2;
+
+template <int W>
+static void launch_ring(const ExtractArgs &a, uint8_t *out, cudaStream_t s) {
+    constexpr uint32_t smem = 8 * ring_warp_bytes<kEmitStages>();
+    static_assert(smem <= 48 * 1024, "K4 ring fits the default dynamic shared memory limit");
+    k_emit_ring<W, kEmitStages><<<a.persist_ctas, 256, smem, s>>>(
+        a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<const typename LaneOf<W>::T *>(a.slot_val),
+        out, a.summary, a.out_cap, a.peer);
 }
 
 template <int W>
@@ -1089,13 +1158,11 @@ static cudaError_t emit_impl(const ExtractArgs &a, uint8_t *out, cudaStream_t s,
     using LT = typename LaneOf<W>::T;
     if (ev) cudaEventRecord(ev[0], s);
     if (a.index_codec)
-        k_emit_tiles<W, true><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
-                                                            static_cast<const LT *>(a.slot_val), out, a.summary,
-                                                            a.out_cap, a.peer);
+        k_emit_fixed<W><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
+                                                       static_cast<const LT *>(a.slot_val), out, a.summary, a.out_cap,
+                                                       a.peer);
     else
-        k_emit_tiles<W, false><<<a.persist_ctas, 256, 0, s>>>(a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes,
-                                                             static_cast<const LT *>(a.slot_val), out, a.summary,
-                                                             a.out_cap, a.peer);
+        launch_ring<W>(a, out, s);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t hb = a.ntensors < 65535u ? (a.ntensors ? a.ntensors : 1u) : 65535u;
     k_headers<<<hb, 128, 0, s>>>(a.table, a.ntensors, a.name_len, a.name_off, a.names, out, a.mode, a.summary,

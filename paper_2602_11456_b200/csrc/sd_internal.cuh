@@ -12,7 +12,7 @@ constexpr int kScanVecs = 8;       // 16-byte vectors per thread per operand per
 constexpr int kTileBytes = kScanThreads * kScanVecs * 16;  // 32 KiB of old + 32 KiB of new
 // lanes per tile: 16384 (16-bit lanes) or 8192 (32-bit lanes) -> a lane offset fits a u16
 constexpr uint32_t kDenseTile = 4096;  // K1: tiles with this many changes (25 %) emit in vector order
-constexpr int kTileThreads = 256;  // threads of the tile-level scan kernels (K2a, K2b)
+constexpr int kTileThreads = 256;  // threads of the tile-level scan kernel (K2)
 constexpr int kTileBlock = kTileThreads * 4;  // tiles per block of the tile-level scans (4 per thread)
 constexpr int kByteChunk = 4096;   // index-stream bytes per A2/A4 chunk (256 threads x 16)
 constexpr int kHalo = 16;          // bytes before a chunk kept for varints that straddle it
@@ -34,7 +34,7 @@ static_assert(sizeof(TileDesc) == 32, "TileDesc is 32 bytes");
 
 // K1 output per tile: changed-lane count, lane offsets (within the tile) of the first and
 // last changed lane, and the LEB128 bytes of the gaps between consecutive changes inside
-// the tile (the first change's gap depends on earlier tiles and is added by K2b).
+// the tile (the first change's gap depends on earlier tiles and is added by K2).
 struct TileMeta {
     uint32_t count;
     uint16_t first_off, last_off;
@@ -43,7 +43,7 @@ struct TileMeta {
 };
 static_assert(sizeof(TileMeta) == 16, "TileMeta is 16 bytes");
 
-// K2b output per tile: everything K4 needs besides its tensor's bases, in one 32-byte load.
+// K2 output per tile: everything K4 needs besides its tensor's bases, in one 32-byte load.
 struct TileEmit {
     unsigned long long ib;   // LEB128 bytes of all tiles before this one (all tensors)
     unsigned long long eb;   // entries of all tiles before this one (all tensors)
@@ -51,16 +51,18 @@ struct TileEmit {
     uint32_t count_internal; // changes in the tile | in-tile gap bytes (FIXED: index width) << 16
     uint32_t k;              // tensor
 };
-// K2a output per block of kTileBlock tiles.
-struct BlockAgg {
-    unsigned long long cnt;    // entries in the block
-    unsigned long long bytes;  // LEB128 bytes, except the first gap of the block's first non-empty tile
-    long long first, last;     // first / last non-empty tile of the block, -1 if none
-    // written by K2a's last CTA: entries / LEB128 bytes before the block, last non-empty tile
-    // before it (-1: none)
-    unsigned long long e0, b0;
-    long long p0;
-    unsigned long long pad;
+// K2's cross-block fold: per block of tiles its aggregate, published with a status word.
+struct LbAgg {
+    unsigned long long cnt;    // entries
+    unsigned long long bytes;  // LEB128 bytes, except the first gap of the first non-empty tile
+    unsigned long long fabs, labs;  // first / last change: lane index within its tensor
+    uint32_t fk, lk;           // ... and its tensor
+    uint32_t any, pad;         // any change at all
+};
+struct LbSlot {
+    LbAgg agg;
+    uint32_t status;           // (launch epoch << 2) | 1 once agg is written
+    uint32_t pad[3];
 };
 
 // Per tensor (written with the offset table): body offset of a tile's first index byte =
@@ -77,7 +79,8 @@ struct ExtractSummary {
     unsigned long long max_count;   // largest per-tile count seen (sizes the slots on retry)
     unsigned long long idx_bytes;   // total LEB128 bytes over all tensors
     unsigned long long body_bytes;  // packed body size
-    unsigned long long blocks_done; // K2b tickets (the last CTA writes the offset table)
+    unsigned long long blocks_done; // K2 tickets (the last CTA writes the offset table)
+    unsigned long long lb_ticket;   // K2 logical block ids (look-back order)
 };
 
 // Sticky outcome of the delta_extract_async calls since the last delta_extract_wait (folded
@@ -147,7 +150,8 @@ struct ExtractArgs {
     void *slot_val;                   // ntiles x C lanes
     TileMeta *meta;                   // ntiles
     TileEmit *plan;                   // ntiles: K4's per-tile plan
-    BlockAgg *agg;                    // per tile block (kTileBlock tiles): K2a aggregates
+    LbSlot *lb = nullptr;             // per tile block: K2's published aggregates
+    uint32_t epoch = 0;               // K2 launch epoch (status words of older launches are stale)
     TensorBase *bases;                // ntensors: K4's per-tensor body bases
     const uint32_t *tensor_first_tile;  // ntensors
     unsigned long long *entry_begin;  // ntensors + 1 (E_k)
@@ -171,7 +175,7 @@ struct ExtractArgs {
     unsigned long long out_cap = ~0ull;
     unsigned long long *size_out = nullptr;
     ExtractSticky *sticky = nullptr;  // async extracts: outcome folded in by K5
-    unsigned long long *scan_size_out = nullptr;  // K2b: the body size, or ~0 if a tile overflowed
+    unsigned long long *scan_size_out = nullptr;  // K2: the body size, or ~0 if a tile overflowed
     PeerDst peer;                     // K4/K5: fused assembly destination
 };
 

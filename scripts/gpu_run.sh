@@ -7,6 +7,8 @@
 #   tests      pytest -m gpu, without the full-size configs
 #   fullsize   pytest tests/test_gpu_fullsize.py (every record of configs[1..4] vs the oracle)
 #   bench      bench.py N=1 (default flags) + the reference arm
+#   k4tune     bench.py over K4's CTAs per SM (K4_CTAS)
+#   k4full     ncu --set full of K4 on the full M3 step
 #   sweep      scripts/sweep.py: configs[0], [1], [4] (0.1/10/50 % uniform + rowblock)
 #   launches   ncu launch list of bench.py (gpu__time_duration, cold, serialised)
 #   traffic    ncu per-launch DRAM bytes + DRAM activity of the path's kernels at M3
@@ -34,6 +36,15 @@ for S in "$@"; do
   bench)
     timeout 900 python bench.py > $OUT/bench_n1.jsonl 2> $OUT/bench_n1.err; echo "bench rc=$?"; tail -1 $OUT/bench_n1.jsonl | cut -c1-400
     timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.jsonl 2> $OUT/bench_ref.err; echo "ref rc=$?";;
+  k4tune)  # K4 grid: CTAs per SM in K4_CTAS
+    for C in ${K4_CTAS:-8 16 24 32}; do
+      timeout 600 python bench.py --no-e2e --no-cpu-baseline --emit-ctas $C > $OUT/k4_c${C}.jsonl 2>/dev/null
+      echo "C=$C $(tail -1 $OUT/k4_c${C}.jsonl | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["kernel_ms_per_step"]["emit_ms"])' 2>&1 | cut -c1-200)"
+    done;;
+  k4full)  # ncu --set full of K4 on the full M3 step (one launch)
+    $BENCH_SMALL > $OUT/plain_k4.log 2>&1 && \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_emit" -c 1 -o $OUT/k4full \
+      python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks > $OUT/ncu_k4full.log 2>&1; echo "k4full rc=$?";;
   sweep)
     timeout 1800 python scripts/sweep.py > $OUT/sweep.jsonl 2> $OUT/sweep.err; echo "sweep rc=$?";;
   launches)
