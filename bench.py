@@ -359,10 +359,19 @@ def launch_ranks(args):
     if world is None:
         if args.gpus <= 1:
             return None
+        import random
         import socket
-        with socket.socket() as sk:
-            sk.bind(("127.0.0.1", 0))
-            port = sk.getsockname()[1]
+        # a free port BELOW the kernel's ephemeral range (32768+), so no socket the ranks or
+        # NCCL open in the meantime can be handed the same number
+        rng = random.Random(os.getpid() ^ int(time.time() * 1e6))
+        for _ in range(100):
+            port = rng.randrange(20000, 32000)
+            with socket.socket() as sk:
+                try:
+                    sk.bind(("127.0.0.1", port))
+                    break
+                except OSError:
+                    continue
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
         print(f"bench: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)

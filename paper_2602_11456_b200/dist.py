@@ -120,6 +120,25 @@ def _ipc_teardown(device, group):
     dist.barrier(group=group)
 
 
+def _map_root_buffers(bufs, rank: int, world: int, root: int, device, group):
+    """CUDA IPC: the root's buffers mapped into every other rank.  The root shares each buffer
+    once PER CONSUMER (every reduce_tensor call carries its own sent-data reference counter,
+    which exactly one consumer's rebuild releases), so after the consumers drop their mappings
+    the root's torch.cuda.ipc_collect() reclaims every share and no counter is left pending
+    at exit.  Returns the mapped tensors on non-root ranks, [] on the root."""
+    shared = ({r: [reduce_tensor(b) for b in bufs] for r in range(world) if r != root}
+              if rank == root else None)
+    handles = [None] * world
+    dist.all_gather_object(handles, shared, group=group)
+    peers = []
+    if rank != root:
+        for fn, args in handles[root][rank]:
+            args = list(args)
+            args[6] = torch.device(device).index  # rebuild on this process's device (peer mapping)
+            peers.append(fn(*args))
+    return peers
+
+
 class NvlinkAssembler:
     """S3 as one kernel over NVLink peer memory (delta_assemble): the root owns the
     assembled-body buffer ``buf``; every other rank maps it into its own address space with
@@ -138,15 +157,7 @@ class NvlinkAssembler:
         self.bufs = ([torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
                      if self.rank == root else [None] * nbuf)
         self.buf = self.bufs[0]
-        handles = [None] * self.world
-        dist.all_gather_object(handles, [reduce_tensor(b) for b in self.bufs] if self.rank == root else None,
-                               group=group)
-        self.peers = []
-        if self.rank != root:
-            for fn, args in handles[root]:
-                args = list(args)
-                args[6] = self.device.index  # rebuild on this process's device (peer mapping)
-                self.peers.append(fn(*args))
+        self.peers = _map_root_buffers(self.bufs, self.rank, self.world, root, self.device, group)
         self.peer = self.peers[0] if self.peers else None
         self.sizes = torch.zeros(self.world, dtype=torch.int64, device=self.device)
         self.size1 = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -194,15 +205,7 @@ class FusedAssembler:
         self.device = torch.device(device)
         self.bufs = ([torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
                      if self.rank == root else [None] * nbuf)
-        handles = [None] * self.world
-        dist.all_gather_object(handles, [reduce_tensor(b) for b in self.bufs] if self.rank == root else None,
-                               group=group)
-        self.peers = []
-        if self.rank != root:
-            for fn, args in handles[root]:
-                args = list(args)
-                args[6] = self.device.index  # rebuild on this process's device (peer mapping)
-                self.peers.append(fn(*args))
+        self.peers = _map_root_buffers(self.bufs, self.rank, self.world, root, self.device, group)
         self.sizes = [torch.zeros(self.world, dtype=torch.int64, device=self.device) for _ in range(nbuf)]
         self.token_t = torch.zeros(1, dtype=torch.float32, device=self.device)
 

@@ -60,6 +60,8 @@ def main():
         ok2 = torch.equal(got2[:tot].cpu(), full_body.cpu())
         print(f"[rank0] NVLink delta_assemble: match = {ok2}", flush=True)
         ok &= ok2
+    del got2
+    asm.close()  # consumers drop their IPC mappings before the root may free its buffer
     # the fused emit + assembly: scan, size all-gather, emit into the local body AND straight
     # into rank 0's buffer at the global offset (three steps over two root buffers)
     fu = sdist.FusedAssembler(ctx, tot + 4096, dev, nbuf=2)

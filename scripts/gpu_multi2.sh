@@ -1,4 +1,4 @@
-# 4-GPU scaling of the default path + assembly knobs.  Usage: bash scripts/gpu_multi2.sh TAG
+# 4-GPU scaling of the default path + the assembly variants (nvlink default, fused, nccl, none).  Usage: bash scripts/gpu_multi2.sh TAG
 TAG=${1:?tag}; OUT=gpurun_out/$TAG; mkdir -p $OUT
 NG=$(nvidia-smi -L | wc -l); echo "gpus: $NG"
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
@@ -9,8 +9,9 @@ NAME=n1 run
 NAME=n2 run --gpus 2
 NAME=n4 run --gpus 4
 NAME=n4_none run --gpus 4 --assembly none
-NAME=n4_ctas32 run --gpus 4 --assemble-ctas 32
-NAME=n4_ctas128 run --gpus 4 --assemble-ctas 128
+NAME=n2_fused run --gpus 2 --assembly fused
+NAME=n4_fused run --gpus 4 --assembly fused
+NAME=n4_nccl run --gpus 4 --assembly nccl
 for f in $OUT/*.jsonl; do python -c "
 import json
 l=[x for x in open('$f') if x.startswith('{')]

@@ -8,7 +8,7 @@
 #   fullsize   pytest tests/test_gpu_fullsize.py (every record of configs[1..4] vs the oracle)
 #   bench      bench.py N=1 (default flags) + the reference arm
 #   k4tune     bench.py over K4's CTAs per SM (K4_CTAS)
-#   k4full     ncu --set full of K4 on the full M3 step
+#   k4full     ncu --set full of one kernel (KFULL regex, default K4) on the full M3 step
 #   sweep      scripts/sweep.py: configs[0], [1], [4] (0.1/10/50 % uniform + rowblock)
 #   launches   ncu launch list of bench.py (gpu__time_duration, cold, serialised)
 #   traffic    ncu per-launch DRAM bytes + DRAM activity of the path's kernels at M3
@@ -24,7 +24,7 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 BENCH_SMALL="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-clocks"
 DRAM="dram__bytes_read.sum,dram__bytes_write.sum,dram__cycles_active.avg,dram__cycles_elapsed.avg,dram__throughput.avg.pct_of_peak_sustained_elapsed,gpu__time_duration.sum,lts__t_sectors_op_read.sum,lts__t_sectors_op_write.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,smsp__issue_active.avg.pct_of_peak_sustained_elapsed"
-KERNELS="k_scan_tiles|k_scatter|k_decode_count|k_emit_tiles|k_tiles|k_locate|k_apply_scan|k_finalize|k_headers|k_blocks"
+KERNELS="k_scan_tiles|k_scatter|k_decode_count|k_emit|k_tiles|k_locate|k_apply_scan|k_headers"
 for S in "$@"; do
   case $S in
   smoke)
@@ -41,9 +41,9 @@ for S in "$@"; do
       timeout 600 python bench.py --no-e2e --no-cpu-baseline --emit-ctas $C > $OUT/k4_c${C}.jsonl 2>/dev/null
       echo "C=$C $(tail -1 $OUT/k4_c${C}.jsonl | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["kernel_ms_per_step"]["emit_ms"])' 2>&1 | cut -c1-200)"
     done;;
-  k4full)  # ncu --set full of K4 on the full M3 step (one launch)
+  k4full)  # ncu --set full of one kernel (regex KFULL, default K4) on the full M3 step (one launch)
     $BENCH_SMALL > $OUT/plain_k4.log 2>&1 && \
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_emit" -c 1 -o $OUT/k4full \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${KFULL:-k_emit}" -c 1 -o $OUT/k4full \
       python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks > $OUT/ncu_k4full.log 2>&1; echo "k4full rc=$?";;
   sweep)
     timeout 1800 python scripts/sweep.py > $OUT/sweep.jsonl 2> $OUT/sweep.err; echo "sweep rc=$?";;
@@ -58,13 +58,13 @@ for S in "$@"; do
   sections)
     timeout 1500 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section Occupancy --section WarpStateStats \
       --section LaunchStats --section SchedulerStats --metrics $DRAM --clock-control none \
-      -k regex:"k_scan_tiles|k_scatter|k_decode_count|k_emit_tiles|k_locate" -c 5 -o $OUT/sections \
+      -k regex:"k_scan_tiles|k_scatter|k_decode_count|k_emit|k_locate|k_tiles_scan" -c 12 -o $OUT/sections \
       python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks > $OUT/ncu_sections.log 2>&1
     echo "sections rc=$?";;
   full)
     SMALL="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-clocks --tensors 40"
     $SMALL > $OUT/plain_full.log 2>&1 && \
-    timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_scan_tiles|k_scatter|k_emit_tiles|k_decode_count" \
+    timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_scan_tiles|k_scatter|k_emit|k_decode_count" \
       -s 4 -c 4 -o $OUT/full $SMALL > $OUT/ncu_full.log 2>&1; echo "full rc=$?";;
   sanitizer)
     for T in ${SAN_TOOLS:-memcheck racecheck synccheck initcheck}; do

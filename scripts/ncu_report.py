@@ -32,6 +32,8 @@ def instr_per_warp(rep, kernel):
         h = next(r for r in rows if "Address" in r)
     except StopIteration:
         return None
+    if "Instructions Executed" not in h:  # a section-only capture has no source counters
+        return None
     ai, ie = h.index("Address"), h.index("Instructions Executed")
     data = [r for r in rows if len(r) > ie and r[ai].startswith("0x")]
     if not data:
@@ -47,5 +49,5 @@ for label, rep in zip(sys.argv[1::2], sys.argv[2::2]):
     print("---|" + "---|" * len(WANT) + "---")
     for k, m in d.items():
         ipw = instr_per_warp(rep, k.split("<")[0].split("::")[-1])
-        print(f"{k} | " + " | ".join(m.get(w, "") for w in WANT) + f" | {ipw:.0f}" if ipw else " | ")
+        print(f"{k} | " + " | ".join(m.get(w, "") for w in WANT) + (f" | {ipw:.0f}" if ipw else " | "))
     print()
