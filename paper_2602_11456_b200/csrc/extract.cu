@@ -596,7 +596,7 @@ __device__ __forceinline__ void lb_publish(LbSlot *s, const LbAgg &x, uint32_t e
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&s->status), "r"((epoch << 2) | 1u) : "memory");
 }
 
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, 4)
 k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ meta, uint32_t ntiles, uint32_t nblk,
              LbSlot *__restrict__ lb, uint32_t epoch, TileEmit *__restrict__ plan, unsigned long long *__restrict__ E,
              unsigned long long *__restrict__ Bk, uint32_t T, const uint32_t *__restrict__ name_len,
@@ -609,50 +609,81 @@ k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ me
     }
     __shared__ uint32_t s_b;
     __shared__ LbAgg s_excl;
-    __shared__ long long s_first;
-    __shared__ unsigned long long s_bytes[kTileThreads / 32];
+    __shared__ unsigned long long s_labs[kTileThreads];  // per thread: its last change (lane index)
+    __shared__ uint32_t s_lk[kTileThreads];              // ... and its tensor
+    __shared__ unsigned long long s_fabs, s_bytes[kTileThreads / 32];
+    __shared__ uint32_t s_fk;
     __shared__ bool s_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_b = atomicAdd(&summary->lb_ticket, 1ull);
     __syncthreads();
     const uint32_t b = s_b;
-    const uint32_t t0 = b * kTileBlock + threadIdx.x * 4;
+    const uint32_t blk0 = b * kTileBlock, t0 = blk0 + threadIdx.x * 4;
+    // the thread's 4 tiles: metadata and (lane base, tensor), all loads issued together
     TileMeta mt[4];
-    unsigned long long c = 0;
-    long long klast = -1, kfirst = -1;
+    unsigned long long lb0[4];
+    uint32_t tk[4], tf[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        mt[e] = t0 + e < ntiles ? meta[t0 + e] : TileMeta{0, 0, 0, 0, 0};
+        const bool in = t0 + e < ntiles;
+        mt[e] = in ? meta[t0 + e] : TileMeta{0, 0, 0, 0, 0};
+        const uint4 q = in ? reinterpret_cast<const uint4 *>(tiles + t0 + e)[1] : make_uint4(0, 0, 0, 0);
+        lb0[e] = (unsigned long long)q.x | ((unsigned long long)q.y << 32);
+        tf[e] = q.w;
+        tk[e] = q.w & kTileTensorMask;
+    }
+    unsigned long long c = 0;
+    long long klast = -1;
+    int elast = -1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
         c += mt[e].count;
         if (mt[e].count) {
             klast = t0 + e;
-            if (kfirst < 0) kfirst = t0 + e;
+            elast = e;
         }
+    }
+    if (elast >= 0) {  // this thread's last change, for the thread after it
+        s_labs[threadIdx.x] = lb0[elast] + mt[elast].last_off;
+        s_lk[threadIdx.x] = tk[elast];
     }
     unsigned long long cex, ctot;
     long long kex, ktot;
-    block_scan_sum_max(c, klast, cex, ctot, kex, ktot);
-    // this thread's tiles: LEB128 bytes with the predecessor inside the block where there is one
-    const long long kex_in = kex;
-    unsigned long long bloc = 0;
-    {
-        long long kp = kex;
+    block_scan_sum_max(c, klast, cex, ctot, kex, ktot);  // its barriers also publish s_labs / s_lk
+    // per tile: its first gap g0 and LEB128 bytes bt, from the last change before it inside the
+    // block (an earlier tile of this thread, else the thread owning tile kex); the block's first
+    // non-empty tile (kex < 0) gets its first gap after the fold
+    bool has_pred = kex >= 0;
+    unsigned long long pabs = has_pred ? s_labs[(kex - blk0) >> 2] : 0ull;
+    uint32_t pk = has_pred ? s_lk[(kex - blk0) >> 2] : 0xFFFFFFFFu;
+    unsigned long long bt[4], g0[4], bloc = 0;
+    int efirst = -1;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t t = t0 + e;
-            if (t >= ntiles || !mt[e].count) continue;
-            unsigned long long g0;
-            if (kp >= 0 || fixed) bloc += tile_bytes(tiles[t], mt[e], tiles, meta, kp, numel, fixed, g0);
-            else bloc += mt[e].internal_bytes;  // the block's first non-empty tile: its first gap after the fold
-            kp = t;
+    for (int e = 0; e < 4; ++e) {
+        bt[e] = 0;
+        g0[e] = 0;
+        if (!mt[e].count) continue;
+        if (fixed) {
+            g0[e] = lb0[e];
+            bt[e] = (unsigned long long)mt[e].count * fixed_index_width(numel[tk[e]]);
+        } else if (has_pred) {
+            g0[e] = lb0[e] + mt[e].first_off - (pk == tk[e] ? pabs : 0ull);
+            bt[e] = mt[e].internal_bytes + leb_len(g0[e]);
+        } else {
+            efirst = e;  // the block's first non-empty tile
+            bt[e] = mt[e].internal_bytes;
         }
+        bloc += bt[e];
+        has_pred = true;
+        pabs = lb0[e] + mt[e].last_off;
+        pk = tk[e];
+    }
+    if (efirst >= 0 && !fixed) {
+        s_fabs = lb0[efirst] + mt[efirst].first_off;
+        s_fk = tk[efirst];
     }
     const unsigned long long bsum = warp_sum(bloc);
-    const long long kf = -warp_max(kfirst < 0 ? -(long long)0x7FFFFFFFFFFFFFFF : -kfirst);
     if (lane == 0) s_bytes[warp] = bsum;
-    if (threadIdx.x == 0) s_first = 0x7FFFFFFFFFFFFFFF;
-    __syncthreads();
-    if (lane == 0) atomicMin(&s_first, kf);
     __syncthreads();
     // ---- publish the block's aggregate, then fold every predecessor's (all threads)
     if (threadIdx.x == 0) {
@@ -660,12 +691,10 @@ k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ me
 #pragma unroll
         for (int w = 0; w < kTileThreads / 32; ++w) agg.bytes += s_bytes[w];
         if (ctot) {
-            const long long f = s_first;
-            const TileDesc df = tiles[f], dl = tiles[ktot];
-            agg.fabs = df.lane_base + meta[f].first_off;
-            agg.fk = df.flags_tensor & kTileTensorMask;
-            agg.labs = dl.lane_base + meta[ktot].last_off;
-            agg.lk = dl.flags_tensor & kTileTensorMask;
+            agg.fabs = fixed ? 0ull : s_fabs;
+            agg.fk = fixed ? 0u : s_fk;
+            agg.labs = s_labs[(ktot - blk0) >> 2];
+            agg.lk = s_lk[(ktot - blk0) >> 2];
         }
         lb_publish(lb + b, agg, epoch);
     }
@@ -696,25 +725,14 @@ k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ me
     }
     __syncthreads();
     const LbAgg ex = s_excl;
-    // ---- place the block's tiles
-    long long kp = kex_in;
-    unsigned long long bt[4], g0[4], mine = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        bt[e] = 0;
-        g0[e] = 0;
-        const uint32_t t = t0 + e;
-        if (t >= ntiles || !mt[e].count) continue;
-        const TileDesc d = tiles[t];
-        if (kp >= 0 || fixed) {
-            bt[e] = tile_bytes(d, mt[e], tiles, meta, kp, numel, fixed, g0[e]);
-        } else {  // the predecessor is the last change before the block (or none)
-            const uint32_t k = d.flags_tensor & kTileTensorMask;
-            g0[e] = d.lane_base + mt[e].first_off - ((ex.any && ex.lk == k) ? ex.labs : 0ull);
-            bt[e] = mt[e].internal_bytes + leb_len(g0[e]);
-        }
-        mine += bt[e];
-        kp = t;
+    // ---- place the block's tiles: the block's first non-empty tile's first gap is to the last
+    // change before the block in its tensor (or its lane index: the first of its tensor)
+    unsigned long long mine = bloc;
+    if (efirst >= 0 && !fixed) {
+        g0[efirst] = lb0[efirst] + mt[efirst].first_off - ((ex.any && ex.lk == tk[efirst]) ? ex.labs : 0ull);
+        const uint32_t l = leb_len(g0[efirst]);
+        bt[efirst] += l;
+        mine += l;
     }
     unsigned long long bex, btot;
     long long d0, d1;
@@ -725,9 +743,9 @@ k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ me
     for (int e = 0; e < 4; ++e) {
         const uint32_t t = t0 + e;
         if (t >= ntiles) break;
-        const uint32_t f = tiles[t].flags_tensor, k = f & kTileTensorMask;
+        const uint32_t k = tk[e];
         plan[t] = TileEmit{byt, ent, g0[e], mt[e].count | (fixed ? fixed_index_width(numel[k]) : mt[e].internal_bytes) << 16, k};
-        if (f & kTileFirstOfTensor) {
+        if (tf[e] & kTileFirstOfTensor) {
             E[k] = ent;
             Bk[k] = byt;
         }
