@@ -1,3 +1,6 @@
+"""K2 (k_tiles_scan) device time on the M3 workload: delta_size (K1 + K2 + size readback) in a
+loop with profiling on, printing K2's CUDA-event time of the last 10 calls (ms).
+    python scripts/k2_time.py      (GPU box)"""
 import os, sys, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import __graft_entry__ as entry
@@ -17,7 +20,7 @@ v = []
 for i in range(12):
     try:
         ctx.delta_size(tl)
-    except Exception as e:
+    except Exception:  # noqa: BLE001 (timing only)
         pass
     v.append(ctx.last_timing()["lens_ms"])
-print(os.environ.get("DELTA_K2_PHASE"), [round(x, 4) for x in v[2:]])
+print("k2_ms", [round(x, 4) for x in v[2:]])
