@@ -69,6 +69,12 @@ def parse():
                         "NVLink (sizes by one NCCL all-gather; the transfer then sits inside the emit); "
                         "'nccl' = NCCL P2P (baseline); 'none' = diagnostics only, no S2/S3")
     p.add_argument("--assemble-ctas", type=int, default=0, help="CTAs of the NVLink assembly kernel (0 = default)")
+    p.add_argument("--partition", default="auto", choices=["auto", "contiguous", "lpt"],
+                   help="N>1 S1: 'contiguous' = balanced tensor ranges (each rank's records are one byte "
+                        "range of the body); 'lpt' = longest-processing-time tensor sets (better balance; "
+                        "the NVLink assembly then copies record by record to global offsets); 'auto' "
+                        "(default) = lpt from 4 GPUs with the nvlink (or no) assembly, else contiguous "
+                        "(measured: lpt 1.3 %% faster at N=4, 1 %% slower at N=2 where ranges balance exactly)")
     p.add_argument("--comm-priority", type=int, default=0,
                    help="CUDA stream priority of the assembly stream (negative = higher)")
     p.add_argument("--sync-step", action="store_true",
@@ -419,9 +425,15 @@ def main():
     specs, rho, pattern, desc = workload(args)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     width = 2 if args.dtype == "bf16" else 4
-    # contiguous ranges: each rank's records are one byte range of the global body
-    b, e = sdist.shard_plan([s.numel for s in specs], world)[rank]
-    mine = list(range(b, e))
+    if args.partition == "auto":
+        args.partition = "lpt" if world >= 4 and args.assembly in ("nvlink", "none") else "contiguous"
+    if args.partition == "lpt":  # LPT tensor sets, ascending global order within the rank
+        mine = sdist.shard_lpt([s.numel for s in specs], world)[rank]
+        if world > 1 and args.assembly not in ("nvlink", "none"):
+            raise SystemExit("bench: --partition lpt supports --assembly nvlink or none")
+    else:  # contiguous ranges: each rank's records are one byte range of the global body
+        b, e = sdist.shard_plan([s.numel for s in specs], world)[rank]
+        mine = list(range(b, e))
 
     # ---- inputs resident in HBM before timing (per-tensor seeds: rank-independent data)
     olds, news, targets = [], [], []
@@ -442,6 +454,7 @@ def main():
     comm = torch.cuda.Stream(dev, priority=args.comm_priority) if world > 1 else None
     nvasm = None
     fuasm = None
+    rasm = None
 
     slot = {"t": 0, "cur": 0}
 
@@ -451,7 +464,12 @@ def main():
         nonlocal root_out
         if args.assembly == "none":
             return
+        if rasm is not None:  # record sizes from this rank's device table, before the next extract
+            rasm.record_sizes(slot["cur"], stream=torch.cuda.current_stream())
         comm.wait_stream(torch.cuda.current_stream())
+        if rasm is not None:  # record-granular NVLink copies (any partition)
+            rasm.assemble(body, slot["cur"], stream=comm)
+            return
         if fuasm is not None:  # the body is already there (fused emit): completion token only
             fuasm.token(comm)
             return
@@ -508,6 +526,8 @@ def main():
                 fuasm = sdist.FusedAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
                 if rank == 0:
                     out = fuasm.bufs[0]  # rank 0's records are the head of the assembled body
+            elif args.partition == "lpt":  # records go to scattered global offsets: rank 0 copies too
+                rasm = sdist.RecordAssembler(ctx, total0 + total0 // 8 + 4096, dev, mine, len(specs), nbuf=2)
             else:
                 nvasm = sdist.NvlinkAssembler(ctx, total0 + total0 // 8 + 4096, dev, nbuf=2)
                 if rank == 0:
@@ -516,7 +536,7 @@ def main():
         size_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         # two (body, size) slots when the NVLink assembly runs on the comm stream: step t+1
         # extracts into the other slot while step t's body is still being copied to rank 0
-        nslots = 2 if (nvasm is not None or fuasm is not None) else 1
+        nslots = 2 if (nvasm is not None or fuasm is not None or rasm is not None) else 1
         root_bufs = nvasm.bufs if nvasm is not None else (fuasm.bufs if fuasm is not None else None)
         outs = [out] + ([root_bufs[1] if (rank == 0 and root_bufs is not None) else torch.empty_like(out)]
                         if nslots == 2 else [])
@@ -530,7 +550,8 @@ def main():
                               "locate_ms", "decode_ms", "apply_scan_ms", "scatter_ms"):
                     acc[kname] = acc.get(kname, 0.0) + t[kname]
 
-        if args.sync_step or (world > 1 and nvasm is None and fuasm is None and args.assembly != "none"):
+        if args.sync_step or (world > 1 and nvasm is None and fuasm is None and rasm is None
+                               and args.assembly != "none"):
             def step(acc=None):
                 # host-sized path: delta_extract reads the size back (sync), the apply takes
                 # the device table; 2 host syncs per step
@@ -575,6 +596,7 @@ def main():
                 return (outs[s][:n] if n is not None else None), None
 
     chained = args.pipeline <= 1 and not (args.sync_step or (world > 1 and nvasm is None and fuasm is None
+                                                             and rasm is None
                                                              and args.assembly != "none"))
     pipelined = chained and args.host_sync == "end"
     for _ in range(max(args.warmup, 0)):
@@ -711,7 +733,8 @@ def main():
         # per rank and step: K1, K2 (tile prefixes + offset table), K4, K5 + A1-A4
         # (fixed-width indices: A1, A2f, A4f) [+ delta_assemble with --assembly nvlink]
         "gpu_launches": ((8 if args.index_codec == "leb128" else 7)
-                         + (1 if world > 1 and nvasm is not None else 0)) * args.steps,
+                         + (1 if world > 1 and nvasm is not None else 0)
+                         + (2 if world > 1 and rasm is not None else 0)) * args.steps,
         "clocks": clk,
     }
     if k1_ms > 0:
@@ -727,6 +750,11 @@ def main():
                      "NVLink (CUDA IPC), sizes by one NCCL all-gather, 2 root buffers",
             "nvlink": "delta_assemble copy kernel over NVLink (CUDA IPC) on a comm stream, 2 body buffers",
             "nccl": "NCCL P2P batch", "none": "NONE (diagnostics: no S2/S3)"}[args.assembly]
+        if rasm is not None:
+            result["config"]["assembly"] = ("record sizes all-reduced (NCCL), delta_assemble_records copies every "
+                                            "record to its global offset in rank 0's buffer over NVLink (CUDA IPC) "
+                                            "on a comm stream, 2 body buffers")
+        result["config"]["partition"] = args.partition
     if pipelined:  # the same steps with the host waiting for each one (latency view)
         ks = max(3, args.steps // 2)
         if world > 1:
@@ -774,6 +802,8 @@ def main():
         print(json.dumps(result), flush=True)
     if nvasm is not None:  # drop the CUDA IPC mapping of rank 0's buffer before rank 0 exits
         nvasm.close()
+    if rasm is not None:
+        rasm.close()
     if fuasm is not None:
         fuasm.close()
     ctx.close()

@@ -188,6 +188,55 @@ class NvlinkAssembler:
         _ipc_teardown(self.device, self.group)
 
 
+class RecordAssembler:
+    """S3 for ANY tensor partition (e.g. ``shard_lpt``): the root owns ``nbuf`` assembled-body
+    buffers, mapped into every other rank with CUDA IPC once.  Per step: ``record_sizes`` (on
+    the extract's stream, right after it: reads this rank's device offset table) writes this
+    rank's record sizes into a global-order vector (zeros elsewhere); ``assemble`` (on a comm
+    stream) sums the vectors over the ranks (one NCCL all-reduce of T int64), then one
+    delta_assemble_records kernel copies every local record to its global offset in the
+    root's buffer (over NVLink; the root copies its own records locally), and a one-element
+    all-reduce orders the copies before the root's readers."""
+
+    def __init__(self, ctx, capacity: int, device, gidx, n_global: int, group=None, root: int = 0,
+                 nbuf: int = 2):
+        self.ctx, self.group, self.root = ctx, group, root
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.device(device)
+        self.bufs = ([torch.empty(capacity, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
+                     if self.rank == root else [None] * nbuf)
+        self.peers = _map_root_buffers(self.bufs, self.rank, self.world, root, self.device, group)
+        self.gidx = torch.tensor(list(gidx), dtype=torch.int32, device=self.device)
+        self.sizes = [torch.zeros(n_global, dtype=torch.int64, device=self.device) for _ in range(nbuf)]
+        self.token = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    def record_sizes(self, slot: int = 0, stream=None):
+        """Enqueue on ``stream`` (the extract's, after it): this rank's record sizes."""
+        if self.gidx.numel():
+            self.ctx.record_sizes(self.ctx.table_dev_ptr(), self.gidx.numel(), self.gidx, self.sizes[slot],
+                                  stream=stream)
+        else:
+            with torch.cuda.stream(stream or torch.cuda.current_stream(self.device)):
+                self.sizes[slot].zero_()
+
+    def assemble(self, body: torch.Tensor, slot: int = 0, stream=None):
+        """Enqueue on ``stream``: size all-reduce, the record copies, completion all-reduce.
+        Returns the assembled buffer on the root, None elsewhere."""
+        stream = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(stream):
+            dist.all_reduce(self.sizes[slot], group=self.group)
+            if self.gidx.numel():
+                dst = self.bufs[slot] if self.rank == self.root else self.peers[slot]
+                self.ctx.assemble_records(body, self.gidx, self.sizes[slot], dst, stream=stream)
+            dist.all_reduce(self.token, group=self.group)
+        return self.bufs[slot] if self.rank == self.root else None
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        self.peers = []
+        _ipc_teardown(self.device, self.group)
+
+
 class FusedAssembler:
     """S2 + S3 fused into the emit (NEXT f2; PAPER.md:405-409 cut-through): the root owns
     ``nbuf`` assembled-body buffers, mapped into every other rank with CUDA IPC once.  Per step

@@ -109,6 +109,31 @@ def main():
         ok &= failed or not mine  # the last rank's records end past tot - 1
         print(f"[rank{rank}] fused assembly into a short buffer reported: {failed}", flush=True)
     fu2.close()
+    # any partition (LPT): record sizes all-reduced, record-by-record NVLink copies (rank 0 too)
+    lpt = sdist.shard_lpt([s.numel for s in specs], world)[rank]
+    lmine = [(specs[k].name, pairs[k][0], pairs[k][1]) for k in lpt]
+    cx2 = sd.DeltaContext(dev)
+    rsm = sdist.RecordAssembler(cx2, tot + 4096, dev, lpt, len(specs), nbuf=1)
+    if lmine:
+        lbody, _ = cx2.delta_extract(lmine, table="device")
+    else:
+        lbody = torch.empty(0, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        rsm.bufs[0].fill_(0xEE)
+        torch.cuda.synchronize()
+    dist.barrier()
+    rsm.record_sizes(0)
+    got3 = rsm.assemble(lbody, 0)
+    torch.cuda.synchronize()
+    cx2.assemble_wait()
+    if rank == 0:
+        ok3 = torch.equal(got3[:tot].cpu(), full_body.cpu())
+        print(f"[rank0] LPT partition {[len(p) for p in sdist.shard_lpt([s.numel for s in specs], world)]} "
+              f"records per rank, delta_assemble_records over NVLink: match = {ok3}", flush=True)
+        ok &= ok3
+    del got3
+    rsm.close()
+    cx2.close()
     if mine:
         targets = [(n, o.clone()) for n, o, _ in mine]
         ctx.delta_apply(targets, body, table=table)
