@@ -601,8 +601,8 @@ def main():
     pipelined = chained and args.host_sync == "end"
     for _ in range(max(args.warmup, 0)):
         body, table = step()
-    if pipelined:  # kernel times accumulated on the device over the timed region
-        ctx.set_profiling(2)
+    if pipelined:  # K1's time accumulated on the device over the timed region (events around
+        ctx.set_profiling(3)  # K1 only: events between every kernel cost ~30 us per step)
         step()  # one more waited warm-up step with the accumulating event ring
         ctx.timing_totals()
     clocks = Clocks(local, enabled=not args.no_clocks)
@@ -643,6 +643,23 @@ def main():
     if not ok:
         raise SystemExit("bench: round trip mismatch")
     ms = ev0.elapsed_time(ev1)
+    breakdown_steps = None
+    if pipelined:  # the other kernels' times: the same loop again, events around every kernel
+        ctx.set_profiling(2)
+        step()
+        ctx.timing_totals()
+        breakdown_steps = max(3, args.steps // 2)
+        if world > 1:
+            dist.barrier()
+        for _ in range(breakdown_steps):
+            step(wait=False)
+        if comm is not None:
+            stream.wait_stream(comm)
+        torch.cuda.synchronize()
+        ctx.extract_wait()
+        ctx.apply_wait()
+        tb, cb = ctx.timing_totals()
+        acc = {**{k: v * args.steps / max(cb, 1) for k, v in tb.items()}, "scan_ms": acc.get("scan_ms", 0.0)}
     rank_view = None
     if world > 1:  # max over ranks; every rank's time and K1 / scatter time for the record
         k1_local = acc.get("scan_ms", 0.0) / args.steps
@@ -715,6 +732,9 @@ def main():
                     "varint_saving_vs_naive": round(naive_total / body_total, 3),
                     "paper_context": PAPER_CPU},
         "kernel_ms_per_step": kernel_ms,
+        "kernel_ms_source": (f"K1 (scan_ms) from the timed region, CUDA events around K1 only; the other kernels "
+                             f"from {breakdown_steps} further steps with events around every kernel"
+                             if breakdown_steps else "CUDA events around every kernel in the timed steps"),
         # per-op time (this rank's kernels) and algorithmic bytes, and the round
         # trip's algorithmic bytes per lane 2w + rho (3w + 2E) against the measured peak
         "ops": ops_view(kernel_ms, local_lanes, width, nnz_local, idx_local, body_local,

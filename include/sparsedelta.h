@@ -466,7 +466,9 @@ int delta_set_option(delta_ctx *ctx, int option, int64_t value);
  * read with delta_last_timing (the synchronising calls fill them); 2 = accumulate over calls
  * without any extra host synchronisation (each call records into the next set of a ring of 8
  * event sets; a set is folded into the running totals when it is reused), read and reset
- * with delta_timing_totals — for timing loops that never wait on the host between calls.
+ * with delta_timing_totals — for timing loops that never wait on the host between calls;
+ * 3 = as 2 but around the compare kernel K1 only (scan_ms; two events per extract, none on
+ * the other kernels, so a timed loop carries almost no profiling work).
  * Changing the mode synchronises the device and resets all timings.  DELTA_EINVAL for other
  * values. */
 int delta_set_profiling(delta_ctx *ctx, int enable);
@@ -475,9 +477,9 @@ int delta_set_profiling(delta_ctx *ctx, int enable);
  * zero in mode 2). */
 int delta_last_timing(const delta_ctx *ctx, delta_timing *out);
 
-/* Mode 2: waits for the recorded events, writes the per-kernel totals since the last call
- * (or since delta_set_profiling) to *out and the number of extract scans they cover to
- * *calls (host), then resets them.  DELTA_EINVAL unless profiling mode is 2. */
+/* Modes 2 and 3: waits for the recorded events, writes the per-kernel totals since the last
+ * call (or since delta_set_profiling) to *out and the number of extract scans they cover to
+ * *calls (host), then resets them.  DELTA_EINVAL unless profiling mode is 2 or 3. */
 int delta_timing_totals(delta_ctx *ctx, delta_timing *out, uint32_t *calls);
 
 #ifdef __cplusplus

@@ -207,12 +207,13 @@ class DeltaContext:
 
     def set_profiling(self, enable):
         """Per-kernel CUDA-event timing inside the library: True / 1 = last calls
-        (last_timing), 2 = accumulated over calls without host waits (timing_totals)."""
+        (last_timing), 2 = accumulated over calls without host waits (timing_totals), 3 = as 2
+        for the compare kernel K1 only."""
         mode = 1 if enable is True else (0 if enable is False else int(enable))
         self._check(self._lib.delta_set_profiling(self._h, mode))
 
     def timing_totals(self):
-        """Profiling mode 2: (per-kernel totals in ms since the last call, extract scans
+        """Profiling modes 2 / 3: (per-kernel totals in ms since the last call, extract scans
         covered); resets the totals."""
         t = _abi.Timing()
         calls = ctypes.c_uint32()

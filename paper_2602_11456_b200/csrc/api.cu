@@ -112,7 +112,8 @@ struct delta_ctx {
     bool advance = false;  // extract-and-advance: old_dev is overwritten with new (synchronous extract only)
 
     // ---- optional per-kernel event timing
-    int profiling = 0;  // 0 off, 1 timings of the last calls, 2 accumulate over calls (ring of event sets)
+    int profiling = 0;  // 0 off, 1 timings of the last calls, 2 accumulate over calls (ring of event
+                        // sets), 3 accumulate the compare kernel K1 only (two events per call)
     cudaEvent_t ev_scan[4] = {}, ev_emit[3] = {}, ev_apply[5] = {};
     static constexpr int kProfRing = 8;
     cudaEvent_t rs_scan[kProfRing][4] = {}, rs_emit[kProfRing][3] = {}, rs_apply[kProfRing][5] = {};
@@ -263,7 +264,7 @@ int delta_set_option(delta_ctx *c, int option, int64_t value) {
 }
 
 int delta_set_profiling(delta_ctx *c, int enable) {
-    if (!c || enable < 0 || enable > 2) return DELTA_EINVAL;
+    if (!c || enable < 0 || enable > 3) return DELTA_EINVAL;
     if (cudaSetDevice(c->device) != cudaSuccess) return DELTA_ECUDA;
     if (enable && !c->profiling) {
         for (auto &e : c->ev_scan) cudaEventCreate(&e);
@@ -308,6 +309,13 @@ int delta_last_timing(const delta_ctx *c, delta_timing *out) {
 // events have long completed) or by delta_timing_totals.
 static void fold_scan(delta_ctx *c, int j) {
     if (!c->ru_scan[j]) return;
+    if (c->profiling == 3) {  // K1 only
+        cudaEventSynchronize(c->rs_scan[j][1]);
+        c->acc.scan_ms += ev_ms(c->rs_scan[j][0], c->rs_scan[j][1]);
+        c->acc_calls += 1;
+        c->ru_scan[j] = false;
+        return;
+    }
     cudaEventSynchronize(c->rs_scan[j][3]);
     c->acc.scan_ms += ev_ms(c->rs_scan[j][0], c->rs_scan[j][1]);
     c->acc.lens_ms += ev_ms(c->rs_scan[j][1], c->rs_scan[j][2]);
@@ -332,13 +340,14 @@ static void fold_apply(delta_ctx *c, int j) {
     c->ru_apply[j] = false;
 }
 static cudaEvent_t *prof_scan(delta_ctx *c) {
-    if (c->profiling != 2) return c->profiling ? c->ev_scan : nullptr;
+    if (c->profiling < 2) return c->profiling ? c->ev_scan : nullptr;
     const int j = (int)(c->ri_scan++ % delta_ctx::kProfRing);
     fold_scan(c, j);
     c->ru_scan[j] = true;
     return c->rs_scan[j];
 }
 static cudaEvent_t *prof_emit(delta_ctx *c) {
+    if (c->profiling == 3) return nullptr;
     if (c->profiling != 2) return c->profiling ? c->ev_emit : nullptr;
     const int j = (int)(c->ri_emit++ % delta_ctx::kProfRing);
     fold_emit(c, j);
@@ -346,6 +355,7 @@ static cudaEvent_t *prof_emit(delta_ctx *c) {
     return c->rs_emit[j];
 }
 static cudaEvent_t *prof_apply(delta_ctx *c) {
+    if (c->profiling == 3) return nullptr;
     if (c->profiling != 2) return c->profiling ? c->ev_apply : nullptr;
     const int j = (int)(c->ri_apply++ % delta_ctx::kProfRing);
     fold_apply(c, j);
@@ -357,7 +367,7 @@ extern "C" {
 
 int delta_timing_totals(delta_ctx *c, delta_timing *out, uint32_t *calls) {
     if (!c || !out || !calls) return DELTA_EINVAL;
-    if (c->profiling != 2) return DELTA_EINVAL;
+    if (c->profiling < 2) return DELTA_EINVAL;
     if (cudaSetDevice(c->device) != cudaSuccess) return DELTA_ECUDA;
     for (int j = 0; j < delta_ctx::kProfRing; ++j) {
         fold_scan(c, j);
@@ -567,6 +577,7 @@ static int run_scan(delta_ctx *ctx, cudaStream_t s) {
         CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
         ExtractArgs a = extract_args(ctx);
         a.redo_cap = redo_cap;
+        a.prof_k1_only = ctx->profiling == 3;
         CK(launch_extract_scan(a, s, prof_scan(ctx)), "extract scan launch");
         CK(cudaMemcpyAsync(ctx->h_summary, ctx->summary.p, sizeof(ExtractSummary), cudaMemcpyDeviceToHost, s), "readback");
         CK(cudaStreamSynchronize(s), "extract scan");
@@ -766,6 +777,7 @@ static int extract_scan_async(delta_ctx *ctx, const delta_tensor *t, uint32_t n,
     CK(cudaMemsetAsync(ctx->summary.p, 0, sizeof(ExtractSummary), s), "memset");
     ExtractArgs a = extract_args(ctx);
     a.scan_size_out = reinterpret_cast<unsigned long long *>(size_dev);
+    a.prof_k1_only = ctx->profiling == 3;
     CK(launch_extract_scan(a, s, prof_scan(ctx)), "extract scan launch");
     if (!n && size_dev) CK(cudaMemsetAsync(size_dev, 0, 8, s), "memset");
     ctx->scan_phase = true;

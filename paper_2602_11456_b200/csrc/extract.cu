@@ -1154,8 +1154,10 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
                                                    a.entry_begin, a.tensor_byte_begin, a.ntensors, a.name_len,
                                                    a.numel, a.table, a.bases, a.width, a.index_codec, a.summary,
                                                    a.scan_size_out);
-    if (ev) cudaEventRecord(ev[2], s);
-    if (ev) cudaEventRecord(ev[3], s);
+    if (ev && !a.prof_k1_only) {
+        cudaEventRecord(ev[2], s);
+        cudaEventRecord(ev[3], s);
+    }
     return cudaGetLastError();
 }
 

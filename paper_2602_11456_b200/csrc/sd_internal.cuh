@@ -169,6 +169,7 @@ struct ExtractArgs {
     int mode;                         // record mode: 0 replace, 1 additive
     int index_codec;                  // 0 LEB128 gaps, 1 fixed-width absolute (R18)
     bool advance = false;             // K1 also stores every changed new lane into old (extract-and-advance)
+    bool prof_k1_only = false;        // profiling mode 3: events around K1 only (ev[0], ev[1])
     uint32_t redo_cap = 0;            // advance retry: only tiles with count > redo_cap run K1 again
     // emit gate (K4/K5 write nothing unless the scan fitted its slots and body <= out_cap);
     // size_out (device, may be NULL) receives the body size, or ~0 when the gate is closed
