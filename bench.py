@@ -723,7 +723,9 @@ def main():
                    "lanes": total_lanes, "weights_bytes": total_lanes * width,
                    "scanned_bytes_per_step": scanned_total, "rho": rho, "pattern": pattern,
                    "seed": args.seed, "index_codec": args.index_codec,
-                   "shard": "contiguous balanced tensor ranges",
+                   "shard": ("one GPU: every tensor" if world == 1 else
+                             "LPT tensor sets (dist.shard_lpt)" if args.partition == "lpt" else
+                             "contiguous balanced tensor ranges (dist.shard_plan)"),
                    "l2": f"inputs ({scanned_total / 1e9:.1f} GB per step) larger than L2 (126 MB); no flush"},
         "payload": {"body_bytes": body_total, "ratio": round(total_lanes * width / body_total, 3),
                     "nnz": nnz_total, "rho_measured": nnz_total / total_lanes,

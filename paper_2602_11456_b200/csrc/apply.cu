@@ -90,7 +90,8 @@ __device__ uint32_t check_record(const uint8_t *body, unsigned long long body_by
     return kOk;
 }
 
-__global__ void __launch_bounds__(256)
+constexpr int kLocateThreads = 512;  // one round of record checks for up to 512 records
+__global__ void __launch_bounds__(kLocateThreads)
 k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
          const unsigned long long *__restrict__ body_bytes_dev,
          const TargetDesc *__restrict__ tg, uint32_t n, const uint8_t *__restrict__ names,
@@ -164,7 +165,7 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
     }
     __syncthreads();
     {   // chunk prefix over the records: block-wide exclusive scan, 256 records per round
-        __shared__ unsigned long long s_w[8];
+        __shared__ unsigned long long s_w[kLocateThreads / 32];
         const bool okst = st->status == kOk;
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         unsigned long long carry = 0;
@@ -176,7 +177,7 @@ k_locate(const uint8_t *__restrict__ body, unsigned long long body_bytes,
             __syncthreads();
             unsigned long long pre = 0, tot = 0;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {
+            for (int w = 0; w < kLocateThreads / 32; ++w) {
                 const unsigned long long y = s_w[w];
                 if (w < warp) pre += y;
                 tot += y;
@@ -428,18 +429,20 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
 // ------------------------------------------------------------------------------ A3
 // One CTA per record: exclusive scan of its chunks' (count, gap sum) -> ordinal and index
 // base of every chunk; count == nnz and last index (= total gap sum) < N.
-__global__ void __launch_bounds__(1024)
+constexpr int kApplyScanThreads = 256;  // most records span one or a few 4 KiB chunks
+__global__ void __launch_bounds__(kApplyScanThreads)
 k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long long *__restrict__ rcb,
              const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
              unsigned long long *__restrict__ ord_base, unsigned long long *__restrict__ idx_base,
              ApplyState *st) {
     if (st->status != kOk) return;
-    __shared__ unsigned long long s_c[32], s_s[32];
+    constexpr int NW = kApplyScanThreads / 32;
+    __shared__ unsigned long long s_c[NW], s_s[NW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
         const unsigned long long c0 = rcb[k], c1 = rcb[k + 1];
         unsigned long long cc = 0, cs = 0;
-        for (unsigned long long b = c0; b < c1; b += 1024) {
+        for (unsigned long long b = c0; b < c1; b += kApplyScanThreads) {
             const unsigned long long c = b + threadIdx.x;
             unsigned long long x = c < c1 ? chunk_count[c] : 0;
             unsigned long long y = c < c1 ? chunk_sum[c] : 0;
@@ -459,7 +462,8 @@ k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long 
             }
             __syncthreads();
             unsigned long long pc = 0, ps = 0, tc = 0, ts = 0;
-            for (int w = 0; w < 32; ++w) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
                 if (w < warp) {
                     pc += s_c[w];
                     ps = sat_add(ps, s_s[w]);
@@ -819,7 +823,7 @@ k_fixed_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ r
 // ------------------------------------------------------------------------------ launchers
 cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], s);
-    k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
+    k_locate<<<1, kLocateThreads, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
                                a.rec_chunk_begin, a.chunk_rec, a.state, a.width, a.index_codec);
     if (ev) cudaEventRecord(ev[1], s);
     if (a.index_codec) {  // fixed-width indices: validate, then the gated scatter (no scans)
@@ -839,7 +843,7 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
                                                   a.chunk_count, a.chunk_sum, a.state);
     if (ev) cudaEventRecord(ev[2], s);
     const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
-    k_apply_scan<<<nb, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
+    k_apply_scan<<<nb, kApplyScanThreads, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[3], s);
 #define SCATTER(WW, EM)                                                                                 \
@@ -858,12 +862,12 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
 
 cudaError_t launch_decode_only(const ApplyArgs &a, unsigned long long *idx_out, void *val_out,
                                const unsigned long long *entry_base, cudaStream_t s) {
-    k_locate<<<1, 256, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
+    k_locate<<<1, kLocateThreads, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
                                a.rec_chunk_begin, a.chunk_rec, a.state, a.width, 0);
     k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
                                                   a.chunk_count, a.chunk_sum, a.state);
     const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
-    k_apply_scan<<<nb, 1024, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
+    k_apply_scan<<<nb, kApplyScanThreads, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (a.width == 2)
         k_decode_write<2><<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.rec_chunk_begin, a.chunk_rec, a.chunk_count,
