@@ -551,14 +551,16 @@ __device__ __forceinline__ void block_scan_sum_max(unsigned long long x, long lo
 }
 
 // ------------------------------------------------------------------------------ K2 / K3
-// The tile-level prefixes and the offset table in ONE launch.  Each block of kTileBlock tiles publishes its aggregate
-// (entries, LEB128 bytes but its first tile's first gap, first / last change as (lane index,
-// tensor)) with a status word, then folds the aggregates of ALL its predecessors in order —
-// 256 threads in parallel, an ordered shuffle tree, one CTA-wide step — into its exclusive
-// prefix.  Between two blocks the first gap of the later one's first change is the LEB128
-// length of its distance to the earlier one's last change when they share a tensor, else of
-// its lane index.  Every tile is then placed (entry and byte prefix, first gap g0:
-// K4's plan), each tensor's E_k / B_k recorded at its first tile, and the last CTA to finish
+// The tile-level prefixes and the offset table in ONE launch.  Each block of kTileBlock tiles
+// publishes its aggregate (entries, LEB128 bytes but its first tile's first gap, first / last
+// change as (lane index, tensor)) with a status word, then runs a decoupled look-back: its 256
+// threads read the 256 nearest predecessors' published values at once, fold them in age order
+// (ordered shuffle trees, then the warps' partials) and stop at the nearest block that has
+// published its inclusive prefix, else look 256 blocks further back; then the block publishes
+// its own inclusive prefix.  Between two blocks the later block's first gap is the LEB128
+// length of its distance to the earlier block's last change when they share a tensor, else of
+// its lane index.  Every tile is then placed (entry and byte prefix, first gap
+// g0: K4's plan), each tensor's E_k / B_k recorded at its first tile, and the last CTA to finish
 // writes the offset table (K3: record sizes and offsets, PAPER.md:382 + SPEC.md:148) and the
 // per-tensor emit bases.  Block ids come from a ticket, so a block only waits for blocks that
 // started before it (no deadlock whatever the residency); status words carry the launch's
@@ -570,13 +572,18 @@ __device__ __forceinline__ LbAgg lb_combine(const LbAgg &a, const LbAgg &b, int 
     return LbAgg{a.cnt + b.cnt, a.bytes + b.bytes + (fixed ? 0ull : (unsigned long long)leb_len(gap)), a.fabs, b.labs,
                  a.fk, b.lk, 1u, 0};
 }
+__device__ __forceinline__ uint32_t lb_status_relaxed(const LbSlot *s) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&s->status) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint32_t lb_status(const LbSlot *s) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&s->status) : "memory");
     return v;
 }
-__device__ __forceinline__ LbAgg lb_load(const LbSlot *s) {
-    const unsigned long long *q = reinterpret_cast<const unsigned long long *>(&s->agg);
+__device__ __forceinline__ LbAgg lb_load(const LbSlot *s, bool inclusive) {
+    const unsigned long long *q = reinterpret_cast<const unsigned long long *>(inclusive ? &s->inc : &s->agg);
     LbAgg x;
     unsigned long long *o = reinterpret_cast<unsigned long long *>(&x);
 #pragma unroll
@@ -591,9 +598,12 @@ __device__ __forceinline__ LbAgg lb_shfl_down(const LbAgg &v, int off) {
     for (int k = 0; k < (int)(sizeof(LbAgg) / 8); ++k) o[k] = __shfl_down_sync(0xffffffffu, i[k], off);
     return x;
 }
-__device__ __forceinline__ void lb_publish(LbSlot *s, const LbAgg &x, uint32_t epoch) {
-    s->agg = x;
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&s->status), "r"((epoch << 2) | 1u) : "memory");
+// status kind 1: the block's aggregate is in agg; 2: its inclusive prefix is in inc
+__device__ __forceinline__ void lb_publish(LbSlot *s, const LbAgg &x, bool inclusive, uint32_t epoch) {
+    if (inclusive) s->inc = x;
+    else s->agg = x;
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&s->status), "r"((epoch << 2) | (inclusive ? 2u : 1u))
+                 : "memory");
 }
 
 __global__ void __launch_bounds__(kTileThreads, 4)
@@ -608,7 +618,7 @@ k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ me
         return;
     }
     __shared__ uint32_t s_b;
-    __shared__ LbAgg s_excl;
+    __shared__ LbAgg s_excl, s_agg;
     __shared__ unsigned long long s_labs[kTileThreads];  // per thread: its last change (lane index)
     __shared__ uint32_t s_lk[kTileThreads];              // ... and its tensor
     __shared__ unsigned long long s_fabs, s_bytes[kTileThreads / 32];
@@ -696,31 +706,59 @@ k_tiles_scan(const TileDesc *__restrict__ tiles, const TileMeta *__restrict__ me
             agg.labs = s_labs[(ktot - blk0) >> 2];
             agg.lk = s_lk[(ktot - blk0) >> 2];
         }
-        lb_publish(lb + b, agg, epoch);
+        lb_publish(lb + b, agg, b == 0, epoch);  // block 0's aggregate is its inclusive prefix
+        s_agg = agg;  // for this thread's inclusive publish below
     }
+    // ---- decoupled look-back over windows of 256 predecessors (thread t polls block hi - t,
+    // nearest first): the window's published values fold in age order (ordered shuffle trees,
+    // then the warps' partials), stopping at the nearest inclusive prefix, else 256 blocks
+    // further back; then this block publishes its inclusive prefix (status kind 2)
     {
-        // thread i folds predecessors [i*c, (i+1)*c) in order once each is published, then an
-        // ordered tree over the lanes (older lanes first) and over the warps
-        const uint32_t c = (b + kTileThreads - 1) / kTileThreads;
-        LbAgg v{0, 0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t j = threadIdx.x * c; j < min(b, (threadIdx.x + 1) * c); ++j) {
-            while ((lb_status(lb + j) >> 2) != epoch) {
+        __shared__ uint32_t s_im[kTileThreads / 32];
+        __shared__ LbAgg s_part[kTileThreads / 32];
+        LbAgg excl{0, 0, 0, 0, 0, 0, 0, 0};
+        long long hi = (long long)b - 1;
+        while (hi >= 0) {
+            const long long j = hi - threadIdx.x;
+            uint32_t st = 0;
+            if (j >= 0) {  // relaxed polls, one acquire once this launch's status is there
+                for (uint32_t ns = 32; (lb_status_relaxed(lb + j) >> 2) != epoch; ns = min(2 * ns, 512u))
+                    __nanosleep(ns);
+                st = lb_status(lb + j);
             }
-            v = lb_combine(v, lb_load(lb + j), fixed);
-        }
+            const bool inc = j >= 0 && (st & 3u) == 2u;
+            const uint32_t im = __ballot_sync(0xffffffffu, inc);
+            if (lane == 0) s_im[warp] = im;
+            __syncthreads();
+            int p = (int)min((long long)kTileThreads - 1, hi);  // threads 0..p take part
+            bool found = false;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const LbAgg o = lb_shfl_down(v, off);
-            if (lane + off < 32) v = lb_combine(v, o, fixed);
+            for (int w = kTileThreads / 32 - 1; w >= 0; --w)
+                if (s_im[w]) {
+                    p = w * 32 + __ffs(s_im[w]) - 1;
+                    found = true;
+                }
+            LbAgg v = (j >= 0 && (int)threadIdx.x <= p) ? lb_load(lb + j, inc) : LbAgg{0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {  // lane l + off holds an older block
+                const LbAgg o = lb_shfl_down(v, off);
+                if (lane + off < 32) v = lb_combine(o, v, fixed);
+            }
+            if (lane == 0) s_part[warp] = v;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                LbAgg wv = s_part[kTileThreads / 32 - 1];  // warp w + 1 holds older blocks than warp w
+#pragma unroll
+                for (int w = kTileThreads / 32 - 2; w >= 0; --w) wv = lb_combine(wv, s_part[w], fixed);
+                excl = lb_combine(wv, excl, fixed);  // older than the windows folded so far
+            }
+            if (found || hi < kTileThreads) break;
+            hi -= kTileThreads;
+            __syncthreads();  // s_im / s_part reused
         }
-        __shared__ LbAgg s_w[kTileThreads / 32];
-        if (lane == 0) s_w[warp] = v;
-        __syncthreads();
         if (threadIdx.x == 0) {
-            LbAgg e = s_w[0];
-#pragma unroll
-            for (int w = 1; w < kTileThreads / 32; ++w) e = lb_combine(e, s_w[w], fixed);
-            s_excl = e;
+            if (b > 0) lb_publish(lb + b, lb_combine(excl, s_agg, fixed), true, epoch);
+            s_excl = excl;
         }
     }
     __syncthreads();

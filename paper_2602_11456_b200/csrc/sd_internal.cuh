@@ -60,8 +60,8 @@ struct LbAgg {
     uint32_t any, pad;         // any change at all
 };
 struct LbSlot {
-    LbAgg agg;
-    uint32_t status;           // (launch epoch << 2) | 1 once agg is written
+    LbAgg agg, inc;            // the block's aggregate; its inclusive prefix (all blocks up to it)
+    uint32_t status;           // (launch epoch << 2) | 1 once agg is written, | 2 once inc is
     uint32_t pad[3];
 };
 
