@@ -360,6 +360,16 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def resolve_partition(partition: str, world: int, assembly: str) -> str:
+    """S1 choice: 'auto' = LPT tensor sets from 4 GPUs when the assembly can place records at
+    scattered offsets (nvlink: delta_assemble_records; none), else contiguous ranges."""
+    if partition == "auto":
+        return "lpt" if world >= 4 and assembly in ("nvlink", "none") else "contiguous"
+    if partition == "lpt" and world > 1 and assembly not in ("nvlink", "none"):
+        raise SystemExit("bench: --partition lpt supports --assembly nvlink or none")
+    return partition
+
+
 def launch_ranks(args):
     """--gpus N with no WORLD_SIZE in the environment: re-exec this command under
     torch.distributed.run, one rank per GPU (rendezvous on 127.0.0.1).  Under a launcher,
@@ -428,12 +438,9 @@ def main():
     specs, rho, pattern, desc = workload(args)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     width = 2 if args.dtype == "bf16" else 4
-    if args.partition == "auto":
-        args.partition = "lpt" if world >= 4 and args.assembly in ("nvlink", "none") else "contiguous"
+    args.partition = resolve_partition(args.partition, world, args.assembly)
     if args.partition == "lpt":  # LPT tensor sets, ascending global order within the rank
         mine = sdist.shard_lpt([s.numel for s in specs], world)[rank]
-        if world > 1 and args.assembly not in ("nvlink", "none"):
-            raise SystemExit("bench: --partition lpt supports --assembly nvlink or none")
     else:  # contiguous ranges: each rank's records are one byte range of the global body
         b, e = sdist.shard_plan([s.numel for s in specs], world)[rank]
         mine = list(range(b, e))

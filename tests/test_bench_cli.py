@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 from conftest import ROOT
 
 
@@ -49,3 +51,19 @@ def test_world_size_mismatch_fails():
                        capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode != 0
     assert "WORLD_SIZE=2 but --gpus 1" in r.stderr
+
+
+def test_partition_resolution():
+    """--partition auto: contiguous ranges up to 2 GPUs (they balance exactly there), LPT
+    from 4 with the NVLink (record-granular) or no assembly; explicit LPT needs one of those."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert bench.resolve_partition("auto", 1, "nvlink") == "contiguous"
+    assert bench.resolve_partition("auto", 2, "nvlink") == "contiguous"
+    assert bench.resolve_partition("auto", 4, "nvlink") == "lpt"
+    assert bench.resolve_partition("auto", 8, "none") == "lpt"
+    assert bench.resolve_partition("auto", 8, "fused") == "contiguous"
+    assert bench.resolve_partition("contiguous", 8, "nvlink") == "contiguous"
+    assert bench.resolve_partition("lpt", 1, "fused") == "lpt"
+    with pytest.raises(SystemExit):
+        bench.resolve_partition("lpt", 4, "nccl")
