@@ -908,26 +908,55 @@ def e2e_shadow(args, sd, names, ks, specs, olds, news, targets, dev, scanned_tot
         h_v[0].append(w.cpu().pin_memory())
         h_v[1].append((w.view(lt) ^ x).view(w.dtype).cpu().pin_memory())
         del x
-    ctx = sd.DeltaContext(dev)
-    ctx.set_option(9, 2)  # DELTA_OPT_ADVANCE
-    tl = sd.TensorList([(n, o, w) for n, o, w in zip(names, olds, news)])
+    # two device copies of the new weights (and of the body): step s+1's H2D (copy stream)
+    # runs while step s extracts and applies (compute stream) and step s-1's body goes D2H
+    # (a third stream; PCIe is full duplex).  One context per buffer set, both advancing the
+    # same shadow, in stream order.
+    news2 = [torch.empty_like(w) for w in news]
+    bufs = [news, news2]
+    ctxs, tls = [], []
+    for nb in bufs:
+        cx = sd.DeltaContext(dev)
+        cx.set_option(9, 2)  # DELTA_OPT_ADVANCE
+        ctxs.append(cx)
+        tls.append(sd.TensorList([(n, o, w) for n, o, w in zip(names, olds, nb)]))
     tg = sd.TargetList([(n, t) for n, t in zip(names, targets)])
     for o, t in zip(olds, targets):  # shadow and actor copy start at the same version
         t.copy_(o)
-    cap = ctx.delta_size(tl)  # compaction cached for the first extract below
-    out = torch.empty(4 * cap + 4096, dtype=torch.uint8, device=dev)
-    h_body = torch.empty(out.numel(), dtype=torch.uint8).pin_memory()
+    cap = ctxs[0].delta_size(tls[0])  # compaction cached for the first extract below
+    outs = [torch.empty(4 * cap + 4096, dtype=torch.uint8, device=dev) for _ in range(2)]
+    h_bodies = [torch.empty(o.numel(), dtype=torch.uint8).pin_memory() for o in outs]
+    cps, dhs = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    free = [None, None]      # compute-stream event: the extract reading buffer i is done
+    out_free = [None, None]  # D2H-stream event: body buffer i has reached the host
     d2h = [0]
-    state = {"v": 0}
+    state = {"s": 0}
 
     def one():
-        hv = h_v[state["v"] % 2]
-        state["v"] += 1
-        for w, hw in zip(news, hv):
-            w.copy_(hw, non_blocking=True)
-        body, table = ctx.delta_extract(tl, out=out, table="device")
-        ctx.delta_apply(tg, body, table=table)
-        h_body[:body.numel()].copy_(body, non_blocking=True)
+        s = state["s"]
+        state["s"] += 1
+        i = s % 2
+        with torch.cuda.stream(cps):  # H2D of this step's W_{t+1} into buffer i
+            if free[i] is not None:
+                cps.wait_event(free[i])
+            for w, hw in zip(bufs[i], h_v[i]):
+                w.copy_(hw, non_blocking=True)
+            loaded[i].record(cps)
+        stream.wait_event(loaded[i])
+        if out_free[i] is not None:
+            stream.wait_event(out_free[i])
+        body, table = ctxs[i].delta_extract(tls[i], out=outs[i], table="device")
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        free[i] = ev
+        ctxs[i].delta_apply(tg, body, table=table)
+        dhs.wait_stream(stream)
+        with torch.cuda.stream(dhs):
+            h_bodies[i][:body.numel()].copy_(body, non_blocking=True)
+            ev2 = torch.cuda.Event()
+            ev2.record(dhs)
+            out_free[i] = ev2
         d2h[0] = body.numel()
     for _ in range(2):
         one()
@@ -938,24 +967,30 @@ def e2e_shadow(args, sd, names, ks, specs, olds, news, targets, dev, scanned_tot
     ev0.record(stream)
     for _ in range(args.e2e_steps):
         one()
+    stream.wait_stream(cps)
+    stream.wait_stream(dhs)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
+    last = bufs[(state["s"] - 1) % 2]
     ok = all(torch.equal(t.view(lt), w.view(lt)) and torch.equal(o.view(lt), w.view(lt))
-             for t, o, w in zip(targets, olds, news))
+             for t, o, w in zip(targets, olds, last))
     if not ok:
         raise SystemExit("bench: e2e (shadow) round trip mismatch")
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    ctx.close()
+    for cx in ctxs:
+        cx.close()
+    del news2, bufs
     h2d = sum(w.numel() * w.element_size() for w in news)
     return {"value": round(scanned_total * args.e2e_steps / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0], "steps": args.e2e_steps,
             "ms_per_step": round(ms / args.e2e_steps, 3),
             "note": ("bytes per rank; W_{t+1} H2D from pinned host (W_t resident as the extract-and-advance "
-                     "shadow), body D2H, apply on device; the compare still scans old+new")}
+                     "shadow), body D2H, apply on device; the compare still scans old+new; step s+1's H2D "
+                     "overlaps step s's kernels and step s-1's D2H (two device buffers)")}
 
 
 if __name__ == "__main__":
