@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--index-codec", default="leb128", choices=["leb128", "fixed"],
                    help="fixed: the paper's naive int32/64 index encoding (PAPER.md:387, 609; R18)")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=4)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     p.add_argument("--no-clocks", action="store_true")
