@@ -103,7 +103,7 @@ struct delta_ctx {
 
     // ---- launch options
     uint32_t lb_epoch = 0;  // K2 look-back launch epoch
-    int apply_ctas_per_sm = 32, emit_ctas_per_sm = 24, scatter_ctas_per_sm = 96, scan_kernel = 0;
+    int apply_ctas_per_sm = 64, emit_ctas_per_sm = 24, scatter_ctas_per_sm = 96, scan_kernel = 0;
     int prefetch_tiles = -1;  // K1 L2 prefetch distance in tiles (-1: one wave = 3 x SMs)
     int assemble_ctas = 32;   // grid of the NVLink assembly kernels (peer stores; 32: measured best at N=4, round 2)
     bool entry_major = true;

@@ -343,9 +343,8 @@ __device__ __forceinline__ bool validate_fast(const ChunkView &v, int p0, uint32
     return true;
 }
 
-__device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cnt,
+__device__ __forceinline__ void validate_thread(const ChunkView &v, int p0, uint32_t &cnt,
                                                 unsigned long long &sum, uint32_t &err) {
-    const int p0 = threadIdx.x * 16;
     const int p1 = min(p0 + 16, (int)v.len);
     if (p0 >= p1) return;
     if (p1 - p0 == 16 && validate_fast(v, p0, cnt, sum)) return;
@@ -377,7 +376,10 @@ __device__ __forceinline__ void validate_thread(const ChunkView &v, uint32_t &cn
 }
 
 // ------------------------------------------------------------------------------ A2
-__global__ void __launch_bounds__(256)
+// 128 threads per 4 KiB chunk, two 16-byte windows each (windows t and t + 128): half the
+// per-chunk staging / reduction instructions of one window per thread
+constexpr int kDecodeThreads = 128, kDecodeWin = kByteChunk / 16 / kDecodeThreads;
+__global__ void __launch_bounds__(kDecodeThreads)
 k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
                const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
                unsigned int *__restrict__ chunk_count,
@@ -395,10 +397,13 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
         __syncthreads();
         uint32_t cnt = 0, err = kOk;
         unsigned long long sum = 0;
-        validate_thread(v, cnt, sum, err);
         const int pl = (int)v.len - 1;  // the stream's last byte must end a varint
-        if (v.last && pl >= threadIdx.x * 16 && pl < threadIdx.x * 16 + 16 && (v.b[pl] & 0x80))
-            err = err ? err : kTruncated;
+#pragma unroll
+        for (int h = 0; h < kDecodeWin; ++h) {
+            const int p0 = (threadIdx.x + h * kDecodeThreads) * 16;
+            validate_thread(v, p0, cnt, sum, err);
+            if (v.last && pl >= p0 && pl < p0 + 16 && (v.b[pl] & 0x80)) err = err ? err : kTruncated;
+        }
         if (err != kOk) set_status(st, err);
         cnt = __reduce_add_sync(0xffffffffu, cnt);
         if (__all_sync(0xffffffffu, sum < (1ull << 26))) {  // 32 lanes x 2^26 < 2^32: no overflow
@@ -415,7 +420,8 @@ k_decode_count(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ re
         if (threadIdx.x == 0) {
             uint32_t tc = 0;
             unsigned long long ts = 0;
-            for (int w = 0; w < 8; ++w) {
+#pragma unroll
+            for (int w = 0; w < kDecodeThreads / 32; ++w) {
                 tc += s_cnt[w];
                 ts = sat_add(ts, s_sum[w]);
             }
@@ -839,7 +845,7 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
         if (ev) cudaEventRecord(ev[4], s);
         return cudaGetLastError();
     }
-    k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
+    k_decode_count<<<a.persist_ctas, kDecodeThreads, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
                                                   a.chunk_count, a.chunk_sum, a.state);
     if (ev) cudaEventRecord(ev[2], s);
     const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
@@ -864,7 +870,7 @@ cudaError_t launch_decode_only(const ApplyArgs &a, unsigned long long *idx_out, 
                                const unsigned long long *entry_base, cudaStream_t s) {
     k_locate<<<1, kLocateThreads, 0, s>>>(a.body, a.body_bytes, a.body_bytes_dev, a.targets, a.n, a.names, a.hint, a.recs,
                                a.rec_chunk_begin, a.chunk_rec, a.state, a.width, 0);
-    k_decode_count<<<a.persist_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
+    k_decode_count<<<a.persist_ctas, kDecodeThreads, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec,
                                                   a.chunk_count, a.chunk_sum, a.state);
     const uint32_t nb = a.n ? (a.n < 65535u ? a.n : 65535u) : 1u;
     k_apply_scan<<<nb, kApplyScanThreads, 0, s>>>(a.recs, a.n, a.rec_chunk_begin, a.chunk_count, a.chunk_sum,
