@@ -13,9 +13,10 @@
 //                       per tile its entry / byte prefix and first gap (the predecessor of the
 //                       tile's first change is the last change before it in its tensor,
 //                       PAPER.md:389) -> K4's plan; the last CTA writes the offset table (K3).
-//   K4  k_emit_ring     E5+E6: one warp per tile: the first gap's LEB128 bytes, then the in-tile
-//                       bytes and the values copied from the slot to their final offsets
-//                       through a cp.async shared-memory ring.  k_emit_fixed: FIXED codec.
+//   K4  k_emit_pair     E5+E6: one half-warp per tile (two tiles per warp step): the first
+//                       gap's LEB128 bytes, then the in-tile bytes and the values copied from
+//                       the slot to their final offsets through a cp.async shared-memory ring.
+//                       k_emit_fixed: FIXED codec.
 //   K5  k_headers       E6: record headers (name_len, name, N, nnz, index_bytes) + mode.
 //
 // Product code written for this library; none of it is shared with the test oracle.
@@ -989,15 +990,13 @@ k_emit_fixed(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ b
     }
 }
 
-// LEB128 K4 with a shared-memory ring: each warp keeps S tiles' slot bytes in flight through
-// cp.async (LDGSTS, no registers held), plans 2S tiles ahead, so a tile's DRAM latency overlaps
-// the stores of the S - 1 tiles before it (a register prefetch held one and ran 0.21 ms vs
-// 0.15 ms at M3; 1-D TMA bulk copies per tile, 0.24 ms, were slower still).  Per
-// warp and stage: 512 + 512 bytes of data (in-tile LEB128 bytes, values), the tensor's emit
-// bases; per warp 2S plans.  Tiles with a segment > kPref bytes take the synchronous copies.
+// LEB128 K4 with a shared-memory ring: each warp keeps S steps of slot bytes in flight through
+// cp.async (LDGSTS, no registers held), plans 2S steps ahead, so a tile's DRAM latency overlaps
+// the stores of the tiles before it (a register prefetch held one tile and ran 0.21 ms vs
+// 0.15 ms at M3; 1-D TMA bulk copies per tile, 0.24 ms, were slower still).  Per tile and
+// stage: 512 + 512 bytes of data (in-tile LEB128 bytes, values) and the tensor's emit bases;
+// plans 2S steps ahead.  Tiles with a segment > kPref bytes take the synchronous copies.
 constexpr uint32_t kRingData = 1024;
-template <int S>
-__host__ __device__ constexpr uint32_t ring_warp_bytes() { return S * (kRingData + 16) + 2 * S * 32; }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
@@ -1024,102 +1023,140 @@ __device__ __forceinline__ void ring_vec(const uint8_t *s, uint8_t *dst, uint32_
         make_uint4(__funnelshift_r(w[QV], w[QV + 1], sh), __funnelshift_r(w[QV + 1], w[QV + 2], sh),
                    __funnelshift_r(w[QV + 2], w[QV + 3], sh), __funnelshift_r(w[QV + 3], w[QV + 4], sh));
 }
-__device__ __forceinline__ void ring_store(const uint8_t *s, uint8_t *dst, uint32_t n, int lane) {
+// K4 proper: each lane group of L = 16 lanes (a half-warp) takes one tile, a warp two at a
+// time, so the per-tile bookkeeping (plans, bases, addresses, first-gap bytes, copy issue)
+// runs once per two tiles in each instruction; a ~330-byte values segment then takes two
+// 16-lane passes instead of one 32-lane (0.154 -> 0.120 ms at M3).
+template <int S, int P>
+__host__ __device__ constexpr uint32_t pair_warp_bytes() { return S * P * (kRingData + 16) + 2 * S * P * 32; }
+
+// n <= kPref bytes staged at s to any destination, by the L lanes hl = 0..L-1 of a lane group
+template <int L>
+__device__ __forceinline__ void ring_store_h(const uint8_t *s, uint8_t *dst, uint32_t n, int hl) {
     const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
     const uint32_t rest = n - head, nv = rest >> 4, tail = rest & 15u;
-    // head bytes on lanes 0-15, tail bytes on lanes 16-31: one predicated byte copy
-    const uint32_t bpos = lane < 16 ? (uint32_t)lane : head + 16u * nv + (uint32_t)(lane - 16);
-    if (lane < 16 ? (uint32_t)lane < head : (uint32_t)(lane - 16) < tail) dst[bpos] = s[bpos];
-    if ((uint32_t)lane < nv) {  // the word offset head / 4 is warp-uniform: one branch, no selects
-        const uint32_t sh = 8u * (head & 3u);
+    for (uint32_t b = hl; b < head; b += L) dst[b] = s[b];
+    for (uint32_t b = hl; b < tail; b += L) dst[head + 16u * nv + b] = s[head + 16u * nv + b];
+    const uint32_t sh = 8u * (head & 3u);
+    for (uint32_t j = hl; j < nv; j += L) {
         switch (head >> 2) {
-        case 0: ring_vec<0>(s, dst, head, sh, lane); break;
-        case 1: ring_vec<1>(s, dst, head, sh, lane); break;
-        case 2: ring_vec<2>(s, dst, head, sh, lane); break;
-        default: ring_vec<3>(s, dst, head, sh, lane); break;
+        case 0: ring_vec<0>(s, dst, head, sh, (int)j); break;
+        case 1: ring_vec<1>(s, dst, head, sh, (int)j); break;
+        case 2: ring_vec<2>(s, dst, head, sh, (int)j); break;
+        default: ring_vec<3>(s, dst, head, sh, (int)j); break;
         }
     }
 }
+// the same from a 16-byte aligned global source of any length (dense tiles)
+template <int L>
+__device__ __forceinline__ void half_copy16(uint8_t *dst, const uint8_t *src, uint32_t n, int hl) {
+    const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
+    const uint32_t rest = n - head, nv = rest >> 4, tail = rest & 15u;
+    for (uint32_t b = hl; b < head; b += L) dst[b] = src[b];
+    for (uint32_t b = hl; b < tail; b += L) dst[head + 16u * nv + b] = src[head + 16u * nv + b];
+    uint4 *d16 = reinterpret_cast<uint4 *>(dst + head);
+    const uint4 *s16 = reinterpret_cast<const uint4 *>(src);
+    const uint32_t qv = head >> 2, sh = 8u * (head & 3u);
+    for (uint32_t j = hl; j < nv; j += L) {
+        const uint4 a = __ldg(s16 + j), b = __ldg(s16 + j + 1);
+        uint32_t w0, w1, w2, w3, w4;
+        if (qv == 0) { w0 = a.x; w1 = a.y; w2 = a.z; w3 = a.w; w4 = b.x; }
+        else if (qv == 1) { w0 = a.y; w1 = a.z; w2 = a.w; w3 = b.x; w4 = b.y; }
+        else if (qv == 2) { w0 = a.z; w1 = a.w; w2 = b.x; w3 = b.y; w4 = b.z; }
+        else { w0 = a.w; w1 = b.x; w2 = b.y; w3 = b.z; w4 = b.w; }
+        d16[j] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                            __funnelshift_r(w3, w4, sh));
+    }
+}
 
-template <int W, int S>
+template <int W, int S, int L>
 __global__ void __launch_bounds__(256)
-k_emit_ring(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
+k_emit_pair(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
             const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
             uint8_t *__restrict__ out, const ExtractSummary *summary, unsigned long long cap, PeerDst peer) {
     const EmitGate gate = emit_gate(summary, cap, peer);
     if (!gate.local) return;  // emit gate (async extract)
     uint8_t *const pout = gate.peer ? peer.base + gate.off : nullptr;  // fused assembly: the same bytes there too
     extern __shared__ __align__(16) uint8_t s_ring[];
-    const int lane = threadIdx.x & 31;
-    uint8_t *const sdata = s_ring + (threadIdx.x >> 5) * ring_warp_bytes<S>();
-    TensorBase *const sbase = reinterpret_cast<TensorBase *>(sdata + S * kRingData);
-    TileEmit *const splan = reinterpret_cast<TileEmit *>(sdata + S * (kRingData + 16));
+    constexpr int P = 32 / L;  // tiles per warp step
+    const int lane = threadIdx.x & 31, h = lane / L, hl = lane % L;
+    uint8_t *const sdata = s_ring + (threadIdx.x >> 5) * pair_warp_bytes<S, P>();
+    TensorBase *const sbase = reinterpret_cast<TensorBase *>(sdata + S * P * kRingData);
+    TileEmit *const splan = reinterpret_cast<TileEmit *>(sdata + S * P * (kRingData + 16));
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
     const uint32_t mine = wg < ntiles ? (ntiles - wg + nw - 1) / nw : 0;  // tiles of this warp: wg + m nw
+    const uint32_t pairs = (mine + P - 1) / P;                            // step q: tiles m = Pq + h
     auto slot_i = [&](uint32_t t) { return slot_bytes + (size_t)t * 2 * slot_cap; };
     auto slot_v = [&](uint32_t t) { return reinterpret_cast<const uint8_t *>(slot_val + (size_t)t * slot_cap); };
     auto fast = [&](const TileEmit &p) {
         return (p.count_internal >> 16) <= kPref && (p.count_internal & 0xFFFFu) * W <= kPref;
     };
-    auto issue_plan = [&](uint32_t m) {  // plan of the warp's m-th tile -> plan slot m % 2S
-        if (m < mine && lane < 2)
-            cp_async16(reinterpret_cast<uint8_t *>(splan + m % (2 * S)) + 16 * lane,
-                       reinterpret_cast<const uint8_t *>(plan + (wg + m * nw)) + 16 * lane);
+    auto issue_plan = [&](uint32_t q) {  // plan of this half's tile of pair q -> plan slot (q % 2S, h)
+        const uint32_t m = P * q + h;
+        if (m < mine && hl < 2)
+            cp_async16(reinterpret_cast<uint8_t *>(splan + (q % (2 * S)) * P + h) + 16 * hl,
+                       reinterpret_cast<const uint8_t *>(plan + (wg + m * nw)) + 16 * hl);
     };
-    auto issue_data = [&](uint32_t m) {  // its slot bytes and emit bases -> stage m % S (plan m landed)
+    auto issue_data = [&](uint32_t q) {  // its slot bytes and emit bases -> stage (q % S, h)
+        const uint32_t m = P * q + h;
         if (m >= mine) return;
-        const TileEmit p = splan[m % (2 * S)];
+        const TileEmit p = splan[(q % (2 * S)) * P + h];
         const uint32_t count = p.count_internal & 0xFFFFu, ni = p.count_internal >> 16, nv = count * W;
         if (count == 0 || !fast(p)) return;
         const uint32_t t = wg + m * nw;
-        uint8_t *d = sdata + (m % S) * kRingData;
-        cp_async16_zfill(d + 16 * lane, slot_i(t) + 16 * lane, (uint32_t)lane <= (ni >> 4));
-        cp_async16_zfill(d + 512 + 16 * lane, slot_v(t) + 16 * lane, (uint32_t)lane <= (nv >> 4));
-        if (lane == 0) cp_async16(sbase + m % S, bases + p.k);
+        uint8_t *d = sdata + ((q % S) * P + h) * kRingData;
+#pragma unroll
+        for (int r = 0; r < 32 / L; ++r) {
+            const uint32_t v = hl + L * r;
+            cp_async16_zfill(d + 16 * v, slot_i(t) + 16 * v, v <= (ni >> 4));
+            cp_async16_zfill(d + 512 + 16 * v, slot_v(t) + 16 * v, v <= (nv >> 4));
+        }
+        if (hl == 0) cp_async16(sbase + (q % S) * P + h, bases + p.k);
     };
-    for (uint32_t m = 0; m < 2 * S - 1; ++m) issue_plan(m);
+    for (uint32_t q = 0; q < 2 * S - 1; ++q) issue_plan(q);
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
-    for (uint32_t m = 0; m < S - 1; ++m) {
-        issue_data(m);
+    for (uint32_t q = 0; q < S - 1; ++q) {
+        issue_data(q);
         cp_async_commit();
     }
-    for (uint32_t n = 0; n < mine; ++n) {
-        issue_plan(n + 2 * S - 1);  // into the slot of tile n - 1 (stored last iteration)
-        issue_data(n + S - 1);      // into the stage of tile n - 1
+    for (uint32_t q = 0; q < pairs; ++q) {
+        issue_plan(q + 2 * S - 1);  // into the slots of pair q - 1 (stored last iteration)
+        issue_data(q + S - 1);      // into the stage of pair q - 1
         cp_async_commit();
-        cp_async_wait<S - 1>();     // tile n's group (and the plan of n + S) landed
+        cp_async_wait<S - 1>();     // pair q's group (and the plans of pair q + S) landed
         __syncwarp();
-        const TileEmit pc = splan[n % (2 * S)];
+        const uint32_t m = P * q + h;
+        const TileEmit pc = m < mine ? splan[(q % (2 * S)) * P + h] : TileEmit{0, 0, 0, 0, 0};
         const uint32_t count = pc.count_internal & 0xFFFFu;
         if (count) {
             const bool f = fast(pc);
-            const TensorBase tb = f ? sbase[n % S] : bases[pc.k];
+            const TensorBase tb = f ? sbase[(q % S) * P + h] : bases[pc.k];
             uint8_t *ib = out + (tb.ib + pc.ib);
             uint8_t *vb = out + (tb.vb + pc.eb * W);
             // the first gap: byte n = 7-bit group n, continuation bit on all but the last
             const unsigned long long g = pc.g0;
             const uint32_t L0 = leb_len(g);
-            const uint8_t g_byte = (uint8_t)(((g >> (7 * lane)) & 0x7Fu) | ((uint32_t)lane + 1 < L0 ? 0x80u : 0u));
             const uint32_t ni = pc.count_internal >> 16, nv = count * W;
-            const uint8_t *sd = sdata + (n % S) * kRingData;
-            const uint32_t t = wg + n * nw;
+            const uint8_t *sd = sdata + ((q % S) * P + h) * kRingData;
+            const uint32_t t = wg + m * nw;
             for (int d = 0; d < (pout ? 2 : 1); ++d) {  // d = 1: fused assembly (NVLink stores)
                 uint8_t *di = d ? pout + (ib - out) : ib;
                 uint8_t *dv = d ? pout + (vb - out) : vb;
-                if ((uint32_t)lane < L0) di[lane] = g_byte;
+                for (uint32_t b = hl; b < L0; b += L)
+                    di[b] = (uint8_t)(((g >> (7 * b)) & 0x7Fu) | (b + 1 < L0 ? 0x80u : 0u));
                 if (f) {
-                    ring_store(sd, di + L0, ni, lane);
-                    ring_store(sd + 512, dv, nv, lane);
+                    ring_store_h<L>(sd, di + L0, ni, hl);
+                    ring_store_h<L>(sd + 512, dv, nv, hl);
                 } else {  // a dense tile: synchronous copies
-                    warp_copy16(di + L0, slot_i(t), ni, lane);
-                    warp_copy16(dv, slot_v(t), nv, lane);
+                    half_copy16<L>(di + L0, slot_i(t), ni, hl);
+                    half_copy16<L>(dv, slot_v(t), nv, hl);
                 }
             }
         }
-        __syncwarp();  // stage n % S and plan slot n % 2S are refilled from the next iterations
+        __syncwarp();  // stage q % S and plan slots q % 2S are refilled from the next iterations
     }
     cp_async_wait<0>();
 }
@@ -1199,16 +1236,27 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
     return cudaGetLastError();
 }
 
-// K4's ring depth: 2 stages (measured: 3, 4, 6, 8 no faster, more shared memory per CTA)
-constexpr int kEmitStages = 2;
+// K4's ring depth: 2 stages (measured: 3, 4, 6, 8 no faster, more shared memory per CTA);
+// 16 lanes per tile, two tiles per warp step (measured: 0.154 ms with 32 lanes per tile,
+// 0.120 with 16, 0.160 with 8 — the 8-lane form fits 3 CTAs per SM)
+constexpr int kEmitStages = 2, kEmitLanes = 16;
+
+template <int W, int L>
+static void launch_pair(const ExtractArgs &a, uint8_t *out, cudaStream_t s) {
+    constexpr uint32_t psmem = 8 * pair_warp_bytes<kEmitStages, 32 / L>();
+    static const bool attr = [] {
+        cudaFuncSetAttribute(k_emit_pair<W, kEmitStages, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        return true;
+    }();
+    (void)attr;
+    k_emit_pair<W, kEmitStages, L><<<a.persist_ctas, 256, psmem, s>>>(
+        a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<const typename LaneOf<W>::T *>(a.slot_val), out,
+        a.summary, a.out_cap, a.peer);
+}
 
 template <int W>
 static void launch_ring(const ExtractArgs &a, uint8_t *out, cudaStream_t s) {
-    constexpr uint32_t smem = 8 * ring_warp_bytes<kEmitStages>();
-    static_assert(smem <= 48 * 1024, "K4 ring fits the default dynamic shared memory limit");
-    k_emit_ring<W, kEmitStages><<<a.persist_ctas, 256, smem, s>>>(
-        a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<const typename LaneOf<W>::T *>(a.slot_val),
-        out, a.summary, a.out_cap, a.peer);
+    launch_pair<W, kEmitLanes>(a, out, s);
 }
 
 template <int W>
