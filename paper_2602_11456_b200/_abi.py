@@ -10,7 +10,7 @@ import os
 from ctypes import POINTER, c_char_p, c_int, c_uint32, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsparsedelta.so")
+LIB_PATH = os.environ.get("SPARSEDELTA_LIB") or os.path.join(HERE, "libsparsedelta.so")  # override: A/B runs only
 
 DELTA_OK, DELTA_EINVAL, DELTA_ESHAPE, DELTA_ECAPACITY = 0, -1, -2, -3
 DELTA_ECORRUPT, DELTA_ENAME, DELTA_ECUDA, DELTA_ENOMEM = -4, -5, -6, -7

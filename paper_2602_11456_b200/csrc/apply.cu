@@ -14,7 +14,8 @@
 //                      and index base; count == nnz and last index < N.
 //   A4 k_scatter       gated on the device status word (all-or-nothing):
 //                      decode again, absolute index = base + running gap sum, value read
-//                      from the record's value array, W[index] = value (replace mode, R1).
+//                      from the record's value array, W[index] = value (replace mode, R1);
+//                      dense chunks rewrite whole 16-byte vectors of the chunk's window.
 //
 // Product code; shares nothing with oracle/.
 #include <cstdint>
@@ -499,17 +500,56 @@ k_apply_scan(const ApplyRec *__restrict__ recs, uint32_t n, const unsigned long 
 }
 
 // ------------------------------------------------------------------------------ A4
+// Dense chunk: >= 256 entries whose gap sum is < 4 per entry, so all its changes fall in a
+// window of < 4 kByteChunk lanes: [wlo, whi] = (previous chunk's last index, own last
+// index] (the record's first chunk: [0, last]).  No other chunk writes a lane of it (indices
+// ascend), so every 16-byte vector of the target lying wholly inside the window can be
+// rewritten whole: unchanged lanes keep the bits just loaded.  The chunk's changes go into a
+// bitmap over the window's vectors; a changed lane's ordinal in the chunk is its rank there.
+constexpr uint32_t kDenseWords = 768;  // bitmap words: >= (4 * kByteChunk + 16) / 32, 3 per thread
+
+template <int W>
+struct DenseLanes {
+    static constexpr int LV = 16 / W;       // lanes per 16-byte vector
+    static constexpr int VPW = 32 / LV;     // vectors per bitmap word
+    static constexpr uint32_t ALL = (1u << LV) - 1u;
+};
+
+// Values [ord0, ord0 + LV) of the chunk (staged at svb + vofs, any byte alignment) as four
+// words: one 20-byte window of aligned shared-memory words, funnel-shifted.
+__device__ __forceinline__ void value_run(const uint8_t *svb, uint32_t b, uint32_t (&p)[4]) {
+    const uint32_t *a = reinterpret_cast<const uint32_t *>(svb) + (b >> 2);
+    const uint32_t sh = (b & 3u) * 8u;
+    uint32_t x[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) x[i] = a[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = __funnelshift_r(x[i], x[i + 1], sh);
+}
+
+// Lane q (0 <= q < LV) of a run of values packed in four words.
+template <int W>
+__device__ __forceinline__ uint32_t run_lane(const uint32_t (&p)[4], uint32_t q) {
+    if constexpr (W == 2) {
+        const unsigned long long lo = p[0] | ((unsigned long long)p[1] << 32);
+        const unsigned long long hi = p[2] | ((unsigned long long)p[3] << 32);
+        return (uint32_t)(((q < 4 ? lo : hi) >> ((q & 3u) * 16u)) & 0xFFFFu);
+    } else {
+        return q < 2 ? (q == 0 ? p[0] : p[1]) : (q == 2 ? p[2] : p[3]);
+    }
+}
+
 // Gated scatter-store: decode again, absolute index = chunk base + running gap sum, value
 // from the chunk's slice of the record's value array (staged in shared memory).
 template <int W, bool ENTRY_MAJOR>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
           const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
           const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
           const unsigned long long *__restrict__ ord_base, const unsigned long long *__restrict__ idx_base,
           ApplyState *st) {
     using LT = typename std::conditional<W == 2, uint16_t, uint32_t>::type;
-    constexpr uint32_t WIN = 8192;  // lanes per dense merge window
+    using D = DenseLanes<W>;
     const uint32_t gate = st->status;
     if (gate != kOk) {  // the gate: nothing is written unless all checks passed
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&st->first_error, 0u, gate);
@@ -520,21 +560,33 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
     __shared__ __align__(16) uint8_t svb[kByteChunk * W + 32];  // at most one varint per byte
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_sum[8];
-    // entry-major order: the chunk's indices relative to idx_base[c], by ordinal; stores are
-    // issued entry i by thread i mod 256 (a warp covers 32 consecutive entries), or, for a
-    // dense chunk, merged into 16 KiB windows of the target and written back whole.
-    __shared__ uint32_t s_rel[ENTRY_MAJOR ? kByteChunk : 1];
-    __shared__ __align__(16) uint8_t s_win[ENTRY_MAJOR ? WIN * W + 32 : 16];
-    __shared__ uint32_t s_iend;
+    __shared__ uint32_t s_wtot[8];
+    // entry-major order (sparse chunks): the chunk's indices relative to idx_base[c], by
+    // ordinal; stores are issued entry i by thread i mod 256 (a warp covers 32 consecutive
+    // entries).  Dense chunks: the change bitmap over the window's vectors and its word prefixes.
+    __shared__ union {
+        uint32_t rel[ENTRY_MAJOR ? kByteChunk : 1];
+        struct {
+            uint32_t bm[kDenseWords];
+            uint32_t pre[kDenseWords];
+        } d;
+    } su;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (unsigned long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const uint32_t k = __ldg(chunk_rec + c);
         const ApplyRec R = recs[k];
-        const ChunkView v = stage_chunk(body, R, c - __ldg(rcb + k), sb + kStagePad);
+        const unsigned long long j = c - __ldg(rcb + k);
+        const ChunkView v = stage_chunk(body, R, j, sb + kStagePad);
         const unsigned long long ob = ord_base[c];
         const uint32_t cn = chunk_count[c];
+        const unsigned long long csum = chunk_sum[c];
+        const bool dense = cn >= 256 && csum < 4ull * cn;
         // this chunk's values (cn lanes, any alignment in the body)
         const uint8_t *vals = stage_bytes(svb, body + R.val_off + ob * W, cn * W);
+        if (dense) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) su.d.bm[threadIdx.x * 3 + i] = 0u;
+        }
         __syncthreads();
         uint32_t cnt = 0;
         unsigned long long sum = 0;
@@ -569,78 +621,120 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
             if constexpr (W == 2) return (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
             else return (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) | ((LT)vals[4 * o + 3] << 24);
         };
-        // entry-major needs the chunk's span to fit 32-bit relative indices
-        if (ENTRY_MAJOR && chunk_sum[c] < 0xFFFFFFFFull) {
-            if (ones) {  // 16 one-byte gaps: no continuation handling
-                uint32_t r = (uint32_t)(idx - base);
+        if (dense) {
+            const unsigned long long wlo = j == 0 ? base : base + 1, whi = base + csum;
+            // vector-aligned lane base of the window (targets are lane-aligned)
+            // (signed: below lane 0 when the target itself is not 16-byte aligned)
+            const long long abase = (long long)wlo - (long long)((reinterpret_cast<uintptr_t>(w + wlo) & 15u) / W);
+            if (ones) {
+                uint32_t r = (uint32_t)(idx - abase);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    r += v.b[p0 + j];
-                    s_rel[ord + j] = r;
+                for (int q = 0; q < 16; ++q) {
+                    r += v.b[p0 + q];
+                    atomicOr(&su.d.bm[r >> 5], 1u << (r & 31u));
                 }
             } else {
                 decode_thread(v, [&](unsigned long long x) {
                     idx += x;
-                    s_rel[ord++] = (uint32_t)(idx - base);
+                    const uint32_t r = (uint32_t)(idx - abase);
+                    atomicOr(&su.d.bm[r >> 5], 1u << (r & 31u));
                 });
             }
             __syncthreads();
-            const uint32_t lo = s_rel[0], hi = s_rel[cn - 1];
-            const unsigned long long span = (unsigned long long)hi - lo + 1;
-            if (cn >= 256 && span <= 4ull * cn) {  // >= 25 % dense: window merge
-                // dense chunk: merge into windows [ws, we) of the target (this chunk owns
-                // exactly the lanes lo..hi, so the write-back never touches another CTA's)
-                uint32_t ibeg = 0;
-                for (unsigned long long ws = lo; ws <= hi; ws += WIN) {
-                    const unsigned long long we = min((unsigned long long)hi + 1, ws + WIN);
-                    LT *gdst = w + base + ws;
-                    const uint32_t nl = (uint32_t)(we - ws);
-                    uint32_t iend = cn;  // entries of this window: [ibeg, iend); a chunk
-                    if (span > WIN) {    // whose span fits one window needs no search
-                        if (threadIdx.x == 0) {
-                            uint32_t l = ibeg, r = cn;
-                            while (l < r) {
-                                const uint32_t m = (l + r) >> 1;
-                                if ((unsigned long long)s_rel[m] < we) l = m + 1;
-                                else r = m;
+            // ranks: exclusive prefix of the words' popcounts (3 words per thread)
+            uint32_t pc[3], tot = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                pc[i] = __popc(su.d.bm[threadIdx.x * 3 + i]);
+                tot += pc[i];
+            }
+            const uint32_t ti = warp_inclusive_sum(tot);
+            if (lane == 31) s_wtot[warp] = ti;
+            __syncthreads();
+            uint32_t wp = ti - tot;
+            for (int w2 = 0; w2 < warp; ++w2) wp += s_wtot[w2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                su.d.pre[threadIdx.x * 3 + i] = wp;
+                wp += pc[i];
+            }
+            __syncthreads();
+            // every vector holding a change: 4 per thread in flight (loads, then stores)
+            const uint32_t vofs = (uint32_t)(vals - svb);
+            const uint32_t nvec = (uint32_t)(((long long)whi - abase) / D::LV) + 1;
+            uint4 *gv = reinterpret_cast<uint4 *>(w + abase);
+            for (uint32_t v0 = threadIdx.x; v0 < nvec; v0 += 4 * blockDim.x) {
+                uint32_t m[4];
+                bool whole[4];
+                uint4 old[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t vi = v0 + u * blockDim.x;
+                    m[u] = vi < nvec ? (su.d.bm[vi / D::VPW] >> ((vi % D::VPW) * D::LV)) & D::ALL : 0u;
+                    const long long l0 = abase + (long long)vi * D::LV;
+                    whole[u] = l0 >= (long long)wlo && l0 + D::LV - 1 <= (long long)whi;
+                    if (m[u] && whole[u] && (add || m[u] != D::ALL)) old[u] = gv[vi];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (!m[u]) continue;
+                    const uint32_t vi = v0 + u * blockDim.x;
+                    const uint32_t wd = vi / D::VPW, sh = (vi % D::VPW) * D::LV;
+                    const uint32_t o0 = su.d.pre[wd] + __popc(su.d.bm[wd] & ((1u << sh) - 1u));
+                    uint32_t p[4];
+                    value_run(svb, vofs + o0 * W, p);
+                    if (whole[u]) {
+                        uint32_t ow[4] = {old[u].x, old[u].y, old[u].z, old[u].w};
+                        if (!add && m[u] == D::ALL) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) ow[i] = p[i];
+                        } else {
+                            uint32_t q = 0;
+#pragma unroll
+                            for (int l = 0; l < D::LV; ++l) {
+                                if (!((m[u] >> l) & 1u)) continue;
+                                uint32_t nv = run_lane<W>(p, q++);
+                                if constexpr (W == 2) {
+                                    const uint32_t sl = (l & 1) * 16;
+                                    if (add) nv = lane_combine<2>((ow[l >> 1] >> sl) & 0xFFFFu, nv, false);
+                                    ow[l >> 1] = (ow[l >> 1] & ~(0xFFFFu << sl)) | (nv << sl);
+                                } else {
+                                    if (add) nv = lane_combine<4>(ow[l], nv, false);
+                                    ow[l] = nv;
+                                }
                             }
-                            s_iend = l;
                         }
-                        __syncthreads();
-                        iend = s_iend;
+                        gv[vi] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                    } else {  // a vector across the window's edge: its changed lanes only
+                        uint32_t q = 0;
+#pragma unroll
+                        for (int l = 0; l < D::LV; ++l) {
+                            if (!((m[u] >> l) & 1u)) continue;
+                            LT &t = w[abase + (long long)vi * D::LV + l];
+                            const uint32_t nv = run_lane<W>(p, q++);
+                            t = add ? (LT)lane_combine<W>(t, nv, false) : (LT)nv;
+                        }
                     }
-                    if (iend == ibeg) {  // nothing changes in this window
-                        __syncthreads();
-                        continue;
-                    }
-                    // stage the target lanes (plain loads: the kernel writes this memory)
-                    const uint4 *ga = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(gdst) & ~uintptr_t(15));
-                    const uint32_t o16 = (uint32_t)(reinterpret_cast<uintptr_t>(gdst) & 15);
-#pragma unroll 4
-                    for (uint32_t j = threadIdx.x; j < (o16 + nl * W + 15) / 16; j += blockDim.x)
-                        reinterpret_cast<uint4 *>(s_win)[j] = ga[j];
-                    __syncthreads();
-                    LT *wl = reinterpret_cast<LT *>(s_win + o16);
-                    for (uint32_t i = ibeg + threadIdx.x; i < iend; i += blockDim.x) {
-                        LT &t = wl[s_rel[i] - ws];
-                        t = add ? (LT)lane_combine<W>(t, value(i), false) : value(i);
-                    }
-                    __syncthreads();
-                    // write back exactly lanes [ws, we): lane head, 16-byte body, lane tail
-                    const uint32_t head = min(nl, ((16u - o16) & 15u) / W);
-                    const uint32_t nv = (nl - head) * W / 16;
-                    if (threadIdx.x < head) gdst[threadIdx.x] = wl[threadIdx.x];
-                    for (uint32_t j = threadIdx.x; j < nv; j += blockDim.x)
-                        reinterpret_cast<uint4 *>(gdst + head)[j] = reinterpret_cast<const uint4 *>(wl + head)[j];
-                    for (uint32_t l2 = head + nv * 16 / W + threadIdx.x; l2 < nl; l2 += blockDim.x) gdst[l2] = wl[l2];
-                    ibeg = iend;
-                    __syncthreads();
+                }
+            }
+        } else if (ENTRY_MAJOR && csum < 0xFFFFFFFFull) {  // needs 32-bit relative indices
+            if (ones) {  // 16 one-byte gaps: no continuation handling
+                uint32_t r = (uint32_t)(idx - base);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    r += v.b[p0 + q];
+                    su.rel[ord + q] = r;
                 }
             } else {
-                for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) {
-                    LT &t = w[base + s_rel[i]];
-                    t = add ? (LT)lane_combine<W>(t, value(i), false) : value(i);
-                }
+                decode_thread(v, [&](unsigned long long x) {
+                    idx += x;
+                    su.rel[ord++] = (uint32_t)(idx - base);
+                });
+            }
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < cn; i += blockDim.x) {
+                LT &t = w[base + su.rel[i]];
+                t = add ? (LT)lane_combine<W>(t, value(i), false) : value(i);
             }
         } else {
             decode_thread(v, [&](unsigned long long x) {
@@ -860,6 +954,7 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
         else SCATTER(2, false);
     } else {
         SCATTER(4, false);  // entry-major's index staging would exceed 48 KB static smem at W = 4
+        // (dense chunks take the bitmap path at either width)
     }
 #undef SCATTER
     if (ev) cudaEventRecord(ev[4], s);

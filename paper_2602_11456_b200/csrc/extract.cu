@@ -335,8 +335,67 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         }
         __syncthreads();
         LT *sv = slot_val + (size_t)t * slot_cap;
-        const LT *sn = reinterpret_cast<const LT *>(s_new);
         uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
+        if constexpr (!ADDITIVE && !OFFSETS) {
+            // values from the registers (s_new is no longer read), compacted into s_new by
+            // rank; the index bytes behind them when they fit, else straight to the slot; then
+            // both leave in 16-byte stores (whole sectors instead of 2- and 1-byte scatters)
+            const uint32_t nb = c - 1u + (tot >> 16) - 1u;  // in-tile index bytes (as meta)
+            const uint32_t vb = (c * W + 15u) & ~15u;
+            const bool bsm = vb + nb + 16u <= (uint32_t)sizeof(s_new);
+            uint8_t *sm = reinterpret_cast<uint8_t *>(s_new);
+            LT *smv = reinterpret_cast<LT *>(s_new);
+            uint8_t *bd = bsm ? sm + vb : sb;
+#pragma unroll
+            for (int r = 0; r < VECS; ++r) {
+                const uint32_t v = r * THREADS + tid;
+                const uint32_t w = v / (64 / LPV), sub = v % (64 / LPV);
+                const unsigned long long Wb = s_bits[w];
+                uint32_t mb = (uint32_t)(Wb >> (sub * LPV)) & ((1u << LPV) - 1u);
+                if (!mb) continue;
+                const unsigned long long below = Wb & ((1ull << (sub * LPV)) - 1ull);
+                const uint32_t ex = s_wex[w], pv = s_wprv[w];
+                uint32_t rank = (ex & 0xFFFFu) + (uint32_t)__popcll((long long)below);
+                const bool hp_w = pv & (1u << 17);
+                const uint32_t bigs = (ex >> 16) - ((hp_w && (ex >> 16)) ? 1u : 0u);
+                const uint32_t bp = rank - 1u + bigs + (below && (pv & (1u << 16)) ? 1u : 0u);
+                const bool has_prev = below ? true : hp_w;
+                const uint32_t prevL = below ? 64u * w + 63u - (uint32_t)__clzll((long long)below) : (pv & 0xFFFFu);
+                // the vector's first change: its gap (from prevL) takes two bytes iff it starts
+                // its word and the word is flagged; the tile's first change has no in-tile gap
+                // (its byte position, -1, is virtual: K4 writes the plan's first gap ahead of
+                // the stream)
+                const bool two = has_prev && below == 0 && (pv & (1u << 16));
+                const uint32_t bq = bp + (two ? 2u : 1u);  // bytes of the vector's later changes
+                // lanes unrolled (static lane extraction, no per-change loop): change k of the
+                // vector goes to rank + k, its gap (< LPV lanes: one byte) to bq + k - 1
+#pragma unroll
+                for (int j = 0; j < LPV; ++j) {
+                    if (!((mb >> j) & 1u)) continue;
+                    const uint32_t low = mb & ((1u << j) - 1u);
+                    const uint32_t k = (uint32_t)__popc(low);
+                    smv[rank + k] = (LT)lane_of<W>(vn[r], j);
+                    if (low) {
+                        bd[bq + k - 1u] = (uint8_t)(j - (31 - __clz(low)));
+                    } else if (has_prev) {
+                        const uint32_t g = v * LPV + j - prevL;
+                        if (two) {
+                            bd[bp] = (uint8_t)(g | 0x80u);
+                            bd[bp + 1] = (uint8_t)(g >> 7);
+                        } else {
+                            bd[bp] = (uint8_t)g;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            const uint4 *src = reinterpret_cast<const uint4 *>(s_new);
+            for (uint32_t i = tid; i < vb / 16u; i += THREADS) reinterpret_cast<uint4 *>(sv)[i] = src[i];
+            if (bsm)
+                for (uint32_t i = tid; i < (nb + 15u) / 16u; i += THREADS) reinterpret_cast<uint4 *>(sb)[i] = src[vb / 16u + i];
+            return;
+        }
+        const LT *sn = reinterpret_cast<const LT *>(s_new);
 #pragma unroll 1
         for (int r = 0; r < VECS; ++r) {
             const uint32_t v = r * THREADS + tid;
@@ -1047,8 +1106,9 @@ __device__ __forceinline__ void ring_store_h(const uint8_t *s, uint8_t *dst, uin
         }
     }
 }
-// the same from a 16-byte aligned global source of any length (dense tiles)
-template <int L>
+// the same from a 16-byte aligned global source of any length (dense tiles), U vectors per
+// lane per round
+template <int L, int U>
 __device__ __forceinline__ void half_copy16(uint8_t *dst, const uint8_t *src, uint32_t n, int hl) {
     const uint32_t head = min(n, (uint32_t)((16u - ((uintptr_t)dst & 15u)) & 15u));
     const uint32_t rest = n - head, nv = rest >> 4, tail = rest & 15u;
@@ -1057,19 +1117,34 @@ __device__ __forceinline__ void half_copy16(uint8_t *dst, const uint8_t *src, ui
     uint4 *d16 = reinterpret_cast<uint4 *>(dst + head);
     const uint4 *s16 = reinterpret_cast<const uint4 *>(src);
     const uint32_t qv = head >> 2, sh = 8u * (head & 3u);
-    for (uint32_t j = hl; j < nv; j += L) {
-        const uint4 a = __ldg(s16 + j), b = __ldg(s16 + j + 1);
-        uint32_t w0, w1, w2, w3, w4;
-        if (qv == 0) { w0 = a.x; w1 = a.y; w2 = a.z; w3 = a.w; w4 = b.x; }
-        else if (qv == 1) { w0 = a.y; w1 = a.z; w2 = a.w; w3 = b.x; w4 = b.y; }
-        else if (qv == 2) { w0 = a.z; w1 = a.w; w2 = b.x; w3 = b.y; w4 = b.z; }
-        else { w0 = a.w; w1 = b.x; w2 = b.y; w3 = b.z; w4 = b.w; }
-        d16[j] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
-                            __funnelshift_r(w3, w4, sh));
+    // all U loads of a round issued before its stores (a dense tile's segment is up to 32 KiB:
+    // with U = 1 every 16 lanes x 16 bytes cost a load-store round trip)
+    for (uint32_t j0 = hl; j0 < nv; j0 += U * L) {
+        uint4 a[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t j = j0 + u * L;
+            if (j < nv) {
+                a[u] = __ldg(s16 + j);
+                b[u] = __ldg(s16 + j + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t j = j0 + u * L;
+            if (j >= nv) break;
+            uint32_t w0, w1, w2, w3, w4;
+            if (qv == 0) { w0 = a[u].x; w1 = a[u].y; w2 = a[u].z; w3 = a[u].w; w4 = b[u].x; }
+            else if (qv == 1) { w0 = a[u].y; w1 = a[u].z; w2 = a[u].w; w3 = b[u].x; w4 = b[u].y; }
+            else if (qv == 2) { w0 = a[u].z; w1 = a[u].w; w2 = b[u].x; w3 = b[u].y; w4 = b[u].z; }
+            else { w0 = a[u].w; w1 = b[u].x; w2 = b[u].y; w3 = b[u].z; w4 = b[u].w; }
+            d16[j] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                                __funnelshift_r(w3, w4, sh));
+        }
     }
 }
 
-template <int W, int S, int L>
+template <int W, int S, int L, int U>
 __global__ void __launch_bounds__(256)
 k_emit_pair(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ bases, uint32_t ntiles, uint32_t slot_cap,
             const uint8_t *__restrict__ slot_bytes, const typename LaneOf<W>::T *__restrict__ slot_val,
@@ -1151,8 +1226,8 @@ k_emit_pair(const TileEmit *__restrict__ plan, const TensorBase *__restrict__ ba
                     ring_store_h<L>(sd, di + L0, ni, hl);
                     ring_store_h<L>(sd + 512, dv, nv, hl);
                 } else {  // a dense tile: synchronous copies
-                    half_copy16<L>(di + L0, slot_i(t), ni, hl);
-                    half_copy16<L>(dv, slot_v(t), nv, hl);
+                    half_copy16<L, U>(di + L0, slot_i(t), ni, hl);
+                    half_copy16<L, U>(dv, slot_v(t), nv, hl);
                 }
             }
         }
@@ -1241,22 +1316,26 @@ static cudaError_t scan_impl(const ExtractArgs &a, cudaStream_t s, cudaEvent_t *
 // 0.120 with 16, 0.160 with 8 — the 8-lane form fits 3 CTAs per SM)
 constexpr int kEmitStages = 2, kEmitLanes = 16;
 
-template <int W, int L>
+template <int W, int L, int U>
 static void launch_pair(const ExtractArgs &a, uint8_t *out, cudaStream_t s) {
     constexpr uint32_t psmem = 8 * pair_warp_bytes<kEmitStages, 32 / L>();
     static const bool attr = [] {
-        cudaFuncSetAttribute(k_emit_pair<W, kEmitStages, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        cudaFuncSetAttribute(k_emit_pair<W, kEmitStages, L, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
         return true;
     }();
     (void)attr;
-    k_emit_pair<W, kEmitStages, L><<<a.persist_ctas, 256, psmem, s>>>(
+    k_emit_pair<W, kEmitStages, L, U><<<a.persist_ctas, 256, psmem, s>>>(
         a.plan, a.bases, a.ntiles, a.slot_cap, a.slot_bytes, static_cast<const typename LaneOf<W>::T *>(a.slot_val), out,
         a.summary, a.out_cap, a.peer);
 }
 
+// Dense tiles (segments > kPref bytes) are copied from global memory; the 4-deep unrolled copy
+// costs registers (53 -> 118: 2 instead of 4 CTAs per SM), so it is taken only once the slots
+// have grown past their initial 2 KiB per tile (some tile held > 1024 bf16 / 512 fp32 entries).
 template <int W>
 static void launch_ring(const ExtractArgs &a, uint8_t *out, cudaStream_t s) {
-    launch_pair<W, kEmitLanes>(a, out, s);
+    if ((size_t)a.slot_cap * W > 2048) launch_pair<W, kEmitLanes, 4>(a, out, s);
+    else launch_pair<W, kEmitLanes, 1>(a, out, s);
 }
 
 template <int W>

@@ -185,3 +185,70 @@ def test_fuzzed_bodies_all_or_nothing(sd):
             rejected += 1
     assert rejected > 60
     ctx.close()
+
+
+def _dense_lanes(n, rho, pattern, width, rng):
+    """old / new lane arrays with a `pattern` change set: "uniform" (each lane with
+    probability rho), "runs" (runs of 1-64 changed lanes, rho of the lanes), "late" (the
+    first 3000 lanes unchanged, then uniform)."""
+    dt = np.uint16 if width == 2 else np.uint32
+    old = rng.integers(0, 1 << (8 * width), n, dtype=np.uint64).astype(dt)
+    if pattern == "runs":
+        m = np.zeros(n, bool)
+        p = 0
+        while p < n:
+            run = int(rng.integers(1, 65))
+            if rng.random() < rho:
+                m[p:p + run] = True
+            p += run
+    else:
+        m = rng.random(n) < rho
+        if pattern == "late":
+            m[:3000] = False
+    flip = rng.integers(1, 1 << (8 * width), n, dtype=np.uint64).astype(dt)
+    new = np.where(m, old ^ flip, old).astype(dt)
+    if width == 2:  # keep additive arithmetic away from NaN patterns (bf16 0x7F80+ exponents)
+        old &= 0xBFFF
+        new &= 0xBFFF
+    else:
+        old &= 0xBFFFFFFF
+        new &= 0xBFFFFFFF
+    return old, new
+
+
+@pytest.mark.parametrize("width", [2, 4])
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("shift", [0, 1, 3, 7])
+def test_dense_scatter_unaligned_targets(sd, width, mode, shift):
+    """A4's dense-chunk path (whole 16-byte vectors rewritten inside a chunk's window, the
+    window's edge vectors lane by lane): targets at every lane alignment, densities from
+    the path's threshold (>= 256 entries, gap sum < 4 per entry) to every lane, runs and a
+    late first change; replace and additive records; lanes equal the oracle's apply and
+    the bytes around every target stay untouched."""
+    rng = np.random.default_rng(100 * width + 10 * mode + shift)
+    cases = [(50_000, 0.26, "uniform"), (200_003, 0.5, "uniform"), (70_001, 0.95, "uniform"),
+             (33_333, 1.0, "uniform"), (120_000, 0.5, "runs"), (60_000, 0.6, "late"), (9, 1.0, "uniform"),
+             (300, 1.0, "uniform")]
+    tensors, np_pairs = [], []
+    for k, (n, rho, pat) in enumerate(cases):
+        o, w = _dense_lanes(n, rho, pat, width, rng)
+        np_pairs.append((f"d{k}.weight", o, w))
+    body_b, _ = oracle.codec.extract([(nm, [o], [w]) for nm, o, w in np_pairs], mode=mode)
+    want = oracle.codec.apply([(nm, o) for nm, o, _ in np_pairs], body_b, width)
+    body = torch.frombuffer(bytearray(body_b), dtype=torch.uint8).to(DEV)
+    tdt = torch.bfloat16 if width == 2 else torch.float32
+    ctx = sd.DeltaContext(DEV)
+    wholes, targets = [], []
+    for nm, o, _ in np_pairs:
+        nb = o.size * width
+        whole, view = _guarded(nb, shift * width)
+        view.copy_(torch.from_numpy(o.view(np.uint8).copy()).to(DEV))
+        wholes.append(whole)
+        targets.append((nm, view.view(tdt)))
+    ctx.delta_apply(targets, body)
+    torch.cuda.synchronize()
+    for (nm, t), exp, whole in zip(targets, want, wholes):
+        got = t.view(torch.int16 if width == 2 else torch.int32).cpu().numpy().view(exp.dtype)
+        assert np.array_equal(got, exp), f"{nm}: {np.flatnonzero(got != exp)[:10]}"
+        assert _intact(whole, G + shift * width, G + shift * width + exp.size * width)
+    ctx.close()
