@@ -303,6 +303,19 @@ __device__ __forceinline__ bool validate_fast(const ChunkView &v, int p0, uint32
 #pragma unroll
     for (int k = 0; k < 5; ++k) w[k] = sh ? __funnelshift_r(W[k], W[k + 1], sh) : W[k];
     if ((long long)v.cs + p0 == 0) w[0] = 0;  // the stream's first byte: nothing before it
+    // 16 one-byte varints (no continuation bit in the window or just before it; the dense
+    // regime's common case): count 16, sum = the byte sum; a 0x00 byte goes to the byte loop
+    if (((w[1] | w[2] | w[3] | w[4]) & 0x80808080u) == 0u && !(w[0] & 0x80000000u)) {
+        uint32_t z = 0;
+#pragma unroll
+        for (int k = 1; k < 5; ++k) z |= ~(((w[k] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w[k]) & 0x80808080u;
+        if (z) return false;
+        const uint32_t s16 = __dp4a(w[1], 0x01010101u, __dp4a(w[2], 0x01010101u, __dp4a(w[3], 0x01010101u, __dp4a(w[4], 0x01010101u, 0u))));
+        if (ones) *ones = true;
+        cnt += 16;
+        sum = sat_add(sum, (unsigned long long)s16);
+        return true;
+    }
     uint32_t C[5], t[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -515,27 +528,24 @@ struct DenseLanes {
     static constexpr uint32_t ALL = (1u << LV) - 1u;
 };
 
-// Values [ord0, ord0 + LV) of the chunk (staged at svb + vofs, any byte alignment) as four
-// words: one 20-byte window of aligned shared-memory words, funnel-shifted.
-__device__ __forceinline__ void value_run(const uint8_t *svb, uint32_t b, uint32_t (&p)[4]) {
-    const uint32_t *a = reinterpret_cast<const uint32_t *>(svb) + (b >> 2);
-    const uint32_t sh = (b & 3u) * 8u;
-    uint32_t x[5];
+// Bytes [src, src + n) into shared memory realigned to buf (16-byte aligned): vector j of
+// buf = source bytes 16 j .. 16 j + 15, funnel-shifted from the two aligned source vectors
+// that hold them (the second only when it lies inside the aligned superset of the range), so
+// the chunk's values are lane-aligned (one LDS per value instead of W byte loads).
+__device__ __forceinline__ void stage_aligned(uint8_t *buf, const uint8_t *src, uint32_t n) {
+    const uint4 *a = reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+    const uint32_t o = (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15);
+    const uint32_t ns = (o + n + 15) / 16, nv = (n + 15) / 16;  // source / output vectors
+    const uint32_t sh = (o & 3u) * 8u, q = o >> 2;
+    for (uint32_t j = threadIdx.x; j < nv; j += blockDim.x) {
+        const uint4 x = __ldg(a + j);
+        const uint4 y = j + 1 < ns ? __ldg(a + j + 1) : make_uint4(0, 0, 0, 0);
+        const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+        uint32_t r[5];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) x[i] = a[i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) p[i] = __funnelshift_r(x[i], x[i + 1], sh);
-}
-
-// Lane q (0 <= q < LV) of a run of values packed in four words.
-template <int W>
-__device__ __forceinline__ uint32_t run_lane(const uint32_t (&p)[4], uint32_t q) {
-    if constexpr (W == 2) {
-        const unsigned long long lo = p[0] | ((unsigned long long)p[1] << 32);
-        const unsigned long long hi = p[2] | ((unsigned long long)p[3] << 32);
-        return (uint32_t)(((q < 4 ? lo : hi) >> ((q & 3u) * 16u)) & 0xFFFFu);
-    } else {
-        return q < 2 ? (q == 0 ? p[0] : p[1]) : (q == 2 ? p[2] : p[3]);
+        for (int i = 0; i < 5; ++i) r[i] = q == 0 ? w[i] : q == 1 ? w[i + 1] : q == 2 ? w[i + 2] : w[i + 3];
+        reinterpret_cast<uint4 *>(buf)[j] = make_uint4(__funnelshift_r(r[0], r[1], sh), __funnelshift_r(r[1], r[2], sh),
+                                                       __funnelshift_r(r[2], r[3], sh), __funnelshift_r(r[3], r[4], sh));
     }
 }
 
@@ -581,8 +591,12 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         const uint32_t cn = chunk_count[c];
         const unsigned long long csum = chunk_sum[c];
         const bool dense = cn >= 256 && csum < 4ull * cn;
-        // this chunk's values (cn lanes, any alignment in the body)
-        const uint8_t *vals = stage_bytes(svb, body + R.val_off + ob * W, cn * W);
+        // this chunk's values (cn lanes, any alignment in the body): lane-aligned in svb for a
+        // dense chunk (one LDS per value in the merge), the aligned superset otherwise
+        const LT *sval = reinterpret_cast<const LT *>(svb);
+        const uint8_t *vals = svb;
+        if (dense) stage_aligned(svb, body + R.val_off + ob * W, cn * W);
+        else vals = stage_bytes(svb, body + R.val_off + ob * W, cn * W);
         if (dense) {
 #pragma unroll
             for (int i = 0; i < 3; ++i) su.d.bm[threadIdx.x * 3 + i] = 0u;
@@ -617,7 +631,7 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
         unsigned long long idx = base + spre + si - sum;
         LT *w = reinterpret_cast<LT *>(R.w);
         const bool add = R.mode == 1;  // additive record: scatter-add
-        auto value = [&](uint32_t o) -> LT {
+        auto value = [&](uint32_t o) -> LT {  // sparse chunks
             if constexpr (W == 2) return (LT)(vals[2 * o] | (vals[2 * o + 1] << 8));
             else return (LT)vals[4 * o] | ((LT)vals[4 * o + 1] << 8) | ((LT)vals[4 * o + 2] << 16) | ((LT)vals[4 * o + 3] << 24);
         };
@@ -660,7 +674,6 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
             }
             __syncthreads();
             // every vector holding a change: 4 per thread in flight (loads, then stores)
-            const uint32_t vofs = (uint32_t)(vals - svb);
             const uint32_t nvec = (uint32_t)(((long long)whi - abase) / D::LV) + 1;
             uint4 *gv = reinterpret_cast<uint4 *>(w + abase);
             for (uint32_t v0 = threadIdx.x; v0 < nvec; v0 += 4 * blockDim.x) {
@@ -680,39 +693,38 @@ k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, u
                     if (!m[u]) continue;
                     const uint32_t vi = v0 + u * blockDim.x;
                     const uint32_t wd = vi / D::VPW, sh = (vi % D::VPW) * D::LV;
-                    const uint32_t o0 = su.d.pre[wd] + __popc(su.d.bm[wd] & ((1u << sh) - 1u));
-                    uint32_t p[4];
-                    value_run(svb, vofs + o0 * W, p);
-                    if (whole[u]) {
+                    uint32_t o = su.d.pre[wd] + __popc(su.d.bm[wd] & ((1u << sh) - 1u));  // first change's ordinal
+                    if (whole[u] && !add && m[u] == D::ALL) {  // every lane replaced: 4 (or 5) LDS.32
+                        const uint32_t *s32 = reinterpret_cast<const uint32_t *>(sval) + (o * W >> 2);
+                        uint32_t x[5];
+#pragma unroll
+                        for (int i = 0; i < 5; ++i) x[i] = s32[i];
+                        const uint32_t sh = (o * W & 3u) * 8u;
+                        gv[vi] = make_uint4(__funnelshift_r(x[0], x[1], sh), __funnelshift_r(x[1], x[2], sh),
+                                            __funnelshift_r(x[2], x[3], sh), __funnelshift_r(x[3], x[4], sh));
+                    } else if (whole[u]) {
                         uint32_t ow[4] = {old[u].x, old[u].y, old[u].z, old[u].w};
-                        if (!add && m[u] == D::ALL) {
+                        // lanes unrolled: the k-th changed lane takes value o + k (one LDS each)
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) ow[i] = p[i];
-                        } else {
-                            uint32_t q = 0;
-#pragma unroll
-                            for (int l = 0; l < D::LV; ++l) {
-                                if (!((m[u] >> l) & 1u)) continue;
-                                uint32_t nv = run_lane<W>(p, q++);
-                                if constexpr (W == 2) {
-                                    const uint32_t sl = (l & 1) * 16;
-                                    if (add) nv = lane_combine<2>((ow[l >> 1] >> sl) & 0xFFFFu, nv, false);
-                                    ow[l >> 1] = (ow[l >> 1] & ~(0xFFFFu << sl)) | (nv << sl);
-                                } else {
-                                    if (add) nv = lane_combine<4>(ow[l], nv, false);
-                                    ow[l] = nv;
-                                }
+                        for (int l = 0; l < D::LV; ++l) {
+                            if (!((m[u] >> l) & 1u)) continue;
+                            uint32_t nv = sval[o++];
+                            if constexpr (W == 2) {
+                                if (add) nv = lane_combine<2>((ow[l >> 1] >> ((l & 1) * 16)) & 0xFFFFu, nv, false);
+                                ow[l >> 1] = __byte_perm(ow[l >> 1], nv, (l & 1) ? 0x5410 : 0x3254);
+                            } else {
+                                if (add) nv = lane_combine<4>(ow[l], nv, false);
+                                ow[l] = nv;
                             }
                         }
                         gv[vi] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
                     } else {  // a vector across the window's edge: its changed lanes only
-                        uint32_t q = 0;
 #pragma unroll
                         for (int l = 0; l < D::LV; ++l) {
                             if (!((m[u] >> l) & 1u)) continue;
                             LT &t = w[abase + (long long)vi * D::LV + l];
-                            const uint32_t nv = run_lane<W>(p, q++);
-                            t = add ? (LT)lane_combine<W>(t, nv, false) : (LT)nv;
+                            const LT nv = sval[o++];
+                            t = add ? (LT)lane_combine<W>(t, nv, false) : nv;
                         }
                     }
                 }

@@ -338,61 +338,79 @@ k_scan_tiles(const TileDesc *__restrict__ tiles, uint32_t ntiles, uint32_t prefe
         uint8_t *sb = slot_bytes + (size_t)t * 2 * slot_cap;
         if constexpr (!ADDITIVE && !OFFSETS) {
             // values from the registers (s_new is no longer read), compacted into s_new by
-            // rank; the index bytes behind them when they fit, else straight to the slot; then
-            // both leave in 16-byte stores (whole sectors instead of 2- and 1-byte scatters)
+            // rank, then the index bytes behind them (or, when both do not fit its 32 KiB,
+            // after the values have left): every store is a shared-memory store, and the slot
+            // is written with 16-byte stores (whole sectors instead of 2- and 1-byte scatters)
             const uint32_t nb = c - 1u + (tot >> 16) - 1u;  // in-tile index bytes (as meta)
             const uint32_t vb = (c * W + 15u) & ~15u;
             const bool bsm = vb + nb + 16u <= (uint32_t)sizeof(s_new);
             uint8_t *sm = reinterpret_cast<uint8_t *>(s_new);
             LT *smv = reinterpret_cast<LT *>(s_new);
-            uint8_t *bd = bsm ? sm + vb : sb;
+            auto copy_out = [&](uint8_t *dst, uint32_t from, uint32_t bytes) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(sm + from);
+                for (uint32_t i = tid; i < (bytes + 15u) / 16u; i += THREADS) reinterpret_cast<uint4 *>(dst)[i] = src[i];
+            };
+            // pass V: change k of vector v goes to rank + k (lanes unrolled: static extraction)
 #pragma unroll
             for (int r = 0; r < VECS; ++r) {
                 const uint32_t v = r * THREADS + tid;
                 const uint32_t w = v / (64 / LPV), sub = v % (64 / LPV);
                 const unsigned long long Wb = s_bits[w];
-                uint32_t mb = (uint32_t)(Wb >> (sub * LPV)) & ((1u << LPV) - 1u);
+                const uint32_t mb = (uint32_t)(Wb >> (sub * LPV)) & ((1u << LPV) - 1u);
+                if (!mb) continue;
+                const unsigned long long below = Wb & ((1ull << (sub * LPV)) - 1ull);
+                const uint32_t rank = (s_wex[w] & 0xFFFFu) + (uint32_t)__popcll((long long)below);
+#pragma unroll
+                for (int j = 0; j < LPV; ++j)
+                    if ((mb >> j) & 1u) smv[rank + (uint32_t)__popc(mb & ((1u << j) - 1u))] = (LT)lane_of<W>(vn[r], j);
+            }
+            if (!bsm) {
+                __syncthreads();
+                copy_out(reinterpret_cast<uint8_t *>(sv), 0, c * W);
+                __syncthreads();
+            }
+            uint8_t *bd = sm + (bsm ? vb : 0u);
+            // pass B: the vector's first change's gap (from prevL) takes two bytes iff it starts
+            // its word and the word is flagged; the tile's first change has no in-tile gap (its
+            // byte position, -1, is virtual: K4 writes the plan's first gap ahead of the stream);
+            // a later change k of the vector: one byte (< LPV lanes) at bq + k - 1
+#pragma unroll
+            for (int r = 0; r < VECS; ++r) {
+                const uint32_t v = r * THREADS + tid;
+                const uint32_t w = v / (64 / LPV), sub = v % (64 / LPV);
+                const unsigned long long Wb = s_bits[w];
+                const uint32_t mb = (uint32_t)(Wb >> (sub * LPV)) & ((1u << LPV) - 1u);
                 if (!mb) continue;
                 const unsigned long long below = Wb & ((1ull << (sub * LPV)) - 1ull);
                 const uint32_t ex = s_wex[w], pv = s_wprv[w];
-                uint32_t rank = (ex & 0xFFFFu) + (uint32_t)__popcll((long long)below);
+                const uint32_t rank = (ex & 0xFFFFu) + (uint32_t)__popcll((long long)below);
                 const bool hp_w = pv & (1u << 17);
                 const uint32_t bigs = (ex >> 16) - ((hp_w && (ex >> 16)) ? 1u : 0u);
                 const uint32_t bp = rank - 1u + bigs + (below && (pv & (1u << 16)) ? 1u : 0u);
                 const bool has_prev = below ? true : hp_w;
                 const uint32_t prevL = below ? 64u * w + 63u - (uint32_t)__clzll((long long)below) : (pv & 0xFFFFu);
-                // the vector's first change: its gap (from prevL) takes two bytes iff it starts
-                // its word and the word is flagged; the tile's first change has no in-tile gap
-                // (its byte position, -1, is virtual: K4 writes the plan's first gap ahead of
-                // the stream)
                 const bool two = has_prev && below == 0 && (pv & (1u << 16));
-                const uint32_t bq = bp + (two ? 2u : 1u);  // bytes of the vector's later changes
-                // lanes unrolled (static lane extraction, no per-change loop): change k of the
-                // vector goes to rank + k, its gap (< LPV lanes: one byte) to bq + k - 1
-#pragma unroll
-                for (int j = 0; j < LPV; ++j) {
-                    if (!((mb >> j) & 1u)) continue;
-                    const uint32_t low = mb & ((1u << j) - 1u);
-                    const uint32_t k = (uint32_t)__popc(low);
-                    smv[rank + k] = (LT)lane_of<W>(vn[r], j);
-                    if (low) {
-                        bd[bq + k - 1u] = (uint8_t)(j - (31 - __clz(low)));
-                    } else if (has_prev) {
-                        const uint32_t g = v * LPV + j - prevL;
-                        if (two) {
-                            bd[bp] = (uint8_t)(g | 0x80u);
-                            bd[bp + 1] = (uint8_t)(g >> 7);
-                        } else {
-                            bd[bp] = (uint8_t)g;
-                        }
+                const uint32_t bq = bp + (two ? 2u : 1u);
+                const uint32_t f = (uint32_t)__ffs(mb) - 1u;  // the vector's first change
+                if (has_prev) {
+                    const uint32_t g = v * LPV + f - prevL;
+                    if (two) {
+                        bd[bp] = (uint8_t)(g | 0x80u);
+                        bd[bp + 1] = (uint8_t)(g >> 7);
+                    } else {
+                        bd[bp] = (uint8_t)g;
                     }
+                }
+#pragma unroll
+                for (int j = 1; j < LPV; ++j) {
+                    const uint32_t low = mb & ((1u << j) - 1u);
+                    if (((mb >> j) & 1u) && low)
+                        bd[bq + (uint32_t)__popc(low) - 1u] = (uint8_t)(j - (31 - __clz(low)));
                 }
             }
             __syncthreads();
-            const uint4 *src = reinterpret_cast<const uint4 *>(s_new);
-            for (uint32_t i = tid; i < vb / 16u; i += THREADS) reinterpret_cast<uint4 *>(sv)[i] = src[i];
-            if (bsm)
-                for (uint32_t i = tid; i < (nb + 15u) / 16u; i += THREADS) reinterpret_cast<uint4 *>(sb)[i] = src[vb / 16u + i];
+            if (bsm) copy_out(reinterpret_cast<uint8_t *>(sv), 0, c * W);
+            copy_out(sb, bsm ? vb : 0u, nb);
             return;
         }
         const LT *sn = reinterpret_cast<const LT *>(s_new);
