@@ -986,6 +986,12 @@ static int apply_enqueue(delta_ctx *ctx, const delta_target *tg, uint32_t n, int
     a.scatter_ctas = ctx->sm_count * ctx->scatter_ctas_per_sm;
     a.entry_major = ctx->entry_major;
     a.index_codec = ctx->index_codec;
+    {  // launch-shape hint only (any value is correct): body bytes per target lane, from the
+       // host size or the capacity of a device-sized body
+        unsigned long long lanes = 0;
+        for (uint32_t k = 0; k < n; ++k) lanes += tg[k].numel;
+        a.dense_hint = (double)body_bytes > 0.125 * (double)w * (double)lanes;
+    }
     CK(launch_apply(a, s, prof_apply(ctx)), "apply launch");
     return DELTA_OK;
 }

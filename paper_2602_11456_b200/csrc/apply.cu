@@ -551,8 +551,11 @@ __device__ __forceinline__ void stage_aligned(uint8_t *buf, const uint8_t *src, 
 
 // Gated scatter-store: decode again, absolute index = chunk base + running gap sum, value
 // from the chunk's slice of the record's value array (staged in shared memory).
-template <int W, bool ENTRY_MAJOR>
-__global__ void __launch_bounds__(256, 6)
+// MINB: CTAs per SM the registers are capped for — 5 (48 registers) for sparse deltas, where
+// the scatter is bound by the HBM access rate; 6 (40 registers) for dense ones, where the
+// merge is issue-bound (A/B r66: 1 % uniform 2.30 vs 2.32 ms with 5; 50 % 13.9 vs 15.6 with 6)
+template <int W, bool ENTRY_MAJOR, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 k_scatter(const uint8_t *__restrict__ body, const ApplyRec *__restrict__ recs, uint32_t n,
           const unsigned long long *__restrict__ rcb, const uint32_t *__restrict__ chunk_rec,
           const unsigned int *__restrict__ chunk_count, const unsigned long long *__restrict__ chunk_sum,
@@ -959,8 +962,9 @@ cudaError_t launch_apply(const ApplyArgs &a, cudaStream_t s, cudaEvent_t *ev) {
                                      a.chunk_ord_base, a.chunk_idx_base, a.state);
     if (ev) cudaEventRecord(ev[3], s);
 #define SCATTER(WW, EM)                                                                                 \
-    k_scatter<WW, EM><<<a.scatter_ctas, 256, 0, s>>>(a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec, a.chunk_count, a.chunk_sum, \
-                                                     a.chunk_ord_base, a.chunk_idx_base, a.state)
+    (a.dense_hint ? k_scatter<WW, EM, 6> : k_scatter<WW, EM, 5>)<<<a.scatter_ctas, 256, 0, s>>>(      \
+        a.body, a.recs, a.n, a.rec_chunk_begin, a.chunk_rec, a.chunk_count, a.chunk_sum, a.chunk_ord_base,    \
+        a.chunk_idx_base, a.state)
     if (a.width == 2) {
         if (a.entry_major) SCATTER(2, true);
         else SCATTER(2, false);

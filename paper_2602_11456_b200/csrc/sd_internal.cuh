@@ -209,6 +209,7 @@ struct ApplyArgs {
     int persist_ctas;
     int scatter_ctas;
     bool entry_major;                 // scatter store order (see k_scatter)
+    bool dense_hint = false;          // body > w / 8 bytes per target lane (~5 % density): A4 at 6 CTAs/SM
     int index_codec;                  // 0 LEB128 gaps, 1 fixed-width absolute indices (R18)
 };
 
