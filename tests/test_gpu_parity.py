@@ -525,7 +525,7 @@ def test_gpu_digest_and_container(sd):
 def test_additive_mode_parity(sd, dtype):
     """DELTA_OPT_MODE = 2: values are new - old (fp32 arithmetic, RNE to bf16) and apply
     adds them — body bytes and the applied lanes byte-exact against the
-    oracle's additive codec, on sparse, dense (window-merge) and full-range bit patterns."""
+    oracle's additive codec, on sparse, dense (whole-vector window rewrite) and full-range bit patterns."""
     import oracle
     from paper_2602_11456_b200 import _abi
     ctx = sd.DeltaContext(DEV)
