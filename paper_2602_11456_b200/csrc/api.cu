@@ -166,7 +166,7 @@ static int cuda_fail(delta_ctx *c, cudaError_t e, const char *where) {
 extern "C" {
 
 const char *delta_version(void) {
-    return "sparsedelta 2 (sm_100a; K1 tile-slot compaction, tile scans, warp-per-tile LEB128 emit, gated scatter)";
+    return "sparsedelta 2 (sm_100a; K1 tile-slot compaction, tile scans, half-warp-per-tile LEB128 emit, gated scatter with dense-window vector rewrite)";
 }
 
 int delta_ctx_create(delta_ctx **out, int device) {
